@@ -1,0 +1,180 @@
+/*
+ * dlic.h — C-ABI of the B200-native DLIC hot path (libdlic.so).
+ *
+ * DLIC (arXiv 2207.05152, /root/reference/PAPER.md cited as P:<line>) codes an
+ * 8-bit grayscale image losslessly: a dense network maps each pixel's causal
+ * window of already-coded neighbours (Fig. 6; dummy value outside
+ * the image P:59) to a 256-way PDF, which drives rANS coder instances,
+ * at most one per pixel row.  Encoding evaluates every pixel at
+ * once; decoding walks the wavefront step(r,c) = c + 3r (WPP).
+ *
+ * The paper states the problem as encode(image, weights) -> bitstream and
+ * decode(bitstream, weights) -> image (Fig. 2); dlic_encode /
+ * dlic_decode follow it.  Readings of everything the paper leaves open
+ * (window shape, fill, quantiser, rANS constants, lane framing) are DESIGN.md
+ * R1-R10.
+ *
+ * Conventions
+ *  - Every call returns dlic_status; no exception crosses the ABI.  On error
+ *    outputs are untouched (except where noted) and dlic_last_error() holds a
+ *    thread-local detail string.  CUDA failures map to DLIC_E_CUDA.
+ *  - Host pointers are plain CPU memory; pointers named d_* are CUDA device
+ *    memory owned by the caller; cuda_stream is a cudaStream_t (NULL = the
+ *    legacy default stream).  The library never takes ownership of caller
+ *    memory; buffers it returns are released with dlic_free.
+ *  - Images are row-major uint8, row_stride >= width bytes.
+ *  - A dlic_model is immutable after load and may be shared by threads.
+ *  - No CPU fallback exists: every pixel-level step runs in CUDA kernels on
+ *    an sm_100a device; without one, calls return DLIC_E_CUDA.
+ */
+#ifndef DLIC_H
+#define DLIC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DLIC_OK = 0,
+  DLIC_E_INVALID_ARG = 1,      /* null pointer, zero size, unsupported option */
+  DLIC_E_SHAPE_MISMATCH = 2,   /* image / tables / model dims disagree */
+  DLIC_E_NONCAUSAL_WINDOW = 3, /* reserved: window id other than the causal 9x9 */
+  DLIC_E_CORRUPT_MODEL = 4,    /* model blob magic/length/hash invalid */
+  DLIC_E_VERSION_MISMATCH = 5, /* container version or window id unknown */
+  DLIC_E_CORRUPT_CONTAINER = 6,/* bad framing, or a lane ended off its invariant */
+  DLIC_E_MODEL_HASH_MISMATCH = 7, /* container coded with another model (checked first) */
+  DLIC_E_STREAM_UNDERFLOW = 8, /* a lane needed a word past its stream end */
+  DLIC_E_SUM_MISMATCH = 9,     /* a frequency table does not sum to 2^16 */
+  DLIC_E_ZERO_FREQUENCY = 10,  /* a frequency of 0 in a table */
+  DLIC_E_BUFFER_TOO_SMALL = 11,
+  DLIC_E_CUDA = 12,            /* CUDA runtime / launch failure, or no sm_100 device */
+  DLIC_E_OUT_OF_MEMORY = 13,
+  DLIC_E_UNSUPPORTED_MODEL = 14 /* the GPU engines implement 78->128x5->256 (P100K) */
+} dlic_status;
+
+/* Precision path of the density estimator (recorded in the container; both
+ * sides of a bitstream must use the same path).
+ *  DLIC_PREC_FP32: fp32 FFMA on CUDA cores, fixed summation order (meets the
+ *                  1e-4 relative logit bar vs the fp64 oracle).
+ *  DLIC_PREC_BF16: bf16 operands on tcgen05 tensor cores, fp32 accumulation in
+ *                  TMEM (bpp gated to within 0.5% of fp32). */
+enum { DLIC_PREC_FP32 = 0, DLIC_PREC_BF16 = 1 };
+
+typedef struct dlic_model dlic_model; /* opaque; immutable after load */
+
+typedef struct {
+  uint32_t precision;  /* DLIC_PREC_* */
+  uint32_t group_rows; /* G: rows per interleaved stream (R7); 0 -> 32 */
+  uint32_t tile_w;     /* independent tiles (Q16); 0,0 = untiled */
+  uint32_t tile_h;
+} dlic_opts;
+
+typedef struct {
+  uint32_t width, height, precision, group_rows, tile_w, tile_h, n_streams, n_units;
+  uint8_t model_sha256[32];
+  uint64_t payload_bytes, header_bytes;
+} dlic_header;
+
+/* ---- models --------------------------------------------------------------
+ * "DLICMDL1" blob: magic, u16 layers, per layer {u32 in, u32 out,
+ * u8 act, u8 pool, f32 W[in][out] row-major, f32 b[out]}, u16 meta count,
+ * SHA-256 of all preceding bytes.  Uploads fp32 and bf16 device copies to
+ * `cuda_device`.  Errors: DLIC_E_CORRUPT_MODEL, DLIC_E_CUDA. */
+dlic_status dlic_model_load(const void* bytes, size_t len, int cuda_device, dlic_model** out);
+/* Same from arrays: dims[n_layers+1]; W[l] row-major [dims[l]][dims[l+1]]
+ * float32; b[l] float32[dims[l+1]].  The blob (and its hash) is built here. */
+dlic_status dlic_model_from_arrays(uint32_t n_layers, const uint32_t* dims, const float* const* W,
+                                   const float* const* b, int cuda_device, dlic_model** out);
+void dlic_model_free(dlic_model* m);
+/* SHA-256 content hash recorded in containers (host only). */
+dlic_status dlic_model_sha256(const dlic_model* m, uint8_t out[32]);
+/* Host-only check of a model blob (magic, length, SHA-256); no device work. */
+dlic_status dlic_model_blob_check(const void* bytes, size_t len, uint8_t sha_out[32]);
+
+/* ---- the paper's statement: encode(image, weights) -> bitstream ----------
+ * Host image in, library-allocated container out (release with dlic_free).
+ * Exactly one host->device copy (the image) and one device->host copy of the
+ * result, on an internal stream.  opts NULL = {DLIC_PREC_BF16, G = 32,
+ * untiled}. */
+dlic_status dlic_encode(const dlic_model* m, const uint8_t* img, uint32_t width, uint32_t height,
+                        size_t row_stride, const dlic_opts* opts, uint8_t** out, size_t* out_len);
+
+/* decode(bitstream, weights) -> image.  Verifies the model hash BEFORE any
+ * pixel work, checks every lane's end state (2^16) and cursor, and writes
+ * width*height bytes (row-major, stride = width) to img.
+ * Errors: DLIC_E_MODEL_HASH_MISMATCH, DLIC_E_CORRUPT_CONTAINER,
+ * DLIC_E_STREAM_UNDERFLOW, DLIC_E_BUFFER_TOO_SMALL. */
+dlic_status dlic_decode(const dlic_model* m, const uint8_t* bits, size_t len, uint8_t* img,
+                        size_t img_capacity);
+
+/* Parse a container header (host only, no device work). */
+dlic_status dlic_peek(const uint8_t* bits, size_t len, dlic_header* out);
+
+/* Upper bound of the container size for (width, height, opts). */
+size_t dlic_max_container_bytes(uint32_t width, uint32_t height, const dlic_opts* opts);
+
+void dlic_free(void* p);
+const char* dlic_status_str(dlic_status s);
+const char* dlic_last_error(void);
+
+/* ---- device-resident batch variants (caller owns memory and stream) -------
+ * n images of width x height, packed (image i at d_imgs + i*width*height).
+ * Encode writes container i at d_out + i*dlic_max_container_bytes(...) and its
+ * byte size to d_sizes[i] (uint64).  out_capacity must be >= n * max bytes.
+ * Asynchronous on cuda_stream except for small internal scratch allocations
+ * (stream-ordered).  Errors are reported for the launch; lane-invariant
+ * failures of decode are reported through d_status[i] (0 = ok, else a
+ * dlic_status) when d_status is non-NULL. */
+dlic_status dlic_encode_batch_device(const dlic_model* m, const uint8_t* d_imgs, uint32_t n,
+                                     uint32_t width, uint32_t height, const dlic_opts* opts,
+                                     uint8_t* d_out, size_t out_capacity, uint64_t* d_sizes,
+                                     void* cuda_stream);
+/* Decode n containers that all share (width, height, opts) — i.e. produced by
+ * dlic_encode_batch_device — located at d_bits + h_offsets[i] (HOST array of
+ * byte offsets).  The headers are re-read on the device; h_header is the
+ * parsed header of container 0 (dlic_peek on a host copy), used for planning. */
+dlic_status dlic_decode_batch_device(const dlic_model* m, const uint8_t* d_bits,
+                                     const uint64_t* h_offsets, uint32_t n,
+                                     const dlic_header* h_header, uint8_t* d_imgs,
+                                     int32_t* d_status, void* cuda_stream);
+
+/* ---- parity / debug taps ---------------------------------------------------
+ * rANS only, fed integer tables (north_star: "the same quantised frequency
+ * tables and bitstream bit-exactly as the oracle when the oracle is fed the
+ * same integer tables").  fc[r*width+c] = f_s | (c_s << 16) of the TRUE symbol
+ * of pixel (r,c) (host array).  Produces the container exactly as dlic_encode
+ * would (precision field = opts->precision, model hash = model_sha256 or zeros). */
+dlic_status dlic_rans_encode_tables(const uint32_t* fc, uint32_t width, uint32_t height,
+                                    const dlic_opts* opts, const uint8_t* model_sha256,
+                                    uint8_t** out, size_t* out_len);
+/* Decode a container given every pixel's full frequency table
+ * freq_tables[(r*width+c)*256 + s] (host, uint16, each table sums to 2^16).
+ * Writes the image to img (width*height bytes). */
+dlic_status dlic_rans_decode_tables(const uint8_t* bits, size_t len, const uint16_t* freq_tables,
+                                    uint8_t* img);
+/* Run the encoder's density-estimator kernels on every pixel of a host image
+ * (tile-aware per opts) and export, per pixel in raster order, any of:
+ * logits[256] (fp32), probs[256] (fp32 softmax as used by the quantiser),
+ * freqs[256] (uint16 integer table), fc (f_s | c_s<<16 of the true symbol).
+ * NULL outputs are skipped. */
+dlic_status dlic_debug_mlp(const dlic_model* m, const uint8_t* img, uint32_t width, uint32_t height,
+                           const dlic_opts* opts, float* logits, float* probs, uint16_t* freqs,
+                           uint32_t* fc);
+
+/* Library / device info: writes a short JSON string (device name, SM count,
+ * kernel variants) into buf.  Returns DLIC_E_BUFFER_TOO_SMALL if cap is short. */
+dlic_status dlic_info(char* buf, size_t cap);
+
+/* Per-kernel timing of the last call on this thread (milliseconds, CUDA
+ * events on the launching stream): names "mlp", "rans_enc", "compact",
+ * "decode".  Returns -1 when not measured.  Enabled by dlic_set_timing(1). */
+void dlic_set_timing(int enable);
+double dlic_last_kernel_ms(const char* name);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DLIC_H */

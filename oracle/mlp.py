@@ -1,0 +1,95 @@
+"""Dense density estimator (oracle; test infrastructure only).
+
+P:96 — "Our proposed model is a dense network consisting of six dense layers
+... The output layer consists of 256 neurons ... uses the softmax function as
+activation function. The number of neurons in the hidden layers varies between
+128 neurons to 4096 neurons per layer".  Eq. (1): the network maps
+the neighbourhood x_j..x_k to P(x_i | ...).
+
+Readings: hidden activation ReLU (R4); optional pooling omitted
+(Q6); presets P100K = 78->128x5->256 (109,184 params) and P350K = 78->256x5->256
+(349,184) matching Table I's ~100K / ~350K rows.
+
+Layers are (W [in][out] float32, b [out] float32).  This module returns the
+LOGITS (pre-softmax); softmax lives in quant.py.
+
+Precision variants:
+  forward_fp64   exact reference (fp64 throughout);
+  forward_fp32   numpy float32 matmul (checks fp32 is within 1e-6 of fp64);
+  forward_bf16   the bf16 path's plain definition: every matmul operand
+                 (inputs, activations, weights) rounded to bf16 (RN-even),
+                 products summed exactly (fp64), bias added in fp64;
+  logits_path    the value the codec uses: fp64 (precision 0) or bf16-emulated
+                 (precision 1) forward, rounded once to float32.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+P100K = (78, 128, 128, 128, 128, 128, 256)
+P350K = (78, 256, 256, 256, 256, 256, 256)
+
+
+def n_params(dims) -> int:
+    return sum(dims[i] * dims[i + 1] + dims[i + 1] for i in range(len(dims) - 1))
+
+
+def flops_per_pixel(dims) -> int:
+    """2 * sum K*N multiply-adds."""
+    return 2 * sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1))
+
+
+def forward_fp64(layers, x: np.ndarray) -> np.ndarray:
+    h = np.asarray(x, dtype=np.float64)
+    n = len(layers)
+    for i, (w, b) in enumerate(layers):
+        h = h @ np.asarray(w, np.float64) + np.asarray(b, np.float64)
+        if i < n - 1:
+            h = np.maximum(h, 0.0)
+    return h
+
+
+def forward_fp32(layers, x: np.ndarray) -> np.ndarray:
+    h = np.asarray(x, dtype=np.float32)
+    n = len(layers)
+    for i, (w, b) in enumerate(layers):
+        h = h @ np.asarray(w, np.float32) + np.asarray(b, np.float32)
+        if i < n - 1:
+            h = np.maximum(h, np.float32(0))
+    return h
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    """Round float values to the nearest bfloat16 (ties to even), returned as
+    float64.  Plain definition on the float32 bit pattern: keep the top 16
+    bits after adding 0x7FFF + lsb (finite inputs only)."""
+    f = np.asarray(a, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    lsb = (u >> 16) & 1
+    u = ((u + 0x7FFF + lsb) >> 16) << 16
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def forward_bf16(layers, x: np.ndarray) -> np.ndarray:
+    """bf16 operands, exact (fp64) accumulation; activations re-rounded to
+    bf16 after bias+ReLU computed in fp32 (the GPU epilogue's precision)."""
+    h = bf16_round(np.asarray(x, dtype=np.float64))
+    n = len(layers)
+    for i, (w, b) in enumerate(layers):
+        acc = h @ bf16_round(w)
+        z = (acc.astype(np.float32) + np.asarray(b, np.float32)).astype(np.float64)
+        if i < n - 1:
+            h = bf16_round(np.maximum(z, 0.0))
+        else:
+            h = z
+    return h
+
+
+def logits_path(layers, x: np.ndarray, precision: int) -> np.ndarray:
+    """Logits used by the oracle codec: fp64 (0) or bf16 emulation (1), as fp32."""
+    if precision == 0:
+        return forward_fp64(layers, x).astype(np.float32)
+    if precision == 1:
+        return forward_bf16(layers, x).astype(np.float32)
+    raise ValueError("precision")

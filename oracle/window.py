@@ -1,0 +1,69 @@
+"""Causal neighbourhood window (oracle; test infrastructure only).
+
+PAPER.md:63 — the neighbourhood window "is masked to only contain the already
+decoded pixels"; P:290 (Fig. 6 caption) — "A 9-by-9 window was used; the target
+pixel is located in the last row, third to last column".  P:59 (Fig. 1 right)
+— pixels outside the image "are substituted with dummy values".
+
+Readings (R1/R2):
+  * the 9x9 box spans dr in [-8, 0], dc in [-6, +2] around the target;
+  * cells at or after the target in raster order ((0,0), (0,1), (0,2)) are
+    masked out and dropped, leaving 78 inputs in row-major order;
+  * the dummy value is pixel value 0; features are v / 256.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+BOX_ROWS = 9
+BOX_COLS = 9
+TARGET_ROW = BOX_ROWS - 1          # last row
+TARGET_COL = BOX_COLS - 3          # third-to-last column
+FILL = 0                           # dummy value (reading R2)
+
+
+def _offsets():
+    offs = []
+    for br in range(BOX_ROWS):
+        for bc in range(BOX_COLS):
+            dr, dc = br - TARGET_ROW, bc - TARGET_COL
+            # raster-order causality mask
+            if dr < 0 or (dr == 0 and dc < 0):
+                offs.append((dr, dc))
+    return tuple(offs)
+
+
+OFFSETS = _offsets()               # 78 (dr, dc) pairs, row-major over the box
+N_INPUTS = len(OFFSETS)
+
+
+def gather(img: np.ndarray, r: int, c: int, fill: int = FILL) -> np.ndarray:
+    """Window values x_j = img[r+dr_j, c+dc_j] (or `fill` outside)."""
+    h, w = img.shape
+    out = np.empty(N_INPUTS, dtype=np.int64)
+    for j, (dr, dc) in enumerate(OFFSETS):
+        rr, cc = r + dr, c + dc
+        out[j] = img[rr, cc] if (0 <= rr < h and 0 <= cc < w) else fill
+    return out
+
+
+def gather_many(img: np.ndarray, rows: np.ndarray, cols: np.ndarray, fill: int = FILL) -> np.ndarray:
+    """Vectorised `gather` for many targets: returns (n, 78) int64.
+
+    Same definition as `gather`: pads the image by the box extent with `fill`
+    and indexes; pinned against `gather` in tests.
+    """
+    h, w = img.shape
+    pad = np.full((h + 8, w + 8), fill, dtype=np.int64)   # 8 above, 6 left, 2 right
+    pad[8:8 + h, 6:6 + w] = img
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    dr = np.array([o[0] for o in OFFSETS], dtype=np.int64)
+    dc = np.array([o[1] for o in OFFSETS], dtype=np.int64)
+    return pad[(rows[:, None] + dr[None, :] + 8), (cols[:, None] + dc[None, :] + 6)]
+
+
+def features(x: np.ndarray) -> np.ndarray:
+    """Network inputs v / 256 (reading R2; exact in fp32 and bf16)."""
+    return np.asarray(x, dtype=np.float64) / 256.0

@@ -1,0 +1,47 @@
+"""Write fixture weights with the ORACLE trainer only (no GPU code involved).
+
+fixtures/p100k_trained.dlicmdl — P100K (78->128x5->256) briefly trained on
+synthetic "natural-like" crops (SURVEY §8(d) C2 generator, sigma_tex=2,
+sigma_n=1), as north_star allows ("briefly trained by the oracle on synthetic
+smooth-plus-noise images").  Run: python scripts/make_fixtures.py
+"""
+
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import synth  # noqa: E402
+from oracle import mlp, model_io, train  # noqa: E402
+
+
+def main():
+    rng = np.random.default_rng(12345)
+    crops = []
+    for s in range(16):
+        img = synth.natural_like(768, 512, seed=1000 + s)
+        for _ in range(6):
+            y = int(rng.integers(0, 512 - 128))
+            x = int(rng.integers(0, 768 - 128))
+            crops.append(np.ascontiguousarray(img[y:y + 128, x:x + 128]))
+    x, y = train.dataset(crops)
+    held = synth.natural_like(768, 512, seed=999)
+    xv, yv = train.dataset([held[:128, :256]])
+    layers = synth.he_uniform_layers(mlp.P100K, seed=7)
+    t = time.time()
+    layers, hist = train.train(layers, x, y, epochs=int(os.environ.get("EPOCHS", "16")), batch=4096,
+                               lr=1e-3, seed=0)
+    print("train %.1fs loss/epoch %s" % (time.time() - t, ["%.3f" % h for h in hist]))
+    print("held-out vloss %.4f bits" % train.vloss_bits(layers, xv, yv))
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "fixtures",
+                       "p100k_trained.dlicmdl")
+    with open(out, "wb") as fh:
+        fh.write(model_io.save(layers))
+    print("wrote", out)
+
+
+if __name__ == "__main__":
+    main()
