@@ -1,0 +1,298 @@
+"""Thin Python binding of libdlic.so (include/dlic.h) — argument marshalling only.
+
+Every function here has the name of the C entry point it wraps and does no
+pixel-level work: the window gather, density estimator, softmax/quantiser,
+rANS lanes, wavefront and stream compaction all run in the CUDA kernels of
+csrc/.  NumPy carries host arrays; PyTorch is used only for device memory and
+streams in the *_batch_device variants.  There is no CPU fallback: importing
+this package without the built library raises ImportError.
+
+Paper: arXiv 2207.05152 (DLIC) — encode(image, weights) -> bitstream,
+decode(bitstream, weights) -> image (Fig. 2).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdlic.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError("libdlic.so not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(nvcc -gencode arch=compute_100a,code=sm_100a)")
+_lib = ctypes.CDLL(LIB_PATH)
+
+PREC_FP32 = 0
+PREC_BF16 = 1
+
+c_u8p = ctypes.POINTER(ctypes.c_uint8)
+c_u8pp = ctypes.POINTER(c_u8p)
+
+
+class dlic_opts(ctypes.Structure):
+    _fields_ = [("precision", ctypes.c_uint32), ("group_rows", ctypes.c_uint32),
+                ("tile_w", ctypes.c_uint32), ("tile_h", ctypes.c_uint32)]
+
+
+class dlic_header(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_uint32), ("height", ctypes.c_uint32), ("precision", ctypes.c_uint32),
+                ("group_rows", ctypes.c_uint32), ("tile_w", ctypes.c_uint32), ("tile_h", ctypes.c_uint32),
+                ("n_streams", ctypes.c_uint32), ("n_units", ctypes.c_uint32),
+                ("model_sha256", ctypes.c_uint8 * 32),
+                ("payload_bytes", ctypes.c_uint64), ("header_bytes", ctypes.c_uint64)]
+
+
+def _sig(name, res, *args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_vp = ctypes.c_void_p
+_st = ctypes.c_int
+_sig("dlic_status_str", ctypes.c_char_p, _st)
+_sig("dlic_last_error", ctypes.c_char_p)
+_sig("dlic_free", None, _vp)
+_sig("dlic_model_load", _st, _vp, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(_vp))
+_sig("dlic_model_from_arrays", _st, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32),
+     ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.c_int, ctypes.POINTER(_vp))
+_sig("dlic_model_free", None, _vp)
+_sig("dlic_model_sha256", _st, _vp, _vp)
+_sig("dlic_model_blob_check", _st, _vp, ctypes.c_size_t, _vp)
+_sig("dlic_encode", _st, _vp, _vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_size_t,
+     ctypes.POINTER(dlic_opts), c_u8pp, ctypes.POINTER(ctypes.c_size_t))
+_sig("dlic_decode", _st, _vp, _vp, ctypes.c_size_t, _vp, ctypes.c_size_t)
+_sig("dlic_peek", _st, _vp, ctypes.c_size_t, ctypes.POINTER(dlic_header))
+_sig("dlic_max_container_bytes", ctypes.c_size_t, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(dlic_opts))
+_sig("dlic_encode_batch_device", _st, _vp, _vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+     ctypes.POINTER(dlic_opts), _vp, ctypes.c_size_t, _vp, _vp)
+_sig("dlic_decode_batch_device", _st, _vp, _vp, _vp, ctypes.c_uint32, ctypes.POINTER(dlic_header), _vp, _vp, _vp)
+_sig("dlic_rans_encode_tables", _st, _vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(dlic_opts), _vp,
+     c_u8pp, ctypes.POINTER(ctypes.c_size_t))
+_sig("dlic_rans_decode_tables", _st, _vp, ctypes.c_size_t, _vp, _vp)
+_sig("dlic_debug_mlp", _st, _vp, _vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(dlic_opts),
+     _vp, _vp, _vp, _vp)
+_sig("dlic_info", _st, ctypes.c_char_p, ctypes.c_size_t)
+_sig("dlic_set_timing", None, ctypes.c_int)
+_sig("dlic_last_kernel_ms", ctypes.c_double, ctypes.c_char_p)
+
+
+class DlicError(RuntimeError):
+    def __init__(self, status, detail):
+        self.status = int(status)
+        super().__init__("%s (%d): %s" % (_lib.dlic_status_str(status).decode(), status, detail))
+
+
+STATUS = {0: "DLIC_OK", 1: "DLIC_E_INVALID_ARG", 2: "DLIC_E_SHAPE_MISMATCH", 3: "DLIC_E_NONCAUSAL_WINDOW",
+          4: "DLIC_E_CORRUPT_MODEL", 5: "DLIC_E_VERSION_MISMATCH", 6: "DLIC_E_CORRUPT_CONTAINER",
+          7: "DLIC_E_MODEL_HASH_MISMATCH", 8: "DLIC_E_STREAM_UNDERFLOW", 9: "DLIC_E_SUM_MISMATCH",
+          10: "DLIC_E_ZERO_FREQUENCY", 11: "DLIC_E_BUFFER_TOO_SMALL", 12: "DLIC_E_CUDA",
+          13: "DLIC_E_OUT_OF_MEMORY", 14: "DLIC_E_UNSUPPORTED_MODEL"}
+
+
+def _check(s):
+    if s != 0:
+        raise DlicError(s, _lib.dlic_last_error().decode(errors="replace"))
+
+
+def _opts(precision=PREC_BF16, group_rows=32, tile=(0, 0)):
+    return dlic_opts(precision, group_rows, tile[0], tile[1])
+
+
+def _take(ptr, n) -> bytes:
+    b = ctypes.string_at(ptr, n)
+    _lib.dlic_free(ptr)
+    return b
+
+
+class Model:
+    """Owns a dlic_model* (uploaded weights)."""
+
+    def __init__(self, handle, device):
+        self._h = _vp(handle)
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def sha256(self) -> bytes:
+        out = (ctypes.c_uint8 * 32)()
+        _check(_lib.dlic_model_sha256(self._h, out))
+        return bytes(out)
+
+    def close(self):
+        if self._h:
+            _lib.dlic_model_free(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------ models
+def dlic_model_load(blob: bytes, device: int = 0) -> Model:
+    h = _vp()
+    buf = ctypes.create_string_buffer(blob, len(blob))
+    _check(_lib.dlic_model_load(buf, len(blob), device, ctypes.byref(h)))
+    return Model(h.value, device)
+
+
+def dlic_model_from_arrays(layers, device: int = 0) -> Model:
+    dims = [layers[0][0].shape[0]] + [w.shape[1] for w, _ in layers]
+    ws = [np.ascontiguousarray(w, np.float32) for w, _ in layers]
+    bs = [np.ascontiguousarray(b, np.float32) for _, b in layers]
+    cd = (ctypes.c_uint32 * len(dims))(*dims)
+    wp = (_vp * len(ws))(*[w.ctypes.data for w in ws])
+    bp = (_vp * len(bs))(*[b.ctypes.data for b in bs])
+    h = _vp()
+    _check(_lib.dlic_model_from_arrays(len(ws), cd, wp, bp, device, ctypes.byref(h)))
+    return Model(h.value, device)
+
+
+def dlic_model_blob_check(blob: bytes) -> bytes:
+    out = (ctypes.c_uint8 * 32)()
+    buf = ctypes.create_string_buffer(blob, len(blob))
+    _check(_lib.dlic_model_blob_check(buf, len(blob), out))
+    return bytes(out)
+
+
+# ------------------------------------------------------------------ codec
+def dlic_encode(model: Model, img: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0)) -> bytes:
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    assert img.ndim == 2
+    h, w = img.shape
+    out = c_u8p()
+    n = ctypes.c_size_t()
+    o = _opts(precision, group_rows, tile)
+    _check(_lib.dlic_encode(model.handle, img.ctypes.data, w, h, w, ctypes.byref(o), ctypes.byref(out),
+                            ctypes.byref(n)))
+    return _take(out, n.value)
+
+
+def dlic_peek(bits: bytes) -> dict:
+    hd = dlic_header()
+    _check(_lib.dlic_peek(bits, len(bits), ctypes.byref(hd)))
+    d = {k: getattr(hd, k) for k, _ in dlic_header._fields_ if k != "model_sha256"}
+    d["model_sha256"] = bytes(hd.model_sha256)
+    return d
+
+
+def dlic_decode(model: Model, bits: bytes) -> np.ndarray:
+    hd = dlic_peek(bits)
+    img = np.empty((hd["height"], hd["width"]), np.uint8)
+    _check(_lib.dlic_decode(model.handle, bits, len(bits), img.ctypes.data, img.size))
+    return img
+
+
+def dlic_max_container_bytes(width, height, precision=PREC_BF16, group_rows=32, tile=(0, 0)) -> int:
+    o = _opts(precision, group_rows, tile)
+    return int(_lib.dlic_max_container_bytes(width, height, ctypes.byref(o)))
+
+
+# ------------------------------------------------------------------ parity taps
+def dlic_rans_encode_tables(fc: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0),
+                            model_sha: bytes | None = None) -> bytes:
+    fc = np.ascontiguousarray(fc, dtype=np.uint32)
+    h, w = fc.shape
+    out = c_u8p()
+    n = ctypes.c_size_t()
+    o = _opts(precision, group_rows, tile)
+    sha = ctypes.create_string_buffer(model_sha, 32) if model_sha else None
+    _check(_lib.dlic_rans_encode_tables(fc.ctypes.data, w, h, ctypes.byref(o), sha, ctypes.byref(out),
+                                        ctypes.byref(n)))
+    return _take(out, n.value)
+
+
+def dlic_rans_decode_tables(bits: bytes, freq_tables: np.ndarray) -> np.ndarray:
+    hd = dlic_peek(bits)
+    ft = np.ascontiguousarray(freq_tables, dtype=np.uint16)
+    assert ft.shape == (hd["height"], hd["width"], 256)
+    img = np.empty((hd["height"], hd["width"]), np.uint8)
+    _check(_lib.dlic_rans_decode_tables(bits, len(bits), ft.ctypes.data, img.ctypes.data))
+    return img
+
+
+def dlic_debug_mlp(model: Model, img: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0),
+                   logits=True, probs=True, freqs=True, fc=True) -> dict:
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    h, w = img.shape
+    out = {}
+    lg = np.empty((h, w, 256), np.float32) if logits else None
+    pb = np.empty((h, w, 256), np.float32) if probs else None
+    fq = np.empty((h, w, 256), np.uint16) if freqs else None
+    f = np.empty((h, w), np.uint32) if fc else None
+    o = _opts(precision, group_rows, tile)
+    _check(_lib.dlic_debug_mlp(model.handle, img.ctypes.data, w, h, ctypes.byref(o),
+                               lg.ctypes.data if logits else None, pb.ctypes.data if probs else None,
+                               fq.ctypes.data if freqs else None, f.ctypes.data if fc else None))
+    for k, v in (("logits", lg), ("probs", pb), ("freqs", fq), ("fc", f)):
+        if v is not None:
+            out[k] = v
+    return out
+
+
+# ------------------------------------------------------------------ device batch (torch memory/streams)
+def _stream_handle(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return _vp(s.cuda_stream)
+
+
+def dlic_encode_batch_device(model: Model, d_imgs, precision=PREC_BF16, group_rows=32, tile=(0, 0),
+                             d_out=None, d_sizes=None, stream=None):
+    """d_imgs: torch uint8 CUDA tensor (n, H, W).  Returns (d_out, d_sizes, stride):
+    container i occupies d_out[i*stride : i*stride + d_sizes[i]]."""
+    import torch
+    n, h, w = d_imgs.shape
+    stride = dlic_max_container_bytes(w, h, precision, group_rows, tile)
+    if stride == 0:
+        raise DlicError(1, "unsupported options")
+    if d_out is None:
+        d_out = torch.empty(n * stride, dtype=torch.uint8, device=d_imgs.device)
+    if d_sizes is None:
+        d_sizes = torch.empty(n, dtype=torch.int64, device=d_imgs.device)
+    o = _opts(precision, group_rows, tile)
+    _check(_lib.dlic_encode_batch_device(model.handle, _vp(d_imgs.data_ptr()), n, w, h, ctypes.byref(o),
+                                         _vp(d_out.data_ptr()), d_out.numel(), _vp(d_sizes.data_ptr()),
+                                         _stream_handle(stream)))
+    return d_out, d_sizes, stride
+
+
+def dlic_decode_batch_device(model: Model, d_bits, h_offsets, header: dict, d_imgs, d_status=None, stream=None):
+    """d_bits: torch uint8 CUDA tensor holding n containers at byte offsets
+    h_offsets (host ints); header: dlic_peek() of container 0; d_imgs: torch
+    uint8 CUDA (n, H, W) output; d_status: optional int32 CUDA (n,) zeroed."""
+    offs = np.ascontiguousarray(np.asarray(h_offsets, dtype=np.uint64))
+    hd = dlic_header()
+    for k, _ in dlic_header._fields_:
+        if k == "model_sha256":
+            ctypes.memmove(hd.model_sha256, header["model_sha256"], 32)
+        else:
+            setattr(hd, k, header[k])
+    _check(_lib.dlic_decode_batch_device(model.handle, _vp(d_bits.data_ptr()), offs.ctypes.data, len(offs),
+                                         ctypes.byref(hd), _vp(d_imgs.data_ptr()),
+                                         _vp(d_status.data_ptr()) if d_status is not None else None,
+                                         _stream_handle(stream)))
+
+
+# ------------------------------------------------------------------ misc
+def dlic_info() -> str:
+    buf = ctypes.create_string_buffer(1024)
+    _check(_lib.dlic_info(buf, 1024))
+    return buf.value.decode()
+
+
+def dlic_set_timing(enable: bool):
+    _lib.dlic_set_timing(1 if enable else 0)
+
+
+def dlic_last_kernel_ms(name: str) -> float:
+    return float(_lib.dlic_last_kernel_ms(name.encode()))

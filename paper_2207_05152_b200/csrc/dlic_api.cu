@@ -1,0 +1,785 @@
+// dlic_api.cpp — the C-ABI of libdlic.so (include/dlic.h).
+//
+// Host side only: model parsing and SHA-256, weight packing
+// into the tcgen05 shared-memory image, planning (units, groups, decode
+// cluster size), the container framing, scratch
+// management and kernel launches.  Every pixel-level step runs in the CUDA
+// kernels of dlic_kernels.cu; there is no CPU fallback.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dlic.h"
+#include "dlic_device.cuh"
+#include "dlic_internal.h"
+#include "sha256.h"
+
+using namespace dlic;
+
+struct dlic_model {
+  int device = 0;
+  std::vector<uint8_t> blob;  // the "DLICMDL1" bytes
+  uint8_t sha[32];
+  std::vector<uint32_t> dims;
+  bool p100k = false;
+  uint8_t* d_wimg = nullptr;
+  float* d_bias = nullptr;
+  float* d_w32 = nullptr;
+  DevWeights dw() const { return DevWeights{d_wimg, d_bias, d_w32}; }
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local bool g_timing = false;
+
+dlic_status fail(dlic_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      return fail(e_ == cudaErrorMemoryAllocation ? DLIC_E_OUT_OF_MEMORY : DLIC_E_CUDA,  \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));                   \
+    }                                                                                    \
+  } while (0)
+
+// ---------------------------------------------------------------- timing
+struct EvPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  bool used = false;
+};
+thread_local std::map<std::string, EvPair> g_ev;
+void ev_begin(const char* name, cudaStream_t st) {
+  if (!g_timing) return;
+  EvPair& e = g_ev[name];
+  if (!e.a) {
+    cudaEventCreate(&e.a);
+    cudaEventCreate(&e.b);
+  }
+  cudaEventRecord(e.a, st);
+}
+void ev_end(const char* name, cudaStream_t st) {
+  if (!g_timing) return;
+  EvPair& e = g_ev[name];
+  cudaEventRecord(e.b, st);
+  e.used = true;
+}
+
+// ---------------------------------------------------------------- device info
+int num_sms(int dev) {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> l(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  cache[dev] = n;
+  return n;
+}
+
+dlic_status check_device(int dev) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return fail(DLIC_E_CUDA, "no CUDA device");
+  if (dev < 0 || dev >= n) return fail(DLIC_E_INVALID_ARG, "bad cuda_device");
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10) return fail(DLIC_E_CUDA, "libdlic kernels are built for sm_100a (B200)");
+  CUDA_TRY(cudaSetDevice(dev));
+  static std::once_flag once[64];
+  if (dev < 64)
+    std::call_once(once[dev], [dev] {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+    });
+  return DLIC_OK;
+}
+
+cudaStream_t my_stream() {
+  thread_local cudaStream_t s = nullptr;
+  thread_local int dev = -1;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (!s || dev != cur) {
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    dev = cur;
+  }
+  return s;
+}
+
+// pinned staging buffers (per thread, grown on demand)
+struct Pinned {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t n) {
+    if (n > cap) {
+      if (p) cudaFreeHost(p);
+      cap = std::max(n, (size_t)1 << 20);
+      if (cudaMallocHost(&p, cap) != cudaSuccess) {
+        p = nullptr;
+        cap = 0;
+      }
+    }
+    return p;
+  }
+};
+thread_local Pinned g_pin_in, g_pin_out;
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// stream-ordered scratch freed at scope exit
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  ~Scratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+  template <class T>
+  cudaError_t alloc(T** out, size_t bytes) {
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 16, st);
+    if (e == cudaSuccess) ptrs.push_back(p);
+    *out = reinterpret_cast<T*>(p);
+    return e;
+  }
+};
+
+// ---------------------------------------------------------------- model parsing
+uint32_t rd32(const uint8_t* p) { return p[0] | (p[1] << 8) | (p[2] << 16) | ((uint32_t)p[3] << 24); }
+uint16_t rd16(const uint8_t* p) { return (uint16_t)(p[0] | (p[1] << 8)); }
+
+struct ParsedModel {
+  std::vector<uint32_t> dims;
+  std::vector<std::vector<float>> W, b;
+};
+
+dlic_status parse_model(const uint8_t* d, size_t len, ParsedModel& pm, uint8_t sha_out[32]) {
+  if (!d || len < 8 + 2 + 2 + 32 || memcmp(d, "DLICMDL1", 8) != 0) return fail(DLIC_E_CORRUPT_MODEL, "model magic");
+  uint8_t h[32];
+  sha256(d, len - 32, h);
+  if (memcmp(h, d + len - 32, 32) != 0) return fail(DLIC_E_CORRUPT_MODEL, "model SHA-256 mismatch");
+  const size_t body = len - 32;
+  size_t off = 8;
+  const uint32_t nl = rd16(d + off);
+  off += 2;
+  if (nl == 0 || nl > 64) return fail(DLIC_E_CORRUPT_MODEL, "layer count");
+  for (uint32_t l = 0; l < nl; ++l) {
+    if (off + 10 > body) return fail(DLIC_E_CORRUPT_MODEL, "truncated layer header");
+    const uint32_t in = rd32(d + off), outd = rd32(d + off + 4);
+    off += 10;
+    if (l == 0) pm.dims.push_back(in);
+    else if (pm.dims.back() != in) return fail(DLIC_E_CORRUPT_MODEL, "layer dims do not chain");
+    pm.dims.push_back(outd);
+    const size_t nw = (size_t)in * outd;
+    if (in == 0 || outd == 0 || off + 4 * (nw + outd) > body) return fail(DLIC_E_CORRUPT_MODEL, "truncated weights");
+    std::vector<float> w(nw), bb(outd);
+    memcpy(w.data(), d + off, 4 * nw);
+    off += 4 * nw;
+    memcpy(bb.data(), d + off, 4 * outd);
+    off += 4 * outd;
+    pm.W.push_back(std::move(w));
+    pm.b.push_back(std::move(bb));
+  }
+  if (off + 2 > body) return fail(DLIC_E_CORRUPT_MODEL, "truncated meta");
+  const uint32_t nmeta = rd16(d + off);
+  off += 2 + 8 * (size_t)nmeta;
+  if (off != body) return fail(DLIC_E_CORRUPT_MODEL, "model length");
+  if (sha_out) memcpy(sha_out, h, 32);
+  return DLIC_OK;
+}
+
+uint16_t bf16_bits(float f) {
+  __nv_bfloat16 h = __float2bfloat16_rn(f);
+  uint16_t u;
+  memcpy(&u, &h, 2);
+  return u;
+}
+
+dlic_status upload_model(dlic_model* m, const ParsedModel& pm) {
+  const uint32_t want[7] = {KIN, HID, HID, HID, HID, HID, NOUT};
+  m->p100k = pm.dims.size() == 7 && std::equal(pm.dims.begin(), pm.dims.end(), want);
+  m->dims = pm.dims;
+  if (!m->p100k) return DLIC_OK;  // loadable; GPU engines refuse it at encode/decode
+  // bf16 UMMA image: layer l, element (n, k) of B = W^T at
+  // (k/8)*(N/8)*128 + (n/8)*128 + (n%8)*16 + (k%8)*2   (K-major, no swizzle)
+  std::vector<uint8_t> img(WIMG_BYTES, 0);
+  for (int l = 0; l < NLAYER; ++l) {
+    const int K = layer_k(l), N = layer_n(l), Kr = (int)pm.dims[l];
+    for (int k = 0; k < K; ++k)
+      for (int n = 0; n < N; ++n) {
+        const float v = k < Kr ? pm.W[l][(size_t)k * N + n] : 0.0f;
+        const uint16_t u = bf16_bits(v);
+        const size_t a = wimg_off(l) + (size_t)(k / 8) * (N / 8) * 128 + (size_t)(n / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
+        memcpy(&img[a], &u, 2);
+      }
+  }
+  std::vector<float> bias(BIAS_TOTAL);
+  for (int l = 0; l < NLAYER; ++l)
+    for (int n = 0; n < layer_n(l); ++n) bias[(l < NLAYER - 1 ? l * HID : BIAS_OFF_LAST) + n] = pm.b[l][n];
+  std::vector<float> w32(f32_off(NLAYER));
+  for (int l = 0; l < NLAYER; ++l) {
+    const int K = f32_k(l), N = layer_n(l);
+    memcpy(&w32[f32_off(l)], pm.W[l].data(), 4 * (size_t)K * N);
+    memcpy(&w32[f32_off(l) + (size_t)K * N], pm.b[l].data(), 4 * (size_t)N);
+  }
+  CUDA_TRY(cudaMalloc(&m->d_wimg, WIMG_BYTES));
+  CUDA_TRY(cudaMalloc(&m->d_bias, bias.size() * 4));
+  CUDA_TRY(cudaMalloc(&m->d_w32, w32.size() * 4));
+  CUDA_TRY(cudaMemcpy(m->d_wimg, img.data(), WIMG_BYTES, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(m->d_bias, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(m->d_w32, w32.data(), w32.size() * 4, cudaMemcpyHostToDevice));
+  return DLIC_OK;
+}
+
+// ---------------------------------------------------------------- planning
+dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Plan& p) {
+  dlic_opts d = {DLIC_PREC_BF16, 32, 0, 0};
+  if (o) d = *o;
+  if (d.group_rows == 0) d.group_rows = 32;
+  if (W == 0 || H == 0 || n == 0) return fail(DLIC_E_INVALID_ARG, "empty image or batch");
+  if (W > 65535 * 16 || H > 65535 * 16) return fail(DLIC_E_INVALID_ARG, "image too large");
+  if (d.precision > 1) return fail(DLIC_E_INVALID_ARG, "precision must be 0 (fp32) or 1 (bf16)");
+  if (32 % d.group_rows != 0) return fail(DLIC_E_INVALID_ARG, "GPU path supports group_rows in {1,2,4,8,16,32}");
+  const bool tiled = d.tile_w != 0 && d.tile_h != 0;
+  if (tiled && (d.tile_w > 65535 || d.tile_h > 65535)) return fail(DLIC_E_INVALID_ARG, "tile too large");
+  p = Plan{};
+  p.W = W;
+  p.H = H;
+  p.n_img = n;
+  p.G = d.group_rows;
+  p.precision = d.precision;
+  p.tw = tiled ? std::min(d.tile_w, W) : W;
+  p.th = tiled ? std::min(d.tile_h, H) : H;
+  p.hdr_tw = tiled ? d.tile_w : 0;
+  p.hdr_th = tiled ? d.tile_h : 0;
+  p.ntx = (W + p.tw - 1) / p.tw;
+  p.nty = (H + p.th - 1) / p.th;
+  p.upi = p.ntx * p.nty;
+  p.gpt = (p.th + p.G - 1) / p.G;
+  const uint32_t hl = H - (p.nty - 1) * p.th;
+  p.gpl = (hl + p.G - 1) / p.G;
+  p.spi = (p.nty - 1) * p.ntx * p.gpt + p.ntx * p.gpl;
+  if (p.gpt > 1024) return fail(DLIC_E_INVALID_ARG, "more than 1024 groups per unit: raise group_rows or tile");
+  p.cap_words = 2 * p.G + p.G * p.tw;
+  p.hdr_bytes = 58 + 4 * p.spi;
+  p.tiles_per_unit = (uint32_t)(((uint64_t)p.tw * p.th + 127) / 128);
+  const uint32_t slots = (p.tw + 2) / 3;  // max rows on one front = ceil(tw/3)
+  p.nc = slots <= 128 ? 1 : slots <= 256 ? 2 : slots <= 512 ? 4 : slots <= 1024 ? 8 : 0;
+  if (p.nc == 0) return fail(DLIC_E_INVALID_ARG, "unit wider than 3072 px: use tiles (tile_w <= 3072)");
+  uint64_t mc = p.hdr_bytes;
+  mc += (uint64_t)p.spi * (4ull * p.G + 2ull * p.G * p.tw);
+  p.max_container = (mc + 15) & ~15ull;
+  return DLIC_OK;
+}
+
+dlic_status check_model_gpu(const dlic_model* m) {
+  if (!m) return fail(DLIC_E_INVALID_ARG, "null model");
+  if (!m->p100k) return fail(DLIC_E_UNSUPPORTED_MODEL, "GPU engines implement 78->128x5->256 (P100K)");
+  return check_device(m->device);
+}
+
+// ---------------------------------------------------------------- header parse
+dlic_status peek(const uint8_t* b, size_t len, dlic_header* h, std::vector<uint32_t>* sizes) {
+  if (!b || len < 58) return fail(DLIC_E_CORRUPT_CONTAINER, "container shorter than its header");
+  if (memcmp(b, "DLIC", 4) != 0) return fail(DLIC_E_CORRUPT_CONTAINER, "container magic");
+  if (b[4] != 1 || b[6] != 1) return fail(DLIC_E_VERSION_MISMATCH, "container version/window");
+  if (b[7] != 0 || b[5] > 1) return fail(DLIC_E_CORRUPT_CONTAINER, "container fill/precision");
+  dlic_header o = {};
+  o.width = rd32(b + 8);
+  o.height = rd32(b + 12);
+  o.tile_w = rd16(b + 16);
+  o.tile_h = rd16(b + 18);
+  o.group_rows = rd16(b + 20);
+  o.precision = b[5];
+  memcpy(o.model_sha256, b + 22, 32);
+  o.n_streams = rd32(b + 54);
+  if (o.width == 0 || o.height == 0 || o.group_rows == 0) return fail(DLIC_E_CORRUPT_CONTAINER, "header dims");
+  if ((uint64_t)58 + 4ull * o.n_streams > len) return fail(DLIC_E_CORRUPT_CONTAINER, "size table");
+  o.header_bytes = 58 + 4ull * o.n_streams;
+  uint64_t tot = 0;
+  if (sizes) sizes->resize(o.n_streams);
+  for (uint32_t s = 0; s < o.n_streams; ++s) {
+    const uint32_t z = rd32(b + 58 + 4 * s);
+    if (z & 1) return fail(DLIC_E_CORRUPT_CONTAINER, "odd stream size");
+    tot += z;
+    if (sizes) (*sizes)[s] = z;
+  }
+  if (o.header_bytes + tot != len) return fail(DLIC_E_CORRUPT_CONTAINER, "container length");
+  o.payload_bytes = tot;
+  const bool tiled = o.tile_w && o.tile_h;
+  const uint32_t tw = tiled ? std::min<uint32_t>(o.tile_w, o.width) : o.width;
+  const uint32_t th = tiled ? std::min<uint32_t>(o.tile_h, o.height) : o.height;
+  o.n_units = ((o.width + tw - 1) / tw) * ((o.height + th - 1) / th);
+  *h = o;
+  return DLIC_OK;
+}
+
+dlic_opts opts_of(const dlic_header& h) {
+  dlic_opts o;
+  o.precision = h.precision;
+  o.group_rows = h.group_rows;
+  o.tile_w = h.tile_w;
+  o.tile_h = h.tile_h;
+  return o;
+}
+
+// copy a host buffer to device through pinned staging when needed
+cudaError_t h2d(void* dst, const void* src, size_t n, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  if (is_pinned(src)) return cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st);
+  void* pin = g_pin_in.get(n);
+  if (!pin) return cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st);
+  cudaError_t e = cudaStreamSynchronize(st);  // staging buffer may still be in flight
+  if (e != cudaSuccess) return e;
+  memcpy(pin, src, n);
+  return cudaMemcpyAsync(dst, pin, n, cudaMemcpyHostToDevice, st);
+}
+
+// encode pipeline on device buffers (shared by dlic_encode and the batch API)
+dlic_status run_encode(const dlic_model* m, const Plan& p, const uint8_t* d_imgs, uint8_t* d_out, uint64_t stride,
+                       uint64_t* d_sizes, cudaStream_t st, Scratch& sc) {
+  uint32_t* d_fc;
+  uint16_t* d_scr;
+  uint32_t* d_words;
+  uint64_t* d_dst;
+  const uint64_t npx = (uint64_t)p.n_img * p.W * p.H;
+  const uint64_t ns = (uint64_t)p.n_img * p.spi;
+  CUDA_TRY(sc.alloc(&d_fc, 4 * npx));
+  CUDA_TRY(sc.alloc(&d_scr, 2ull * p.cap_words * ns));
+  CUDA_TRY(sc.alloc(&d_words, 4 * ns));
+  CUDA_TRY(sc.alloc(&d_dst, 8 * ns));
+  ev_begin("mlp", st);
+  CUDA_TRY(launch_enc_mlp(p, m->dw(), d_imgs, d_fc, nullptr, nullptr, nullptr, st, num_sms(m->device)));
+  ev_end("mlp", st);
+  ev_begin("rans_enc", st);
+  CUDA_TRY(launch_rans_enc(p, d_fc, d_scr, d_words, st));
+  ev_end("rans_enc", st);
+  ev_begin("compact", st);
+  CUDA_TRY(launch_container(p, m->sha, d_words, d_scr, d_out, stride, d_sizes, d_dst, st));
+  ev_end("compact", st);
+  return DLIC_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+const char* dlic_status_str(dlic_status s) {
+  switch (s) {
+    case DLIC_OK: return "ok";
+    case DLIC_E_INVALID_ARG: return "invalid argument";
+    case DLIC_E_SHAPE_MISMATCH: return "shape mismatch";
+    case DLIC_E_NONCAUSAL_WINDOW: return "non-causal window";
+    case DLIC_E_CORRUPT_MODEL: return "corrupt model";
+    case DLIC_E_VERSION_MISMATCH: return "version mismatch";
+    case DLIC_E_CORRUPT_CONTAINER: return "corrupt container";
+    case DLIC_E_MODEL_HASH_MISMATCH: return "model hash mismatch";
+    case DLIC_E_STREAM_UNDERFLOW: return "stream underflow";
+    case DLIC_E_SUM_MISMATCH: return "frequency sum mismatch";
+    case DLIC_E_ZERO_FREQUENCY: return "zero frequency";
+    case DLIC_E_BUFFER_TOO_SMALL: return "buffer too small";
+    case DLIC_E_CUDA: return "CUDA error";
+    case DLIC_E_OUT_OF_MEMORY: return "out of memory";
+    case DLIC_E_UNSUPPORTED_MODEL: return "unsupported model architecture";
+  }
+  return "unknown status";
+}
+
+const char* dlic_last_error(void) { return g_err.c_str(); }
+
+void dlic_free(void* p) { free(p); }
+
+dlic_status dlic_model_blob_check(const void* bytes, size_t len, uint8_t sha_out[32]) {
+  ParsedModel pm;
+  return parse_model(static_cast<const uint8_t*>(bytes), len, pm, sha_out);
+}
+
+dlic_status dlic_model_load(const void* bytes, size_t len, int cuda_device, dlic_model** out) {
+  if (!out) return fail(DLIC_E_INVALID_ARG, "null out");
+  ParsedModel pm;
+  uint8_t sha[32];
+  dlic_status s = parse_model(static_cast<const uint8_t*>(bytes), len, pm, sha);
+  if (s != DLIC_OK) return s;
+  s = check_device(cuda_device);
+  if (s != DLIC_OK) return s;
+  dlic_model* m = new dlic_model();
+  m->device = cuda_device;
+  m->blob.assign(static_cast<const uint8_t*>(bytes), static_cast<const uint8_t*>(bytes) + len);
+  memcpy(m->sha, sha, 32);
+  s = upload_model(m, pm);
+  if (s != DLIC_OK) {
+    dlic_model_free(m);
+    return s;
+  }
+  *out = m;
+  return DLIC_OK;
+}
+
+dlic_status dlic_model_from_arrays(uint32_t n_layers, const uint32_t* dims, const float* const* W,
+                                   const float* const* b, int cuda_device, dlic_model** out) {
+  if (!dims || !W || !b || n_layers == 0 || n_layers > 64) return fail(DLIC_E_INVALID_ARG, "bad arrays");
+  std::vector<uint8_t> blob(8);
+  memcpy(blob.data(), "DLICMDL1", 8);
+  auto put16 = [&](uint32_t v) { blob.push_back((uint8_t)v); blob.push_back((uint8_t)(v >> 8)); };
+  auto put32 = [&](uint32_t v) { for (int i = 0; i < 4; ++i) blob.push_back((uint8_t)(v >> (8 * i))); };
+  put16(n_layers);
+  for (uint32_t l = 0; l < n_layers; ++l) {
+    put32(dims[l]);
+    put32(dims[l + 1]);
+    blob.push_back(l + 1 < n_layers ? 1 : 0);
+    blob.push_back(0);
+    const uint8_t* wp = reinterpret_cast<const uint8_t*>(W[l]);
+    blob.insert(blob.end(), wp, wp + 4ull * dims[l] * dims[l + 1]);
+    const uint8_t* bp = reinterpret_cast<const uint8_t*>(b[l]);
+    blob.insert(blob.end(), bp, bp + 4ull * dims[l + 1]);
+  }
+  put16(0);
+  uint8_t h[32];
+  sha256(blob.data(), blob.size(), h);
+  blob.insert(blob.end(), h, h + 32);
+  return dlic_model_load(blob.data(), blob.size(), cuda_device, out);
+}
+
+void dlic_model_free(dlic_model* m) {
+  if (!m) return;
+  cudaSetDevice(m->device);
+  if (m->d_wimg) cudaFree(m->d_wimg);
+  if (m->d_bias) cudaFree(m->d_bias);
+  if (m->d_w32) cudaFree(m->d_w32);
+  delete m;
+}
+
+dlic_status dlic_model_sha256(const dlic_model* m, uint8_t out[32]) {
+  if (!m || !out) return fail(DLIC_E_INVALID_ARG, "null");
+  memcpy(out, m->sha, 32);
+  return DLIC_OK;
+}
+
+size_t dlic_max_container_bytes(uint32_t width, uint32_t height, const dlic_opts* opts) {
+  Plan p;
+  if (make_plan(width, height, 1, opts, p) != DLIC_OK) return 0;
+  return p.max_container;
+}
+
+dlic_status dlic_peek(const uint8_t* bits, size_t len, dlic_header* out) {
+  if (!out) return fail(DLIC_E_INVALID_ARG, "null out");
+  return peek(bits, len, out, nullptr);
+}
+
+dlic_status dlic_encode(const dlic_model* m, const uint8_t* img, uint32_t width, uint32_t height, size_t row_stride,
+                        const dlic_opts* opts, uint8_t** out, size_t* out_len) {
+  if (!img || !out || !out_len) return fail(DLIC_E_INVALID_ARG, "null pointer");
+  if (row_stride == 0) row_stride = width;
+  if (row_stride < width) return fail(DLIC_E_SHAPE_MISMATCH, "row_stride < width");
+  dlic_status s = check_model_gpu(m);
+  if (s != DLIC_OK) return s;
+  Plan p;
+  s = make_plan(width, height, 1, opts, p);
+  if (s != DLIC_OK) return s;
+  cudaStream_t st = my_stream();
+  Scratch sc(st);
+  uint8_t *d_img, *d_out;
+  uint64_t* d_size;
+  CUDA_TRY(sc.alloc(&d_img, (size_t)width * height));
+  CUDA_TRY(sc.alloc(&d_out, p.max_container));
+  CUDA_TRY(sc.alloc(&d_size, 8));
+  if (row_stride == width) {
+    CUDA_TRY(h2d(d_img, img, (size_t)width * height, st));
+  } else {
+    CUDA_TRY(cudaMemcpy2DAsync(d_img, width, img, row_stride, width, height, cudaMemcpyHostToDevice, st));
+  }
+  s = run_encode(m, p, d_img, d_out, p.max_container, d_size, st, sc);
+  if (s != DLIC_OK) return s;
+  uint64_t* hs = static_cast<uint64_t*>(g_pin_out.get(p.max_container + 64));
+  if (!hs) return fail(DLIC_E_OUT_OF_MEMORY, "pinned staging");
+  CUDA_TRY(cudaMemcpyAsync(hs, d_size, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  const uint64_t n = hs[0];
+  if (n > p.max_container) return fail(DLIC_E_CUDA, "container size out of range");
+  uint8_t* hb = reinterpret_cast<uint8_t*>(hs) + 64;
+  CUDA_TRY(cudaMemcpyAsync(hb, d_out, n, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  uint8_t* res = static_cast<uint8_t*>(malloc(n));
+  if (!res) return fail(DLIC_E_OUT_OF_MEMORY, "malloc");
+  memcpy(res, hb, n);
+  *out = res;
+  *out_len = n;
+  return DLIC_OK;
+}
+
+static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_t len, const uint16_t* tables,
+                                 uint8_t* img, size_t cap) {
+  dlic_header h;
+  dlic_status s = peek(bits, len, &h, nullptr);
+  if (s != DLIC_OK) return s;
+  if (m && memcmp(h.model_sha256, m->sha, 32) != 0)
+    return fail(DLIC_E_MODEL_HASH_MISMATCH, "container was coded with another model");
+  if (!img || cap < (size_t)h.width * h.height) return fail(DLIC_E_BUFFER_TOO_SMALL, "image buffer");
+  if (m) {
+    s = check_model_gpu(m);
+  } else {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    s = check_device(dev);
+  }
+  if (s != DLIC_OK) return s;
+  dlic_opts o = opts_of(h);
+  Plan p;
+  s = make_plan(h.width, h.height, 1, &o, p);
+  if (s != DLIC_OK) return s;
+  if (p.spi != h.n_streams) return fail(DLIC_E_CORRUPT_CONTAINER, "stream count does not match the header dims");
+  cudaStream_t st = my_stream();
+  Scratch sc(st);
+  uint8_t *d_bits, *d_img;
+  uint32_t *d_sbase, *d_slen;
+  int32_t* d_status;
+  uint64_t* d_meta;  // [0] = container offset (0), [1] = length
+  CUDA_TRY(sc.alloc(&d_bits, len));
+  CUDA_TRY(sc.alloc(&d_img, (size_t)h.width * h.height));
+  CUDA_TRY(sc.alloc(&d_sbase, 4ull * p.spi));
+  CUDA_TRY(sc.alloc(&d_slen, 4ull * p.spi));
+  CUDA_TRY(sc.alloc(&d_status, 4));
+  CUDA_TRY(sc.alloc(&d_meta, 16));
+  uint8_t* pin = static_cast<uint8_t*>(g_pin_in.get(len + 16));
+  if (!pin) return fail(DLIC_E_OUT_OF_MEMORY, "pinned staging");
+  CUDA_TRY(cudaStreamSynchronize(st));
+  uint64_t meta[2] = {0, (uint64_t)len};
+  memcpy(pin, meta, 16);
+  memcpy(pin + 16, bits, len);
+  CUDA_TRY(cudaMemcpyAsync(d_meta, pin, 16, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_bits, pin + 16, len, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_dec_prep(p, d_bits, d_meta, d_meta + 1, d_sbase, d_slen, d_status, st));
+  if (tables) {
+    uint16_t* d_tab;
+    const size_t tb = (size_t)h.width * h.height * NOUT * 2;
+    CUDA_TRY(sc.alloc(&d_tab, tb));
+    CUDA_TRY(cudaMemcpyAsync(d_tab, tables, tb, cudaMemcpyHostToDevice, st));
+    ev_begin("decode", st);
+    CUDA_TRY(launch_rans_dec_tables(p, d_bits, d_sbase, d_slen, d_tab, d_img, d_status, st));
+    ev_end("decode", st);
+  } else {
+    ev_begin("decode", st);
+    CUDA_TRY(launch_decode(p, m->dw(), d_bits, d_meta, d_sbase, d_slen, d_img, d_status, st));
+    ev_end("decode", st);
+  }
+  uint8_t* ho = static_cast<uint8_t*>(g_pin_out.get((size_t)h.width * h.height + 64));
+  if (!ho) return fail(DLIC_E_OUT_OF_MEMORY, "pinned staging");
+  CUDA_TRY(cudaMemcpyAsync(ho, d_status, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(ho + 64, d_img, (size_t)h.width * h.height, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  int32_t stat;
+  memcpy(&stat, ho, 4);
+  if (stat != 0) return fail((dlic_status)stat, "lane invariant / framing check failed on the device");
+  memcpy(img, ho + 64, (size_t)h.width * h.height);
+  return DLIC_OK;
+}
+
+dlic_status dlic_decode(const dlic_model* m, const uint8_t* bits, size_t len, uint8_t* img, size_t img_capacity) {
+  if (!m) return fail(DLIC_E_INVALID_ARG, "null model");
+  return decode_common(m, bits, len, nullptr, img, img_capacity);
+}
+
+dlic_status dlic_rans_decode_tables(const uint8_t* bits, size_t len, const uint16_t* freq_tables, uint8_t* img) {
+  if (!freq_tables) return fail(DLIC_E_INVALID_ARG, "null tables");
+  dlic_header h;
+  dlic_status s = peek(bits, len, &h, nullptr);
+  if (s != DLIC_OK) return s;
+  return decode_common(nullptr, bits, len, freq_tables, img, (size_t)h.width * h.height);
+}
+
+dlic_status dlic_rans_encode_tables(const uint32_t* fc, uint32_t width, uint32_t height, const dlic_opts* opts,
+                                    const uint8_t* model_sha256, uint8_t** out, size_t* out_len) {
+  if (!fc || !out || !out_len) return fail(DLIC_E_INVALID_ARG, "null pointer");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dlic_status s = check_device(dev);
+  if (s != DLIC_OK) return s;
+  Plan p;
+  s = make_plan(width, height, 1, opts, p);
+  if (s != DLIC_OK) return s;
+  // tables must be valid: f >= 1 and c + f <= 2^16
+  for (size_t i = 0; i < (size_t)width * height; ++i) {
+    const uint32_t f = fc[i] & 0xFFFF, c = fc[i] >> 16;
+    if (f == 0) return fail(DLIC_E_ZERO_FREQUENCY, "f_s == 0");
+    if (c + f > 65536) return fail(DLIC_E_SUM_MISMATCH, "c_s + f_s > 2^16");
+  }
+  // fc arrives in image raster order; the kernels read it unit by unit
+  std::vector<uint32_t> fcu((size_t)width * height);
+  for (uint32_t u = 0; u < p.upi; ++u) {
+    const Unit un = unit_info(p, u);
+    for (uint32_t r = 0; r < un.h; ++r)
+      memcpy(&fcu[un.fc_off + (size_t)r * un.w], &fc[(size_t)(un.y0 + r) * width + un.x0], 4ull * un.w);
+  }
+  cudaStream_t st = my_stream();
+  Scratch sc(st);
+  uint32_t *d_fc, *d_words;
+  uint16_t* d_scr;
+  uint64_t *d_dst, *d_size;
+  uint8_t* d_out;
+  const uint64_t ns = p.spi;
+  CUDA_TRY(sc.alloc(&d_fc, 4ull * width * height));
+  CUDA_TRY(sc.alloc(&d_scr, 2ull * p.cap_words * ns));
+  CUDA_TRY(sc.alloc(&d_words, 4 * ns));
+  CUDA_TRY(sc.alloc(&d_dst, 8 * ns));
+  CUDA_TRY(sc.alloc(&d_size, 8));
+  CUDA_TRY(sc.alloc(&d_out, p.max_container));
+  CUDA_TRY(cudaMemcpyAsync(d_fc, fcu.data(), 4ull * width * height, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_rans_enc(p, d_fc, d_scr, d_words, st));
+  CUDA_TRY(launch_container(p, model_sha256, d_words, d_scr, d_out, p.max_container, d_size, d_dst, st));
+  uint64_t n = 0;
+  CUDA_TRY(cudaMemcpyAsync(&n, d_size, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  uint8_t* res = static_cast<uint8_t*>(malloc(n));
+  if (!res) return fail(DLIC_E_OUT_OF_MEMORY, "malloc");
+  CUDA_TRY(cudaMemcpyAsync(res, d_out, n, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *out = res;
+  *out_len = n;
+  return DLIC_OK;
+}
+
+dlic_status dlic_debug_mlp(const dlic_model* m, const uint8_t* img, uint32_t width, uint32_t height,
+                           const dlic_opts* opts, float* logits, float* probs, uint16_t* freqs, uint32_t* fc) {
+  if (!img) return fail(DLIC_E_INVALID_ARG, "null image");
+  dlic_status s = check_model_gpu(m);
+  if (s != DLIC_OK) return s;
+  Plan p;
+  s = make_plan(width, height, 1, opts, p);
+  if (s != DLIC_OK) return s;
+  cudaStream_t st = my_stream();
+  Scratch sc(st);
+  const size_t npx = (size_t)width * height;
+  uint8_t* d_img;
+  uint32_t* d_fc;
+  float *d_lg = nullptr, *d_pb = nullptr;
+  uint16_t* d_fq = nullptr;
+  CUDA_TRY(sc.alloc(&d_img, npx));
+  CUDA_TRY(sc.alloc(&d_fc, 4 * npx));
+  if (logits) CUDA_TRY(sc.alloc(&d_lg, 4 * npx * NOUT));
+  if (probs) CUDA_TRY(sc.alloc(&d_pb, 4 * npx * NOUT));
+  if (freqs) CUDA_TRY(sc.alloc(&d_fq, 2 * npx * NOUT));
+  CUDA_TRY(cudaMemcpyAsync(d_img, img, npx, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_enc_mlp(p, m->dw(), d_img, d_fc, d_lg, d_pb, d_fq, st, num_sms(m->device)));
+  if (logits) CUDA_TRY(cudaMemcpyAsync(logits, d_lg, 4 * npx * NOUT, cudaMemcpyDeviceToHost, st));
+  if (probs) CUDA_TRY(cudaMemcpyAsync(probs, d_pb, 4 * npx * NOUT, cudaMemcpyDeviceToHost, st));
+  if (freqs) CUDA_TRY(cudaMemcpyAsync(freqs, d_fq, 2 * npx * NOUT, cudaMemcpyDeviceToHost, st));
+  std::vector<uint32_t> fcu;
+  if (fc) {
+    fcu.resize(npx);
+    CUDA_TRY(cudaMemcpyAsync(fcu.data(), d_fc, 4 * npx, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (fc) {
+    for (uint32_t u = 0; u < p.upi; ++u) {
+      const Unit un = unit_info(p, u);
+      for (uint32_t r = 0; r < un.h; ++r)
+        memcpy(&fc[(size_t)(un.y0 + r) * width + un.x0], &fcu[un.fc_off + (size_t)r * un.w], 4ull * un.w);
+    }
+  }
+  return DLIC_OK;
+}
+
+dlic_status dlic_encode_batch_device(const dlic_model* m, const uint8_t* d_imgs, uint32_t n, uint32_t width,
+                                     uint32_t height, const dlic_opts* opts, uint8_t* d_out, size_t out_capacity,
+                                     uint64_t* d_sizes, void* cuda_stream) {
+  if (!d_imgs || !d_out || !d_sizes) return fail(DLIC_E_INVALID_ARG, "null pointer");
+  dlic_status s = check_model_gpu(m);
+  if (s != DLIC_OK) return s;
+  Plan p;
+  s = make_plan(width, height, n, opts, p);
+  if (s != DLIC_OK) return s;
+  if (out_capacity < p.max_container * n) return fail(DLIC_E_BUFFER_TOO_SMALL, "out_capacity < n * max bytes");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  Scratch sc(st);
+  return run_encode(m, p, d_imgs, d_out, p.max_container, d_sizes, st, sc);
+}
+
+dlic_status dlic_decode_batch_device(const dlic_model* m, const uint8_t* d_bits, const uint64_t* h_offsets,
+                                     uint32_t n, const dlic_header* h_header, uint8_t* d_imgs, int32_t* d_status,
+                                     void* cuda_stream) {
+  if (!d_bits || !h_offsets || !h_header || !d_imgs || n == 0) return fail(DLIC_E_INVALID_ARG, "null pointer");
+  dlic_status s = check_model_gpu(m);
+  if (s != DLIC_OK) return s;
+  if (memcmp(h_header->model_sha256, m->sha, 32) != 0)
+    return fail(DLIC_E_MODEL_HASH_MISMATCH, "container was coded with another model");
+  dlic_opts o = opts_of(*h_header);
+  Plan p;
+  s = make_plan(h_header->width, h_header->height, n, &o, p);
+  if (s != DLIC_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  Scratch sc(st);
+  uint64_t* d_off;
+  uint32_t *d_sbase, *d_slen;
+  int32_t* d_st = d_status;
+  CUDA_TRY(sc.alloc(&d_off, 8ull * n));
+  CUDA_TRY(sc.alloc(&d_sbase, 4ull * n * p.spi));
+  CUDA_TRY(sc.alloc(&d_slen, 4ull * n * p.spi));
+  if (!d_st) CUDA_TRY(sc.alloc(&d_st, 4ull * n));
+  CUDA_TRY(cudaMemcpyAsync(d_off, h_offsets, 8ull * n, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_dec_prep(p, d_bits, d_off, nullptr, d_sbase, d_slen, d_st, st));
+  ev_begin("decode", st);
+  CUDA_TRY(launch_decode(p, m->dw(), d_bits, d_off, d_sbase, d_slen, d_imgs, d_st, st));
+  ev_end("decode", st);
+  return DLIC_OK;
+}
+
+dlic_status dlic_info(char* buf, size_t cap) {
+  int dev = 0, n = 0;
+  char name[256] = "none";
+  int sms = 0, cc = 0;
+  if (cudaGetDeviceCount(&n) == cudaSuccess && n > 0) {
+    cudaGetDevice(&dev);
+    cudaDeviceProp pr;
+    if (cudaGetDeviceProperties(&pr, dev) == cudaSuccess) {
+      snprintf(name, sizeof(name), "%s", pr.name);
+      sms = pr.multiProcessorCount;
+      cc = pr.major * 10 + pr.minor;
+    }
+  } else {
+    cudaGetLastError();
+  }
+  char tmp[512];
+  snprintf(tmp, sizeof(tmp),
+           "{\"device\": \"%s\", \"sm_count\": %d, \"cc\": %d, \"arch\": \"sm_100a\", "
+           "\"engines\": [\"fp32_ffma\", \"bf16_tcgen05\"], \"enc_smem\": [%zu, %zu], \"dec_smem\": [%zu, %zu]}",
+           name, sms, cc, enc_smem_bytes(0), enc_smem_bytes(1), dec_smem_bytes(0), dec_smem_bytes(1));
+  if (strlen(tmp) + 1 > cap) return fail(DLIC_E_BUFFER_TOO_SMALL, "info buffer");
+  memcpy(buf, tmp, strlen(tmp) + 1);
+  return DLIC_OK;
+}
+
+void dlic_set_timing(int enable) { g_timing = enable != 0; }
+
+double dlic_last_kernel_ms(const char* name) {
+  auto it = g_ev.find(name ? name : "");
+  if (it == g_ev.end() || !it->second.used) return -1.0;
+  if (cudaEventSynchronize(it->second.b) != cudaSuccess) return -1.0;
+  float ms = -1.0f;
+  if (cudaEventElapsedTime(&ms, it->second.a, it->second.b) != cudaSuccess) return -1.0;
+  return ms;
+}
+
+}  // extern "C"

@@ -1,0 +1,600 @@
+// dlic_kernels.cu — the B200 kernels of the DLIC hot path (sm_100a).
+//
+//   k_enc_mlp   every pixel at once (north_star (b)): window gather (P:63,
+//               P:290; fill 0 P:59) -> dense network -> softmax -> Q1
+//               table (R5) -> (f_s, c_s) of the true symbol.  Persistent CTAs
+//               over 128-pixel tiles; tcgen05 (bf16) or FFMA (fp32) engine.
+//   k_rans_enc  one warp per G-row group stream ("at most one [coder
+//               instance] per pixel row"; R7): lanes = rows, walks the
+//               wavefront in reverse (t desc, r desc), ballot/popc word
+//               emission.
+//   k_container / k_copy  header + prefix-sum stream compaction (a6).
+//   k_dec_prep  parses container framing on the device (batch decode).
+//   k_decode    persistent per-unit wavefront decoder: one
+//               cluster of nc CTAs x 128 slots; every front: gather from a
+//               shared-memory ring -> same network -> Q1 search -> rANS step
+//               -> publish pixel (DSMEM mirror) -> cluster barrier.
+#include <cstdint>
+
+#include "dlic_device.cuh"
+#include "dlic_internal.h"
+
+namespace dlic {
+
+// window offset j (row-major over the 9x9 box, causal cells only; R1)
+__device__ __forceinline__ int off_dr(int j) { return j < 72 ? j / 9 - 8 : 0; }
+__device__ __forceinline__ int off_dc(int j) { return j < 72 ? j % 9 - 6 : j - 78; }
+
+constexpr int RING_ROWS = ROWS + 8;                  // own 128 slots + 8 halo rows
+constexpr uint32_t RING_BYTES = 2u * RING_ROWS * 32u;  // 2 banks x 136 rows x 32 cols
+constexpr uint32_t MAX_GROUPS = 1024;                // per unit (cursor array in smem)
+constexpr uint32_t F32_BUF_BYTES = (NOUT + HID) * ROWS * 4u;  // 196608
+
+size_t enc_smem_bytes(uint32_t precision) { return precision == 1 ? WIMG_BYTES : F32_BUF_BYTES; }
+size_t dec_smem_bytes(uint32_t precision) {
+  return (precision == 1 ? WIMG_BYTES : F32_BUF_BYTES) + RING_BYTES + MAX_GROUPS * 4u;
+}
+
+// ------------------------------------------------------------ engine setup
+template <int PREC>
+struct EngineSel;
+template <>
+struct EngineSel<1> {
+  using T = TcEngine;
+};
+template <>
+struct EngineSel<0> {
+  using T = Fp32Engine;
+};
+
+__device__ __forceinline__ void load_wimg(uint8_t* smem, const uint8_t* wimg) {
+  const int4* src = reinterpret_cast<const int4*>(wimg);
+  int4* dst = reinterpret_cast<int4*>(smem);
+  for (uint32_t i = threadIdx.x; i < WIMG_BYTES / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+}
+
+// Build the engine input for this thread's row from a value getter.
+template <class Get>
+__device__ __forceinline__ void feed_tc(uint32_t (&a)[40], Get get) {
+#pragma unroll
+  for (int i = 0; i < 39; ++i) {
+    const float x0 = (float)get(2 * i) * 0.00390625f;      // v / 256, exact (R2)
+    const float x1 = (float)get(2 * i + 1) * 0.00390625f;
+    a[i] = pack_bf16(x0, x1);
+  }
+  a[39] = 0u;  // K padding 78, 79
+}
+template <class Get>
+__device__ __forceinline__ void feed_f32(float* buf0, Get get) {
+#pragma unroll
+  for (int j = 0; j < KIN; ++j) buf0[j * ROWS + threadIdx.x] = (float)get(j) * 0.00390625f;
+}
+
+// ------------------------------------------------------------ encoder MLP
+template <int PREC>
+__global__ void __launch_bounds__(128, 1)
+    k_enc_mlp(Plan p, DevWeights w, const uint8_t* __restrict__ imgs, uint32_t* __restrict__ fc,
+              float* __restrict__ dbg_logits, float* __restrict__ dbg_probs, uint16_t* __restrict__ dbg_freqs) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x;
+  typename EngineSel<PREC>::T eng;
+  if constexpr (PREC == 1) {
+    load_wimg(smem, w.wimg);
+    if (tid < 32) tmem_alloc(smem_u32(&tslot), TM_COLS);
+    if (tid == 0) {
+      mbar_init(smem_u32(&bar), 1);
+      fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    eng.tmem = tslot;
+    eng.wsmem = smem_u32(smem);
+    eng.bias = w.bias;
+    eng.bar = smem_u32(&bar);
+    eng.phase = 0;
+  } else {
+    eng.buf0 = reinterpret_cast<float*>(smem);
+    eng.buf1 = eng.buf0 + NOUT * ROWS;
+    eng.w = w.w32;
+  }
+  const uint64_t total = (uint64_t)p.n_img * p.upi * p.tiles_per_unit;
+#pragma unroll 1
+  for (uint64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    const uint32_t u = (uint32_t)(tile / p.tiles_per_unit);
+    const uint32_t k = (uint32_t)(tile % p.tiles_per_unit);
+    const Unit un = unit_info(p, u);
+    const uint32_t q = k * 128u + (uint32_t)tid;
+    const bool valid = q < un.w * un.h;
+    const int r = valid ? (int)(q / un.w) : 0, c = valid ? (int)(q % un.w) : 0;
+    const uint8_t* img = imgs + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
+    const int uw = (int)un.w;
+    auto get = [&](int j) -> uint32_t {
+      const int rr = r + off_dr(j), cc = c + off_dc(j);
+      return (valid && rr >= 0 && cc >= 0 && cc < uw) ? (uint32_t)__ldg(img + (uint64_t)rr * p.W + cc) : 0u;
+    };
+    if constexpr (PREC == 1) {
+      uint32_t a[40];
+      feed_tc(a, get);
+      eng.run(a);
+    } else {
+      feed_f32(eng.buf0, get);
+      eng.run();
+    }
+    const int sym = valid ? (int)__ldg(img + (uint64_t)r * p.W + c) : 0;
+    const uint32_t v = q1_encode(eng, sym);
+    if (valid) fc[un.fc_off + q] = v;
+    if (dbg_logits || dbg_probs || dbg_freqs) {
+      const uint64_t gi = (uint64_t)un.img * p.W * p.H + (uint64_t)(un.y0 + r) * p.W + (un.x0 + c);
+      if (dbg_logits) {
+#pragma unroll 1
+        for (int j = 0; j < NOUT / 32; ++j) {
+          float o[32];
+          eng.logits32(j, o);
+          if (valid)
+            for (int i = 0; i < 32; ++i) dbg_logits[gi * NOUT + 32 * j + i] = o[i];
+        }
+      }
+      q1_export(eng, (valid && dbg_probs) ? dbg_probs + gi * NOUT : nullptr,
+                (valid && dbg_freqs) ? dbg_freqs + gi * NOUT : nullptr);
+    }
+  }
+  if constexpr (PREC == 1) {
+    tc_fence_before();
+    __syncthreads();
+    if (tid < 32) tmem_dealloc(eng.tmem, TM_COLS);
+  }
+}
+
+// ------------------------------------------------------------ rANS encoder
+// One warp per stream.  Lane i = row r0+i of the group.  Fronts walked in
+// reverse (LIFO); within a front rows descending = lanes descending, so
+// lane i's emitted word goes after those of lanes > i.  Words are written
+// backwards from the end of the stream's scratch region so the region tail is
+// already in decoder order (t asc, r asc).
+__global__ void __launch_bounds__(128) k_rans_enc(Plan p, const uint32_t* __restrict__ fc,
+                                                  uint16_t* __restrict__ scratch, uint32_t* __restrict__ words) {
+  const uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nstreams = p.n_img * p.spi;
+  if (s >= nstreams) return;  // warp-uniform
+  uint32_t u, g;
+  stream_info(p, s, u, g);
+  const Unit un = unit_info(p, u);
+  const uint32_t r0 = g * p.G;
+  const uint32_t nr = min(p.G, un.h - r0);
+  uint16_t* region = scratch + (uint64_t)s * p.cap_words;
+  const uint32_t cap = p.cap_words;
+  const bool lane_ok = lane < nr;
+  const int r = (int)(r0 + lane);
+  const uint32_t* frow = fc + un.fc_off + (uint64_t)r * un.w;
+  uint32_t x = RANS_L;
+  uint32_t n = 0;
+  const int t_hi = 3 * (int)(r0 + nr - 1) + (int)un.w - 1;
+  const int t_lo = 3 * (int)r0;
+#pragma unroll 1
+  for (int t = t_hi; t >= t_lo; --t) {
+    const int c = t - 3 * r;
+    const bool act = lane_ok && c >= 0 && c < (int)un.w;
+    uint32_t f = 1, cum = 0;
+    if (act) {
+      const uint32_t v = __ldg(frow + c);
+      f = v & 0xFFFFu;
+      cum = v >> 16;
+    }
+    const bool emit = act && (x >> 16) >= f;  // x >= f * 2^16  (renormalise first, R6)
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, emit);
+    if (emit) {
+      const uint32_t k = n + __popc(m >> lane >> 1);  // lanes above emit first
+      region[cap - 1 - k] = (uint16_t)(x & 0xFFFFu);
+      x >>= 16;
+    }
+    n += __popc(m);
+    if (act) x = ((x / f) << 16) + (x % f) + cum;
+  }
+  if (lane_ok) {
+    region[2 * lane] = (uint16_t)(x >> 16);
+    region[2 * lane + 1] = (uint16_t)(x & 0xFFFFu);
+  }
+  if (lane == 0) words[s] = 2 * nr + n;
+}
+
+// ------------------------------------------------------------ container
+struct Sha {
+  uint8_t b[32];
+};
+
+__device__ __forceinline__ void put_u16(uint8_t* o, uint32_t v) {
+  o[0] = (uint8_t)v;
+  o[1] = (uint8_t)(v >> 8);
+}
+__device__ __forceinline__ void put_u32(uint8_t* o, uint32_t v) {
+  o[0] = (uint8_t)v;
+  o[1] = (uint8_t)(v >> 8);
+  o[2] = (uint8_t)(v >> 16);
+  o[3] = (uint8_t)(v >> 24);
+}
+
+__global__ void k_container(Plan p, Sha sha, const uint32_t* __restrict__ words, uint8_t* __restrict__ out,
+                            uint64_t stride, uint64_t* __restrict__ sizes, uint64_t* __restrict__ dst) {
+  const uint32_t img = blockIdx.x;
+  uint8_t* o = out + (uint64_t)img * stride;
+  if (threadIdx.x == 0) {
+    o[0] = 'D';
+    o[1] = 'L';
+    o[2] = 'I';
+    o[3] = 'C';
+    o[4] = 1;  // version
+    o[5] = (uint8_t)p.precision;
+    o[6] = 1;  // window id (R1)
+    o[7] = 0;  // fill (R2)
+    put_u32(o + 8, p.W);
+    put_u32(o + 12, p.H);
+    put_u16(o + 16, p.hdr_tw);
+    put_u16(o + 18, p.hdr_th);
+    put_u16(o + 20, p.G);
+    for (int i = 0; i < 32; ++i) o[22 + i] = sha.b[i];
+    put_u32(o + 54, p.spi);
+    uint64_t off = p.hdr_bytes;
+    for (uint32_t s = 0; s < p.spi; ++s) {
+      const uint32_t sz = 2u * words[(uint64_t)img * p.spi + s];
+      put_u32(o + 58 + 4 * s, sz);
+      dst[(uint64_t)img * p.spi + s] = off;
+      off += sz;
+    }
+    sizes[img] = off;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_copy(Plan p, const uint32_t* __restrict__ words,
+                                              const uint16_t* __restrict__ scratch,
+                                              const uint64_t* __restrict__ dst, uint8_t* __restrict__ out,
+                                              uint64_t stride) {
+  const uint32_t s = blockIdx.x;
+  uint32_t u, g;
+  stream_info(p, s, u, g);
+  const Unit un = unit_info(p, u);
+  const uint32_t nr = min(p.G, un.h - g * p.G);
+  const uint32_t nw = words[s], ns = 2 * nr, ne = nw - ns;
+  const uint16_t* region = scratch + (uint64_t)s * p.cap_words;
+  uint16_t* o = reinterpret_cast<uint16_t*>(out + (uint64_t)un.img * stride + dst[s]);
+  for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x)
+    o[i] = i < ns ? region[i] : region[p.cap_words - ne + (i - ns)];
+}
+
+// ------------------------------------------------------------ table-driven rANS decode
+// Parity tap for the coder alone: every pixel's full integer table is given
+// (north_star "when the oracle is fed the same integer tables"), so groups are
+// independent; one warp per stream mirrors k_rans_enc in decoder order.
+__global__ void __launch_bounds__(128) k_rans_dec_tables(Plan p, const uint8_t* __restrict__ bits,
+                                                         const uint32_t* __restrict__ sbase,
+                                                         const uint32_t* __restrict__ slen,
+                                                         const uint16_t* __restrict__ tables,
+                                                         uint8_t* __restrict__ out, int32_t* __restrict__ status) {
+  const uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (s >= p.n_img * p.spi) return;
+  uint32_t u, g;
+  stream_info(p, s, u, g);
+  const Unit un = unit_info(p, u);
+  const uint32_t r0 = g * p.G, nr = min(p.G, un.h - r0);
+  const uint16_t* sw = reinterpret_cast<const uint16_t*>(bits + sbase[s]);
+  const uint32_t sl = slen[s];
+  const bool lane_ok = lane < nr;
+  const int r = (int)(r0 + lane);
+  int err = 0;
+  uint32_t x = 0;
+  if (lane_ok) {
+    if (2 * lane + 1 < sl) x = ((uint32_t)sw[2 * lane] << 16) | sw[2 * lane + 1];
+    else err = 8;
+  }
+  uint32_t cur = 2 * nr;
+  const int t_hi = 3 * (int)(r0 + nr - 1) + (int)un.w - 1;
+#pragma unroll 1
+  for (int t = 3 * (int)r0; t <= t_hi; ++t) {
+    const int c = t - 3 * r;
+    const bool act = lane_ok && c >= 0 && c < (int)un.w;
+    bool need = false;
+    if (act) {
+      const uint64_t gi = (uint64_t)un.img * p.W * p.H + (uint64_t)(un.y0 + r) * p.W + un.x0 + c;
+      const uint16_t* tab = tables + gi * NOUT;
+      const uint32_t slot = x & 0xFFFFu;
+      uint32_t cum = 0, fsel = 0, csel = 0;
+      int sym = 0;
+      for (int i = 0; i < NOUT; ++i) {
+        const uint32_t f = __ldg(tab + i);
+        if (slot - cum < f) {
+          sym = i;
+          fsel = f;
+          csel = cum;
+        }
+        cum += f;
+      }
+      if (cum != 65536u || fsel == 0) err = 9;
+      x = fsel * (x >> 16) + slot - csel;
+      need = x < RANS_L;
+      out[gi] = (uint8_t)sym;
+    }
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, need);
+    if (need) {
+      const uint32_t wi = cur + __popc(m & ((1u << lane) - 1u));
+      if (wi < sl) x = (x << 16) | sw[wi];
+      else err = 8;
+    }
+    cur += __popc(m);
+  }
+  if (lane_ok && x != RANS_L) err = err ? err : 6;
+  if (lane == 0 && cur != sl) err = err ? err : 6;
+  if (err) atomicMax(status + un.img, err);
+}
+
+cudaError_t launch_rans_dec_tables(const Plan& p, const uint8_t* d_bits, const uint32_t* d_sbase,
+                                   const uint32_t* d_slen, const uint16_t* d_tables, uint8_t* d_out,
+                                   int32_t* d_status, cudaStream_t st) {
+  const uint32_t ns = p.n_img * p.spi;
+  k_rans_dec_tables<<<(ns + 3) / 4, 128, 0, st>>>(p, d_bits, d_sbase, d_slen, d_tables, d_out, d_status);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ decode prep
+__device__ __forceinline__ uint32_t get_u32(const uint8_t* b) {
+  return (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
+}
+__device__ __forceinline__ uint32_t get_u16(const uint8_t* b) { return (uint32_t)b[0] | ((uint32_t)b[1] << 8); }
+
+__global__ void k_dec_prep(Plan p, const uint8_t* __restrict__ bits, const uint64_t* __restrict__ cont_off,
+                           const uint64_t* __restrict__ cont_len, uint32_t* __restrict__ sbase,
+                           uint32_t* __restrict__ slen, int32_t* __restrict__ status) {
+  const uint32_t img = blockIdx.x * blockDim.x + threadIdx.x;
+  if (img >= p.n_img) return;
+  const uint8_t* b = bits + cont_off[img];
+  const uint64_t len = cont_len ? cont_len[img] : ~0ull;
+  int err = 0;
+  if (b[0] != 'D' || b[1] != 'L' || b[2] != 'I' || b[3] != 'C') err = 6;
+  else if (b[4] != 1 || b[6] != 1 || b[7] != 0) err = 5;
+  else if (get_u32(b + 8) != p.W || get_u32(b + 12) != p.H || get_u16(b + 16) != p.hdr_tw ||
+           get_u16(b + 18) != p.hdr_th || get_u16(b + 20) != p.G || b[5] != p.precision ||
+           get_u32(b + 54) != p.spi)
+    err = 2;
+  uint64_t off = p.hdr_bytes;
+  for (uint32_t s = 0; s < p.spi; ++s) {
+    uint32_t sz = err ? 0u : get_u32(b + 58 + 4 * s);
+    if ((sz & 1u) || off + sz > len) {
+      err = 6;
+      sz = 0;
+    }
+    sbase[(uint64_t)img * p.spi + s] = (uint32_t)off;
+    slen[(uint64_t)img * p.spi + s] = err ? 0u : sz / 2;
+    off += sz;
+  }
+  if (cont_len && off != len && !err) err = 6;
+  status[img] = err;
+}
+
+// ------------------------------------------------------------ decoder
+template <int PREC>
+__global__ void __launch_bounds__(128, 1)
+    k_decode(Plan p, DevWeights w, const uint8_t* __restrict__ bits, const uint64_t* __restrict__ cont_off,
+             const uint32_t* __restrict__ sbase, const uint32_t* __restrict__ slen, uint8_t* __restrict__ out,
+             int32_t* __restrict__ status) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x;
+  const uint32_t lane = lane_id();
+  const uint32_t NC = p.nc, NS = ROWS * NC;
+  const uint32_t ns_shift = 7u + (NC == 1 ? 0u : NC == 2 ? 1u : NC == 4 ? 2u : 3u);
+  const uint32_t rank = NC > 1 ? cluster_rank() : 0u;
+  const uint32_t u = blockIdx.x / NC;
+  const Unit un = unit_info(p, u);
+  const uint32_t S = rank * ROWS + (uint32_t)tid;
+
+  typename EngineSel<PREC>::T eng;
+  uint8_t* ring;
+  if constexpr (PREC == 1) {
+    ring = smem + WIMG_BYTES;
+    load_wimg(smem, w.wimg);
+    if (tid < 32) tmem_alloc(smem_u32(&tslot), TM_COLS);
+    if (tid == 0) {
+      mbar_init(smem_u32(&bar), 1);
+      fence_mbar_init();
+    }
+  } else {
+    ring = smem + F32_BUF_BYTES;
+    eng.buf0 = reinterpret_cast<float*>(smem);
+    eng.buf1 = eng.buf0 + NOUT * ROWS;
+    eng.w = w.w32;
+  }
+  uint32_t* cursor = reinterpret_cast<uint32_t*>(ring + RING_BYTES);
+  const uint32_t G = p.G;
+  for (uint32_t g = tid; g < un.ngroups; g += ROWS) {
+    if ((((G * g) & (NS - 1)) >> 7) == rank) cursor[g] = 2u * min(G, un.h - G * g);
+  }
+  if constexpr (PREC == 1) {
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    eng.tmem = tslot;
+    eng.wsmem = smem_u32(smem);
+    eng.bias = w.bias;
+    eng.bar = smem_u32(&bar);
+    eng.phase = 0;
+  }
+  if (NC > 1) cluster_sync_all();
+  else __syncthreads();
+
+  const uint8_t* cbase = bits + cont_off[un.img];
+  uint8_t* oimg = out + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t halo_rank = (rank + 1) % NC;
+  const uint32_t halo_base = NC > 1 ? map_cluster(ring_s, halo_rank) : ring_s;
+  const int uw = (int)un.w, uh = (int)un.h;
+  const int T = uw + 3 * (uh - 1);
+  uint32_t x = 0;
+  int err = 0;
+
+#pragma unroll 1
+  for (int t = 0; t < T; ++t) {
+    const int rlo = t - uw + 1 > 0 ? (t - uw + 3) / 3 : 0;
+    const int rhi = min(uh - 1, t / 3);
+    bool active = false;
+    int r = 0, c = 0;
+    if (rlo <= rhi) {
+      r = rlo + (int)((S + NS - ((uint32_t)rlo & (NS - 1))) & (NS - 1));
+      active = r <= rhi;
+      c = t - 3 * r;
+    }
+    if (__syncthreads_or(active)) {
+      const uint32_t g = active ? (uint32_t)r / G : 0u;
+      const uint32_t sidx = un.first_stream + g;
+      const uint16_t* sw = reinterpret_cast<const uint16_t*>(cbase + (active ? sbase[sidx] : 0u));
+      const uint32_t sl = active ? slen[sidx] : 0u;
+      if (active && c == 0) {  // the row's lane starts: flushed state (hi, lo)
+        const uint32_t i = 2u * ((uint32_t)r - G * g);
+        if (i + 1 < sl) x = ((uint32_t)sw[i] << 16) | (uint32_t)sw[i + 1];
+        else err = 8;
+      }
+      // window gather from the ring (rows r-8..r of this slot's neighbourhood)
+      auto get = [&](int j) -> uint32_t {
+        const int d = -off_dr(j);
+        const int rr = r - d, cc = c + off_dc(j);
+        if (!active || rr < 0 || cc < 0 || cc >= uw) return 0u;
+        const uint32_t bank = ((uint32_t)rr >> ns_shift) & 1u;
+        return ring[(bank * RING_ROWS + (uint32_t)(tid - d + 8)) * 32u + ((uint32_t)cc & 31u)];
+      };
+      if constexpr (PREC == 1) {
+        uint32_t a[40];
+        feed_tc(a, get);
+        eng.run(a);
+      } else {
+        feed_f32(eng.buf0, get);
+        eng.run();
+      }
+      const uint32_t slot = x & 0xFFFFu;
+      uint32_t fs, cs;
+      const int sym = q1_decode(eng, slot, fs, cs);
+      bool need = false;
+      if (active) {
+        x = fs * (x >> 16) + slot - cs;
+        need = x < RANS_L;
+      }
+      const uint32_t key = active ? g : (0x80000000u | lane);
+      const uint32_t gm = __match_any_sync(0xFFFFFFFFu, key);
+      const uint32_t readers = __ballot_sync(0xFFFFFFFFu, need) & gm;
+      uint32_t cur = 0;
+      if (active) cur = cursor[g];
+      __syncwarp();
+      if (need) {
+        const uint32_t wi = cur + __popc(readers & ((1u << lane) - 1u));
+        if (wi < sl) x = (x << 16) | (uint32_t)sw[wi];
+        else err = 8;
+      }
+      if (active && lane == (uint32_t)(__ffs(gm) - 1)) cursor[g] = cur + __popc(readers);
+      if (active) {
+        oimg[(uint64_t)r * p.W + c] = (uint8_t)sym;
+        const uint32_t bank = ((uint32_t)r >> ns_shift) & 1u;
+        const uint32_t col = (uint32_t)c & 31u;
+        ring[(bank * RING_ROWS + (uint32_t)tid + 8u) * 32u + col] = (uint8_t)sym;
+        if (tid >= ROWS - 8) {
+          const uint32_t hoff = (bank * RING_ROWS + (uint32_t)(tid - (ROWS - 8))) * 32u + col;
+          if (NC > 1) st_cluster_u8(halo_base + hoff, (uint32_t)sym);
+          else ring[hoff] = (uint8_t)sym;
+        }
+        if (c == uw - 1 && x != RANS_L) err = 6;  // end-of-lane invariant
+      }
+    }
+    if (NC > 1) cluster_sync_all();
+    else __syncthreads();
+  }
+  for (uint32_t g = tid; g < un.ngroups; g += ROWS) {
+    if ((((G * g) & (NS - 1)) >> 7) == rank && cursor[g] != slen[un.first_stream + g]) err = 6;
+  }
+  if (err) atomicMax(status + un.img, err);
+  if constexpr (PREC == 1) {
+    tc_fence_before();
+    __syncthreads();
+    if (tid < 32) tmem_dealloc(eng.tmem, TM_COLS);
+  }
+  if (NC > 1) cluster_sync_all();  // keep DSMEM alive until every CTA is done
+}
+
+// ------------------------------------------------------------ launchers
+template <class K>
+static cudaError_t set_smem(K kern, size_t bytes) {
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+cudaError_t launch_enc_mlp(const Plan& p, const DevWeights& w, const uint8_t* d_imgs, uint32_t* d_fc,
+                           float* dbg_logits, float* dbg_probs, uint16_t* dbg_freqs, cudaStream_t st,
+                           int num_sms) {
+  const uint64_t total = (uint64_t)p.n_img * p.upi * p.tiles_per_unit;
+  const uint32_t grid = (uint32_t)(total < (uint64_t)num_sms ? total : (uint64_t)num_sms);
+  const size_t sm = enc_smem_bytes(p.precision);
+  if (p.precision == 1) {
+    cudaError_t e = set_smem(k_enc_mlp<1>, sm);
+    if (e != cudaSuccess) return e;
+    k_enc_mlp<1><<<grid, 128, sm, st>>>(p, w, d_imgs, d_fc, dbg_logits, dbg_probs, dbg_freqs);
+  } else {
+    cudaError_t e = set_smem(k_enc_mlp<0>, sm);
+    if (e != cudaSuccess) return e;
+    k_enc_mlp<0><<<grid, 128, sm, st>>>(p, w, d_imgs, d_fc, dbg_logits, dbg_probs, dbg_freqs);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rans_enc(const Plan& p, const uint32_t* d_fc, uint16_t* d_scratch, uint32_t* d_words,
+                            cudaStream_t st) {
+  const uint32_t ns = p.n_img * p.spi;
+  k_rans_enc<<<(ns + 3) / 4, 128, 0, st>>>(p, d_fc, d_scratch, d_words);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_container(const Plan& p, const uint8_t* model_sha, const uint32_t* d_words,
+                             const uint16_t* d_scratch, uint8_t* d_out, uint64_t out_stride, uint64_t* d_sizes,
+                             uint64_t* d_stream_dst, cudaStream_t st) {
+  Sha sha;
+  for (int i = 0; i < 32; ++i) sha.b[i] = model_sha ? model_sha[i] : 0;
+  k_container<<<p.n_img, 32, 0, st>>>(p, sha, d_words, d_out, out_stride, d_sizes, d_stream_dst);
+  k_copy<<<p.n_img * p.spi, 128, 0, st>>>(p, d_words, d_scratch, d_stream_dst, d_out, out_stride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dec_prep(const Plan& p, const uint8_t* d_bits, const uint64_t* d_cont_off,
+                            const uint64_t* d_cont_len, uint32_t* d_sbase, uint32_t* d_slen, int32_t* d_status,
+                            cudaStream_t st) {
+  k_dec_prep<<<(p.n_img + 63) / 64, 64, 0, st>>>(p, d_bits, d_cont_off, d_cont_len, d_sbase, d_slen, d_status);
+  return cudaGetLastError();
+}
+
+template <int PREC>
+static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uint8_t* d_bits,
+                                   const uint64_t* d_cont_off, const uint32_t* d_sbase, const uint32_t* d_slen,
+                                   uint8_t* d_imgs, int32_t* d_status, cudaStream_t st) {
+  const size_t sm = dec_smem_bytes(PREC);
+  cudaError_t e = set_smem(k_decode<PREC>, sm);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.n_img * p.upi * p.nc);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = p.nc;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_decode<PREC>, p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status);
+}
+
+cudaError_t launch_decode(const Plan& p, const DevWeights& w, const uint8_t* d_bits, const uint64_t* d_cont_off,
+                          const uint32_t* d_sbase, const uint32_t* d_slen, uint8_t* d_imgs, int32_t* d_status,
+                          cudaStream_t st) {
+  if (p.precision == 1) return launch_decode_t<1>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st);
+  return launch_decode_t<0>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st);
+}
+
+}  // namespace dlic
