@@ -1,0 +1,389 @@
+"""bench.py — DLIC hot path on B200: encode + decode Mpixel/s (8-bit gray) and bpp.
+
+One step = one pass of the whole hot path over one
+batch of synthetic input: encode every pixel at once (window gather -> MLP ->
+softmax/Q1 -> rANS lanes -> compaction) and wavefront-decode the containers
+back.  Default workload: BASELINE.json configs[1] (C2, one 768x512 Kodak-shaped
+image per GPU), bf16 tcgen05 path, trained P100K weights, G = 32.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dlic|reference]
+                  [--config C2] [--batch B] [--precision bf16|fp32]
+
+N > 1 runs under torchrun (one process per GPU, NCCL): every rank codes its own
+images (weak scaling; units are independent, P:103 lanes never cross images);
+the only collective is the all_gather of container sizes (north_star).
+--impl reference times the CPU oracle (oracle/) on a bounded sample of the
+same workload (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOP_PER_PX = 216576            # P100K, SURVEY App. A item 1 (2 * sum K*N)
+CONFIG_DESC = {
+    "C1": "C1 32x32 gradient+noise, single stream (G=32=H)",
+    "C2": "C2 768x512 Kodak-shaped natural-like, 1 image per GPU per step",
+    "C3": "C3 256x256 MRI-like slices",
+    "C4": "C4 1920x1080 natural-like, tiles 384x360",
+    "C5": "C5 3840x2160 natural-like, tiles 768x720",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dlic", choices=["dlic", "reference"])
+    ap.add_argument("--config", default="C2", choices=list(CONFIG_DESC))
+    ap.add_argument("--batch", type=int, default=0, help="images per GPU per step (0 = config default)")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.25)
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    return ws, rank, local
+
+
+def images_for(args, rank, n):
+    import synth
+    cfg = args.config
+    if cfg == "C1":
+        return np.stack([synth.gradient_noise(32, 32, seed=rank * 1000 + i) for i in range(n)])
+    if cfg == "C2":
+        return np.stack([synth.natural_like(768, 512, seed=rank * 1000 + i) for i in range(n)])
+    if cfg == "C3":
+        return synth.mri_like_slices(n, 256, seed0=rank * 100)
+    if cfg == "C4":
+        return np.stack([synth.natural_like(1920, 1080, seed=100 + rank * 1000 + i, wavelength_scale=2.5)
+                         for i in range(n)])
+    return np.stack([synth.natural_like(3840, 2160, seed=200 + rank * 1000 + i, wavelength_scale=5.0)
+                     for i in range(n)])
+
+
+def opts_for(cfg):
+    c = {"C1": (32, (0, 0)), "C2": (32, (0, 0)), "C3": (32, (0, 0)), "C4": (32, (384, 360)),
+         "C5": (32, (768, 720))}[cfg]
+    return c
+
+
+def default_batch(cfg):
+    return {"C1": 1, "C2": 1, "C3": 64, "C4": 1, "C5": 8}[cfg]
+
+
+# ------------------------------------------------------------------ reference arm (CPU oracle)
+def run_reference(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import codec  # the one other place bench.py executes oracle/
+    with open(os.path.join(ROOT, "fixtures", "p100k_trained.dlicmdl"), "rb") as fh:
+        blob = fh.read()
+    img = images_for(args, 0, 1)[0]
+    sh, sw = min(img.shape[0], 128), min(img.shape[1], 192)
+    sample = np.ascontiguousarray(img[:sh, :sw])
+    prec = 1 if args.precision == "bf16" else 0
+    g, _ = opts_for(args.config)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        b = codec.encode(sample, blob, prec, g)
+        out = codec.decode(b, blob)
+        dt = time.perf_counter() - t0
+        assert np.array_equal(out, sample)
+        if i >= args.warmup:
+            times.append(dt)
+    ms = statistics.mean(times) * 1e3
+    mpx = sample.size / (ms / 1e3) / 1e6
+    cores = 1
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count() or 1
+    line = {
+        "impl": "reference", "metric": "encode+decode Mpixel/s (8-bit gray, round trip)", "value": mpx,
+        "unit": "Mpixel/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64-accum bf16-emulated" if prec else "f64", "data": "synthetic",
+        "config": {"workload": CONFIG_DESC[args.config], "sample": "%dx%d crop" % (sw, sh),
+                   "precision": args.precision},
+        "cpu_baseline": {"value": mpx, "unit": "Mpixel/s", "cores": cores, "kind": "oracle",
+                         "sample": "top-left %dx%d crop of the %s image, oracle encode+decode per step"
+                                   % (sw, sh, args.config)},
+        "e2e": {"value": mpx, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(args, img):
+    """Oracle (as it stands) on a bounded sample of the workload (~10 s)."""
+    from oracle import codec
+    with open(os.path.join(ROOT, "fixtures", "p100k_trained.dlicmdl"), "rb") as fh:
+        blob = fh.read()
+    sh, sw = min(img.shape[0], 128), min(img.shape[1], 256)
+    sample = np.ascontiguousarray(img[:sh, :sw])
+    prec = 1 if args.precision == "bf16" else 0
+    t0 = time.perf_counter()
+    b = codec.encode(sample, blob, prec, 32)
+    out = codec.decode(b, blob)
+    dt = time.perf_counter() - t0
+    assert np.array_equal(out, sample)
+    cores = os.cpu_count() or 1
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    except Exception:
+        pass
+    return {"value": sample.size / dt / 1e6, "unit": "Mpixel/s", "cores": cores, "kind": "oracle",
+            "sample": "top-left %dx%d crop of the %s image: oracle encode+decode (%.1f s)" % (sw, sh, args.config, dt)}
+
+
+# ------------------------------------------------------------------ product arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    ws, rank, local = dist_setup(args)
+    import paper_2207_05152_b200 as dl
+
+    dev = torch.device("cuda", local)
+    with open(os.path.join(ROOT, "fixtures", "p100k_trained.dlicmdl"), "rb") as fh:
+        blob = fh.read()
+    model = dl.dlic_model_load(blob, local)
+    prec = 1 if args.precision == "bf16" else 0
+    g, tile = opts_for(args.config)
+    n = args.batch or default_batch(args.config)
+    imgs = images_for(args, rank, n)
+    _, H, W = imgs.shape
+    px_rank = n * H * W
+    stream = torch.cuda.current_stream(dev)
+    d_imgs = torch.from_numpy(imgs).to(dev)
+    d_dec = torch.empty_like(d_imgs)
+    d_status = torch.zeros(n, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    dl.dlic_set_timing(True)
+
+    # first pass: planning header + correctness check of this batch
+    d_out, d_sizes, stride = dl.dlic_encode_batch_device(model, d_imgs, prec, g, tile)
+    torch.cuda.synchronize()
+    sizes = d_sizes.cpu().numpy()
+    hdr = dl.dlic_peek(d_out[:int(sizes[0])].cpu().numpy().tobytes())
+    offs = [i * stride for i in range(n)]
+    dl.dlic_decode_batch_device(model, d_out, offs, hdr, d_dec, d_status)
+    torch.cuda.synchronize()
+    assert int(d_status.abs().sum()) == 0 and torch.equal(d_dec, d_imgs), "round trip failed"
+    total_bytes = int(sizes.sum())
+    payload = total_bytes - n * hdr["header_bytes"]
+
+    def step():
+        dl.dlic_encode_batch_device(model, d_imgs, prec, g, tile, d_out=d_out, d_sizes=d_sizes)
+        if ws > 1:
+            import torch.distributed as dist
+            gathered = [torch.empty_like(d_sizes) for _ in range(ws)]
+            dist.all_gather(gathered, d_sizes)      # the only collective: container sizes
+        dl.dlic_decode_batch_device(model, d_out, offs, hdr, d_dec, d_status)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    enc_ms, dec_ms = [], []
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)                    # L2 flush between timed steps (not timed)
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+            enc_ms.append(dl.dlic_last_kernel_ms("mlp") + dl.dlic_last_kernel_ms("rans_enc")
+                          + dl.dlic_last_kernel_ms("compact"))
+            dec_ms.append(dl.dlic_last_kernel_ms("decode"))
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = statistics.mean(step_ms)
+    t_enc = statistics.mean(enc_ms)
+    t_dec = statistics.mean(dec_ms)
+    mlp_ms = dl.dlic_last_kernel_ms("mlp")
+    if ws > 1:
+        t = torch.tensor([ms, t_enc, t_dec], dtype=torch.float64, device=dev)
+        allt = [torch.empty_like(t) for _ in range(ws)]
+        dist.all_gather(allt, t)
+        ms, t_enc, t_dec = (max(float(x[i]) for x in allt) for i in range(3))
+    assert int(d_status.abs().sum()) == 0 and torch.equal(d_dec, d_imgs)
+    clocks = clk.summary()
+
+    # ---- e2e: public host API, host buffers, H2D/D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        pin_imgs = torch.from_numpy(imgs).pin_memory().numpy()
+        e_ms = []
+        h2d = d2h = 0
+        for i in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            tot_in = tot_out = 0
+            for k in range(n):
+                b = dl.dlic_encode(model, pin_imgs[k], prec, g, tile)
+                back = dl.dlic_decode(model, b)
+                tot_in += pin_imgs[k].nbytes + len(b)
+                tot_out += len(b) + back.nbytes
+            dt = (time.perf_counter() - t0) * 1e3
+            if i >= args.warmup:
+                e_ms.append(dt)
+                h2d, d2h = tot_in, tot_out
+            assert np.array_equal(back, pin_imgs[n - 1])
+        em = statistics.mean(e_ms)
+        if ws > 1:
+            t = torch.tensor([em], dtype=torch.float64, device=dev)
+            allt = [torch.empty_like(t) for _ in range(ws)]
+            dist.all_gather(allt, t)
+            em = max(float(x[0]) for x in allt)
+        e2e = {"value": ws * px_rank / (em / 1e3) / 1e6, "unit": "Mpixel/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": em}
+
+    if rank == 0:
+        peaks, src = load_peaks()
+        # dominant kernel: the wavefront decoder (latency-bound front chain)
+        dec_flops = FLOP_PER_PX * px_rank
+        achieved = dec_flops / (t_dec / 1e3) / 1e12
+        # fp32 path runs on CUDA-core FFMA: 148 SMs x 128 FMA/clk x 2 x sm_max
+        peak = peaks["bf16_tflops"] if prec == 1 else 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "decode_traffic.json")) as fh:
+                traffic = json.load(fh).get("%s_%s" % (args.config, args.precision))
+        except (OSError, ValueError):
+            pass
+        T = W + 3 * (H - 1) if tile == (0, 0) else tile[0] + 3 * (tile[1] - 1)
+        floor_ms = T * 3392 / (peaks.get("sm_max_mhz", 1965.0) * 1e3)   # MMA-chain floor per front (App. A)
+        cpu = cpu_baseline_sample(args, imgs[0])
+        line = {
+            "metric": "encode+decode Mpixel/s (8-bit gray, round trip) and bpp",
+            "value": ws * px_rank / (ms / 1e3) / 1e6,
+            "unit": "Mpixel/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16" if prec == 1 else "f32", "data": "synthetic",
+            "config": {"workload": CONFIG_DESC[args.config], "images_per_gpu": n, "width": W, "height": H,
+                       "tile": list(tile), "group_rows": g, "precision": args.precision,
+                       "weights": "P100K briefly trained by the oracle (fixtures/p100k_trained.dlicmdl)",
+                       "l2": "flushed between timed steps (256 MiB write, untimed)", "parallelism": "dp%d" % ws},
+            "encode_mpx_s": ws * px_rank / (t_enc / 1e3) / 1e6,
+            "decode_mpx_s": ws * px_rank / (t_dec / 1e3) / 1e6,
+            "encode_ms": t_enc, "decode_ms": t_dec, "mlp_ms": mlp_ms,
+            "bpp_total": 8.0 * total_bytes / px_rank, "bpp_payload": 8.0 * payload / px_rank,
+            "roofline": {"kernel": "k_decode<%s>" % args.precision, "bound": "tensor" if prec == 1 else "alu", "achieved": achieved,
+                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": src + (" bf16_tflops" if prec == 1 else " sm_max_mhz x 148 SM x 128 FFMA x 2 (DESIGN.md)"),
+                         "latency_floor_ms": floor_ms, "latency_frac": floor_ms / t_dec},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 6 * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

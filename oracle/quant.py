@@ -5,12 +5,16 @@ probability of a 8-bit grayscale value. The output layer uses the softmax
 function as activation function."
 
 The paper is silent on turning the PDF into the integer table rANS needs
-(SPEC S:224 calls it "invented — artifact plumbing").  Reading R5 ("Q1"):
-with precision k (2^k total) and n symbols,
-    f_i = 1 + floor(fl32(p_i * (2^k - n)))            (fp32 multiply, RN)
-    R   = 2^k - sum_i f_i ;  a = first index of max_i f_i ;  f_a += R
+(SPEC S:224 calls it "invented — artifact plumbing").  Reading R5 (DESIGN.md,
+"Q1'"): with precision k (total 2^k) and n symbols,
+    f_i = 1 + floor(fl32(p_i * (2^k - n - 1)))         (fp32 multiply, RN)
+    R   = 2^k - sum_i f_i   (>= 0, see below) ;  f_{n-1} += R
     c_i = sum_{j<i} f_j                                (exclusive prefix sum)
-For k = 16, n = 256 the scale is 65280.
+For k = 16, n = 256 the scale is 65279.  Because sum_i p_i <= 1 + 258*2^-24
+for an fp32 softmax, sum_i fl(p_i * 65279) < 65281, so sum_i f_i <= 2^16 and
+R >= 0: every f_i >= 1 without a guard.  Putting the residual on the LAST
+symbol leaves c_i unchanged for i < n-1, so a decoder can search the slot in
+the same pass that builds the table.
 """
 
 from __future__ import annotations
@@ -27,15 +31,14 @@ def softmax_fp64(logits: np.ndarray) -> np.ndarray:
 
 
 def q1(p: np.ndarray, k: int = 16) -> np.ndarray:
-    """Reading R5 on float32 probabilities; works on (..., n). Returns int64 f."""
+    """Reading R5 (Q1') on float32 probabilities; works on (..., n). Returns int64 f."""
     p = np.asarray(p, dtype=np.float32)
     n = p.shape[-1]
-    scale = np.float32((1 << k) - n)
+    scale = np.float32((1 << k) - n - 1)
     f = 1 + np.floor(p * scale).astype(np.int64)        # fp32 product, then floor
-    tot = f.sum(axis=-1, keepdims=True)
-    r = (1 << k) - tot
-    a = np.argmax(f, axis=-1)                             # first index of the max
-    np.put_along_axis(f, a[..., None], np.take_along_axis(f, a[..., None], -1) + r, -1)
+    r = (1 << k) - f.sum(axis=-1)
+    assert np.all(r >= 0), "sum of probabilities exceeds 1 + 258 ulp"
+    f[..., n - 1] += r
     assert np.all(f.sum(axis=-1) == (1 << k)) and np.all(f >= 1)
     return f
 

@@ -281,7 +281,8 @@ dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Pl
   const uint32_t hl = H - (p.nty - 1) * p.th;
   p.gpl = (hl + p.G - 1) / p.G;
   p.spi = (p.nty - 1) * p.ntx * p.gpt + p.ntx * p.gpl;
-  if (p.gpt > 1024) return fail(DLIC_E_INVALID_ARG, "more than 1024 groups per unit: raise group_rows or tile");
+  if (dec_smem_bytes(d.precision, std::max(p.gpt, (H - (p.nty - 1) * p.th + p.G - 1) / p.G)) > dec_smem_limit())
+    return fail(DLIC_E_INVALID_ARG, "too many row groups per unit for the decoder's shared memory: raise group_rows or tile");
   p.cap_words = 2 * p.G + p.G * p.tw;
   p.hdr_bytes = 58 + 4 * p.spi;
   p.tiles_per_unit = (uint32_t)(((uint64_t)p.tw * p.th + 127) / 128);
@@ -765,7 +766,7 @@ dlic_status dlic_info(char* buf, size_t cap) {
   snprintf(tmp, sizeof(tmp),
            "{\"device\": \"%s\", \"sm_count\": %d, \"cc\": %d, \"arch\": \"sm_100a\", "
            "\"engines\": [\"fp32_ffma\", \"bf16_tcgen05\"], \"enc_smem\": [%zu, %zu], \"dec_smem\": [%zu, %zu]}",
-           name, sms, cc, enc_smem_bytes(0), enc_smem_bytes(1), dec_smem_bytes(0), dec_smem_bytes(1));
+           name, sms, cc, enc_smem_bytes(0), enc_smem_bytes(1), dec_smem_bytes(0, 16), dec_smem_bytes(1, 16));
   if (strlen(tmp) + 1 > cap) return fail(DLIC_E_BUFFER_TOO_SMALL, "info buffer");
   memcpy(buf, tmp, strlen(tmp) + 1);
   return DLIC_OK;

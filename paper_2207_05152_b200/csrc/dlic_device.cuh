@@ -2,16 +2,22 @@
 //
 // * PTX wrappers for tcgen05 (MMA with A in TMEM, TMEM ld/st/alloc), mbarrier
 //   and thread-block-cluster (DSMEM) operations, sm_100a only.
+// * Thread organisation shared by the encoder and the decoder: 512 threads =
+//   16 warps per CTA; threadIdx = 128*j + row.  `row` (0..127) is the pixel
+//   row of the M=128 tile = the TMEM lane, so warp w serves lane quadrant w&3
+//   (the tcgen05.ld/st rule) and column group j = w>>2 of every row.  Each
+//   row's network evaluation is split over its 4 column groups; the groups
+//   combine partial results through spare TMEM columns (TcEngine) or shared
+//   memory (Fp32Engine).
 // * The two density-estimator engines (P:96 dense network, reading R4):
 //     TcEngine   bf16 operands on 5th-gen tensor cores; weights resident in
 //                shared memory in the UMMA no-swizzle K-major core-matrix
-//                layout; activations and accumulators live in TMEM; one
-//                thread owns one TMEM lane = one pixel row of the M=128 tile.
-//     Fp32Engine fp32 FFMA on CUDA cores, one thread per pixel, k ascending.
-// * The deterministic softmax -> Q1 table -> CDF step (reading R5),
-//   written with explicit _rn/_rd intrinsics so encoder and decoder derive
-//   bit-identical tables ("the same matrices ... rounding errors ... are
-//   the same").
+//                layout; activations and accumulators live in TMEM.
+//     Fp32Engine fp32 FFMA on CUDA cores, k ascending for every output.
+// * The deterministic softmax -> Q1' table -> CDF step (reading R5),
+//   written with explicit _rn/_rd intrinsics and a fixed reduction tree so
+//   encoder and decoder derive bit-identical tables ("the same matrices
+//   ... rounding errors ... are the same during encoding and decoding").
 #pragma once
 #include <cstdint>
 #include <cuda_bf16.h>
@@ -25,10 +31,12 @@ constexpr int KPAD = 80;       // layer-1 K padded to a multiple of 16 for kind:
 constexpr int HID = 128;       // P100K hidden width (R4)
 constexpr int NOUT = 256;      // 8-bit alphabet
 constexpr int NLAYER = 6;      // "six dense layers"
-constexpr int ROWS = 128;      // rows per CTA = TMEM lanes = threads
+constexpr int ROWS = 128;      // rows per CTA = TMEM lanes
+constexpr int NGRP = 4;        // column groups per row
+constexpr int NTHREADS = ROWS * NGRP;
 constexpr uint32_t RANS_L = 1u << 16;
 constexpr float LOG2E = 1.4426950408889634f;
-constexpr float Q1_SCALE = 65280.0f;  // 2^16 - 256 (R5)
+constexpr float Q1_SCALE = 65279.0f;  // 2^16 - 257 (R5, Q1')
 
 // bf16 weight image (bytes) per layer, core-matrix layout (see host packer)
 __host__ __device__ constexpr int layer_k(int l) { return l == 0 ? KPAD : HID; }
@@ -39,6 +47,7 @@ __host__ __device__ constexpr uint32_t wimg_off(int l) {
 constexpr uint32_t WIMG_BYTES = 217088;  // 20480 + 4*32768 + 65536
 constexpr int BIAS_OFF_LAST = 5 * HID;   // biases: 5 x 128 hidden, then 256
 constexpr int BIAS_TOTAL = 5 * HID + NOUT;
+constexpr uint32_t BIAS_BYTES = BIAS_TOTAL * 4;
 
 // fp32 weight blob: per layer W[K][N] then b[N]; K of layer 0 is KIN (78)
 __host__ __device__ constexpr int f32_k(int l) { return l == 0 ? KIN : HID; }
@@ -49,15 +58,24 @@ __host__ __device__ constexpr uint32_t f32_off(int l) {
 }
 
 // TMEM column map (one 512-column allocation per CTA)
-constexpr uint32_t TM_D = 0;     // accumulator, up to 256 columns
+constexpr uint32_t TM_D = 0;     // accumulator / logits / e / f, 256 columns
 constexpr uint32_t TM_A = 256;   // A operand, K/2 columns (bf16 pairs), up to 64
+constexpr uint32_t TM_X = 320;   // exchange slots: 4 columns (one per group) per slot
 constexpr uint32_t TM_COLS = 512;
+constexpr int NXSLOT = 7;  // 0 max, 1 Z, 2 F, 3 fc, 4/5 search result, 6 slot
 
 // ------------------------------------------------------------- small PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int tile_row() { return threadIdx.x & (ROWS - 1); }
+__device__ __forceinline__ int col_grp() { return threadIdx.x >> 7; }
+
+// named barrier over the 4 warps that share one TMEM lane quadrant
+__device__ __forceinline__ void quad_sync() {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + ((threadIdx.x >> 5) & 3)), "r"(128) : "memory");
+}
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
@@ -128,10 +146,12 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
                : "memory");
 }
 
-#define DLIC_R8(i) "=r"(v[i]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3]), "=r"(v[i + 4]), "=r"(v[i + 5]), "=r"(v[i + 6]), "=r"(v[i + 7])
+#define DLIC_R4(i) "=r"(v[i]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3])
+#define DLIC_R8(i) DLIC_R4(i), DLIC_R4(i + 4)
+#define DLIC_W2(i) "r"(v[i]), "r"(v[i + 1])
 #define DLIC_W8(i) "r"(v[i]), "r"(v[i + 1]), "r"(v[i + 2]), "r"(v[i + 3]), "r"(v[i + 4]), "r"(v[i + 5]), "r"(v[i + 6]), "r"(v[i + 7])
 
-// 32 lanes (one per thread of the warp) x 32 consecutive 32-bit columns
+// 32 lanes (one per thread of the warp) x N consecutive 32-bit columns
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -139,7 +159,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : DLIC_R8(0), DLIC_R8(8), DLIC_R8(16), DLIC_R8(24)
       : "r"(taddr));
 }
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];" : DLIC_R4(0) : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      DLIC_W8(0), DLIC_W8(8), DLIC_W8(16), DLIC_W8(24)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
           taddr),
@@ -150,6 +180,12 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
                DLIC_W8(0)
                : "memory");
+}
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), DLIC_W2(0) : "memory");
+}
+__device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
 }
 
 // ---- clusters / DSMEM
@@ -181,24 +217,32 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 // ---------------------------------------------------------------- engines
-// Both engines expose:  run(...) then logits32(j, v) giving logits
-// [32j, 32j+32) of this thread's row, bias included, as fp32.
+// Common engine interface (per thread = (row, group j)):
+//   ld32(col, v) / st32(col, v)   32 columns [col, col+32) of this row's
+//                                 logit/work space (256 columns), raw bits
+//   bias_last(col)                final-layer bias (added once in pass 1)
+//   xput(slot, v); xsync(); xget4(slot, v4)   exchange one word per group
 
 struct TcEngine {
   uint32_t tmem;       // TMEM base (lane 0, column base)
   uint32_t wsmem;      // shared address of the bf16 weight image
-  const float* bias;   // global [BIAS_TOTAL]
+  const float* bias;   // shared [BIAS_TOTAL]
   uint32_t bar;        // shared address of the MMA-completion mbarrier
   uint32_t phase;
 
   __device__ __forceinline__ uint32_t lane_off() const { return ((threadIdx.x >> 5) & 3u) << 21; }
 
-  // a[40]: this row's 80 bf16 inputs packed in pairs (element 2i in bits 0-15)
-  __device__ void run(const uint32_t (&a)[40]) {
+  // Layer-1 input: this thread's 10 packed bf16 pairs = inputs [20j, 20j+20).
+  __device__ __forceinline__ void put_input(const uint32_t (&a)[10]) const {
+    const uint32_t base = tmem + lane_off() + TM_A + 10u * (uint32_t)col_grp();
+    tmem_st8(base, a);
+    tmem_st2(base + 8, a + 8);
+  }
+
+  // Runs the 6 layers; the input must have been stored with put_input.
+  __device__ void run() {
     const uint32_t lo = lane_off();
-    tmem_st16(tmem + lo + TM_A, *reinterpret_cast<const uint32_t(*)[16]>(&a[0]));
-    tmem_st16(tmem + lo + TM_A + 16, *reinterpret_cast<const uint32_t(*)[16]>(&a[16]));
-    tmem_st8(tmem + lo + TM_A + 32, &a[32]);
+    const int j = col_grp();
     tc_wait_st();
 #pragma unroll 1
     for (int l = 0; l < NLAYER; ++l) {
@@ -208,8 +252,8 @@ struct TcEngine {
         tc_fence_after();
         const int K = layer_k(l), N = layer_n(l);
         const uint32_t id = umma_idesc(128, N);
-        const uint32_t lbo = (uint32_t)N * 16u;        // next 8-wide K core matrix
-        const uint32_t kstep = 2u * (uint32_t)(N / 8) * 128u;  // one K=16 slice
+        const uint32_t lbo = (uint32_t)N * 16u;                 // next 8-wide K core matrix
+        const uint32_t kstep = 2u * (uint32_t)(N / 8) * 128u;   // one K=16 slice
         for (int kk = 0; kk < K / 16; ++kk) {
           const uint64_t bd = umma_desc(wsmem + wimg_off(l) + (uint32_t)kk * kstep, lbo, 128u);
           umma_ts(tmem + TM_D, tmem + TM_A + (uint32_t)kk * 8u, bd, id, kk > 0 ? 1u : 0u);
@@ -219,60 +263,81 @@ struct TcEngine {
       mbar_wait(bar, phase);
       phase ^= 1u;
       tc_fence_after();
-      if (l < NLAYER - 1) {
-        const float* b = bias + l * HID;
-#pragma unroll 1
-        for (int j = 0; j < HID / 32; ++j) {
-          uint32_t v[32];
-          tmem_ld32(tmem + lo + TM_D + (uint32_t)j * 32u, v);
-          tc_wait_ld();
-          uint32_t p[16];
+      if (l < NLAYER - 1) {  // bias + ReLU + bf16 -> next A; this group: columns [32j, 32j+32)
+        const float4* b4 = reinterpret_cast<const float4*>(bias + l * HID + 32 * j);
+        uint32_t v[32];
+        tmem_ld32(tmem + lo + TM_D + 32u * (uint32_t)j, v);
+        tc_wait_ld();
+        uint32_t p[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float x0 = fmaxf(__fadd_rn(__uint_as_float(v[2 * i]), __ldg(b + 32 * j + 2 * i)), 0.0f);
-            const float x1 = fmaxf(__fadd_rn(__uint_as_float(v[2 * i + 1]), __ldg(b + 32 * j + 2 * i + 1)), 0.0f);
-            p[i] = pack_bf16(x0, x1);
-          }
-          tmem_st16(tmem + lo + TM_A + (uint32_t)j * 16u, p);
+        for (int q = 0; q < 8; ++q) {
+          const float4 b = b4[q];
+          const float x0 = fmaxf(__fadd_rn(__uint_as_float(v[4 * q + 0]), b.x), 0.0f);
+          const float x1 = fmaxf(__fadd_rn(__uint_as_float(v[4 * q + 1]), b.y), 0.0f);
+          const float x2 = fmaxf(__fadd_rn(__uint_as_float(v[4 * q + 2]), b.z), 0.0f);
+          const float x3 = fmaxf(__fadd_rn(__uint_as_float(v[4 * q + 3]), b.w), 0.0f);
+          p[2 * q] = pack_bf16(x0, x1);
+          p[2 * q + 1] = pack_bf16(x2, x3);
         }
+        tmem_st16(tmem + lo + TM_A + 16u * (uint32_t)j, p);
         tc_wait_st();
       }
     }
   }
 
-  __device__ __forceinline__ void logits32(int j, float (&o)[32]) const {
-    uint32_t v[32];
-    tmem_ld32(tmem + lane_off() + TM_D + (uint32_t)j * 32u, v);
+  __device__ __forceinline__ void ld32(int col, uint32_t (&v)[32]) const {
+    tmem_ld32(tmem + lane_off() + TM_D + (uint32_t)col, v);
     tc_wait_ld();
-    const float* b = bias + BIAS_OFF_LAST + 32 * j;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) o[i] = __fadd_rn(__uint_as_float(v[i]), __ldg(b + i));
+  }
+  __device__ __forceinline__ void st32(int col, const uint32_t (&v)[32]) const {
+    tmem_st32(tmem + lane_off() + TM_D + (uint32_t)col, v);
+  }
+  __device__ __forceinline__ float4 bias4_last(int col) const {
+    return *reinterpret_cast<const float4*>(bias + BIAS_OFF_LAST + col);
+  }
+  __device__ __forceinline__ void xput(int slot, uint32_t v) const {
+    tmem_st1(tmem + lane_off() + TM_X + 4u * (uint32_t)slot + (uint32_t)col_grp(), v);
+  }
+  __device__ __forceinline__ void xsync() const {
+    tc_wait_st();
+    tc_fence_before();
+    quad_sync();
+    tc_fence_after();
+  }
+  __device__ __forceinline__ void xget4(int slot, uint32_t (&v)[4]) const {
+    tmem_ld4(tmem + lane_off() + TM_X + 4u * (uint32_t)slot, v);
+    tc_wait_ld();
   }
 };
 
-// CUDA-core fp32 engine.  buf0: [256][ROWS] floats, buf1: [128][ROWS] floats
-// (shared, column = thread).  The input features must be written by the
-// caller to buf0[k*ROWS + tid], k < 78.  Each thread reads/writes only its own
-// column, so no barriers are needed.
+// CUDA-core fp32 engine.  Shared buffers, column = row of the tile:
+//   buf0: [256][ROWS] floats (input features / hidden / logits), buf1: [128][ROWS],
+//   xbuf: [NXSLOT][NGRP][ROWS] words.  Group j computes outputs
+//   [N/4*j, N/4*(j+1)) of every layer for its row, k ascending.
 struct Fp32Engine {
   float* buf0;
   float* buf1;
+  uint32_t* xbuf;
   const float* w;  // global fp32 blob (f32_off layout)
 
+  __device__ __forceinline__ void put_input(int k, float x) const { buf0[k * ROWS + tile_row()] = x; }
+
   __device__ void run() {
-    const int t = threadIdx.x;
+    const int t = tile_row(), j = col_grp();
 #pragma unroll 1
     for (int l = 0; l < NLAYER; ++l) {
+      quad_sync();  // inputs of this layer (written by the row's 4 groups) are complete
       const float* in = (l & 1) ? buf1 : buf0;
       float* out = (l & 1) ? buf0 : buf1;
       const int K = f32_k(l), N = layer_n(l);
       const float* W = w + f32_off(l);
       const float* B = W + K * N;
+      const int nq = N / NGRP;
 #pragma unroll 1
-      for (int n0 = 0; n0 < N; n0 += 32) {
+      for (int n0 = j * nq; n0 < (j + 1) * nq; n0 += 32) {
         float acc[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
+        for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
 #pragma unroll 2
         for (int k = 0; k < K; ++k) {
           const float a = in[k * ROWS + t];
@@ -286,165 +351,242 @@ struct Fp32Engine {
             acc[4 * q + 3] = __fmaf_rn(a, w4.w, acc[4 * q + 3]);
           }
         }
+        // the next layer reads `out` only after quad_sync; `in` of this layer
+        // is not overwritten here (ping-pong buffers), except that layer 5
+        // writes buf0, which layer 4 read: ordered by the sync at layer 5's top.
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float z = __fadd_rn(acc[j], __ldg(B + n0 + j));
+        for (int i = 0; i < 32; ++i) {
+          float z = __fadd_rn(acc[i], __ldg(B + n0 + i));
           if (l < NLAYER - 1) z = fmaxf(z, 0.0f);
-          out[(n0 + j) * ROWS + t] = z;
+          out[(n0 + i) * ROWS + t] = z;
         }
       }
     }
+    quad_sync();  // logits complete
   }
-  __device__ __forceinline__ void logits32(int j, float (&o)[32]) const {
-    const int t = threadIdx.x;
+  __device__ __forceinline__ void ld32(int col, uint32_t (&v)[32]) const {
+    const int t = tile_row();
 #pragma unroll
-    for (int i = 0; i < 32; ++i) o[i] = buf0[(32 * j + i) * ROWS + t];
+    for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(buf0[(col + i) * ROWS + t]);
+  }
+  __device__ __forceinline__ void st32(int col, const uint32_t (&v)[32]) const {
+    const int t = tile_row();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) buf0[(col + i) * ROWS + t] = __uint_as_float(v[i]);
+  }
+  __device__ __forceinline__ float4 bias4_last(int) const { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ __forceinline__ void xput(int slot, uint32_t v) const {
+    xbuf[(slot * NGRP + col_grp()) * ROWS + tile_row()] = v;
+  }
+  __device__ __forceinline__ void xsync() const { quad_sync(); }
+  __device__ __forceinline__ void xget4(int slot, uint32_t (&v)[4]) const {
+#pragma unroll
+    for (int g = 0; g < NGRP; ++g) v[g] = xbuf[(slot * NGRP + g) * ROWS + tile_row()];
   }
 };
 
-// ------------------------------------------------- softmax -> Q1 -> CDF
-// Reading R5: p_i = fl(e_i * fl(1/Z)), e_i = 2^(l_i*log2e - m*log2e) (MUFU ex2,
-// identical instruction in encoder and decoder), Z summed i = 0..255 in order;
-// f_i = 1 + floor(fl(p_i * 65280)); R = 65536 - sum f; f_a += R at the first
-// argmax a; c = exclusive prefix sum.
+// ------------------------------------------------- softmax -> Q1' -> CDF
+// Reading R5 (Q1'), per row, with group j owning logits [64j, 64j+64):
+//   m = max_i l_i ;  e_i = 2^(l_i*log2e - m*log2e) (MUFU ex2, FFMA form);
+//   Z = ((Z_0 + Z_1) + Z_2) + Z_3, Z_j = sum over the group's i ascending;
+//   p_i = e_i * (1/Z) (RN);  f_i = 1 + floor(p_i * 65279);
+//   R = 2^16 - sum f_i >= 0 ; f_255 += R ;  c_i = exclusive prefix sum.
+// The logit space is overwritten in place: biased logits, then e, then f.
 
-struct SoftmaxStats {
-  float nm;   // -m * log2e
-  float inv;  // 1 / Z
+struct Q1Row {
+  uint32_t F[NGRP];  // per-group sums of the unadjusted f
+  uint32_t R;        // residual on symbol 255
 };
 
-template <class Eng>
-__device__ __forceinline__ SoftmaxStats softmax_stats(const Eng& e) {
-  float m = -INFINITY;
-#pragma unroll 1
-  for (int j = 0; j < NOUT / 32; ++j) {
-    float v[32];
-    e.logits32(j, v);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) m = fmaxf(m, v[i]);
-  }
-  SoftmaxStats s;
-  s.nm = __fmul_rn(-m, LOG2E);
-  float z = 0.0f;
-#pragma unroll 1
-  for (int j = 0; j < NOUT / 32; ++j) {
-    float v[32];
-    e.logits32(j, v);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) z = __fadd_rn(z, ex2_approx(__fmaf_rn(v[i], LOG2E, s.nm)));
-  }
-  s.inv = __frcp_rn(z);
-  return s;
-}
-
-__device__ __forceinline__ float q1_prob(float l, const SoftmaxStats& s) {
-  return __fmul_rn(ex2_approx(__fmaf_rn(l, LOG2E, s.nm)), s.inv);
-}
-// 1 + floor(p * 65280) for p in [0, 1]: x + 2^23 rounded toward -inf has ulp 1.
+// 1 + floor(p * 65279) for p in [0, 1.00002]: x + 2^23 rounded toward -inf has ulp 1.
 __device__ __forceinline__ uint32_t q1_freq(float p) {
   const float x = __fmul_rn(p, Q1_SCALE);
   return __float_as_uint(__fadd_rd(x, 8388608.0f)) - 0x4B000000u + 1u;
 }
 
-// Pass over the unadjusted table: total F, first argmax a (and f_a), and for
-// `sym` its f and exclusive cum.
+// Passes 1, 2, A.  `sym` (encoder, else -1): returns through fs/cs_local the
+// unadjusted f and group-local exclusive cum of sym if it lies in this group.
+// probs (nullable): p_i of this group's columns (debug export).
 template <class Eng>
-__device__ __forceinline__ void q1_scan(const Eng& e, const SoftmaxStats& s, int sym, uint32_t& F, int& a,
-                                        uint32_t& fsym, uint32_t& csym) {
-  F = 0;
-  a = 0;
-  uint32_t best = 0;
-  fsym = 0;
-  csym = 0;
-#pragma unroll 1
-  for (int j = 0; j < NOUT / 32; ++j) {
-    float v[32];
-    e.logits32(j, v);
+__device__ __forceinline__ Q1Row q1_table(const Eng& e, int sym, uint32_t& fs, uint32_t& cs_local,
+                                          float* probs) {
+  const int j = col_grp();
+  const int c0 = 64 * j;
+  // pass 1: biased logits, stored back; max
+  float m = -INFINITY;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t v[32];
+    e.ld32(c0 + 32 * h, v);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 b = e.bias4_last(c0 + 32 * h + 4 * q);
+      const float l0 = __fadd_rn(__uint_as_float(v[4 * q + 0]), b.x);
+      const float l1 = __fadd_rn(__uint_as_float(v[4 * q + 1]), b.y);
+      const float l2 = __fadd_rn(__uint_as_float(v[4 * q + 2]), b.z);
+      const float l3 = __fadd_rn(__uint_as_float(v[4 * q + 3]), b.w);
+      v[4 * q + 0] = __float_as_uint(l0);
+      v[4 * q + 1] = __float_as_uint(l1);
+      v[4 * q + 2] = __float_as_uint(l2);
+      v[4 * q + 3] = __float_as_uint(l3);
+      m = fmaxf(m, fmaxf(fmaxf(l0, l1), fmaxf(l2, l3)));
+    }
+    e.st32(c0 + 32 * h, v);
+  }
+  e.xput(0, __float_as_uint(m));
+  e.xsync();
+  uint32_t x4[4];
+  e.xget4(0, x4);
+  m = fmaxf(fmaxf(__uint_as_float(x4[0]), __uint_as_float(x4[1])),
+            fmaxf(__uint_as_float(x4[2]), __uint_as_float(x4[3])));
+  const float nm = __fmul_rn(-m, LOG2E);
+  // pass 2: e_i stored back; Z_j in index order
+  float z = 0.0f;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t v[32];
+    e.ld32(c0 + 32 * h, v);
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      const uint32_t f = q1_freq(q1_prob(v[i], s));
-      const int idx = 32 * j + i;
-      if (idx == sym) {
-        fsym = f;
-        csym = F;
+      const float ei = ex2_approx(__fmaf_rn(__uint_as_float(v[i]), LOG2E, nm));
+      z = __fadd_rn(z, ei);
+      v[i] = __float_as_uint(ei);
+    }
+    e.st32(c0 + 32 * h, v);
+  }
+  e.xput(1, __float_as_uint(z));
+  e.xsync();
+  e.xget4(1, x4);
+  const float Z = __fadd_rn(__fadd_rn(__fadd_rn(__uint_as_float(x4[0]), __uint_as_float(x4[1])),
+                                      __uint_as_float(x4[2])),
+                            __uint_as_float(x4[3]));
+  const float inv = __frcp_rn(Z);
+  // pass A: p_i, f_i (stored back as integers), group sum
+  uint32_t F = 0;
+  fs = 0;
+  cs_local = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t v[32];
+    e.ld32(c0 + 32 * h, v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float p = __fmul_rn(__uint_as_float(v[i]), inv);
+      const uint32_t f = q1_freq(p);
+      if (c0 + 32 * h + i == sym) {
+        fs = f;
+        cs_local = F;
       }
-      if (f > best) {
-        best = f;
-        a = idx;
-      }
+      if (probs) probs[c0 + 32 * h + i] = p;
       F += f;
+      v[i] = f;
+    }
+    e.st32(c0 + 32 * h, v);
+  }
+  e.xput(2, F);
+  e.xsync();
+  e.xget4(2, x4);
+  Q1Row r;
+#pragma unroll
+  for (int g = 0; g < NGRP; ++g) r.F[g] = x4[g];
+  r.R = 65536u - (x4[0] + x4[1] + x4[2] + x4[3]);
+  return r;
+}
+
+// Final integer table of this group's 64 columns (debug export).
+template <class Eng>
+__device__ __forceinline__ void q1_store_freqs(const Eng& e, const Q1Row& r, uint16_t* freqs) {
+  const int j = col_grp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t v[32];
+    e.ld32(64 * j + 32 * h, v);  // all lanes load (tcgen05.ld is .sync.aligned)
+    if (freqs) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        uint32_t f = v[i];
+        if (j == NGRP - 1 && h == 1 && i == 31) f += r.R;
+        freqs[64 * j + 32 * h + i] = (uint16_t)f;
+      }
     }
   }
 }
 
-// Encoder: (f_s, c_s) of the true symbol after the residual adjustment.
+// Encoder: (f_s | c_s << 16) of the true symbol (all threads of the row).
+// probs/freqs (nullable, per row, 256 entries): debug export.
 template <class Eng>
-__device__ __forceinline__ uint32_t q1_encode(const Eng& e, int sym) {
-  const SoftmaxStats s = softmax_stats(e);
-  uint32_t F, fs, cs;
-  int a;
-  q1_scan(e, s, sym, F, a, fs, cs);
-  const uint32_t R = 65536u - F;  // may wrap if F > 65536 (guarded: unsigned add is exact mod 2^32)
-  if (a == sym) fs += R;
-  if (a < sym) cs += R;
-  return fs | (cs << 16);
+__device__ __forceinline__ uint32_t q1_encode(const Eng& e, int sym, float* probs = nullptr,
+                                              uint16_t* freqs = nullptr, bool export_freqs = false) {
+  uint32_t fs, csl;
+  const Q1Row r = q1_table(e, sym, fs, csl, probs);
+  if (export_freqs) q1_store_freqs(e, r, freqs);
+  const int j = col_grp();
+  uint32_t packed = 0;
+  if ((sym >> 6) == j) {
+    uint32_t base = 0;
+    for (int g = 0; g < j; ++g) base += r.F[g];
+    if (sym == NOUT - 1) fs += r.R;
+    packed = fs | ((base + csl) << 16);
+  }
+  e.xput(3, packed);
+  e.xsync();
+  uint32_t x4[4];
+  e.xget4(3, x4);
+  return x4[0] | x4[1] | x4[2] | x4[3];
 }
 
-// Decoder: symbol s with c_s <= slot < c_s + f_s.  Returns s; fs/cs adjusted.
+// Decoder: symbol s with c_s <= slot < c_s + f_s (all threads of the row).
+// Only the group whose range holds the slot finds it; the search is
+// predicated (every lane executes the same TMEM loads).
+// `slot` is read from group 0 (the rANS lane owner), published through
+// exchange slot 6 and picked up after q1_table's first exchange barrier.
 template <class Eng>
-__device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot, uint32_t& fs_out, uint32_t& cs_out) {
-  const SoftmaxStats s = softmax_stats(e);
-  uint32_t F, fs, cs;
-  int a;
-  q1_scan(e, s, -1, F, a, fs, cs);
-  const uint32_t R = 65536u - F;
-  uint32_t cum = 0;
+__device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot0, uint32_t& fs_out, uint32_t& cs_out) {
+  uint32_t fs, csl;
+  e.xput(6, slot0);
+  const Q1Row r = q1_table(e, -1, fs, csl, nullptr);
+  uint32_t s4[4];
+  e.xget4(6, s4);
+  const uint32_t slot = s4[0];
+  const int j = col_grp();
+  uint32_t base = 0;
+#pragma unroll
+  for (int g = 0; g < NGRP; ++g)
+    if (g < j) base += r.F[g];
+  const uint32_t top = base + r.F[j] + (j == NGRP - 1 ? r.R : 0u);
+  const bool mine = slot >= base && slot < top;
+  uint32_t cum = base;
   int sym = 0;
-  uint32_t f_sel = 0, c_sel = 0;
-#pragma unroll 1
-  for (int j = 0; j < NOUT / 32; ++j) {
-    float v[32];
-    e.logits32(j, v);
+  uint32_t fsel = 0, csel = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t v[32];
+    e.ld32(64 * j + 32 * h, v);
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      const int idx = 32 * j + i;
-      uint32_t f = q1_freq(q1_prob(v[i], s));
-      if (idx == a) f += R;
-      if (slot - cum < f) {  // cum <= slot < cum + f (unsigned: slot >= cum)
-        sym = idx;
-        f_sel = f;
-        c_sel = cum;
+      uint32_t f = v[i];
+      if (j == NGRP - 1 && h == 1 && i == 31) f += r.R;
+      if (slot - cum < f) {  // cum <= slot < cum + f
+        sym = 64 * j + 32 * h + i;
+        fsel = f;
+        csel = cum;
       }
       cum += f;
     }
   }
-  fs_out = f_sel;
-  cs_out = c_sel;
-  return sym;
-}
-
-// Debug export of p (fp32) and the final integer table.
-template <class Eng>
-__device__ void q1_export(const Eng& e, float* probs, uint16_t* freqs) {
-  const SoftmaxStats s = softmax_stats(e);
-  uint32_t F, fs, cs;
-  int a;
-  q1_scan(e, s, -1, F, a, fs, cs);
-  const uint32_t R = 65536u - F;
-#pragma unroll 1
-  for (int j = 0; j < NOUT / 32; ++j) {
-    float v[32];
-    e.logits32(j, v);
+  e.xput(4, mine ? ((uint32_t)sym | (fsel << 8)) : 0xFFFFFFFFu);
+  e.xput(5, csel);
+  e.xsync();
+  uint32_t k4[4], c4[4];
+  e.xget4(4, k4);
+  e.xget4(5, c4);
+  int g = 0;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int idx = 32 * j + i;
-      const float p = q1_prob(v[i], s);
-      uint32_t f = q1_freq(p);
-      if (idx == a) f += R;
-      if (probs) probs[idx] = p;
-      if (freqs) freqs[idx] = (uint16_t)f;
-    }
-  }
+  for (int q = 0; q < NGRP; ++q)
+    if (k4[q] != 0xFFFFFFFFu) g = q;
+  fs_out = k4[g] >> 8;
+  cs_out = c4[g];
+  return (int)(k4[g] & 0xFFu);
 }
 
 }  // namespace dlic

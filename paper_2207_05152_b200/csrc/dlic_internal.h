@@ -90,7 +90,8 @@ cudaError_t launch_rans_dec_tables(const Plan& p, const uint8_t* d_bits, const u
                                    const uint32_t* d_slen, const uint16_t* d_tables, uint8_t* d_out,
                                    int32_t* d_status, cudaStream_t st);
 
-size_t dec_smem_bytes(uint32_t precision);
+size_t dec_smem_bytes(uint32_t precision, uint32_t max_groups);
+size_t dec_smem_limit();
 size_t enc_smem_bytes(uint32_t precision);
 
 }  // namespace dlic

@@ -27,13 +27,18 @@ __device__ __forceinline__ int off_dc(int j) { return j < 72 ? j % 9 - 6 : j - 7
 
 constexpr int RING_ROWS = ROWS + 8;                  // own 128 slots + 8 halo rows
 constexpr uint32_t RING_BYTES = 2u * RING_ROWS * 32u;  // 2 banks x 136 rows x 32 cols
-constexpr uint32_t MAX_GROUPS = 1024;                // per unit (cursor array in smem)
-constexpr uint32_t F32_BUF_BYTES = (NOUT + HID) * ROWS * 4u;  // 196608
+constexpr uint32_t F32_BUF_BYTES = (NOUT + HID) * ROWS * 4u;          // 196608
+constexpr uint32_t F32_X_BYTES = NXSLOT * NGRP * ROWS * 4u;          // 12288
+constexpr uint32_t MAX_DYN_SMEM = 232448 - 64;                       // 227 KB minus static
 
-size_t enc_smem_bytes(uint32_t precision) { return precision == 1 ? WIMG_BYTES : F32_BUF_BYTES; }
-size_t dec_smem_bytes(uint32_t precision) {
-  return (precision == 1 ? WIMG_BYTES : F32_BUF_BYTES) + RING_BYTES + MAX_GROUPS * 4u;
+size_t enc_smem_bytes(uint32_t precision) {
+  return precision == 1 ? WIMG_BYTES + BIAS_BYTES : F32_BUF_BYTES + F32_X_BYTES;
 }
+static uint32_t cursor_bytes(uint32_t ngroups) { return (ngroups * 4u + 15u) & ~15u; }
+size_t dec_smem_bytes(uint32_t precision, uint32_t max_groups) {
+  return enc_smem_bytes(precision) + RING_BYTES + cursor_bytes(max_groups);
+}
+size_t dec_smem_limit() { return MAX_DYN_SMEM; }
 
 // ------------------------------------------------------------ engine setup
 template <int PREC>
@@ -47,105 +52,129 @@ struct EngineSel<0> {
   using T = Fp32Engine;
 };
 
-__device__ __forceinline__ void load_wimg(uint8_t* smem, const uint8_t* wimg) {
-  const int4* src = reinterpret_cast<const int4*>(wimg);
-  int4* dst = reinterpret_cast<int4*>(smem);
-  for (uint32_t i = threadIdx.x; i < WIMG_BYTES / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+__device__ __forceinline__ void load_smem(uint8_t* dst, const void* src, uint32_t bytes) {
+  const int4* s4 = reinterpret_cast<const int4*>(src);
+  int4* d4 = reinterpret_cast<int4*>(dst);
+  for (uint32_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) d4[i] = __ldg(s4 + i);
 }
 
-// Build the engine input for this thread's row from a value getter.
-template <class Get>
-__device__ __forceinline__ void feed_tc(uint32_t (&a)[40], Get get) {
-#pragma unroll
-  for (int i = 0; i < 39; ++i) {
-    const float x0 = (float)get(2 * i) * 0.00390625f;      // v / 256, exact (R2)
-    const float x1 = (float)get(2 * i + 1) * 0.00390625f;
-    a[i] = pack_bf16(x0, x1);
-  }
-  a[39] = 0u;  // K padding 78, 79
-}
-template <class Get>
-__device__ __forceinline__ void feed_f32(float* buf0, Get get) {
-#pragma unroll
-  for (int j = 0; j < KIN; ++j) buf0[j * ROWS + threadIdx.x] = (float)get(j) * 0.00390625f;
-}
-
-// ------------------------------------------------------------ encoder MLP
+// Shared setup of both engines at kernel start (all threads).  Returns the
+// end of the engine's shared-memory region.
 template <int PREC>
-__global__ void __launch_bounds__(128, 1)
-    k_enc_mlp(Plan p, DevWeights w, const uint8_t* __restrict__ imgs, uint32_t* __restrict__ fc,
-              float* __restrict__ dbg_logits, float* __restrict__ dbg_probs, uint16_t* __restrict__ dbg_freqs) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar;
-  __shared__ uint32_t tslot;
-  const int tid = threadIdx.x;
-  typename EngineSel<PREC>::T eng;
+__device__ __forceinline__ uint8_t* engine_setup(typename EngineSel<PREC>::T& eng, uint8_t* smem, const DevWeights& w,
+                                                 uint64_t* bar, uint32_t* tslot) {
   if constexpr (PREC == 1) {
-    load_wimg(smem, w.wimg);
-    if (tid < 32) tmem_alloc(smem_u32(&tslot), TM_COLS);
-    if (tid == 0) {
-      mbar_init(smem_u32(&bar), 1);
+    load_smem(smem, w.wimg, WIMG_BYTES);
+    load_smem(smem + WIMG_BYTES, w.bias, BIAS_BYTES);
+    if (threadIdx.x < 32) tmem_alloc(smem_u32(tslot), TM_COLS);
+    if (threadIdx.x == 0) {
+      mbar_init(smem_u32(bar), 1);
       fence_mbar_init();
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    eng.tmem = tslot;
+    eng.tmem = *tslot;
     eng.wsmem = smem_u32(smem);
-    eng.bias = w.bias;
-    eng.bar = smem_u32(&bar);
+    eng.bias = reinterpret_cast<const float*>(smem + WIMG_BYTES);
+    eng.bar = smem_u32(bar);
     eng.phase = 0;
+    return smem + WIMG_BYTES + BIAS_BYTES;
   } else {
     eng.buf0 = reinterpret_cast<float*>(smem);
     eng.buf1 = eng.buf0 + NOUT * ROWS;
+    eng.xbuf = reinterpret_cast<uint32_t*>(smem + F32_BUF_BYTES);
     eng.w = w.w32;
+    return smem + F32_BUF_BYTES + F32_X_BYTES;
   }
+}
+
+template <int PREC>
+__device__ __forceinline__ void engine_teardown(typename EngineSel<PREC>::T& eng) {
+  if constexpr (PREC == 1) {
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) tmem_dealloc(eng.tmem, TM_COLS);
+  }
+}
+
+// Feed this thread's share of the 78 (80) window inputs: group j owns inputs
+// [20j, 20j+20); get(k) returns the pixel value of window offset k (0 fill).
+template <int PREC, class Eng, class Get>
+__device__ __forceinline__ void feed(const Eng& eng, Get get) {
+  const int j = col_grp();
+  if constexpr (PREC == 1) {
+    uint32_t a[10];
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+      const int k0 = 20 * j + 2 * i;
+      const float x0 = k0 < KIN ? (float)get(k0) * 0.00390625f : 0.0f;   // v / 256, exact (R2)
+      const float x1 = k0 + 1 < KIN ? (float)get(k0 + 1) * 0.00390625f : 0.0f;
+      a[i] = pack_bf16(x0, x1);
+    }
+    eng.put_input(a);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 20; ++i) {
+      const int k = 20 * j + i;
+      if (k < KIN) eng.put_input(k, (float)get(k) * 0.00390625f);
+    }
+  }
+}
+
+// ------------------------------------------------------------ encoder MLP
+// Persistent CTAs over 128-pixel tiles of the units' raster order.  Thread
+// (row, j): pixel = tile*128 + row; group j owns inputs [20j,20j+20), hidden
+// columns [32j,32j+32) and logits [64j,64j+64) (dlic_device.cuh).
+template <int PREC>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_enc_mlp(Plan p, DevWeights w, const uint8_t* __restrict__ imgs, uint32_t* __restrict__ fc,
+              float* __restrict__ dbg_logits, float* __restrict__ dbg_probs, uint16_t* __restrict__ dbg_freqs) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int row = tile_row(), j = col_grp();
+  typename EngineSel<PREC>::T eng;
+  engine_setup<PREC>(eng, smem, w, &bar, &tslot);
   const uint64_t total = (uint64_t)p.n_img * p.upi * p.tiles_per_unit;
+  const bool dbg = dbg_logits || dbg_probs || dbg_freqs;
 #pragma unroll 1
   for (uint64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
     const uint32_t u = (uint32_t)(tile / p.tiles_per_unit);
     const uint32_t k = (uint32_t)(tile % p.tiles_per_unit);
     const Unit un = unit_info(p, u);
-    const uint32_t q = k * 128u + (uint32_t)tid;
+    const uint32_t q = k * 128u + (uint32_t)row;
     const bool valid = q < un.w * un.h;
     const int r = valid ? (int)(q / un.w) : 0, c = valid ? (int)(q % un.w) : 0;
     const uint8_t* img = imgs + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
     const int uw = (int)un.w;
-    auto get = [&](int j) -> uint32_t {
-      const int rr = r + off_dr(j), cc = c + off_dc(j);
+    auto get = [&](int kk) -> uint32_t {
+      const int rr = r + off_dr(kk), cc = c + off_dc(kk);
       return (valid && rr >= 0 && cc >= 0 && cc < uw) ? (uint32_t)__ldg(img + (uint64_t)rr * p.W + cc) : 0u;
     };
-    if constexpr (PREC == 1) {
-      uint32_t a[40];
-      feed_tc(a, get);
-      eng.run(a);
-    } else {
-      feed_f32(eng.buf0, get);
-      eng.run();
-    }
+    feed<PREC>(eng, get);
+    eng.run();
     const int sym = valid ? (int)__ldg(img + (uint64_t)r * p.W + c) : 0;
-    const uint32_t v = q1_encode(eng, sym);
-    if (valid) fc[un.fc_off + q] = v;
-    if (dbg_logits || dbg_probs || dbg_freqs) {
-      const uint64_t gi = (uint64_t)un.img * p.W * p.H + (uint64_t)(un.y0 + r) * p.W + (un.x0 + c);
-      if (dbg_logits) {
+    const uint64_t gi = (uint64_t)un.img * p.W * p.H + (uint64_t)(un.y0 + r) * p.W + (un.x0 + c);
+    if (dbg && dbg_logits) {  // raw logits (bias added) of this group's 64 columns
 #pragma unroll 1
-        for (int j = 0; j < NOUT / 32; ++j) {
-          float o[32];
-          eng.logits32(j, o);
-          if (valid)
-            for (int i = 0; i < 32; ++i) dbg_logits[gi * NOUT + 32 * j + i] = o[i];
-        }
+      for (int h = 0; h < 2; ++h) {
+        uint32_t v[32];
+        eng.ld32(64 * j + 32 * h, v);
+        if (valid)
+          for (int i = 0; i < 32; ++i) {
+            const int cc = 64 * j + 32 * h + i;
+            float lv = __uint_as_float(v[i]);
+            if constexpr (PREC == 1) lv = __fadd_rn(lv, eng.bias[BIAS_OFF_LAST + cc]);
+            dbg_logits[gi * NOUT + cc] = lv;
+          }
       }
-      q1_export(eng, (valid && dbg_probs) ? dbg_probs + gi * NOUT : nullptr,
-                (valid && dbg_freqs) ? dbg_freqs + gi * NOUT : nullptr);
     }
+    const uint32_t v = q1_encode(eng, sym, (dbg && valid && dbg_probs) ? dbg_probs + gi * NOUT : nullptr,
+                                 (dbg && valid && dbg_freqs) ? dbg_freqs + gi * NOUT : nullptr, dbg);
+    if (valid && j == 0) fc[un.fc_off + q] = v;
   }
-  if constexpr (PREC == 1) {
-    tc_fence_before();
-    __syncthreads();
-    if (tid < 32) tmem_dealloc(eng.tmem, TM_COLS);
-  }
+  engine_teardown<PREC>(eng);
 }
 
 // ------------------------------------------------------------ rANS encoder
@@ -374,53 +403,35 @@ __global__ void k_dec_prep(Plan p, const uint8_t* __restrict__ bits, const uint6
 }
 
 // ------------------------------------------------------------ decoder
+// One cluster of nc CTAs per unit; slot S = rank*128 + row holds rows
+// r = S (mod 128*nc) in turn.  Per front t: all 4 groups of a row
+// gather their share of the window from the shared-memory ring, run the
+// network, and search the Q1' table; group 0 (warps 0-3) owns the row's rANS
+// lane: state update, interleaved word reads (ballot/popc within the G-row
+// group, G | 32 so a group never leaves its warp), pixel publication.
 template <int PREC>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(NTHREADS, 1)
     k_decode(Plan p, DevWeights w, const uint8_t* __restrict__ bits, const uint64_t* __restrict__ cont_off,
              const uint32_t* __restrict__ sbase, const uint32_t* __restrict__ slen, uint8_t* __restrict__ out,
              int32_t* __restrict__ status) {
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
-  const int tid = threadIdx.x;
+  const int row = tile_row(), j = col_grp();
   const uint32_t lane = lane_id();
   const uint32_t NC = p.nc, NS = ROWS * NC;
   const uint32_t ns_shift = 7u + (NC == 1 ? 0u : NC == 2 ? 1u : NC == 4 ? 2u : 3u);
   const uint32_t rank = NC > 1 ? cluster_rank() : 0u;
   const uint32_t u = blockIdx.x / NC;
   const Unit un = unit_info(p, u);
-  const uint32_t S = rank * ROWS + (uint32_t)tid;
+  const uint32_t S = rank * ROWS + (uint32_t)row;
 
   typename EngineSel<PREC>::T eng;
-  uint8_t* ring;
-  if constexpr (PREC == 1) {
-    ring = smem + WIMG_BYTES;
-    load_wimg(smem, w.wimg);
-    if (tid < 32) tmem_alloc(smem_u32(&tslot), TM_COLS);
-    if (tid == 0) {
-      mbar_init(smem_u32(&bar), 1);
-      fence_mbar_init();
-    }
-  } else {
-    ring = smem + F32_BUF_BYTES;
-    eng.buf0 = reinterpret_cast<float*>(smem);
-    eng.buf1 = eng.buf0 + NOUT * ROWS;
-    eng.w = w.w32;
-  }
+  uint8_t* ring = engine_setup<PREC>(eng, smem, w, &bar, &tslot);
   uint32_t* cursor = reinterpret_cast<uint32_t*>(ring + RING_BYTES);
   const uint32_t G = p.G;
-  for (uint32_t g = tid; g < un.ngroups; g += ROWS) {
+  for (uint32_t g = threadIdx.x; g < un.ngroups; g += NTHREADS) {
     if ((((G * g) & (NS - 1)) >> 7) == rank) cursor[g] = 2u * min(G, un.h - G * g);
-  }
-  if constexpr (PREC == 1) {
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    eng.tmem = tslot;
-    eng.wsmem = smem_u32(smem);
-    eng.bias = w.bias;
-    eng.bar = smem_u32(&bar);
-    eng.phase = 0;
   }
   if (NC > 1) cluster_sync_all();
   else __syncthreads();
@@ -428,8 +439,7 @@ __global__ void __launch_bounds__(128, 1)
   const uint8_t* cbase = bits + cont_off[un.img];
   uint8_t* oimg = out + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
   const uint32_t ring_s = smem_u32(ring);
-  const uint32_t halo_rank = (rank + 1) % NC;
-  const uint32_t halo_base = NC > 1 ? map_cluster(ring_s, halo_rank) : ring_s;
+  const uint32_t halo_base = NC > 1 ? map_cluster(ring_s, (rank + 1) % NC) : ring_s;
   const int uw = (int)un.w, uh = (int)un.h;
   const int T = uw + 3 * (uh - 1);
   uint32_t x = 0;
@@ -451,72 +461,64 @@ __global__ void __launch_bounds__(128, 1)
       const uint32_t sidx = un.first_stream + g;
       const uint16_t* sw = reinterpret_cast<const uint16_t*>(cbase + (active ? sbase[sidx] : 0u));
       const uint32_t sl = active ? slen[sidx] : 0u;
-      if (active && c == 0) {  // the row's lane starts: flushed state (hi, lo)
+      if (j == 0 && active && c == 0) {  // the row's lane starts: flushed state (hi, lo)
         const uint32_t i = 2u * ((uint32_t)r - G * g);
         if (i + 1 < sl) x = ((uint32_t)sw[i] << 16) | (uint32_t)sw[i + 1];
         else err = 8;
       }
       // window gather from the ring (rows r-8..r of this slot's neighbourhood)
-      auto get = [&](int j) -> uint32_t {
-        const int d = -off_dr(j);
-        const int rr = r - d, cc = c + off_dc(j);
+      auto get = [&](int kk) -> uint32_t {
+        const int d = -off_dr(kk);
+        const int rr = r - d, cc = c + off_dc(kk);
         if (!active || rr < 0 || cc < 0 || cc >= uw) return 0u;
         const uint32_t bank = ((uint32_t)rr >> ns_shift) & 1u;
-        return ring[(bank * RING_ROWS + (uint32_t)(tid - d + 8)) * 32u + ((uint32_t)cc & 31u)];
+        return ring[(bank * RING_ROWS + (uint32_t)(row - d + 8)) * 32u + ((uint32_t)cc & 31u)];
       };
-      if constexpr (PREC == 1) {
-        uint32_t a[40];
-        feed_tc(a, get);
-        eng.run(a);
-      } else {
-        feed_f32(eng.buf0, get);
-        eng.run();
-      }
+      feed<PREC>(eng, get);
+      eng.run();
       const uint32_t slot = x & 0xFFFFu;
       uint32_t fs, cs;
       const int sym = q1_decode(eng, slot, fs, cs);
-      bool need = false;
-      if (active) {
-        x = fs * (x >> 16) + slot - cs;
-        need = x < RANS_L;
-      }
-      const uint32_t key = active ? g : (0x80000000u | lane);
-      const uint32_t gm = __match_any_sync(0xFFFFFFFFu, key);
-      const uint32_t readers = __ballot_sync(0xFFFFFFFFu, need) & gm;
-      uint32_t cur = 0;
-      if (active) cur = cursor[g];
-      __syncwarp();
-      if (need) {
-        const uint32_t wi = cur + __popc(readers & ((1u << lane) - 1u));
-        if (wi < sl) x = (x << 16) | (uint32_t)sw[wi];
-        else err = 8;
-      }
-      if (active && lane == (uint32_t)(__ffs(gm) - 1)) cursor[g] = cur + __popc(readers);
-      if (active) {
-        oimg[(uint64_t)r * p.W + c] = (uint8_t)sym;
-        const uint32_t bank = ((uint32_t)r >> ns_shift) & 1u;
-        const uint32_t col = (uint32_t)c & 31u;
-        ring[(bank * RING_ROWS + (uint32_t)tid + 8u) * 32u + col] = (uint8_t)sym;
-        if (tid >= ROWS - 8) {
-          const uint32_t hoff = (bank * RING_ROWS + (uint32_t)(tid - (ROWS - 8))) * 32u + col;
-          if (NC > 1) st_cluster_u8(halo_base + hoff, (uint32_t)sym);
-          else ring[hoff] = (uint8_t)sym;
+      if (j == 0) {
+        bool need = false;
+        if (active) {
+          x = fs * (x >> 16) + slot - cs;
+          need = x < RANS_L;
         }
-        if (c == uw - 1 && x != RANS_L) err = 6;  // end-of-lane invariant
+        const uint32_t key = active ? g : (0x80000000u | lane);
+        const uint32_t gm = __match_any_sync(0xFFFFFFFFu, key);
+        const uint32_t readers = __ballot_sync(0xFFFFFFFFu, need) & gm;
+        uint32_t cur = 0;
+        if (active) cur = cursor[g];
+        __syncwarp();
+        if (need) {
+          const uint32_t wi = cur + __popc(readers & ((1u << lane) - 1u));
+          if (wi < sl) x = (x << 16) | (uint32_t)sw[wi];
+          else err = 8;
+        }
+        if (active && lane == (uint32_t)(__ffs(gm) - 1)) cursor[g] = cur + __popc(readers);
+        if (active) {
+          oimg[(uint64_t)r * p.W + c] = (uint8_t)sym;
+          const uint32_t bank = ((uint32_t)r >> ns_shift) & 1u;
+          const uint32_t col = (uint32_t)c & 31u;
+          ring[(bank * RING_ROWS + (uint32_t)row + 8u) * 32u + col] = (uint8_t)sym;
+          if (row >= ROWS - 8) {
+            const uint32_t hoff = (bank * RING_ROWS + (uint32_t)(row - (ROWS - 8))) * 32u + col;
+            if (NC > 1) st_cluster_u8(halo_base + hoff, (uint32_t)sym);
+            else ring[hoff] = (uint8_t)sym;
+          }
+          if (c == uw - 1 && x != RANS_L) err = 6;  // end-of-lane invariant
+        }
       }
     }
     if (NC > 1) cluster_sync_all();
     else __syncthreads();
   }
-  for (uint32_t g = tid; g < un.ngroups; g += ROWS) {
+  for (uint32_t g = threadIdx.x; g < un.ngroups; g += NTHREADS) {
     if ((((G * g) & (NS - 1)) >> 7) == rank && cursor[g] != slen[un.first_stream + g]) err = 6;
   }
   if (err) atomicMax(status + un.img, err);
-  if constexpr (PREC == 1) {
-    tc_fence_before();
-    __syncthreads();
-    if (tid < 32) tmem_dealloc(eng.tmem, TM_COLS);
-  }
+  engine_teardown<PREC>(eng);
   if (NC > 1) cluster_sync_all();  // keep DSMEM alive until every CTA is done
 }
 
@@ -535,11 +537,11 @@ cudaError_t launch_enc_mlp(const Plan& p, const DevWeights& w, const uint8_t* d_
   if (p.precision == 1) {
     cudaError_t e = set_smem(k_enc_mlp<1>, sm);
     if (e != cudaSuccess) return e;
-    k_enc_mlp<1><<<grid, 128, sm, st>>>(p, w, d_imgs, d_fc, dbg_logits, dbg_probs, dbg_freqs);
+    k_enc_mlp<1><<<grid, NTHREADS, sm, st>>>(p, w, d_imgs, d_fc, dbg_logits, dbg_probs, dbg_freqs);
   } else {
     cudaError_t e = set_smem(k_enc_mlp<0>, sm);
     if (e != cudaSuccess) return e;
-    k_enc_mlp<0><<<grid, 128, sm, st>>>(p, w, d_imgs, d_fc, dbg_logits, dbg_probs, dbg_freqs);
+    k_enc_mlp<0><<<grid, NTHREADS, sm, st>>>(p, w, d_imgs, d_fc, dbg_logits, dbg_probs, dbg_freqs);
   }
   return cudaGetLastError();
 }
@@ -572,12 +574,12 @@ template <int PREC>
 static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uint8_t* d_bits,
                                    const uint64_t* d_cont_off, const uint32_t* d_sbase, const uint32_t* d_slen,
                                    uint8_t* d_imgs, int32_t* d_status, cudaStream_t st) {
-  const size_t sm = dec_smem_bytes(PREC);
+  const size_t sm = dec_smem_bytes(PREC, p.gpt > p.gpl ? p.gpt : p.gpl);
   cudaError_t e = set_smem(k_decode<PREC>, sm);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.n_img * p.upi * p.nc);
-  cfg.blockDim = dim3(128);
+  cfg.blockDim = dim3(NTHREADS);
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
   cudaLaunchAttribute at[1];

