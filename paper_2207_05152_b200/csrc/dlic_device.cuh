@@ -215,6 +215,59 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// relu then RN to bf16, lo in bits 0-15 (F2FP.RELU.BF16.PACK_AB)
+__device__ __forceinline__ uint32_t pack_bf16_relu(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// packed fp32 pairs (FADD2 / FMUL2 / FFMA2 on sm_100); each lane is IEEE RN
+// (or RM for add_rm), bit-identical to the scalar instruction.
+struct f2 {
+  uint64_t v;
+};
+__device__ __forceinline__ f2 f2_make(float a, float b) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ f2 f2_bits(uint32_t a, uint32_t b) { return f2_make(__uint_as_float(a), __uint_as_float(b)); }
+__device__ __forceinline__ void f2_split(f2 x, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v));
+}
+__device__ __forceinline__ f2 f2_add(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 f2_add_rm(f2 a, f2 b) {
+  f2 r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 f2_mul(f2 a, f2 b) {
+  f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 f2_fma(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return r;
+}
+
+// Optional phase profiler (debug: thread 0, clock64 deltas).
+struct Prof {
+  unsigned long long t = 0, acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  bool on = false;
+  __device__ __forceinline__ void mark(int k) {
+    if (on) {
+      const unsigned long long n = clock64();
+      acc[k] += n - t;
+      t = n;
+    }
+  }
+};
 
 // ---------------------------------------------------------------- engines
 // Common engine interface (per thread = (row, group j)):
@@ -254,9 +307,14 @@ struct TcEngine {
         const uint32_t id = umma_idesc(128, N);
         const uint32_t lbo = (uint32_t)N * 16u;                 // next 8-wide K core matrix
         const uint32_t kstep = 2u * (uint32_t)(N / 8) * 128u;   // one K=16 slice
-        for (int kk = 0; kk < K / 16; ++kk) {
-          const uint64_t bd = umma_desc(wsmem + wimg_off(l) + (uint32_t)kk * kstep, lbo, 128u);
-          umma_ts(tmem + TM_D, tmem + TM_A + (uint32_t)kk * 8u, bd, id, kk > 0 ? 1u : 0u);
+        // start-address field (bits 0-13, 16-byte units) advances by kstep/16
+        uint64_t bd = umma_desc(wsmem + wimg_off(l), lbo, 128u);
+        uint32_t at = tmem + TM_A;
+        umma_ts(tmem + TM_D, at, bd, id, 0u);
+        for (int kk = 1; kk < K / 16; ++kk) {
+          bd += kstep >> 4;
+          at += 8u;
+          umma_ts(tmem + TM_D, at, bd, id, 1u);
         }
         umma_commit(bar);
       }
@@ -272,12 +330,11 @@ struct TcEngine {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const float4 b = b4[q];
-          const float x0 = fmaxf(__fadd_rn(__uint_as_float(v[4 * q + 0]), b.x), 0.0f);
-          const float x1 = fmaxf(__fadd_rn(__uint_as_float(v[4 * q + 1]), b.y), 0.0f);
-          const float x2 = fmaxf(__fadd_rn(__uint_as_float(v[4 * q + 2]), b.z), 0.0f);
-          const float x3 = fmaxf(__fadd_rn(__uint_as_float(v[4 * q + 3]), b.w), 0.0f);
-          p[2 * q] = pack_bf16(x0, x1);
-          p[2 * q + 1] = pack_bf16(x2, x3);
+          float x0, x1, x2, x3;
+          f2_split(f2_add(f2_bits(v[4 * q + 0], v[4 * q + 1]), f2_make(b.x, b.y)), x0, x1);
+          f2_split(f2_add(f2_bits(v[4 * q + 2], v[4 * q + 3]), f2_make(b.z, b.w)), x2, x3);
+          p[2 * q] = pack_bf16_relu(x0, x1);  // relu(x) rounded to bf16 (RN)
+          p[2 * q + 1] = pack_bf16_relu(x2, x3);
         }
         tmem_st16(tmem + lo + TM_A + 16u * (uint32_t)j, p);
         tc_wait_st();
@@ -388,28 +445,55 @@ struct Fp32Engine {
 // ------------------------------------------------- softmax -> Q1' -> CDF
 // Reading R5 (Q1'), per row, with group j owning logits [64j, 64j+64):
 //   m = max_i l_i ;  e_i = 2^(l_i*log2e - m*log2e) (MUFU ex2, FFMA form);
-//   Z = ((Z_0 + Z_1) + Z_2) + Z_3, Z_j = sum over the group's i ascending;
-//   p_i = e_i * (1/Z) (RN);  f_i = 1 + floor(p_i * 65279);
-//   R = 2^16 - sum f_i >= 0 ; f_255 += R ;  c_i = exclusive prefix sum.
-// The logit space is overwritten in place: biased logits, then e, then f.
+//   Z_j = sum over the group's even i + sum over its odd i (each ascending),
+//   Z = ((Z_0 + Z_1) + Z_2) + Z_3;  p_i = e_i * (1/Z) (RN);
+//   f_i = 1 + floor(p_i * 65279);  R = 2^16 - sum f_i >= 0 ; f_255 += R ;
+//   c_i = exclusive prefix sum.
+// Integers are carried as exact integer-valued floats (< 2^24).  The logit
+// space is overwritten in place: biased logits, then e, then f.
 
 struct Q1Row {
-  uint32_t F[NGRP];  // per-group sums of the unadjusted f
-  uint32_t R;        // residual on symbol 255
+  float F[NGRP];  // per-group sums of the unadjusted f (exact integers)
+  float R;        // residual on symbol 255
 };
 
-// 1 + floor(p * 65279) for p in [0, 1.00002]: x + 2^23 rounded toward -inf has ulp 1.
-__device__ __forceinline__ uint32_t q1_freq(float p) {
-  const float x = __fmul_rn(p, Q1_SCALE);
-  return __float_as_uint(__fadd_rd(x, 8388608.0f)) - 0x4B000000u + 1u;
+__device__ __forceinline__ f2 f2_splat(float a) { return f2_make(a, a); }
+
+// 2^t for a pair, t <= ~0, on the FMA pipe (offloads MUFU, FA4-style):
+// n = floor(t) via a round-toward-minus-infinity add of 1.5*2^23, f = t - n in
+// [0,1), degree-5 fit of 2^f (max rel. error 1.8e-7, ~1.5 ulp, comparable to
+// ex2.approx), exponent inserted with an integer add.  Clamped at -126 so the
+// result stays normal (smaller values are < 2^-126 relative to the row max).
+__device__ __forceinline__ f2 f2_exp2_poly(f2 t) {
+  float t0, t1;
+  f2_split(t, t0, t1);
+  t = f2_make(fmaxf(t0, -126.0f), fmaxf(t1, -126.0f));
+  const f2 magic = f2_splat(12582912.0f);  // 1.5 * 2^23
+  const f2 j = f2_add_rm(t, magic);
+  const f2 n = f2_add(j, f2_splat(-12582912.0f));
+  float n0, n1;
+  f2_split(n, n0, n1);
+  const f2 f = f2_add(t, f2_make(-n0, -n1));
+  f2 p = f2_splat(0.0018951073288917542f);
+  p = f2_fma(p, f, f2_splat(0.00894621480256319f));
+  p = f2_fma(p, f, f2_splat(0.055863283574581146f));
+  p = f2_fma(p, f, f2_splat(0.24014076590538025f));
+  p = f2_fma(p, f, f2_splat(0.6931546330451965f));
+  p = f2_fma(p, f, f2_splat(0.9999998807907104f));
+  float j0, j1, p0, p1;
+  f2_split(j, j0, j1);
+  f2_split(p, p0, p1);
+  const uint32_t r0 = __float_as_uint(p0) + ((__float_as_uint(j0) - 0x4B400000u) << 23);
+  const uint32_t r1 = __float_as_uint(p1) + ((__float_as_uint(j1) - 0x4B400000u) << 23);
+  return f2_bits(r0, r1);
 }
 
-// Passes 1, 2, A.  `sym` (encoder, else -1): returns through fs/cs_local the
-// unadjusted f and group-local exclusive cum of sym if it lies in this group.
-// probs (nullable): p_i of this group's columns (debug export).
-template <class Eng>
-__device__ __forceinline__ Q1Row q1_table(const Eng& e, int sym, uint32_t& fs, uint32_t& cs_local,
-                                          float* probs) {
+// Passes 1, 2, A.  ENC: also returns f and the group-local exclusive cum of
+// `sym` when it lies in this group.  probs (nullable): p_i of this group's
+// columns (debug export).
+template <bool ENC, class Eng>
+__device__ __forceinline__ Q1Row q1_table(const Eng& e, int sym, float& fs, float& cs_local, float* probs,
+                                          Prof* pf = nullptr) {
   const int j = col_grp();
   const int c0 = 64 * j;
   // pass 1: biased logits, stored back; max
@@ -421,10 +505,9 @@ __device__ __forceinline__ Q1Row q1_table(const Eng& e, int sym, uint32_t& fs, u
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const float4 b = e.bias4_last(c0 + 32 * h + 4 * q);
-      const float l0 = __fadd_rn(__uint_as_float(v[4 * q + 0]), b.x);
-      const float l1 = __fadd_rn(__uint_as_float(v[4 * q + 1]), b.y);
-      const float l2 = __fadd_rn(__uint_as_float(v[4 * q + 2]), b.z);
-      const float l3 = __fadd_rn(__uint_as_float(v[4 * q + 3]), b.w);
+      float l0, l1, l2, l3;
+      f2_split(f2_add(f2_bits(v[4 * q + 0], v[4 * q + 1]), f2_make(b.x, b.y)), l0, l1);
+      f2_split(f2_add(f2_bits(v[4 * q + 2], v[4 * q + 3]), f2_make(b.z, b.w)), l2, l3);
       v[4 * q + 0] = __float_as_uint(l0);
       v[4 * q + 1] = __float_as_uint(l1);
       v[4 * q + 2] = __float_as_uint(l2);
@@ -433,63 +516,105 @@ __device__ __forceinline__ Q1Row q1_table(const Eng& e, int sym, uint32_t& fs, u
     }
     e.st32(c0 + 32 * h, v);
   }
+  if (pf) pf->mark(4);
   e.xput(0, __float_as_uint(m));
   e.xsync();
   uint32_t x4[4];
   e.xget4(0, x4);
+  if (pf) pf->mark(5);
   m = fmaxf(fmaxf(__uint_as_float(x4[0]), __uint_as_float(x4[1])),
             fmaxf(__uint_as_float(x4[2]), __uint_as_float(x4[3])));
-  const float nm = __fmul_rn(-m, LOG2E);
-  // pass 2: e_i stored back; Z_j in index order
-  float z = 0.0f;
+  const f2 nm = f2_splat(__fmul_rn(-m, LOG2E));
+  const f2 l2e = f2_splat(LOG2E);
+  // pass 2: e_i stored back; Z_j as even/odd partial sums
+  f2 zz = f2_splat(0.0f);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     uint32_t v[32];
     e.ld32(c0 + 32 * h, v);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float ei = ex2_approx(__fmaf_rn(__uint_as_float(v[i]), LOG2E, nm));
-      z = __fadd_rn(z, ei);
-      v[i] = __float_as_uint(ei);
+    for (int q = 0; q < 16; ++q) {
+      const f2 t = f2_fma(f2_bits(v[2 * q], v[2 * q + 1]), l2e, nm);
+      float e0, e1;
+      if (q % 8 >= 5) {  // 6 of 16 pairs on the FMA pipe, the rest on MUFU
+        f2_split(f2_exp2_poly(t), e0, e1);
+      } else {
+        float t0, t1;
+        f2_split(t, t0, t1);
+        e0 = ex2_approx(t0);
+        e1 = ex2_approx(t1);
+      }
+      zz = f2_add(zz, f2_make(e0, e1));
+      v[2 * q] = __float_as_uint(e0);
+      v[2 * q + 1] = __float_as_uint(e1);
     }
     e.st32(c0 + 32 * h, v);
   }
-  e.xput(1, __float_as_uint(z));
+  float za, zb;
+  f2_split(zz, za, zb);
+  if (pf) pf->mark(6);
+  e.xput(1, __float_as_uint(__fadd_rn(za, zb)));
   e.xsync();
   e.xget4(1, x4);
+  if (pf) pf->mark(5);
   const float Z = __fadd_rn(__fadd_rn(__fadd_rn(__uint_as_float(x4[0]), __uint_as_float(x4[1])),
                                       __uint_as_float(x4[2])),
                             __uint_as_float(x4[3]));
-  const float inv = __frcp_rn(Z);
-  // pass A: p_i, f_i (stored back as integers), group sum
-  uint32_t F = 0;
-  fs = 0;
-  cs_local = 0;
+  const f2 inv = f2_splat(__frcp_rn(Z));
+  const f2 scale = f2_splat(Q1_SCALE);
+  const f2 two23 = f2_splat(8388608.0f);
+  const f2 fbias = f2_splat(-8388607.0f);  // y - 2^23 + 1 = 1 + floor(x), exact
+  // pass A: p_i, f_i = 1 + floor(p_i * 65279) (x + 2^23 rounded toward -inf
+  // has ulp 1), stored back as floats; group sum
+  f2 FF = f2_splat(0.0f);
+  fs = 0.0f;
+  cs_local = 0.0f;
+  float cum = 0.0f;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     uint32_t v[32];
     e.ld32(c0 + 32 * h, v);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float p = __fmul_rn(__uint_as_float(v[i]), inv);
-      const uint32_t f = q1_freq(p);
-      if (c0 + 32 * h + i == sym) {
-        fs = f;
-        cs_local = F;
+    for (int q = 0; q < 16; ++q) {
+      const f2 p = f2_mul(f2_bits(v[2 * q], v[2 * q + 1]), inv);
+      const f2 f = f2_add(f2_add_rm(f2_mul(p, scale), two23), fbias);
+      FF = f2_add(FF, f);
+      float f0, f1;
+      f2_split(f, f0, f1);
+      if (ENC) {
+        const int i0 = c0 + 32 * h + 2 * q;
+        if (i0 == sym) {
+          fs = f0;
+          cs_local = cum;
+        }
+        if (i0 + 1 == sym) {
+          fs = f1;
+          cs_local = __fadd_rn(cum, f0);
+        }
+        cum = __fadd_rn(cum, __fadd_rn(f0, f1));
       }
-      if (probs) probs[c0 + 32 * h + i] = p;
-      F += f;
-      v[i] = f;
+      if (probs) {
+        float p0, p1;
+        f2_split(p, p0, p1);
+        probs[c0 + 32 * h + 2 * q] = p0;
+        probs[c0 + 32 * h + 2 * q + 1] = p1;
+      }
+      v[2 * q] = __float_as_uint(f0);
+      v[2 * q + 1] = __float_as_uint(f1);
     }
     e.st32(c0 + 32 * h, v);
   }
-  e.xput(2, F);
+  float Fa, Fb;
+  f2_split(FF, Fa, Fb);
+  if (pf) pf->mark(7);
+  e.xput(2, __float_as_uint(__fadd_rn(Fa, Fb)));
   e.xsync();
   e.xget4(2, x4);
+  if (pf) pf->mark(5);
   Q1Row r;
 #pragma unroll
-  for (int g = 0; g < NGRP; ++g) r.F[g] = x4[g];
-  r.R = 65536u - (x4[0] + x4[1] + x4[2] + x4[3]);
+  for (int g = 0; g < NGRP; ++g) r.F[g] = __uint_as_float(x4[g]);
+  r.R = 65536.0f - (((r.F[0] + r.F[1]) + r.F[2]) + r.F[3]);
   return r;
 }
 
@@ -504,7 +629,7 @@ __device__ __forceinline__ void q1_store_freqs(const Eng& e, const Q1Row& r, uin
     if (freqs) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        uint32_t f = v[i];
+        float f = __uint_as_float(v[i]);
         if (j == NGRP - 1 && h == 1 && i == 31) f += r.R;
         freqs[64 * j + 32 * h + i] = (uint16_t)f;
       }
@@ -517,16 +642,16 @@ __device__ __forceinline__ void q1_store_freqs(const Eng& e, const Q1Row& r, uin
 template <class Eng>
 __device__ __forceinline__ uint32_t q1_encode(const Eng& e, int sym, float* probs = nullptr,
                                               uint16_t* freqs = nullptr, bool export_freqs = false) {
-  uint32_t fs, csl;
-  const Q1Row r = q1_table(e, sym, fs, csl, probs);
+  float fs, csl;
+  const Q1Row r = q1_table<true>(e, sym, fs, csl, probs);
   if (export_freqs) q1_store_freqs(e, r, freqs);
   const int j = col_grp();
   uint32_t packed = 0;
   if ((sym >> 6) == j) {
-    uint32_t base = 0;
+    float base = 0.0f;
     for (int g = 0; g < j; ++g) base += r.F[g];
     if (sym == NOUT - 1) fs += r.R;
-    packed = fs | ((base + csl) << 16);
+    packed = (uint32_t)fs | ((uint32_t)(base + csl) << 16);
   }
   e.xput(3, packed);
   e.xsync();
@@ -536,50 +661,54 @@ __device__ __forceinline__ uint32_t q1_encode(const Eng& e, int sym, float* prob
 }
 
 // Decoder: symbol s with c_s <= slot < c_s + f_s (all threads of the row).
-// Only the group whose range holds the slot finds it; the search is
-// predicated (every lane executes the same TMEM loads).
 // `slot` is read from group 0 (the rANS lane owner), published through
 // exchange slot 6 and picked up after q1_table's first exchange barrier.
+// Search: reverse scan of the group's 64 entries with the monotone test
+// slot < c_{i+1}; the last hit is the smallest such i = s.  Every lane
+// executes the same TMEM loads (tcgen05.ld is .sync.aligned).
 template <class Eng>
-__device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot0, uint32_t& fs_out, uint32_t& cs_out) {
-  uint32_t fs, csl;
+__device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot0, uint32_t& fs_out, uint32_t& cs_out,
+                                         Prof* pf = nullptr) {
+  float fs, csl;
   e.xput(6, slot0);
-  const Q1Row r = q1_table(e, -1, fs, csl, nullptr);
+  const Q1Row r = q1_table<false>(e, -1, fs, csl, nullptr, pf);
   uint32_t s4[4];
   e.xget4(6, s4);
-  const uint32_t slot = s4[0];
+  const float slot = (float)s4[0];
   const int j = col_grp();
-  uint32_t base = 0;
+  float base = 0.0f;
 #pragma unroll
   for (int g = 0; g < NGRP; ++g)
     if (g < j) base += r.F[g];
-  const uint32_t top = base + r.F[j] + (j == NGRP - 1 ? r.R : 0u);
-  const bool mine = slot >= base && slot < top;
-  uint32_t cum = base;
+  float cum = base + r.F[j] + (j == NGRP - 1 ? r.R : 0.0f);  // c_64 of this group
+  const bool mine = slot >= base && slot < cum;
   int sym = 0;
-  uint32_t fsel = 0, csel = 0;
+  float fsel = 0.0f, csel = 0.0f;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 1; h >= 0; --h) {
     uint32_t v[32];
     e.ld32(64 * j + 32 * h, v);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      uint32_t f = v[i];
+    for (int i = 31; i >= 0; --i) {
+      float f = __uint_as_float(v[i]);
       if (j == NGRP - 1 && h == 1 && i == 31) f += r.R;
-      if (slot - cum < f) {  // cum <= slot < cum + f
+      const float lo = cum - f;  // exact
+      if (slot < cum) {
         sym = 64 * j + 32 * h + i;
         fsel = f;
-        csel = cum;
+        csel = lo;
       }
-      cum += f;
+      cum = lo;
     }
   }
-  e.xput(4, mine ? ((uint32_t)sym | (fsel << 8)) : 0xFFFFFFFFu);
-  e.xput(5, csel);
+  if (pf) pf->mark(8);
+  e.xput(4, mine ? ((uint32_t)sym | ((uint32_t)fsel << 8)) : 0xFFFFFFFFu);
+  e.xput(5, (uint32_t)csel);
   e.xsync();
   uint32_t k4[4], c4[4];
   e.xget4(4, k4);
   e.xget4(5, c4);
+  if (pf) pf->mark(5);
   int g = 0;
 #pragma unroll
   for (int q = 0; q < NGRP; ++q)

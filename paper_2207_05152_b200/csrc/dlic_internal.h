@@ -84,7 +84,7 @@ cudaError_t launch_dec_prep(const Plan& p, const uint8_t* d_bits, const uint64_t
                             int32_t* d_status, cudaStream_t st);
 cudaError_t launch_decode(const Plan& p, const DevWeights& w, const uint8_t* d_bits, const uint64_t* d_cont_off,
                           const uint32_t* d_sbase, const uint32_t* d_slen, uint8_t* d_imgs, int32_t* d_status,
-                          cudaStream_t st);
+                          cudaStream_t st, unsigned long long* prof = nullptr);
 
 cudaError_t launch_rans_dec_tables(const Plan& p, const uint8_t* d_bits, const uint32_t* d_sbase,
                                    const uint32_t* d_slen, const uint16_t* d_tables, uint8_t* d_out,

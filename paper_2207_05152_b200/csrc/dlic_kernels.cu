@@ -25,8 +25,12 @@ namespace dlic {
 __device__ __forceinline__ int off_dr(int j) { return j < 72 ? j / 9 - 8 : 0; }
 __device__ __forceinline__ int off_dc(int j) { return j < 72 ? j % 9 - 6 : j - 78; }
 
+// Decoded-pixel ring, column-major so the 32 lanes of a warp (consecutive
+// rows) touch distinct shared-memory banks: byte (bank, col, ringrow) at
+// (bank*32 + col)*RING_ROWS + ringrow; ringrow = 8 + slot-in-CTA, rows 0..7
+// mirror the previous CTA's last 8 slots (halo).
 constexpr int RING_ROWS = ROWS + 8;                  // own 128 slots + 8 halo rows
-constexpr uint32_t RING_BYTES = 2u * RING_ROWS * 32u;  // 2 banks x 136 rows x 32 cols
+constexpr uint32_t RING_BYTES = 2u * RING_ROWS * 32u;  // 2 banks x 32 cols x 136 rows
 constexpr uint32_t F32_BUF_BYTES = (NOUT + HID) * ROWS * 4u;          // 196608
 constexpr uint32_t F32_X_BYTES = NXSLOT * NGRP * ROWS * 4u;          // 12288
 constexpr uint32_t MAX_DYN_SMEM = 232448 - 64;                       // 227 KB minus static
@@ -36,7 +40,7 @@ size_t enc_smem_bytes(uint32_t precision) {
 }
 static uint32_t cursor_bytes(uint32_t ngroups) { return (ngroups * 4u + 15u) & ~15u; }
 size_t dec_smem_bytes(uint32_t precision, uint32_t max_groups) {
-  return enc_smem_bytes(precision) + RING_BYTES + cursor_bytes(max_groups);
+  return enc_smem_bytes(precision) + RING_BYTES + 16 + cursor_bytes(max_groups);
 }
 size_t dec_smem_limit() { return MAX_DYN_SMEM; }
 
@@ -100,25 +104,39 @@ __device__ __forceinline__ void engine_teardown(typename EngineSel<PREC>::T& eng
 
 // Feed this thread's share of the 78 (80) window inputs: group j owns inputs
 // [20j, 20j+20); get(k) returns the pixel value of window offset k (0 fill).
-template <int PREC, class Eng, class Get>
-__device__ __forceinline__ void feed(const Eng& eng, Get get) {
-  const int j = col_grp();
+// J is a compile-time constant so every window offset folds to an immediate.
+template <int PREC, int J, class Eng, class Get>
+__device__ __forceinline__ void feed_j(const Eng& eng, Get& get) {
   if constexpr (PREC == 1) {
+    // v/256 exactly: (1 + v/256) has v in the top 8 mantissa bits; minus 1 is exact.
+    const f2 m1 = f2_make(-1.0f, -1.0f);
     uint32_t a[10];
 #pragma unroll
     for (int i = 0; i < 10; ++i) {
-      const int k0 = 20 * j + 2 * i;
-      const float x0 = k0 < KIN ? (float)get(k0) * 0.00390625f : 0.0f;   // v / 256, exact (R2)
-      const float x1 = k0 + 1 < KIN ? (float)get(k0 + 1) * 0.00390625f : 0.0f;
+      constexpr int base = 20 * J;
+      const int k0 = base + 2 * i;
+      const uint32_t v0 = k0 < KIN ? get(k0) : 0u;
+      const uint32_t v1 = k0 + 1 < KIN ? get(k0 + 1) : 0u;
+      float x0, x1;
+      f2_split(f2_add(f2_bits(0x3F800000u | (v0 << 15), 0x3F800000u | (v1 << 15)), m1), x0, x1);
       a[i] = pack_bf16(x0, x1);
     }
     eng.put_input(a);
   } else {
 #pragma unroll
     for (int i = 0; i < 20; ++i) {
-      const int k = 20 * j + i;
-      if (k < KIN) eng.put_input(k, (float)get(k) * 0.00390625f);
+      const int k = 20 * J + i;
+      if (k < KIN) eng.put_input(k, __fadd_rn(__uint_as_float(0x3F800000u | (get(k) << 15)), -1.0f));
     }
+  }
+}
+template <int PREC, class Eng, class Get>
+__device__ __forceinline__ void feed(const Eng& eng, Get get) {
+  switch (col_grp()) {  // warp-uniform
+    case 0: feed_j<PREC, 0>(eng, get); break;
+    case 1: feed_j<PREC, 1>(eng, get); break;
+    case 2: feed_j<PREC, 2>(eng, get); break;
+    default: feed_j<PREC, 3>(eng, get); break;
   }
 }
 
@@ -148,9 +166,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int r = valid ? (int)(q / un.w) : 0, c = valid ? (int)(q % un.w) : 0;
     const uint8_t* img = imgs + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
     const int uw = (int)un.w;
-    auto get = [&](int kk) -> uint32_t {
+    auto get = [&](int kk) -> uint32_t {  // branch-free: invalid taps load the target and mask
       const int rr = r + off_dr(kk), cc = c + off_dc(kk);
-      return (valid && rr >= 0 && cc >= 0 && cc < uw) ? (uint32_t)__ldg(img + (uint64_t)rr * p.W + cc) : 0u;
+      const bool ok = valid && rr >= 0 && (unsigned)cc < (unsigned)uw;
+      const uint32_t v = __ldg(img + (ok ? (int64_t)rr * p.W + cc : (int64_t)r * p.W + c));
+      return ok ? v : 0u;
     };
     feed<PREC>(eng, get);
     eng.run();
@@ -413,13 +433,18 @@ template <int PREC>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_decode(Plan p, DevWeights w, const uint8_t* __restrict__ bits, const uint64_t* __restrict__ cont_off,
              const uint32_t* __restrict__ sbase, const uint32_t* __restrict__ slen, uint8_t* __restrict__ out,
-             int32_t* __restrict__ status) {
+             int32_t* __restrict__ status, unsigned long long* __restrict__ prof) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
   const int row = tile_row(), j = col_grp();
   const uint32_t lane = lane_id();
   const uint32_t NC = p.nc, NS = ROWS * NC;
+  // optional phase profile (thread 0 of each CTA), see Prof in dlic_device.cuh:
+  // 0 top 1 gather 2 put 3 mlp 4 pass1 5 exchanges 6 pass2 7 passA 8 search 9 rans 10 barrier
+  Prof pf;
+  pf.on = prof != nullptr && threadIdx.x == 0;
+#define DLIC_PROF_MARK(k) pf.mark(k);
   const uint32_t ns_shift = 7u + (NC == 1 ? 0u : NC == 2 ? 1u : NC == 4 ? 2u : 3u);
   const uint32_t rank = NC > 1 ? cluster_rank() : 0u;
   const uint32_t u = blockIdx.x / NC;
@@ -428,8 +453,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   typename EngineSel<PREC>::T eng;
   uint8_t* ring = engine_setup<PREC>(eng, smem, w, &bar, &tslot);
-  uint32_t* cursor = reinterpret_cast<uint32_t*>(ring + RING_BYTES);
+  uint32_t* cursor = reinterpret_cast<uint32_t*>(ring + RING_BYTES + 16);  // 16 zero bytes after the ring
+  if (threadIdx.x < 16) ring[RING_BYTES + threadIdx.x] = 0;
   const uint32_t G = p.G;
+  const uint32_t g_shift = (uint32_t)(__ffs((int)G) - 1);
   for (uint32_t g = threadIdx.x; g < un.ngroups; g += NTHREADS) {
     if ((((G * g) & (NS - 1)) >> 7) == rank) cursor[g] = 2u * min(G, un.h - G * g);
   }
@@ -445,6 +472,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint32_t x = 0;
   int err = 0;
 
+  if (pf.on) pf.t = clock64();
 #pragma unroll 1
   for (int t = 0; t < T; ++t) {
     const int rlo = t - uw + 1 > 0 ? (t - uw + 3) / 3 : 0;
@@ -456,30 +484,39 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       active = r <= rhi;
       c = t - 3 * r;
     }
-    if (__syncthreads_or(active)) {
-      const uint32_t g = active ? (uint32_t)r / G : 0u;
-      const uint32_t sidx = un.first_stream + g;
-      const uint16_t* sw = reinterpret_cast<const uint16_t*>(cbase + (active ? sbase[sidx] : 0u));
-      const uint32_t sl = active ? slen[sidx] : 0u;
+    const bool any = __syncthreads_or(active);
+    DLIC_PROF_MARK(0)
+    if (any) {
+      const uint32_t g = (uint32_t)r >> g_shift;  // G is a power of two dividing 32
       if (j == 0 && active && c == 0) {  // the row's lane starts: flushed state (hi, lo)
+        const uint32_t sidx = un.first_stream + g;
+        const uint16_t* sw = reinterpret_cast<const uint16_t*>(cbase + sbase[sidx]);
         const uint32_t i = 2u * ((uint32_t)r - G * g);
-        if (i + 1 < sl) x = ((uint32_t)sw[i] << 16) | (uint32_t)sw[i + 1];
+        if (i + 1 < slen[sidx]) x = ((uint32_t)sw[i] << 16) | (uint32_t)sw[i + 1];
         else err = 8;
       }
       // window gather from the ring (rows r-8..r of this slot's neighbourhood)
-      auto get = [&](int kk) -> uint32_t {
+      auto get = [&](int kk) -> uint32_t {  // branch-free: invalid taps read a zero byte
         const int d = -off_dr(kk);
         const int rr = r - d, cc = c + off_dc(kk);
-        if (!active || rr < 0 || cc < 0 || cc >= uw) return 0u;
+        const bool ok = active && rr >= 0 && (unsigned)cc < (unsigned)uw;
         const uint32_t bank = ((uint32_t)rr >> ns_shift) & 1u;
-        return ring[(bank * RING_ROWS + (uint32_t)(row - d + 8)) * 32u + ((uint32_t)cc & 31u)];
+        const uint32_t a = (bank * 32u + ((uint32_t)cc & 31u)) * RING_ROWS + (uint32_t)(row - d + 8);
+        return ring[ok ? a : RING_BYTES];
       };
       feed<PREC>(eng, get);
+      DLIC_PROF_MARK(1)
+      if constexpr (PREC == 1) tc_wait_st();
+      DLIC_PROF_MARK(2)
       eng.run();
+      DLIC_PROF_MARK(3)
       const uint32_t slot = x & 0xFFFFu;
       uint32_t fs, cs;
-      const int sym = q1_decode(eng, slot, fs, cs);
+      const int sym = q1_decode(eng, slot, fs, cs, &pf);
       if (j == 0) {
+        const uint32_t sidx = un.first_stream + g;
+        const uint16_t* sw = reinterpret_cast<const uint16_t*>(cbase + (active ? sbase[sidx] : 0u));
+        const uint32_t sl = active ? slen[sidx] : 0u;
         bool need = false;
         if (active) {
           x = fs * (x >> 16) + slot - cs;
@@ -501,19 +538,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           oimg[(uint64_t)r * p.W + c] = (uint8_t)sym;
           const uint32_t bank = ((uint32_t)r >> ns_shift) & 1u;
           const uint32_t col = (uint32_t)c & 31u;
-          ring[(bank * RING_ROWS + (uint32_t)row + 8u) * 32u + col] = (uint8_t)sym;
+          ring[(bank * 32u + col) * RING_ROWS + (uint32_t)row + 8u] = (uint8_t)sym;
           if (row >= ROWS - 8) {
-            const uint32_t hoff = (bank * RING_ROWS + (uint32_t)(row - (ROWS - 8))) * 32u + col;
+            const uint32_t hoff = (bank * 32u + col) * RING_ROWS + (uint32_t)(row - (ROWS - 8));
             if (NC > 1) st_cluster_u8(halo_base + hoff, (uint32_t)sym);
             else ring[hoff] = (uint8_t)sym;
           }
           if (c == uw - 1 && x != RANS_L) err = 6;  // end-of-lane invariant
         }
       }
+      DLIC_PROF_MARK(9)
     }
     if (NC > 1) cluster_sync_all();
     else __syncthreads();
+    DLIC_PROF_MARK(10)
   }
+  if (pf.on)
+    for (int k = 0; k < 11; ++k) atomicAdd(prof + k, pf.acc[k]);
+#undef DLIC_PROF_MARK
   for (uint32_t g = threadIdx.x; g < un.ngroups; g += NTHREADS) {
     if ((((G * g) & (NS - 1)) >> 7) == rank && cursor[g] != slen[un.first_stream + g]) err = 6;
   }
@@ -573,7 +615,8 @@ cudaError_t launch_dec_prep(const Plan& p, const uint8_t* d_bits, const uint64_t
 template <int PREC>
 static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uint8_t* d_bits,
                                    const uint64_t* d_cont_off, const uint32_t* d_sbase, const uint32_t* d_slen,
-                                   uint8_t* d_imgs, int32_t* d_status, cudaStream_t st) {
+                                   uint8_t* d_imgs, int32_t* d_status, cudaStream_t st,
+                                   unsigned long long* prof) {
   const size_t sm = dec_smem_bytes(PREC, p.gpt > p.gpl ? p.gpt : p.gpl);
   cudaError_t e = set_smem(k_decode<PREC>, sm);
   if (e != cudaSuccess) return e;
@@ -589,14 +632,16 @@ static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uin
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_decode<PREC>, p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status);
+  return cudaLaunchKernelEx(&cfg, k_decode<PREC>, p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status,
+                            prof);
 }
 
 cudaError_t launch_decode(const Plan& p, const DevWeights& w, const uint8_t* d_bits, const uint64_t* d_cont_off,
                           const uint32_t* d_sbase, const uint32_t* d_slen, uint8_t* d_imgs, int32_t* d_status,
-                          cudaStream_t st) {
-  if (p.precision == 1) return launch_decode_t<1>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st);
-  return launch_decode_t<0>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st);
+                          cudaStream_t st, unsigned long long* prof) {
+  if (p.precision == 1)
+    return launch_decode_t<1>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof);
+  return launch_decode_t<0>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof);
 }
 
 }  // namespace dlic
