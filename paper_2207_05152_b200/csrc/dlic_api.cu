@@ -285,9 +285,14 @@ dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Pl
     return fail(DLIC_E_INVALID_ARG, "too many row groups per unit for the decoder's shared memory: raise group_rows or tile");
   p.cap_words = 2 * p.G + p.G * p.tw;
   p.hdr_bytes = 58 + 4 * p.spi;
-  p.tiles_per_unit = (uint32_t)(((uint64_t)p.tw * p.th + 127) / 128);
+  p.tiles_per_unit = (uint32_t)(((uint64_t)p.tw * p.th + ROWS - 1) / ROWS);
   const uint32_t slots = (p.tw + 2) / 3;  // max rows on one front = ceil(tw/3)
-  p.nc = slots <= 128 ? 1 : slots <= 256 ? 2 : slots <= 512 ? 4 : slots <= 1024 ? 8 : 0;
+  p.nc = 0;
+  for (uint32_t nc = 1; nc <= 16; nc *= 2)
+    if (slots <= ROWS * nc) {
+      p.nc = nc;
+      break;
+    }
   if (p.nc == 0) return fail(DLIC_E_INVALID_ARG, "unit wider than 3072 px: use tiles (tile_w <= 3072)");
   uint64_t mc = p.hdr_bytes;
   mc += (uint64_t)p.spi * (4ull * p.G + 2ull * p.G * p.tw);

@@ -3,12 +3,14 @@
 // * PTX wrappers for tcgen05 (MMA with A in TMEM, TMEM ld/st/alloc), mbarrier
 //   and thread-block-cluster (DSMEM) operations, sm_100a only.
 // * Thread organisation shared by the encoder and the decoder: 512 threads =
-//   16 warps per CTA; threadIdx = 128*j + row.  `row` (0..127) is the pixel
-//   row of the M=128 tile = the TMEM lane, so warp w serves lane quadrant w&3
-//   (the tcgen05.ld/st rule) and column group j = w>>2 of every row.  Each
-//   row's network evaluation is split over its 4 column groups; the groups
-//   combine partial results through spare TMEM columns (TcEngine) or shared
-//   memory (Fp32Engine).
+//   16 warps per CTA and 64 pixel rows = an M=64 tcgen05 tile, whose rows sit
+//   in the half-subpartition TMEM layout (row m -> lane (m%16) + 32*(m/16)).
+//   Warp w serves lane quadrant q = w&3 (rows 16q..16q+15) and column group
+//   j = w>>2; its two half-warps h (lanes 0-15 / 16-31) address the same 16
+//   rows at two column offsets (tcgen05 .16x32bx2 shape).  Each row is thus
+//   served by 8 threads (4 groups x 2 halves), each owning a contiguous column
+//   range; per-row partials combine with one shuffle (xor 16) and an exchange
+//   through spare TMEM columns (TcEngine) or shared memory (Fp32Engine).
 // * The two density-estimator engines (P:96 dense network, reading R4):
 //     TcEngine   bf16 operands on 5th-gen tensor cores; weights resident in
 //                shared memory in the UMMA no-swizzle K-major core-matrix
@@ -31,9 +33,9 @@ constexpr int KPAD = 80;       // layer-1 K padded to a multiple of 16 for kind:
 constexpr int HID = 128;       // P100K hidden width (R4)
 constexpr int NOUT = 256;      // 8-bit alphabet
 constexpr int NLAYER = 6;      // "six dense layers"
-constexpr int ROWS = 128;      // rows per CTA = TMEM lanes
-constexpr int NGRP = 4;        // column groups per row
-constexpr int NTHREADS = ROWS * NGRP;
+constexpr int ROWS = 64;       // pixel rows per CTA = M of the tcgen05 tile
+constexpr int NGRP = 4;        // column groups per row (4 warps each)
+constexpr int NTHREADS = 512;
 constexpr uint32_t RANS_L = 1u << 16;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float Q1_SCALE = 65279.0f;  // 2^16 - 257 (R5, Q1')
@@ -60,7 +62,8 @@ __host__ __device__ constexpr uint32_t f32_off(int l) {
 // TMEM column map (one 512-column allocation per CTA)
 constexpr uint32_t TM_D = 0;     // accumulator / logits / e / f, 256 columns
 constexpr uint32_t TM_A = 256;   // A operand, K/2 columns (bf16 pairs), up to 64
-constexpr uint32_t TM_X = 320;   // exchange slots: 4 columns (one per group) per slot
+constexpr uint32_t TM_X = 320;   // exchange slot s: columns TM_X+4s+j (lower half-warp)
+constexpr uint32_t TM_XUP = 32;  //   and TM_X+32+4s+j (upper half-warp copy)
 constexpr uint32_t TM_COLS = 512;
 constexpr int NXSLOT = 7;  // 0 max, 1 Z, 2 F, 3 fc, 4/5 search result, 6 slot
 
@@ -69,8 +72,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
-__device__ __forceinline__ int tile_row() { return threadIdx.x & (ROWS - 1); }
+__device__ __forceinline__ int quad() { return (threadIdx.x >> 5) & 3; }
 __device__ __forceinline__ int col_grp() { return threadIdx.x >> 7; }
+__device__ __forceinline__ int half_id() { return (threadIdx.x >> 4) & 1; }
+__device__ __forceinline__ int tile_row() { return 16 * quad() + (threadIdx.x & 15); }
 
 // named barrier over the 4 warps that share one TMEM lane quadrant
 __device__ __forceinline__ void quad_sync() {
@@ -188,6 +193,53 @@ __device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
 }
 
+// .16x32bx2: lanes 0-15 of the warp address TMEM lanes base..base+15 at
+// column taddr, lanes 16-31 the same TMEM lanes at column taddr + OFF;
+// .xN = N consecutive columns per thread.
+template <int OFF>
+__device__ __forceinline__ void tmem_ld32h(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x32bx2.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32], %33;"
+      : DLIC_R8(0), DLIC_R8(8), DLIC_R8(16), DLIC_R8(24)
+      : "r"(taddr), "n"(OFF));
+}
+template <int OFF>
+__device__ __forceinline__ void tmem_ld16h(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x32bx2.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16], %17;"
+      : DLIC_R8(0), DLIC_R8(8)
+      : "r"(taddr), "n"(OFF));
+}
+template <int OFF>
+__device__ __forceinline__ void tmem_ld4h(uint32_t taddr, uint32_t (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x4.b32 {%0,%1,%2,%3}, [%4], %5;" : DLIC_R4(0) : "r"(taddr), "n"(OFF));
+}
+template <int OFF>
+__device__ __forceinline__ void tmem_st32h(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x32bx2.x32.b32 [%0], %1, {%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33};" ::"r"(taddr),
+      "n"(OFF), DLIC_W8(0), DLIC_W8(8), DLIC_W8(16), DLIC_W8(24)
+      : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void tmem_st8h(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.16x32bx2.x8.b32 [%0], %1, {%2,%3,%4,%5,%6,%7,%8,%9};" ::"r"(taddr), "n"(OFF),
+               DLIC_W8(0)
+               : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void tmem_st4h(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.16x32bx2.x4.b32 [%0], %1, {%2,%3,%4,%5};" ::"r"(taddr), "n"(OFF),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void tmem_st1h(uint32_t taddr, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.16x32bx2.x1.b32 [%0], %1, {%2};" ::"r"(taddr), "n"(OFF), "r"(v) : "memory");
+}
+
 // ---- clusters / DSMEM
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -270,11 +322,11 @@ struct Prof {
 };
 
 // ---------------------------------------------------------------- engines
-// Common engine interface (per thread = (row, group j)):
-//   ld32(col, v) / st32(col, v)   32 columns [col, col+32) of this row's
-//                                 logit/work space (256 columns), raw bits
-//   bias_last(col)                final-layer bias (added once in pass 1)
+// Common engine interface (per thread = one row, group j, half h):
+//   ld32(v) / st32(v)   this thread's 32 logit/work columns [64j+32h, +32)
+//   bias_pair(i)        final-layer bias of its columns 2i, 2i+1 (added once)
 //   xput(slot, v); xsync(); xget4(slot, v4)   exchange one word per group
+//                        (v must already be equal in both half-warps)
 
 struct TcEngine {
   uint32_t tmem;       // TMEM base (lane 0, column base)
@@ -285,17 +337,18 @@ struct TcEngine {
 
   __device__ __forceinline__ uint32_t lane_off() const { return ((threadIdx.x >> 5) & 3u) << 21; }
 
-  // Layer-1 input: this thread's 10 packed bf16 pairs = inputs [20j, 20j+20).
-  __device__ __forceinline__ void put_input(const uint32_t (&a)[10]) const {
+  // Layer-1 input: this thread's 5 packed bf16 pairs = inputs [20j+10h, +10)
+  // (A packed columns [10j+5h, +5)).
+  __device__ __forceinline__ void put_input(const uint32_t (&a)[5]) const {
     const uint32_t base = tmem + lane_off() + TM_A + 10u * (uint32_t)col_grp();
-    tmem_st8(base, a);
-    tmem_st2(base + 8, a + 8);
+    tmem_st4h<5>(base, a);
+    tmem_st1h<5>(base + 4, a[4]);
   }
 
-  // Runs the 6 layers; the input must have been stored with put_input.
+  // Runs the 6 layers (M=64); the input must have been stored with put_input.
   __device__ void run() {
     const uint32_t lo = lane_off();
-    const int j = col_grp();
+    const int j = col_grp(), h = half_id();
     tc_wait_st();
 #pragma unroll 1
     for (int l = 0; l < NLAYER; ++l) {
@@ -304,7 +357,7 @@ struct TcEngine {
       if (threadIdx.x == 0) {
         tc_fence_after();
         const int K = layer_k(l), N = layer_n(l);
-        const uint32_t id = umma_idesc(128, N);
+        const uint32_t id = umma_idesc(64, N);
         const uint32_t lbo = (uint32_t)N * 16u;                 // next 8-wide K core matrix
         const uint32_t kstep = 2u * (uint32_t)(N / 8) * 128u;   // one K=16 slice
         // start-address field (bits 0-13, 16-byte units) advances by kstep/16
@@ -321,39 +374,38 @@ struct TcEngine {
       mbar_wait(bar, phase);
       phase ^= 1u;
       tc_fence_after();
-      if (l < NLAYER - 1) {  // bias + ReLU + bf16 -> next A; this group: columns [32j, 32j+32)
-        const float4* b4 = reinterpret_cast<const float4*>(bias + l * HID + 32 * j);
-        uint32_t v[32];
-        tmem_ld32(tmem + lo + TM_D + 32u * (uint32_t)j, v);
+      if (l < NLAYER - 1) {  // bias + ReLU + bf16 -> next A; columns [32j+16h, +16)
+        const float2* b2 = reinterpret_cast<const float2*>(bias + l * HID + 32 * j + 16 * h);
+        uint32_t v[16];
+        tmem_ld16h<16>(tmem + lo + TM_D + 32u * (uint32_t)j, v);
         tc_wait_ld();
-        uint32_t p[16];
+        uint32_t p[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const float4 b = b4[q];
-          float x0, x1, x2, x3;
-          f2_split(f2_add(f2_bits(v[4 * q + 0], v[4 * q + 1]), f2_make(b.x, b.y)), x0, x1);
-          f2_split(f2_add(f2_bits(v[4 * q + 2], v[4 * q + 3]), f2_make(b.z, b.w)), x2, x3);
-          p[2 * q] = pack_bf16_relu(x0, x1);  // relu(x) rounded to bf16 (RN)
-          p[2 * q + 1] = pack_bf16_relu(x2, x3);
+          const float2 b = b2[q];
+          float x0, x1;
+          f2_split(f2_add(f2_bits(v[2 * q], v[2 * q + 1]), f2_make(b.x, b.y)), x0, x1);
+          p[q] = pack_bf16_relu(x0, x1);  // relu(x) rounded to bf16 (RN)
         }
-        tmem_st16(tmem + lo + TM_A + 16u * (uint32_t)j, p);
+        // packed column 16j+8h+q holds activations 32j+16h+2q, +1: identity K order
+        tmem_st8h<8>(tmem + lo + TM_A + 16u * (uint32_t)j, p);
         tc_wait_st();
       }
     }
   }
 
-  __device__ __forceinline__ void ld32(int col, uint32_t (&v)[32]) const {
-    tmem_ld32(tmem + lane_off() + TM_D + (uint32_t)col, v);
+  __device__ __forceinline__ void ld32(uint32_t (&v)[32]) const {
+    tmem_ld32h<32>(tmem + lane_off() + TM_D + 64u * (uint32_t)col_grp(), v);
     tc_wait_ld();
   }
-  __device__ __forceinline__ void st32(int col, const uint32_t (&v)[32]) const {
-    tmem_st32(tmem + lane_off() + TM_D + (uint32_t)col, v);
+  __device__ __forceinline__ void st32(const uint32_t (&v)[32]) const {
+    tmem_st32h<32>(tmem + lane_off() + TM_D + 64u * (uint32_t)col_grp(), v);
   }
-  __device__ __forceinline__ float4 bias4_last(int col) const {
-    return *reinterpret_cast<const float4*>(bias + BIAS_OFF_LAST + col);
+  __device__ __forceinline__ float2 bias_pair(int i) const {
+    return reinterpret_cast<const float2*>(bias + BIAS_OFF_LAST + 64 * col_grp() + 32 * half_id())[i];
   }
   __device__ __forceinline__ void xput(int slot, uint32_t v) const {
-    tmem_st1(tmem + lane_off() + TM_X + 4u * (uint32_t)slot + (uint32_t)col_grp(), v);
+    tmem_st1h<TM_XUP>(tmem + lane_off() + TM_X + 4u * (uint32_t)slot + (uint32_t)col_grp(), v);
   }
   __device__ __forceinline__ void xsync() const {
     tc_wait_st();
@@ -362,15 +414,15 @@ struct TcEngine {
     tc_fence_after();
   }
   __device__ __forceinline__ void xget4(int slot, uint32_t (&v)[4]) const {
-    tmem_ld4(tmem + lane_off() + TM_X + 4u * (uint32_t)slot, v);
+    tmem_ld4h<TM_XUP>(tmem + lane_off() + TM_X + 4u * (uint32_t)slot, v);
     tc_wait_ld();
   }
 };
 
-// CUDA-core fp32 engine.  Shared buffers, column = row of the tile:
+// CUDA-core fp32 engine.  Shared buffers, column index = tile row (64):
 //   buf0: [256][ROWS] floats (input features / hidden / logits), buf1: [128][ROWS],
-//   xbuf: [NXSLOT][NGRP][ROWS] words.  Group j computes outputs
-//   [N/4*j, N/4*(j+1)) of every layer for its row, k ascending.
+//   xbuf: [NXSLOT][NGRP][ROWS] words.  Thread (row, j, h) computes outputs
+//   [N/4*j + N/8*h, +N/8) of every layer for its row, k ascending.
 struct Fp32Engine {
   float* buf0;
   float* buf1;
@@ -380,27 +432,27 @@ struct Fp32Engine {
   __device__ __forceinline__ void put_input(int k, float x) const { buf0[k * ROWS + tile_row()] = x; }
 
   __device__ void run() {
-    const int t = tile_row(), j = col_grp();
+    const int t = tile_row(), j = col_grp(), h = half_id();
 #pragma unroll 1
     for (int l = 0; l < NLAYER; ++l) {
-      quad_sync();  // inputs of this layer (written by the row's 4 groups) are complete
+      quad_sync();  // this layer's inputs (written by the row's 8 threads) are complete
       const float* in = (l & 1) ? buf1 : buf0;
       float* out = (l & 1) ? buf0 : buf1;
       const int K = f32_k(l), N = layer_n(l);
       const float* W = w + f32_off(l);
       const float* B = W + K * N;
-      const int nq = N / NGRP;
+      const int n8 = N / 8;
 #pragma unroll 1
-      for (int n0 = j * nq; n0 < (j + 1) * nq; n0 += 32) {
-        float acc[32];
+      for (int n0 = j * 2 * n8 + h * n8; n0 < j * 2 * n8 + (h + 1) * n8; n0 += 16) {
+        float acc[16];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
+        for (int i = 0; i < 16; ++i) acc[i] = 0.0f;
 #pragma unroll 2
         for (int k = 0; k < K; ++k) {
           const float a = in[k * ROWS + t];
           const float4* wr = reinterpret_cast<const float4*>(W + k * N + n0);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
+          for (int q = 0; q < 4; ++q) {
             const float4 w4 = __ldg(wr + q);
             acc[4 * q + 0] = __fmaf_rn(a, w4.x, acc[4 * q + 0]);
             acc[4 * q + 1] = __fmaf_rn(a, w4.y, acc[4 * q + 1]);
@@ -408,11 +460,10 @@ struct Fp32Engine {
             acc[4 * q + 3] = __fmaf_rn(a, w4.w, acc[4 * q + 3]);
           }
         }
-        // the next layer reads `out` only after quad_sync; `in` of this layer
-        // is not overwritten here (ping-pong buffers), except that layer 5
-        // writes buf0, which layer 4 read: ordered by the sync at layer 5's top.
+        // ping-pong buffers: `out` was last read by the previous layer, which
+        // every thread of the row finished before this layer's top sync.
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
+        for (int i = 0; i < 16; ++i) {
           float z = __fadd_rn(acc[i], __ldg(B + n0 + i));
           if (l < NLAYER - 1) z = fmaxf(z, 0.0f);
           out[(n0 + i) * ROWS + t] = z;
@@ -421,19 +472,19 @@ struct Fp32Engine {
     }
     quad_sync();  // logits complete
   }
-  __device__ __forceinline__ void ld32(int col, uint32_t (&v)[32]) const {
-    const int t = tile_row();
+  __device__ __forceinline__ void ld32(uint32_t (&v)[32]) const {
+    const int t = tile_row(), c0 = 64 * col_grp() + 32 * half_id();
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(buf0[(col + i) * ROWS + t]);
+    for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(buf0[(c0 + i) * ROWS + t]);
   }
-  __device__ __forceinline__ void st32(int col, const uint32_t (&v)[32]) const {
-    const int t = tile_row();
+  __device__ __forceinline__ void st32(const uint32_t (&v)[32]) const {
+    const int t = tile_row(), c0 = 64 * col_grp() + 32 * half_id();
 #pragma unroll
-    for (int i = 0; i < 32; ++i) buf0[(col + i) * ROWS + t] = __uint_as_float(v[i]);
+    for (int i = 0; i < 32; ++i) buf0[(c0 + i) * ROWS + t] = __uint_as_float(v[i]);
   }
-  __device__ __forceinline__ float4 bias4_last(int) const { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ __forceinline__ float2 bias_pair(int) const { return make_float2(0.f, 0.f); }
   __device__ __forceinline__ void xput(int slot, uint32_t v) const {
-    xbuf[(slot * NGRP + col_grp()) * ROWS + tile_row()] = v;
+    if (half_id() == 0) xbuf[(slot * NGRP + col_grp()) * ROWS + tile_row()] = v;
   }
   __device__ __forceinline__ void xsync() const { quad_sync(); }
   __device__ __forceinline__ void xget4(int slot, uint32_t (&v)[4]) const {
@@ -443,9 +494,10 @@ struct Fp32Engine {
 };
 
 // ------------------------------------------------- softmax -> Q1' -> CDF
-// Reading R5 (Q1'), per row, with group j owning logits [64j, 64j+64):
-//   m = max_i l_i ;  e_i = 2^(l_i*log2e - m*log2e) (MUFU ex2, FFMA form);
-//   Z_j = sum over the group's even i + sum over its odd i (each ascending),
+// Reading R5 (Q1'), per row; thread (j, h) owns logits [64j+32h, +32):
+//   m = max_i l_i ;  e_i = 2^(l_i*log2e - m*log2e) (MUFU ex2 or the FMA-pipe
+//   polynomial, fixed per column);  z_jh = (sum of even-position terms) +
+//   (sum of odd-position terms), each ascending;  Z_j = z_j0 + z_j1;
 //   Z = ((Z_0 + Z_1) + Z_2) + Z_3;  p_i = e_i * (1/Z) (RN);
 //   f_i = 1 + floor(p_i * 65279);  R = 2^16 - sum f_i >= 0 ; f_255 += R ;
 //   c_i = exclusive prefix sum.
@@ -455,6 +507,8 @@ struct Fp32Engine {
 struct Q1Row {
   float F[NGRP];  // per-group sums of the unadjusted f (exact integers)
   float R;        // residual on symbol 255
+  float Fmine;    // this thread's half-group sum
+  float hbase;    // sum of the lower half of this group if h == 1, else 0
 };
 
 __device__ __forceinline__ f2 f2_splat(float a) { return f2_make(a, a); }
@@ -468,8 +522,7 @@ __device__ __forceinline__ f2 f2_exp2_poly(f2 t) {
   float t0, t1;
   f2_split(t, t0, t1);
   t = f2_make(fmaxf(t0, -126.0f), fmaxf(t1, -126.0f));
-  const f2 magic = f2_splat(12582912.0f);  // 1.5 * 2^23
-  const f2 j = f2_add_rm(t, magic);
+  const f2 j = f2_add_rm(t, f2_splat(12582912.0f));  // 1.5 * 2^23 + floor(t)
   const f2 n = f2_add(j, f2_splat(-12582912.0f));
   float n0, n1;
   f2_split(n, n0, n1);
@@ -488,151 +541,148 @@ __device__ __forceinline__ f2 f2_exp2_poly(f2 t) {
   return f2_bits(r0, r1);
 }
 
-// Passes 1, 2, A.  ENC: also returns f and the group-local exclusive cum of
-// `sym` when it lies in this group.  probs (nullable): p_i of this group's
-// columns (debug export).
+// Passes 1, 2, A.  ENC: also returns f and the half-local exclusive cum of
+// `sym` when it lies in this thread's columns.  probs (nullable): p_i of the
+// row (debug export, 256 entries).
 template <bool ENC, class Eng>
 __device__ __forceinline__ Q1Row q1_table(const Eng& e, int sym, float& fs, float& cs_local, float* probs,
                                           Prof* pf = nullptr) {
-  const int j = col_grp();
-  const int c0 = 64 * j;
+  const int j = col_grp(), h = half_id();
+  const int c0 = 64 * j + 32 * h;
+  uint32_t v[32];
   // pass 1: biased logits, stored back; max
+  e.ld32(v);
   float m = -INFINITY;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    uint32_t v[32];
-    e.ld32(c0 + 32 * h, v);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float4 b = e.bias4_last(c0 + 32 * h + 4 * q);
-      float l0, l1, l2, l3;
-      f2_split(f2_add(f2_bits(v[4 * q + 0], v[4 * q + 1]), f2_make(b.x, b.y)), l0, l1);
-      f2_split(f2_add(f2_bits(v[4 * q + 2], v[4 * q + 3]), f2_make(b.z, b.w)), l2, l3);
-      v[4 * q + 0] = __float_as_uint(l0);
-      v[4 * q + 1] = __float_as_uint(l1);
-      v[4 * q + 2] = __float_as_uint(l2);
-      v[4 * q + 3] = __float_as_uint(l3);
-      m = fmaxf(m, fmaxf(fmaxf(l0, l1), fmaxf(l2, l3)));
-    }
-    e.st32(c0 + 32 * h, v);
+  for (int q = 0; q < 16; ++q) {
+    const float2 b = e.bias_pair(q);
+    float l0, l1;
+    f2_split(f2_add(f2_bits(v[2 * q], v[2 * q + 1]), f2_make(b.x, b.y)), l0, l1);
+    v[2 * q] = __float_as_uint(l0);
+    v[2 * q + 1] = __float_as_uint(l1);
+    m = fmaxf(m, fmaxf(l0, l1));
   }
+  e.st32(v);
+  m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, 16));
   if (pf) pf->mark(4);
   e.xput(0, __float_as_uint(m));
   e.xsync();
   uint32_t x4[4];
   e.xget4(0, x4);
-  if (pf) pf->mark(5);
   m = fmaxf(fmaxf(__uint_as_float(x4[0]), __uint_as_float(x4[1])),
             fmaxf(__uint_as_float(x4[2]), __uint_as_float(x4[3])));
+  if (pf) pf->mark(5);
   const f2 nm = f2_splat(__fmul_rn(-m, LOG2E));
   const f2 l2e = f2_splat(LOG2E);
-  // pass 2: e_i stored back; Z_j as even/odd partial sums
+  // pass 2: e_i stored back; z as even/odd pair partial sums
+  e.ld32(v);
   f2 zz = f2_splat(0.0f);
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    uint32_t v[32];
-    e.ld32(c0 + 32 * h, v);
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const f2 t = f2_fma(f2_bits(v[2 * q], v[2 * q + 1]), l2e, nm);
-      float e0, e1;
-      if (q % 8 >= 5) {  // 6 of 16 pairs on the FMA pipe, the rest on MUFU
-        f2_split(f2_exp2_poly(t), e0, e1);
-      } else {
-        float t0, t1;
-        f2_split(t, t0, t1);
-        e0 = ex2_approx(t0);
-        e1 = ex2_approx(t1);
-      }
-      zz = f2_add(zz, f2_make(e0, e1));
-      v[2 * q] = __float_as_uint(e0);
-      v[2 * q + 1] = __float_as_uint(e1);
+  for (int q = 0; q < 16; ++q) {
+    const f2 t = f2_fma(f2_bits(v[2 * q], v[2 * q + 1]), l2e, nm);
+    float e0, e1;
+    if (q % 8 >= 5) {  // 6 of 16 pairs on the FMA pipe, the rest on MUFU
+      f2_split(f2_exp2_poly(t), e0, e1);
+    } else {
+      float t0, t1;
+      f2_split(t, t0, t1);
+      e0 = ex2_approx(t0);
+      e1 = ex2_approx(t1);
     }
-    e.st32(c0 + 32 * h, v);
+    zz = f2_add(zz, f2_make(e0, e1));
+    v[2 * q] = __float_as_uint(e0);
+    v[2 * q + 1] = __float_as_uint(e1);
   }
+  e.st32(v);
   float za, zb;
   f2_split(zz, za, zb);
+  float z = __fadd_rn(za, zb);
+  z = __fadd_rn(z, __shfl_xor_sync(0xFFFFFFFFu, z, 16));  // commutative: identical in both halves
   if (pf) pf->mark(6);
-  e.xput(1, __float_as_uint(__fadd_rn(za, zb)));
+  e.xput(1, __float_as_uint(z));
   e.xsync();
   e.xget4(1, x4);
-  if (pf) pf->mark(5);
   const float Z = __fadd_rn(__fadd_rn(__fadd_rn(__uint_as_float(x4[0]), __uint_as_float(x4[1])),
                                       __uint_as_float(x4[2])),
                             __uint_as_float(x4[3]));
+  if (pf) pf->mark(5);
   const f2 inv = f2_splat(__frcp_rn(Z));
   const f2 scale = f2_splat(Q1_SCALE);
   const f2 two23 = f2_splat(8388608.0f);
   const f2 fbias = f2_splat(-8388607.0f);  // y - 2^23 + 1 = 1 + floor(x), exact
   // pass A: p_i, f_i = 1 + floor(p_i * 65279) (x + 2^23 rounded toward -inf
-  // has ulp 1), stored back as floats; group sum
+  // has ulp 1), stored back as floats; half sum
+  e.ld32(v);
   f2 FF = f2_splat(0.0f);
   fs = 0.0f;
   cs_local = 0.0f;
   float cum = 0.0f;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    uint32_t v[32];
-    e.ld32(c0 + 32 * h, v);
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const f2 p = f2_mul(f2_bits(v[2 * q], v[2 * q + 1]), inv);
-      const f2 f = f2_add(f2_add_rm(f2_mul(p, scale), two23), fbias);
-      FF = f2_add(FF, f);
-      float f0, f1;
-      f2_split(f, f0, f1);
-      if (ENC) {
-        const int i0 = c0 + 32 * h + 2 * q;
-        if (i0 == sym) {
-          fs = f0;
-          cs_local = cum;
-        }
-        if (i0 + 1 == sym) {
-          fs = f1;
-          cs_local = __fadd_rn(cum, f0);
-        }
-        cum = __fadd_rn(cum, __fadd_rn(f0, f1));
+  for (int q = 0; q < 16; ++q) {
+    const f2 p = f2_mul(f2_bits(v[2 * q], v[2 * q + 1]), inv);
+    const f2 f = f2_add(f2_add_rm(f2_mul(p, scale), two23), fbias);
+    FF = f2_add(FF, f);
+    float f0, f1;
+    f2_split(f, f0, f1);
+    if (ENC) {
+      const int i0 = c0 + 2 * q;
+      if (i0 == sym) {
+        fs = f0;
+        cs_local = cum;
       }
-      if (probs) {
-        float p0, p1;
-        f2_split(p, p0, p1);
-        probs[c0 + 32 * h + 2 * q] = p0;
-        probs[c0 + 32 * h + 2 * q + 1] = p1;
+      if (i0 + 1 == sym) {
+        fs = f1;
+        cs_local = __fadd_rn(cum, f0);
       }
-      v[2 * q] = __float_as_uint(f0);
-      v[2 * q + 1] = __float_as_uint(f1);
+      cum = __fadd_rn(cum, __fadd_rn(f0, f1));
     }
-    e.st32(c0 + 32 * h, v);
+    if (probs) {
+      float p0, p1;
+      f2_split(p, p0, p1);
+      probs[c0 + 2 * q] = p0;
+      probs[c0 + 2 * q + 1] = p1;
+    }
+    v[2 * q] = __float_as_uint(f0);
+    v[2 * q + 1] = __float_as_uint(f1);
   }
+  e.st32(v);
   float Fa, Fb;
   f2_split(FF, Fa, Fb);
+  Q1Row r;
+  r.Fmine = __fadd_rn(Fa, Fb);
+  const float Fo = __shfl_xor_sync(0xFFFFFFFFu, r.Fmine, 16);
+  r.hbase = h ? Fo : 0.0f;
   if (pf) pf->mark(7);
-  e.xput(2, __float_as_uint(__fadd_rn(Fa, Fb)));
+  e.xput(2, __float_as_uint(__fadd_rn(r.Fmine, Fo)));  // exact integer sum
   e.xsync();
   e.xget4(2, x4);
-  if (pf) pf->mark(5);
-  Q1Row r;
 #pragma unroll
   for (int g = 0; g < NGRP; ++g) r.F[g] = __uint_as_float(x4[g]);
   r.R = 65536.0f - (((r.F[0] + r.F[1]) + r.F[2]) + r.F[3]);
   return r;
 }
 
-// Final integer table of this group's 64 columns (debug export).
+__device__ __forceinline__ float q1_base(const Q1Row& r) {
+  const int j = col_grp();
+  float base = r.hbase;
+#pragma unroll
+  for (int g = 0; g < NGRP; ++g)
+    if (g < j) base += r.F[g];
+  return base;
+}
+
+// Final integer table of this thread's 32 columns (debug export).
 template <class Eng>
 __device__ __forceinline__ void q1_store_freqs(const Eng& e, const Q1Row& r, uint16_t* freqs) {
-  const int j = col_grp();
+  const int c0 = 64 * col_grp() + 32 * half_id();
+  uint32_t v[32];
+  e.ld32(v);  // all lanes load (tcgen05.ld is .sync.aligned)
+  if (freqs) {
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    uint32_t v[32];
-    e.ld32(64 * j + 32 * h, v);  // all lanes load (tcgen05.ld is .sync.aligned)
-    if (freqs) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        float f = __uint_as_float(v[i]);
-        if (j == NGRP - 1 && h == 1 && i == 31) f += r.R;
-        freqs[64 * j + 32 * h + i] = (uint16_t)f;
-      }
+    for (int i = 0; i < 32; ++i) {
+      float f = __uint_as_float(v[i]);
+      if (c0 + i == NOUT - 1) f += r.R;
+      freqs[c0 + i] = (uint16_t)f;
     }
   }
 }
@@ -645,14 +695,13 @@ __device__ __forceinline__ uint32_t q1_encode(const Eng& e, int sym, float* prob
   float fs, csl;
   const Q1Row r = q1_table<true>(e, sym, fs, csl, probs);
   if (export_freqs) q1_store_freqs(e, r, freqs);
-  const int j = col_grp();
+  const int c0 = 64 * col_grp() + 32 * half_id();
   uint32_t packed = 0;
-  if ((sym >> 6) == j) {
-    float base = 0.0f;
-    for (int g = 0; g < j; ++g) base += r.F[g];
+  if (sym >= c0 && sym < c0 + 32) {
     if (sym == NOUT - 1) fs += r.R;
-    packed = (uint32_t)fs | ((uint32_t)(base + csl) << 16);
+    packed = (uint32_t)fs | ((uint32_t)(q1_base(r) + csl) << 16);
   }
+  packed |= __shfl_xor_sync(0xFFFFFFFFu, packed, 16);
   e.xput(3, packed);
   e.xsync();
   uint32_t x4[4];
@@ -661,60 +710,62 @@ __device__ __forceinline__ uint32_t q1_encode(const Eng& e, int sym, float* prob
 }
 
 // Decoder: symbol s with c_s <= slot < c_s + f_s (all threads of the row).
-// `slot` is read from group 0 (the rANS lane owner), published through
-// exchange slot 6 and picked up after q1_table's first exchange barrier.
-// Search: reverse scan of the group's 64 entries with the monotone test
-// slot < c_{i+1}; the last hit is the smallest such i = s.  Every lane
-// executes the same TMEM loads (tcgen05.ld is .sync.aligned).
+// `slot0` is valid in the rANS owner (group 0, lower half); it is broadcast to
+// the upper half by a shuffle and to groups 1-3 through exchange slot 6,
+// picked up after q1_table's first exchange barrier.  Search: reverse scan of
+// this thread's 32 entries with the monotone test slot < c_{i+1}; the last hit
+// is the smallest such i = s.  Every lane executes the same TMEM loads.
 template <class Eng>
 __device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot0, uint32_t& fs_out, uint32_t& cs_out,
                                          Prof* pf = nullptr) {
   float fs, csl;
-  e.xput(6, slot0);
+  e.xput(6, __shfl_sync(0xFFFFFFFFu, slot0, threadIdx.x & 15));
   const Q1Row r = q1_table<false>(e, -1, fs, csl, nullptr, pf);
   uint32_t s4[4];
   e.xget4(6, s4);
   const float slot = (float)s4[0];
-  const int j = col_grp();
-  float base = 0.0f;
-#pragma unroll
-  for (int g = 0; g < NGRP; ++g)
-    if (g < j) base += r.F[g];
-  float cum = base + r.F[j] + (j == NGRP - 1 ? r.R : 0.0f);  // c_64 of this group
+  const int c0 = 64 * col_grp() + 32 * half_id();
+  const float base = q1_base(r);
+  float cum = base + r.Fmine + (c0 == NOUT - 32 ? r.R : 0.0f);  // c at the end of my columns
   const bool mine = slot >= base && slot < cum;
   int sym = 0;
   float fsel = 0.0f, csel = 0.0f;
+  uint32_t v[32];
+  e.ld32(v);
 #pragma unroll
-  for (int h = 1; h >= 0; --h) {
-    uint32_t v[32];
-    e.ld32(64 * j + 32 * h, v);
-#pragma unroll
-    for (int i = 31; i >= 0; --i) {
-      float f = __uint_as_float(v[i]);
-      if (j == NGRP - 1 && h == 1 && i == 31) f += r.R;
-      const float lo = cum - f;  // exact
-      if (slot < cum) {
-        sym = 64 * j + 32 * h + i;
-        fsel = f;
-        csel = lo;
-      }
-      cum = lo;
+  for (int i = 31; i >= 0; --i) {
+    float f = __uint_as_float(v[i]);
+    if (i == 31 && c0 == NOUT - 32) f += r.R;
+    const float lo = cum - f;  // exact
+    if (slot < cum) {
+      sym = c0 + i;
+      fsel = f;
+      csel = lo;
     }
+    cum = lo;
   }
   if (pf) pf->mark(8);
-  e.xput(4, mine ? ((uint32_t)sym | ((uint32_t)fsel << 8)) : 0xFFFFFFFFu);
-  e.xput(5, (uint32_t)csel);
+  uint32_t pk = mine ? ((uint32_t)sym | ((uint32_t)fsel << 8)) : 0xFFFFFFFFu;
+  uint32_t pc = (uint32_t)csel;
+  const uint32_t opk = __shfl_xor_sync(0xFFFFFFFFu, pk, 16);
+  const uint32_t opc = __shfl_xor_sync(0xFFFFFFFFu, pc, 16);
+  if (!mine) {
+    pk = opk;
+    pc = opc;
+  }
+  e.xput(4, pk);
+  e.xput(5, pc);
   e.xsync();
   uint32_t k4[4], c4[4];
   e.xget4(4, k4);
   e.xget4(5, c4);
-  if (pf) pf->mark(5);
   int g = 0;
 #pragma unroll
   for (int q = 0; q < NGRP; ++q)
     if (k4[q] != 0xFFFFFFFFu) g = q;
   fs_out = k4[g] >> 8;
   cs_out = c4[g];
+  if (pf) pf->mark(5);
   return (int)(k4[g] & 0xFFu);
 }
 

@@ -29,10 +29,10 @@ __device__ __forceinline__ int off_dc(int j) { return j < 72 ? j % 9 - 6 : j - 7
 // rows) touch distinct shared-memory banks: byte (bank, col, ringrow) at
 // (bank*32 + col)*RING_ROWS + ringrow; ringrow = 8 + slot-in-CTA, rows 0..7
 // mirror the previous CTA's last 8 slots (halo).
-constexpr int RING_ROWS = ROWS + 8;                  // own 128 slots + 8 halo rows
-constexpr uint32_t RING_BYTES = 2u * RING_ROWS * 32u;  // 2 banks x 32 cols x 136 rows
-constexpr uint32_t F32_BUF_BYTES = (NOUT + HID) * ROWS * 4u;          // 196608
-constexpr uint32_t F32_X_BYTES = NXSLOT * NGRP * ROWS * 4u;          // 12288
+constexpr int RING_ROWS = ROWS + 8;                  // own 64 slots + 8 halo rows
+constexpr uint32_t RING_BYTES = 2u * RING_ROWS * 32u;  // 2 banks x 32 cols x 72 rows
+constexpr uint32_t F32_BUF_BYTES = (NOUT + HID) * ROWS * 4u;          // 98304
+constexpr uint32_t F32_X_BYTES = NXSLOT * NGRP * ROWS * 4u;          // 7168
 constexpr uint32_t MAX_DYN_SMEM = 232448 - 64;                       // 227 KB minus static
 
 size_t enc_smem_bytes(uint32_t precision) {
@@ -102,21 +102,30 @@ __device__ __forceinline__ void engine_teardown(typename EngineSel<PREC>::T& eng
   }
 }
 
-// Feed this thread's share of the 78 (80) window inputs: group j owns inputs
-// [20j, 20j+20); get(k) returns the pixel value of window offset k (0 fill).
-// J is a compile-time constant so every window offset folds to an immediate.
-template <int PREC, int J, class Eng, class Get>
-__device__ __forceinline__ void feed_j(const Eng& eng, Get& get) {
+// Feed this thread's share of the 78 (80) window inputs: thread (j, h) owns
+// inputs [20j+10h, +10) = A packed columns [10j+5h, +5); get(dr, dc) returns
+// the pixel value of that window offset (0 fill).  Offsets come from the tap
+// index with a multiply-shift division by 9 (exact for k < 80).
+__device__ __forceinline__ void tap_offset(int k, int& dr, int& dc) {
+  const int q9 = (k * 57) >> 9;  // k / 9
+  dr = q9 - 8;
+  dc = k - 9 * q9 - 6;
+}
+template <int PREC, class Eng, class Get>
+__device__ __forceinline__ void feed(const Eng& eng, Get get) {
+  const int kb = 20 * col_grp() + 10 * half_id();
   if constexpr (PREC == 1) {
     // v/256 exactly: (1 + v/256) has v in the top 8 mantissa bits; minus 1 is exact.
     const f2 m1 = f2_make(-1.0f, -1.0f);
-    uint32_t a[10];
+    uint32_t a[5];
 #pragma unroll
-    for (int i = 0; i < 10; ++i) {
-      constexpr int base = 20 * J;
-      const int k0 = base + 2 * i;
-      const uint32_t v0 = k0 < KIN ? get(k0) : 0u;
-      const uint32_t v1 = k0 + 1 < KIN ? get(k0 + 1) : 0u;
+    for (int i = 0; i < 5; ++i) {
+      const int k0 = kb + 2 * i;
+      int dr0, dc0, dr1, dc1;
+      tap_offset(k0, dr0, dc0);
+      tap_offset(k0 + 1, dr1, dc1);
+      const uint32_t v0 = k0 < KIN ? get(dr0, dc0) : 0u;
+      const uint32_t v1 = k0 + 1 < KIN ? get(dr1, dc1) : 0u;
       float x0, x1;
       f2_split(f2_add(f2_bits(0x3F800000u | (v0 << 15), 0x3F800000u | (v1 << 15)), m1), x0, x1);
       a[i] = pack_bf16(x0, x1);
@@ -124,26 +133,19 @@ __device__ __forceinline__ void feed_j(const Eng& eng, Get& get) {
     eng.put_input(a);
   } else {
 #pragma unroll
-    for (int i = 0; i < 20; ++i) {
-      const int k = 20 * J + i;
-      if (k < KIN) eng.put_input(k, __fadd_rn(__uint_as_float(0x3F800000u | (get(k) << 15)), -1.0f));
+    for (int i = 0; i < 10; ++i) {
+      const int k = kb + i;
+      int dr, dc;
+      tap_offset(k, dr, dc);
+      if (k < KIN) eng.put_input(k, __fadd_rn(__uint_as_float(0x3F800000u | (get(dr, dc) << 15)), -1.0f));
     }
-  }
-}
-template <int PREC, class Eng, class Get>
-__device__ __forceinline__ void feed(const Eng& eng, Get get) {
-  switch (col_grp()) {  // warp-uniform
-    case 0: feed_j<PREC, 0>(eng, get); break;
-    case 1: feed_j<PREC, 1>(eng, get); break;
-    case 2: feed_j<PREC, 2>(eng, get); break;
-    default: feed_j<PREC, 3>(eng, get); break;
   }
 }
 
 // ------------------------------------------------------------ encoder MLP
-// Persistent CTAs over 128-pixel tiles of the units' raster order.  Thread
-// (row, j): pixel = tile*128 + row; group j owns inputs [20j,20j+20), hidden
-// columns [32j,32j+32) and logits [64j,64j+64) (dlic_device.cuh).
+// Persistent CTAs over 64-pixel tiles of the units' raster order.  Thread
+// (row, j, h): pixel = tile*64 + row; (j, h) owns inputs [20j+10h, +10),
+// hidden columns [32j+16h, +16) and logits [64j+32h, +32) (dlic_device.cuh).
 template <int PREC>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_enc_mlp(Plan p, DevWeights w, const uint8_t* __restrict__ imgs, uint32_t* __restrict__ fc,
@@ -151,7 +153,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
-  const int row = tile_row(), j = col_grp();
+  const int row = tile_row();
   typename EngineSel<PREC>::T eng;
   engine_setup<PREC>(eng, smem, w, &bar, &tslot);
   const uint64_t total = (uint64_t)p.n_img * p.upi * p.tiles_per_unit;
@@ -161,13 +163,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t u = (uint32_t)(tile / p.tiles_per_unit);
     const uint32_t k = (uint32_t)(tile % p.tiles_per_unit);
     const Unit un = unit_info(p, u);
-    const uint32_t q = k * 128u + (uint32_t)row;
+    const uint32_t q = k * (uint32_t)ROWS + (uint32_t)row;
     const bool valid = q < un.w * un.h;
     const int r = valid ? (int)(q / un.w) : 0, c = valid ? (int)(q % un.w) : 0;
     const uint8_t* img = imgs + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
     const int uw = (int)un.w;
-    auto get = [&](int kk) -> uint32_t {  // branch-free: invalid taps load the target and mask
-      const int rr = r + off_dr(kk), cc = c + off_dc(kk);
+    auto get = [&](int dr, int dc) -> uint32_t {  // branch-free: invalid taps load the target and mask
+      const int rr = r + dr, cc = c + dc;
       const bool ok = valid && rr >= 0 && (unsigned)cc < (unsigned)uw;
       const uint32_t v = __ldg(img + (ok ? (int64_t)rr * p.W + cc : (int64_t)r * p.W + c));
       return ok ? v : 0u;
@@ -176,23 +178,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     eng.run();
     const int sym = valid ? (int)__ldg(img + (uint64_t)r * p.W + c) : 0;
     const uint64_t gi = (uint64_t)un.img * p.W * p.H + (uint64_t)(un.y0 + r) * p.W + (un.x0 + c);
-    if (dbg && dbg_logits) {  // raw logits (bias added) of this group's 64 columns
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        uint32_t v[32];
-        eng.ld32(64 * j + 32 * h, v);
-        if (valid)
-          for (int i = 0; i < 32; ++i) {
-            const int cc = 64 * j + 32 * h + i;
-            float lv = __uint_as_float(v[i]);
-            if constexpr (PREC == 1) lv = __fadd_rn(lv, eng.bias[BIAS_OFF_LAST + cc]);
-            dbg_logits[gi * NOUT + cc] = lv;
-          }
-      }
+    if (dbg && dbg_logits) {  // raw logits (bias added) of this thread's 32 columns
+      uint32_t v[32];
+      eng.ld32(v);
+      if (valid)
+        for (int i = 0; i < 32; ++i) {
+          const int cc = 64 * col_grp() + 32 * half_id() + i;
+          float lv = __uint_as_float(v[i]);
+          if constexpr (PREC == 1) lv = __fadd_rn(lv, eng.bias[BIAS_OFF_LAST + cc]);
+          dbg_logits[gi * NOUT + cc] = lv;
+        }
     }
     const uint32_t v = q1_encode(eng, sym, (dbg && valid && dbg_probs) ? dbg_probs + gi * NOUT : nullptr,
                                  (dbg && valid && dbg_freqs) ? dbg_freqs + gi * NOUT : nullptr, dbg);
-    if (valid && j == 0) fc[un.fc_off + q] = v;
+    if (valid && threadIdx.x < ROWS * 2 && half_id() == 0) fc[un.fc_off + q] = v;
   }
   engine_teardown<PREC>(eng);
 }
@@ -423,12 +422,14 @@ __global__ void k_dec_prep(Plan p, const uint8_t* __restrict__ bits, const uint6
 }
 
 // ------------------------------------------------------------ decoder
-// One cluster of nc CTAs per unit; slot S = rank*128 + row holds rows
-// r = S (mod 128*nc) in turn.  Per front t: all 4 groups of a row
+// One cluster of nc CTAs per unit; slot S = rank*64 + row holds rows
+// r = S (mod 64*nc) in turn.  Per front t: the 8 threads of a row
 // gather their share of the window from the shared-memory ring, run the
-// network, and search the Q1' table; group 0 (warps 0-3) owns the row's rANS
-// lane: state update, interleaved word reads (ballot/popc within the G-row
-// group, G | 32 so a group never leaves its warp), pixel publication.
+// network, and search the Q1' table; the lower half-warps of group 0 (warps
+// 0-3, lanes 0-15, one thread per row) own the rows' rANS lanes: state
+// update, interleaved word reads (ballot/popc within a warp; a G = 32 group
+// spans two warps and adds the first warp's count through shared memory),
+// pixel publication to HBM, the ring and the next CTA's halo (DSMEM).
 template <int PREC>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_decode(Plan p, DevWeights w, const uint8_t* __restrict__ bits, const uint64_t* __restrict__ cont_off,
@@ -437,15 +438,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
-  const int row = tile_row(), j = col_grp();
+  __shared__ uint32_t s_cnt[4][2];  // per owner warp and pass parity: readers | active<<16
+  const int row = tile_row();
   const uint32_t lane = lane_id();
+  const bool owner = threadIdx.x < 128 && half_id() == 0;  // group 0, lower half-warp
   const uint32_t NC = p.nc, NS = ROWS * NC;
+  const uint32_t ns_shift = 6u + (uint32_t)(__ffs((int)NC) - 1);
   // optional phase profile (thread 0 of each CTA), see Prof in dlic_device.cuh:
   // 0 top 1 gather 2 put 3 mlp 4 pass1 5 exchanges 6 pass2 7 passA 8 search 9 rans 10 barrier
   Prof pf;
   pf.on = prof != nullptr && threadIdx.x == 0;
-#define DLIC_PROF_MARK(k) pf.mark(k);
-  const uint32_t ns_shift = 7u + (NC == 1 ? 0u : NC == 2 ? 1u : NC == 4 ? 2u : 3u);
   const uint32_t rank = NC > 1 ? cluster_rank() : 0u;
   const uint32_t u = blockIdx.x / NC;
   const Unit un = unit_info(p, u);
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t G = p.G;
   const uint32_t g_shift = (uint32_t)(__ffs((int)G) - 1);
   for (uint32_t g = threadIdx.x; g < un.ngroups; g += NTHREADS) {
-    if ((((G * g) & (NS - 1)) >> 7) == rank) cursor[g] = 2u * min(G, un.h - G * g);
+    if ((((G * g) & (NS - 1)) >> 6) == rank) cursor[g] = 2u * min(G, un.h - G * g);
   }
   if (NC > 1) cluster_sync_all();
   else __syncthreads();
@@ -469,6 +471,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t halo_base = NC > 1 ? map_cluster(ring_s, (rank + 1) % NC) : ring_s;
   const int uw = (int)un.w, uh = (int)un.h;
   const int T = uw + 3 * (uh - 1);
+  const int wq = (int)(threadIdx.x >> 5);  // owner warp = quadrant (0..3)
   uint32_t x = 0;
   int err = 0;
 
@@ -485,56 +488,123 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       c = t - 3 * r;
     }
     const bool any = __syncthreads_or(active);
-    DLIC_PROF_MARK(0)
+    pf.mark(0);
     if (any) {
       const uint32_t g = (uint32_t)r >> g_shift;  // G is a power of two dividing 32
-      if (j == 0 && active && c == 0) {  // the row's lane starts: flushed state (hi, lo)
-        const uint32_t sidx = un.first_stream + g;
-        const uint16_t* sw = reinterpret_cast<const uint16_t*>(cbase + sbase[sidx]);
+      const bool act = owner && active;
+      const uint32_t bk = ((uint32_t)r >> ns_shift) & 1u;  // pass parity over the slots
+      // Prefetch this front's candidate stream words into registers now, so the
+      // L2 latency hides behind the network (shared memory leaves almost no L1).
+      //  G = 32: a warp's active rows of one pass parity form one group; lanes
+      //          0-31 hold words cur..cur+31 of it (the odd warp of the pair
+      //          starts after the even warp's readers, <= 16 of them).
+      //  G < 32: each owner lane holds the word it reads if every earlier row
+      //          of its group in this warp reads one.
+      uint32_t pw0 = 0, pw1 = 0, first_lane = 0;
+      uint32_t my_sb = 0, my_sl = 0, my_cur = 0;
+      if (threadIdx.x < 128) {
+        if (act) {
+          const uint32_t sidx = un.first_stream + g;
+          my_sb = sbase[sidx];
+          my_sl = slen[sidx];
+          my_cur = cursor[g];
+        }
+        if (G == 32) {
+#pragma unroll
+          for (uint32_t b = 0; b < 2; ++b) {
+            const uint32_t mb = __ballot_sync(0xFFFFFFFFu, act && bk == b);
+            if (mb) {
+              const uint32_t src = (uint32_t)__ffs(mb) - 1u;
+              const uint32_t sb = __shfl_sync(0xFFFFFFFFu, my_sb, src);
+              const uint32_t sl = __shfl_sync(0xFFFFFFFFu, my_sl, src);
+              const uint32_t cu = __shfl_sync(0xFFFFFFFFu, my_cur, src);
+              const uint16_t* swb = reinterpret_cast<const uint16_t*>(cbase + sb);
+              const uint32_t idx = cu + lane;
+              const uint32_t wv = idx < sl ? (uint32_t)__ldg(swb + idx) : 0u;
+              if (b == 0) pw0 = wv;
+              else pw1 = wv;
+            }
+          }
+        } else {
+          const uint32_t key = act ? g : (0x80000000u | lane);
+          const uint32_t gm = __match_any_sync(0xFFFFFFFFu, key);
+          first_lane = (uint32_t)__ffs(gm) - 1u;
+          const uint32_t idx = my_cur + (lane - first_lane);
+          const uint16_t* swm = reinterpret_cast<const uint16_t*>(cbase + my_sb);
+          pw0 = (act && idx < my_sl) ? (uint32_t)__ldg(swm + idx) : 0u;
+        }
+      }
+      if (act && c == 0) {  // the row's lane starts: flushed state (hi, lo)
+        const uint16_t* sw = reinterpret_cast<const uint16_t*>(cbase + my_sb);
         const uint32_t i = 2u * ((uint32_t)r - G * g);
-        if (i + 1 < slen[sidx]) x = ((uint32_t)sw[i] << 16) | (uint32_t)sw[i + 1];
+        if (i + 1 < my_sl) x = ((uint32_t)__ldg(sw + i) << 16) | (uint32_t)__ldg(sw + i + 1);
         else err = 8;
       }
       // window gather from the ring (rows r-8..r of this slot's neighbourhood)
-      auto get = [&](int kk) -> uint32_t {  // branch-free: invalid taps read a zero byte
-        const int d = -off_dr(kk);
-        const int rr = r - d, cc = c + off_dc(kk);
+      auto get = [&](int dr, int dc) -> uint32_t {  // branch-free: invalid taps read a zero byte
+        const int rr = r + dr, cc = c + dc;
         const bool ok = active && rr >= 0 && (unsigned)cc < (unsigned)uw;
         const uint32_t bank = ((uint32_t)rr >> ns_shift) & 1u;
-        const uint32_t a = (bank * 32u + ((uint32_t)cc & 31u)) * RING_ROWS + (uint32_t)(row - d + 8);
+        const uint32_t a = (bank * 32u + ((uint32_t)cc & 31u)) * RING_ROWS + (uint32_t)(row + dr + 8);
         return ring[ok ? a : RING_BYTES];
       };
       feed<PREC>(eng, get);
-      DLIC_PROF_MARK(1)
+      pf.mark(1);
       if constexpr (PREC == 1) tc_wait_st();
-      DLIC_PROF_MARK(2)
+      pf.mark(2);
       eng.run();
-      DLIC_PROF_MARK(3)
+      pf.mark(3);
       const uint32_t slot = x & 0xFFFFu;
       uint32_t fs, cs;
       const int sym = q1_decode(eng, slot, fs, cs, &pf);
-      if (j == 0) {
-        const uint32_t sidx = un.first_stream + g;
-        const uint16_t* sw = reinterpret_cast<const uint16_t*>(cbase + (active ? sbase[sidx] : 0u));
-        const uint32_t sl = active ? slen[sidx] : 0u;
+      if (threadIdx.x < 128) {  // warps 0-3: rANS lanes in the lower half-warps
         bool need = false;
-        if (active) {
+        if (act) {
           x = fs * (x >> 16) + slot - cs;
           need = x < RANS_L;
         }
-        const uint32_t key = active ? g : (0x80000000u | lane);
+        const uint32_t key = act ? g : (0x80000000u | lane);
         const uint32_t gm = __match_any_sync(0xFFFFFFFFu, key);
-        const uint32_t readers = __ballot_sync(0xFFFFFFFFu, need) & gm;
-        uint32_t cur = 0;
-        if (active) cur = cursor[g];
-        __syncwarp();
+        // A warp may hold rows of two groups at once: one finishing and one of
+        // the next pass over the slots (rows NS apart).  They differ in the
+        // pass parity bk, which keys the cross-warp counts below.
+        const uint32_t nb0 = __ballot_sync(0xFFFFFFFFu, need && bk == 0);
+        const uint32_t nb1 = __ballot_sync(0xFFFFFFFFu, need && bk == 1);
+        const uint32_t a0 = __ballot_sync(0xFFFFFFFFu, act && bk == 0);
+        const uint32_t a1 = __ballot_sync(0xFFFFFFFFu, act && bk == 1);
+        const uint32_t readers = (nb0 | nb1) & gm;
+        const uint32_t nmine = __popc(readers);          // this warp's readers of my group
+        const uint32_t cur = my_cur;
+        if (lane == 0) {
+          s_cnt[wq][0] = __popc(nb0) | (a0 ? 0x10000u : 0u);
+          s_cnt[wq][1] = __popc(nb1) | (a1 ? 0x10000u : 0u);
+        }
+        asm volatile("bar.sync 5, 128;" ::: "memory");
+        // G = 32: rows of the group's upper 16 (odd warp) read after the even warp's
+        uint32_t before = 0, total = nmine;
+        bool writer = lane == (uint32_t)(__ffs(gm) - 1);
+        if (G == 32) {
+          const uint32_t other = s_cnt[wq ^ 1][bk];
+          if (wq & 1) {
+            before = other & 0xFFFFu;
+            total = before + nmine;
+          } else {
+            total = nmine + (other & 0xFFFFu);
+            writer = writer && !(other & 0x10000u);  // the odd warp writes when it is active
+          }
+        }
+        const uint32_t rk = __popc(readers & ((1u << lane) - 1u));
+        // word from the prefetch registers (all lanes take part in the shuffles)
+        const uint32_t src = G == 32 ? (before + rk) & 31u : (first_lane + rk) & 31u;
+        const uint32_t w0 = __shfl_sync(0xFFFFFFFFu, pw0, src);
+        const uint32_t w1 = __shfl_sync(0xFFFFFFFFu, pw1, src);
         if (need) {
-          const uint32_t wi = cur + __popc(readers & ((1u << lane) - 1u));
-          if (wi < sl) x = (x << 16) | (uint32_t)sw[wi];
+          const uint32_t wi = cur + before + rk;
+          if (wi < my_sl) x = (x << 16) | (G == 32 && bk == 1 ? w1 : w0);
           else err = 8;
         }
-        if (active && lane == (uint32_t)(__ffs(gm) - 1)) cursor[g] = cur + __popc(readers);
-        if (active) {
+        if (act && writer) cursor[g] = cur + total;
+        if (act) {
           oimg[(uint64_t)r * p.W + c] = (uint8_t)sym;
           const uint32_t bank = ((uint32_t)r >> ns_shift) & 1u;
           const uint32_t col = (uint32_t)c & 31u;
@@ -547,17 +617,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (c == uw - 1 && x != RANS_L) err = 6;  // end-of-lane invariant
         }
       }
-      DLIC_PROF_MARK(9)
+      pf.mark(9);
     }
     if (NC > 1) cluster_sync_all();
     else __syncthreads();
-    DLIC_PROF_MARK(10)
+    pf.mark(10);
   }
   if (pf.on)
-    for (int k = 0; k < 11; ++k) atomicAdd(prof + k, pf.acc[k]);
-#undef DLIC_PROF_MARK
+    for (int kk = 0; kk < 11; ++kk) atomicAdd(prof + kk, pf.acc[kk]);
   for (uint32_t g = threadIdx.x; g < un.ngroups; g += NTHREADS) {
-    if ((((G * g) & (NS - 1)) >> 7) == rank && cursor[g] != slen[un.first_stream + g]) err = 6;
+    if ((((G * g) & (NS - 1)) >> 6) == rank && cursor[g] != slen[un.first_stream + g]) err = 6;
   }
   if (err) atomicMax(status + un.img, err);
   engine_teardown<PREC>(eng);
@@ -625,6 +694,10 @@ static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uin
   cfg.blockDim = dim3(NTHREADS);
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
+  if (p.nc > 8) {
+    e = cudaFuncSetAttribute(k_decode<PREC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = p.nc;
