@@ -40,7 +40,7 @@ size_t enc_smem_bytes(uint32_t precision) {
 }
 static uint32_t cursor_bytes(uint32_t ngroups) { return (ngroups * 4u + 15u) & ~15u; }
 size_t dec_smem_bytes(uint32_t precision, uint32_t max_groups) {
-  return enc_smem_bytes(precision) + RING_BYTES + 16 + cursor_bytes(max_groups);
+  return enc_smem_bytes(precision) + RING_BYTES + 16 + 3 * cursor_bytes(max_groups);
 }
 size_t dec_smem_limit() { return MAX_DYN_SMEM; }
 
@@ -456,11 +456,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   typename EngineSel<PREC>::T eng;
   uint8_t* ring = engine_setup<PREC>(eng, smem, w, &bar, &tslot);
   uint32_t* cursor = reinterpret_cast<uint32_t*>(ring + RING_BYTES + 16);  // 16 zero bytes after the ring
+  uint32_t* s_sbase = cursor + ((un.ngroups + 3u) & ~3u);                   // per-group stream table
+  uint32_t* s_slen = s_sbase + ((un.ngroups + 3u) & ~3u);
   if (threadIdx.x < 16) ring[RING_BYTES + threadIdx.x] = 0;
   const uint32_t G = p.G;
   const uint32_t g_shift = (uint32_t)(__ffs((int)G) - 1);
   for (uint32_t g = threadIdx.x; g < un.ngroups; g += NTHREADS) {
     if ((((G * g) & (NS - 1)) >> 6) == rank) cursor[g] = 2u * min(G, un.h - G * g);
+    s_sbase[g] = sbase[un.first_stream + g];
+    s_slen[g] = slen[un.first_stream + g];
   }
   if (NC > 1) cluster_sync_all();
   else __syncthreads();
@@ -504,9 +508,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       uint32_t my_sb = 0, my_sl = 0, my_cur = 0;
       if (threadIdx.x < 128) {
         if (act) {
-          const uint32_t sidx = un.first_stream + g;
-          my_sb = sbase[sidx];
-          my_sl = slen[sidx];
+          my_sb = s_sbase[g];
+          my_sl = s_slen[g];
           my_cur = cursor[g];
         }
         if (G == 32) {
