@@ -66,7 +66,7 @@ __device__ __forceinline__ void load_smem(uint8_t* dst, const void* src, uint32_
 // end of the engine's shared-memory region.
 template <int PREC>
 __device__ __forceinline__ uint8_t* engine_setup(typename EngineSel<PREC>::T& eng, uint8_t* smem, const DevWeights& w,
-                                                 uint64_t* bar, uint32_t* tslot) {
+                                                 uint64_t* bar, uint32_t* tslot) {  // bar: 2 mbarriers
   if constexpr (PREC == 1) {
     load_smem(smem, w.wimg, WIMG_BYTES);
     load_smem(smem + WIMG_BYTES, w.bias, BIAS_BYTES);
@@ -151,11 +151,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     k_enc_mlp(Plan p, DevWeights w, const uint8_t* __restrict__ imgs, uint32_t* __restrict__ fc,
               float* __restrict__ dbg_logits, float* __restrict__ dbg_probs, uint16_t* __restrict__ dbg_freqs) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar[2];
   __shared__ uint32_t tslot;
   const int row = tile_row();
   typename EngineSel<PREC>::T eng;
-  engine_setup<PREC>(eng, smem, w, &bar, &tslot);
+  engine_setup<PREC>(eng, smem, w, bar, &tslot);
   const uint64_t total = (uint64_t)p.n_img * p.upi * p.tiles_per_unit;
   const bool dbg = dbg_logits || dbg_probs || dbg_freqs;
 #pragma unroll 1
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
              const uint32_t* __restrict__ sbase, const uint32_t* __restrict__ slen, uint8_t* __restrict__ out,
              int32_t* __restrict__ status, unsigned long long* __restrict__ prof) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar[2];
   __shared__ uint32_t tslot;
   __shared__ uint32_t s_cnt[4][2];  // per owner warp and pass parity: readers | active<<16
   const int row = tile_row();
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t S = rank * ROWS + (uint32_t)row;
 
   typename EngineSel<PREC>::T eng;
-  uint8_t* ring = engine_setup<PREC>(eng, smem, w, &bar, &tslot);
+  uint8_t* ring = engine_setup<PREC>(eng, smem, w, bar, &tslot);
   uint32_t* cursor = reinterpret_cast<uint32_t*>(ring + RING_BYTES + 16);  // 16 zero bytes after the ring
   uint32_t* s_sbase = cursor + ((un.ngroups + 3u) & ~3u);                   // per-group stream table
   uint32_t* s_slen = s_sbase + ((un.ngroups + 3u) & ~3u);
@@ -478,6 +478,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int wq = (int)(threadIdx.x >> 5);  // owner warp = quadrant (0..3)
   uint32_t x = 0;
   int err = 0;
+  int pix = 0;
 
   if (pf.on) pf.t = clock64();
 #pragma unroll 1
@@ -560,6 +561,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t slot = x & 0xFFFFu;
       uint32_t fs, cs;
       const int sym = q1_decode(eng, slot, fs, cs, &pf);
+      pix = sym;
       if (threadIdx.x < 128) {  // warps 0-3: rANS lanes in the lower half-warps
         bool need = false;
         if (act) {
@@ -608,7 +610,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         if (act && writer) cursor[g] = cur + total;
         if (act) {
-          oimg[(uint64_t)r * p.W + c] = (uint8_t)sym;
           const uint32_t bank = ((uint32_t)r >> ns_shift) & 1u;
           const uint32_t col = (uint32_t)c & 31u;
           ring[(bank * 32u + col) * RING_ROWS + (uint32_t)row + 8u] = (uint8_t)sym;
@@ -624,6 +625,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     if (NC > 1) cluster_sync_all();
     else __syncthreads();
+    // the pixel's HBM store after the barrier: its release need not wait for it
+    if (owner && active) oimg[(uint64_t)r * p.W + c] = (uint8_t)pix;
     pf.mark(10);
   }
   if (pf.on)
