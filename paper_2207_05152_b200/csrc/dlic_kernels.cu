@@ -222,25 +222,33 @@ __global__ void __launch_bounds__(128) k_rans_enc(Plan p, const uint32_t* __rest
   uint32_t n = 0;
   const int t_hi = 3 * (int)(r0 + nr - 1) + (int)un.w - 1;
   const int t_lo = 3 * (int)r0;
+  // Software pipeline: the (f, c) of the next 16 steps of this lane are
+  // independent loads (its row read backwards), issued together; the 16
+  // dependent encode steps then run from registers.
+  constexpr int CH = 16;
 #pragma unroll 1
-  for (int t = t_hi; t >= t_lo; --t) {
-    const int c = t - 3 * r;
-    const bool act = lane_ok && c >= 0 && c < (int)un.w;
-    uint32_t f = 1, cum = 0;
-    if (act) {
-      const uint32_t v = __ldg(frow + c);
-      f = v & 0xFFFFu;
-      cum = v >> 16;
+  for (int t0 = t_hi; t0 >= t_lo; t0 -= CH) {
+    uint32_t fcv[CH];
+#pragma unroll
+    for (int s = 0; s < CH; ++s) {
+      const int c = t0 - s - 3 * r;
+      const bool act = lane_ok && t0 - s >= t_lo && c >= 0 && c < (int)un.w;
+      fcv[s] = act ? __ldg(frow + c) : 0u;  // 0 = inactive (f >= 1 for real pixels)
     }
-    const bool emit = act && (x >> 16) >= f;  // x >= f * 2^16  (renormalise first, R6)
-    const uint32_t m = __ballot_sync(0xFFFFFFFFu, emit);
-    if (emit) {
-      const uint32_t k = n + __popc(m >> lane >> 1);  // lanes above emit first
-      region[cap - 1 - k] = (uint16_t)(x & 0xFFFFu);
-      x >>= 16;
+#pragma unroll
+    for (int s = 0; s < CH; ++s) {
+      const bool act = fcv[s] != 0u;
+      const uint32_t f = act ? (fcv[s] & 0xFFFFu) : 1u, cum = fcv[s] >> 16;
+      const bool emit = act && (x >> 16) >= f;  // x >= f * 2^16  (renormalise first, R6)
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, emit);
+      if (emit) {
+        const uint32_t kk = n + __popc(m >> lane >> 1);  // lanes above emit first
+        region[cap - 1 - kk] = (uint16_t)(x & 0xFFFFu);
+        x >>= 16;
+      }
+      n += __popc(m);
+      if (act) x = ((x / f) << 16) + (x % f) + cum;
     }
-    n += __popc(m);
-    if (act) x = ((x / f) << 16) + (x % f) + cum;
   }
   if (lane_ok) {
     region[2 * lane] = (uint16_t)(x >> 16);
