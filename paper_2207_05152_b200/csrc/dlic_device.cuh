@@ -495,10 +495,11 @@ struct Fp32Engine {
 
 // ------------------------------------------------- softmax -> Q1' -> CDF
 // Reading R5 (Q1'), per row; thread (j, h) owns logits [64j+32h, +32):
-//   m = max_i l_i ;  e_i = 2^(l_i*log2e - m*log2e) (MUFU ex2 or the FMA-pipe
-//   polynomial, fixed per column);  z_jh = (sum of even-position terms) +
-//   (sum of odd-position terms), each ascending;  Z_j = z_j0 + z_j1;
-//   Z = ((Z_0 + Z_1) + Z_2) + Z_3;  p_i = e_i * (1/Z) (RN);
+//   m_j = max over group j;  e_i = 2^(l_i*log2e - m_j*log2e) (MUFU ex2 or the
+//   FMA-pipe polynomial, fixed per column);  z_jh = (sum of even-position
+//   terms) + (sum of odd-position terms), each ascending;  z_j = z_j0 + z_j1;
+//   M = max_j m_j;  w_j = 2^(m_j*log2e - M*log2e);
+//   Z = ((z_0 w_0 + z_1 w_1) + z_2 w_2) + z_3 w_3;  p_i = e_i * (w_j * (1/Z));
 //   f_i = 1 + floor(p_i * 65279);  R = 2^16 - sum f_i >= 0 ; f_255 += R ;
 //   c_i = exclusive prefix sum.
 // Integers are carried as exact integer-valued floats (< 2^24).  The logit
@@ -550,7 +551,9 @@ __device__ __forceinline__ Q1Row q1_table(const Eng& e, int sym, float& fs, floa
   const int j = col_grp(), h = half_id();
   const int c0 = 64 * j + 32 * h;
   uint32_t v[32];
-  // pass 1: biased logits, stored back; max
+  // pass 1 (one TMEM round trip): biased logits, the group max m_j, and
+  // e_i = 2^(l_i*log2e - m_j*log2e) relative to the group max, stored back;
+  // z_j as even/odd pair partial sums, combined across the half-warps.
   e.ld32(v);
   float m = -INFINITY;
 #pragma unroll
@@ -562,20 +565,9 @@ __device__ __forceinline__ Q1Row q1_table(const Eng& e, int sym, float& fs, floa
     v[2 * q + 1] = __float_as_uint(l1);
     m = fmaxf(m, fmaxf(l0, l1));
   }
-  e.st32(v);
-  m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, 16));
-  if (pf) pf->mark(4);
-  e.xput(0, __float_as_uint(m));
-  e.xsync();
-  uint32_t x4[4];
-  e.xget4(0, x4);
-  m = fmaxf(fmaxf(__uint_as_float(x4[0]), __uint_as_float(x4[1])),
-            fmaxf(__uint_as_float(x4[2]), __uint_as_float(x4[3])));
-  if (pf) pf->mark(5);
+  m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, 16));  // m_j, equal in both halves
   const f2 nm = f2_splat(__fmul_rn(-m, LOG2E));
   const f2 l2e = f2_splat(LOG2E);
-  // pass 2: e_i stored back; z as even/odd pair partial sums
-  e.ld32(v);
   f2 zz = f2_splat(0.0f);
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
@@ -598,15 +590,31 @@ __device__ __forceinline__ Q1Row q1_table(const Eng& e, int sym, float& fs, floa
   f2_split(zz, za, zb);
   float z = __fadd_rn(za, zb);
   z = __fadd_rn(z, __shfl_xor_sync(0xFFFFFFFFu, z, 16));  // commutative: identical in both halves
-  if (pf) pf->mark(6);
+  if (pf) pf->mark(4);
+  e.xput(0, __float_as_uint(m));
   e.xput(1, __float_as_uint(z));
   e.xsync();
-  e.xget4(1, x4);
-  const float Z = __fadd_rn(__fadd_rn(__fadd_rn(__uint_as_float(x4[0]), __uint_as_float(x4[1])),
-                                      __uint_as_float(x4[2])),
-                            __uint_as_float(x4[3]));
+  uint32_t x4[4], z4[4];
+  e.xget4(0, x4);
+  e.xget4(1, z4);
+  // M = max_j m_j;  Z = sum_j z_j 2^(m_j - M) in a fixed order;  group scale
+  // s_j = 2^(m_j - M) / Z, so p_i = e_i * s_j = exp(l_i - M) / Z.
+  const float M = fmaxf(fmaxf(__uint_as_float(x4[0]), __uint_as_float(x4[1])),
+                        fmaxf(__uint_as_float(x4[2]), __uint_as_float(x4[3])));
+  const float nM = __fmul_rn(-M, LOG2E);
+  float wg[4];
+#pragma unroll
+  for (int g = 0; g < NGRP; ++g) wg[g] = ex2_approx(__fmaf_rn(__uint_as_float(x4[g]), LOG2E, nM));
+  const float Z = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(__uint_as_float(z4[0]), wg[0]),
+                                                __fmul_rn(__uint_as_float(z4[1]), wg[1])),
+                                      __fmul_rn(__uint_as_float(z4[2]), wg[2])),
+                            __fmul_rn(__uint_as_float(z4[3]), wg[3]));
+  float wmine = wg[0];
+#pragma unroll
+  for (int g = 1; g < NGRP; ++g)
+    if (g == j) wmine = wg[g];
+  const f2 inv = f2_splat(__fmul_rn(wmine, __frcp_rn(Z)));
   if (pf) pf->mark(5);
-  const f2 inv = f2_splat(__frcp_rn(Z));
   const f2 scale = f2_splat(Q1_SCALE);
   const f2 two23 = f2_splat(8388608.0f);
   const f2 fbias = f2_splat(-8388607.0f);  // y - 2^23 + 1 = 1 + floor(x), exact
