@@ -246,6 +246,12 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -311,12 +317,21 @@ __device__ __forceinline__ f2 f2_fma(f2 a, f2 b, f2 c) {
 // Optional phase profiler (debug: thread 0, clock64 deltas).
 struct Prof {
   unsigned long long t = 0, acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long t2 = 0, acc2[4] = {0, 0, 0, 0};
   bool on = false;
   __device__ __forceinline__ void mark(int k) {
     if (on) {
       const unsigned long long n = clock64();
       acc[k] += n - t;
       t = n;
+      t2 = n;
+    }
+  }
+  __device__ __forceinline__ void mark2(int k) {  // sub-phases of the network
+    if (on) {
+      const unsigned long long n = clock64();
+      acc2[k] += n - t2;
+      t2 = n;
     }
   }
 };
@@ -346,7 +361,8 @@ struct TcEngine {
   }
 
   // Runs the 6 layers (M=64); the input must have been stored with put_input.
-  __device__ void run() {
+  // pf (debug): 0 sync, 1 issue, 2 mma wait, 3 epilogue (accumulated in acc[8..11]... see below)
+  __device__ void run(Prof* pf = nullptr) {
     const uint32_t lo = lane_off();
     const int j = col_grp(), h = half_id();
     tc_wait_st();
@@ -354,6 +370,7 @@ struct TcEngine {
     for (int l = 0; l < NLAYER; ++l) {
       tc_fence_before();
       __syncthreads();
+      if (pf) pf->mark2(0);
       if (threadIdx.x == 0) {
         tc_fence_after();
         const int K = layer_k(l), N = layer_n(l);
@@ -371,9 +388,11 @@ struct TcEngine {
         }
         umma_commit(bar);
       }
+      if (pf) pf->mark2(1);
       mbar_wait(bar, phase);
       phase ^= 1u;
       tc_fence_after();
+      if (pf) pf->mark2(2);
       if (l < NLAYER - 1) {  // bias + ReLU + bf16 -> next A; columns [32j+16h, +16)
         const float2* b2 = reinterpret_cast<const float2*>(bias + l * HID + 32 * j + 16 * h);
         uint32_t v[16];
@@ -390,6 +409,7 @@ struct TcEngine {
         // packed column 16j+8h+q holds activations 32j+16h+2q, +1: identity K order
         tmem_st8h<8>(tmem + lo + TM_A + 16u * (uint32_t)j, p);
         tc_wait_st();
+        if (pf) pf->mark2(3);
       }
     }
   }

@@ -570,6 +570,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       uint32_t fs, cs;
       const int sym = q1_decode(eng, slot, fs, cs, &pf);
       pix = sym;
+      // publish the pixel first (own ring; the successor's halo through DSMEM
+      // for the CTA's last 8 rows) so the stores have landed by the time the
+      // end-of-front cluster barrier's release executes
+      if (owner && active) {
+        const uint32_t bank = ((uint32_t)r >> ns_shift) & 1u;
+        const uint32_t col = (uint32_t)c & 31u;
+        ring[(bank * 32u + col) * RING_ROWS + (uint32_t)row + 8u] = (uint8_t)sym;
+        if (row >= ROWS - 8) {
+          const uint32_t hoff = (bank * 32u + col) * RING_ROWS + (uint32_t)(row - (ROWS - 8));
+          if (NC > 1) st_cluster_u8(halo_base + hoff, (uint32_t)sym);
+          else ring[hoff] = (uint8_t)sym;
+        }
+      }
       if (threadIdx.x < 128) {  // warps 0-3: rANS lanes in the lower half-warps
         bool need = false;
         if (act) {
@@ -617,17 +630,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           else err = 8;
         }
         if (act && writer) cursor[g] = cur + total;
-        if (act) {
-          const uint32_t bank = ((uint32_t)r >> ns_shift) & 1u;
-          const uint32_t col = (uint32_t)c & 31u;
-          ring[(bank * 32u + col) * RING_ROWS + (uint32_t)row + 8u] = (uint8_t)sym;
-          if (row >= ROWS - 8) {
-            const uint32_t hoff = (bank * 32u + col) * RING_ROWS + (uint32_t)(row - (ROWS - 8));
-            if (NC > 1) st_cluster_u8(halo_base + hoff, (uint32_t)sym);
-            else ring[hoff] = (uint8_t)sym;
-          }
-          if (c == uw - 1 && x != RANS_L) err = 6;  // end-of-lane invariant
-        }
+        if (act && c == uw - 1 && x != RANS_L) err = 6;  // end-of-lane invariant
       }
       pf.mark(9);
     }
