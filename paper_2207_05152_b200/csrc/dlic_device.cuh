@@ -562,15 +562,16 @@ __device__ __forceinline__ f2 f2_exp2_poly(f2 t) {
   return f2_bits(r0, r1);
 }
 
-// Passes 1, 2, A.  ENC: also returns f and the half-local exclusive cum of
-// `sym` when it lies in this thread's columns.  probs (nullable): p_i of the
+// Passes 1 and A over this thread's 32 values, held in registers throughout:
+// v = raw logits on entry (ld32), the integer table f (as floats) on return.
+// ENC: also returns f and the half-local exclusive cum of `sym` when it lies in
+// this thread's columns.  probs (nullable): p_i of the
 // row (debug export, 256 entries).
 template <bool ENC, class Eng>
-__device__ __forceinline__ Q1Row q1_table(const Eng& e, int sym, float& fs, float& cs_local, float* probs,
-                                          Prof* pf = nullptr) {
+__device__ __forceinline__ Q1Row q1_table(const Eng& e, uint32_t (&v)[32], int sym, float& fs, float& cs_local,
+                                          float* probs, Prof* pf = nullptr) {
   const int j = col_grp(), h = half_id();
   const int c0 = 64 * j + 32 * h;
-  uint32_t v[32];
   // pass 1 (one TMEM round trip): biased logits, the group max m_j, and
   // e_i = 2^(l_i*log2e - m_j*log2e) relative to the group max, stored back;
   // z_j as even/odd pair partial sums, combined across the half-warps.
@@ -605,7 +606,6 @@ __device__ __forceinline__ Q1Row q1_table(const Eng& e, int sym, float& fs, floa
     v[2 * q] = __float_as_uint(e0);
     v[2 * q + 1] = __float_as_uint(e1);
   }
-  e.st32(v);
   float za, zb;
   f2_split(zz, za, zb);
   float z = __fadd_rn(za, zb);
@@ -639,8 +639,7 @@ __device__ __forceinline__ Q1Row q1_table(const Eng& e, int sym, float& fs, floa
   const f2 two23 = f2_splat(8388608.0f);
   const f2 fbias = f2_splat(-8388607.0f);  // y - 2^23 + 1 = 1 + floor(x), exact
   // pass A: p_i, f_i = 1 + floor(p_i * 65279) (x + 2^23 rounded toward -inf
-  // has ulp 1), stored back as floats; half sum
-  e.ld32(v);
+  // has ulp 1), kept in v as floats; half sum
   f2 FF = f2_splat(0.0f);
   fs = 0.0f;
   cs_local = 0.0f;
@@ -673,7 +672,6 @@ __device__ __forceinline__ Q1Row q1_table(const Eng& e, int sym, float& fs, floa
     v[2 * q] = __float_as_uint(f0);
     v[2 * q + 1] = __float_as_uint(f1);
   }
-  e.st32(v);
   float Fa, Fb;
   f2_split(FF, Fa, Fb);
   Q1Row r;
@@ -700,11 +698,8 @@ __device__ __forceinline__ float q1_base(const Q1Row& r) {
 }
 
 // Final integer table of this thread's 32 columns (debug export).
-template <class Eng>
-__device__ __forceinline__ void q1_store_freqs(const Eng& e, const Q1Row& r, uint16_t* freqs) {
+__device__ __forceinline__ void q1_store_freqs(const uint32_t (&v)[32], const Q1Row& r, uint16_t* freqs) {
   const int c0 = 64 * col_grp() + 32 * half_id();
-  uint32_t v[32];
-  e.ld32(v);  // all lanes load (tcgen05.ld is .sync.aligned)
   if (freqs) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
@@ -721,8 +716,10 @@ template <class Eng>
 __device__ __forceinline__ uint32_t q1_encode(const Eng& e, int sym, float* probs = nullptr,
                                               uint16_t* freqs = nullptr, bool export_freqs = false) {
   float fs, csl;
-  const Q1Row r = q1_table<true>(e, sym, fs, csl, probs);
-  if (export_freqs) q1_store_freqs(e, r, freqs);
+  uint32_t v[32];
+  e.ld32(v);
+  const Q1Row r = q1_table<true>(e, v, sym, fs, csl, probs);
+  if (export_freqs) q1_store_freqs(v, r, freqs);
   const int c0 = 64 * col_grp() + 32 * half_id();
   uint32_t packed = 0;
   if (sym >= c0 && sym < c0 + 32) {
@@ -748,7 +745,9 @@ __device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot0, uint32_t&
                                          Prof* pf = nullptr) {
   float fs, csl;
   e.xput(6, __shfl_sync(0xFFFFFFFFu, slot0, threadIdx.x & 15));
-  const Q1Row r = q1_table<false>(e, -1, fs, csl, nullptr, pf);
+  uint32_t v[32];
+  e.ld32(v);
+  const Q1Row r = q1_table<false>(e, v, -1, fs, csl, nullptr, pf);
   uint32_t s4[4];
   e.xget4(6, s4);
   const float slot = (float)s4[0];
@@ -758,8 +757,6 @@ __device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot0, uint32_t&
   const bool mine = slot >= base && slot < cum;
   int sym = 0;
   float fsel = 0.0f, csel = 0.0f;
-  uint32_t v[32];
-  e.ld32(v);
 #pragma unroll
   for (int i = 31; i >= 0; --i) {
     float f = __uint_as_float(v[i]);
