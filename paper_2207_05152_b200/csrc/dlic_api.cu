@@ -229,7 +229,8 @@ dlic_status upload_model(dlic_model* m, const ParsedModel& pm) {
     const int K = layer_k(l), N = layer_n(l), Kr = (int)pm.dims[l];
     for (int k = 0; k < K; ++k)
       for (int n = 0; n < N; ++n) {
-        const float v = k < Kr ? pm.W[l][(size_t)k * N + n] : 0.0f;
+        const int kt = l == 0 ? kpos_tap(k) : k;  // layer 1: the engine's K order
+        const float v = kt >= 0 && kt < Kr ? pm.W[l][(size_t)kt * N + n] : 0.0f;
         const uint16_t u = bf16_bits(v);
         const size_t a = wimg_off(l) + (size_t)(k / 8) * (N / 8) * 128 + (size_t)(n / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
         memcpy(&img[a], &u, 2);

@@ -40,6 +40,18 @@ constexpr uint32_t RANS_L = 1u << 16;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float Q1_SCALE = 65279.0f;  // 2^16 - 257 (R5, Q1')
 
+// Layer-1 K order of the bf16 engine.  K position p = 10u + i belongs to
+// thread u = 2j + h (column group j, half h), which feeds A packed columns
+// [5u, 5u + 5).  Thread u owns window row dr = u - 8 (i < 9: dc = i - 6) and
+// one tap of the target row (i = 9, u < 6: dc = u - 6); positions 69 and 79
+// are zero pads.  With this order every tap of a thread is a fixed offset from
+// one per-thread ring address (decoder gather).  Returns the R1 row-major
+// tap index of position p, or -1 for a pad; the host packer permutes
+// W1's rows the same way, so the product is unchanged.
+__host__ __device__ constexpr int kpos_tap(int p) {
+  return p % 10 < 9 ? 9 * (p / 10) + p % 10 : (p / 10 < 6 ? 72 + p / 10 : -1);
+}
+
 // bf16 weight image (bytes) per layer, core-matrix layout (see host packer)
 __host__ __device__ constexpr int layer_k(int l) { return l == 0 ? KPAD : HID; }
 __host__ __device__ constexpr int layer_n(int l) { return l == NLAYER - 1 ? NOUT : HID; }

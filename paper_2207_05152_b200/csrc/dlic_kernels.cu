@@ -21,16 +21,21 @@
 
 namespace dlic {
 
-// window offset j (row-major over the 9x9 box, causal cells only; R1)
-__device__ __forceinline__ int off_dr(int j) { return j < 72 ? j / 9 - 8 : 0; }
-__device__ __forceinline__ int off_dc(int j) { return j < 72 ? j % 9 - 6 : j - 78; }
-
 // Decoded-pixel ring, column-major so the 32 lanes of a warp (consecutive
-// rows) touch distinct shared-memory banks: byte (bank, col, ringrow) at
-// (bank*32 + col)*RING_ROWS + ringrow; ringrow = 8 + slot-in-CTA, rows 0..7
-// mirror the previous CTA's last 8 slots (halo).
-constexpr int RING_ROWS = ROWS + 8;                  // own 64 slots + 8 halo rows
-constexpr uint32_t RING_BYTES = 2u * RING_ROWS * 32u;  // 2 banks x 32 cols x 72 rows
+// rows) touch distinct shared-memory banks: byte (bank, pos, ringrow) at
+// bank*RING_BANK + pos*RING_ROWS + ringrow.  ringrow = 8 + slot-in-CTA; rows
+// 0..7 mirror the previous CTA's last 8 slots (halo).  bank = pass parity of
+// the READER's row (the wrap-around halo, written by the last CTA for the
+// first CTA's next pass, flips it).  Column c lives at pos c & 31 and, for
+// c & 31 < 8, also at pos 32 + (c & 31), so a window (dc in [-6, 2]) never
+// wraps: it is read from pos cb + dc with cb = (c & 31) < 6 ? (c & 31) + 32 :
+// (c & 31).  Out-of-image taps read zeros that the writers keep in place: the
+// ring starts zeroed, a row clears its right pad (columns W, W+1) when it
+// ends and the left pad (pos 26..31) of its slot's next row in the other bank.
+constexpr int RING_ROWS = ROWS + 8;                           // own 64 slots + 8 halo rows
+constexpr int RING_COLS = 40;                                 // 32-column ring + copies of 0..7
+constexpr uint32_t RING_BANK = (uint32_t)RING_COLS * RING_ROWS;  // 2880
+constexpr uint32_t RING_BYTES = 2u * RING_BANK;               // 5760
 constexpr uint32_t F32_BUF_BYTES = (NOUT + HID) * ROWS * 4u;          // 98304
 constexpr uint32_t F32_X_BYTES = NXSLOT * NGRP * ROWS * 4u;          // 7168
 constexpr uint32_t MAX_DYN_SMEM = 232448 - 64;                       // 227 KB minus static
@@ -102,42 +107,45 @@ __device__ __forceinline__ void engine_teardown(typename EngineSel<PREC>::T& eng
   }
 }
 
-// Feed this thread's share of the 78 (80) window inputs: thread (j, h) owns
-// inputs [20j+10h, +10) = A packed columns [10j+5h, +5); get(dr, dc) returns
-// the pixel value of that window offset (0 fill).  Offsets come from the tap
-// index with a multiply-shift division by 9 (exact for k < 80).
-__device__ __forceinline__ void tap_offset(int k, int& dr, int& dc) {
-  const int q9 = (k * 57) >> 9;  // k / 9
-  dr = q9 - 8;
-  dc = k - 9 * q9 - 6;
+// Feed this thread's share of the window inputs (encoder; the decoder has its
+// own ring gather).  bf16: thread u = 2j + h owns K positions [10u, +10) in
+// the kpos_tap order; get(dr, dc) returns the pixel value of that window
+// offset (0 fill).  fp32: the same taps, stored at their R1 index.
+__device__ __forceinline__ void tap_of(int u, int i, int& dr, int& dc) {
+  if (i < 9) {
+    dr = u - 8;
+    dc = i - 6;
+  } else {
+    dr = 0;
+    dc = u - 6;
+  }
 }
 template <int PREC, class Eng, class Get>
 __device__ __forceinline__ void feed(const Eng& eng, Get get) {
-  const int kb = 20 * col_grp() + 10 * half_id();
+  const int u = 2 * col_grp() + half_id();
   if constexpr (PREC == 1) {
     // v/256 exactly: (1 + v/256) has v in the top 8 mantissa bits; minus 1 is exact.
     const f2 m1 = f2_make(-1.0f, -1.0f);
     uint32_t a[5];
 #pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      const int k0 = kb + 2 * i;
+    for (int q = 0; q < 5; ++q) {
       int dr0, dc0, dr1, dc1;
-      tap_offset(k0, dr0, dc0);
-      tap_offset(k0 + 1, dr1, dc1);
-      const uint32_t v0 = k0 < KIN ? get(dr0, dc0) : 0u;
-      const uint32_t v1 = k0 + 1 < KIN ? get(dr1, dc1) : 0u;
+      tap_of(u, 2 * q, dr0, dc0);
+      tap_of(u, 2 * q + 1, dr1, dc1);
+      const uint32_t v0 = get(dr0, dc0);
+      const uint32_t v1 = (q < 4 || u < 6) ? get(dr1, dc1) : 0u;
       float x0, x1;
       f2_split(f2_add(f2_bits(0x3F800000u | (v0 << 15), 0x3F800000u | (v1 << 15)), m1), x0, x1);
-      a[i] = pack_bf16(x0, x1);
+      a[q] = pack_bf16(x0, x1);
     }
     eng.put_input(a);
   } else {
 #pragma unroll
     for (int i = 0; i < 10; ++i) {
-      const int k = kb + i;
       int dr, dc;
-      tap_offset(k, dr, dc);
-      if (k < KIN) eng.put_input(k, __fadd_rn(__uint_as_float(0x3F800000u | (get(dr, dc) << 15)), -1.0f));
+      tap_of(u, i, dr, dc);
+      if (i < 9 || u < 6)
+        eng.put_input(i < 9 ? 9 * u + i : 72 + u, __fadd_rn(__uint_as_float(0x3F800000u | (get(dr, dc) << 15)), -1.0f));
     }
   }
 }
@@ -438,7 +446,7 @@ __global__ void k_dec_prep(Plan p, const uint8_t* __restrict__ bits, const uint6
 // update, interleaved word reads (ballot/popc within a warp; a G = 32 group
 // spans two warps and adds the first warp's count through shared memory),
 // pixel publication to HBM, the ring and the next CTA's halo (DSMEM).
-template <int PREC>
+template <int PREC, bool PROF>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_decode(Plan p, DevWeights w, const uint8_t* __restrict__ bits, const uint64_t* __restrict__ cont_off,
              const uint32_t* __restrict__ sbase, const uint32_t* __restrict__ slen, uint8_t* __restrict__ out,
@@ -455,7 +463,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // optional phase profile (thread 0 of each CTA), see Prof in dlic_device.cuh:
   // 0 top 1 gather 2 put 3 mlp 4 pass1 5 exchanges 6 pass2 7 passA 8 search 9 rans 10 barrier
   Prof pf;
-  pf.on = prof != nullptr && threadIdx.x == 0;
+  pf.on = PROF && threadIdx.x == 0;
   const uint32_t rank = NC > 1 ? cluster_rank() : 0u;
   const uint32_t u = blockIdx.x / NC;
   const Unit un = unit_info(p, u);
@@ -466,7 +474,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint32_t* cursor = reinterpret_cast<uint32_t*>(ring + RING_BYTES + 16);  // 16 zero bytes after the ring
   uint32_t* s_sbase = cursor + ((un.ngroups + 3u) & ~3u);                   // per-group stream table
   uint32_t* s_slen = s_sbase + ((un.ngroups + 3u) & ~3u);
-  if (threadIdx.x < 16) ring[RING_BYTES + threadIdx.x] = 0;
+  for (uint32_t i = threadIdx.x; i < RING_BYTES / 16; i += NTHREADS)
+    reinterpret_cast<int4*>(ring)[i] = make_int4(0, 0, 0, 0);
   const uint32_t G = p.G;
   const uint32_t g_shift = (uint32_t)(__ffs((int)G) - 1);
   for (uint32_t g = threadIdx.x; g < un.ngroups; g += NTHREADS) {
@@ -481,6 +490,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint8_t* oimg = out + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
   const uint32_t ring_s = smem_u32(ring);
   const uint32_t halo_base = NC > 1 ? map_cluster(ring_s, (rank + 1) % NC) : ring_s;
+  const uint32_t halo_flip = rank == NC - 1 ? 1u : 0u;  // wrap-around halo feeds the next pass
+  // gather: thread u = 2j + h reads window row dr = u - 8 at ringrow row + u
+  // and (u < 6) the target-row tap dc = u - 6 at ringrow row + 8 (kpos_tap)
+  const int gu = 2 * col_grp() + half_id();
+  const int g9 = gu < 6 ? (8 - gu) + (gu - 6) * RING_ROWS : 0;
   const int uw = (int)un.w, uh = (int)un.h;
   const int T = uw + 3 * (uh - 1);
   const int wq = (int)(threadIdx.x >> 5);  // owner warp = quadrant (0..3)
@@ -552,15 +566,33 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (i + 1 < my_sl) x = ((uint32_t)__ldg(sw + i) << 16) | (uint32_t)__ldg(sw + i + 1);
         else err = 8;
       }
-      // window gather from the ring (rows r-8..r of this slot's neighbourhood)
-      auto get = [&](int dr, int dc) -> uint32_t {  // branch-free: invalid taps read a zero byte
-        const int rr = r + dr, cc = c + dc;
-        const bool ok = active && rr >= 0 && (unsigned)cc < (unsigned)uw;
-        const uint32_t bank = ((uint32_t)rr >> ns_shift) & 1u;
-        const uint32_t a = (bank * 32u + ((uint32_t)cc & 31u)) * RING_ROWS + (uint32_t)(row + dr + 8);
-        return ring[ok ? a : RING_BYTES];
-      };
-      feed<PREC>(eng, get);
+      // window gather from the ring: one load per tap, no bounds tests
+      {
+        const uint32_t col = (uint32_t)c & 31u;
+        const uint32_t cb = col < 6u ? col + 32u : col;
+        const uint8_t* bp = ring + (((uint32_t)r >> ns_shift) & 1u) * RING_BANK + cb * RING_ROWS + (uint32_t)(row + gu);
+        uint32_t tv[10];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) tv[i] = bp[(i - 6) * RING_ROWS];
+        tv[9] = bp[g9];
+        if constexpr (PREC == 1) {
+          const f2 m1 = f2_make(-1.0f, -1.0f);
+          uint32_t a[5];
+#pragma unroll
+          for (int q = 0; q < 5; ++q) {
+            float x0, x1;
+            f2_split(f2_add(f2_bits(0x3F800000u | (tv[2 * q] << 15), 0x3F800000u | (tv[2 * q + 1] << 15)), m1), x0,
+                     x1);
+            a[q] = pack_bf16(x0, x1);
+          }
+          eng.put_input(a);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 10; ++i)
+            if (i < 9 || gu < 6)
+              eng.put_input(i < 9 ? 9 * gu + i : 72 + gu, __fadd_rn(__uint_as_float(0x3F800000u | (tv[i] << 15)), -1.0f));
+        }
+      }
       pf.mark(1);
       if constexpr (PREC == 1) tc_wait_st();
       pf.mark(2);
@@ -576,11 +608,37 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (owner && active) {
         const uint32_t bank = ((uint32_t)r >> ns_shift) & 1u;
         const uint32_t col = (uint32_t)c & 31u;
-        ring[(bank * 32u + col) * RING_ROWS + (uint32_t)row + 8u] = (uint8_t)sym;
-        if (row >= ROWS - 8) {
-          const uint32_t hoff = (bank * 32u + col) * RING_ROWS + (uint32_t)(row - (ROWS - 8));
-          if (NC > 1) st_cluster_u8(halo_base + hoff, (uint32_t)sym);
-          else ring[hoff] = (uint8_t)sym;
+        uint8_t* rp = ring + (uint32_t)row + 8u;
+        rp[bank * RING_BANK + col * RING_ROWS] = (uint8_t)sym;
+        if (col < 8u) rp[bank * RING_BANK + (col + 32u) * RING_ROWS] = (uint8_t)sym;
+        const bool halo = row >= ROWS - 8;
+        const uint32_t hb = bank ^ halo_flip;
+        const uint32_t hrow = (uint32_t)(row - (ROWS - 8));
+        auto hput = [&](uint32_t b, uint32_t pos, uint32_t v) {
+          const uint32_t off = b * RING_BANK + pos * RING_ROWS + hrow;
+          if (NC > 1) st_cluster_u8(halo_base + off, v);
+          else ring[off] = (uint8_t)v;
+        };
+        if (halo) {
+          hput(hb, col, (uint32_t)sym);
+          if (col < 8u) hput(hb, col + 32u, (uint32_t)sym);
+        }
+        if (c == uw - 1) {  // row end: right pad of this row, left pad of the slot's next row
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const uint32_t pc = (uint32_t)(uw + e) & 31u;
+            rp[bank * RING_BANK + pc * RING_ROWS] = 0;
+            if (pc < 8u) rp[bank * RING_BANK + (pc + 32u) * RING_ROWS] = 0;
+            if (halo) {
+              hput(hb, pc, 0u);
+              if (pc < 8u) hput(hb, pc + 32u, 0u);
+            }
+          }
+#pragma unroll
+          for (uint32_t pc = 26; pc < 32; ++pc) {
+            rp[(bank ^ 1u) * RING_BANK + pc * RING_ROWS] = 0;
+            if (halo) hput(hb ^ 1u, pc, 0u);
+          }
         }
       }
       if (threadIdx.x < 128) {  // warps 0-3: rANS lanes in the lower half-warps
@@ -698,13 +756,13 @@ cudaError_t launch_dec_prep(const Plan& p, const uint8_t* d_bits, const uint64_t
   return cudaGetLastError();
 }
 
-template <int PREC>
+template <int PREC, bool PROF>
 static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uint8_t* d_bits,
                                    const uint64_t* d_cont_off, const uint32_t* d_sbase, const uint32_t* d_slen,
                                    uint8_t* d_imgs, int32_t* d_status, cudaStream_t st,
                                    unsigned long long* prof) {
   const size_t sm = dec_smem_bytes(PREC, p.gpt > p.gpl ? p.gpt : p.gpl);
-  cudaError_t e = set_smem(k_decode<PREC>, sm);
+  cudaError_t e = set_smem(k_decode<PREC, PROF>, sm);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.n_img * p.upi * p.nc);
@@ -712,7 +770,7 @@ static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uin
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
   if (p.nc > 8) {
-    e = cudaFuncSetAttribute(k_decode<PREC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(k_decode<PREC, PROF>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchAttribute at[1];
@@ -722,16 +780,21 @@ static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uin
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_decode<PREC>, p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status,
+  return cudaLaunchKernelEx(&cfg, k_decode<PREC, PROF>, p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status,
                             prof);
 }
 
 cudaError_t launch_decode(const Plan& p, const DevWeights& w, const uint8_t* d_bits, const uint64_t* d_cont_off,
                           const uint32_t* d_sbase, const uint32_t* d_slen, uint8_t* d_imgs, int32_t* d_status,
                           cudaStream_t st, unsigned long long* prof) {
+  if (prof) {
+    if (p.precision == 1)
+      return launch_decode_t<1, true>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof);
+    return launch_decode_t<0, true>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof);
+  }
   if (p.precision == 1)
-    return launch_decode_t<1>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof);
-  return launch_decode_t<0>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof);
+    return launch_decode_t<1, false>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof);
+  return launch_decode_t<0, false>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof);
 }
 
 }  // namespace dlic
