@@ -373,7 +373,60 @@ struct TcEngine {
   }
 
   // Runs the 6 layers (M=64); the input must have been stored with put_input.
-  // pf (debug): 0 sync, 1 issue, 2 mma wait, 3 epilogue (accumulated in acc[8..11]... see below)
+  // hook(l) runs (all threads) after layer l's MMAs are issued, before the
+  // wait for them: work that overlaps the tensor core.
+  // The MMAs are issued by thread MMA_ISSUER (warp 8), outside the warps that
+  // run hook work.
+  static constexpr unsigned MMA_ISSUER = 256;
+  template <class Hook>
+  __device__ __forceinline__ void run(Hook&& hook) {
+    const uint32_t lo = lane_off();
+    const int j = col_grp(), h = half_id();
+    tc_wait_st();
+#pragma unroll 1
+    for (int l = 0; l < NLAYER; ++l) {
+      tc_fence_before();
+      __syncthreads();
+      if (threadIdx.x == MMA_ISSUER) {
+        tc_fence_after();
+        const int K = layer_k(l), N = layer_n(l);
+        const uint32_t id = umma_idesc(64, N);
+        const uint32_t lbo = (uint32_t)N * 16u;                 // next 8-wide K core matrix
+        const uint32_t kstep = 2u * (uint32_t)(N / 8) * 128u;   // one K=16 slice
+        uint64_t bd = umma_desc(wsmem + wimg_off(l), lbo, 128u);
+        uint32_t at = tmem + TM_A;
+        umma_ts(tmem + TM_D, at, bd, id, 0u);
+        for (int kk = 1; kk < K / 16; ++kk) {
+          bd += kstep >> 4;
+          at += 8u;
+          umma_ts(tmem + TM_D, at, bd, id, 1u);
+        }
+        umma_commit(bar);
+      }
+      hook(l);
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+      tc_fence_after();
+      if (l < NLAYER - 1) {
+        const float2* b2 = reinterpret_cast<const float2*>(bias + l * HID + 32 * j + 16 * h);
+        uint32_t v[16];
+        tmem_ld16h<16>(tmem + lo + TM_D + 32u * (uint32_t)j, v);
+        tc_wait_ld();
+        uint32_t p[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float2 b = b2[q];
+          float x0, x1;
+          f2_split(f2_add(f2_bits(v[2 * q], v[2 * q + 1]), f2_make(b.x, b.y)), x0, x1);
+          p[q] = pack_bf16_relu(x0, x1);
+        }
+        tmem_st8h<8>(tmem + lo + TM_A + 16u * (uint32_t)j, p);
+        tc_wait_st();
+      }
+    }
+  }
+
+  // pf (debug): 0 sync, 1 issue, 2 mma wait, 3 epilogue (accumulated in acc2)
   __device__ void run(Prof* pf = nullptr) {
     const uint32_t lo = lane_off();
     const int j = col_grp(), h = half_id();
@@ -463,6 +516,12 @@ struct Fp32Engine {
 
   __device__ __forceinline__ void put_input(int k, float x) const { buf0[k * ROWS + tile_row()] = x; }
 
+  template <class Hook>
+  __device__ __forceinline__ void run(Hook&& hook) {
+#pragma unroll 1
+    for (int l = 0; l < NLAYER; ++l) hook(l);
+    run();
+  }
   __device__ void run() {
     const int t = tile_row(), j = col_grp(), h = half_id();
 #pragma unroll 1

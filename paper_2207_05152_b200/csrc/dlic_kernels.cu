@@ -501,6 +501,125 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint32_t x = 0;
   int err = 0;
   int pix = 0;
+  // The rANS step of a front is applied one front late, inside the next
+  // front's network (while warps 0-3 would wait on the layer-0/1 MMAs): the
+  // state it produces is first needed by that front's symbol search.
+  //   p_*    the previous front's result of this slot (owners)
+  //   pw0/1  stream words prefetched for it; my_cur/my_sl its group's cursor/length
+  bool p_act = false;
+  int p_r = 0, p_c = 0;
+  uint32_t p_fs = 0, p_cs = 0, p_slot = 0;
+  uint32_t pw0 = 0, pw1 = 0, first_lane = 0, my_sl = 0, my_cur = 0;
+
+  // (a) x' = f*(x>>16) + slot - c for the previous front's rows, renormalised
+  // with interleaved word reads (ballot/popc within a warp; a G = 32 group
+  // spans two warps and adds the first warp's count through shared memory).
+  auto rans_apply = [&]() {
+    if (threadIdx.x >= 128) return;
+    const bool act = owner && p_act;
+    const uint32_t g = (uint32_t)p_r >> g_shift;  // G is a power of two dividing 32
+    const uint32_t bk = ((uint32_t)p_r >> ns_shift) & 1u;  // pass parity over the slots
+    bool need = false;
+    if (act) {
+      x = p_fs * (x >> 16) + p_slot - p_cs;
+      need = x < RANS_L;
+    }
+    const uint32_t key = act ? g : (0x80000000u | lane);
+    const uint32_t gm = __match_any_sync(0xFFFFFFFFu, key);
+    // A warp may hold rows of two groups at once: one finishing and one of
+    // the next pass over the slots (rows NS apart).  They differ in the
+    // pass parity bk, which keys the cross-warp counts below.
+    const uint32_t nb0 = __ballot_sync(0xFFFFFFFFu, need && bk == 0);
+    const uint32_t nb1 = __ballot_sync(0xFFFFFFFFu, need && bk == 1);
+    const uint32_t a0 = __ballot_sync(0xFFFFFFFFu, act && bk == 0);
+    const uint32_t a1 = __ballot_sync(0xFFFFFFFFu, act && bk == 1);
+    const uint32_t readers = (nb0 | nb1) & gm;
+    const uint32_t nmine = __popc(readers);  // this warp's readers of my group
+    if (lane == 0) {
+      s_cnt[wq][0] = __popc(nb0) | (a0 ? 0x10000u : 0u);
+      s_cnt[wq][1] = __popc(nb1) | (a1 ? 0x10000u : 0u);
+    }
+    asm volatile("bar.sync 5, 128;" ::: "memory");
+    // G = 32: rows of the group's upper 16 (odd warp) read after the even warp's
+    uint32_t before = 0, total = nmine;
+    bool writer = lane == (uint32_t)(__ffs(gm) - 1);
+    if (G == 32) {
+      const uint32_t other = s_cnt[wq ^ 1][bk];
+      if (wq & 1) {
+        before = other & 0xFFFFu;
+        total = before + nmine;
+      } else {
+        total = nmine + (other & 0xFFFFu);
+        writer = writer && !(other & 0x10000u);  // the odd warp writes when it is active
+      }
+    }
+    const uint32_t rk = __popc(readers & ((1u << lane) - 1u));
+    // word from the prefetch registers (all lanes take part in the shuffles)
+    const uint32_t src = G == 32 ? (before + rk) & 31u : (first_lane + rk) & 31u;
+    const uint32_t w0 = __shfl_sync(0xFFFFFFFFu, pw0, src);
+    const uint32_t w1 = __shfl_sync(0xFFFFFFFFu, pw1, src);
+    if (need) {
+      const uint32_t wi = my_cur + before + rk;
+      if (wi < my_sl) x = (x << 16) | (G == 32 && bk == 1 ? w1 : w0);
+      else err = 8;
+    }
+    if (act && writer) cursor[g] = my_cur + total;
+    if (act && p_c == uw - 1 && x != RANS_L) err = 6;  // end-of-lane invariant
+  };
+  // (b) start the lanes of rows beginning at this front and (c) prefetch the
+  // words this front's step may read into registers, so the L2 latency hides
+  // behind a whole front (the cluster barrier invalidates L1).
+  //  G = 32: a warp's active rows of one pass parity form one group; lanes
+  //          0-31 hold words cur..cur+31 of it (the odd warp of the pair
+  //          starts after the even warp's readers, <= 16 of them).
+  //  G < 32: each owner lane holds the word it reads if every earlier row
+  //          of its group in this warp reads one.
+  auto rans_prefetch = [&](int r, int c, bool active) {
+    if (threadIdx.x >= 128) return;
+    asm volatile("bar.sync 5, 128;" ::: "memory");  // cursor updates of (a) visible
+    const uint32_t g = (uint32_t)r >> g_shift;
+    const bool act = owner && active;
+    const uint32_t bk = ((uint32_t)r >> ns_shift) & 1u;
+    uint32_t my_sb = 0;
+    my_sl = 0;
+    my_cur = 0;
+    pw0 = pw1 = 0;
+    if (act) {
+      my_sb = s_sbase[g];
+      my_sl = s_slen[g];
+      my_cur = cursor[g];
+    }
+    if (G == 32) {
+#pragma unroll
+      for (uint32_t b = 0; b < 2; ++b) {
+        const uint32_t mb = __ballot_sync(0xFFFFFFFFu, act && bk == b);
+        if (mb) {
+          const uint32_t src = (uint32_t)__ffs(mb) - 1u;
+          const uint32_t sb = __shfl_sync(0xFFFFFFFFu, my_sb, src);
+          const uint32_t sl = __shfl_sync(0xFFFFFFFFu, my_sl, src);
+          const uint32_t cu = __shfl_sync(0xFFFFFFFFu, my_cur, src);
+          const uint16_t* swb = reinterpret_cast<const uint16_t*>(cbase + sb);
+          const uint32_t idx = cu + lane;
+          const uint32_t wv = idx < sl ? (uint32_t)__ldg(swb + idx) : 0u;
+          if (b == 0) pw0 = wv;
+          else pw1 = wv;
+        }
+      }
+    } else {
+      const uint32_t key = act ? g : (0x80000000u | lane);
+      const uint32_t gm = __match_any_sync(0xFFFFFFFFu, key);
+      first_lane = (uint32_t)__ffs(gm) - 1u;
+      const uint32_t idx = my_cur + (lane - first_lane);
+      const uint16_t* swm = reinterpret_cast<const uint16_t*>(cbase + my_sb);
+      pw0 = (act && idx < my_sl) ? (uint32_t)__ldg(swm + idx) : 0u;
+    }
+    if (act && c == 0) {  // the row's lane starts: flushed state (hi, lo)
+      const uint16_t* sw = reinterpret_cast<const uint16_t*>(cbase + my_sb);
+      const uint32_t i = 2u * ((uint32_t)r - G * g);
+      if (i + 1 < my_sl) x = ((uint32_t)__ldg(sw + i) << 16) | (uint32_t)__ldg(sw + i + 1);
+      else err = 8;
+    }
+  };
 
   if (pf.on) pf.t = clock64();
 #pragma unroll 1
@@ -517,55 +636,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const bool any = __syncthreads_or(active);
     pf.mark(0);
     if (any) {
-      const uint32_t g = (uint32_t)r >> g_shift;  // G is a power of two dividing 32
-      const bool act = owner && active;
-      const uint32_t bk = ((uint32_t)r >> ns_shift) & 1u;  // pass parity over the slots
-      // Prefetch this front's candidate stream words into registers now, so the
-      // L2 latency hides behind the network (shared memory leaves almost no L1).
-      //  G = 32: a warp's active rows of one pass parity form one group; lanes
-      //          0-31 hold words cur..cur+31 of it (the odd warp of the pair
-      //          starts after the even warp's readers, <= 16 of them).
-      //  G < 32: each owner lane holds the word it reads if every earlier row
-      //          of its group in this warp reads one.
-      uint32_t pw0 = 0, pw1 = 0, first_lane = 0;
-      uint32_t my_sb = 0, my_sl = 0, my_cur = 0;
-      if (threadIdx.x < 128) {
-        if (act) {
-          my_sb = s_sbase[g];
-          my_sl = s_slen[g];
-          my_cur = cursor[g];
-        }
-        if (G == 32) {
-#pragma unroll
-          for (uint32_t b = 0; b < 2; ++b) {
-            const uint32_t mb = __ballot_sync(0xFFFFFFFFu, act && bk == b);
-            if (mb) {
-              const uint32_t src = (uint32_t)__ffs(mb) - 1u;
-              const uint32_t sb = __shfl_sync(0xFFFFFFFFu, my_sb, src);
-              const uint32_t sl = __shfl_sync(0xFFFFFFFFu, my_sl, src);
-              const uint32_t cu = __shfl_sync(0xFFFFFFFFu, my_cur, src);
-              const uint16_t* swb = reinterpret_cast<const uint16_t*>(cbase + sb);
-              const uint32_t idx = cu + lane;
-              const uint32_t wv = idx < sl ? (uint32_t)__ldg(swb + idx) : 0u;
-              if (b == 0) pw0 = wv;
-              else pw1 = wv;
-            }
-          }
-        } else {
-          const uint32_t key = act ? g : (0x80000000u | lane);
-          const uint32_t gm = __match_any_sync(0xFFFFFFFFu, key);
-          first_lane = (uint32_t)__ffs(gm) - 1u;
-          const uint32_t idx = my_cur + (lane - first_lane);
-          const uint16_t* swm = reinterpret_cast<const uint16_t*>(cbase + my_sb);
-          pw0 = (act && idx < my_sl) ? (uint32_t)__ldg(swm + idx) : 0u;
-        }
-      }
-      if (act && c == 0) {  // the row's lane starts: flushed state (hi, lo)
-        const uint16_t* sw = reinterpret_cast<const uint16_t*>(cbase + my_sb);
-        const uint32_t i = 2u * ((uint32_t)r - G * g);
-        if (i + 1 < my_sl) x = ((uint32_t)__ldg(sw + i) << 16) | (uint32_t)__ldg(sw + i + 1);
-        else err = 8;
-      }
       // window gather from the ring: one load per tap, no bounds tests
       {
         const uint32_t col = (uint32_t)c & 31u;
@@ -596,15 +666,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       pf.mark(1);
       if constexpr (PREC == 1) tc_wait_st();
       pf.mark(2);
-      eng.run();
+      // network; the deferred rANS step runs in the layer-1 / layer-3 MMA waits
+      eng.run([&](int l) {
+        if (l == 1) rans_apply();
+        else if (l == 3) rans_prefetch(r, c, active);
+      });
       pf.mark(3);
       const uint32_t slot = x & 0xFFFFu;
       uint32_t fs, cs;
       const int sym = q1_decode(eng, slot, fs, cs, &pf);
       pix = sym;
-      // publish the pixel first (own ring; the successor's halo through DSMEM
-      // for the CTA's last 8 rows) so the stores have landed by the time the
-      // end-of-front cluster barrier's release executes
+      // publish the pixel (own ring; the successor's halo through DSMEM for
+      // the CTA's last 8 rows) before the end-of-front cluster barrier
       if (owner && active) {
         const uint32_t bank = ((uint32_t)r >> ns_shift) & 1u;
         const uint32_t col = (uint32_t)c & 31u;
@@ -641,63 +714,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
       }
-      if (threadIdx.x < 128) {  // warps 0-3: rANS lanes in the lower half-warps
-        bool need = false;
-        if (act) {
-          x = fs * (x >> 16) + slot - cs;
-          need = x < RANS_L;
-        }
-        const uint32_t key = act ? g : (0x80000000u | lane);
-        const uint32_t gm = __match_any_sync(0xFFFFFFFFu, key);
-        // A warp may hold rows of two groups at once: one finishing and one of
-        // the next pass over the slots (rows NS apart).  They differ in the
-        // pass parity bk, which keys the cross-warp counts below.
-        const uint32_t nb0 = __ballot_sync(0xFFFFFFFFu, need && bk == 0);
-        const uint32_t nb1 = __ballot_sync(0xFFFFFFFFu, need && bk == 1);
-        const uint32_t a0 = __ballot_sync(0xFFFFFFFFu, act && bk == 0);
-        const uint32_t a1 = __ballot_sync(0xFFFFFFFFu, act && bk == 1);
-        const uint32_t readers = (nb0 | nb1) & gm;
-        const uint32_t nmine = __popc(readers);          // this warp's readers of my group
-        const uint32_t cur = my_cur;
-        if (lane == 0) {
-          s_cnt[wq][0] = __popc(nb0) | (a0 ? 0x10000u : 0u);
-          s_cnt[wq][1] = __popc(nb1) | (a1 ? 0x10000u : 0u);
-        }
-        asm volatile("bar.sync 5, 128;" ::: "memory");
-        // G = 32: rows of the group's upper 16 (odd warp) read after the even warp's
-        uint32_t before = 0, total = nmine;
-        bool writer = lane == (uint32_t)(__ffs(gm) - 1);
-        if (G == 32) {
-          const uint32_t other = s_cnt[wq ^ 1][bk];
-          if (wq & 1) {
-            before = other & 0xFFFFu;
-            total = before + nmine;
-          } else {
-            total = nmine + (other & 0xFFFFu);
-            writer = writer && !(other & 0x10000u);  // the odd warp writes when it is active
-          }
-        }
-        const uint32_t rk = __popc(readers & ((1u << lane) - 1u));
-        // word from the prefetch registers (all lanes take part in the shuffles)
-        const uint32_t src = G == 32 ? (before + rk) & 31u : (first_lane + rk) & 31u;
-        const uint32_t w0 = __shfl_sync(0xFFFFFFFFu, pw0, src);
-        const uint32_t w1 = __shfl_sync(0xFFFFFFFFu, pw1, src);
-        if (need) {
-          const uint32_t wi = cur + before + rk;
-          if (wi < my_sl) x = (x << 16) | (G == 32 && bk == 1 ? w1 : w0);
-          else err = 8;
-        }
-        if (act && writer) cursor[g] = cur + total;
-        if (act && c == uw - 1 && x != RANS_L) err = 6;  // end-of-lane invariant
-      }
+      p_fs = fs;
+      p_cs = cs;
+      p_slot = slot;
       pf.mark(9);
+    } else {
+      rans_apply();
+      rans_prefetch(r, c, active);
     }
+    p_act = active;
+    p_r = r;
+    p_c = c;
     if (NC > 1) cluster_sync_all();
     else __syncthreads();
     // the pixel's HBM store after the barrier: its release need not wait for it
     if (owner && active) oimg[(uint64_t)r * p.W + c] = (uint8_t)pix;
     pf.mark(10);
   }
+  rans_apply();  // the last front's step
+  __syncthreads();
   if (pf.on)
     for (int kk = 0; kk < 11; ++kk) atomicAdd(prof + kk, pf.acc[kk]);
   for (uint32_t g = threadIdx.x; g < un.ngroups; g += NTHREADS) {
