@@ -230,15 +230,28 @@ dlic_status upload_model(dlic_model* m, const ParsedModel& pm) {
     for (int k = 0; k < K; ++k)
       for (int n = 0; n < N; ++n) {
         const int kt = l == 0 ? kpos_tap(k) : k;  // layer 1: the engine's K order
-        const float v = kt >= 0 && kt < Kr ? pm.W[l][(size_t)kt * N + n] : 0.0f;
+        const bool fresh = l == 0 && (kt == TAP_FA || kt == TAP_FB);  // applied in the epilogue
+        const float v = kt >= 0 && kt < Kr && !fresh ? pm.W[l][(size_t)kt * N + n] : 0.0f;
         const uint16_t u = bf16_bits(v);
         const size_t a = wimg_off(l) + (size_t)(k / 8) * (N / 8) * 128 + (size_t)(n / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
         memcpy(&img[a], &u, 2);
       }
   }
-  std::vector<float> bias(BIAS_TOTAL);
+  std::vector<float> bias(BIAS_TOTAL + FRESH_FLOATS);
   for (int l = 0; l < NLAYER; ++l)
     for (int n = 0; n < layer_n(l); ++n) bias[(l < NLAYER - 1 ? l * HID : BIAS_OFF_LAST) + n] = pm.b[l][n];
+  // fresh-tap weights (bf16-rounded like the MMA image), float4 per pair n, n+1
+  auto bf16f = [](float v) {
+    const uint32_t u = (uint32_t)bf16_bits(v) << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+  };
+  for (int n = 0; n < HID; ++n) {
+    const size_t q = FRESH_OFF + 4 * (size_t)(n / 2) + (n & 1);
+    bias[q] = bf16f(pm.W[0][(size_t)TAP_FA * HID + n]);
+    bias[q + 2] = bf16f(pm.W[0][(size_t)TAP_FB * HID + n]);
+  }
   std::vector<float> w32(f32_off(NLAYER));
   for (int l = 0; l < NLAYER; ++l) {
     const int K = f32_k(l), N = layer_n(l);
@@ -591,8 +604,8 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
     unsigned long long* d_prof = nullptr;
     const bool prof = getenv("DLIC_PROF") != nullptr;
     if (prof) {
-      CUDA_TRY(sc.alloc(&d_prof, 16 * 8));
-      CUDA_TRY(cudaMemsetAsync(d_prof, 0, 16 * 8, st));
+      CUDA_TRY(sc.alloc(&d_prof, 300 * 8));
+      CUDA_TRY(cudaMemsetAsync(d_prof, 0, 300 * 8, st));
     }
     ev_begin("decode", st);
     CUDA_TRY(launch_decode(p, m->dw(), d_bits, d_meta, d_sbase, d_slen, d_img, d_status, st, d_prof));

@@ -61,7 +61,19 @@ __host__ __device__ constexpr uint32_t wimg_off(int l) {
 constexpr uint32_t WIMG_BYTES = 217088;  // 20480 + 4*32768 + 65536
 constexpr int BIAS_OFF_LAST = 5 * HID;   // biases: 5 x 128 hidden, then 256
 constexpr int BIAS_TOTAL = 5 * HID + NOUT;
-constexpr uint32_t BIAS_BYTES = BIAS_TOTAL * 4;
+// The two "fresh" taps of the wavefront: the only window cells of pixel
+// (r, c) decoded on the immediately preceding front (c-1+3r and c+2+3(r-1)
+// both equal step(r,c) - 1, reading R3).  Their layer-1 weights are taken out
+// of the bf16 MMA image and applied on the CUDA cores in the layer-1
+// epilogue (exact products v/256 * bf16 weight, fp32 FMA), so that the MMA
+// over the other 76 taps can be issued one front early.
+constexpr int TAP_FA = 77;  // (dr, dc) = (0, -1)
+constexpr int TAP_FB = 71;  // (dr, dc) = (-1, +2)
+// fresh-tap weight table after the biases: float4 per output pair n, n+1 =
+// {wa[n], wa[n+1], wb[n], wb[n+1]} (bf16-rounded, as fp32)
+constexpr int FRESH_OFF = BIAS_TOTAL;
+constexpr int FRESH_FLOATS = 2 * HID;
+constexpr uint32_t BIAS_BYTES = (BIAS_TOTAL + FRESH_FLOATS) * 4;
 
 // fp32 weight blob: per layer W[K][N] then b[N]; K of layer 0 is KIN (78)
 __host__ __device__ constexpr int f32_k(int l) { return l == 0 ? KIN : HID; }
@@ -99,6 +111,9 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 }
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
@@ -376,106 +391,90 @@ struct TcEngine {
   // hook(l) runs (all threads) after layer l's MMAs are issued, before the
   // wait for them: work that overlaps the tensor core.
   // The MMAs are issued by thread MMA_ISSUER (warp 8), outside the warps that
-  // run hook work.
+  // run hook work (decoder rANS lanes, warps 0-3).
   static constexpr unsigned MMA_ISSUER = 256;
-  template <class Hook>
-  __device__ __forceinline__ void run(Hook&& hook) {
-    const uint32_t lo = lane_off();
-    const int j = col_grp(), h = half_id();
-    tc_wait_st();
-#pragma unroll 1
-    for (int l = 0; l < NLAYER; ++l) {
-      tc_fence_before();
-      __syncthreads();
-      if (threadIdx.x == MMA_ISSUER) {
-        tc_fence_after();
-        const int K = layer_k(l), N = layer_n(l);
-        const uint32_t id = umma_idesc(64, N);
-        const uint32_t lbo = (uint32_t)N * 16u;                 // next 8-wide K core matrix
-        const uint32_t kstep = 2u * (uint32_t)(N / 8) * 128u;   // one K=16 slice
-        uint64_t bd = umma_desc(wsmem + wimg_off(l), lbo, 128u);
-        uint32_t at = tmem + TM_A;
-        umma_ts(tmem + TM_D, at, bd, id, 0u);
-        for (int kk = 1; kk < K / 16; ++kk) {
-          bd += kstep >> 4;
-          at += 8u;
-          umma_ts(tmem + TM_D, at, bd, id, 1u);
-        }
-        umma_commit(bar);
-      }
-      hook(l);
-      mbar_wait(bar, phase);
-      phase ^= 1u;
-      tc_fence_after();
-      if (l < NLAYER - 1) {
-        const float2* b2 = reinterpret_cast<const float2*>(bias + l * HID + 32 * j + 16 * h);
-        uint32_t v[16];
-        tmem_ld16h<16>(tmem + lo + TM_D + 32u * (uint32_t)j, v);
-        tc_wait_ld();
-        uint32_t p[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float2 b = b2[q];
-          float x0, x1;
-          f2_split(f2_add(f2_bits(v[2 * q], v[2 * q + 1]), f2_make(b.x, b.y)), x0, x1);
-          p[q] = pack_bf16_relu(x0, x1);
-        }
-        tmem_st8h<8>(tmem + lo + TM_A + 16u * (uint32_t)j, p);
-        tc_wait_st();
-      }
-    }
-  }
 
-  // pf (debug): 0 sync, 1 issue, 2 mma wait, 3 epilogue (accumulated in acc2)
-  __device__ void run(Prof* pf = nullptr) {
+  // Issuer only: layer l's MMAs (K/16 slices, M=64) and their commit.
+  __device__ __forceinline__ void issue(int l) const {
+    tc_fence_after();
+    const int K = layer_k(l), N = layer_n(l);
+    const uint32_t id = umma_idesc(64, N);
+    const uint32_t lbo = (uint32_t)N * 16u;                // next 8-wide K core matrix
+    const uint32_t kstep = 2u * (uint32_t)(N / 8) * 128u;  // one K=16 slice
+    // start-address field (bits 0-13, 16-byte units) advances by kstep/16
+    uint64_t bd = umma_desc(wsmem + wimg_off(l), lbo, 128u);
+    uint32_t at = tmem + TM_A;
+    umma_ts(tmem + TM_D, at, bd, id, 0u);
+    for (int kk = 1; kk < K / 16; ++kk) {
+      bd += kstep >> 4;
+      at += 8u;
+      umma_ts(tmem + TM_D, at, bd, id, 1u);
+    }
+    umma_commit(bar);
+  }
+  // Layer 0 over the 76 early taps (fresh weights are zero in the image),
+  // after put_input (all threads; the caller supplies the barrier).
+  __device__ __forceinline__ void issue_l0() const {
+    if (threadIdx.x == MMA_ISSUER) issue(0);
+  }
+  // Encoder: input stored -> barrier -> layer 0 issued.
+  __device__ __forceinline__ void start_l0() const {
+    tc_wait_st();
+    tc_fence_before();
+    __syncthreads();
+    issue_l0();
+  }
+  __device__ __forceinline__ void wait_mma() {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    tc_fence_after();
+  }
+  // bias + ReLU + bf16 -> next A; this thread's columns [32j+16h, +16)
+  // (packed column 16j+8h+q holds activations 32j+16h+2q, +1: identity K order).
+  // Layer 0 also adds the fresh taps: fma(xb, wb, fma(xa, wa, acc)) + bias.
+  template <bool L0>
+  __device__ __forceinline__ void epilogue(int l, float xa, float xb) const {
     const uint32_t lo = lane_off();
     const int j = col_grp(), h = half_id();
+    const float2* b2 = reinterpret_cast<const float2*>(bias + l * HID + 32 * j + 16 * h);
+    const float4* fw = reinterpret_cast<const float4*>(bias + FRESH_OFF) + 16 * j + 8 * h;
+    uint32_t v[16];
+    tmem_ld16h<16>(tmem + lo + TM_D + 32u * (uint32_t)j, v);
+    tc_wait_ld();
+    const f2 xa2 = f2_make(xa, xa), xb2 = f2_make(xb, xb);
+    uint32_t p[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float2 b = b2[q];
+      f2 acc = f2_bits(v[2 * q], v[2 * q + 1]);
+      if constexpr (L0) {
+        const float4 w = fw[q];
+        acc = f2_fma(xa2, f2_make(w.x, w.y), acc);
+        acc = f2_fma(xb2, f2_make(w.z, w.w), acc);
+      }
+      float x0, x1;
+      f2_split(f2_add(acc, f2_make(b.x, b.y)), x0, x1);
+      p[q] = pack_bf16_relu(x0, x1);  // relu(x) rounded to bf16 (RN)
+    }
+    tmem_st8h<8>(tmem + lo + TM_A + 16u * (uint32_t)j, p);
     tc_wait_st();
+  }
+  // Layers 1..6 after layer 0's MMAs were issued (start_l0 / issue_l0):
+  // wait, layer-0 epilogue with the fresh taps (xa, xb), then per layer:
+  // barrier, issue, hook(l) (all threads; overlaps the tensor core), wait,
+  // epilogue.  The logits are left in TMEM columns [0, 256).
+  template <class Hook>
+  __device__ __forceinline__ void run_rest(float xa, float xb, Hook&& hook) {
+    wait_mma();
+    epilogue<true>(0, xa, xb);
 #pragma unroll 1
-    for (int l = 0; l < NLAYER; ++l) {
+    for (int l = 1; l < NLAYER; ++l) {
       tc_fence_before();
       __syncthreads();
-      if (pf) pf->mark2(0);
-      if (threadIdx.x == 0) {
-        tc_fence_after();
-        const int K = layer_k(l), N = layer_n(l);
-        const uint32_t id = umma_idesc(64, N);
-        const uint32_t lbo = (uint32_t)N * 16u;                 // next 8-wide K core matrix
-        const uint32_t kstep = 2u * (uint32_t)(N / 8) * 128u;   // one K=16 slice
-        // start-address field (bits 0-13, 16-byte units) advances by kstep/16
-        uint64_t bd = umma_desc(wsmem + wimg_off(l), lbo, 128u);
-        uint32_t at = tmem + TM_A;
-        umma_ts(tmem + TM_D, at, bd, id, 0u);
-        for (int kk = 1; kk < K / 16; ++kk) {
-          bd += kstep >> 4;
-          at += 8u;
-          umma_ts(tmem + TM_D, at, bd, id, 1u);
-        }
-        umma_commit(bar);
-      }
-      if (pf) pf->mark2(1);
-      mbar_wait(bar, phase);
-      phase ^= 1u;
-      tc_fence_after();
-      if (pf) pf->mark2(2);
-      if (l < NLAYER - 1) {  // bias + ReLU + bf16 -> next A; columns [32j+16h, +16)
-        const float2* b2 = reinterpret_cast<const float2*>(bias + l * HID + 32 * j + 16 * h);
-        uint32_t v[16];
-        tmem_ld16h<16>(tmem + lo + TM_D + 32u * (uint32_t)j, v);
-        tc_wait_ld();
-        uint32_t p[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float2 b = b2[q];
-          float x0, x1;
-          f2_split(f2_add(f2_bits(v[2 * q], v[2 * q + 1]), f2_make(b.x, b.y)), x0, x1);
-          p[q] = pack_bf16_relu(x0, x1);  // relu(x) rounded to bf16 (RN)
-        }
-        // packed column 16j+8h+q holds activations 32j+16h+2q, +1: identity K order
-        tmem_st8h<8>(tmem + lo + TM_A + 16u * (uint32_t)j, p);
-        tc_wait_st();
-        if (pf) pf->mark2(3);
-      }
+      if (threadIdx.x == MMA_ISSUER) issue(l);
+      hook(l);
+      wait_mma();
+      if (l < NLAYER - 1) epilogue<false>(l, 0.0f, 0.0f);
     }
   }
 
@@ -516,10 +515,17 @@ struct Fp32Engine {
 
   __device__ __forceinline__ void put_input(int k, float x) const { buf0[k * ROWS + tile_row()] = x; }
 
+  __device__ __forceinline__ void issue_l0() const {}
+  __device__ __forceinline__ void start_l0() const {}
+  // Same interface as TcEngine: the whole network on the CUDA cores, after
+  // the fresh taps are stored with the others (the fp32 engine has no early
+  // layer 0).
   template <class Hook>
-  __device__ __forceinline__ void run(Hook&& hook) {
+  __device__ __forceinline__ void run_rest(float xa, float xb, Hook&& hook) {
+    put_input(TAP_FA, xa);
+    put_input(TAP_FB, xb);
 #pragma unroll 1
-    for (int l = 0; l < NLAYER; ++l) hook(l);
+    for (int l = 1; l < NLAYER; ++l) hook(l);
     run();
   }
   __device__ void run() {
@@ -646,7 +652,6 @@ __device__ __forceinline__ Q1Row q1_table(const Eng& e, uint32_t (&v)[32], int s
   // pass 1 (one TMEM round trip): biased logits, the group max m_j, and
   // e_i = 2^(l_i*log2e - m_j*log2e) relative to the group max, stored back;
   // z_j as even/odd pair partial sums, combined across the half-warps.
-  e.ld32(v);
   float m = -INFINITY;
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
@@ -811,13 +816,14 @@ __device__ __forceinline__ uint32_t q1_encode(const Eng& e, int sym, float* prob
 // picked up after q1_table's first exchange barrier.  Search: reverse scan of
 // this thread's 32 entries with the monotone test slot < c_{i+1}; the last hit
 // is the smallest such i = s.  Every lane executes the same TMEM loads.
-template <class Eng>
-__device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot0, uint32_t& fs_out, uint32_t& cs_out,
+template <class Eng, class Mid>
+__device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot0, uint32_t& fs_out, uint32_t& cs_out, Mid&& mid,
                                          Prof* pf = nullptr) {
   float fs, csl;
   e.xput(6, __shfl_sync(0xFFFFFFFFu, slot0, threadIdx.x & 15));
   uint32_t v[32];
   e.ld32(v);
+  mid();  // all threads: the network's TMEM output is now free
   const Q1Row r = q1_table<false>(e, v, -1, fs, csl, nullptr, pf);
   uint32_t s4[4];
   e.xget4(6, s4);

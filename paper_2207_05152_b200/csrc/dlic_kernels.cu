@@ -150,6 +150,11 @@ __device__ __forceinline__ void feed(const Eng& eng, Get get) {
   }
 }
 
+// v/256 exactly (v < 256)
+__device__ __forceinline__ float u8_unit(uint32_t v) {
+  return __fadd_rn(__uint_as_float(0x3F800000u | (v << 15)), -1.0f);
+}
+
 // ------------------------------------------------------------ encoder MLP
 // Persistent CTAs over 64-pixel tiles of the units' raster order.  Thread
 // (row, j, h): pixel = tile*64 + row; (j, h) owns inputs [20j+10h, +10),
@@ -183,7 +188,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       return ok ? v : 0u;
     };
     feed<PREC>(eng, get);
-    eng.run();
+    eng.start_l0();
+    eng.run_rest(u8_unit(get(0, -1)), u8_unit(get(-1, 2)), [](int) {});
     const int sym = valid ? (int)__ldg(img + (uint64_t)r * p.W + c) : 0;
     const uint64_t gi = (uint64_t)un.img * p.W * p.H + (uint64_t)(un.y0 + r) * p.W + (un.x0 + c);
     if (dbg && dbg_logits) {  // raw logits (bias added) of this thread's 32 columns
@@ -621,60 +627,117 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   };
 
+  // slot geometry at front t: row r (active if decoded on front t), column c
+  auto front_rc = [&](int t, int& r, int& c) -> bool {
+    const int rlo = t - uw + 1 > 0 ? (t - uw + 3) / 3 : 0;
+    const int rhi = min(uh - 1, t / 3);
+    r = 0;
+    c = 0;
+    if (rlo > rhi) return false;
+    r = rlo + (int)((S + NS - ((uint32_t)rlo & (NS - 1))) & (NS - 1));
+    c = t - 3 * r;
+    return r <= rhi;
+  };
+  // ring base of slot (r, c): window cell (dr, dc) of the K order at
+  // bp + (dc)*RING_ROWS for dr = u - 8, tap 9 at bp + g9 (see the ring notes)
+  auto ring_at = [&](int r, int c) -> const uint8_t* {
+    const uint32_t col = (uint32_t)c & 31u;
+    const uint32_t cb = col < 6u ? col + 32u : col;
+    return ring + (((uint32_t)r >> ns_shift) & 1u) * RING_BANK + cb * RING_ROWS + (uint32_t)row;
+  };
+  // Early part of a front (one front ahead): the 76 taps decoded before the
+  // preceding front -> layer-1 input (the two fresh taps' weights are zero in
+  // the MMA image; fp32: overwritten by run_rest).
+  auto early_put = [&](int r, int c) {
+    const uint8_t* bp = ring_at(r, c) + gu;
+    uint32_t tv[10];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) tv[i] = bp[(i - 6) * RING_ROWS];
+    tv[9] = bp[g9];
+    if constexpr (PREC == 1) {
+      const f2 m1 = f2_make(-1.0f, -1.0f);
+      uint32_t a[5];
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        float x0, x1;
+        f2_split(f2_add(f2_bits(0x3F800000u | (tv[2 * q] << 15), 0x3F800000u | (tv[2 * q + 1] << 15)), m1), x0, x1);
+        a[q] = pack_bf16(x0, x1);
+      }
+      eng.put_input(a);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 10; ++i)
+        if (i < 9 || gu < 6) eng.put_input(i < 9 ? 9 * gu + i : 72 + gu, u8_unit(tv[i]));
+    }
+  };
+  // does any slot of this CTA hold an active row at front t (uniform)
+  auto cta_any = [&](int t) -> bool {
+    const int rlo = t - uw + 1 > 0 ? (t - uw + 3) / 3 : 0;
+    const int rhi = min(uh - 1, t / 3);
+    if (rlo > rhi) return false;
+    const uint32_t m = (uint32_t)rlo & (NS - 1), b = rank * ROWS;
+    const uint32_t d = m - b < (uint32_t)ROWS ? 0u : ((b - m) & (NS - 1));
+    return rlo + (int)d <= rhi;
+  };
+  // early part of front t+1, once this thread is done with the network's
+  // output of front t: gather -> layer-1 input; each warp then arrives on
+  // a_ready, which the MMA issuer waits on before issuing layer 0 (issue_early)
+  const uint32_t a_ready = smem_u32(&bar[1]);
+  uint32_t a_phase = 0;
+  auto early = [&](int rn, int cn) {
+    if constexpr (PREC == 1) {
+      early_put(rn, cn);
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_ready);
+    } else {
+      quad_sync();  // the row's logits are loaded: its buffer columns are free
+      early_put(rn, cn);
+    }
+  };
+  auto issue_early = [&](bool any_n) {
+    if constexpr (PREC == 1) {
+      if (any_n && threadIdx.x == TcEngine::MMA_ISSUER) {
+        mbar_wait(a_ready, a_phase);
+        eng.issue_l0();
+      }
+      a_phase ^= 1u;  // every warp arrives once per front
+    }
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(a_ready, NTHREADS / 32);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  int r, c;
+  bool active = front_rc(0, r, c);
+  bool any = cta_any(0);
+  early(r, c);
+  issue_early(any);
   if (pf.on) pf.t = clock64();
 #pragma unroll 1
   for (int t = 0; t < T; ++t) {
-    const int rlo = t - uw + 1 > 0 ? (t - uw + 3) / 3 : 0;
-    const int rhi = min(uh - 1, t / 3);
-    bool active = false;
-    int r = 0, c = 0;
-    if (rlo <= rhi) {
-      r = rlo + (int)((S + NS - ((uint32_t)rlo & (NS - 1))) & (NS - 1));
-      active = r <= rhi;
-      c = t - 3 * r;
-    }
-    const bool any = __syncthreads_or(active);
+    int rn, cn;
+    const bool active_n = front_rc(t + 1, rn, cn);
+    const bool any_n = cta_any(t + 1);
     pf.mark(0);
     if (any) {
-      // window gather from the ring: one load per tap, no bounds tests
-      {
-        const uint32_t col = (uint32_t)c & 31u;
-        const uint32_t cb = col < 6u ? col + 32u : col;
-        const uint8_t* bp = ring + (((uint32_t)r >> ns_shift) & 1u) * RING_BANK + cb * RING_ROWS + (uint32_t)(row + gu);
-        uint32_t tv[10];
-#pragma unroll
-        for (int i = 0; i < 9; ++i) tv[i] = bp[(i - 6) * RING_ROWS];
-        tv[9] = bp[g9];
-        if constexpr (PREC == 1) {
-          const f2 m1 = f2_make(-1.0f, -1.0f);
-          uint32_t a[5];
-#pragma unroll
-          for (int q = 0; q < 5; ++q) {
-            float x0, x1;
-            f2_split(f2_add(f2_bits(0x3F800000u | (tv[2 * q] << 15), 0x3F800000u | (tv[2 * q + 1] << 15)), m1), x0,
-                     x1);
-            a[q] = pack_bf16(x0, x1);
-          }
-          eng.put_input(a);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 10; ++i)
-            if (i < 9 || gu < 6)
-              eng.put_input(i < 9 ? 9 * gu + i : 72 + gu, __fadd_rn(__uint_as_float(0x3F800000u | (tv[i] << 15)), -1.0f));
-        }
-      }
+      // the fresh taps (0,-1) and (-1,+2), decoded on front t-1
+      const uint8_t* fp = ring_at(r, c) + 8;
+      const float xa = u8_unit(fp[-RING_ROWS]);
+      const float xb = u8_unit(fp[2 * RING_ROWS - 1]);
       pf.mark(1);
-      if constexpr (PREC == 1) tc_wait_st();
-      pf.mark(2);
       // network; the deferred rANS step runs in the layer-1 / layer-3 MMA waits
-      eng.run([&](int l) {
+      eng.run_rest(xa, xb, [&](int l) {
         if (l == 1) rans_apply();
         else if (l == 3) rans_prefetch(r, c, active);
       });
       pf.mark(3);
       const uint32_t slot = x & 0xFFFFu;
       uint32_t fs, cs;
-      const int sym = q1_decode(eng, slot, fs, cs, &pf);
+      const int sym = q1_decode(eng, slot, fs, cs, [&]() { early(rn, cn); }, &pf);
       pix = sym;
       // publish the pixel (own ring; the successor's halo through DSMEM for
       // the CTA's last 8 rows) before the end-of-front cluster barrier
@@ -696,7 +759,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           hput(hb, col, (uint32_t)sym);
           if (col < 8u) hput(hb, col + 32u, (uint32_t)sym);
         }
-        if (c == uw - 1) {  // row end: right pad of this row, left pad of the slot's next row
+        if (c == uw - 1) {  // row end: right pad (columns W, W+1) of this row
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const uint32_t pc = (uint32_t)(uw + e) & 31u;
@@ -707,6 +770,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               if (pc < 8u) hput(hb, pc + 32u, 0u);
             }
           }
+        }
+        // left pad (pos 26..31) of the slot's next row, in the other bank:
+        // after the previous occupant's readers are done (front 3r + 23 at
+        // the latest, W <= 3*NS) and well before the next row's early gather
+        if (c == min(24, uw - 1)) {
 #pragma unroll
           for (uint32_t pc = 26; pc < 32; ++pc) {
             rp[(bank ^ 1u) * RING_BANK + pc * RING_ROWS] = 0;
@@ -721,18 +789,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else {
       rans_apply();
       rans_prefetch(r, c, active);
+      early(rn, cn);
     }
     p_act = active;
     p_r = r;
     p_c = c;
-    if (NC > 1) cluster_sync_all();
-    else __syncthreads();
+    // end-of-front barrier; the next front's layer-0 MMA is issued between
+    // its arrive and wait
+    if (NC > 1) {
+      cluster_arrive();
+      issue_early(any_n);
+      cluster_wait();
+    } else {
+      issue_early(any_n);
+      __syncthreads();
+    }
     // the pixel's HBM store after the barrier: its release need not wait for it
     if (owner && active) oimg[(uint64_t)r * p.W + c] = (uint8_t)pix;
     pf.mark(10);
+    r = rn;
+    c = cn;
+    active = active_n;
+    any = any_n;
   }
   rans_apply();  // the last front's step
   __syncthreads();
+
   if (pf.on)
     for (int kk = 0; kk < 11; ++kk) atomicAdd(prof + kk, pf.acc[kk]);
   for (uint32_t g = threadIdx.x; g < un.ngroups; g += NTHREADS) {
