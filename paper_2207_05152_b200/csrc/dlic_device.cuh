@@ -85,7 +85,8 @@ __host__ __device__ constexpr uint32_t f32_off(int l) {
 
 // TMEM column map (one 512-column allocation per CTA)
 constexpr uint32_t TM_D = 0;     // accumulator / logits / e / f, 256 columns
-constexpr uint32_t TM_A = 256;   // A operand, K/2 columns (bf16 pairs), up to 64
+constexpr uint32_t TM_A = 256;   // A operand of layers 2-6, K/2 columns (bf16 pairs), 64
+constexpr uint32_t TM_A0 = 384;  // A operand of layer 1 (80 inputs -> 40 columns)
 constexpr uint32_t TM_X = 320;   // exchange slot s: columns TM_X+4s+j (lower half-warp)
 constexpr uint32_t TM_XUP = 32;  //   and TM_X+32+4s+j (upper half-warp copy)
 constexpr uint32_t TM_COLS = 512;
@@ -382,7 +383,7 @@ struct TcEngine {
   // Layer-1 input: this thread's 5 packed bf16 pairs = inputs [20j+10h, +10)
   // (A packed columns [10j+5h, +5)).
   __device__ __forceinline__ void put_input(const uint32_t (&a)[5]) const {
-    const uint32_t base = tmem + lane_off() + TM_A + 10u * (uint32_t)col_grp();
+    const uint32_t base = tmem + lane_off() + TM_A0 + 10u * (uint32_t)col_grp();
     tmem_st4h<5>(base, a);
     tmem_st1h<5>(base + 4, a[4]);
   }
@@ -391,8 +392,11 @@ struct TcEngine {
   // hook(l) runs (all threads) after layer l's MMAs are issued, before the
   // wait for them: work that overlaps the tensor core.
   // The MMAs are issued by thread MMA_ISSUER (warp 8), outside the warps that
-  // run hook work (decoder rANS lanes, warps 0-3).
+  // run hook work (decoder rANS lanes, warps 0-3); layer 3's by MMA_ISSUER2
+  // (warp 9), so that warp 8 is free for the hook work of that layer.
   static constexpr unsigned MMA_ISSUER = 256;
+  static constexpr unsigned MMA_ISSUER2 = 288;
+  __device__ __forceinline__ static unsigned issuer(int l) { return l == 2 ? MMA_ISSUER2 : MMA_ISSUER; }
 
   // Issuer only: layer l's MMAs (K/16 slices, M=64) and their commit.
   __device__ __forceinline__ void issue(int l) const {
@@ -403,7 +407,7 @@ struct TcEngine {
     const uint32_t kstep = 2u * (uint32_t)(N / 8) * 128u;  // one K=16 slice
     // start-address field (bits 0-13, 16-byte units) advances by kstep/16
     uint64_t bd = umma_desc(wsmem + wimg_off(l), lbo, 128u);
-    uint32_t at = tmem + TM_A;
+    uint32_t at = tmem + (l == 0 ? TM_A0 : TM_A);
     umma_ts(tmem + TM_D, at, bd, id, 0u);
     for (int kk = 1; kk < K / 16; ++kk) {
       bd += kstep >> 4;
@@ -471,7 +475,7 @@ struct TcEngine {
     for (int l = 1; l < NLAYER; ++l) {
       tc_fence_before();
       __syncthreads();
-      if (threadIdx.x == MMA_ISSUER) issue(l);
+      if (threadIdx.x == issuer(l)) issue(l);
       hook(l);
       wait_mma();
       if (l < NLAYER - 1) epilogue<false>(l, 0.0f, 0.0f);
@@ -607,9 +611,16 @@ struct Q1Row {
   float R;        // residual on symbol 255
   float Fmine;    // this thread's half-group sum
   float hbase;    // sum of the lower half of this group if h == 1, else 0
+  float P[3];     // this thread's prefix sums after 8, 16, 24 of its 32 entries
 };
 
 __device__ __forceinline__ f2 f2_splat(float a) { return f2_make(a, a); }
+// max of three (FMNMX3)
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
 
 // 2^t for a pair, t <= ~0, on the FMA pipe (offloads MUFU, FA4-style):
 // n = floor(t) via a round-toward-minus-infinity add of 1.5*2^23, f = t - n in
@@ -660,7 +671,7 @@ __device__ __forceinline__ Q1Row q1_table(const Eng& e, uint32_t (&v)[32], int s
     f2_split(f2_add(f2_bits(v[2 * q], v[2 * q + 1]), f2_make(b.x, b.y)), l0, l1);
     v[2 * q] = __float_as_uint(l0);
     v[2 * q + 1] = __float_as_uint(l1);
-    m = fmaxf(m, fmaxf(l0, l1));
+    m = fmax3(m, l0, l1);
   }
   m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, 16));  // m_j, equal in both halves
   const f2 nm = f2_splat(__fmul_rn(-m, LOG2E));
@@ -716,7 +727,7 @@ __device__ __forceinline__ Q1Row q1_table(const Eng& e, uint32_t (&v)[32], int s
   const f2 fbias = f2_splat(-8388607.0f);  // y - 2^23 + 1 = 1 + floor(x), exact
   // pass A: p_i, f_i = 1 + floor(p_i * 65279) (x + 2^23 rounded toward -inf
   // has ulp 1), kept in v as floats; half sum
-  f2 FF = f2_splat(0.0f);
+  f2 FB[4] = {f2_splat(0.0f), f2_splat(0.0f), f2_splat(0.0f), f2_splat(0.0f)};  // 8-entry blocks
   fs = 0.0f;
   cs_local = 0.0f;
   float cum = 0.0f;
@@ -724,7 +735,7 @@ __device__ __forceinline__ Q1Row q1_table(const Eng& e, uint32_t (&v)[32], int s
   for (int q = 0; q < 16; ++q) {
     const f2 p = f2_mul(f2_bits(v[2 * q], v[2 * q + 1]), inv);
     const f2 f = f2_add(f2_add_rm(f2_mul(p, scale), two23), fbias);
-    FF = f2_add(FF, f);
+    FB[q >> 2] = f2_add(FB[q >> 2], f);
     float f0, f1;
     f2_split(f, f0, f1);
     if (ENC) {
@@ -748,10 +759,18 @@ __device__ __forceinline__ Q1Row q1_table(const Eng& e, uint32_t (&v)[32], int s
     v[2 * q] = __float_as_uint(f0);
     v[2 * q + 1] = __float_as_uint(f1);
   }
-  float Fa, Fb;
-  f2_split(FF, Fa, Fb);
+  float B[4];  // exact integer block sums
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    float Fa, Fb;
+    f2_split(FB[b], Fa, Fb);
+    B[b] = __fadd_rn(Fa, Fb);
+  }
   Q1Row r;
-  r.Fmine = __fadd_rn(Fa, Fb);
+  r.P[0] = B[0];
+  r.P[1] = B[0] + B[1];
+  r.P[2] = r.P[1] + B[2];
+  r.Fmine = r.P[2] + B[3];
   const float Fo = __shfl_xor_sync(0xFFFFFFFFu, r.Fmine, 16);
   r.hbase = h ? Fo : 0.0f;
   if (pf) pf->mark(7);
@@ -830,22 +849,32 @@ __device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot0, uint32_t&
   const float slot = (float)s4[0];
   const int c0 = 64 * col_grp() + 32 * half_id();
   const float base = q1_base(r);
-  float cum = base + r.Fmine + (c0 == NOUT - 32 ? r.R : 0.0f);  // c at the end of my columns
+  const bool last = c0 == NOUT - 32;  // symbol 255 carries the residual R
+  const float cum = base + r.Fmine + (last ? r.R : 0.0f);  // c at the end of my columns
   const bool mine = slot >= base && slot < cum;
+  if (last) v[31] = __float_as_uint(__uint_as_float(v[31]) + r.R);
+  // level 1: the 8-entry block holding the slot (block prefix sums from pass A)
+  const float sl = slot - base;  // exact
+  const int kb = (sl >= r.P[0]) + (sl >= r.P[1]) + (sl >= r.P[2]);
+  float cend = kb == 0 ? r.P[0] : (kb == 1 ? r.P[1] : (kb == 2 ? r.P[2] : cum - base));
+  // level 2: reverse scan of the block's 8 entries, test sl < c_{i+1}
   int sym = 0;
   float fsel = 0.0f, csel = 0.0f;
 #pragma unroll
-  for (int i = 31; i >= 0; --i) {
-    float f = __uint_as_float(v[i]);
-    if (i == 31 && c0 == NOUT - 32) f += r.R;
-    const float lo = cum - f;  // exact
-    if (slot < cum) {
-      sym = c0 + i;
+  for (int i = 7; i >= 0; --i) {
+    const uint32_t lo01 = (kb & 1) ? v[8 + i] : v[i];
+    const uint32_t hi01 = (kb & 1) ? v[24 + i] : v[16 + i];
+    const float f = __uint_as_float((kb & 2) ? hi01 : lo01);
+    const float lo = cend - f;  // exact
+    if (sl < cend) {
+      sym = i;
       fsel = f;
       csel = lo;
     }
-    cum = lo;
+    cend = lo;
   }
+  sym += c0 + 8 * kb;
+  csel += base;
   if (pf) pf->mark(8);
   uint32_t pk = mine ? ((uint32_t)sym | ((uint32_t)fsel << 8)) : 0xFFFFFFFFu;
   uint32_t pc = (uint32_t)csel;

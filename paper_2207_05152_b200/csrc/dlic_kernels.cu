@@ -684,9 +684,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // a_ready, which the MMA issuer waits on before issuing layer 0 (issue_early)
   const uint32_t a_ready = smem_u32(&bar[1]);
   uint32_t a_phase = 0;
-  auto early = [&](int rn, int cn) {
+  // bf16: the layer-1 input has its own TMEM columns (TM_A0), so the gather
+  // can run during the network (early_gather in the layer-3 MMA wait); the
+  // signal only has to follow this thread's load of the logits (the layer-1
+  // MMA overwrites them).  fp32: the input shares the logits buffer.
+  auto early_gather = [&](int rn, int cn) {
+    if constexpr (PREC == 1) early_put(rn, cn);
+  };
+  auto early_signal = [&](int rn, int cn) {
     if constexpr (PREC == 1) {
-      early_put(rn, cn);
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -695,6 +701,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       quad_sync();  // the row's logits are loaded: its buffer columns are free
       early_put(rn, cn);
     }
+  };
+  auto early = [&](int rn, int cn) {
+    early_gather(rn, cn);
+    early_signal(rn, cn);
   };
   auto issue_early = [&](bool any_n) {
     if constexpr (PREC == 1) {
@@ -729,15 +739,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const float xa = u8_unit(fp[-RING_ROWS]);
       const float xb = u8_unit(fp[2 * RING_ROWS - 1]);
       pf.mark(1);
-      // network; the deferred rANS step runs in the layer-1 / layer-3 MMA waits
+      // network; the deferred rANS step (layers 1, 3) and the next front's
+      // early gather (layer 2) run in the MMA waits
       eng.run_rest(xa, xb, [&](int l) {
+        const bool w9 = (threadIdx.x >> 5) == (TcEngine::MMA_ISSUER2 >> 5);  // issues layer 3
         if (l == 1) rans_apply();
+        else if (l == (w9 ? 4 : 2)) early_gather(rn, cn);
         else if (l == 3) rans_prefetch(r, c, active);
       });
       pf.mark(3);
       const uint32_t slot = x & 0xFFFFu;
       uint32_t fs, cs;
-      const int sym = q1_decode(eng, slot, fs, cs, [&]() { early(rn, cn); }, &pf);
+      const int sym = q1_decode(eng, slot, fs, cs, [&]() { early_signal(rn, cn); }, &pf);
       pix = sym;
       // publish the pixel (own ring; the successor's halo through DSMEM for
       // the CTA's last 8 rows) before the end-of-front cluster barrier
