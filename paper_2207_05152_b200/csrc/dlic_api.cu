@@ -611,8 +611,8 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
     CUDA_TRY(launch_decode(p, m->dw(), d_bits, d_meta, d_sbase, d_slen, d_img, d_status, st, d_prof));
     ev_end("decode", st);
     if (prof) {
-      unsigned long long hp[16];
-      CUDA_TRY(cudaMemcpyAsync(hp, d_prof, 128, cudaMemcpyDeviceToHost, st));
+      unsigned long long hp[40];
+      CUDA_TRY(cudaMemcpyAsync(hp, d_prof, 40 * 8, cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
       const double ctas = (double)p.n_img * p.upi * p.nc;
       const double T = (double)(p.tw + 3 * (p.th - 1));
@@ -620,8 +620,8 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
                             "barrier"};
       fprintf(stderr, "[dlic prof] cycles per front per CTA:");
       for (int k = 0; k < 11; ++k) fprintf(stderr, " %s %.0f", nm[k], hp[k] / ctas / T);
-      fprintf(stderr, "\n[dlic prof] network per front: sync %.0f issue %.0f mma-wait %.0f epilogue %.0f\n",
-              hp[12] / ctas / T, hp[13] / ctas / T, hp[14] / ctas / T, hp[15] / ctas / T);
+      fprintf(stderr, "\n[dlic prof] network per front (sum over layers): sync %.0f issue+hook %.0f mma-wait %.0f "
+              "epilogue %.0f\n", hp[16] / ctas / T, hp[17] / ctas / T, hp[18] / ctas / T, hp[19] / ctas / T);
     }
   }
   uint8_t* ho = static_cast<uint8_t*>(g_pin_out.get((size_t)h.width * h.height + 64));
