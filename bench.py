@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="images per GPU per step (0 = config default)")
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tile", default="", help="WxH independent tiles (default: the config's)")
+    ap.add_argument("--no-variants", action="store_true", help="skip the strip-tiled C2 side measurement")
     return ap.parse_args()
 
 
@@ -157,6 +159,37 @@ def opts_for(cfg):
     return c
 
 
+def tile_for(args):
+    g, tile = opts_for(args.config)
+    if args.tile:
+        w, h = (int(x) for x in args.tile.lower().split("x"))
+        tile = (w, h)
+    return g, tile
+
+
+def measure_variant(dl, model, d_imgs, prec, g, tile, reps=5):
+    """Decode time (CUDA events inside the library, best of reps) and bpp of
+    the same images coded with another tile shape (device batch API)."""
+    import torch
+    n = d_imgs.shape[0]
+    d_out, d_sizes, stride = dl.dlic_encode_batch_device(model, d_imgs, prec, g, tile)
+    torch.cuda.synchronize()
+    sizes = d_sizes.cpu().numpy()
+    hdr = dl.dlic_peek(d_out[:int(sizes[0])].cpu().numpy().tobytes())
+    d_dec = torch.empty_like(d_imgs)
+    d_status = torch.zeros(n, dtype=torch.int32, device=d_imgs.device)
+    offs = [i * stride for i in range(n)]
+    best = 1e30
+    for _ in range(reps):
+        dl.dlic_decode_batch_device(model, d_out, offs, hdr, d_dec, d_status)
+        torch.cuda.synchronize()
+        best = min(best, dl.dlic_last_kernel_ms("decode"))
+    assert int(d_status.abs().sum()) == 0 and torch.equal(d_dec, d_imgs), "variant round trip failed"
+    px = d_imgs.numel()
+    return {"tile": list(tile), "decode_ms": best, "decode_mpx_s": px / (best / 1e3) / 1e6,
+            "bpp_total": 8.0 * float(sizes.sum()) / px}
+
+
 def default_batch(cfg):
     return {"C1": 1, "C2": 1, "C3": 64, "C4": 1, "C5": 8}[cfg]
 
@@ -245,7 +278,7 @@ def main():
         blob = fh.read()
     model = dl.dlic_model_load(blob, local)
     prec = 1 if args.precision == "bf16" else 0
-    g, tile = opts_for(args.config)
+    g, tile = tile_for(args)
     n = args.batch or default_batch(args.config)
     imgs = images_for(args, rank, n)
     _, H, W = imgs.shape
@@ -340,6 +373,12 @@ def main():
         e2e = {"value": ws * px_rank / (em / 1e3) / 1e6, "unit": "Mpixel/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": em}
 
+    variants = None
+    if rank == 0 and args.config == "C2" and tile == (0, 0) and not args.no_variants:
+        # the same image as 4 independent 768x128 strips (north_star: "independent
+        # image tiles with their own streams"): 1149 instead of 2301 fronts
+        variants = {"strips_768x128": measure_variant(dl, model, d_imgs, prec, g, (768, 128))}
+
     if rank == 0:
         peaks, src = load_peaks()
         # dominant kernel: the wavefront decoder (latency-bound front chain)
@@ -353,8 +392,11 @@ def main():
                 traffic = json.load(fh).get("%s_%s" % (args.config, args.precision))
         except (OSError, ValueError):
             pass
-        T = W + 3 * (H - 1) if tile == (0, 0) else tile[0] + 3 * (tile[1] - 1)
-        floor_ms = T * 3392 / (peaks.get("sm_max_mhz", 1965.0) * 1e3)   # MMA-chain floor per front (App. A)
+        tw, th = (W, H) if tile == (0, 0) else (min(tile[0], W), min(tile[1], H))
+        T = tw + 3 * (th - 1)
+        # per front, layers 2-6 are a dependent MMA chain (layer 1 is issued a
+        # front early): 4 x 8 x 64 + 8 x 128 = 3072 cycles at M=64
+        floor_ms = T * 3072 / (peaks.get("sm_max_mhz", 1965.0) * 1e3)
         cpu = cpu_baseline_sample(args, imgs[0])
         line = {
             "metric": "encode+decode Mpixel/s (8-bit gray, round trip) and bpp",
@@ -375,6 +417,7 @@ def main():
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": src + (" bf16_tflops" if prec == 1 else " sm_max_mhz x 148 SM x 128 FFMA x 2 (DESIGN.md)"),
                          "latency_floor_ms": floor_ms, "latency_frac": floor_ms / t_dec},
+            "variants": variants,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": 6 * args.steps,

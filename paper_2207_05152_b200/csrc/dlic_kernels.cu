@@ -3,7 +3,7 @@
 //   k_enc_mlp   every pixel at once (north_star (b)): window gather (P:63,
 //               P:290; fill 0 P:59) -> dense network -> softmax -> Q1
 //               table (R5) -> (f_s, c_s) of the true symbol.  Persistent CTAs
-//               over 128-pixel tiles; tcgen05 (bf16) or FFMA (fp32) engine.
+//               over 64-pixel tiles; tcgen05 (bf16) or FFMA (fp32) engine.
 //   k_rans_enc  one warp per G-row group stream ("at most one [coder
 //               instance] per pixel row"; R7): lanes = rows, walks the
 //               wavefront in reverse (t desc, r desc), ballot/popc word
@@ -11,9 +11,11 @@
 //   k_container / k_copy  header + prefix-sum stream compaction (a6).
 //   k_dec_prep  parses container framing on the device (batch decode).
 //   k_decode    persistent per-unit wavefront decoder: one
-//               cluster of nc CTAs x 128 slots; every front: gather from a
-//               shared-memory ring -> same network -> Q1 search -> rANS step
-//               -> publish pixel (DSMEM mirror) -> cluster barrier.
+//               cluster of nc CTAs x 64 slots; every front: fresh taps from a
+//               shared-memory ring -> same network (layer 1 over the older
+//               taps issued a front early) -> Q1 search -> publish pixel
+//               (DSMEM mirror) -> cluster barrier; the rANS step runs one
+//               front late inside the next front's network.
 #include <cstdint>
 
 #include "dlic_device.cuh"
