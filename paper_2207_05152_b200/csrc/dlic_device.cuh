@@ -854,24 +854,22 @@ __device__ __forceinline__ uint32_t q1_encode(const Eng& e, int sym, float* prob
   return x4[0] | x4[1] | x4[2] | x4[3];
 }
 
-// Decoder: symbol s with c_s <= slot < c_s + f_s (all threads of the row).
-// `slot0` is valid in the rANS owner (group 0, lower half); it is broadcast to
-// the upper half by a shuffle and to groups 1-3 through exchange slot 6,
-// picked up after q1_table's first exchange barrier.  Search: reverse scan of
-// this thread's 32 entries with the monotone test slot < c_{i+1}; the last hit
-// is the smallest such i = s.  Every lane executes the same TMEM loads.
+// Decoder: symbol s with c_s <= slot < c_s + f_s (all threads of the row call
+// it with the row's slot).  Exactly one of the row's 8 threads holds the slot
+// in its column range (the ranges partition [0, 2^16)): it returns mine = true
+// with the symbol and its (f_s, c_s); the others return mine = false.
+// Search: 8-entry block sums from pass A pick the block, a reverse scan of its
+// 8 entries with the monotone test slot < c_{i+1} finds s.  mid() runs (all
+// threads) once the logits are loaded: the network's TMEM output is free.
 template <class Eng, class Mid>
-__device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot0, uint32_t& fs_out, uint32_t& cs_out, Mid&& mid,
-                                         Prof* pf = nullptr) {
+__device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot_u, bool& mine_out, uint32_t& fs_out,
+                                         uint32_t& cs_out, Mid&& mid, Prof* pf = nullptr) {
   float fs, csl;
-  e.xput(6, __shfl_sync(0xFFFFFFFFu, slot0, threadIdx.x & 15));
   uint32_t v[32];
   e.ld32(v);
-  mid();  // all threads: the network's TMEM output is now free
+  mid();
   const Q1Row r = q1_table<false>(e, v, -1, fs, csl, nullptr, pf);
-  uint32_t s4[4];
-  e.xget4(6, s4);
-  const float slot = (float)s4[0];
+  const float slot = (float)slot_u;
   const int c0 = 64 * col_grp() + 32 * half_id();
   const float base = q1_base(r);
   const bool last = c0 == NOUT - 32;  // symbol 255 carries the residual R
@@ -898,31 +896,11 @@ __device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot0, uint32_t&
     }
     cend = lo;
   }
-  sym += c0 + 8 * kb;
-  csel += base;
   if (pf) pf->mark(8);
-  uint32_t pk = mine ? ((uint32_t)sym | ((uint32_t)fsel << 8)) : 0xFFFFFFFFu;
-  uint32_t pc = (uint32_t)csel;
-  const uint32_t opk = __shfl_xor_sync(0xFFFFFFFFu, pk, 16);
-  const uint32_t opc = __shfl_xor_sync(0xFFFFFFFFu, pc, 16);
-  if (!mine) {
-    pk = opk;
-    pc = opc;
-  }
-  e.xput(4, pk);
-  e.xput(5, pc);
-  e.xsync();
-  uint32_t k4[4], c4[4];
-  e.xget4(4, k4);
-  e.xget4(5, c4);
-  int g = 0;
-#pragma unroll
-  for (int q = 0; q < NGRP; ++q)
-    if (k4[q] != 0xFFFFFFFFu) g = q;
-  fs_out = k4[g] >> 8;
-  cs_out = c4[g];
-  if (pf) pf->mark(5);
-  return (int)(k4[g] & 0xFFu);
+  mine_out = mine;
+  fs_out = (uint32_t)fsel;
+  cs_out = (uint32_t)(csel + base);
+  return sym + c0 + 8 * kb;
 }
 
 }  // namespace dlic

@@ -40,7 +40,7 @@ constexpr uint32_t RING_BANK = (uint32_t)RING_COLS * RING_ROWS;  // 2880
 constexpr uint32_t RING_BYTES = 2u * RING_BANK;               // 5760
 constexpr uint32_t F32_BUF_BYTES = (NOUT + HID) * ROWS * 4u;          // 98304
 constexpr uint32_t F32_X_BYTES = NXSLOT * NGRP * ROWS * 4u;          // 7168
-constexpr uint32_t MAX_DYN_SMEM = 232448 - 64;                       // 227 KB minus static
+constexpr uint32_t MAX_DYN_SMEM = 232448 - 1024;                     // 227 KB minus static (k_decode: 896 B)
 
 size_t enc_smem_bytes(uint32_t precision) {
   return precision == 1 ? WIMG_BYTES + BIAS_BYTES : F32_BUF_BYTES + F32_X_BYTES;
@@ -463,6 +463,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __shared__ uint64_t bar[2];
   __shared__ uint32_t tslot;
   __shared__ uint32_t s_cnt[4][2];  // per owner warp and pass parity: readers | active<<16
+  __shared__ uint32_t s_slot[ROWS];  // the row's rANS slot x & 0xFFFF (owner -> the row's 8 threads)
+  __shared__ uint2 s_res[ROWS];      // (f_s, c_s) of the decoded symbol (finder -> owner, next front)
   const int row = tile_row();
   const uint32_t lane = lane_id();
   const bool owner = threadIdx.x < 128 && half_id() == 0;  // group 0, lower half-warp
@@ -516,7 +518,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   //   pw0/1  stream words prefetched for it; my_cur/my_sl its group's cursor/length
   bool p_act = false;
   int p_r = 0, p_c = 0;
-  uint32_t p_fs = 0, p_cs = 0, p_slot = 0;
   uint32_t pw0 = 0, pw1 = 0, first_lane = 0, my_sl = 0, my_cur = 0;
 
   // (a) x' = f*(x>>16) + slot - c for the previous front's rows, renormalised
@@ -529,7 +530,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t bk = ((uint32_t)p_r >> ns_shift) & 1u;  // pass parity over the slots
     bool need = false;
     if (act) {
-      x = p_fs * (x >> 16) + p_slot - p_cs;
+      const uint2 fc = s_res[row];  // written by the thread that found the symbol
+      x = fc.x * (x >> 16) + (x & 0xFFFFu) - fc.y;
       need = x < RANS_L;
     }
     const uint32_t key = act ? g : (0x80000000u | lane);
@@ -627,6 +629,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (i + 1 < my_sl) x = ((uint32_t)__ldg(sw + i) << 16) | (uint32_t)__ldg(sw + i + 1);
       else err = 8;
     }
+    if (owner) s_slot[row] = x & 0xFFFFu;  // read by the row's threads after the next layer barrier
   };
 
   // slot geometry at front t: row r (active if decoded on front t), column c
@@ -734,6 +737,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     int rn, cn;
     const bool active_n = front_rc(t + 1, rn, cn);
     const bool any_n = cta_any(t + 1);
+    bool pub = false;
     pf.mark(0);
     if (any) {
       // the fresh taps (0,-1) and (-1,+2), decoded on front t-1
@@ -750,13 +754,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         else if (l == 3) rans_prefetch(r, c, active);
       }, PROF ? &pf : nullptr);
       pf.mark(3);
-      const uint32_t slot = x & 0xFFFFu;
       uint32_t fs, cs;
-      const int sym = q1_decode(eng, slot, fs, cs, [&]() { early_signal(rn, cn); }, &pf);
+      bool mine;
+      const int sym = q1_decode(eng, s_slot[row], mine, fs, cs, [&]() { early_signal(rn, cn); }, &pf);
+      // the thread that found the symbol publishes it: own ring, the
+      // successor's halo through DSMEM for the CTA's last 8 rows, zero pads,
+      // and (f_s, c_s) for the row's rANS owner (applied next front)
+      pub = mine && active;
       pix = sym;
-      // publish the pixel (own ring; the successor's halo through DSMEM for
-      // the CTA's last 8 rows) before the end-of-front cluster barrier
-      if (owner && active) {
+      if (pub) {
+        s_res[row] = make_uint2(fs, cs);
         const uint32_t bank = ((uint32_t)r >> ns_shift) & 1u;
         const uint32_t col = (uint32_t)c & 31u;
         uint8_t* rp = ring + (uint32_t)row + 8u;
@@ -797,9 +804,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
       }
-      p_fs = fs;
-      p_cs = cs;
-      p_slot = slot;
       pf.mark(9);
     } else {
       rans_apply();
@@ -821,7 +825,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       __syncthreads();
     }
     // the pixel's HBM store after the barrier: its release need not wait for it
-    if (owner && active) oimg[(uint64_t)r * p.W + c] = (uint8_t)pix;
+    if (pub) oimg[(uint64_t)r * p.W + c] = (uint8_t)pix;
     pf.mark(10);
     r = rn;
     c = cn;
