@@ -554,7 +554,10 @@ struct Fp32Engine {
     put_input(TAP_FA, xa);
     put_input(TAP_FB, xb);
 #pragma unroll 1
-    for (int l = 1; l < NLAYER; ++l) hook(l);
+    for (int l = 1; l < NLAYER; ++l) {
+      if (l > 1) __syncthreads();  // the hooks rely on the layer barriers between them
+      hook(l);
+    }
     run();
   }
   __device__ void run() {

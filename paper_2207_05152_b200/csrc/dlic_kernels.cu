@@ -523,38 +523,45 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // (a) x' = f*(x>>16) + slot - c for the previous front's rows, renormalised
   // with interleaved word reads (ballot/popc within a warp; a G = 32 group
   // spans two warps and adds the first warp's count through shared memory).
-  auto rans_apply = [&]() {
+  // Split in two halves around a layer barrier of the network (no barrier of
+  // its own): rans_a updates the states and publishes the warps' reader
+  // counts, rans_b assigns the words and advances the cursors.
+  bool ra_act = false, ra_need = false;
+  uint32_t ra_g = 0, ra_bk = 0, ra_gm = 0, ra_readers = 0;
+  auto rans_a = [&]() {
     if (threadIdx.x >= 128) return;
-    const bool act = owner && p_act;
-    const uint32_t g = (uint32_t)p_r >> g_shift;  // G is a power of two dividing 32
-    const uint32_t bk = ((uint32_t)p_r >> ns_shift) & 1u;  // pass parity over the slots
-    bool need = false;
-    if (act) {
+    ra_act = owner && p_act;
+    ra_g = (uint32_t)p_r >> g_shift;  // G is a power of two dividing 32
+    ra_bk = ((uint32_t)p_r >> ns_shift) & 1u;  // pass parity over the slots
+    ra_need = false;
+    if (ra_act) {
       const uint2 fc = s_res[row];  // written by the thread that found the symbol
       x = fc.x * (x >> 16) + (x & 0xFFFFu) - fc.y;
-      need = x < RANS_L;
+      ra_need = x < RANS_L;
     }
-    const uint32_t key = act ? g : (0x80000000u | lane);
-    const uint32_t gm = __match_any_sync(0xFFFFFFFFu, key);
+    const uint32_t key = ra_act ? ra_g : (0x80000000u | lane);
+    ra_gm = __match_any_sync(0xFFFFFFFFu, key);
     // A warp may hold rows of two groups at once: one finishing and one of
     // the next pass over the slots (rows NS apart).  They differ in the
     // pass parity bk, which keys the cross-warp counts below.
-    const uint32_t nb0 = __ballot_sync(0xFFFFFFFFu, need && bk == 0);
-    const uint32_t nb1 = __ballot_sync(0xFFFFFFFFu, need && bk == 1);
-    const uint32_t a0 = __ballot_sync(0xFFFFFFFFu, act && bk == 0);
-    const uint32_t a1 = __ballot_sync(0xFFFFFFFFu, act && bk == 1);
-    const uint32_t readers = (nb0 | nb1) & gm;
-    const uint32_t nmine = __popc(readers);  // this warp's readers of my group
+    const uint32_t nb0 = __ballot_sync(0xFFFFFFFFu, ra_need && ra_bk == 0);
+    const uint32_t nb1 = __ballot_sync(0xFFFFFFFFu, ra_need && ra_bk == 1);
+    const uint32_t a0 = __ballot_sync(0xFFFFFFFFu, ra_act && ra_bk == 0);
+    const uint32_t a1 = __ballot_sync(0xFFFFFFFFu, ra_act && ra_bk == 1);
+    ra_readers = (nb0 | nb1) & ra_gm;
     if (lane == 0) {
       s_cnt[wq][0] = __popc(nb0) | (a0 ? 0x10000u : 0u);
       s_cnt[wq][1] = __popc(nb1) | (a1 ? 0x10000u : 0u);
     }
-    asm volatile("bar.sync 5, 128;" ::: "memory");
+  };
+  auto rans_b = [&]() {  // after a CTA barrier following rans_a
+    if (threadIdx.x >= 128) return;
+    const uint32_t nmine = __popc(ra_readers);  // this warp's readers of my group
     // G = 32: rows of the group's upper 16 (odd warp) read after the even warp's
     uint32_t before = 0, total = nmine;
-    bool writer = lane == (uint32_t)(__ffs(gm) - 1);
+    bool writer = lane == (uint32_t)(__ffs(ra_gm) - 1);
     if (G == 32) {
-      const uint32_t other = s_cnt[wq ^ 1][bk];
+      const uint32_t other = s_cnt[wq ^ 1][ra_bk];
       if (wq & 1) {
         before = other & 0xFFFFu;
         total = before + nmine;
@@ -563,18 +570,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         writer = writer && !(other & 0x10000u);  // the odd warp writes when it is active
       }
     }
-    const uint32_t rk = __popc(readers & ((1u << lane) - 1u));
+    const uint32_t rk = __popc(ra_readers & ((1u << lane) - 1u));
     // word from the prefetch registers (all lanes take part in the shuffles)
     const uint32_t src = G == 32 ? (before + rk) & 31u : (first_lane + rk) & 31u;
     const uint32_t w0 = __shfl_sync(0xFFFFFFFFu, pw0, src);
     const uint32_t w1 = __shfl_sync(0xFFFFFFFFu, pw1, src);
-    if (need) {
+    if (ra_need) {
       const uint32_t wi = my_cur + before + rk;
-      if (wi < my_sl) x = (x << 16) | (G == 32 && bk == 1 ? w1 : w0);
+      if (wi < my_sl) x = (x << 16) | (G == 32 && ra_bk == 1 ? w1 : w0);
       else err = 8;
     }
-    if (act && writer) cursor[g] = my_cur + total;
-    if (act && p_c == uw - 1 && x != RANS_L) err = 6;  // end-of-lane invariant
+    if (ra_act && writer) cursor[ra_g] = my_cur + total;
+    if (ra_act && p_c == uw - 1 && x != RANS_L) err = 6;  // end-of-lane invariant
   };
   // (b) start the lanes of rows beginning at this front and (c) prefetch the
   // words this front's step may read into registers, so the L2 latency hides
@@ -584,9 +591,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   //          starts after the even warp's readers, <= 16 of them).
   //  G < 32: each owner lane holds the word it reads if every earlier row
   //          of its group in this warp reads one.
-  auto rans_prefetch = [&](int r, int c, bool active) {
+  auto rans_prefetch = [&](int r, int c, bool active) {  // after a CTA barrier following rans_b
     if (threadIdx.x >= 128) return;
-    asm volatile("bar.sync 5, 128;" ::: "memory");  // cursor updates of (a) visible
     const uint32_t g = (uint32_t)r >> g_shift;
     const bool act = owner && active;
     const uint32_t bk = ((uint32_t)r >> ns_shift) & 1u;
@@ -745,13 +751,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const float xa = u8_unit(fp[-RING_ROWS]);
       const float xb = u8_unit(fp[2 * RING_ROWS - 1]);
       pf.mark(1);
-      // network; the deferred rANS step (layers 1, 3) and the next front's
-      // early gather (layer 2) run in the MMA waits
+      // network; the deferred rANS step and the next front's early gather
+      // run in the MMA waits
       eng.run_rest(xa, xb, [&](int l) {
-        const bool w9 = (threadIdx.x >> 5) == (TcEngine::MMA_ISSUER2 >> 5);  // issues layer 3
-        if (l == 1) rans_apply();
-        else if (l == (w9 ? 4 : 2)) early_gather(rn, cn);
-        else if (l == 3) rans_prefetch(r, c, active);
+        // warps 0-3: rANS (a) / (b) / prefetch in the layer 2 / 3 / 4 waits
+        // (the layer barriers order them); the next front's early gather in
+        // the layer-3 wait, or the layer-5 wait for warps 0-3 and warp 9
+        // (which issues layer 3)
+        const bool late = threadIdx.x < 128 || (threadIdx.x >> 5) == (TcEngine::MMA_ISSUER2 >> 5);
+        if (l == 1) rans_a();
+        else if (l == 2) {
+          rans_b();
+          if (!late) early_gather(rn, cn);
+        } else if (l == 3) rans_prefetch(r, c, active);
+        else if (l == 4 && late) early_gather(rn, cn);
       }, PROF ? &pf : nullptr);
       pf.mark(3);
       uint32_t fs, cs;
@@ -806,7 +819,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       pf.mark(9);
     } else {
-      rans_apply();
+      rans_a();
+      __syncthreads();
+      rans_b();
+      __syncthreads();
       rans_prefetch(r, c, active);
       early(rn, cn);
     }
@@ -832,7 +848,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     active = active_n;
     any = any_n;
   }
-  rans_apply();  // the last front's step
+  rans_a();  // the last front's step
+  __syncthreads();
+  rans_b();
   __syncthreads();
 
   if (pf.on) {
