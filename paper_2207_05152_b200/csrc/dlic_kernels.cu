@@ -526,6 +526,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // Split in two halves around a layer barrier of the network (no barrier of
   // its own): rans_a updates the states and publishes the warps' reader
   // counts, rans_b assigns the words and advances the cursors.
+  // Lanes of my rANS group among this warp's owner lanes (0-15, rows 16q +
+  // lane of the CTA): the slots' rows are 16-aligned per pass, so a group is
+  // all active lanes of my pass parity (G >= 16) or a G-aligned lane range
+  // of them (G < 16).
+  auto group_mask = [&](bool act, uint32_t bk, uint32_t am, uint32_t bm) -> uint32_t {
+    if (!act) return 0u;
+    const uint32_t same = am & (bk ? bm : ~bm);
+    return G >= 16 ? same : same & (((1u << G) - 1u) << (lane & ~(G - 1u)));
+  };
   bool ra_act = false, ra_need = false;
   uint32_t ra_g = 0, ra_bk = 0, ra_gm = 0, ra_readers = 0;
   auto rans_a = [&]() {
@@ -539,16 +548,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       x = fc.x * (x >> 16) + (x & 0xFFFFu) - fc.y;
       ra_need = x < RANS_L;
     }
-    const uint32_t key = ra_act ? ra_g : (0x80000000u | lane);
-    ra_gm = __match_any_sync(0xFFFFFFFFu, key);
     // A warp may hold rows of two groups at once: one finishing and one of
     // the next pass over the slots (rows NS apart).  They differ in the
     // pass parity bk, which keys the cross-warp counts below.
-    const uint32_t nb0 = __ballot_sync(0xFFFFFFFFu, ra_need && ra_bk == 0);
-    const uint32_t nb1 = __ballot_sync(0xFFFFFFFFu, ra_need && ra_bk == 1);
-    const uint32_t a0 = __ballot_sync(0xFFFFFFFFu, ra_act && ra_bk == 0);
-    const uint32_t a1 = __ballot_sync(0xFFFFFFFFu, ra_act && ra_bk == 1);
-    ra_readers = (nb0 | nb1) & ra_gm;
+    const uint32_t am = __ballot_sync(0xFFFFFFFFu, ra_act);
+    const uint32_t bm = __ballot_sync(0xFFFFFFFFu, ra_bk != 0);
+    const uint32_t nm = __ballot_sync(0xFFFFFFFFu, ra_need);
+    ra_gm = group_mask(ra_act, ra_bk, am, bm);
+    const uint32_t nb0 = nm & ~bm, nb1 = nm & bm;
+    const bool a0 = (am & ~bm) != 0, a1 = (am & bm) != 0;
+    ra_readers = nm & ra_gm;
     if (lane == 0) {
       s_cnt[wq][0] = __popc(nb0) | (a0 ? 0x10000u : 0u);
       s_cnt[wq][1] = __popc(nb1) | (a1 ? 0x10000u : 0u);
@@ -605,10 +614,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       my_sl = s_slen[g];
       my_cur = cursor[g];
     }
+    const uint32_t am = __ballot_sync(0xFFFFFFFFu, act);
+    const uint32_t bm = __ballot_sync(0xFFFFFFFFu, bk != 0);
     if (G == 32) {
 #pragma unroll
       for (uint32_t b = 0; b < 2; ++b) {
-        const uint32_t mb = __ballot_sync(0xFFFFFFFFu, act && bk == b);
+        const uint32_t mb = am & (b ? bm : ~bm);
         if (mb) {
           const uint32_t src = (uint32_t)__ffs(mb) - 1u;
           const uint32_t sb = __shfl_sync(0xFFFFFFFFu, my_sb, src);
@@ -622,9 +633,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
     } else {
-      const uint32_t key = act ? g : (0x80000000u | lane);
-      const uint32_t gm = __match_any_sync(0xFFFFFFFFu, key);
-      first_lane = (uint32_t)__ffs(gm) - 1u;
+      const uint32_t gm = group_mask(act, bk, am, bm);
+      first_lane = gm ? (uint32_t)__ffs(gm) - 1u : lane;
       const uint32_t idx = my_cur + (lane - first_lane);
       const uint16_t* swm = reinterpret_cast<const uint16_t*>(cbase + my_sb);
       pw0 = (act && idx < my_sl) ? (uint32_t)__ldg(swm + idx) : 0u;
