@@ -102,6 +102,9 @@ __device__ __forceinline__ int col_grp() { return threadIdx.x >> 7; }
 __device__ __forceinline__ int half_id() { return (threadIdx.x >> 4) & 1; }
 __device__ __forceinline__ int tile_row() { return 16 * quad() + (threadIdx.x & 15); }
 
+// named barrier over the 16 row warps (the decoder's rANS warp is not part)
+__device__ __forceinline__ void row_sync() { asm volatile("bar.sync 6, 512;" ::: "memory"); }
+
 // named barrier over the 4 warps that share one TMEM lane quadrant
 __device__ __forceinline__ void quad_sync() {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + ((threadIdx.x >> 5) & 3)), "r"(128) : "memory");
@@ -443,7 +446,7 @@ struct TcEngine {
   __device__ __forceinline__ void start_l0() const {
     tc_wait_st();
     tc_fence_before();
-    __syncthreads();
+    row_sync();
     issue_l0();
   }
   __device__ __forceinline__ void wait_mma() {
@@ -495,7 +498,7 @@ struct TcEngine {
 #pragma unroll 1
     for (int l = 1; l < NLAYER; ++l) {
       tc_fence_before();
-      __syncthreads();
+      row_sync();
       if (pf) pf->mark2(0);
       if (threadIdx.x == issuer(l)) issue(l);
       hook(l);
@@ -555,7 +558,7 @@ struct Fp32Engine {
     put_input(TAP_FB, xb);
 #pragma unroll 1
     for (int l = 1; l < NLAYER; ++l) {
-      if (l > 1) __syncthreads();  // the hooks rely on the layer barriers between them
+      if (l > 1) row_sync();  // the hooks rely on the layer barriers between them
       hook(l);
     }
     run();

@@ -447,27 +447,35 @@ __global__ void k_dec_prep(Plan p, const uint8_t* __restrict__ bits, const uint6
 
 // ------------------------------------------------------------ decoder
 // One cluster of nc CTAs per unit; slot S = rank*64 + row holds rows
-// r = S (mod 64*nc) in turn.  Per front t: the 8 threads of a row
-// gather their share of the window from the shared-memory ring, run the
-// network, and search the Q1' table; the lower half-warps of group 0 (warps
-// 0-3, lanes 0-15, one thread per row) own the rows' rANS lanes: state
-// update, interleaved word reads (ballot/popc within a warp; a G = 32 group
-// spans two warps and adds the first warp's count through shared memory),
-// pixel publication to HBM, the ring and the next CTA's halo (DSMEM).
+// r = S (mod 64*nc) in turn.  A CTA has 16 row warps (the network, softmax and
+// symbol search of its 64 slots, 8 threads per row, as the encoder) and one
+// rANS warp (lane l owns the rANS lanes of CTA rows l and l + 32).
+//
+// Per front t, row warps: the two fresh taps -> network (layer 1 over
+// the 76 older taps was issued during front t-1; the next front's older taps
+// are gathered in an MMA wait) -> wait for the rANS warp's slots of front t ->
+// softmax / Q1' / search -> the finder thread publishes the pixel (ring, the
+// next CTA's halo via DSMEM, zero pads, HBM) and (f_s, c_s) for the rANS warp
+// -> cluster barrier (the next front's layer-1 MMA is issued between its
+// arrive and wait).
+// rANS warp: apply front t-1's steps (state update, renormalisation words
+// from registers prefetched a front earlier, one ballot per 32-row half, group
+// cursors) -> start rows beginning at front t -> publish the slots x & 0xFFFF
+// (named barrier 7: arrive) -> prefetch the words front t's steps may read ->
+// cluster barrier.  Its work overlaps the row warps' network entirely.
+constexpr int DEC_THREADS = NTHREADS + 32;
+
 template <int PREC, bool PROF>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(DEC_THREADS, 1)
     k_decode(Plan p, DevWeights w, const uint8_t* __restrict__ bits, const uint64_t* __restrict__ cont_off,
              const uint32_t* __restrict__ sbase, const uint32_t* __restrict__ slen, uint8_t* __restrict__ out,
              int32_t* __restrict__ status, unsigned long long* __restrict__ prof) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t bar[2];
+  __shared__ uint64_t bar[3];  // 0 MMA completion, 1 a_ready (16 row warps), 2 spare
   __shared__ uint32_t tslot;
-  __shared__ uint32_t s_cnt[4][2];  // per owner warp and pass parity: readers | active<<16
-  __shared__ uint32_t s_slot[ROWS];  // the row's rANS slot x & 0xFFFF (owner -> the row's 8 threads)
-  __shared__ uint2 s_res[ROWS];      // (f_s, c_s) of the decoded symbol (finder -> owner, next front)
-  const int row = tile_row();
+  __shared__ uint32_t s_slot[ROWS];  // the row's rANS slot x & 0xFFFF (rANS warp -> the row's 8 threads)
+  __shared__ uint2 s_res[ROWS];      // (f_s, c_s) of the decoded symbol (finder -> rANS warp, next front)
   const uint32_t lane = lane_id();
-  const bool owner = threadIdx.x < 128 && half_id() == 0;  // group 0, lower half-warp
   const uint32_t NC = p.nc, NS = ROWS * NC;
   const uint32_t ns_shift = 6u + (uint32_t)(__ffs((int)NC) - 1);
   // optional phase profile (thread 0 of each CTA), see Prof in dlic_device.cuh:
@@ -477,179 +485,36 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t rank = NC > 1 ? cluster_rank() : 0u;
   const uint32_t u = blockIdx.x / NC;
   const Unit un = unit_info(p, u);
-  const uint32_t S = rank * ROWS + (uint32_t)row;
 
   typename EngineSel<PREC>::T eng;
   uint8_t* ring = engine_setup<PREC>(eng, smem, w, bar, &tslot);
   uint32_t* cursor = reinterpret_cast<uint32_t*>(ring + RING_BYTES + 16);  // 16 zero bytes after the ring
   uint32_t* s_sbase = cursor + ((un.ngroups + 3u) & ~3u);                   // per-group stream table
   uint32_t* s_slen = s_sbase + ((un.ngroups + 3u) & ~3u);
-  for (uint32_t i = threadIdx.x; i < RING_BYTES / 16; i += NTHREADS)
+  for (uint32_t i = threadIdx.x; i < RING_BYTES / 16; i += blockDim.x)
     reinterpret_cast<int4*>(ring)[i] = make_int4(0, 0, 0, 0);
   const uint32_t G = p.G;
   const uint32_t g_shift = (uint32_t)(__ffs((int)G) - 1);
-  for (uint32_t g = threadIdx.x; g < un.ngroups; g += NTHREADS) {
+  for (uint32_t g = threadIdx.x; g < un.ngroups; g += blockDim.x) {
     if ((((G * g) & (NS - 1)) >> 6) == rank) cursor[g] = 2u * min(G, un.h - G * g);
     s_sbase[g] = sbase[un.first_stream + g];
     s_slen[g] = slen[un.first_stream + g];
+  }
+  const uint32_t a_ready = smem_u32(&bar[1]);
+  // named barrier 7 (16 row warps sync, the rANS warp arrives): slots ready
+  if (threadIdx.x == 0) {
+    mbar_init(a_ready, NTHREADS / 32);
+    fence_mbar_init();
   }
   if (NC > 1) cluster_sync_all();
   else __syncthreads();
 
   const uint8_t* cbase = bits + cont_off[un.img];
-  uint8_t* oimg = out + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
-  const uint32_t ring_s = smem_u32(ring);
-  const uint32_t halo_base = NC > 1 ? map_cluster(ring_s, (rank + 1) % NC) : ring_s;
-  const uint32_t halo_flip = rank == NC - 1 ? 1u : 0u;  // wrap-around halo feeds the next pass
-  // gather: thread u = 2j + h reads window row dr = u - 8 at ringrow row + u
-  // and (u < 6) the target-row tap dc = u - 6 at ringrow row + 8 (kpos_tap)
-  const int gu = 2 * col_grp() + half_id();
-  const int g9 = gu < 6 ? (8 - gu) + (gu - 6) * RING_ROWS : 0;
   const int uw = (int)un.w, uh = (int)un.h;
   const int T = uw + 3 * (uh - 1);
-  const int wq = (int)(threadIdx.x >> 5);  // owner warp = quadrant (0..3)
-  uint32_t x = 0;
   int err = 0;
-  int pix = 0;
-  // The rANS step of a front is applied one front late, inside the next
-  // front's network (while warps 0-3 would wait on the layer-0/1 MMAs): the
-  // state it produces is first needed by that front's symbol search.
-  //   p_*    the previous front's result of this slot (owners)
-  //   pw0/1  stream words prefetched for it; my_cur/my_sl its group's cursor/length
-  bool p_act = false;
-  int p_r = 0, p_c = 0;
-  uint32_t pw0 = 0, pw1 = 0, first_lane = 0, my_sl = 0, my_cur = 0;
-
-  // (a) x' = f*(x>>16) + slot - c for the previous front's rows, renormalised
-  // with interleaved word reads (ballot/popc within a warp; a G = 32 group
-  // spans two warps and adds the first warp's count through shared memory).
-  // Split in two halves around a layer barrier of the network (no barrier of
-  // its own): rans_a updates the states and publishes the warps' reader
-  // counts, rans_b assigns the words and advances the cursors.
-  // Lanes of my rANS group among this warp's owner lanes (0-15, rows 16q +
-  // lane of the CTA): the slots' rows are 16-aligned per pass, so a group is
-  // all active lanes of my pass parity (G >= 16) or a G-aligned lane range
-  // of them (G < 16).
-  auto group_mask = [&](bool act, uint32_t bk, uint32_t am, uint32_t bm) -> uint32_t {
-    if (!act) return 0u;
-    const uint32_t same = am & (bk ? bm : ~bm);
-    return G >= 16 ? same : same & (((1u << G) - 1u) << (lane & ~(G - 1u)));
-  };
-  bool ra_act = false, ra_need = false;
-  uint32_t ra_g = 0, ra_bk = 0, ra_gm = 0, ra_readers = 0;
-  auto rans_a = [&]() {
-    if (threadIdx.x >= 128) return;
-    ra_act = owner && p_act;
-    ra_g = (uint32_t)p_r >> g_shift;  // G is a power of two dividing 32
-    ra_bk = ((uint32_t)p_r >> ns_shift) & 1u;  // pass parity over the slots
-    ra_need = false;
-    if (ra_act) {
-      const uint2 fc = s_res[row];  // written by the thread that found the symbol
-      x = fc.x * (x >> 16) + (x & 0xFFFFu) - fc.y;
-      ra_need = x < RANS_L;
-    }
-    // A warp may hold rows of two groups at once: one finishing and one of
-    // the next pass over the slots (rows NS apart).  They differ in the
-    // pass parity bk, which keys the cross-warp counts below.
-    const uint32_t am = __ballot_sync(0xFFFFFFFFu, ra_act);
-    const uint32_t bm = __ballot_sync(0xFFFFFFFFu, ra_bk != 0);
-    const uint32_t nm = __ballot_sync(0xFFFFFFFFu, ra_need);
-    ra_gm = group_mask(ra_act, ra_bk, am, bm);
-    const uint32_t nb0 = nm & ~bm, nb1 = nm & bm;
-    const bool a0 = (am & ~bm) != 0, a1 = (am & bm) != 0;
-    ra_readers = nm & ra_gm;
-    if (lane == 0) {
-      s_cnt[wq][0] = __popc(nb0) | (a0 ? 0x10000u : 0u);
-      s_cnt[wq][1] = __popc(nb1) | (a1 ? 0x10000u : 0u);
-    }
-  };
-  auto rans_b = [&]() {  // after a CTA barrier following rans_a
-    if (threadIdx.x >= 128) return;
-    const uint32_t nmine = __popc(ra_readers);  // this warp's readers of my group
-    // G = 32: rows of the group's upper 16 (odd warp) read after the even warp's
-    uint32_t before = 0, total = nmine;
-    bool writer = lane == (uint32_t)(__ffs(ra_gm) - 1);
-    if (G == 32) {
-      const uint32_t other = s_cnt[wq ^ 1][ra_bk];
-      if (wq & 1) {
-        before = other & 0xFFFFu;
-        total = before + nmine;
-      } else {
-        total = nmine + (other & 0xFFFFu);
-        writer = writer && !(other & 0x10000u);  // the odd warp writes when it is active
-      }
-    }
-    const uint32_t rk = __popc(ra_readers & ((1u << lane) - 1u));
-    // word from the prefetch registers (all lanes take part in the shuffles)
-    const uint32_t src = G == 32 ? (before + rk) & 31u : (first_lane + rk) & 31u;
-    const uint32_t w0 = __shfl_sync(0xFFFFFFFFu, pw0, src);
-    const uint32_t w1 = __shfl_sync(0xFFFFFFFFu, pw1, src);
-    if (ra_need) {
-      const uint32_t wi = my_cur + before + rk;
-      if (wi < my_sl) x = (x << 16) | (G == 32 && ra_bk == 1 ? w1 : w0);
-      else err = 8;
-    }
-    if (ra_act && writer) cursor[ra_g] = my_cur + total;
-    if (ra_act && p_c == uw - 1 && x != RANS_L) err = 6;  // end-of-lane invariant
-  };
-  // (b) start the lanes of rows beginning at this front and (c) prefetch the
-  // words this front's step may read into registers, so the L2 latency hides
-  // behind a whole front (the cluster barrier invalidates L1).
-  //  G = 32: a warp's active rows of one pass parity form one group; lanes
-  //          0-31 hold words cur..cur+31 of it (the odd warp of the pair
-  //          starts after the even warp's readers, <= 16 of them).
-  //  G < 32: each owner lane holds the word it reads if every earlier row
-  //          of its group in this warp reads one.
-  auto rans_prefetch = [&](int r, int c, bool active) {  // after a CTA barrier following rans_b
-    if (threadIdx.x >= 128) return;
-    const uint32_t g = (uint32_t)r >> g_shift;
-    const bool act = owner && active;
-    const uint32_t bk = ((uint32_t)r >> ns_shift) & 1u;
-    uint32_t my_sb = 0;
-    my_sl = 0;
-    my_cur = 0;
-    pw0 = pw1 = 0;
-    if (act) {
-      my_sb = s_sbase[g];
-      my_sl = s_slen[g];
-      my_cur = cursor[g];
-    }
-    const uint32_t am = __ballot_sync(0xFFFFFFFFu, act);
-    const uint32_t bm = __ballot_sync(0xFFFFFFFFu, bk != 0);
-    if (G == 32) {
-#pragma unroll
-      for (uint32_t b = 0; b < 2; ++b) {
-        const uint32_t mb = am & (b ? bm : ~bm);
-        if (mb) {
-          const uint32_t src = (uint32_t)__ffs(mb) - 1u;
-          const uint32_t sb = __shfl_sync(0xFFFFFFFFu, my_sb, src);
-          const uint32_t sl = __shfl_sync(0xFFFFFFFFu, my_sl, src);
-          const uint32_t cu = __shfl_sync(0xFFFFFFFFu, my_cur, src);
-          const uint16_t* swb = reinterpret_cast<const uint16_t*>(cbase + sb);
-          const uint32_t idx = cu + lane;
-          const uint32_t wv = idx < sl ? (uint32_t)__ldg(swb + idx) : 0u;
-          if (b == 0) pw0 = wv;
-          else pw1 = wv;
-        }
-      }
-    } else {
-      const uint32_t gm = group_mask(act, bk, am, bm);
-      first_lane = gm ? (uint32_t)__ffs(gm) - 1u : lane;
-      const uint32_t idx = my_cur + (lane - first_lane);
-      const uint16_t* swm = reinterpret_cast<const uint16_t*>(cbase + my_sb);
-      pw0 = (act && idx < my_sl) ? (uint32_t)__ldg(swm + idx) : 0u;
-    }
-    if (act && c == 0) {  // the row's lane starts: flushed state (hi, lo)
-      const uint16_t* sw = reinterpret_cast<const uint16_t*>(cbase + my_sb);
-      const uint32_t i = 2u * ((uint32_t)r - G * g);
-      if (i + 1 < my_sl) x = ((uint32_t)__ldg(sw + i) << 16) | (uint32_t)__ldg(sw + i + 1);
-      else err = 8;
-    }
-    if (owner) s_slot[row] = x & 0xFFFFu;  // read by the row's threads after the next layer barrier
-  };
-
-  // slot geometry at front t: row r (active if decoded on front t), column c
-  auto front_rc = [&](int t, int& r, int& c) -> bool {
+  // geometry of slot S at front t: row r (active if decoded on front t), column c
+  auto slot_rc = [&](uint32_t S, int t, int& r, int& c) -> bool {
     const int rlo = t - uw + 1 > 0 ? (t - uw + 3) / 3 : 0;
     const int rhi = min(uh - 1, t / 3);
     r = 0;
@@ -659,215 +524,324 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     c = t - 3 * r;
     return r <= rhi;
   };
-  // ring base of slot (r, c): window cell (dr, dc) of the K order at
-  // bp + (dc)*RING_ROWS for dr = u - 8, tap 9 at bp + g9 (see the ring notes)
-  auto ring_at = [&](int r, int c) -> const uint8_t* {
-    const uint32_t col = (uint32_t)c & 31u;
-    const uint32_t cb = col < 6u ? col + 32u : col;
-    return ring + (((uint32_t)r >> ns_shift) & 1u) * RING_BANK + cb * RING_ROWS + (uint32_t)row;
-  };
-  // Early part of a front (one front ahead): the 76 taps decoded before the
-  // preceding front -> layer-1 input (the two fresh taps' weights are zero in
-  // the MMA image; fp32: overwritten by run_rest).
-  auto early_put = [&](int r, int c) {
-    const uint8_t* bp = ring_at(r, c) + gu;
-    uint32_t tv[10];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) tv[i] = bp[(i - 6) * RING_ROWS];
-    tv[9] = bp[g9];
-    if constexpr (PREC == 1) {
-      const f2 m1 = f2_make(-1.0f, -1.0f);
-      uint32_t a[5];
-#pragma unroll
-      for (int q = 0; q < 5; ++q) {
-        float x0, x1;
-        f2_split(f2_add(f2_bits(0x3F800000u | (tv[2 * q] << 15), 0x3F800000u | (tv[2 * q + 1] << 15)), m1), x0, x1);
-        a[q] = pack_bf16(x0, x1);
-      }
-      eng.put_input(a);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 10; ++i)
-        if (i < 9 || gu < 6) eng.put_input(i < 9 ? 9 * gu + i : 72 + gu, u8_unit(tv[i]));
-    }
-  };
-  // does any slot of this CTA hold an active row at front t (uniform)
-  auto cta_any = [&](int t) -> bool {
-    const int rlo = t - uw + 1 > 0 ? (t - uw + 3) / 3 : 0;
-    const int rhi = min(uh - 1, t / 3);
-    if (rlo > rhi) return false;
-    const uint32_t m = (uint32_t)rlo & (NS - 1), b = rank * ROWS;
-    const uint32_t d = m - b < (uint32_t)ROWS ? 0u : ((b - m) & (NS - 1));
-    return rlo + (int)d <= rhi;
-  };
-  // early part of front t+1, once this thread is done with the network's
-  // output of front t: gather -> layer-1 input; each warp then arrives on
-  // a_ready, which the MMA issuer waits on before issuing layer 0 (issue_early)
-  const uint32_t a_ready = smem_u32(&bar[1]);
-  uint32_t a_phase = 0;
-  // bf16: the layer-1 input has its own TMEM columns (TM_A0), so the gather
-  // can run during the network (early_gather in the layer-3 MMA wait); the
-  // signal only has to follow this thread's load of the logits (the layer-1
-  // MMA overwrites them).  fp32: the input shares the logits buffer.
-  auto early_gather = [&](int rn, int cn) {
-    if constexpr (PREC == 1) early_put(rn, cn);
-  };
-  auto early_signal = [&](int rn, int cn) {
-    if constexpr (PREC == 1) {
-      tc_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(a_ready);
-    } else {
-      quad_sync();  // the row's logits are loaded: its buffer columns are free
-      early_put(rn, cn);
-    }
-  };
-  auto early = [&](int rn, int cn) {
-    early_gather(rn, cn);
-    early_signal(rn, cn);
-  };
-  auto issue_early = [&](bool any_n) {
-    if constexpr (PREC == 1) {
-      if (any_n && threadIdx.x == TcEngine::MMA_ISSUER) {
-        mbar_wait(a_ready, a_phase);
-        eng.issue_l0();
-      }
-      a_phase ^= 1u;  // every warp arrives once per front
-    }
+  auto front_end = [&]() {
+    if (NC > 1) cluster_sync_all();
+    else __syncthreads();
   };
 
-  if (threadIdx.x == 0) {
-    mbar_init(a_ready, NTHREADS / 32);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  int r, c;
-  bool active = front_rc(0, r, c);
-  bool any = cta_any(0);
-  early(r, c);
-  issue_early(any);
-  if (pf.on) pf.t = clock64();
-#pragma unroll 1
-  for (int t = 0; t < T; ++t) {
-    int rn, cn;
-    const bool active_n = front_rc(t + 1, rn, cn);
-    const bool any_n = cta_any(t + 1);
-    bool pub = false;
-    pf.mark(0);
-    if (any) {
-      // the fresh taps (0,-1) and (-1,+2), decoded on front t-1
-      const uint8_t* fp = ring_at(r, c) + 8;
-      const float xa = u8_unit(fp[-RING_ROWS]);
-      const float xb = u8_unit(fp[2 * RING_ROWS - 1]);
-      pf.mark(1);
-      // network; the deferred rANS step and the next front's early gather
-      // run in the MMA waits
-      eng.run_rest(xa, xb, [&](int l) {
-        // warps 0-3: rANS (a) / (b) / prefetch in the layer 2 / 3 / 4 waits
-        // (the layer barriers order them); the next front's early gather in
-        // the layer-3 wait, or the layer-5 wait for warps 0-3 and warp 9
-        // (which issues layer 3)
-        const bool late = threadIdx.x < 128 || (threadIdx.x >> 5) == (TcEngine::MMA_ISSUER2 >> 5);
-        if (l == 1) rans_a();
-        else if (l == 2) {
-          rans_b();
-          if (!late) early_gather(rn, cn);
-        } else if (l == 3) rans_prefetch(r, c, active);
-        else if (l == 4 && late) early_gather(rn, cn);
-      }, PROF ? &pf : nullptr);
-      pf.mark(3);
-      uint32_t fs, cs;
-      bool mine;
-      const int sym = q1_decode(eng, s_slot[row], mine, fs, cs, [&]() { early_signal(rn, cn); }, &pf);
-      // the thread that found the symbol publishes it: own ring, the
-      // successor's halo through DSMEM for the CTA's last 8 rows, zero pads,
-      // and (f_s, c_s) for the row's rANS owner (applied next front)
-      pub = mine && active;
-      pix = sym;
-      if (pub) {
-        s_res[row] = make_uint2(fs, cs);
-        const uint32_t bank = ((uint32_t)r >> ns_shift) & 1u;
-        const uint32_t col = (uint32_t)c & 31u;
-        uint8_t* rp = ring + (uint32_t)row + 8u;
-        rp[bank * RING_BANK + col * RING_ROWS] = (uint8_t)sym;
-        if (col < 8u) rp[bank * RING_BANK + (col + 32u) * RING_ROWS] = (uint8_t)sym;
-        const bool halo = row >= ROWS - 8;
-        const uint32_t hb = bank ^ halo_flip;
-        const uint32_t hrow = (uint32_t)(row - (ROWS - 8));
-        auto hput = [&](uint32_t b, uint32_t pos, uint32_t v) {
-          const uint32_t off = b * RING_BANK + pos * RING_ROWS + hrow;
-          if (NC > 1) st_cluster_u8(halo_base + off, v);
-          else ring[off] = (uint8_t)v;
-        };
-        if (halo) {
-          hput(hb, col, (uint32_t)sym);
-          if (col < 8u) hput(hb, col + 32u, (uint32_t)sym);
-        }
-        if (c == uw - 1) {  // row end: right pad (columns W, W+1) of this row
+  if (threadIdx.x >= NTHREADS) {
+    // ======================================================= rANS warp
+    // Lanes of my group among the warp's lanes for one 32-row half: rows are
+    // 32-aligned per pass, so a group is all active lanes of my pass parity
+    // (G = 32) or a G-aligned lane range of them.
+    auto group_mask = [&](bool act, uint32_t bk, uint32_t am, uint32_t bm) -> uint32_t {
+      if (!act) return 0u;
+      const uint32_t same = am & (bk ? bm : ~bm);
+      return G >= 32 ? same : same & (((1u << G) - 1u) << (lane & ~(G - 1u)));
+    };
+    uint32_t xs[2] = {0u, 0u};                // states of CTA rows lane, lane + 32
+    uint32_t pw[2][2] = {{0u, 0u}, {0u, 0u}};  // prefetched words [half][pass parity]
+    uint32_t fl[2] = {0u, 0u}, cur[2] = {0u, 0u}, sl[2] = {0u, 0u};
+    // apply the step of front t (rows of half hf): x' = f*(x>>16) + slot - c,
+    // renormalised with words in decoder order within each group
+    auto apply = [&](int hf, int t) {
+      int r, c;
+      const bool act = slot_rc(rank * ROWS + 32u * hf + lane, t, r, c);
+      const uint32_t g = (uint32_t)r >> g_shift;
+      const uint32_t bk = ((uint32_t)r >> ns_shift) & 1u;
+      bool need = false;
+      uint32_t x = xs[hf];
+      if (act) {
+        const uint2 fc = s_res[32 * hf + lane];  // written by the thread that found the symbol
+        x = fc.x * (x >> 16) + (x & 0xFFFFu) - fc.y;
+        need = x < RANS_L;
+      }
+      const uint32_t am = __ballot_sync(0xFFFFFFFFu, act);
+      const uint32_t bm = __ballot_sync(0xFFFFFFFFu, bk != 0);
+      const uint32_t nm = __ballot_sync(0xFFFFFFFFu, need);
+      const uint32_t gm = group_mask(act, bk, am, bm);
+      const uint32_t readers = nm & gm;
+      const uint32_t rk = __popc(readers & ((1u << lane) - 1u));
+      const uint32_t src = G == 32 ? rk : (fl[hf] + rk) & 31u;
+      const uint32_t w0 = __shfl_sync(0xFFFFFFFFu, pw[hf][0], src);
+      const uint32_t w1 = __shfl_sync(0xFFFFFFFFu, pw[hf][1], src);
+      if (need) {
+        if (cur[hf] + rk < sl[hf]) x = (x << 16) | (G == 32 && bk == 1 ? w1 : w0);
+        else err = 8;
+      }
+      if (act && lane == (uint32_t)(__ffs(gm) - 1)) cursor[g] = cur[hf] + __popc(readers);
+      if (act && c == uw - 1 && x != RANS_L) err = 6;  // end-of-lane invariant
+      xs[hf] = x;
+    };
+    // prefetch the words the steps of front t may read (registers; the L2
+    // latency hides behind a whole front -- the cluster barrier invalidates L1)
+    //  G = 32: lanes hold words cur..cur+31 of the group of each pass parity
+    //  G < 32: each lane holds the word it reads if every earlier row of its
+    //          group reads one
+    auto prefetch = [&](int hf, int t) {
+      int r, c;
+      const bool act = slot_rc(rank * ROWS + 32u * hf + lane, t, r, c);
+      const uint32_t g = (uint32_t)r >> g_shift;
+      const uint32_t bk = ((uint32_t)r >> ns_shift) & 1u;
+      uint32_t sb = 0;
+      sl[hf] = 0;
+      cur[hf] = 0;
+      pw[hf][0] = pw[hf][1] = 0;
+      if (act) {
+        sb = s_sbase[g];
+        sl[hf] = s_slen[g];
+        cur[hf] = cursor[g];
+      }
+      const uint32_t am = __ballot_sync(0xFFFFFFFFu, act);
+      const uint32_t bm = __ballot_sync(0xFFFFFFFFu, bk != 0);
+      if (G == 32) {
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const uint32_t pc = (uint32_t)(uw + e) & 31u;
-            rp[bank * RING_BANK + pc * RING_ROWS] = 0;
-            if (pc < 8u) rp[bank * RING_BANK + (pc + 32u) * RING_ROWS] = 0;
-            if (halo) {
-              hput(hb, pc, 0u);
-              if (pc < 8u) hput(hb, pc + 32u, 0u);
+        for (uint32_t b = 0; b < 2; ++b) {
+          const uint32_t mb = am & (b ? bm : ~bm);
+          if (mb) {
+            const uint32_t s0 = (uint32_t)__ffs(mb) - 1u;
+            const uint32_t sbb = __shfl_sync(0xFFFFFFFFu, sb, s0);
+            const uint32_t slb = __shfl_sync(0xFFFFFFFFu, sl[hf], s0);
+            const uint32_t cub = __shfl_sync(0xFFFFFFFFu, cur[hf], s0);
+            const uint16_t* swb = reinterpret_cast<const uint16_t*>(cbase + sbb);
+            const uint32_t idx = cub + lane;
+            pw[hf][b] = idx < slb ? (uint32_t)__ldg(swb + idx) : 0u;
+          }
+        }
+      } else {
+        const uint32_t gm = group_mask(act, bk, am, bm);
+        fl[hf] = gm ? (uint32_t)__ffs(gm) - 1u : lane;
+        const uint32_t idx = cur[hf] + (lane - fl[hf]);
+        const uint16_t* swm = reinterpret_cast<const uint16_t*>(cbase + sb);
+        pw[hf][0] = (act && idx < sl[hf]) ? (uint32_t)__ldg(swm + idx) : 0u;
+      }
+    };
+#pragma unroll 1
+    for (int t = 0; t < T; ++t) {
+      if (t > 0) {
+        apply(0, t - 1);
+        apply(1, t - 1);
+        __syncwarp();  // cursor updates before the prefetch reads them
+      }
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {  // rows starting at front t: flushed state (hi, lo)
+        int r, c;
+        if (slot_rc(rank * ROWS + 32u * hf + lane, t, r, c) && c == 0) {
+          const uint32_t g = (uint32_t)r >> g_shift;
+          const uint16_t* sw = reinterpret_cast<const uint16_t*>(cbase + s_sbase[g]);
+          const uint32_t i = 2u * ((uint32_t)r - G * g);
+          if (i + 1 < s_slen[g]) xs[hf] = ((uint32_t)__ldg(sw + i) << 16) | (uint32_t)__ldg(sw + i + 1);
+          else err = 8;
+        }
+        s_slot[32 * hf + lane] = xs[hf] & 0xFFFFu;
+      }
+      asm volatile("bar.arrive 7, %0;" ::"n"(DEC_THREADS) : "memory");  // slots of front t published
+      prefetch(0, t);
+      prefetch(1, t);
+      front_end();
+    }
+    if (T > 0) {  // the last front's steps
+      apply(0, T - 1);
+      apply(1, T - 1);
+    }
+    __syncthreads();  // (1) cursors final
+  } else {
+    // ======================================================= row warps
+    const int row = tile_row();
+    const uint32_t S = rank * ROWS + (uint32_t)row;
+    uint8_t* oimg = out + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
+    const uint32_t ring_s = smem_u32(ring);
+    const uint32_t halo_base = NC > 1 ? map_cluster(ring_s, (rank + 1) % NC) : ring_s;
+    const uint32_t halo_flip = rank == NC - 1 ? 1u : 0u;  // wrap-around halo feeds the next pass
+    // gather: thread u = 2j + h reads window row dr = u - 8 at ringrow row + u
+    // and (u < 6) the target-row tap dc = u - 6 at ringrow row + 8 (kpos_tap)
+    const int gu = 2 * col_grp() + half_id();
+    const int g9 = gu < 6 ? (8 - gu) + (gu - 6) * RING_ROWS : 0;
+    int pix = 0;
+    // ring base of slot (r, c): window cell (dr, dc) of the K order at
+    // bp + (dc)*RING_ROWS for dr = u - 8, tap 9 at bp + g9 (see the ring notes)
+    auto ring_at = [&](int r, int c) -> const uint8_t* {
+      const uint32_t col = (uint32_t)c & 31u;
+      const uint32_t cb = col < 6u ? col + 32u : col;
+      return ring + (((uint32_t)r >> ns_shift) & 1u) * RING_BANK + cb * RING_ROWS + (uint32_t)row;
+    };
+    // Early part of a front (one front ahead): the 76 taps decoded before the
+    // preceding front -> layer-1 input (the two fresh taps' weights are zero in
+    // the MMA image; fp32: overwritten by run_rest).
+    auto early_put = [&](int r, int c) {
+      const uint8_t* bp = ring_at(r, c) + gu;
+      uint32_t tv[10];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) tv[i] = bp[(i - 6) * RING_ROWS];
+      tv[9] = bp[g9];
+      if constexpr (PREC == 1) {
+        const f2 m1 = f2_make(-1.0f, -1.0f);
+        uint32_t a[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          float x0, x1;
+          f2_split(f2_add(f2_bits(0x3F800000u | (tv[2 * q] << 15), 0x3F800000u | (tv[2 * q + 1] << 15)), m1), x0,
+                   x1);
+          a[q] = pack_bf16(x0, x1);
+        }
+        eng.put_input(a);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 10; ++i)
+          if (i < 9 || gu < 6) eng.put_input(i < 9 ? 9 * gu + i : 72 + gu, u8_unit(tv[i]));
+      }
+    };
+    // does any slot of this CTA hold an active row at front t (uniform)
+    auto cta_any = [&](int t) -> bool {
+      const int rlo = t - uw + 1 > 0 ? (t - uw + 3) / 3 : 0;
+      const int rhi = min(uh - 1, t / 3);
+      if (rlo > rhi) return false;
+      const uint32_t m = (uint32_t)rlo & (NS - 1), b = rank * ROWS;
+      const uint32_t d = m - b < (uint32_t)ROWS ? 0u : ((b - m) & (NS - 1));
+      return rlo + (int)d <= rhi;
+    };
+    // early part of front t+1 once this thread is done with the network's
+    // output of front t: gather -> layer-1 input; each warp then arrives on
+    // a_ready, which the MMA issuer waits on before issuing layer 1
+    // (issue_early).  bf16: the layer-1 input has its own TMEM columns
+    // (TM_A0), so the gather runs during the network; the signal only has to
+    // follow this thread's load of the logits (the MMA overwrites them).
+    // fp32: the input shares the logits buffer.
+    uint32_t a_phase = 0;
+    auto early_gather = [&](int rn, int cn) {
+      if constexpr (PREC == 1) early_put(rn, cn);
+    };
+    auto early_signal = [&](int rn, int cn) {
+      if constexpr (PREC == 1) {
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_ready);
+      } else {
+        quad_sync();  // the row's logits are loaded: its buffer columns are free
+        early_put(rn, cn);
+      }
+    };
+    auto issue_early = [&](bool any_n) {
+      if constexpr (PREC == 1) {
+        if (any_n && threadIdx.x == TcEngine::MMA_ISSUER) {
+          mbar_wait(a_ready, a_phase);
+          eng.issue_l0();
+        }
+        a_phase ^= 1u;  // every warp arrives once per front
+      }
+    };
+
+    int r, c;
+    bool active = slot_rc(S, 0, r, c);
+    bool any = cta_any(0);
+    early_gather(r, c);
+    early_signal(r, c);
+    issue_early(any);
+    if (pf.on) pf.t = clock64();
+#pragma unroll 1
+    for (int t = 0; t < T; ++t) {
+      int rn, cn;
+      const bool active_n = slot_rc(S, t + 1, rn, cn);
+      const bool any_n = cta_any(t + 1);
+      bool pub = false;
+      pf.mark(0);
+      if (any) {
+        // the fresh taps (0,-1) and (-1,+2), decoded on front t-1
+        const uint8_t* fp = ring_at(r, c) + 8;
+        const float xa = u8_unit(fp[-RING_ROWS]);
+        const float xb = u8_unit(fp[2 * RING_ROWS - 1]);
+        pf.mark(1);
+        // network; the next front's early gather runs in the layer-3 MMA
+        // wait (layer 5 for warp 9, which issues layer 3)
+        eng.run_rest(xa, xb, [&](int l) {
+          const bool w9 = (threadIdx.x >> 5) == (TcEngine::MMA_ISSUER2 >> 5);
+          if (l == (w9 ? 4 : 2)) early_gather(rn, cn);
+        }, PROF ? &pf : nullptr);
+        pf.mark(3);
+        asm volatile("bar.sync 7, %0;" ::"n"(DEC_THREADS) : "memory");  // this front's slots (rANS warp)
+        uint32_t fs, cs;
+        bool mine;
+        const int sym = q1_decode(eng, s_slot[row], mine, fs, cs, [&]() { early_signal(rn, cn); }, &pf);
+        // the thread that found the symbol publishes it: own ring, the
+        // successor's halo through DSMEM for the CTA's last 8 rows, zero
+        // pads, and (f_s, c_s) for the rANS warp (applied next front)
+        pub = mine && active;
+        pix = sym;
+        if (pub) {
+          s_res[row] = make_uint2(fs, cs);
+          const uint32_t bank = ((uint32_t)r >> ns_shift) & 1u;
+          const uint32_t col = (uint32_t)c & 31u;
+          uint8_t* rp = ring + (uint32_t)row + 8u;
+          rp[bank * RING_BANK + col * RING_ROWS] = (uint8_t)sym;
+          if (col < 8u) rp[bank * RING_BANK + (col + 32u) * RING_ROWS] = (uint8_t)sym;
+          const bool halo = row >= ROWS - 8;
+          const uint32_t hb = bank ^ halo_flip;
+          const uint32_t hrow = (uint32_t)(row - (ROWS - 8));
+          auto hput = [&](uint32_t b, uint32_t pos, uint32_t v) {
+            const uint32_t off = b * RING_BANK + pos * RING_ROWS + hrow;
+            if (NC > 1) st_cluster_u8(halo_base + off, v);
+            else ring[off] = (uint8_t)v;
+          };
+          if (halo) {
+            hput(hb, col, (uint32_t)sym);
+            if (col < 8u) hput(hb, col + 32u, (uint32_t)sym);
+          }
+          if (c == uw - 1) {  // row end: right pad (columns W, W+1) of this row
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const uint32_t pc = (uint32_t)(uw + e) & 31u;
+              rp[bank * RING_BANK + pc * RING_ROWS] = 0;
+              if (pc < 8u) rp[bank * RING_BANK + (pc + 32u) * RING_ROWS] = 0;
+              if (halo) {
+                hput(hb, pc, 0u);
+                if (pc < 8u) hput(hb, pc + 32u, 0u);
+              }
+            }
+          }
+          // left pad (pos 26..31) of the slot's next row, in the other bank:
+          // after the previous occupant's readers are done (front 3r + 23 at
+          // the latest, W <= 3*NS) and well before the next row's early gather
+          if (c == min(24, uw - 1)) {
+#pragma unroll
+            for (uint32_t pc = 26; pc < 32; ++pc) {
+              rp[(bank ^ 1u) * RING_BANK + pc * RING_ROWS] = 0;
+              if (halo) hput(hb ^ 1u, pc, 0u);
             }
           }
         }
-        // left pad (pos 26..31) of the slot's next row, in the other bank:
-        // after the previous occupant's readers are done (front 3r + 23 at
-        // the latest, W <= 3*NS) and well before the next row's early gather
-        if (c == min(24, uw - 1)) {
-#pragma unroll
-          for (uint32_t pc = 26; pc < 32; ++pc) {
-            rp[(bank ^ 1u) * RING_BANK + pc * RING_ROWS] = 0;
-            if (halo) hput(hb ^ 1u, pc, 0u);
-          }
-        }
+        pf.mark(9);
+      } else {
+        asm volatile("bar.sync 7, %0;" ::"n"(DEC_THREADS) : "memory");  // keep the barrier in step
+        early_gather(rn, cn);
+        early_signal(rn, cn);
       }
-      pf.mark(9);
-    } else {
-      rans_a();
-      __syncthreads();
-      rans_b();
-      __syncthreads();
-      rans_prefetch(r, c, active);
-      early(rn, cn);
+      // end-of-front barrier; the next front's layer-1 MMA is issued between
+      // its arrive and wait.  (A point-to-point variant -- halo writers
+      // arriving remotely on a successor mbarrier -- measured slower.)
+      if (NC > 1) {
+        cluster_arrive();
+        issue_early(any_n);
+        cluster_wait();
+      } else {
+        issue_early(any_n);
+        __syncthreads();
+      }
+      // the pixel's HBM store after the barrier: its release need not wait for it
+      if (pub) oimg[(uint64_t)r * p.W + c] = (uint8_t)pix;
+      pf.mark(10);
+      r = rn;
+      c = cn;
+      active = active_n;
+      any = any_n;
     }
-    p_act = active;
-    p_r = r;
-    p_c = c;
-    // end-of-front barrier; the next front's layer-0 MMA is issued between
-    // its arrive and wait.  (A point-to-point variant -- halo writers arriving
-    // remotely on a successor mbarrier -- measured slower: 15.5 vs 15.05 ms.)
-    if (NC > 1) {
-      cluster_arrive();
-      issue_early(any_n);
-      cluster_wait();
-    } else {
-      issue_early(any_n);
-      __syncthreads();
-    }
-    // the pixel's HBM store after the barrier: its release need not wait for it
-    if (pub) oimg[(uint64_t)r * p.W + c] = (uint8_t)pix;
-    pf.mark(10);
-    r = rn;
-    c = cn;
-    active = active_n;
-    any = any_n;
+    __syncthreads();  // (1) cursors final
   }
-  rans_a();  // the last front's step
-  __syncthreads();
-  rans_b();
-  __syncthreads();
-
   if (pf.on) {
     for (int kk = 0; kk < 11; ++kk) atomicAdd(prof + kk, pf.acc[kk]);
     for (int kk = 0; kk < 4; ++kk) atomicAdd(prof + 16 + kk, pf.acc2[kk]);
   }
-  for (uint32_t g = threadIdx.x; g < un.ngroups; g += NTHREADS) {
+  for (uint32_t g = threadIdx.x; g < un.ngroups; g += blockDim.x) {
     if ((((G * g) & (NS - 1)) >> 6) == rank && cursor[g] != slen[un.first_stream + g]) err = 6;
   }
   if (err) atomicMax(status + un.img, err);
@@ -933,7 +907,7 @@ static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uin
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.n_img * p.upi * p.nc);
-  cfg.blockDim = dim3(NTHREADS);
+  cfg.blockDim = dim3(DEC_THREADS);
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
   if (p.nc > 8) {
