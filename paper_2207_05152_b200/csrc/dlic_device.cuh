@@ -457,11 +457,17 @@ struct TcEngine {
   // bias + ReLU + bf16 -> next A; this thread's columns [32j+16h, +16)
   // (packed column 16j+8h+q holds activations 32j+16h+2q, +1: identity K order).
   // Layer 0 also adds the fresh taps: fma(xb, wb, fma(xa, wa, acc)) + bias.
+  // this thread's 16 biases of layer l (loaded before the MMA wait, so the
+  // adds after the TMEM load are register-only)
+  __device__ __forceinline__ void load_bias(int l, float2 (&bq)[8]) const {
+    const float2* b2 = reinterpret_cast<const float2*>(bias + l * HID + 32 * col_grp() + 16 * half_id());
+#pragma unroll
+    for (int q = 0; q < 8; ++q) bq[q] = b2[q];
+  }
   template <bool L0>
-  __device__ __forceinline__ void epilogue(int l, float xa, float xb) const {
+  __device__ __forceinline__ void epilogue(const float2 (&b2)[8], float xa, float xb) const {
     const uint32_t lo = lane_off();
     const int j = col_grp(), h = half_id();
-    const float2* b2 = reinterpret_cast<const float2*>(bias + l * HID + 32 * j + 16 * h);
     const float4* fw = reinterpret_cast<const float4*>(bias + FRESH_OFF) + 16 * j + 8 * h;
     uint32_t v[16];
     tmem_ld16h<16>(tmem + lo + TM_D + 32u * (uint32_t)j, v);
@@ -491,9 +497,11 @@ struct TcEngine {
   template <class Hook>
   __device__ __forceinline__ void run_rest(float xa, float xb, Hook&& hook, Prof* pf = nullptr) {
     if (pf) pf->t2 = clock64();
+    float2 bq[8];
+    load_bias(0, bq);
     wait_mma();
     if (pf) pf->mark2(2);
-    epilogue<true>(0, xa, xb);
+    epilogue<true>(bq, xa, xb);
     if (pf) pf->mark2(3);
 #pragma unroll 1
     for (int l = 1; l < NLAYER; ++l) {
@@ -503,9 +511,10 @@ struct TcEngine {
       if (threadIdx.x == issuer(l)) issue(l);
       hook(l);
       if (pf) pf->mark2(1);
+      if (l < NLAYER - 1) load_bias(l, bq);
       wait_mma();
       if (pf) pf->mark2(2);
-      if (l < NLAYER - 1) epilogue<false>(l, 0.0f, 0.0f);
+      if (l < NLAYER - 1) epilogue<false>(bq, 0.0f, 0.0f);
       if (pf) pf->mark2(3);
     }
   }
