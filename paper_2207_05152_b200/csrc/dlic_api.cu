@@ -300,6 +300,8 @@ dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Pl
   p.cap_words = 2 * p.G + p.G * p.tw;
   p.hdr_bytes = 58 + 4 * p.spi;
   p.tiles_per_unit = (uint32_t)(((uint64_t)p.tw * p.th + ROWS - 1) / ROWS);
+  if ((uint64_t)n * p.upi * p.tiles_per_unit >= (1ull << 32))
+    return fail(DLIC_E_INVALID_ARG, "batch too large for one call (>= 2^32 encoder tiles): split it");
   const uint32_t slots = (p.tw + 2) / 3;  // max rows on one front = ceil(tw/3)
   p.nc = 0;
   for (uint32_t nc = 1; nc <= 16; nc *= 2)

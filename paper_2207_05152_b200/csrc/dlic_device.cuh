@@ -460,7 +460,7 @@ struct TcEngine {
   // this thread's 16 biases of layer l (loaded before the MMA wait, so the
   // adds after the TMEM load are register-only)
   __device__ __forceinline__ void load_bias(int l, float2 (&bq)[8]) const {
-    const float2* b2 = reinterpret_cast<const float2*>(bias + l * HID + 32 * col_grp() + 16 * half_id());
+    const float2* b2 = reinterpret_cast<const float2*>(bias + 32 * col_grp() + 16 * half_id()) + l * (HID / 2);
 #pragma unroll
     for (int q = 0; q < 8; ++q) bq[q] = b2[q];
   }
@@ -695,132 +695,181 @@ __device__ __forceinline__ f2 f2_exp2_poly(f2 t) {
 // ENC: also returns f and the half-local exclusive cum of `sym` when it lies in
 // this thread's columns.  probs (nullable): p_i of the
 // row (debug export, 256 entries).
+// The softmax -> Q1' -> CDF computation of one row in stages, so that the
+// encoder can interleave them with the next tile's network (each stage is a
+// fixed instruction sequence; q1_table runs them back to back and gives the
+// decoder the identical arithmetic):
+//   s1a  biased logits (in place) and the group max m_j
+//   s1b  e_i = 2^(l_i*log2e - m_j*log2e) for pairs [q0, q1) (in place),
+//        accumulated into the even/odd pair sums zz in pair order
+//   s1c  z_j (halves combined)
+//   x1   one exchange of (m_j, z_j): M = max_j m_j, Z = sum_j z_j 2^(m_j - M)
+//        in a fixed order, this group's scale w_j / Z
+//   sA   pass A: f_i = 1 + floor(p_i * 65279) (x + 2^23 rounded toward -inf
+//        has ulp 1) in place, block sums; posts the group sum
+//   x2   the F exchange: per-group sums, residual R
+template <bool ENC>
+struct Q1Work {
+  float m = 0.0f, z = 0.0f;
+  f2 zz;
+  f2 inv;
+  float fs = 0.0f, cs_local = 0.0f;
+  Q1Row r;
+
+  template <class Eng>
+  __device__ __forceinline__ void s1a(const Eng& e, uint32_t (&v)[32]) {
+    float mm = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const float2 b = e.bias_pair(q);
+      float l0, l1;
+      f2_split(f2_add(f2_bits(v[2 * q], v[2 * q + 1]), f2_make(b.x, b.y)), l0, l1);
+      v[2 * q] = __float_as_uint(l0);
+      v[2 * q + 1] = __float_as_uint(l1);
+      mm = fmax3(mm, l0, l1);
+    }
+    m = fmaxf(mm, __shfl_xor_sync(0xFFFFFFFFu, mm, 16));  // m_j, equal in both halves
+    zz = f2_splat(0.0f);
+  }
+  template <int Q0, int Q1>
+  __device__ __forceinline__ void s1b(uint32_t (&v)[32]) {
+    const f2 nm = f2_splat(__fmul_rn(-m, LOG2E));
+    const f2 l2e = f2_splat(LOG2E);
+#pragma unroll
+    for (int q = Q0; q < Q1; ++q) {
+      const f2 t = f2_fma(f2_bits(v[2 * q], v[2 * q + 1]), l2e, nm);
+      float e0, e1;
+      if (q % 8 >= 5) {  // 6 of 16 pairs on the FMA pipe, the rest on MUFU
+        f2_split(f2_exp2_poly(t), e0, e1);
+      } else {
+        float t0, t1;
+        f2_split(t, t0, t1);
+        e0 = ex2_approx(t0);
+        e1 = ex2_approx(t1);
+      }
+      zz = f2_add(zz, f2_make(e0, e1));
+      v[2 * q] = __float_as_uint(e0);
+      v[2 * q + 1] = __float_as_uint(e1);
+    }
+  }
+  __device__ __forceinline__ void s1c() {
+    float za, zb;
+    f2_split(zz, za, zb);
+    const float zl = __fadd_rn(za, zb);
+    z = __fadd_rn(zl, __shfl_xor_sync(0xFFFFFFFFu, zl, 16));  // commutative: identical in both halves
+  }
+  template <class Eng>
+  __device__ __forceinline__ void x1(const Eng& e) {
+    const int j = col_grp();
+    e.xput(0, __float_as_uint(m));
+    e.xput(1, __float_as_uint(z));
+    e.xsync();
+    uint32_t x4[4], z4[4];
+    e.xget4(0, x4);
+    e.xget4(1, z4);
+    // M = max_j m_j;  Z = sum_j z_j 2^(m_j - M) in a fixed order;  group scale
+    // s_j = 2^(m_j - M) / Z, so p_i = e_i * s_j = exp(l_i - M) / Z.
+    const float M = fmaxf(fmaxf(__uint_as_float(x4[0]), __uint_as_float(x4[1])),
+                          fmaxf(__uint_as_float(x4[2]), __uint_as_float(x4[3])));
+    const float nM = __fmul_rn(-M, LOG2E);
+    float wg[4];
+#pragma unroll
+    for (int g = 0; g < NGRP; ++g) wg[g] = ex2_approx(__fmaf_rn(__uint_as_float(x4[g]), LOG2E, nM));
+    const float Z = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(__uint_as_float(z4[0]), wg[0]),
+                                                  __fmul_rn(__uint_as_float(z4[1]), wg[1])),
+                                        __fmul_rn(__uint_as_float(z4[2]), wg[2])),
+                              __fmul_rn(__uint_as_float(z4[3]), wg[3]));
+    float wmine = wg[0];
+#pragma unroll
+    for (int g = 1; g < NGRP; ++g)
+      if (g == j) wmine = wg[g];
+    inv = f2_splat(__fmul_rn(wmine, __frcp_rn(Z)));
+  }
+  template <class Eng>
+  __device__ __forceinline__ void sA(const Eng& e, uint32_t (&v)[32], int sym, float* probs) {
+    const int h = half_id();
+    const int c0 = 64 * col_grp() + 32 * h;
+    const f2 scale = f2_splat(Q1_SCALE);
+    const f2 two23 = f2_splat(8388608.0f);
+    const f2 fbias = f2_splat(-8388607.0f);  // y - 2^23 + 1 = 1 + floor(x), exact
+    f2 FB[4] = {f2_splat(0.0f), f2_splat(0.0f), f2_splat(0.0f), f2_splat(0.0f)};  // 8-entry blocks
+    fs = 0.0f;
+    cs_local = 0.0f;
+    float cum = 0.0f;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const f2 p = f2_mul(f2_bits(v[2 * q], v[2 * q + 1]), inv);
+      const f2 f = f2_add(f2_add_rm(f2_mul(p, scale), two23), fbias);
+      FB[q >> 2] = f2_add(FB[q >> 2], f);
+      float f0, f1;
+      f2_split(f, f0, f1);
+      if (ENC) {
+        const int i0 = c0 + 2 * q;
+        if (i0 == sym) {
+          fs = f0;
+          cs_local = cum;
+        }
+        if (i0 + 1 == sym) {
+          fs = f1;
+          cs_local = __fadd_rn(cum, f0);
+        }
+        cum = __fadd_rn(cum, __fadd_rn(f0, f1));
+      }
+      if (probs) {
+        float p0, p1;
+        f2_split(p, p0, p1);
+        probs[c0 + 2 * q] = p0;
+        probs[c0 + 2 * q + 1] = p1;
+      }
+      v[2 * q] = __float_as_uint(f0);
+      v[2 * q + 1] = __float_as_uint(f1);
+    }
+    float B[4];  // exact integer block sums
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      float Fa, Fb;
+      f2_split(FB[b], Fa, Fb);
+      B[b] = __fadd_rn(Fa, Fb);
+    }
+    r.P[0] = B[0];
+    r.P[1] = B[0] + B[1];
+    r.P[2] = r.P[1] + B[2];
+    r.Fmine = r.P[2] + B[3];
+    const float Fo = __shfl_xor_sync(0xFFFFFFFFu, r.Fmine, 16);
+    r.hbase = h ? Fo : 0.0f;
+    e.xput(2, __float_as_uint(__fadd_rn(r.Fmine, Fo)));  // exact integer sum
+  }
+  template <class Eng>
+  __device__ __forceinline__ void x2(const Eng& e) {
+    e.xsync();
+    uint32_t x4[4];
+    e.xget4(2, x4);
+#pragma unroll
+    for (int g = 0; g < NGRP; ++g) r.F[g] = __uint_as_float(x4[g]);
+    r.R = 65536.0f - (((r.F[0] + r.F[1]) + r.F[2]) + r.F[3]);
+  }
+};
+
+// Passes 1 and A over this thread's 32 values, held in registers throughout:
+// v = raw logits on entry (ld32), the integer table f (as floats) on return.
+// ENC: also returns f and the half-local exclusive cum of `sym` when it lies
+// in this thread's columns.  probs (nullable): p_i of the row (debug export).
 template <bool ENC, class Eng>
 __device__ __forceinline__ Q1Row q1_table(const Eng& e, uint32_t (&v)[32], int sym, float& fs, float& cs_local,
                                           float* probs, Prof* pf = nullptr) {
-  const int j = col_grp(), h = half_id();
-  const int c0 = 64 * j + 32 * h;
-  // pass 1 (one TMEM round trip): biased logits, the group max m_j, and
-  // e_i = 2^(l_i*log2e - m_j*log2e) relative to the group max, stored back;
-  // z_j as even/odd pair partial sums, combined across the half-warps.
-  float m = -INFINITY;
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const float2 b = e.bias_pair(q);
-    float l0, l1;
-    f2_split(f2_add(f2_bits(v[2 * q], v[2 * q + 1]), f2_make(b.x, b.y)), l0, l1);
-    v[2 * q] = __float_as_uint(l0);
-    v[2 * q + 1] = __float_as_uint(l1);
-    m = fmax3(m, l0, l1);
-  }
-  m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, 16));  // m_j, equal in both halves
-  const f2 nm = f2_splat(__fmul_rn(-m, LOG2E));
-  const f2 l2e = f2_splat(LOG2E);
-  f2 zz = f2_splat(0.0f);
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const f2 t = f2_fma(f2_bits(v[2 * q], v[2 * q + 1]), l2e, nm);
-    float e0, e1;
-    if (q % 8 >= 5) {  // 6 of 16 pairs on the FMA pipe, the rest on MUFU
-      f2_split(f2_exp2_poly(t), e0, e1);
-    } else {
-      float t0, t1;
-      f2_split(t, t0, t1);
-      e0 = ex2_approx(t0);
-      e1 = ex2_approx(t1);
-    }
-    zz = f2_add(zz, f2_make(e0, e1));
-    v[2 * q] = __float_as_uint(e0);
-    v[2 * q + 1] = __float_as_uint(e1);
-  }
-  float za, zb;
-  f2_split(zz, za, zb);
-  float z = __fadd_rn(za, zb);
-  z = __fadd_rn(z, __shfl_xor_sync(0xFFFFFFFFu, z, 16));  // commutative: identical in both halves
+  Q1Work<ENC> w;
+  w.s1a(e, v);
+  w.template s1b<0, 16>(v);
+  w.s1c();
   if (pf) pf->mark(4);
-  e.xput(0, __float_as_uint(m));
-  e.xput(1, __float_as_uint(z));
-  e.xsync();
-  uint32_t x4[4], z4[4];
-  e.xget4(0, x4);
-  e.xget4(1, z4);
-  // M = max_j m_j;  Z = sum_j z_j 2^(m_j - M) in a fixed order;  group scale
-  // s_j = 2^(m_j - M) / Z, so p_i = e_i * s_j = exp(l_i - M) / Z.
-  const float M = fmaxf(fmaxf(__uint_as_float(x4[0]), __uint_as_float(x4[1])),
-                        fmaxf(__uint_as_float(x4[2]), __uint_as_float(x4[3])));
-  const float nM = __fmul_rn(-M, LOG2E);
-  float wg[4];
-#pragma unroll
-  for (int g = 0; g < NGRP; ++g) wg[g] = ex2_approx(__fmaf_rn(__uint_as_float(x4[g]), LOG2E, nM));
-  const float Z = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(__uint_as_float(z4[0]), wg[0]),
-                                                __fmul_rn(__uint_as_float(z4[1]), wg[1])),
-                                      __fmul_rn(__uint_as_float(z4[2]), wg[2])),
-                            __fmul_rn(__uint_as_float(z4[3]), wg[3]));
-  float wmine = wg[0];
-#pragma unroll
-  for (int g = 1; g < NGRP; ++g)
-    if (g == j) wmine = wg[g];
-  const f2 inv = f2_splat(__fmul_rn(wmine, __frcp_rn(Z)));
+  w.x1(e);
   if (pf) pf->mark(5);
-  const f2 scale = f2_splat(Q1_SCALE);
-  const f2 two23 = f2_splat(8388608.0f);
-  const f2 fbias = f2_splat(-8388607.0f);  // y - 2^23 + 1 = 1 + floor(x), exact
-  // pass A: p_i, f_i = 1 + floor(p_i * 65279) (x + 2^23 rounded toward -inf
-  // has ulp 1), kept in v as floats; half sum
-  f2 FB[4] = {f2_splat(0.0f), f2_splat(0.0f), f2_splat(0.0f), f2_splat(0.0f)};  // 8-entry blocks
-  fs = 0.0f;
-  cs_local = 0.0f;
-  float cum = 0.0f;
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const f2 p = f2_mul(f2_bits(v[2 * q], v[2 * q + 1]), inv);
-    const f2 f = f2_add(f2_add_rm(f2_mul(p, scale), two23), fbias);
-    FB[q >> 2] = f2_add(FB[q >> 2], f);
-    float f0, f1;
-    f2_split(f, f0, f1);
-    if (ENC) {
-      const int i0 = c0 + 2 * q;
-      if (i0 == sym) {
-        fs = f0;
-        cs_local = cum;
-      }
-      if (i0 + 1 == sym) {
-        fs = f1;
-        cs_local = __fadd_rn(cum, f0);
-      }
-      cum = __fadd_rn(cum, __fadd_rn(f0, f1));
-    }
-    if (probs) {
-      float p0, p1;
-      f2_split(p, p0, p1);
-      probs[c0 + 2 * q] = p0;
-      probs[c0 + 2 * q + 1] = p1;
-    }
-    v[2 * q] = __float_as_uint(f0);
-    v[2 * q + 1] = __float_as_uint(f1);
-  }
-  float B[4];  // exact integer block sums
-#pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    float Fa, Fb;
-    f2_split(FB[b], Fa, Fb);
-    B[b] = __fadd_rn(Fa, Fb);
-  }
-  Q1Row r;
-  r.P[0] = B[0];
-  r.P[1] = B[0] + B[1];
-  r.P[2] = r.P[1] + B[2];
-  r.Fmine = r.P[2] + B[3];
-  const float Fo = __shfl_xor_sync(0xFFFFFFFFu, r.Fmine, 16);
-  r.hbase = h ? Fo : 0.0f;
+  w.sA(e, v, sym, probs);
   if (pf) pf->mark(7);
-  e.xput(2, __float_as_uint(__fadd_rn(r.Fmine, Fo)));  // exact integer sum
-  e.xsync();
-  e.xget4(2, x4);
-#pragma unroll
-  for (int g = 0; g < NGRP; ++g) r.F[g] = __uint_as_float(x4[g]);
-  r.R = 65536.0f - (((r.F[0] + r.F[1]) + r.F[2]) + r.F[3]);
-  return r;
+  w.x2(e);
+  fs = w.fs;
+  cs_local = w.cs_local;
+  return w.r;
 }
 
 __device__ __forceinline__ float q1_base(const Q1Row& r) {

@@ -166,48 +166,146 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     k_enc_mlp(Plan p, DevWeights w, const uint8_t* __restrict__ imgs, uint32_t* __restrict__ fc,
               float* __restrict__ dbg_logits, float* __restrict__ dbg_probs, uint16_t* __restrict__ dbg_freqs) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t bar[2];
+  __shared__ uint64_t bar[3];  // 0 MMA completion, 2 spare (engine)
   __shared__ uint32_t tslot;
   const int row = tile_row();
   typename EngineSel<PREC>::T eng;
   engine_setup<PREC>(eng, smem, w, bar, &tslot);
   const uint64_t total = (uint64_t)p.n_img * p.upi * p.tiles_per_unit;
   const bool dbg = dbg_logits || dbg_probs || dbg_freqs;
-#pragma unroll 1
-  for (uint64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
-    const uint32_t u = (uint32_t)(tile / p.tiles_per_unit);
-    const uint32_t k = (uint32_t)(tile % p.tiles_per_unit);
-    const Unit un = unit_info(p, u);
-    const uint32_t q = k * (uint32_t)ROWS + (uint32_t)row;
-    const bool valid = q < un.w * un.h;
-    const int r = valid ? (int)(q / un.w) : 0, c = valid ? (int)(q % un.w) : 0;
-    const uint8_t* img = imgs + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
-    const int uw = (int)un.w;
-    auto get = [&](int dr, int dc) -> uint32_t {  // branch-free: invalid taps load the target and mask
-      const int rr = r + dr, cc = c + dc;
-      const bool ok = valid && rr >= 0 && (unsigned)cc < (unsigned)uw;
-      const uint32_t v = __ldg(img + (ok ? (int64_t)rr * p.W + cc : (int64_t)r * p.W + c));
+
+  // this thread's pixel of a tile (64 consecutive pixels of a unit in raster
+  // order).  The pipelined loop walks its tiles in order, so the unit (and
+  // its divisions) is recomputed only when a tile starts a new unit.
+  struct Px {
+    bool valid;
+    int r, c, uw, sym;
+    const uint8_t* img;
+    uint64_t gi, fci;
+  };
+  uint32_t cu = 0xFFFFFFFFu;  // cached unit
+  Unit cun;
+  auto pixel = [&](uint64_t tile) -> Px {
+    Px x;
+    const uint32_t t32 = (uint32_t)tile;  // < 2^32 tiles (checked by the planner)
+    const uint32_t u = t32 / p.tiles_per_unit;
+    const uint32_t kt = t32 - u * p.tiles_per_unit;
+    if (u != cu) {
+      cu = u;
+      cun = unit_info(p, u);
+    }
+    const uint32_t q = kt * (uint32_t)ROWS + (uint32_t)row;
+    x.valid = q < cun.w * cun.h;
+    x.r = x.valid ? (int)(q / cun.w) : 0;
+    x.c = x.valid ? (int)(q - (uint32_t)x.r * cun.w) : 0;
+    x.uw = (int)cun.w;
+    x.img = imgs + (uint64_t)cun.img * p.W * p.H + (uint64_t)cun.y0 * p.W + cun.x0;
+    x.sym = x.valid ? (int)__ldg(x.img + (uint64_t)x.r * p.W + x.c) : 0;
+    x.gi = (uint64_t)cun.img * p.W * p.H + (uint64_t)(cun.y0 + x.r) * p.W + (cun.x0 + x.c);
+    x.fci = cun.fc_off + q;
+    return x;
+  };
+  auto getter = [&](const Px& x) {
+    return [&x, &p](int dr, int dc) -> uint32_t {  // branch-free: invalid taps load the target and mask
+      const int rr = x.r + dr, cc = x.c + dc;
+      const bool ok = x.valid && rr >= 0 && (unsigned)cc < (unsigned)x.uw;
+      const uint32_t v = __ldg(x.img + (ok ? (int64_t)rr * p.W + cc : (int64_t)x.r * p.W + x.c));
       return ok ? v : 0u;
     };
-    feed<PREC>(eng, get);
-    eng.start_l0();
-    eng.run_rest(u8_unit(get(0, -1)), u8_unit(get(-1, 2)), [](int) {});
-    const int sym = valid ? (int)__ldg(img + (uint64_t)r * p.W + c) : 0;
-    const uint64_t gi = (uint64_t)un.img * p.W * p.H + (uint64_t)(un.y0 + r) * p.W + (un.x0 + c);
-    if (dbg && dbg_logits) {  // raw logits (bias added) of this thread's 32 columns
-      uint32_t v[32];
-      eng.ld32(v);
-      if (valid)
-        for (int i = 0; i < 32; ++i) {
-          const int cc = 64 * col_grp() + 32 * half_id() + i;
-          float lv = __uint_as_float(v[i]);
-          if constexpr (PREC == 1) lv = __fadd_rn(lv, eng.bias[BIAS_OFF_LAST + cc]);
-          dbg_logits[gi * NOUT + cc] = lv;
-        }
+  };
+
+  if (dbg) {  // debug exports: one tile at a time
+#pragma unroll 1
+    for (uint64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const Px x = pixel(tile);
+      auto get = getter(x);
+      feed<PREC>(eng, get);
+      eng.start_l0();
+      eng.run_rest(u8_unit(get(0, -1)), u8_unit(get(-1, 2)), [](int) {});
+      const uint32_t v = q1_encode(eng, x.sym, (x.valid && dbg_probs) ? dbg_probs + x.gi * NOUT : nullptr,
+                                   (x.valid && dbg_freqs) ? dbg_freqs + x.gi * NOUT : nullptr, dbg_freqs != nullptr);
+      if (dbg_logits) {  // raw logits (bias added) of this thread's 32 columns
+        uint32_t lv[32];
+        eng.ld32(lv);
+        if (x.valid)
+          for (int i = 0; i < 32; ++i) {
+            const int cc = 64 * col_grp() + 32 * half_id() + i;
+            float l = __uint_as_float(lv[i]);
+            if constexpr (PREC == 1) l = __fadd_rn(l, eng.bias[BIAS_OFF_LAST + cc]);
+            dbg_logits[x.gi * NOUT + cc] = l;
+          }
+      }
+      if (x.valid && threadIdx.x < ROWS * 2 && half_id() == 0) fc[x.fci] = v;
     }
-    const uint32_t v = q1_encode(eng, sym, (dbg && valid && dbg_probs) ? dbg_probs + gi * NOUT : nullptr,
-                                 (dbg && valid && dbg_freqs) ? dbg_freqs + gi * NOUT : nullptr, dbg);
-    if (valid && threadIdx.x < ROWS * 2 && half_id() == 0) fc[un.fc_off + q] = v;
+    engine_teardown<PREC>(eng);
+    return;
+  }
+
+  // Software pipeline over this CTA's tiles: the softmax -> Q1' stages of
+  // tile k run in the MMA waits of tile k+1's network (its logits are in
+  // registers once loaded, which frees the accumulator columns).  The thread
+  // whose columns hold the true symbol writes (f_s | c_s << 16).
+  auto write_fc = [&](const Px& x, const Q1Work<true>& qw) {
+    const int c0 = 64 * col_grp() + 32 * half_id();
+    if (x.valid && x.sym >= c0 && x.sym < c0 + 32) {
+      float fsv = qw.fs;
+      if (x.sym == NOUT - 1) fsv += qw.r.R;
+      fc[x.fci] = (uint32_t)fsv | ((uint32_t)(q1_base(qw.r) + qw.cs_local) << 16);
+    }
+  };
+  // each CTA takes a contiguous range of tiles: consecutive 64-pixel tiles
+  // share most of their 9-row windows, which then hit L1
+  const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
+  const uint64_t tend = min(total, per * (blockIdx.x + 1));
+  uint64_t tile = per * blockIdx.x;
+  if (tile < tend) {
+    Px cur = pixel(tile);
+    {
+      auto get = getter(cur);
+      feed<PREC>(eng, get);
+      eng.start_l0();
+      eng.run_rest(u8_unit(get(0, -1)), u8_unit(get(-1, 2)), [](int) {});
+    }
+#pragma unroll 1
+    for (;;) {
+      uint32_t v[32];
+      eng.ld32(v);  // tile's logits
+      Q1Work<true> qw;
+      const uint64_t nxt = tile + 1;
+      if (nxt < tend) {
+        const Px nx = pixel(nxt);
+        auto get = getter(nx);
+        if constexpr (PREC == 0) quad_sync();  // fp32: the logits buffer also holds the inputs
+        feed<PREC>(eng, get);
+        eng.start_l0();
+        eng.run_rest(u8_unit(get(0, -1)), u8_unit(get(-1, 2)), [&](int l) {
+          if (l == 1) {
+            qw.s1a(eng, v);
+            qw.template s1b<0, 8>(v);
+          } else if (l == 2) {
+            qw.template s1b<8, 16>(v);
+            qw.s1c();
+            qw.x1(eng);
+          } else if (l == 3) {
+            qw.sA(eng, v, cur.sym, nullptr);
+          } else if (l == 4) {
+            qw.x2(eng);
+            write_fc(cur, qw);
+          }
+        });
+        cur = nx;
+        tile = nxt;
+      } else {
+        qw.s1a(eng, v);
+        qw.template s1b<0, 16>(v);
+        qw.s1c();
+        qw.x1(eng);
+        qw.sA(eng, v, cur.sym, nullptr);
+        qw.x2(eng);
+        write_fc(cur, qw);
+        break;
+      }
+    }
   }
   engine_teardown<PREC>(eng);
 }
