@@ -200,10 +200,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     x.c = x.valid ? (int)(q - (uint32_t)x.r * cun.w) : 0;
     x.uw = (int)cun.w;
     x.img = imgs + (uint64_t)cun.img * p.W * p.H + (uint64_t)cun.y0 * p.W + cun.x0;
-    x.sym = x.valid ? (int)__ldg(x.img + (uint64_t)x.r * p.W + x.c) : 0;
+    x.sym = 0;  // loaded by load_sym() when needed (its L2 latency off the tile start)
     x.gi = (uint64_t)cun.img * p.W * p.H + (uint64_t)(cun.y0 + x.r) * p.W + (cun.x0 + x.c);
     x.fci = cun.fc_off + q;
     return x;
+  };
+  auto load_sym = [&](Px& x) {
+    if (x.valid) x.sym = (int)__ldg(x.img + (uint64_t)x.r * p.W + x.c);
+  };
+  // L1 prefetch of a tile's window rows (its 10 taps + the target), issued a
+  // tile ahead so the feed's loads hit L1 (no registers held)
+  auto prefetch_px = [&](const Px& x) {
+    if (!x.valid) return;
+    const int u = 2 * col_grp() + half_id();
+    const int rr = max(x.r + u - 8, 0);
+    const uint8_t* a = x.img + (int64_t)rr * p.W + max(x.c - 6, 0);
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(x.img + (int64_t)x.r * p.W + x.c));
   };
   auto getter = [&](const Px& x) {
     return [&x, &p](int dr, int dc) -> uint32_t {  // branch-free: invalid taps load the target and mask
@@ -217,7 +230,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (dbg) {  // debug exports: one tile at a time
 #pragma unroll 1
     for (uint64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      const Px x = pixel(tile);
+      Px x = pixel(tile);
+      load_sym(x);
       auto get = getter(x);
       feed<PREC>(eng, get);
       eng.start_l0();
@@ -264,7 +278,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       auto get = getter(cur);
       feed<PREC>(eng, get);
       eng.start_l0();
+      if (tile + 1 < tend) prefetch_px(pixel(tile + 1));
       eng.run_rest(u8_unit(get(0, -1)), u8_unit(get(-1, 2)), [](int) {});
+      load_sym(cur);
     }
 #pragma unroll 1
     for (;;) {
@@ -273,11 +289,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       Q1Work<true> qw;
       const uint64_t nxt = tile + 1;
       if (nxt < tend) {
-        const Px nx = pixel(nxt);
+        Px nx = pixel(nxt);
         auto get = getter(nx);
         if constexpr (PREC == 0) quad_sync();  // fp32: the logits buffer also holds the inputs
         feed<PREC>(eng, get);
         eng.start_l0();
+        // tile k's softmax -> Q1' stages in the MMA waits of tile k+1's
+        // layers 2-6 (the last, N=256, has the longest wait); tile k+2's
+        // window is prefetched into L1 meanwhile
         eng.run_rest(u8_unit(get(0, -1)), u8_unit(get(-1, 2)), [&](int l) {
           if (l == 1) {
             qw.s1a(eng, v);
@@ -285,12 +304,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           } else if (l == 2) {
             qw.template s1b<8, 16>(v);
             qw.s1c();
-            qw.x1(eng);
           } else if (l == 3) {
-            qw.sA(eng, v, cur.sym, nullptr);
+            qw.x1(eng);
+            load_sym(nx);
           } else if (l == 4) {
+            qw.sA(eng, v, cur.sym, nullptr);
+          } else {
             qw.x2(eng);
             write_fc(cur, qw);
+            if (nxt + 1 < tend) prefetch_px(pixel(nxt + 1));
           }
         });
         cur = nx;
