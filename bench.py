@@ -374,7 +374,7 @@ def main():
                "d2h_bytes_per_step": d2h, "ms_per_step": em}
 
     variants = None
-    if rank == 0 and args.config == "C2" and tile == (0, 0) and not args.no_variants:
+    if rank == 0 and ws == 1 and args.config == "C2" and tile == (0, 0) and not args.no_variants:
         # the same image as 4 independent 768x128 strips (north_star: "independent
         # image tiles with their own streams"): 1149 instead of 2301 fronts
         variants = {"strips_768x128": measure_variant(dl, model, d_imgs, prec, g, (768, 128))}
@@ -397,7 +397,7 @@ def main():
         # per front, layers 2-6 are a dependent MMA chain (layer 1 is issued a
         # front early): 4 x 8 x 64 + 8 x 128 = 3072 cycles at M=64
         floor_ms = T * 3072 / (peaks.get("sm_max_mhz", 1965.0) * 1e3)
-        cpu = cpu_baseline_sample(args, imgs[0])
+        cpu = cpu_baseline_sample(args, imgs[0]) if ws == 1 else None   # N=1 only (contract)
         line = {
             "metric": "encode+decode Mpixel/s (8-bit gray, round trip) and bpp",
             "value": ws * px_rank / (ms / 1e3) / 1e6,
