@@ -852,6 +852,29 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
       }
     };
 
+    // Front range [rlo, rhi] of active rows, kept incrementally (no
+    // divisions): t = 3*q3 + m3, W = 3*qw + mw, rhi = min(H-1, q3),
+    // rlo = t >= W-1 ? q3 - qw + 1 - (m3 < mw) : 0 = ceil((t - W + 1) / 3).
+    const int qw = uw / 3, mw = uw - 3 * (uw / 3);
+    int q3 = 0, m3 = 0;  // of front t + 1 inside the loop
+    auto range = [&](int t, int q, int m, int& rlo, int& rhi) {
+      rhi = min(uh - 1, q);
+      rlo = t >= uw - 1 ? q - qw + 1 - (m < mw ? 1 : 0) : 0;
+    };
+    auto slot_at = [&](int t, int rlo, int rhi, int& r, int& c) -> bool {
+      r = 0;
+      c = 0;
+      if (rlo > rhi) return false;
+      r = rlo + (int)((S + NS - ((uint32_t)rlo & (NS - 1))) & (NS - 1));
+      c = t - 3 * r;
+      return r <= rhi;
+    };
+    auto any_at = [&](int rlo, int rhi) -> bool {
+      if (rlo > rhi) return false;
+      const uint32_t m = (uint32_t)rlo & (NS - 1), b = rank * ROWS;
+      const uint32_t d = m - b < (uint32_t)ROWS ? 0u : ((b - m) & (NS - 1));
+      return rlo + (int)d <= rhi;
+    };
     int r, c;
     bool active = slot_rc(S, 0, r, c);
     bool any = cta_any(0);
@@ -861,9 +884,14 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
     if (pf.on) pf.t = clock64();
 #pragma unroll 1
     for (int t = 0; t < T; ++t) {
-      int rn, cn;
-      const bool active_n = slot_rc(S, t + 1, rn, cn);
-      const bool any_n = cta_any(t + 1);
+      int rn, cn, rlo, rhi;
+      if (++m3 == 3) {
+        m3 = 0;
+        ++q3;
+      }
+      range(t + 1, q3, m3, rlo, rhi);
+      const bool active_n = slot_at(t + 1, rlo, rhi, rn, cn);
+      const bool any_n = any_at(rlo, rhi);
       bool pub = false;
       pf.mark(0);
       if (any) {
