@@ -527,7 +527,7 @@ struct Fp32Engine {
         float acc[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = 0.0f;
-#pragma unroll 2
+#pragma unroll 4
         for (int k = 0; k < K; ++k) {
           const float a = in[k * ROWS + t];
           const float4* wr = reinterpret_cast<const float4*>(W + k * N + n0);
