@@ -85,13 +85,23 @@ __global__ void __launch_bounds__(512, 1) k(int iters, unsigned long long* out) 
       const unsigned long long ti0 = clock64();
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t id = umma_idesc(M, N);
-      uint64_t bd = umma_desc(smem_u32(sm), N * 16u, 128u);
       const uint32_t kstep = 2u * (N / 8) * 128u;
       uint32_t at = tmem + 256;
-      for (int kk = 0; kk < 8; ++kk) {
-        umma_ts(tmem, at, bd, id, kk > 0);
-        bd += kstep >> 4;
-        at += 8;
+      if (EPI == 7) {  // B in the 128-byte-swizzled K-major layout: atoms of 8 rows x 64 K
+        const uint64_t sw = (uint64_t)2 << 61;  // SWIZZLE_128B
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t addr = smem_u32(sm) + (uint32_t)(kk / 4) * N * 128u + (uint32_t)(kk % 4) * 32u;
+          const uint64_t bd = umma_desc(addr, 16u, 1024u) | sw;
+          umma_ts(tmem, at, bd, id, kk > 0);
+          at += 8;
+        }
+      } else {
+        uint64_t bd = umma_desc(smem_u32(sm), N * 16u, 128u);
+        for (int kk = 0; kk < 8; ++kk) {
+          umma_ts(tmem, at, bd, id, kk > 0);
+          bd += kstep >> 4;
+          at += 8;
+        }
       }
       if (EPI == 6) {  // a second batch of 8 (as the split last layer)
         uint64_t bd2 = umma_desc(smem_u32(sm), N * 16u, 128u);
@@ -202,5 +212,7 @@ int main() {
   run<64, 128, 4>("  .. no bias");
   run<64, 128, 5>("  .. ld16 + st8 only");
   run<64, 128, 6>("M=64 2 x 8 x N=128 chain");
+  run<64, 128, 7>("M=64  N=128 chain, B SWIZZLE_128B");
+  run<64, 256, 7>("M=64  N=256 chain, B SWIZZLE_128B");
   return 0;
 }
