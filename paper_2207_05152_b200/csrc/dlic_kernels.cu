@@ -901,7 +901,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
         const float xb = u8_unit(fp[2 * RING_ROWS - 1]);
         pf.mark(1);
         // network; the next front's early gather runs in the layer-3 MMA
-        // wait (layer 5 for warp 9, which issues layer 3)
+        // wait (layer 5 for the warp that issues layer 3)
         eng.run_rest(xa, xb, [&](int l) {
           const bool w9 = (threadIdx.x >> 5) == (TcEngine::MMA_ISSUER2 >> 5);
           if (l == (w9 ? 4 : 2)) early_gather(rn, cn);
