@@ -98,7 +98,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ int quad() { return (threadIdx.x >> 5) & 3; }
-__device__ __forceinline__ int col_grp() { return threadIdx.x >> 7; }
+// (& 3: in the decoder the row warps are warps 1-16 after the rANS warp 0;
+// warp 16 then takes (quadrant 0, group 0), every pair still exactly once)
+__device__ __forceinline__ int col_grp() { return (threadIdx.x >> 7) & 3; }
 __device__ __forceinline__ int half_id() { return (threadIdx.x >> 4) & 1; }
 __device__ __forceinline__ int tile_row() { return 16 * quad() + (threadIdx.x & 15); }
 
