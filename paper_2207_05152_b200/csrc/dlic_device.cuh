@@ -91,6 +91,7 @@ constexpr uint32_t TM_X = 320;   // exchange slot s: columns TM_X+4s+j (lower ha
 constexpr uint32_t TM_XUP = 32;  //   and TM_X+32+4s+j (upper half-warp copy)
 constexpr uint32_t TM_COLS = 512;
 constexpr int NXSLOT = 7;  // 0 max, 1 Z, 2 F, 3 fc, 4/5 search result, 6 slot
+constexpr int NXS_SMEM = 4;  // shared-memory exchange slots of the encoder engines (0 max, 1 Z, 2 F, 3 fc)
 
 // ------------------------------------------------------------- small PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -336,19 +337,27 @@ struct Prof {
 //   xput(slot, v); xsync(); xget4(slot, v4)   exchange one word per group
 //                        (v must already be equal in both half-warps)
 
-struct TcEngine {
+// Template parameters: the TMEM columns of the hidden-layer accumulator (DH),
+// of the A operand of layers 2-6 (AO) and of layer 1 (A0O); the logits always
+// land in columns [TM_D, TM_D + 256).  XS: exchange words through shared
+// memory (xs) instead of TMEM columns.  The decoder uses the default map
+// (TcEngine); the encoder runs two tiles in flight with two maps (k_enc_pp).
+// The per-row arithmetic is the same instruction sequence for every map.
+template <uint32_t DH, uint32_t AO, uint32_t A0O, bool XS>
+struct TcEngineT {
   uint32_t tmem;       // TMEM base (lane 0, column base)
   uint32_t wsmem;      // shared address of the bf16 weight image
   const float* bias;   // shared [BIAS_TOTAL]
   uint32_t bar;        // shared address of the MMA-completion mbarrier
   uint32_t phase;
+  uint32_t* xs;        // XS: shared exchange words [NXS_SMEM][NGRP][ROWS]
 
   __device__ __forceinline__ uint32_t lane_off() const { return ((threadIdx.x >> 5) & 3u) << 21; }
 
   // Layer-1 input: this thread's 5 packed bf16 pairs = inputs [20j+10h, +10)
   // (A packed columns [10j+5h, +5)).
   __device__ __forceinline__ void put_input(const uint32_t (&a)[5]) const {
-    const uint32_t base = tmem + lane_off() + TM_A0 + 10u * (uint32_t)col_grp();
+    const uint32_t base = tmem + lane_off() + A0O + 10u * (uint32_t)col_grp();
     tmem_st4h<5>(base, a);
     tmem_st1h<5>(base + 4, a[4]);
   }
@@ -374,12 +383,13 @@ struct TcEngine {
     const uint32_t kstep = 2u * (uint32_t)(N / 8) * 128u;  // one K=16 slice
     // start-address field (bits 0-13, 16-byte units) advances by kstep/16
     uint64_t bd = umma_desc(wsmem + wimg_off(l), lbo, 128u);
-    uint32_t at = tmem + (l == 0 ? TM_A0 : TM_A);
-    umma_ts(tmem + TM_D, at, bd, id, 0u);
+    uint32_t at = tmem + (l == 0 ? A0O : AO);
+    const uint32_t dt = tmem + (l == NLAYER - 1 ? TM_D : DH);
+    umma_ts(dt, at, bd, id, 0u);
     for (int kk = 1; kk < K / 16; ++kk) {
       bd += kstep >> 4;
       at += 8u;
-      umma_ts(tmem + TM_D, at, bd, id, 1u);
+      umma_ts(dt, at, bd, id, 1u);
     }
     umma_commit(bar);
   }
@@ -406,9 +416,13 @@ struct TcEngine {
   // this thread's 16 biases of layer l (loaded before the MMA wait, so the
   // adds after the TMEM load are register-only)
   __device__ __forceinline__ void load_bias(int l, float2 (&bq)[8]) const {
-    const float2* b2 = reinterpret_cast<const float2*>(bias + 32 * col_grp() + 16 * half_id()) + l * (HID / 2);
+    const float4* b4 = reinterpret_cast<const float4*>(bias + 32 * col_grp() + 16 * half_id() + l * HID);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) bq[q] = b2[q];
+    for (int q = 0; q < 4; ++q) {
+      const float4 b = b4[q];
+      bq[2 * q] = make_float2(b.x, b.y);
+      bq[2 * q + 1] = make_float2(b.z, b.w);
+    }
   }
   template <bool L0>
   __device__ __forceinline__ void epilogue(const float2 (&b2)[8], float xa, float xb) const {
@@ -416,7 +430,7 @@ struct TcEngine {
     const int j = col_grp(), h = half_id();
     const float4* fw = reinterpret_cast<const float4*>(bias + FRESH_OFF) + 16 * j + 8 * h;
     uint32_t v[16];
-    tmem_ld16h<16>(tmem + lo + TM_D + 32u * (uint32_t)j, v);
+    tmem_ld16h<16>(tmem + lo + DH + 32u * (uint32_t)j, v);
     tc_wait_ld();
     const f2 xa2 = f2_make(xa, xa), xb2 = f2_make(xb, xb);
     uint32_t p[8];
@@ -433,7 +447,7 @@ struct TcEngine {
       f2_split(f2_add(acc, f2_make(b.x, b.y)), x0, x1);
       p[q] = pack_bf16_relu(x0, x1);  // relu(x) rounded to bf16 (RN)
     }
-    tmem_st8h<8>(tmem + lo + TM_A + 16u * (uint32_t)j, p);
+    tmem_st8h<8>(tmem + lo + AO + 16u * (uint32_t)j, p);
     tc_wait_st();
   }
   // Layers 1..6 after layer 0's MMAs were issued (start_l0 / issue_l0):
@@ -473,19 +487,33 @@ struct TcEngine {
     return reinterpret_cast<const float2*>(bias + BIAS_OFF_LAST + 64 * col_grp() + 32 * half_id())[i];
   }
   __device__ __forceinline__ void xput(int slot, uint32_t v) const {
-    tmem_st1h<TM_XUP>(tmem + lane_off() + TM_X + 4u * (uint32_t)slot + (uint32_t)col_grp(), v);
+    if constexpr (XS) {
+      if (half_id() == 0) xs[(slot * NGRP + col_grp()) * ROWS + tile_row()] = v;
+    } else {
+      tmem_st1h<TM_XUP>(tmem + lane_off() + TM_X + 4u * (uint32_t)slot + (uint32_t)col_grp(), v);
+    }
   }
   __device__ __forceinline__ void xsync() const {
-    tc_wait_st();
-    tc_fence_before();
-    quad_sync();
-    tc_fence_after();
+    if constexpr (XS) {
+      quad_sync();
+    } else {
+      tc_wait_st();
+      tc_fence_before();
+      quad_sync();
+      tc_fence_after();
+    }
   }
   __device__ __forceinline__ void xget4(int slot, uint32_t (&v)[4]) const {
-    tmem_ld4h<TM_XUP>(tmem + lane_off() + TM_X + 4u * (uint32_t)slot, v);
-    tc_wait_ld();
+    if constexpr (XS) {
+#pragma unroll
+      for (int g = 0; g < NGRP; ++g) v[g] = xs[(slot * NGRP + g) * ROWS + tile_row()];
+    } else {
+      tmem_ld4h<TM_XUP>(tmem + lane_off() + TM_X + 4u * (uint32_t)slot, v);
+      tc_wait_ld();
+    }
   }
 };
+using TcEngine = TcEngineT<TM_D, TM_A, TM_A0, false>;
 
 // CUDA-core fp32 engine.  Shared buffers, column index = tile row (64):
 //   buf0: [256][ROWS] floats (input features / hidden / logits), buf1: [128][ROWS],
@@ -731,9 +759,6 @@ struct Q1Work {
     const f2 two23 = f2_splat(8388608.0f);
     const f2 fbias = f2_splat(-8388607.0f);  // y - 2^23 + 1 = 1 + floor(x), exact
     f2 FB[4] = {f2_splat(0.0f), f2_splat(0.0f), f2_splat(0.0f), f2_splat(0.0f)};  // 8-entry blocks
-    fs = 0.0f;
-    cs_local = 0.0f;
-    float cum = 0.0f;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const f2 p = f2_mul(f2_bits(v[2 * q], v[2 * q + 1]), inv);
@@ -741,18 +766,6 @@ struct Q1Work {
       FB[q >> 2] = f2_add(FB[q >> 2], f);
       float f0, f1;
       f2_split(f, f0, f1);
-      if (ENC) {
-        const int i0 = c0 + 2 * q;
-        if (i0 == sym) {
-          fs = f0;
-          cs_local = cum;
-        }
-        if (i0 + 1 == sym) {
-          fs = f1;
-          cs_local = __fadd_rn(cum, f0);
-        }
-        cum = __fadd_rn(cum, __fadd_rn(f0, f1));
-      }
       if (probs) {
         float p0, p1;
         f2_split(p, p0, p1);
@@ -773,6 +786,25 @@ struct Q1Work {
     r.P[1] = B[0] + B[1];
     r.P[2] = r.P[1] + B[2];
     r.Fmine = r.P[2] + B[3];
+    if (ENC) {
+      // f_s and the exclusive cum of s within this thread's 32 columns (when
+      // s lies there): the 8-entry block of s from the block sums, then the
+      // block's entries.  All values are integers < 2^16 and all partial
+      // sums < 2^24, so every fp32 sum here is exact in any order.
+      const int d = sym - c0;
+      const int kb = (d >> 3) & 3, ib = d & 7;
+      float within = 0.0f, fsel = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t lo01 = (kb & 1) ? v[8 + i] : v[i];
+        const uint32_t hi01 = (kb & 1) ? v[24 + i] : v[16 + i];
+        const float f = __uint_as_float((kb & 2) ? hi01 : lo01);
+        within += i < ib ? f : 0.0f;
+        fsel = i == ib ? f : fsel;
+      }
+      fs = fsel;
+      cs_local = (kb == 0 ? 0.0f : (kb == 1 ? r.P[0] : (kb == 2 ? r.P[1] : r.P[2]))) + within;
+    }
     const float Fo = __shfl_xor_sync(0xFFFFFFFFu, r.Fmine, 16);
     r.hbase = h ? Fo : 0.0f;
     e.xput(2, __float_as_uint(__fadd_rn(r.Fmine, Fo)));  // exact integer sum

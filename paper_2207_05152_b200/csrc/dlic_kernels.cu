@@ -332,6 +332,277 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   engine_teardown<PREC>(eng);
 }
 
+// ------------------------------------------------------------ encoder MLP, two tiles in flight
+// bf16 production encoder.  The tensor core would idle in every epilogue and
+// softmax of a single tile chain, so each CTA keeps two 64-pixel tiles in
+// flight (slot a, slot b) and a dedicated issuer warp (warp 16) alternates
+// their MMAs: while the 16 row warps run the epilogue of a's layer l, b's
+// layer l runs on the tensor core, and vice versa.  TMEM map (512 columns):
+//   [0,128)   a: hidden accumulator      [0,256) logits of a and of b
+//   [256,320) a: A operand (layer-1 input in its first 40 columns)
+//   [320,448) b: hidden accumulator      [448,512) b: A operand
+// The logits of the two slots share [0,256): b's last layer is issued after
+// a's logits are in registers, and the next a's first layer after b's.
+// Row warps arrive on rdy[s] (16 arrivals) when slot s's next MMA may go;
+// the issuer commits each layer to mma[s].  Exchanges go through shared
+// memory (one region per slot).  Every row sees exactly the decoder's
+// per-row instruction sequence (same engine code, same Q1Work stages), so
+// the tables stay bit-identical (R8).
+constexpr int ENC_PP_THREADS = NTHREADS + 32;
+constexpr uint32_t ENC_PP_XS_BYTES = 2u * NXS_SMEM * NGRP * ROWS * 4u;
+using EngA = TcEngineT<0, 256, 256, true>;
+using EngB = TcEngineT<320, 448, 448, true>;
+
+size_t enc_pp_smem_bytes() { return WIMG_BYTES + BIAS_BYTES + ENC_PP_XS_BYTES; }
+
+__global__ void __launch_bounds__(ENC_PP_THREADS, 1)
+    k_enc_pp(Plan p, DevWeights w, const uint8_t* __restrict__ imgs, uint32_t* __restrict__ fc) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t bars[4];  // mma[0], mma[1] (tcgen05.commit), rdy[0], rdy[1] (16 row warps)
+  __shared__ uint32_t tslot;
+  load_smem(smem, w.wimg, WIMG_BYTES);
+  load_smem(smem + WIMG_BYTES, w.bias, BIAS_BYTES);
+  if (threadIdx.x < 32) tmem_alloc(smem_u32(&tslot), TM_COLS);
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bars[0]), 1);
+    mbar_init(smem_u32(&bars[1]), 1);
+    mbar_init(smem_u32(&bars[2]), NTHREADS / 32);
+    mbar_init(smem_u32(&bars[3]), NTHREADS / 32);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  EngA ea;
+  EngB eb;
+  uint32_t* xsb = reinterpret_cast<uint32_t*>(smem + WIMG_BYTES + BIAS_BYTES);
+  ea.tmem = eb.tmem = tslot;
+  ea.wsmem = eb.wsmem = smem_u32(smem);
+  ea.bias = eb.bias = reinterpret_cast<const float*>(smem + WIMG_BYTES);
+  ea.bar = smem_u32(&bars[0]);
+  eb.bar = smem_u32(&bars[1]);
+  ea.phase = eb.phase = 0;
+  ea.xs = xsb;
+  eb.xs = xsb + NXS_SMEM * NGRP * ROWS;
+  const uint32_t rdy0 = smem_u32(&bars[2]), rdy1 = smem_u32(&bars[3]);
+
+  const uint64_t total = (uint64_t)p.n_img * p.upi * p.tiles_per_unit;
+  const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
+  const uint64_t t0 = per * blockIdx.x;
+  const uint64_t tend = min(total, per * (blockIdx.x + 1));
+  const uint32_t ntl = t0 < tend ? (uint32_t)(tend - t0) : 0u;  // tiles of this CTA
+  const uint32_t npairs = (ntl + 1) / 2;
+
+  if (threadIdx.x >= NTHREADS) {
+    // ================================================ issuer warp
+    if (threadIdx.x == NTHREADS) {
+      uint32_t ph0 = 0, ph1 = 0;
+#pragma unroll 1
+      for (uint32_t k = 0; k < npairs; ++k) {
+#pragma unroll 1
+        for (int l = 0; l < NLAYER; ++l) {
+          mbar_wait(rdy0, ph0);
+          ph0 ^= 1u;
+          ea.issue(l);
+          mbar_wait(rdy1, ph1);
+          ph1 ^= 1u;
+          eb.issue(l);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ================================================ 16 row warps
+    const int row = tile_row();
+    const uint32_t lane = lane_id();
+    // Feed cursor: this thread's pixel in the next tile to feed.  Tiles are
+    // fed in order (t0, t0+1, ...), so the pixel advances by 64 raster
+    // positions per tile without divisions; unit geometry is reloaded only
+    // when a tile starts a new unit.
+    uint32_t fu = 0, fkt = 0, fw = 1, fwh = 0;
+    int fr = 0, fcol = 0;
+    const uint8_t* fimg = imgs;
+    uint64_t ffc = 0;
+    auto set_unit = [&](uint32_t u) {
+      const Unit un = unit_info(p, u);
+      fu = u;
+      fkt = 0;
+      fw = un.w;
+      fwh = un.w * un.h;
+      fr = (int)((uint32_t)row / un.w);
+      fcol = row - fr * (int)un.w;
+      fimg = imgs + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
+      ffc = un.fc_off;
+    };
+    if (t0 < tend) {
+      const uint32_t u0 = (uint32_t)(t0 / p.tiles_per_unit);
+      set_unit(u0);
+      fkt = (uint32_t)(t0 - (uint64_t)u0 * p.tiles_per_unit);
+      const uint32_t q = fkt * (uint32_t)ROWS + (uint32_t)row;
+      fr = (int)(q / fw);
+      fcol = (int)(q - (uint32_t)fr * fw);
+    }
+    auto advance = [&]() {
+      if (++fkt == p.tiles_per_unit) {
+        if (fu + 1 < p.n_img * p.upi) set_unit(fu + 1);  // else stays past the end (fkt == tiles_per_unit)
+      } else {
+        fcol += ROWS;
+        if (fw >= (uint32_t)ROWS) {
+          if (fcol >= (int)fw) {
+            fcol -= (int)fw;
+            ++fr;
+          }
+        } else {
+          const int k = fcol / (int)fw;
+          fr += k;
+          fcol -= k * (int)fw;
+        }
+      }
+    };
+    // what a tile's softmax needs later: the output index and the true
+    // symbol (-1 for a pixel outside the unit)
+    struct Px {
+      uint64_t fci;
+      int sym;
+    };
+    // the cursor's tile -> layer-1 input of a slot; fresh taps, symbol.
+    // Thread u = 2j + h reads window row dr = u - 8 (taps dc = -6..2) and,
+    // for u < 6, the target-row tap dc = u - 6 (kpos_tap order).
+    const int gu = 2 * col_grp() + half_id();
+    auto feed_px = [&](auto& eng, bool live, float& xa, float& xb) -> Px {
+      const uint32_t q = fkt * (uint32_t)ROWS + (uint32_t)row;
+      const bool valid = live && q < fwh;
+      const int rr = fr + gu - 8;
+      const uint8_t* rp = fimg + (int64_t)rr * p.W + fcol;  // window row, column c
+      const uint8_t* tp = fimg + (int64_t)fr * p.W + fcol;  // target row, column c
+      uint32_t tv[10];
+      if (valid && rr >= 0 && fcol >= 6 && fcol + 2 < (int)fw) {
+#pragma unroll
+        for (int i = 0; i < 9; ++i) tv[i] = __ldg(rp + i - 6);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+          const int cc = fcol + i - 6;
+          tv[i] = (valid && rr >= 0 && cc >= 0 && cc < (int)fw) ? (uint32_t)__ldg(rp + i - 6) : 0u;
+        }
+      }
+      tv[9] = (valid && gu < 6 && fcol + gu - 6 >= 0) ? (uint32_t)__ldg(tp + gu - 6) : 0u;
+      const f2 m1 = f2_make(-1.0f, -1.0f);
+      uint32_t a[5];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        float x0, x1;
+        f2_split(f2_add(f2_bits(0x3F800000u | (tv[2 * k] << 15), 0x3F800000u | (tv[2 * k + 1] << 15)), m1), x0,
+                 x1);
+        a[k] = pack_bf16(x0, x1);
+      }
+      eng.put_input(a);
+      // fresh taps (0,-1) and (-1,+2)
+      xa = u8_unit((valid && fcol >= 1) ? (uint32_t)__ldg(tp - 1) : 0u);
+      xb = u8_unit((valid && fr >= 1 && fcol + 2 < (int)fw) ? (uint32_t)__ldg(tp - p.W + 2) : 0u);
+      Px o;
+      o.fci = ffc + q;
+      o.sym = valid ? (int)__ldg(tp) : -1;
+      if (live) advance();
+      return o;
+    };
+    // L1 prefetch of this thread's window row `ahead` tiles past the cursor
+    // (a hint: the address is clamped into the unit image, row wrap ignored)
+    auto prefetch_ahead = [&](int ahead) {
+      if (fkt + (uint32_t)ahead >= p.tiles_per_unit) return;
+      const int cc = min(fcol + ahead * ROWS, (int)fw - 1);
+      const int rr = max(fr + gu - 8, 0);
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(fimg + (int64_t)rr * p.W + max(cc - 6, 0)));
+    };
+    auto signal = [&](uint32_t bar) {
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar);
+    };
+    auto write_fc = [&](const Px& x, const Q1Work<true>& qw) {
+      const int c0 = 64 * col_grp() + 32 * half_id();
+      if (x.sym >= c0 && x.sym < c0 + 32) {
+        float fsv = qw.fs;
+        if (x.sym == NOUT - 1) fsv += qw.r.R;
+        fc[x.fci] = (uint32_t)fsv | ((uint32_t)(q1_base(qw.r) + qw.cs_local) << 16);
+      }
+    };
+
+    // one tile's softmax -> Q1' -> (f_s, c_s), logits in v
+    auto finish = [&](auto& eng, uint32_t (&v)[32], const Px& x) {
+      Q1Work<true> qw;
+      qw.s1a(eng, v);
+      qw.template s1b<0, 16>(v);
+      qw.s1c();
+      qw.x1(eng);
+      qw.sA(eng, v, x.sym, nullptr);
+      qw.x2(eng);
+      write_fc(x, qw);
+    };
+    if (npairs > 0) {
+      float xaA, xbA, xaB, xbB;
+      Px A = feed_px(ea, true, xaA, xbA);
+      signal(rdy0);
+      Px B = feed_px(eb, ntl > 1, xaB, xbB);
+      signal(rdy1);
+      float2 bq[8];
+#pragma unroll 1
+      for (uint32_t k = 0; k < npairs; ++k) {
+        // layers 1..5 of a and b alternating on the tensor core; each
+        // epilogue releases that slot's next layer.  Layer 1 adds the fresh
+        // taps in its epilogue (same split as the decoder).
+        ea.load_bias(0, bq);
+        ea.wait_mma();
+        ea.template epilogue<true>(bq, xaA, xbA);
+        signal(rdy0);
+        eb.load_bias(0, bq);
+        eb.wait_mma();
+        eb.template epilogue<true>(bq, xaB, xbB);
+        signal(rdy1);
+#pragma unroll 1
+        for (int l = 1; l < NLAYER - 1; ++l) {
+          ea.load_bias(l, bq);
+          ea.wait_mma();
+          ea.template epilogue<false>(bq, 0.0f, 0.0f);
+          signal(rdy0);  // l = 4: a's last layer (logits -> [0,256))
+          if (l == 2) prefetch_ahead(0);
+          if (l == 3) prefetch_ahead(1);
+          eb.load_bias(l, bq);
+          eb.wait_mma();
+          eb.template epilogue<false>(bq, 0.0f, 0.0f);
+          if (l < NLAYER - 2) signal(rdy1);
+        }
+        const bool more = k + 1 < npairs;
+        {
+          // a's logits -> registers; b's last layer may then overwrite [0,256)
+          uint32_t v[32];
+          ea.wait_mma();
+          ea.ld32(v);
+          signal(rdy1);
+          finish(ea, v, A);  // overlaps b's last layer
+        }
+        if (more) A = feed_px(ea, true, xaA, xbA);  // a's A operand is free: its last layer is done
+        {
+          uint32_t v[32];
+          eb.wait_mma();
+          eb.ld32(v);
+          const Px Bc = B;
+          if (more) {
+            signal(rdy0);  // next a's layer 1: input written, b's logits out of [0,256)
+            B = feed_px(eb, 2 * k + 3 < ntl, xaB, xbB);
+            signal(rdy1);
+          }
+          finish(eb, v, Bc);  // overlaps the next pair's layer 1
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tslot, TM_COLS);
+}
+
 // ------------------------------------------------------------ rANS encoder
 // One warp per stream.  Lane i = row r0+i of the group.  Fronts walked in
 // reverse (LIFO); within a front rows descending = lanes descending, so
@@ -1012,7 +1283,12 @@ cudaError_t launch_enc_mlp(const Plan& p, const DevWeights& w, const uint8_t* d_
   const uint64_t total = (uint64_t)p.n_img * p.upi * p.tiles_per_unit;
   const uint32_t grid = (uint32_t)(total < (uint64_t)num_sms ? total : (uint64_t)num_sms);
   const size_t sm = enc_smem_bytes(p.precision);
-  if (p.precision == 1) {
+  if (p.precision == 1 && !dbg_logits && !dbg_probs && !dbg_freqs) {
+    const size_t sp = enc_pp_smem_bytes();
+    cudaError_t e = set_smem(k_enc_pp, sp);
+    if (e != cudaSuccess) return e;
+    k_enc_pp<<<grid, ENC_PP_THREADS, sp, st>>>(p, w, d_imgs, d_fc);
+  } else if (p.precision == 1) {
     cudaError_t e = set_smem(k_enc_mlp<1>, sm);
     if (e != cudaSuccess) return e;
     k_enc_mlp<1><<<grid, NTHREADS, sm, st>>>(p, w, d_imgs, d_fc, dbg_logits, dbg_probs, dbg_freqs);
