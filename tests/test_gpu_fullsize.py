@@ -1,0 +1,110 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configurations bench.py times.
+
+C3 (64 MRI-like 256x256 slices per GPU, batch device API), C4 (1920x1080 in
+384x360 tiles) and C5 (3840x2160 in 768x720 tiles, a batch of 2 through the
+device API).  For each:
+  * GPU encode -> GPU decode reconstructs every pixel (north_star: lossless);
+  * the GPU container is byte-identical to the oracle's rANS coder + container
+    (oracle/codec.encode_with_tables) fed the GPU's per-pixel (f_s, c_s)
+    (north_star: same bitstream when the oracle is fed the same tables);
+  * sampled pixels' bf16 logits match the oracle's bf16 definition within
+    BF16_TOL, windows cut at tile borders (fill 0, Q16).
+"""
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import codec, container, mlp, model_io, window
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 2e-2
+
+
+@pytest.fixture(scope="module")
+def dl():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2207_05152_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def trained(dl, trained_blob):
+    return dl.dlic_model_load(trained_blob, 0)
+
+
+def _oracle_bytes(dl, trained, blob, img, tile):
+    h, w = img.shape
+    fc = dl.dlic_debug_mlp(trained, img, precision=1, tile=tile, logits=False, probs=False, freqs=False)["fc"]
+    return codec.encode_with_tables((fc & 0xFFFF).astype(np.int64), (fc >> 16).astype(np.int64), w, h, 1, 32,
+                                    tile[0], tile[1], model_io.digest(blob))
+
+
+def _sampled_logits_ok(dl, trained, blob, img, tile, n=256, seed=0):
+    """n random pixels of one tile: GPU logits (debug export of that tile as its
+    own image: a tile is an independent unit) vs the oracle's bf16 network."""
+    layers = model_io.load(blob)
+    h, w = img.shape
+    tiles = container.tiles(w, h, tile[0], tile[1]) if tile[0] else [(0, 0, w, h)]
+    rng = np.random.default_rng(seed)
+    x0, y0, tw, th = tiles[int(rng.integers(len(tiles)))]
+    sub = np.ascontiguousarray(img[y0:y0 + th, x0:x0 + tw])
+    out = dl.dlic_debug_mlp(trained, sub, precision=1, probs=False, freqs=False, fc=False)["logits"]
+    sel = rng.choice(th * tw, n, replace=False)
+    rows, cols = np.divmod(sel, tw)
+    ref = mlp.forward_bf16(layers, window.features(window.gather_many(sub, rows, cols)))
+    g = out[rows, cols]
+    rel = np.abs(g - ref).max(-1) / np.maximum(np.abs(ref).max(-1), 1e-6)
+    return float(rel.max())
+
+
+def test_c4_full_size_tiled(dl, trained, trained_blob):
+    img = synth.config_images("C4", count=1)[0]
+    assert img.shape == (1080, 1920)
+    tile = (384, 360)
+    bits = dl.dlic_encode(trained, img, precision=1, tile=tile)
+    assert np.array_equal(dl.dlic_decode(trained, bits), img)
+    assert bits == _oracle_bytes(dl, trained, trained_blob, img, tile)
+    assert _sampled_logits_ok(dl, trained, trained_blob, img, tile) <= BF16_TOL
+
+
+def _batch_roundtrip(dl, trained, imgs, tile):
+    import torch
+    n = imgs.shape[0]
+    d_imgs = torch.from_numpy(np.ascontiguousarray(imgs)).cuda()
+    d_out, d_sizes, stride = dl.dlic_encode_batch_device(trained, d_imgs, precision=1, tile=tile)
+    torch.cuda.synchronize()
+    sizes = d_sizes.cpu().numpy()
+    host = d_out.cpu().numpy()
+    offs = [i * stride for i in range(n)]
+    hdr = dl.dlic_peek(host[:sizes[0]].tobytes())
+    d_dec = torch.empty_like(d_imgs)
+    d_st = torch.zeros(n, dtype=torch.int32, device="cuda")
+    dl.dlic_decode_batch_device(trained, d_out, offs, hdr, d_dec, d_st)
+    torch.cuda.synchronize()
+    assert d_st.cpu().numpy().tolist() == [0] * n
+    assert np.array_equal(d_dec.cpu().numpy(), imgs)
+    return [host[o:o + s].tobytes() for o, s in zip(offs, sizes)]
+
+
+def test_c3_full_batch(dl, trained, trained_blob):
+    imgs = synth.config_images("C3", count=64)
+    assert imgs.shape == (64, 256, 256)
+    conts = _batch_roundtrip(dl, trained, imgs, (0, 0))
+    for i in (0, 17, 63):
+        assert conts[i] == _oracle_bytes(dl, trained, trained_blob, imgs[i], (0, 0))
+    assert _sampled_logits_ok(dl, trained, trained_blob, imgs[17], (0, 0), seed=17) <= BF16_TOL
+
+
+def test_c5_full_size_batch(dl, trained, trained_blob):
+    imgs = synth.config_images("C5", count=2)
+    assert imgs.shape == (2, 2160, 3840)
+    tile = (768, 720)
+    conts = _batch_roundtrip(dl, trained, imgs, tile)
+    assert conts[1] == _oracle_bytes(dl, trained, trained_blob, imgs[1], tile)
+    assert _sampled_logits_ok(dl, trained, trained_blob, imgs[1], tile, seed=5) <= BF16_TOL
