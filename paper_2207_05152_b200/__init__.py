@@ -19,7 +19,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdlic.so")
+LIB_PATH = os.environ.get("DLIC_LIB") or os.path.join(_HERE, "libdlic.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError("libdlic.so not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
                       "(nvcc -gencode arch=compute_100a,code=sm_100a)")
