@@ -120,6 +120,25 @@ void dlic_free(void* p);
 const char* dlic_status_str(dlic_status s);
 const char* dlic_last_error(void);
 
+/* ---- host batch: the same calls over n independent images ----------------
+ * (units are whole images, R7/Q16; each container is byte-identical to what
+ * dlic_encode produces for that image alone).  One host->device copy of all
+ * images and one device->host copy of all containers per call.
+ * encode: imgs = n*height*width bytes (image i at imgs + i*width*height,
+ * row-major); *out = library-allocated buffer (dlic_free) holding the n
+ * containers back to back, *out_len its total size, sizes[i] (caller array of
+ * n) the size of container i.
+ * decode: container i at bits + offsets[i] (offsets ascending, all containers
+ * of the same width/height/options and model); writes n*width*height bytes to
+ * imgs.  Each header is checked on the host (hash before any pixel work), each
+ * container's lane invariants on the device; the first failing image's status
+ * is returned. */
+dlic_status dlic_encode_batch(const dlic_model* m, const uint8_t* imgs, uint32_t n, uint32_t width,
+                              uint32_t height, const dlic_opts* opts, uint8_t** out, size_t* out_len,
+                              uint64_t* sizes);
+dlic_status dlic_decode_batch(const dlic_model* m, const uint8_t* bits, size_t len, const uint64_t* offsets,
+                              uint32_t n, uint8_t* imgs, size_t img_capacity);
+
 /* ---- device-resident batch variants (caller owns memory and stream) -------
  * n images of width x height, packed (image i at d_imgs + i*width*height).
  * Encode writes container i at d_out + i*dlic_max_container_bytes(...) and its

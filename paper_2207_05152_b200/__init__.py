@@ -68,6 +68,9 @@ _sig("dlic_encode", _st, _vp, _vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_si
 _sig("dlic_decode", _st, _vp, _vp, ctypes.c_size_t, _vp, ctypes.c_size_t)
 _sig("dlic_peek", _st, _vp, ctypes.c_size_t, ctypes.POINTER(dlic_header))
 _sig("dlic_max_container_bytes", ctypes.c_size_t, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(dlic_opts))
+_sig("dlic_encode_batch", _st, _vp, _vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+     ctypes.POINTER(dlic_opts), c_u8pp, ctypes.POINTER(ctypes.c_size_t), _vp)
+_sig("dlic_decode_batch", _st, _vp, _vp, ctypes.c_size_t, _vp, ctypes.c_uint32, _vp, ctypes.c_size_t)
 _sig("dlic_encode_batch_device", _st, _vp, _vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
      ctypes.POINTER(dlic_opts), _vp, ctypes.c_size_t, _vp, _vp)
 _sig("dlic_decode_batch_device", _st, _vp, _vp, _vp, ctypes.c_uint32, ctypes.POINTER(dlic_header), _vp, _vp, _vp)
@@ -190,6 +193,31 @@ def dlic_decode(model: Model, bits: bytes) -> np.ndarray:
     img = np.empty((hd["height"], hd["width"]), np.uint8)
     _check(_lib.dlic_decode(model.handle, bits, len(bits), img.ctypes.data, img.size))
     return img
+
+
+def dlic_encode_batch(model: Model, imgs: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0)):
+    """imgs (n, H, W) u8 host -> (blob, sizes): the n containers back to back."""
+    imgs = np.ascontiguousarray(imgs, dtype=np.uint8)
+    n, h, w = imgs.shape
+    out = c_u8p()
+    tot = ctypes.c_size_t()
+    sizes = np.zeros(n, np.uint64)
+    o = _opts(precision, group_rows, tile)
+    _check(_lib.dlic_encode_batch(model.handle, imgs.ctypes.data, n, w, h, ctypes.byref(o), ctypes.byref(out),
+                                  ctypes.byref(tot), sizes.ctypes.data))
+    return _take(out, tot.value), [int(x) for x in sizes]
+
+
+def dlic_decode_batch(model: Model, blob: bytes, sizes) -> np.ndarray:
+    """n containers back to back (sizes[i] bytes each) -> (n, H, W) u8."""
+    sizes = [int(x) for x in sizes]
+    offs = np.zeros(len(sizes), np.uint64)
+    offs[1:] = np.cumsum(sizes[:-1])
+    hd = dlic_peek(blob[:sizes[0]])
+    imgs = np.empty((len(sizes), hd["height"], hd["width"]), np.uint8)
+    _check(_lib.dlic_decode_batch(model.handle, blob, len(blob), offs.ctypes.data, len(sizes), imgs.ctypes.data,
+                                  imgs.size))
+    return imgs
 
 
 def dlic_max_container_bytes(width, height, precision=PREC_BF16, group_rows=32, tile=(0, 0)) -> int:

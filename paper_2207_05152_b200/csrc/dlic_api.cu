@@ -743,6 +743,125 @@ dlic_status dlic_debug_mlp(const dlic_model* m, const uint8_t* img, uint32_t wid
   return DLIC_OK;
 }
 
+dlic_status dlic_encode_batch(const dlic_model* m, const uint8_t* imgs, uint32_t n, uint32_t width,
+                              uint32_t height, const dlic_opts* opts, uint8_t** out, size_t* out_len,
+                              uint64_t* sizes) {
+  if (!imgs || !out || !out_len || !sizes || n == 0) return fail(DLIC_E_INVALID_ARG, "null pointer or n = 0");
+  dlic_status s = check_model_gpu(m);
+  if (s != DLIC_OK) return s;
+  Plan p;
+  s = make_plan(width, height, n, opts, p);
+  if (s != DLIC_OK) return s;
+  cudaStream_t st = my_stream();
+  Scratch sc(st);
+  const size_t npx = (size_t)n * width * height;
+  uint8_t *d_imgs, *d_out;
+  uint64_t* d_sizes;
+  CUDA_TRY(sc.alloc(&d_imgs, npx));
+  CUDA_TRY(sc.alloc(&d_out, p.max_container * n));
+  CUDA_TRY(sc.alloc(&d_sizes, 8ull * n));
+  CUDA_TRY(h2d(d_imgs, imgs, npx, st));
+  s = run_encode(m, p, d_imgs, d_out, p.max_container, d_sizes, st, sc);
+  if (s != DLIC_OK) return s;
+  std::vector<uint64_t> hs(n);
+  CUDA_TRY(cudaMemcpyAsync(hs.data(), d_sizes, 8ull * n, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  uint64_t total = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (hs[i] > p.max_container) return fail(DLIC_E_CUDA, "container size out of range");
+    total += hs[i];
+  }
+  // pack the containers back to back on the device, then one D2H
+  uint8_t* d_pack;
+  CUDA_TRY(sc.alloc(&d_pack, total));
+  uint64_t off = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    CUDA_TRY(cudaMemcpyAsync(d_pack + off, d_out + (size_t)i * p.max_container, hs[i], cudaMemcpyDeviceToDevice,
+                             st));
+    off += hs[i];
+  }
+  uint8_t* hb = static_cast<uint8_t*>(g_pin_out.get(total + 64));
+  if (!hb) return fail(DLIC_E_OUT_OF_MEMORY, "pinned staging");
+  CUDA_TRY(cudaMemcpyAsync(hb, d_pack, total, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  uint8_t* res = static_cast<uint8_t*>(malloc(total ? total : 1));
+  if (!res) return fail(DLIC_E_OUT_OF_MEMORY, "malloc");
+  memcpy(res, hb, total);
+  for (uint32_t i = 0; i < n; ++i) sizes[i] = hs[i];
+  *out = res;
+  *out_len = total;
+  return DLIC_OK;
+}
+
+dlic_status dlic_decode_batch(const dlic_model* m, const uint8_t* bits, size_t len, const uint64_t* offsets,
+                              uint32_t n, uint8_t* imgs, size_t img_capacity) {
+  if (!bits || !offsets || !imgs || n == 0) return fail(DLIC_E_INVALID_ARG, "null pointer or n = 0");
+  dlic_status s = check_model_gpu(m);
+  if (s != DLIC_OK) return s;
+  std::vector<uint64_t> lens(n);
+  dlic_header h0;
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint64_t end = i + 1 < n ? offsets[i + 1] : (uint64_t)len;
+    if (offsets[i] > end || end > len) return fail(DLIC_E_INVALID_ARG, "offsets not ascending within len");
+    lens[i] = end - offsets[i];
+    dlic_header h;
+    s = peek(bits + offsets[i], lens[i], &h, nullptr);
+    if (s != DLIC_OK) return s;
+    if (memcmp(h.model_sha256, m->sha, 32) != 0)
+      return fail(DLIC_E_MODEL_HASH_MISMATCH, "container was coded with another model");
+    if (i == 0) {
+      h0 = h;
+    } else if (h.width != h0.width || h.height != h0.height || h.precision != h0.precision ||
+               h.group_rows != h0.group_rows || h.tile_w != h0.tile_w || h.tile_h != h0.tile_h) {
+      return fail(DLIC_E_SHAPE_MISMATCH, "batch containers differ in dims or options");
+    }
+  }
+  const size_t npx = (size_t)n * h0.width * h0.height;
+  if (img_capacity < npx) return fail(DLIC_E_BUFFER_TOO_SMALL, "image buffer");
+  dlic_opts o = opts_of(h0);
+  Plan p;
+  s = make_plan(h0.width, h0.height, n, &o, p);
+  if (s != DLIC_OK) return s;
+  if (p.spi != h0.n_streams) return fail(DLIC_E_CORRUPT_CONTAINER, "stream count does not match the header dims");
+  cudaStream_t st = my_stream();
+  Scratch sc(st);
+  uint8_t *d_bits, *d_imgs;
+  uint64_t* d_meta;  // [0, n) offsets, [n, 2n) lengths
+  uint32_t *d_sbase, *d_slen;
+  int32_t* d_status;
+  CUDA_TRY(sc.alloc(&d_bits, len));
+  CUDA_TRY(sc.alloc(&d_imgs, npx));
+  CUDA_TRY(sc.alloc(&d_meta, 16ull * n));
+  CUDA_TRY(sc.alloc(&d_sbase, 4ull * n * p.spi));
+  CUDA_TRY(sc.alloc(&d_slen, 4ull * n * p.spi));
+  CUDA_TRY(sc.alloc(&d_status, 4ull * n));
+  CUDA_TRY(cudaMemsetAsync(d_status, 0, 4ull * n, st));
+  std::vector<uint64_t> meta(2ull * n);
+  for (uint32_t i = 0; i < n; ++i) {
+    meta[i] = offsets[i];
+    meta[n + i] = lens[i];
+  }
+  CUDA_TRY(cudaMemcpyAsync(d_meta, meta.data(), 16ull * n, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(h2d(d_bits, bits, len, st));
+  CUDA_TRY(launch_dec_prep(p, d_bits, d_meta, d_meta + n, d_sbase, d_slen, d_status, st));
+  ev_begin("decode", st);
+  CUDA_TRY(launch_decode(p, m->dw(), d_bits, d_meta, d_sbase, d_slen, d_imgs, d_status, st));
+  ev_end("decode", st);
+  uint8_t* ho = static_cast<uint8_t*>(g_pin_out.get(npx + 4ull * n + 64));
+  if (!ho) return fail(DLIC_E_OUT_OF_MEMORY, "pinned staging");
+  CUDA_TRY(cudaMemcpyAsync(ho, d_status, 4ull * n, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(ho + ((4ull * n + 63) & ~63ull), d_imgs, npx, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (uint32_t i = 0; i < n; ++i) {
+    int32_t stat;
+    memcpy(&stat, ho + 4ull * i, 4);
+    if (stat != 0) return fail((dlic_status)stat, "lane invariant / framing check failed on the device (image " +
+                                                      std::to_string(i) + ")");
+  }
+  memcpy(imgs, ho + ((4ull * n + 63) & ~63ull), npx);
+  return DLIC_OK;
+}
+
 dlic_status dlic_encode_batch_device(const dlic_model* m, const uint8_t* d_imgs, uint32_t n, uint32_t width,
                                      uint32_t height, const dlic_opts* opts, uint8_t* d_out, size_t out_capacity,
                                      uint64_t* d_sizes, void* cuda_stream) {

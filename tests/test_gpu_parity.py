@@ -223,3 +223,25 @@ def test_batch_device_api_matches_single(dl, trained):
     torch.cuda.synchronize()
     assert d_st.cpu().numpy().tolist() == [0] * 6
     assert np.array_equal(d_dec.cpu().numpy(), imgs)
+
+
+def test_host_batch_api_matches_single(dl, trained, trained_blob):
+    """dlic_encode_batch / dlic_decode_batch: each container byte-identical to a
+    single-image dlic_encode (images are independent units); lossless decode;
+    the model hash is checked before pixel work."""
+    imgs = synth.mri_like_slices(5, 256, seed0=4)[:, :70, :90].copy()
+    blob, sizes = dl.dlic_encode_batch(trained, imgs, precision=1, tile=(40, 32))
+    assert sum(sizes) == len(blob)
+    off = 0
+    for i in range(5):
+        assert blob[off:off + sizes[i]] == dl.dlic_encode(trained, imgs[i], precision=1, tile=(40, 32))
+        off += sizes[i]
+    assert np.array_equal(dl.dlic_decode_batch(trained, blob, sizes), imgs)
+    other = dl.dlic_model_load(model_io.save(synth.he_uniform_layers(mlp.P100K, seed=98)), 0)
+    with pytest.raises(dl.DlicError) as e:
+        dl.dlic_decode_batch(other, blob, sizes)
+    assert e.value.status == 7
+    bad = bytearray(blob)
+    bad[sizes[0] + dl.dlic_peek(blob[sizes[0]:sizes[0] + sizes[1]])["header_bytes"] + 3] ^= 0x40   # payload of image 1
+    with pytest.raises(dl.DlicError):
+        dl.dlic_decode_batch(trained, bytes(bad), sizes)
