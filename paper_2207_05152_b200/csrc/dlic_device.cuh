@@ -135,6 +135,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   } while (!ok);
 }
 
+// pure spin on the phase (mbarrier.test_wait never suspends the thread)
+__device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
 // ---- tcgen05
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -178,6 +192,26 @@ __device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Warp-wide variants: all 32 lanes execute them (converged, identical
+// operands) and one elected lane issues, so the operands can live in uniform
+// registers instead of a per-MMA elect/broadcast loop.
+__device__ __forceinline__ void umma_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_warp(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
@@ -393,6 +427,24 @@ struct TcEngineT {
     }
     umma_commit(bar);
   }
+  // The same, executed by a whole (converged) warp; one elected lane issues.
+  __device__ __forceinline__ void issue_warp(int l) const {
+    tc_fence_after();
+    const int K = layer_k(l), N = layer_n(l);
+    const uint32_t id = umma_idesc(64, N);
+    const uint32_t lbo = (uint32_t)N * 16u;
+    const uint32_t kstep = 2u * (uint32_t)(N / 8) * 128u;
+    uint64_t bd = umma_desc(wsmem + wimg_off(l), lbo, 128u);
+    uint32_t at = tmem + (l == 0 ? A0O : AO);
+    const uint32_t dt = tmem + (l == NLAYER - 1 ? TM_D : DH);
+    umma_ts_warp(dt, at, bd, id, 0u);
+    for (int kk = 1; kk < K / 16; ++kk) {
+      bd += kstep >> 4;
+      at += 8u;
+      umma_ts_warp(dt, at, bd, id, 1u);
+    }
+    umma_commit_warp(bar);
+  }
   // Layer 0 over the 76 early taps (fresh weights are zero in the image),
   // after put_input (all threads; the caller supplies the barrier).
   __device__ __forceinline__ void issue_l0() const {
@@ -463,12 +515,12 @@ struct TcEngineT {
     if (pf) pf->mark2(2);
     epilogue<true>(bq, xa, xb);
     if (pf) pf->mark2(3);
-#pragma unroll 1
+#pragma unroll
     for (int l = 1; l < NLAYER; ++l) {
       tc_fence_before();
       row_sync();
       if (pf) pf->mark2(0);
-      if (threadIdx.x == issuer(l)) issue(l);
+      if ((threadIdx.x >> 5) == (issuer(l) >> 5)) issue_warp(l);  // the whole (converged) issuer warp
       hook(l);
       if (pf) pf->mark2(1);
       if (l < NLAYER - 1) load_bias(l, bq);

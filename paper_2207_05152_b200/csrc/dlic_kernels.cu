@@ -17,9 +17,12 @@
 //               (DSMEM mirror) -> cluster barrier; the rANS step runs one
 //               front late inside the next front's network.
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "dlic_device.cuh"
 #include "dlic_internal.h"
+
 
 namespace dlic {
 
@@ -356,7 +359,8 @@ using EngB = TcEngineT<320, 448, 448, true>;
 size_t enc_pp_smem_bytes() { return WIMG_BYTES + BIAS_BYTES + ENC_PP_XS_BYTES; }
 
 __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
-    k_enc_pp(Plan p, DevWeights w, const uint8_t* __restrict__ imgs, uint32_t* __restrict__ fc) {
+    k_enc_pp(Plan p, DevWeights w, const uint8_t* __restrict__ imgs, uint32_t* __restrict__ fc,
+             unsigned long long* __restrict__ prof) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bars[4];  // mma[0], mma[1] (tcgen05.commit), rdy[0], rdy[1] (16 row warps)
   __shared__ uint32_t tslot;
@@ -395,22 +399,31 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
 
   if (threadIdx.x >= NTHREADS) {
     // ================================================ issuer warp
-    if (threadIdx.x == NTHREADS) {
-      uint32_t ph0 = 0, ph1 = 0;
+    // (the whole warp runs the loop converged; one elected lane issues, the
+    // per-layer descriptors are compile-time constants + the TMEM/smem bases)
+    uint32_t ph0 = 0, ph1 = 0;
+    unsigned long long idle = 0, t0c = prof ? clock64() : 0;
 #pragma unroll 1
-      for (uint32_t k = 0; k < npairs; ++k) {
-#pragma unroll 1
-        for (int l = 0; l < NLAYER; ++l) {
-          mbar_wait(rdy0, ph0);
-          ph0 ^= 1u;
-          ea.issue(l);
-          mbar_wait(rdy1, ph1);
-          ph1 ^= 1u;
-          eb.issue(l);
-        }
+    for (uint32_t k = 0; k < npairs; ++k) {
+#pragma unroll
+      for (int l = 0; l < NLAYER; ++l) {
+        const unsigned long long c0 = prof ? clock64() : 0;
+        mbar_wait(rdy0, ph0);
+        ph0 ^= 1u;
+        ea.issue_warp(l);
+        const unsigned long long c1 = prof ? clock64() : 0;
+        mbar_wait(rdy1, ph1);
+        ph1 ^= 1u;
+        if (prof) idle += clock64() - c1;
+        eb.issue_warp(l);
+        (void)c0;
       }
     }
-    __syncwarp();
+    if (prof && threadIdx.x == NTHREADS) {
+      atomicAdd(prof + 8, idle);
+      atomicAdd(prof + 9, clock64() - t0c);
+      atomicAdd(prof + 10, (unsigned long long)npairs);
+    }
   } else {
     // ================================================ 16 row warps
     const int row = tile_row();
@@ -547,6 +560,15 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
       Px B = feed_px(eb, ntl > 1, xaB, xbB);
       signal(rdy1);
       float2 bq[8];
+      const bool pon = prof != nullptr && threadIdx.x == 0;
+      unsigned long long pt = pon ? clock64() : 0;
+      auto pmark = [&](int i) {
+        if (pon) {
+          const unsigned long long n = clock64();
+          atomicAdd(prof + i, n - pt);
+          pt = n;
+        }
+      };
 #pragma unroll 1
       for (uint32_t k = 0; k < npairs; ++k) {
         // layers 1..5 of a and b alternating on the tensor core; each
@@ -560,18 +582,27 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
         eb.wait_mma();
         eb.template epilogue<true>(bq, xaB, xbB);
         signal(rdy1);
+        pmark(0);
 #pragma unroll 1
         for (int l = 1; l < NLAYER - 1; ++l) {
           ea.load_bias(l, bq);
+          pmark(6);
           ea.wait_mma();
+          pmark(7);
           ea.template epilogue<false>(bq, 0.0f, 0.0f);
+          pmark(11);
           signal(rdy0);  // l = 4: a's last layer (logits -> [0,256))
+          pmark(12);
           if (l == 2) prefetch_ahead(0);
           if (l == 3) prefetch_ahead(1);
           eb.load_bias(l, bq);
+          pmark(6);
           eb.wait_mma();
+          pmark(7);
           eb.template epilogue<false>(bq, 0.0f, 0.0f);
+          pmark(11);
           if (l < NLAYER - 2) signal(rdy1);
+          pmark(12);
         }
         const bool more = k + 1 < npairs;
         {
@@ -580,9 +611,12 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
           ea.wait_mma();
           ea.ld32(v);
           signal(rdy1);
+          pmark(1);
           finish(ea, v, A);  // overlaps b's last layer
+          pmark(2);
         }
         if (more) A = feed_px(ea, true, xaA, xbA);  // a's A operand is free: its last layer is done
+        pmark(3);
         {
           uint32_t v[32];
           eb.wait_mma();
@@ -593,7 +627,9 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
             B = feed_px(eb, 2 * k + 3 < ntl, xaB, xbB);
             signal(rdy1);
           }
+          pmark(4);
           finish(eb, v, Bc);  // overlaps the next pair's layer 1
+          pmark(5);
         }
       }
     }
@@ -1118,9 +1154,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
     };
     auto issue_early = [&](bool any_n) {
       if constexpr (PREC == 1) {
-        if (any_n && threadIdx.x == TcEngine::MMA_ISSUER) {
+        if (any_n && (threadIdx.x >> 5) == (TcEngine::MMA_ISSUER >> 5)) {  // whole warp, one lane issues
           mbar_wait(a_ready, a_phase);
-          eng.issue_l0();
+          eng.issue_warp(0);
         }
         a_phase ^= 1u;  // every warp arrives once per front
       }
@@ -1287,7 +1323,22 @@ cudaError_t launch_enc_mlp(const Plan& p, const DevWeights& w, const uint8_t* d_
     const size_t sp = enc_pp_smem_bytes();
     cudaError_t e = set_smem(k_enc_pp, sp);
     if (e != cudaSuccess) return e;
-    k_enc_pp<<<grid, ENC_PP_THREADS, sp, st>>>(p, w, d_imgs, d_fc);
+    static unsigned long long* d_prof = nullptr;
+    const bool prof = getenv("DLIC_PROF_ENC") != nullptr;
+    if (prof && !d_prof) cudaMalloc(&d_prof, 16 * 8);
+    if (prof) cudaMemsetAsync(d_prof, 0, 16 * 8, st);
+    k_enc_pp<<<grid, ENC_PP_THREADS, sp, st>>>(p, w, d_imgs, d_fc, prof ? d_prof : nullptr);
+    if (prof) {
+      unsigned long long h[16];
+      cudaMemcpyAsync(h, d_prof, 16 * 8, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      const double np = (double)h[10];
+      fprintf(stderr, "[enc prof] cycles per pair (thread 0): layer0 %.0f a-logits %.0f finish-a %.0f feed-a %.0f "
+              "b-logits+feed-b %.0f finish-b %.0f | layers1-4 (8 epilogues): bias %.0f mma-wait %.0f epilogue %.0f "
+              "signal %.0f | issuer: total %.0f waiting for b %.0f\n", h[0] / np, h[1] / np,
+              h[2] / np, h[3] / np, h[4] / np, h[5] / np, h[6] / np, h[7] / np, h[11] / np, h[12] / np, h[9] / np,
+              h[8] / np);
+    }
   } else if (p.precision == 1) {
     cudaError_t e = set_smem(k_enc_mlp<1>, sm);
     if (e != cudaSuccess) return e;
