@@ -445,6 +445,21 @@ struct TcEngineT {
     }
     umma_commit_warp(bar);
   }
+  // K-slices [s0, s1) of layer l into the accumulator at column dcol (whole
+  // converged warp, one elected lane issues; no commit).
+  __device__ __forceinline__ void issue_slices(int l, int s0, int s1, uint32_t dcol) const {
+    tc_fence_after();
+    const int N = layer_n(l);
+    const uint32_t id = umma_idesc(64, N);
+    const uint32_t lbo = (uint32_t)N * 16u;
+    const uint32_t kstep = 2u * (uint32_t)(N / 8) * 128u;
+    const uint64_t bd = umma_desc(wsmem + wimg_off(l), lbo, 128u);
+    const uint32_t at = tmem + (l == 0 ? A0O : AO);
+    for (int kk = s0; kk < s1; ++kk)
+      umma_ts_warp(tmem + dcol, at + 8u * (uint32_t)kk, bd + (uint64_t)((kstep >> 4) * (uint32_t)kk), id,
+                   kk > 0 ? 1u : 0u);
+  }
+  __device__ __forceinline__ void commit_warp() const { umma_commit_warp(bar); }
   // Layer 0 over the 76 early taps (fresh weights are zero in the image),
   // after put_input (all threads; the caller supplies the barrier).
   __device__ __forceinline__ void issue_l0() const {
@@ -478,11 +493,17 @@ struct TcEngineT {
   }
   template <bool L0>
   __device__ __forceinline__ void epilogue(const float2 (&b2)[8], float xa, float xb) const {
+    epilogue_at<L0>(DH, b2, xa, xb);
+  }
+  // the same with the accumulator at TMEM column dcol (the decoder's
+  // double-buffered hidden accumulator)
+  template <bool L0>
+  __device__ __forceinline__ void epilogue_at(uint32_t dcol, const float2 (&b2)[8], float xa, float xb) const {
     const uint32_t lo = lane_off();
     const int j = col_grp(), h = half_id();
     const float4* fw = reinterpret_cast<const float4*>(bias + FRESH_OFF) + 16 * j + 8 * h;
     uint32_t v[16];
-    tmem_ld16h<16>(tmem + lo + DH + 32u * (uint32_t)j, v);
+    tmem_ld16h<16>(tmem + lo + dcol + 32u * (uint32_t)j, v);
     tc_wait_ld();
     const f2 xa2 = f2_make(xa, xa), xb2 = f2_make(xb, xb);
     uint32_t p[8];
@@ -528,6 +549,59 @@ struct TcEngineT {
       if (pf) pf->mark2(2);
       if (l < NLAYER - 1) epilogue<false>(bq, 0.0f, 0.0f);
       if (pf) pf->mark2(3);
+    }
+  }
+
+  // Decoder network with a dedicated issuer warp (k_decode): the 16 row warps
+  // never meet at a CTA barrier inside the network.  Each warp arrives on
+  // grp[j] (j = its column group, 4 warps) once its epilogue of layer l is in
+  // TMEM; the issuer issues layer l+1's K-slices 2j, 2j+1 (the activations of
+  // group j) as soon as group j has arrived, so the MMA starts while the other
+  // groups still finish.  Hidden accumulators alternate between columns
+  // [0,128) and [128,256) (layer l at 128*(l&1)); the logits take [0,256)
+  // after every group's last hidden epilogue (dec_issue_network).
+  static __device__ __forceinline__ uint32_t dcol_of(int l) { return (l & 1) ? 128u : 0u; }
+  // group j signals on named barrier 8 + j (its 4 warps arrive, the issuer
+  // warp syncs: 160 threads)
+  template <class Hook>
+  __device__ __forceinline__ void run_rest_ws(float xa, float xb, Hook&& hook) {
+    float2 bq[8];
+    const uint32_t gbar = 8u + (uint32_t)col_grp();
+    auto signal = [&]() {
+      tc_fence_before();
+      asm volatile("bar.arrive %0, 160;" ::"r"(gbar) : "memory");
+    };
+    load_bias(0, bq);
+    wait_mma();
+    epilogue_at<true>(0u, bq, xa, xb);
+    signal();
+#pragma unroll 1
+    for (int l = 1; l < NLAYER; ++l) {
+      hook(l);
+      if (l < NLAYER - 1) load_bias(l, bq);
+      wait_mma();
+      if (l < NLAYER - 1) {
+        epilogue_at<false>(dcol_of(l), bq, 0.0f, 0.0f);
+        signal();
+      }
+    }
+  }
+  // issuer side of run_rest_ws for layers 2..6 (whole warp)
+  __device__ __forceinline__ void dec_issue_network() const {
+#pragma unroll
+    for (int l = 1; l < NLAYER; ++l) {
+      if (l < NLAYER - 1) {
+#pragma unroll
+        for (int j = 0; j < NGRP; ++j) {
+          asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
+          issue_slices(l, 2 * j, 2 * j + 2, dcol_of(l));
+        }
+      } else {  // logits over [0,256): after every group's last hidden epilogue
+#pragma unroll
+        for (int j = 0; j < NGRP; ++j) asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
+        issue_slices(l, 0, 8, TM_D);
+      }
+      commit_warp();
     }
   }
 

@@ -893,8 +893,11 @@ __global__ void k_dec_prep(Plan p, const uint8_t* __restrict__ bits, const uint6
 // cluster barrier.  Its work overlaps the row warps' network entirely.
 constexpr int DEC_THREADS = NTHREADS + 32;
 
+// bf16: one more warp (the 18th) only issues the network's MMAs (run_rest_ws)
+__host__ __device__ constexpr int dec_block(int prec) { return prec == 1 ? DEC_THREADS + 32 : DEC_THREADS; }
+
 template <int PREC, bool PROF>
-__global__ void __launch_bounds__(DEC_THREADS, 1)
+__global__ void __launch_bounds__(dec_block(PREC), 1)
     k_decode(Plan p, DevWeights w, const uint8_t* __restrict__ bits, const uint64_t* __restrict__ cont_off,
              const uint32_t* __restrict__ sbase, const uint32_t* __restrict__ slen, uint8_t* __restrict__ out,
              int32_t* __restrict__ status, unsigned long long* __restrict__ prof) {
@@ -1075,6 +1078,43 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
       apply(1, T - 1);
     }
     __syncthreads();  // (1) cursors final
+  } else if (PREC == 1 && threadIdx.x >= DEC_THREADS) {
+    // ======================================================= MMA issuer warp (bf16)
+    if constexpr (PREC == 1) {
+      uint32_t aph = 0;
+      auto any_t = [&](int t) -> bool {  // does any slot of this CTA hold an active row at front t
+        const int rlo = t - uw + 1 > 0 ? (t - uw + 3) / 3 : 0;
+        const int rhi = min(uh - 1, t / 3);
+        if (rlo > rhi) return false;
+        const uint32_t m = (uint32_t)rlo & (NS - 1), b = rank * ROWS;
+        const uint32_t d = m - b < (uint32_t)ROWS ? 0u : ((b - m) & (NS - 1));
+        return rlo + (int)d <= rhi;
+      };
+      // layer 1 of front t over the 76 early taps, once every row warp has
+      // written them and loaded the previous logits (a_ready)
+      auto issue_l0 = [&](bool a) {
+        if (a) {
+          mbar_wait(a_ready, aph);
+          eng.issue_warp(0);
+        }
+        aph ^= 1u;  // every row warp arrives once per front
+      };
+      issue_l0(any_t(0));
+#pragma unroll 1
+      for (int t = 0; t < T; ++t) {
+        if (any_t(t)) eng.dec_issue_network();
+        const bool an = any_t(t + 1);
+        if (NC > 1) {
+          cluster_arrive();
+          issue_l0(an);
+          cluster_wait();
+        } else {
+          issue_l0(an);
+          __syncthreads();
+        }
+      }
+    }
+    __syncthreads();  // (1) cursors final
   } else {
     // ======================================================= row warps
     const int row = tile_row();
@@ -1137,7 +1177,6 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
     // (TM_A0), so the gather runs during the network; the signal only has to
     // follow this thread's load of the logits (the MMA overwrites them).
     // fp32: the input shares the logits buffer.
-    uint32_t a_phase = 0;
     auto early_gather = [&](int rn, int cn) {
       if constexpr (PREC == 1) early_put(rn, cn);
     };
@@ -1152,15 +1191,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
         early_put(rn, cn);
       }
     };
-    auto issue_early = [&](bool any_n) {
-      if constexpr (PREC == 1) {
-        if (any_n && (threadIdx.x >> 5) == (TcEngine::MMA_ISSUER >> 5)) {  // whole warp, one lane issues
-          mbar_wait(a_ready, a_phase);
-          eng.issue_warp(0);
-        }
-        a_phase ^= 1u;  // every warp arrives once per front
-      }
-    };
+    auto issue_early = [&](bool) {};  // bf16: the issuer warp issues layer 1
 
     // Front range [rlo, rhi] of active rows, kept incrementally (no
     // divisions): t = 3*q3 + m3, W = 3*qw + mw, rhi = min(H-1, q3),
@@ -1212,10 +1243,13 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
         pf.mark(1);
         // network; the next front's early gather runs in the layer-3 MMA
         // wait (layer 5 for the warp that issues layer 3)
-        eng.run_rest(xa, xb, [&](int l) {
-          const bool w9 = (threadIdx.x >> 5) == (TcEngine::MMA_ISSUER2 >> 5);
-          if (l == (w9 ? 4 : 2)) early_gather(rn, cn);
-        }, PROF ? &pf : nullptr);
+        if constexpr (PREC == 1) {
+          eng.run_rest_ws(xa, xb, [&](int l) {
+            if (l == 2) early_gather(rn, cn);
+          });
+        } else {
+          eng.run_rest(xa, xb, [&](int) {}, PROF ? &pf : nullptr);
+        }
         pf.mark(3);
         asm volatile("bar.sync 7, %0;" ::"n"(DEC_THREADS) : "memory");  // this front's slots (rANS warp)
         uint32_t fs, cs;
@@ -1385,7 +1419,7 @@ static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uin
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.n_img * p.upi * p.nc);
-  cfg.blockDim = dim3(DEC_THREADS);
+  cfg.blockDim = dim3(dec_block(PREC));
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
   if (p.nc > 8) {
