@@ -91,6 +91,15 @@ constexpr uint32_t TM_X = 320;   // exchange slot s: columns TM_X+4s+j (lower ha
 constexpr uint32_t TM_XUP = 32;  //   and TM_X+32+4s+j (upper half-warp copy)
 constexpr uint32_t TM_COLS = 512;
 constexpr int NXSLOT = 7;  // 0 max, 1 Z, 2 F, 3 fc, 4/5 search result, 6 slot
+#ifndef DLIC_SPLIT_LOGITS
+#define DLIC_SPLIT_LOGITS 1
+#endif
+
+// decoder: last layer as two N=128 halves, the first issued per column group
+constexpr bool DEC_SPLIT_LOGITS = DLIC_SPLIT_LOGITS != 0;
+// decoder hidden accumulator of odd layers (layer l at dcol_of(l)); with the
+// split logits, layer 5 (l = 4) must sit in [128,256)
+constexpr uint32_t DEC_D_ODD = DEC_SPLIT_LOGITS ? 0u : 128u;
 constexpr int NXS_SMEM = 4;  // shared-memory exchange slots of the encoder engines (0 max, 1 Z, 2 F, 3 fc)
 
 // ------------------------------------------------------------- small PTX
@@ -447,13 +456,15 @@ struct TcEngineT {
   }
   // K-slices [s0, s1) of layer l into the accumulator at column dcol (whole
   // converged warp, one elected lane issues; no commit).
-  __device__ __forceinline__ void issue_slices(int l, int s0, int s1, uint32_t dcol) const {
+  // NI/N0: instruction N and first output column (a column range of the
+  // layer's weight image; NI = 0 -> the whole layer)
+  __device__ __forceinline__ void issue_slices(int l, int s0, int s1, uint32_t dcol, int NI = 0, int N0 = 0) const {
     tc_fence_after();
     const int N = layer_n(l);
-    const uint32_t id = umma_idesc(64, N);
+    const uint32_t id = umma_idesc(64, NI ? NI : N);
     const uint32_t lbo = (uint32_t)N * 16u;
     const uint32_t kstep = 2u * (uint32_t)(N / 8) * 128u;
-    const uint64_t bd = umma_desc(wsmem + wimg_off(l), lbo, 128u);
+    const uint64_t bd = umma_desc(wsmem + wimg_off(l) + (uint32_t)(N0 / 8) * 128u, lbo, 128u);
     const uint32_t at = tmem + (l == 0 ? A0O : AO);
     for (int kk = s0; kk < s1; ++kk)
       umma_ts_warp(tmem + dcol, at + 8u * (uint32_t)kk, bd + (uint64_t)((kstep >> 4) * (uint32_t)kk), id,
@@ -560,7 +571,7 @@ struct TcEngineT {
   // groups still finish.  Hidden accumulators alternate between columns
   // [0,128) and [128,256) (layer l at 128*(l&1)); the logits take [0,256)
   // after every group's last hidden epilogue (dec_issue_network).
-  static __device__ __forceinline__ uint32_t dcol_of(int l) { return (l & 1) ? 128u : 0u; }
+  static __device__ __forceinline__ uint32_t dcol_of(int l) { return (l & 1) ? DEC_D_ODD : 128u - DEC_D_ODD; }
   // group j signals on named barrier 8 + j (its 4 warps arrive, the issuer
   // warp syncs: 160 threads)
   template <class Hook>
@@ -573,7 +584,7 @@ struct TcEngineT {
     };
     load_bias(0, bq);
     wait_mma();
-    epilogue_at<true>(0u, bq, xa, xb);
+    epilogue_at<true>(dcol_of(0), bq, xa, xb);
     signal();
 #pragma unroll 1
     for (int l = 1; l < NLAYER; ++l) {
@@ -596,6 +607,16 @@ struct TcEngineT {
           asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
           issue_slices(l, 2 * j, 2 * j + 2, dcol_of(l));
         }
+      } else if (DEC_SPLIT_LOGITS) {
+        // logits columns [0,128) into [0,128) (layer 4's accumulator, long
+        // read) group by group; [128,256) over layer 5's accumulator after
+        // every group's epilogue
+#pragma unroll
+        for (int j = 0; j < NGRP; ++j) {
+          asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
+          issue_slices(l, 2 * j, 2 * j + 2, TM_D, 128, 0);
+        }
+        issue_slices(l, 0, 8, TM_D + 128u, 128, 128);
       } else {  // logits over [0,256): after every group's last hidden epilogue
 #pragma unroll
         for (int j = 0; j < NGRP; ++j) asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");

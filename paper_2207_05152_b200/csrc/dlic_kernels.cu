@@ -1095,7 +1095,8 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       auto issue_l0 = [&](bool a) {
         if (a) {
           mbar_wait(a_ready, aph);
-          eng.issue_warp(0);
+          eng.issue_slices(0, 0, KPAD / 16, TcEngine::dcol_of(0));
+          eng.commit_warp();
         }
         aph ^= 1u;  // every row warp arrives once per front
       };
