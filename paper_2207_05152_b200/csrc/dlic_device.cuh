@@ -39,6 +39,11 @@ constexpr int NTHREADS = 512;
 constexpr uint32_t RANS_L = 1u << 16;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float Q1_SCALE = 65279.0f;  // 2^16 - 257 (R5, Q1')
+// exp pairs q with q % 8 >= DLIC_POLY_FROM use the FMA-pipe polynomial (4 of
+// 16 pairs), the rest MUFU ex2 (measured best split on C2 decode)
+#ifndef DLIC_POLY_FROM
+#define DLIC_POLY_FROM 6
+#endif
 
 // Layer-1 K order of the bf16 engine.  K position p = 10u + i belongs to
 // thread u = 2j + h (column group j, half h), which feeds A packed columns
@@ -852,7 +857,7 @@ struct Q1Work {
     for (int q = Q0; q < Q1; ++q) {
       const f2 t = f2_fma(f2_bits(v[2 * q], v[2 * q + 1]), l2e, nm);
       float e0, e1;
-      if (q % 8 >= 5) {  // 6 of 16 pairs on the FMA pipe, the rest on MUFU
+      if (q % 8 >= DLIC_POLY_FROM) {  // 4 of 16 pairs on the FMA pipe, the rest on MUFU
         f2_split(f2_exp2_poly(t), e0, e1);
       } else {
         float t0, t1;
