@@ -24,6 +24,7 @@
 #include "dlic_internal.h"
 
 
+
 namespace dlic {
 
 // Decoded-pixel ring, column-major so the 32 lanes of a warp (consecutive
@@ -1052,6 +1053,10 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
 #pragma unroll 1
     for (int t = 0; t < T; ++t) {
       if (t > 0) {
+        // the words front t-1's steps may read: loaded here, after the
+        // barrier (the L2 latency is in this warp's slack, not in its arrive)
+        prefetch(0, t - 1);
+        prefetch(1, t - 1);
         apply(0, t - 1);
         apply(1, t - 1);
         __syncwarp();  // cursor updates before the prefetch reads them
@@ -1069,11 +1074,11 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         s_slot[32 * hf + lane] = xs[hf] & 0xFFFFu;
       }
       asm volatile("bar.arrive 7, %0;" ::"n"(DEC_THREADS) : "memory");  // slots of front t published
-      prefetch(0, t);
-      prefetch(1, t);
       front_end();
     }
     if (T > 0) {  // the last front's steps
+      prefetch(0, T - 1);
+      prefetch(1, T - 1);
       apply(0, T - 1);
       apply(1, T - 1);
     }
