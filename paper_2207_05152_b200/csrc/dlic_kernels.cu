@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 //   [320,448) b: hidden accumulator      [448,512) b: A operand
 // The logits of the two slots share [0,256): b's last layer is issued after
 // a's logits are in registers, and the next a's first layer after b's.
-// Row warps arrive on rdy[s] (16 arrivals) when slot s's next MMA may go;
+// Row warps arrive on named barrier 8 + s when slot s's next MMA may go;
 // the issuer commits each layer to mma[s].  Exchanges go through shared
 // memory (one region per slot).  Every row sees exactly the decoder's
 // per-row instruction sequence (same engine code, same Q1Work stages), so
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
     k_enc_pp(Plan p, DevWeights w, const uint8_t* __restrict__ imgs, uint32_t* __restrict__ fc,
              unsigned long long* __restrict__ prof) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t bars[4];  // mma[0], mma[1] (tcgen05.commit), rdy[0], rdy[1] (16 row warps)
+  __shared__ uint64_t bars[2];  // mma[0], mma[1] (tcgen05.commit)
   __shared__ uint32_t tslot;
   load_smem(smem, w.wimg, WIMG_BYTES);
   load_smem(smem + WIMG_BYTES, w.bias, BIAS_BYTES);
@@ -371,8 +371,6 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
   if (threadIdx.x == 0) {
     mbar_init(smem_u32(&bars[0]), 1);
     mbar_init(smem_u32(&bars[1]), 1);
-    mbar_init(smem_u32(&bars[2]), NTHREADS / 32);
-    mbar_init(smem_u32(&bars[3]), NTHREADS / 32);
     fence_mbar_init();
   }
   tc_fence_before();
@@ -389,7 +387,6 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
   ea.phase = eb.phase = 0;
   ea.xs = xsb;
   eb.xs = xsb + NXS_SMEM * NGRP * ROWS;
-  const uint32_t rdy0 = smem_u32(&bars[2]), rdy1 = smem_u32(&bars[3]);
 
   const uint64_t total = (uint64_t)p.n_img * p.upi * p.tiles_per_unit;
   const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
@@ -402,19 +399,16 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
     // ================================================ issuer warp
     // (the whole warp runs the loop converged; one elected lane issues, the
     // per-layer descriptors are compile-time constants + the TMEM/smem bases)
-    uint32_t ph0 = 0, ph1 = 0;
     unsigned long long idle = 0, t0c = prof ? clock64() : 0;
 #pragma unroll 1
     for (uint32_t k = 0; k < npairs; ++k) {
 #pragma unroll
       for (int l = 0; l < NLAYER; ++l) {
         const unsigned long long c0 = prof ? clock64() : 0;
-        mbar_wait(rdy0, ph0);
-        ph0 ^= 1u;
+        asm volatile("bar.sync 8, %0;" ::"n"(ENC_PP_THREADS) : "memory");  // slot a ready
         ea.issue_warp(l);
         const unsigned long long c1 = prof ? clock64() : 0;
-        mbar_wait(rdy1, ph1);
-        ph1 ^= 1u;
+        asm volatile("bar.sync 9, %0;" ::"n"(ENC_PP_THREADS) : "memory");  // slot b ready
         if (prof) idle += clock64() - c1;
         eb.issue_warp(l);
         (void)c0;
@@ -528,11 +522,13 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
       const int rr = max(fr + gu - 8, 0);
       asm volatile("prefetch.global.L1 [%0];" ::"l"(fimg + (int64_t)rr * p.W + max(cc - 6, 0)));
     };
-    auto signal = [&](uint32_t bar) {
+    // slot s's next MMA may go: named barrier 8 + s (the 16 row warps
+    // arrive, the issuer warp syncs)
+    auto signal = [&](int slot) {
       tc_wait_st();
       tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar);
+      if (slot == 0) asm volatile("bar.arrive 8, %0;" ::"n"(ENC_PP_THREADS) : "memory");
+      else asm volatile("bar.arrive 9, %0;" ::"n"(ENC_PP_THREADS) : "memory");
     };
     auto write_fc = [&](const Px& x, const Q1Work<true>& qw) {
       const int c0 = 64 * col_grp() + 32 * half_id();
@@ -557,9 +553,9 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
     if (npairs > 0) {
       float xaA, xbA, xaB, xbB;
       Px A = feed_px(ea, true, xaA, xbA);
-      signal(rdy0);
+      signal(0);
       Px B = feed_px(eb, ntl > 1, xaB, xbB);
-      signal(rdy1);
+      signal(1);
       float2 bq[8];
       const bool pon = prof != nullptr && threadIdx.x == 0;
       unsigned long long pt = pon ? clock64() : 0;
@@ -578,11 +574,11 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
         ea.load_bias(0, bq);
         ea.wait_mma();
         ea.template epilogue<true>(bq, xaA, xbA);
-        signal(rdy0);
+        signal(0);
         eb.load_bias(0, bq);
         eb.wait_mma();
         eb.template epilogue<true>(bq, xaB, xbB);
-        signal(rdy1);
+        signal(1);
         pmark(0);
 #pragma unroll 1
         for (int l = 1; l < NLAYER - 1; ++l) {
@@ -592,7 +588,7 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
           pmark(7);
           ea.template epilogue<false>(bq, 0.0f, 0.0f);
           pmark(11);
-          signal(rdy0);  // l = 4: a's last layer (logits -> [0,256))
+          signal(0);  // l = 4: a's last layer (logits -> [0,256))
           pmark(12);
           if (l == 2) prefetch_ahead(0);
           if (l == 3) prefetch_ahead(1);
@@ -602,7 +598,7 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
           pmark(7);
           eb.template epilogue<false>(bq, 0.0f, 0.0f);
           pmark(11);
-          if (l < NLAYER - 2) signal(rdy1);
+          if (l < NLAYER - 2) signal(1);
           pmark(12);
         }
         const bool more = k + 1 < npairs;
@@ -611,7 +607,7 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
           uint32_t v[32];
           ea.wait_mma();
           ea.ld32(v);
-          signal(rdy1);
+          signal(1);
           pmark(1);
           finish(ea, v, A);  // overlaps b's last layer
           pmark(2);
@@ -624,9 +620,9 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
           eb.ld32(v);
           const Px Bc = B;
           if (more) {
-            signal(rdy0);  // next a's layer 1: input written, b's logits out of [0,256)
+            signal(0);  // next a's layer 1: input written, b's logits out of [0,256)
             B = feed_px(eb, 2 * k + 3 < ntl, xaB, xbB);
-            signal(rdy1);
+            signal(1);
           }
           pmark(4);
           finish(eb, v, Bc);  // overlaps the next pair's layer 1
