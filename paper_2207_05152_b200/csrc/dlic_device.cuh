@@ -591,7 +591,7 @@ struct TcEngineT {
     wait_mma();
     epilogue_at<true>(dcol_of(0), bq, xa, xb);
     signal();
-#pragma unroll 1
+#pragma unroll
     for (int l = 1; l < NLAYER; ++l) {
       hook(l);
       if (l < NLAYER - 1) load_bias(l, bq);
