@@ -422,6 +422,13 @@ def main():
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": src + (" bf16_tflops" if prec == 1 else " sm_max_mhz x 148 SM x 128 FFMA x 2 (DESIGN.md)"),
                          "latency_floor_ms": floor_ms, "latency_frac": floor_ms / t_dec},
+            # the throughput-bound encoder MLP (all pixels at once) against the same peak
+            "roofline_encode": {"kernel": "k_enc_pp" if prec == 1 else "k_enc_mlp<fp32>",
+                                "bound": "tensor" if prec == 1 else "alu",
+                                "achieved": FLOP_PER_PX * px_rank / (mlp_ms / 1e3) / 1e12, "peak": peak,
+                                "unit": "TFLOP/s",
+                                "frac": FLOP_PER_PX * px_rank / (mlp_ms / 1e3) / 1e12 / peak,
+                                "note": "M=64 tcgen05 tiles cost as M=128: ceiling 0.5 of peak (DESIGN.md)"},
             "variants": variants,
             "cpu_baseline": cpu,
             "e2e": e2e,
