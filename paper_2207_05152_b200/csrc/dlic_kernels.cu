@@ -1224,17 +1224,23 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
     early_gather(r, c);
     early_signal(r, c);
     issue_early(any);
-    if (pf.on) pf.t = clock64();
-#pragma unroll 1
-    for (int t = 0; t < T; ++t) {
-      int rn, cn, rlo, rhi;
+    // front t+1 (used by front t's early gather); advanced in the end-of-front
+    // barrier window, off the critical path
+    int rn, cn;
+    bool active_n, any_n;
+    {
+      int rlo, rhi;
       if (++m3 == 3) {
         m3 = 0;
         ++q3;
       }
-      range(t + 1, q3, m3, rlo, rhi);
-      const bool active_n = slot_at(t + 1, rlo, rhi, rn, cn);
-      const bool any_n = any_at(rlo, rhi);
+      range(1, q3, m3, rlo, rhi);
+      active_n = slot_at(1, rlo, rhi, rn, cn);
+      any_n = any_at(rlo, rhi);
+    }
+    if (pf.on) pf.t = clock64();
+#pragma unroll 1
+    for (int t = 0; t < T; ++t) {
       bool pub = false;
       pf.mark(0);
       if (any) {
@@ -1313,12 +1319,32 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       // end-of-front barrier; the next front's layer-1 MMA is issued between
       // its arrive and wait.  (A point-to-point variant -- halo writers
       // arriving remotely on a successor mbarrier -- measured slower.)
+      int rn2, cn2;
+      bool active_n2, any_n2;
       if (NC > 1) {
         cluster_arrive();
         issue_early(any_n);
+        {  // front t+2's geometry while the cluster arrives
+          int rlo, rhi;
+          if (++m3 == 3) {
+            m3 = 0;
+            ++q3;
+          }
+          range(t + 2, q3, m3, rlo, rhi);
+          active_n2 = slot_at(t + 2, rlo, rhi, rn2, cn2);
+          any_n2 = any_at(rlo, rhi);
+        }
         cluster_wait();
       } else {
         issue_early(any_n);
+        int rlo, rhi;
+        if (++m3 == 3) {
+          m3 = 0;
+          ++q3;
+        }
+        range(t + 2, q3, m3, rlo, rhi);
+        active_n2 = slot_at(t + 2, rlo, rhi, rn2, cn2);
+        any_n2 = any_at(rlo, rhi);
         __syncthreads();
       }
       // the pixel's HBM store after the barrier: its release need not wait for it
@@ -1328,6 +1354,10 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       c = cn;
       active = active_n;
       any = any_n;
+      rn = rn2;
+      cn = cn2;
+      active_n = active_n2;
+      any_n = any_n2;
     }
     __syncthreads();  // (1) cursors final
   }
