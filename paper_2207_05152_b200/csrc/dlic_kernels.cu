@@ -1238,6 +1238,9 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       active_n = slot_at(1, rlo, rhi, rn, cn);
       any_n = any_at(rlo, rhi);
     }
+    uint32_t fpo = (uint32_t)(ring_at(r, c) - ring) + 8u;  // the front's fresh-tap ring position
+    uint8_t* optr = nullptr;  // deferred pixel store
+    int opix = 0;
     if (pf.on) pf.t = clock64();
 #pragma unroll 1
     for (int t = 0; t < T; ++t) {
@@ -1245,18 +1248,22 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       pf.mark(0);
       if (any) {
         // the fresh taps (0,-1) and (-1,+2), decoded on front t-1
-        const uint8_t* fp = ring_at(r, c) + 8;
+        const uint8_t* fp = ring + fpo;
         const float xa = u8_unit(fp[-RING_ROWS]);
         const float xb = u8_unit(fp[2 * RING_ROWS - 1]);
         pf.mark(1);
-        // network; the next front's early gather runs in the layer-3 MMA
-        // wait (layer 5 for the warp that issues layer 3)
+        // network; the previous front's pixel goes to HBM in the layer-2 MMA
+        // wait, the next front's early gather in the layer-3 MMA wait
         if constexpr (PREC == 1) {
           eng.run_rest_ws(xa, xb, [&](int l) {
+            if (l == 1 && optr) *optr = (uint8_t)opix;
             if (l == 2) early_gather(rn, cn);
           });
         } else {
-          eng.run_rest(xa, xb, [&](int) {}, PROF ? &pf : nullptr);
+          eng.run_rest(xa, xb, [&](int l) {
+            if (l == 1 && optr) *optr = (uint8_t)opix;
+            (void)l;
+          }, PROF ? &pf : nullptr);
         }
         pf.mark(3);
         asm volatile("bar.sync 7, %0;" ::"n"(DEC_THREADS) : "memory");  // this front's slots (rANS warp)
@@ -1313,6 +1320,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         pf.mark(9);
       } else {
         asm volatile("bar.sync 7, %0;" ::"n"(DEC_THREADS) : "memory");  // keep the barrier in step
+        if (optr) *optr = (uint8_t)opix;
         early_gather(rn, cn);
         early_signal(rn, cn);
       }
@@ -1321,9 +1329,11 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       // arriving remotely on a successor mbarrier -- measured slower.)
       int rn2, cn2;
       bool active_n2, any_n2;
+      uint32_t fpo_n;
       if (NC > 1) {
         cluster_arrive();
         issue_early(any_n);
+        fpo_n = (uint32_t)(ring_at(rn, cn) - ring) + 8u;
         {  // front t+2's geometry while the cluster arrives
           int rlo, rhi;
           if (++m3 == 3) {
@@ -1337,6 +1347,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         cluster_wait();
       } else {
         issue_early(any_n);
+        fpo_n = (uint32_t)(ring_at(rn, cn) - ring) + 8u;
         int rlo, rhi;
         if (++m3 == 3) {
           m3 = 0;
@@ -1347,8 +1358,10 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         any_n2 = any_at(rlo, rhi);
         __syncthreads();
       }
-      // the pixel's HBM store after the barrier: its release need not wait for it
-      if (pub) oimg[(uint64_t)r * p.W + c] = (uint8_t)pix;
+      // the pixel's HBM store: issued in the next front's layer-2 MMA wait (off
+      // the post-barrier critical path; the barrier's release never waits for it)
+      optr = pub ? oimg + (uint64_t)r * p.W + c : nullptr;
+      opix = pix;
       pf.mark(10);
       r = rn;
       c = cn;
@@ -1358,7 +1371,9 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       cn = cn2;
       active_n = active_n2;
       any_n = any_n2;
+      fpo = fpo_n;
     }
+    if (optr) *optr = (uint8_t)opix;  // the last front's pixel
     __syncthreads();  // (1) cursors final
   }
   if (pf.on) {
