@@ -258,6 +258,12 @@ __device__ __forceinline__ void tmem_ld16h(uint32_t taddr, uint32_t (&v)[16]) {
       : "r"(taddr), "n"(OFF));
 }
 template <int OFF>
+__device__ __forceinline__ void tmem_ld8h(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : DLIC_R8(0)
+               : "r"(taddr), "n"(OFF));
+}
+template <int OFF>
 __device__ __forceinline__ void tmem_ld4h(uint32_t taddr, uint32_t (&v)[4]) {
   asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x4.b32 {%0,%1,%2,%3}, [%4], %5;" : DLIC_R4(0) : "r"(taddr), "n"(OFF));
 }
@@ -655,6 +661,16 @@ struct TcEngineT {
       tc_fence_after();
     }
   }
+  // slots s and s+1 (adjacent TMEM columns) with one load
+  __device__ __forceinline__ void xget8(int slot, uint32_t (&v)[8]) const {
+    if constexpr (XS) {
+#pragma unroll
+      for (int g = 0; g < 2 * NGRP; ++g) v[g] = xs[(slot * NGRP + g) * ROWS + tile_row()];
+    } else {
+      tmem_ld8h<TM_XUP>(tmem + lane_off() + TM_X + 4u * (uint32_t)slot, v);
+      tc_wait_ld();
+    }
+  }
   __device__ __forceinline__ void xget4(int slot, uint32_t (&v)[4]) const {
     if constexpr (XS) {
 #pragma unroll
@@ -746,6 +762,10 @@ struct Fp32Engine {
     if (half_id() == 0) xbuf[(slot * NGRP + col_grp()) * ROWS + tile_row()] = v;
   }
   __device__ __forceinline__ void xsync() const { quad_sync(); }
+  __device__ __forceinline__ void xget8(int slot, uint32_t (&v)[8]) const {  // slots s, s+1
+#pragma unroll
+    for (int g = 0; g < 2 * NGRP; ++g) v[g] = xbuf[(slot * NGRP + g) * ROWS + tile_row()];
+  }
   __device__ __forceinline__ void xget4(int slot, uint32_t (&v)[4]) const {
 #pragma unroll
     for (int g = 0; g < NGRP; ++g) v[g] = xbuf[(slot * NGRP + g) * ROWS + tile_row()];
@@ -882,9 +902,10 @@ struct Q1Work {
     e.xput(0, __float_as_uint(m));
     e.xput(1, __float_as_uint(z));
     e.xsync();
-    uint32_t x4[4], z4[4];
-    e.xget4(0, x4);
-    e.xget4(1, z4);
+    uint32_t x8[8];
+    e.xget8(0, x8);  // m_j (slot 0) and z_j (slot 1) in one load
+    const uint32_t* x4 = x8;
+    const uint32_t* z4 = x8 + 4;
     // M = max_j m_j;  Z = sum_j z_j 2^(m_j - M) in a fixed order;  group scale
     // s_j = 2^(m_j - M) / Z, so p_i = e_i * s_j = exp(l_i - M) / Z.
     const float M = fmaxf(fmaxf(__uint_as_float(x4[0]), __uint_as_float(x4[1])),
