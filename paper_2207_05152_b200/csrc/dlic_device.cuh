@@ -105,6 +105,14 @@ constexpr bool DEC_SPLIT_LOGITS = DLIC_SPLIT_LOGITS != 0;
 // decoder hidden accumulator of odd layers (layer l at dcol_of(l)); with the
 // split logits, layer 5 (l = 4) must sit in [128,256)
 constexpr uint32_t DEC_D_ODD = DEC_SPLIT_LOGITS ? 0u : 128u;
+#ifndef DLIC_NSPLIT
+#define DLIC_NSPLIT 1
+#endif
+#ifndef DLIC_NSPLIT_ORDER
+#define DLIC_NSPLIT_ORDER 1
+#endif
+// decoder: hidden layers as two N=64 halves committed separately
+constexpr bool DEC_NSPLIT = DLIC_NSPLIT != 0;
 constexpr int NXS_SMEM = 4;  // shared-memory exchange slots of the encoder engines (0 max, 1 Z, 2 F, 3 fc)
 
 // ------------------------------------------------------------- small PTX
@@ -405,6 +413,7 @@ struct TcEngineT {
   uint32_t bar;        // shared address of the MMA-completion mbarrier
   uint32_t phase;
   uint32_t* xs;        // XS: shared exchange words [NXS_SMEM][NGRP][ROWS]
+  uint32_t bar2;       // decoder (DEC_NSPLIT): completion of the hidden layers' columns [64,128)
 
   __device__ __forceinline__ uint32_t lane_off() const { return ((threadIdx.x >> 5) & 3u) << 21; }
 
@@ -498,6 +507,18 @@ struct TcEngineT {
     mbar_wait(bar, phase);
     phase ^= 1u;
     tc_fence_after();
+  }
+  // decoder: column groups 0-1 wait on `bar`, groups 2-3 on `bar2` (the two
+  // N=64 halves of a hidden layer complete separately)
+  __device__ __forceinline__ void wait_mma_g() {
+    if (DEC_NSPLIT) mbar_wait(col_grp() < 2 ? bar : bar2, phase);
+    else mbar_wait(bar, phase);
+    phase ^= 1u;
+    tc_fence_after();
+  }
+  __device__ __forceinline__ void commit_both() const {
+    umma_commit_warp(bar);
+    if (DEC_NSPLIT) umma_commit_warp(bar2);
   }
   // bias + ReLU + bf16 -> next A; this thread's columns [32j+16h, +16)
   // (packed column 16j+8h+q holds activations 32j+16h+2q, +1: identity K order).
@@ -594,14 +615,14 @@ struct TcEngineT {
       asm volatile("bar.arrive %0, 160;" ::"r"(gbar) : "memory");
     };
     load_bias(0, bq);
-    wait_mma();
+    wait_mma_g();
     epilogue_at<true>(dcol_of(0), bq, xa, xb);
     signal();
 #pragma unroll
     for (int l = 1; l < NLAYER; ++l) {
       hook(l);
       if (l < NLAYER - 1) load_bias(l, bq);
-      wait_mma();
+      wait_mma_g();
       if (l < NLAYER - 1) {
         epilogue_at<false>(dcol_of(l), bq, 0.0f, 0.0f);
         signal();
@@ -612,6 +633,30 @@ struct TcEngineT {
   __device__ __forceinline__ void dec_issue_network() const {
 #pragma unroll
     for (int l = 1; l < NLAYER; ++l) {
+      if (l < NLAYER - 1 && DEC_NSPLIT) {
+        // two N=64 halves: columns [0,64) (groups 0-1's next epilogue) are
+        // committed to bar first, [64,128) to bar2
+        const uint32_t d = dcol_of(l);
+        asm volatile("bar.sync 8, 160;" ::: "memory");
+        issue_slices(l, 0, 2, d, 64, 0);
+        asm volatile("bar.sync 9, 160;" ::: "memory");
+        issue_slices(l, 2, 4, d, 64, 0);
+#if DLIC_NSPLIT_ORDER == 0
+        issue_slices(l, 0, 4, d + 64u, 64, 64);
+#endif
+        asm volatile("bar.sync 10, 160;" ::: "memory");
+        issue_slices(l, 4, 6, d, 64, 0);
+        asm volatile("bar.sync 11, 160;" ::: "memory");
+        issue_slices(l, 6, 8, d, 64, 0);
+        umma_commit_warp(bar);
+#if DLIC_NSPLIT_ORDER == 0
+        issue_slices(l, 4, 8, d + 64u, 64, 64);
+#else
+        issue_slices(l, 0, 8, d + 64u, 64, 64);
+#endif
+        umma_commit_warp(bar2);
+        continue;
+      }
       if (l < NLAYER - 1) {
 #pragma unroll
         for (int j = 0; j < NGRP; ++j) {
@@ -633,7 +678,7 @@ struct TcEngineT {
         for (int j = 0; j < NGRP; ++j) asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
         issue_slices(l, 0, 8, TM_D);
       }
-      commit_warp();
+      commit_both();
     }
   }
 

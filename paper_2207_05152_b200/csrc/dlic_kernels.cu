@@ -916,6 +916,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
 
   typename EngineSel<PREC>::T eng;
   uint8_t* ring = engine_setup<PREC>(eng, smem, w, bar, &tslot);
+  if constexpr (PREC == 1) eng.bar2 = smem_u32(&bar[2]);
   uint32_t* cursor = reinterpret_cast<uint32_t*>(ring + RING_BYTES + 16);  // 16 zero bytes after the ring
   uint32_t* s_sbase = cursor + ((un.ngroups + 3u) & ~3u);                   // per-group stream table
   uint32_t* s_slen = s_sbase + ((un.ngroups + 3u) & ~3u);
@@ -932,6 +933,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
   // named barrier 7 (16 row warps sync, the rANS warp arrives): slots ready
   if (threadIdx.x == 0) {
     mbar_init(a_ready, NTHREADS / 32);
+    mbar_init(smem_u32(&bar[2]), 1);  // second MMA-completion barrier (DEC_NSPLIT)
     fence_mbar_init();
   }
   if (NC > 1) cluster_sync_all();
@@ -1097,7 +1099,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         if (a) {
           mbar_wait(a_ready, aph);
           eng.issue_slices(0, 0, KPAD / 16, TcEngine::dcol_of(0));
-          eng.commit_warp();
+          eng.commit_both();
         }
         aph ^= 1u;  // every row warp arrives once per front
       };
