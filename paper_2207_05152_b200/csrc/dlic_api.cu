@@ -618,7 +618,7 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
       CUDA_TRY(cudaStreamSynchronize(st));
       const double ctas = (double)p.n_img * p.upi * p.nc;
       const double T = (double)(p.tw + 3 * (p.th - 1));
-      const char* nm[11] = {"top", "gather", "put", "mlp", "pass1", "xchg", "pass2", "passA", "search", "rans",
+      const char* nm[11] = {"top", "gather", "put", "mlp", "pass1", "xchg", "bar7", "passA", "search", "rans",
                             "barrier"};
       fprintf(stderr, "[dlic prof] cycles per front per CTA:");
       for (int k = 0; k < 11; ++k) fprintf(stderr, " %s %.0f", nm[k], hp[k] / ctas / T);

@@ -108,6 +108,9 @@ constexpr uint32_t DEC_D_ODD = DEC_SPLIT_LOGITS ? 0u : 128u;
 #ifndef DLIC_NSPLIT
 #define DLIC_NSPLIT 1
 #endif
+#ifndef DLIC_LOGIT_EARLY
+#define DLIC_LOGIT_EARLY 1
+#endif
 #ifndef DLIC_NSPLIT_ORDER
 #define DLIC_NSPLIT_ORDER 1
 #endif
@@ -672,6 +675,14 @@ struct TcEngineT {
           asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
           issue_slices(l, 2 * j, 2 * j + 2, TM_D, 128, 0);
         }
+#if DLIC_LOGIT_EARLY
+        if (DEC_NSPLIT) {  // groups 0-1's logits are columns [0,128): their softmax may start
+          umma_commit_warp(bar);
+          issue_slices(l, 0, 8, TM_D + 128u, 128, 128);
+          umma_commit_warp(bar2);
+          continue;
+        }
+#endif
         issue_slices(l, 0, 8, TM_D + 128u, 128, 128);
       } else {  // logits over [0,256): after every group's last hidden epilogue
 #pragma unroll

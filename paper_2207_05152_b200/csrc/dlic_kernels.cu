@@ -1269,6 +1269,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         }
         pf.mark(3);
         asm volatile("bar.sync 7, %0;" ::"n"(DEC_THREADS) : "memory");  // this front's slots (rANS warp)
+        pf.mark(6);  // profile: time spent waiting for the rANS warp's slots
         uint32_t fs, cs;
         bool mine;
         const int sym = q1_decode(eng, s_slot[row], mine, fs, cs, [&]() { early_signal(rn, cn); }, &pf);
