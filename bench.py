@@ -195,6 +195,17 @@ def default_batch(cfg):
 
 
 # ------------------------------------------------------------------ reference arm (CPU oracle)
+METRIC = "encode+decode Mpixel/s (8-bit gray, round trip) and bpp"
+
+
+def arm_config(args, n, W, H, tile, g, ws):
+    """The config object of the JSON line (both arms)."""
+    return {"workload": CONFIG_DESC[args.config], "images_per_gpu": n, "width": W, "height": H,
+            "tile": list(tile), "group_rows": g, "precision": args.precision,
+            "weights": "P100K briefly trained by the oracle (fixtures/p100k_trained.dlicmdl)",
+            "l2": "flushed between timed steps (256 MiB write, untimed)", "parallelism": "dp%d" % ws}
+
+
 def run_reference(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -226,12 +237,13 @@ def run_reference(args):
     except Exception:
         cores = os.cpu_count() or 1
     line = {
-        "impl": "reference", "metric": "encode+decode Mpixel/s (8-bit gray, round trip)", "value": mpx,
+        "impl": "reference", "metric": METRIC, "value": mpx,
         "unit": "Mpixel/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64-accum bf16-emulated" if prec else "f64", "data": "synthetic",
-        "config": {"workload": CONFIG_DESC[args.config], "sample": "%dx%d crop" % (sw, sh),
-                   "precision": args.precision},
+        "config": dict(arm_config(args, default_batch(args.config) if not args.batch else args.batch,
+                                  img.shape[1], img.shape[0], tile_for(args)[1], g, ws),
+                       sample="per step the oracle codes a top-left %dx%d crop of one image (untiled)" % (sw, sh)),
         "cpu_baseline": {"value": mpx, "unit": "Mpixel/s", "cores": cores, "kind": "oracle",
                          "sample": "top-left %dx%d crop of the %s image, oracle encode+decode per step"
                                    % (sw, sh, args.config)},
@@ -404,16 +416,13 @@ def main():
         floor_ms = T * 3072 / (peaks.get("sm_max_mhz", 1965.0) * 1e3)
         cpu = cpu_baseline_sample(args, imgs[0]) if ws == 1 else None   # N=1 only (contract)
         line = {
-            "metric": "encode+decode Mpixel/s (8-bit gray, round trip) and bpp",
+            "metric": METRIC,
             "value": ws * px_rank / (ms / 1e3) / 1e6,
             "unit": "Mpixel/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16" if prec == 1 else "f32", "data": "synthetic",
-            "config": {"workload": CONFIG_DESC[args.config], "images_per_gpu": n, "width": W, "height": H,
-                       "tile": list(tile), "group_rows": g, "precision": args.precision,
-                       "weights": "P100K briefly trained by the oracle (fixtures/p100k_trained.dlicmdl)",
-                       "l2": "flushed between timed steps (256 MiB write, untimed)", "parallelism": "dp%d" % ws},
+            "config": arm_config(args, n, W, H, tile, g, ws),
             "encode_mpx_s": ws * px_rank / (t_enc / 1e3) / 1e6,
             "decode_mpx_s": ws * px_rank / (t_dec / 1e3) / 1e6,
             "encode_ms": t_enc, "decode_ms": t_dec, "mlp_ms": mlp_ms,
