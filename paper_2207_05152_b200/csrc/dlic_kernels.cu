@@ -1055,6 +1055,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         // barrier (the L2 latency is in this warp's slack, not in its arrive)
         prefetch(0, t - 1);
         prefetch(1, t - 1);
+        __syncwarp();  // cursor reads before apply's cursor updates
         apply(0, t - 1);
         apply(1, t - 1);
         __syncwarp();  // cursor updates before the prefetch reads them
@@ -1077,6 +1078,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
     if (T > 0) {  // the last front's steps
       prefetch(0, T - 1);
       prefetch(1, T - 1);
+      __syncwarp();
       apply(0, T - 1);
       apply(1, T - 1);
     }
