@@ -108,6 +108,9 @@ constexpr uint32_t DEC_D_ODD = DEC_SPLIT_LOGITS ? 0u : 128u;
 #ifndef DLIC_NSPLIT
 #define DLIC_NSPLIT 1
 #endif
+#ifndef DLIC_EPI2H
+#define DLIC_EPI2H 1
+#endif
 #ifndef DLIC_LOGIT_EARLY
 #define DLIC_LOGIT_EARLY 1
 #endif
@@ -541,6 +544,27 @@ struct TcEngineT {
   __device__ __forceinline__ void epilogue(const float2 (&b2)[8], float xa, float xb) const {
     epilogue_at<L0>(DH, b2, xa, xb);
   }
+  // hidden-layer epilogue in two 8-column halves (the second TMEM load is in
+  // flight while the first half is converted)
+  __device__ __forceinline__ void epilogue_2h(uint32_t dcol, const float2 (&b2)[8]) const {
+    const uint32_t lo = lane_off();
+    const int j = col_grp();
+    uint32_t va[8], vb[8];
+    tmem_ld8h<16>(tmem + lo + dcol + 32u * (uint32_t)j, va);
+    tmem_ld8h<16>(tmem + lo + dcol + 32u * (uint32_t)j + 8u, vb);
+    tc_wait_ld();
+    uint32_t p[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float x0, x1;
+      f2_split(f2_add(f2_bits(va[2 * q], va[2 * q + 1]), f2_make(b2[q].x, b2[q].y)), x0, x1);
+      p[q] = pack_bf16_relu(x0, x1);
+      f2_split(f2_add(f2_bits(vb[2 * q], vb[2 * q + 1]), f2_make(b2[4 + q].x, b2[4 + q].y)), x0, x1);
+      p[4 + q] = pack_bf16_relu(x0, x1);
+    }
+    tmem_st8h<8>(tmem + lo + AO + 16u * (uint32_t)j, p);
+    tc_wait_st();
+  }
   // the same with the accumulator at TMEM column dcol (the decoder's
   // double-buffered hidden accumulator)
   template <bool L0>
@@ -627,7 +651,11 @@ struct TcEngineT {
       if (l < NLAYER - 1) load_bias(l, bq);
       wait_mma_g();
       if (l < NLAYER - 1) {
+#if DLIC_EPI2H
+        epilogue_2h(dcol_of(l), bq);
+#else
         epilogue_at<false>(dcol_of(l), bq, 0.0f, 0.0f);
+#endif
         signal();
       }
     }
