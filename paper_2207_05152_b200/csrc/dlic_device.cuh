@@ -92,6 +92,10 @@ __host__ __device__ constexpr uint32_t f32_off(int l) {
 constexpr uint32_t TM_D = 0;     // accumulator / logits / e / f, 256 columns
 constexpr uint32_t TM_A = 256;   // A operand of layers 2-6, K/2 columns (bf16 pairs), 64
 constexpr uint32_t TM_A0 = 384;  // A operand of layer 1 (80 inputs -> 40 columns)
+// decoder: second A buffer.  With split layers the epilogue of layer l starts
+// (column groups 0-1) while the second half of layer l still reads its input,
+// so consecutive layers' inputs alternate between TM_A and TM_A2.
+constexpr uint32_t TM_A2 = 448;
 constexpr uint32_t TM_X = 320;   // exchange slot s: columns TM_X+4s+j (lower half-warp)
 constexpr uint32_t TM_XUP = 32;  //   and TM_X+32+4s+j (upper half-warp copy)
 constexpr uint32_t TM_COLS = 512;
@@ -484,14 +488,15 @@ struct TcEngineT {
   // converged warp, one elected lane issues; no commit).
   // NI/N0: instruction N and first output column (a column range of the
   // layer's weight image; NI = 0 -> the whole layer)
-  __device__ __forceinline__ void issue_slices(int l, int s0, int s1, uint32_t dcol, int NI = 0, int N0 = 0) const {
+  __device__ __forceinline__ void issue_slices(int l, int s0, int s1, uint32_t dcol, int NI = 0, int N0 = 0,
+                                               uint32_t acol = 0xFFFFFFFFu) const {
     tc_fence_after();
     const int N = layer_n(l);
     const uint32_t id = umma_idesc(64, NI ? NI : N);
     const uint32_t lbo = (uint32_t)N * 16u;
     const uint32_t kstep = 2u * (uint32_t)(N / 8) * 128u;
     const uint64_t bd = umma_desc(wsmem + wimg_off(l) + (uint32_t)(N0 / 8) * 128u, lbo, 128u);
-    const uint32_t at = tmem + (l == 0 ? A0O : AO);
+    const uint32_t at = tmem + (acol != 0xFFFFFFFFu ? acol : (l == 0 ? A0O : AO));
     for (int kk = s0; kk < s1; ++kk)
       umma_ts_warp(tmem + dcol, at + 8u * (uint32_t)kk, bd + (uint64_t)((kstep >> 4) * (uint32_t)kk), id,
                    kk > 0 ? 1u : 0u);
@@ -542,11 +547,11 @@ struct TcEngineT {
   }
   template <bool L0>
   __device__ __forceinline__ void epilogue(const float2 (&b2)[8], float xa, float xb) const {
-    epilogue_at<L0>(DH, b2, xa, xb);
+    epilogue_at<L0>(DH, b2, xa, xb, AO);
   }
   // hidden-layer epilogue in two 8-column halves (the second TMEM load is in
   // flight while the first half is converted)
-  __device__ __forceinline__ void epilogue_2h(uint32_t dcol, const float2 (&b2)[8]) const {
+  __device__ __forceinline__ void epilogue_2h(uint32_t dcol, uint32_t acol, const float2 (&b2)[8]) const {
     const uint32_t lo = lane_off();
     const int j = col_grp();
     uint32_t va[8], vb[8];
@@ -562,13 +567,14 @@ struct TcEngineT {
       f2_split(f2_add(f2_bits(vb[2 * q], vb[2 * q + 1]), f2_make(b2[4 + q].x, b2[4 + q].y)), x0, x1);
       p[4 + q] = pack_bf16_relu(x0, x1);
     }
-    tmem_st8h<8>(tmem + lo + AO + 16u * (uint32_t)j, p);
+    tmem_st8h<8>(tmem + lo + acol + 16u * (uint32_t)j, p);
     tc_wait_st();
   }
   // the same with the accumulator at TMEM column dcol (the decoder's
   // double-buffered hidden accumulator)
   template <bool L0>
-  __device__ __forceinline__ void epilogue_at(uint32_t dcol, const float2 (&b2)[8], float xa, float xb) const {
+  __device__ __forceinline__ void epilogue_at(uint32_t dcol, const float2 (&b2)[8], float xa, float xb,
+                                              uint32_t acol) const {
     const uint32_t lo = lane_off();
     const int j = col_grp(), h = half_id();
     const float4* fw = reinterpret_cast<const float4*>(bias + FRESH_OFF) + 16 * j + 8 * h;
@@ -590,7 +596,7 @@ struct TcEngineT {
       f2_split(f2_add(acc, f2_make(b.x, b.y)), x0, x1);
       p[q] = pack_bf16_relu(x0, x1);  // relu(x) rounded to bf16 (RN)
     }
-    tmem_st8h<8>(tmem + lo + AO + 16u * (uint32_t)j, p);
+    tmem_st8h<8>(tmem + lo + acol + 16u * (uint32_t)j, p);
     tc_wait_st();
   }
   // Layers 1..6 after layer 0's MMAs were issued (start_l0 / issue_l0):
@@ -630,6 +636,8 @@ struct TcEngineT {
   // groups still finish.  Hidden accumulators alternate between columns
   // [0,128) and [128,256) (layer l at 128*(l&1)); the logits take [0,256)
   // after every group's last hidden epilogue (dec_issue_network).
+  // input columns of layer l >= 1 (its A operand), alternating
+  static __device__ __forceinline__ uint32_t ao_of(int l) { return (l & 1) ? TM_A : TM_A2; }
   static __device__ __forceinline__ uint32_t dcol_of(int l) { return (l & 1) ? DEC_D_ODD : 128u - DEC_D_ODD; }
   // group j signals on named barrier 8 + j (its 4 warps arrive, the issuer
   // warp syncs: 160 threads)
@@ -643,7 +651,7 @@ struct TcEngineT {
     };
     load_bias(0, bq);
     wait_mma_g();
-    epilogue_at<true>(dcol_of(0), bq, xa, xb);
+    epilogue_at<true>(dcol_of(0), bq, xa, xb, ao_of(1));
     signal();
 #pragma unroll
     for (int l = 1; l < NLAYER; ++l) {
@@ -652,9 +660,9 @@ struct TcEngineT {
       wait_mma_g();
       if (l < NLAYER - 1) {
 #if DLIC_EPI2H
-        epilogue_2h(dcol_of(l), bq);
+        epilogue_2h(dcol_of(l), ao_of(l + 1), bq);
 #else
-        epilogue_at<false>(dcol_of(l), bq, 0.0f, 0.0f);
+        epilogue_at<false>(dcol_of(l), bq, 0.0f, 0.0f, ao_of(l + 1));
 #endif
         signal();
       }
@@ -669,21 +677,21 @@ struct TcEngineT {
         // committed to bar first, [64,128) to bar2
         const uint32_t d = dcol_of(l);
         asm volatile("bar.sync 8, 160;" ::: "memory");
-        issue_slices(l, 0, 2, d, 64, 0);
+        issue_slices(l, 0, 2, d, 64, 0, ao_of(l));
         asm volatile("bar.sync 9, 160;" ::: "memory");
-        issue_slices(l, 2, 4, d, 64, 0);
+        issue_slices(l, 2, 4, d, 64, 0, ao_of(l));
 #if DLIC_NSPLIT_ORDER == 0
-        issue_slices(l, 0, 4, d + 64u, 64, 64);
+        issue_slices(l, 0, 4, d + 64u, 64, 64, ao_of(l));
 #endif
         asm volatile("bar.sync 10, 160;" ::: "memory");
-        issue_slices(l, 4, 6, d, 64, 0);
+        issue_slices(l, 4, 6, d, 64, 0, ao_of(l));
         asm volatile("bar.sync 11, 160;" ::: "memory");
-        issue_slices(l, 6, 8, d, 64, 0);
+        issue_slices(l, 6, 8, d, 64, 0, ao_of(l));
         umma_commit_warp(bar);
 #if DLIC_NSPLIT_ORDER == 0
-        issue_slices(l, 4, 8, d + 64u, 64, 64);
+        issue_slices(l, 4, 8, d + 64u, 64, 64, ao_of(l));
 #else
-        issue_slices(l, 0, 8, d + 64u, 64, 64);
+        issue_slices(l, 0, 8, d + 64u, 64, 64, ao_of(l));
 #endif
         umma_commit_warp(bar2);
         continue;
@@ -692,7 +700,7 @@ struct TcEngineT {
 #pragma unroll
         for (int j = 0; j < NGRP; ++j) {
           asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
-          issue_slices(l, 2 * j, 2 * j + 2, dcol_of(l));
+          issue_slices(l, 2 * j, 2 * j + 2, dcol_of(l), 0, 0, ao_of(l));
         }
       } else if (DEC_SPLIT_LOGITS) {
         // logits columns [0,128) into [0,128) (layer 4's accumulator, long
@@ -701,21 +709,21 @@ struct TcEngineT {
 #pragma unroll
         for (int j = 0; j < NGRP; ++j) {
           asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
-          issue_slices(l, 2 * j, 2 * j + 2, TM_D, 128, 0);
+          issue_slices(l, 2 * j, 2 * j + 2, TM_D, 128, 0, ao_of(l));
         }
 #if DLIC_LOGIT_EARLY
         if (DEC_NSPLIT) {  // groups 0-1's logits are columns [0,128): their softmax may start
           umma_commit_warp(bar);
-          issue_slices(l, 0, 8, TM_D + 128u, 128, 128);
+          issue_slices(l, 0, 8, TM_D + 128u, 128, 128, ao_of(l));
           umma_commit_warp(bar2);
           continue;
         }
 #endif
-        issue_slices(l, 0, 8, TM_D + 128u, 128, 128);
+        issue_slices(l, 0, 8, TM_D + 128u, 128, 128, ao_of(l));
       } else {  // logits over [0,256): after every group's last hidden epilogue
 #pragma unroll
         for (int j = 0; j < NGRP; ++j) asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
-        issue_slices(l, 0, 8, TM_D);
+        issue_slices(l, 0, 8, TM_D, 0, 0, ao_of(l));
       }
       commit_both();
     }
