@@ -435,16 +435,13 @@ struct TcEngineT {
     tmem_st1h<5>(base + 4, a[4]);
   }
 
-  // Runs the 6 layers (M=64); the input must have been stored with put_input.
-  // hook(l) runs (all threads) after layer l's MMAs are issued, before the
-  // wait for them: work that overlaps the tensor core.
-  // The MMAs are issued by thread MMA_ISSUER (warp 13); layer 3's by
-  // MMA_ISSUER2 (warp 14), so that warp 13 is free for the decoder's hook
-  // work of that layer.  Issuing 8 MMAs keeps the issuing thread busy most of
-  // the layer; both issuers sit on SMSPs without the decoder's rANS warp
-  // (warp 16, SMSP 0), which measured 1.2% faster than warps 8/9.
-  static constexpr unsigned MMA_ISSUER = 416;   // warp 13 (SMSP 1, not shared with the decoder's rANS warp)
-  static constexpr unsigned MMA_ISSUER2 = 448;  // warp 14 (SMSP 2)
+  // Issuers of run_rest (the single-tile-chain path: k_enc_mlp, i.e. the fp32
+  // path's tables and the debug exports): the MMAs of a layer are issued by
+  // warp 13 (layer 3's by warp 14) after a CTA barrier.  The production
+  // encoder (k_enc_pp) and the decoder (run_rest_ws) use a dedicated issuer
+  // warp instead.
+  static constexpr unsigned MMA_ISSUER = 416;   // warp 13
+  static constexpr unsigned MMA_ISSUER2 = 448;  // warp 14
   __device__ __forceinline__ static unsigned issuer(int l) { return l == 2 ? MMA_ISSUER2 : MMA_ISSUER; }
 
   // Issuer only: layer l's MMAs (K/16 slices, M=64) and their commit.
