@@ -435,8 +435,8 @@ struct TcEngineT {
     tmem_st1h<5>(base + 4, a[4]);
   }
 
-  // Issuers of run_rest (the single-tile-chain path: k_enc_mlp, i.e. the fp32
-  // path's tables and the debug exports): the MMAs of a layer are issued by
+  // Issuers of run_rest (the single-tile-chain path k_enc_mlp<1>, used for the
+  // bf16 debug exports of logits/probabilities/tables): the MMAs of a layer are issued by
   // warp 13 (layer 3's by warp 14) after a CTA barrier.  The production
   // encoder (k_enc_pp) and the decoder (run_rest_ws) use a dedicated issuer
   // warp instead.
