@@ -1,0 +1,25 @@
+"""bench.py contract, CPU side: the reference arm (the oracle, timed on the host)
+prints one JSON line with the same metric/config keys as the GPU arm."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_json_line():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "C1",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference"
+    assert d["metric"] == "encode+decode Mpixel/s (8-bit gray, round trip) and bpp"
+    assert d["unit"] == "Mpixel/s" and d["higher_is_better"] is True and d["value"] > 0
+    for k in ("workload", "images_per_gpu", "width", "height", "tile", "group_rows", "precision"):
+        assert k in d["config"], k
+    assert d["config"]["width"] == 32 and d["config"]["height"] == 32
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["unit"] == "Mpixel/s"
