@@ -665,20 +665,26 @@ __global__ void __launch_bounds__(128) k_rans_enc(Plan p, const uint32_t* __rest
   // Software pipeline: the (f, c) of the next 16 steps of this lane are
   // independent loads (its row read backwards), issued together; the 16
   // dependent encode steps then run from registers.
+  // The next chunk's loads are issued before the current chunk's steps (two
+  // register buffers), so a chunk never starts on an L2 round trip.
   constexpr int CH = 16;
-#pragma unroll 1
-  for (int t0 = t_hi; t0 >= t_lo; t0 -= CH) {
-    uint32_t fcv[CH];
+  auto load_chunk = [&](int t0, uint32_t (&fcv)[CH]) {
 #pragma unroll
     for (int s = 0; s < CH; ++s) {
       const int c = t0 - s - 3 * r;
       const bool act = lane_ok && t0 - s >= t_lo && c >= 0 && c < (int)un.w;
       fcv[s] = act ? __ldg(frow + c) : 0u;  // 0 = inactive (f >= 1 for real pixels)
     }
+  };
+  uint32_t cur[CH], nxt[CH];
+  load_chunk(t_hi, cur);
+#pragma unroll 1
+  for (int t0 = t_hi; t0 >= t_lo; t0 -= CH) {
+    if (t0 - CH >= t_lo) load_chunk(t0 - CH, nxt);
 #pragma unroll
     for (int s = 0; s < CH; ++s) {
-      const bool act = fcv[s] != 0u;
-      const uint32_t f = act ? (fcv[s] & 0xFFFFu) : 1u, cum = fcv[s] >> 16;
+      const bool act = cur[s] != 0u;
+      const uint32_t f = act ? (cur[s] & 0xFFFFu) : 1u, cum = cur[s] >> 16;
       const bool emit = act && (x >> 16) >= f;  // x >= f * 2^16  (renormalise first, R6)
       const uint32_t m = __ballot_sync(0xFFFFFFFFu, emit);
       if (emit) {
@@ -689,6 +695,8 @@ __global__ void __launch_bounds__(128) k_rans_enc(Plan p, const uint32_t* __rest
       n += __popc(m);
       if (act) x = ((x / f) << 16) + (x % f) + cum;
     }
+#pragma unroll
+    for (int s = 0; s < CH; ++s) cur[s] = nxt[s];
   }
   if (lane_ok) {
     region[2 * lane] = (uint16_t)(x >> 16);
