@@ -179,9 +179,10 @@ def measure_variant(dl, model, d_imgs, prec, g, tile, reps=5):
     d_dec = torch.empty_like(d_imgs)
     d_status = torch.zeros(n, dtype=torch.int32, device=d_imgs.device)
     offs = [i * stride for i in range(n)]
+    lens = [int(x) for x in sizes]
     best = 1e30
     for _ in range(reps):
-        dl.dlic_decode_batch_device(model, d_out, offs, hdr, d_dec, d_status)
+        dl.dlic_decode_batch_device(model, d_out, offs, lens, hdr, d_dec, d_status)
         torch.cuda.synchronize()
         best = min(best, dl.dlic_last_kernel_ms("decode"))
     assert int(d_status.abs().sum()) == 0 and torch.equal(d_dec, d_imgs), "variant round trip failed"
@@ -308,7 +309,8 @@ def main():
     sizes = d_sizes.cpu().numpy()
     hdr = dl.dlic_peek(d_out[:int(sizes[0])].cpu().numpy().tobytes())
     offs = [i * stride for i in range(n)]
-    dl.dlic_decode_batch_device(model, d_out, offs, hdr, d_dec, d_status)
+    lens = [int(x) for x in sizes]       # the encoder is deterministic: every step writes these sizes
+    dl.dlic_decode_batch_device(model, d_out, offs, lens, hdr, d_dec, d_status)
     torch.cuda.synchronize()
     assert int(d_status.abs().sum()) == 0 and torch.equal(d_dec, d_imgs), "round trip failed"
     total_bytes = int(sizes.sum())
@@ -320,7 +322,7 @@ def main():
             import torch.distributed as dist
             gathered = [torch.empty_like(d_sizes) for _ in range(ws)]
             dist.all_gather(gathered, d_sizes)      # the only collective: container sizes
-        dl.dlic_decode_batch_device(model, d_out, offs, hdr, d_dec, d_status)
+        dl.dlic_decode_batch_device(model, d_out, offs, lens, hdr, d_dec, d_status)
 
     for _ in range(args.warmup):
         step()

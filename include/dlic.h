@@ -72,8 +72,18 @@ typedef struct {
   uint32_t tile_h;
 } dlic_opts;
 
+/* Container (version 2, little-endian):
+ *   "DLIC", u8 version 2, u8 precision, u8 window id 1 (R1), u8 fill 0 (R2),
+ *   u32 width, u32 height, u16 tile_w, u16 tile_h (0,0 = untiled; Q16),
+ *   u16 G (rows per stream, R7), u16 numerics (arithmetic revision of the
+ *   tables, see dlic_numerics_rev), 32-byte SHA-256 of the model file,
+ *   u32 n_streams, u32 sizes[n_streams] (bytes), then the streams tile-major,
+ *   group-major within a tile.  Each stream: the group's flushed rANS states
+ *   (rows ascending, hi word then lo word) followed by its renormalisation
+ *   words in decoder order (front ascending, row ascending), 16-bit LE words. */
 typedef struct {
   uint32_t width, height, precision, group_rows, tile_w, tile_h, n_streams, n_units;
+  uint32_t numerics; /* arithmetic revision recorded by the encoder */
   uint8_t model_sha256[32];
   uint64_t payload_bytes, header_bytes;
 } dlic_header;
@@ -102,16 +112,25 @@ dlic_status dlic_model_blob_check(const void* bytes, size_t len, uint8_t sha_out
 dlic_status dlic_encode(const dlic_model* m, const uint8_t* img, uint32_t width, uint32_t height,
                         size_t row_stride, const dlic_opts* opts, uint8_t** out, size_t* out_len);
 
-/* decode(bitstream, weights) -> image.  Verifies the model hash BEFORE any
- * pixel work, checks every lane's end state (2^16) and cursor, and writes
- * width*height bytes (row-major, stride = width) to img.
- * Errors: DLIC_E_MODEL_HASH_MISMATCH, DLIC_E_CORRUPT_CONTAINER,
+/* decode(bitstream, weights) -> image.  Verifies the model hash and the
+ * arithmetic revision BEFORE any pixel work, checks every lane's end state
+ * (2^16) and cursor, and writes width*height bytes (row-major, stride =
+ * width) to img.
+ * Errors: DLIC_E_MODEL_HASH_MISMATCH, DLIC_E_VERSION_MISMATCH (container of
+ * another version or numerics revision), DLIC_E_CORRUPT_CONTAINER,
  * DLIC_E_STREAM_UNDERFLOW, DLIC_E_BUFFER_TOO_SMALL. */
 dlic_status dlic_decode(const dlic_model* m, const uint8_t* bits, size_t len, uint8_t* img,
                         size_t img_capacity);
 
-/* Parse a container header (host only, no device work). */
+/* Parse a container header (host only, no device work; any numerics value). */
 dlic_status dlic_peek(const uint8_t* bits, size_t len, dlic_header* out);
+
+/* Arithmetic revision of this build's density estimator + softmax/quantiser
+ * (the integer tables depend on the exact instruction sequence, "as long
+ * as the precision of the floating point arithmetic is the same").  Written
+ * into every container; decode rejects any other value with
+ * DLIC_E_VERSION_MISMATCH.  0 is reserved for the CPU oracle's arithmetic. */
+uint32_t dlic_numerics_rev(void);
 
 /* Upper bound of the container size for (width, height, opts). */
 size_t dlic_max_container_bytes(uint32_t width, uint32_t height, const dlic_opts* opts);
@@ -144,21 +163,56 @@ dlic_status dlic_decode_batch(const dlic_model* m, const uint8_t* bits, size_t l
  * Encode writes container i at d_out + i*dlic_max_container_bytes(...) and its
  * byte size to d_sizes[i] (uint64).  out_capacity must be >= n * max bytes.
  * Asynchronous on cuda_stream except for small internal scratch allocations
- * (stream-ordered).  Errors are reported for the launch; lane-invariant
- * failures of decode are reported through d_status[i] (0 = ok, else a
- * dlic_status) when d_status is non-NULL. */
+ * (stream-ordered).  Errors are reported for the launch; framing and
+ * lane-invariant failures of decode are reported through d_status[i] (0 = ok,
+ * else a dlic_status), which is required. */
 dlic_status dlic_encode_batch_device(const dlic_model* m, const uint8_t* d_imgs, uint32_t n,
                                      uint32_t width, uint32_t height, const dlic_opts* opts,
                                      uint8_t* d_out, size_t out_capacity, uint64_t* d_sizes,
                                      void* cuda_stream);
 /* Decode n containers that all share (width, height, opts) — i.e. produced by
- * dlic_encode_batch_device — located at d_bits + h_offsets[i] (HOST array of
- * byte offsets).  The headers are re-read on the device; h_header is the
- * parsed header of container 0 (dlic_peek on a host copy), used for planning. */
+ * dlic_encode_batch_device — container i at d_bits + h_offsets[i], exactly
+ * h_lengths[i] bytes long (HOST arrays).  The headers are re-read on the
+ * device and every stream size is checked against h_lengths[i] before any
+ * payload byte is read (a truncated or corrupt size table cannot make the
+ * decoder read outside its container); h_header is the parsed header of
+ * container 0 (dlic_peek on a host copy), used for planning.  d_status (n
+ * int32, device) is required: framing errors and lane-invariant failures of
+ * image i land in d_status[i] (callers zero it first).
+ * Errors (returned): DLIC_E_INVALID_ARG (incl. d_status NULL),
+ * DLIC_E_MODEL_HASH_MISMATCH, DLIC_E_VERSION_MISMATCH, DLIC_E_CUDA. */
 dlic_status dlic_decode_batch_device(const dlic_model* m, const uint8_t* d_bits,
-                                     const uint64_t* h_offsets, uint32_t n,
-                                     const dlic_header* h_header, uint8_t* d_imgs,
+                                     const uint64_t* h_offsets, const uint64_t* h_lengths,
+                                     uint32_t n, const dlic_header* h_header, uint8_t* d_imgs,
                                      int32_t* d_status, void* cuda_stream);
+
+/* ---- unit ranges: one image's independent tiles split across GPUs ---------
+ * (north_star: "independent image tiles with their own streams are
+ * partitioned across the GPUs"; units = tiles of Q16 in row-major order,
+ * untiled = one unit).  A rank codes units [unit_lo, unit_hi) of the image;
+ * the only exchange is the per-stream sizes (NCCL all_gather), from which any
+ * rank frames the container with dlic_container_build.
+ *
+ * dlic_unit_streams: the streams [first, first + n) of those units (host only).
+ * dlic_encode_units: host image in (the whole image; only the range's units are
+ *   coded); *payload = library-allocated concatenation of the range's streams
+ *   in container order (dlic_free), stream_sizes (caller array of n_streams of
+ *   dlic_unit_streams) their byte sizes.  Bytes are identical to the
+ *   corresponding streams of dlic_encode's container.
+ * dlic_container_build: host-only framing of a complete container from all
+ *   n_streams sizes and the concatenated payload (*out: dlic_free).
+ * dlic_decode_units: decodes only units [unit_lo, unit_hi) of a container
+ *   into img (width*height bytes); the other pixels of img are left untouched. */
+dlic_status dlic_unit_streams(uint32_t width, uint32_t height, const dlic_opts* opts, uint32_t unit_lo,
+                              uint32_t unit_hi, uint32_t* first_stream, uint32_t* n_streams);
+dlic_status dlic_encode_units(const dlic_model* m, const uint8_t* img, uint32_t width, uint32_t height,
+                              size_t row_stride, const dlic_opts* opts, uint32_t unit_lo, uint32_t unit_hi,
+                              uint8_t** payload, size_t* payload_len, uint32_t* stream_sizes);
+dlic_status dlic_container_build(uint32_t width, uint32_t height, const dlic_opts* opts,
+                                 const uint8_t* model_sha256, const uint32_t* stream_sizes, uint32_t n_streams,
+                                 const uint8_t* payload, size_t payload_len, uint8_t** out, size_t* out_len);
+dlic_status dlic_decode_units(const dlic_model* m, const uint8_t* bits, size_t len, uint32_t unit_lo,
+                              uint32_t unit_hi, uint8_t* img, size_t img_capacity);
 
 /* ---- parity / debug taps ---------------------------------------------------
  * rANS only, fed integer tables (north_star: "the same quantised frequency
@@ -174,8 +228,10 @@ dlic_status dlic_rans_encode_tables(const uint32_t* fc, uint32_t width, uint32_t
  * Writes the image to img (width*height bytes). */
 dlic_status dlic_rans_decode_tables(const uint8_t* bits, size_t len, const uint16_t* freq_tables,
                                     uint8_t* img);
-/* Run the encoder's density-estimator kernels on every pixel of a host image
- * (tile-aware per opts) and export, per pixel in raster order, any of:
+/* Run the encoder's density-estimator kernel on every pixel of a host image
+ * (tile-aware per opts) and export, per pixel in raster order, any of
+ * (bf16: the production kernel k_enc_pp itself, with its debug exports
+ * compiled in; fp32: k_enc_mlp<fp32>):
  * logits[256] (fp32), probs[256] (fp32 softmax as used by the quantiser),
  * freqs[256] (uint16 integer table), fc (f_s | c_s<<16 of the true symbol).
  * NULL outputs are skipped. */

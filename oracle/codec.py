@@ -66,14 +66,16 @@ def all_pixel_tables(layers, precision: int, img: np.ndarray, chunk: int = 65536
 
 def encode_with_tables(fs_img: np.ndarray, cs_img: np.ndarray, width: int, height: int,
                        precision: int, group_rows: int, tile_w: int, tile_h: int,
-                       model_sha: bytes) -> bytes:
+                       model_sha: bytes, numerics: int = container.ORACLE_NUMERICS) -> bytes:
     """Container from given per-pixel (f_s, c_s) of the true symbols — the
-    "oracle fed the same integer tables" leg (north_star)."""
+    "oracle fed the same integer tables" leg (north_star).  `numerics` is the
+    header field naming the arithmetic that produced the tables (the caller's;
+    0 = this oracle's own)."""
     out = []
     for (x0, y0, tw, th) in container.tiles(width, height, tile_w, tile_h):
         sts = streams.encode_unit(fs_img[y0:y0 + th, x0:x0 + tw], cs_img[y0:y0 + th, x0:x0 + tw], group_rows)
         out += [streams.rans.words_to_bytes(s) for s in sts]
-    return container.write(width, height, precision, group_rows, tile_w, tile_h, model_sha, out)
+    return container.write(width, height, precision, group_rows, tile_w, tile_h, model_sha, out, numerics)
 
 
 def encode(img: np.ndarray, model_blob: bytes, precision: int = 0, group_rows: int = 32,
@@ -112,6 +114,8 @@ def decode(blob: bytes, model_blob: bytes) -> np.ndarray:
     hdr = container.parse(blob)
     if hdr["model_sha"] != model_io.digest(model_blob):      # before any pixel work
         raise ModelHashMismatch()
+    if hdr["numerics"] != container.ORACLE_NUMERICS:         # tables of another arithmetic
+        raise container.CorruptContainer("numerics revision %d is not the oracle's" % hdr["numerics"])
     layers = model_io.load(model_blob)
     prec = hdr["precision"]
     out = np.zeros((hdr["height"], hdr["width"]), np.uint8)
@@ -144,6 +148,8 @@ def raster_decode(blob: bytes, model_blob: bytes) -> np.ndarray:
     hdr = container.parse(blob)
     if hdr["group_rows"] != 1:
         raise ValueError("raster decoder needs G = 1")
+    if hdr["numerics"] != container.ORACLE_NUMERICS:
+        raise container.CorruptContainer("numerics revision %d is not the oracle's" % hdr["numerics"])
     layers = model_io.load(model_blob)
     prec = hdr["precision"]
     out = np.zeros((hdr["height"], hdr["width"]), np.uint8)

@@ -1,17 +1,22 @@
 """Container bytes (oracle; test infrastructure only).
 
-The paper states no framing.  Layout, little-endian:
+The paper states no framing.  Layout (SURVEY §8(c) O8 plus the numerics field
+of DESIGN.md "Container", version 2), little-endian:
   off  0  4s  magic "DLIC"
-  off  4  u8  version (1)
+  off  4  u8  version (2)
   off  5  u8  precision path (0 = fp32, 1 = bf16)
   off  6  u8  window id (1 = 9x9 causal, 78 inputs; R1)
   off  7  u8  fill value (0; R2)
   off  8  u32 width        off 12 u32 height
   off 16  u16 tile_w       off 18 u16 tile_h    (0, 0 = untiled)
   off 20  u16 group rows G
-  off 22  32s SHA-256 of the model file
-  off 54  u32 n_streams
-  off 58  u32 sizes[n_streams]  (bytes per stream)
+  off 22  u16 numerics: which arithmetic produced the integer tables (0 = this
+              oracle's own network/softmax; the GPU build writes its revision).
+              P:90: encoder and decoder agree only "as long as the precision
+              of the floating point arithmetic is the same".
+  off 24  32s SHA-256 of the model file
+  off 56  u32 n_streams
+  off 60  u32 sizes[n_streams]  (bytes per stream)
   then the streams, tile-major (tiles row-major), group-major within a tile.
 """
 
@@ -20,9 +25,10 @@ from __future__ import annotations
 import struct
 
 MAGIC = b"DLIC"
-VERSION = 1
+VERSION = 2
 WINDOW_ID = 1
-HEADER_FIXED = 58
+HEADER_FIXED = 60
+ORACLE_NUMERICS = 0
 
 
 class CorruptContainer(Exception):
@@ -40,10 +46,11 @@ def tiles(width: int, height: int, tile_w: int, tile_h: int):
     return out
 
 
-def write(width, height, precision, group_rows, tile_w, tile_h, model_sha, stream_bytes) -> bytes:
+def write(width, height, precision, group_rows, tile_w, tile_h, model_sha, stream_bytes,
+          numerics=ORACLE_NUMERICS) -> bytes:
     assert len(model_sha) == 32
-    hdr = MAGIC + struct.pack("<BBBBIIHHH", VERSION, precision, WINDOW_ID, 0, width, height,
-                              tile_w, tile_h, group_rows)
+    hdr = MAGIC + struct.pack("<BBBBIIHHHH", VERSION, precision, WINDOW_ID, 0, width, height,
+                              tile_w, tile_h, group_rows, numerics)
     hdr += model_sha + struct.pack("<I", len(stream_bytes))
     hdr += b"".join(struct.pack("<I", len(s)) for s in stream_bytes)
     return hdr + b"".join(stream_bytes)
@@ -52,11 +59,11 @@ def write(width, height, precision, group_rows, tile_w, tile_h, model_sha, strea
 def parse(blob: bytes):
     if len(blob) < HEADER_FIXED or blob[:4] != MAGIC:
         raise CorruptContainer("magic")
-    ver, prec, win, fill, w, h, tw, th, g = struct.unpack_from("<BBBBIIHHH", blob, 4)
+    ver, prec, win, fill, w, h, tw, th, g, num = struct.unpack_from("<BBBBIIHHHH", blob, 4)
     if ver != VERSION or win != WINDOW_ID or fill != 0 or prec > 1 or g == 0:
         raise CorruptContainer("header fields")
-    sha = blob[22:54]
-    (n,) = struct.unpack_from("<I", blob, 54)
+    sha = blob[24:56]
+    (n,) = struct.unpack_from("<I", blob, 56)
     if len(blob) < HEADER_FIXED + 4 * n:
         raise CorruptContainer("size table")
     sizes = struct.unpack_from("<%dI" % n, blob, HEADER_FIXED)
@@ -69,5 +76,5 @@ def parse(blob: bytes):
         off += s
     if off != len(blob):
         raise CorruptContainer("trailing bytes")
-    return dict(width=w, height=h, precision=prec, tile_w=tw, tile_h=th, group_rows=g,
+    return dict(width=w, height=h, precision=prec, tile_w=tw, tile_h=th, group_rows=g, numerics=num,
                 model_sha=sha, streams=streams, header_bytes=HEADER_FIXED + 4 * n)

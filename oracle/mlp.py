@@ -18,7 +18,9 @@ Precision variants:
   forward_fp32   numpy float32 matmul (checks fp32 is within 1e-6 of fp64);
   forward_bf16   the bf16 path's plain definition: every matmul operand
                  (inputs, activations, weights) rounded to bf16 (RN-even),
-                 products summed exactly (fp64), bias added in fp64;
+                 products summed exactly (fp64) and rounded once to fp32,
+                 bias added in fp32 (RN), ReLU, and the hidden activation
+                 rounded to bf16 (RN-even) before it enters the next layer;
   logits_path    the value the codec uses: fp64 (precision 0) or bf16-emulated
                  (precision 1) forward, rounded once to float32.
 """

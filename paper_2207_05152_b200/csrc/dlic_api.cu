@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -298,7 +299,11 @@ dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Pl
   if (dec_smem_bytes(d.precision, std::max(p.gpt, (H - (p.nty - 1) * p.th + p.G - 1) / p.G)) > dec_smem_limit())
     return fail(DLIC_E_INVALID_ARG, "too many row groups per unit for the decoder's shared memory: raise group_rows or tile");
   p.cap_words = 2 * p.G + p.G * p.tw;
-  p.hdr_bytes = 58 + 4 * p.spi;
+  p.hdr_bytes = HDR_FIXED + 4 * p.spi;
+  p.u_lo = 0;
+  p.u_cnt = n * p.upi;
+  p.s_lo = 0;
+  p.s_cnt = n * p.spi;
   p.tiles_per_unit = (uint32_t)(((uint64_t)p.tw * p.th + ROWS - 1) / ROWS);
   if ((uint64_t)n * p.upi * p.tiles_per_unit >= (1ull << 32))
     return fail(DLIC_E_INVALID_ARG, "batch too large for one call (>= 2^32 encoder tiles): split it");
@@ -322,11 +327,48 @@ dlic_status check_model_gpu(const dlic_model* m) {
   return check_device(m->device);
 }
 
+// Restrict p to units [lo, hi) of image 0 (unit-range calls).
+dlic_status restrict_units(Plan& p, uint32_t lo, uint32_t hi) {
+  if (p.n_img != 1 || lo >= hi || hi > p.upi) return fail(DLIC_E_INVALID_ARG, "unit range outside [0, n_units)");
+  p.u_lo = lo;
+  p.u_cnt = hi - lo;
+  p.s_lo = unit_info(p, lo).first_stream;
+  p.s_cnt = (hi < p.upi ? unit_info(p, hi).first_stream : p.spi) - p.s_lo;
+  return DLIC_OK;
+}
+
+// The decode launch for p must be schedulable on this device: a cluster of
+// p.nc CTAs with the decoder's shared memory (16-CTA clusters are
+// non-portable; checked once per (precision, nc, smem), on the current device).
+dlic_status check_schedulable(const Plan& p) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, uint32_t, uint32_t, size_t>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const size_t sm = dec_smem_bytes(p.precision, std::max(p.gpt, p.gpl));
+  const auto key = std::make_tuple(dev, p.precision, p.nc, sm);
+  int n;
+  {
+    std::lock_guard<std::mutex> l(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      n = it->second;
+    } else {
+      n = dec_max_active_clusters(p.precision, p.nc, sm);
+      cache[key] = n;
+    }
+  }
+  if (n <= 0)
+    return fail(DLIC_E_INVALID_ARG, "a " + std::to_string(p.nc) +
+                                        "-CTA decode cluster cannot be scheduled on this device: use tiles (narrower units)");
+  return DLIC_OK;
+}
+
 // ---------------------------------------------------------------- header parse
 dlic_status peek(const uint8_t* b, size_t len, dlic_header* h, std::vector<uint32_t>* sizes) {
-  if (!b || len < 58) return fail(DLIC_E_CORRUPT_CONTAINER, "container shorter than its header");
+  if (!b || len < HDR_FIXED) return fail(DLIC_E_CORRUPT_CONTAINER, "container shorter than its header");
   if (memcmp(b, "DLIC", 4) != 0) return fail(DLIC_E_CORRUPT_CONTAINER, "container magic");
-  if (b[4] != 1 || b[6] != 1) return fail(DLIC_E_VERSION_MISMATCH, "container version/window");
+  if (b[4] != CONTAINER_VERSION || b[6] != 1) return fail(DLIC_E_VERSION_MISMATCH, "container version/window");
   if (b[7] != 0 || b[5] > 1) return fail(DLIC_E_CORRUPT_CONTAINER, "container fill/precision");
   dlic_header o = {};
   o.width = rd32(b + 8);
@@ -335,15 +377,16 @@ dlic_status peek(const uint8_t* b, size_t len, dlic_header* h, std::vector<uint3
   o.tile_h = rd16(b + 18);
   o.group_rows = rd16(b + 20);
   o.precision = b[5];
-  memcpy(o.model_sha256, b + 22, 32);
-  o.n_streams = rd32(b + 54);
+  o.numerics = rd16(b + 22);
+  memcpy(o.model_sha256, b + 24, 32);
+  o.n_streams = rd32(b + 56);
   if (o.width == 0 || o.height == 0 || o.group_rows == 0) return fail(DLIC_E_CORRUPT_CONTAINER, "header dims");
-  if ((uint64_t)58 + 4ull * o.n_streams > len) return fail(DLIC_E_CORRUPT_CONTAINER, "size table");
-  o.header_bytes = 58 + 4ull * o.n_streams;
+  if ((uint64_t)HDR_FIXED + 4ull * o.n_streams > len) return fail(DLIC_E_CORRUPT_CONTAINER, "size table");
+  o.header_bytes = HDR_FIXED + 4ull * o.n_streams;
   uint64_t tot = 0;
   if (sizes) sizes->resize(o.n_streams);
   for (uint32_t s = 0; s < o.n_streams; ++s) {
-    const uint32_t z = rd32(b + 58 + 4 * s);
+    const uint32_t z = rd32(b + HDR_FIXED + 4 * s);
     if (z & 1) return fail(DLIC_E_CORRUPT_CONTAINER, "odd stream size");
     tot += z;
     if (sizes) (*sizes)[s] = z;
@@ -381,7 +424,7 @@ cudaError_t h2d(void* dst, const void* src, size_t n, cudaStream_t st) {
 
 // encode pipeline on device buffers (shared by dlic_encode and the batch API)
 dlic_status run_encode(const dlic_model* m, const Plan& p, const uint8_t* d_imgs, uint8_t* d_out, uint64_t stride,
-                       uint64_t* d_sizes, cudaStream_t st, Scratch& sc) {
+                       uint64_t* d_sizes, cudaStream_t st, Scratch& sc, uint32_t** words_out = nullptr) {
   uint32_t* d_fc;
   uint16_t* d_scr;
   uint32_t* d_words;
@@ -399,8 +442,9 @@ dlic_status run_encode(const dlic_model* m, const Plan& p, const uint8_t* d_imgs
   CUDA_TRY(launch_rans_enc(p, d_fc, d_scr, d_words, st));
   ev_end("rans_enc", st);
   ev_begin("compact", st);
-  CUDA_TRY(launch_container(p, m->sha, d_words, d_scr, d_out, stride, d_sizes, d_dst, st));
+  CUDA_TRY(launch_container(p, m->sha, d_words, d_scr, d_out, stride, d_sizes, d_dst, st, words_out != nullptr));
   ev_end("compact", st);
+  if (words_out) *words_out = d_words;
   return DLIC_OK;
 }
 
@@ -521,6 +565,8 @@ dlic_status dlic_encode(const dlic_model* m, const uint8_t* img, uint32_t width,
   Plan p;
   s = make_plan(width, height, 1, opts, p);
   if (s != DLIC_OK) return s;
+  s = check_schedulable(p);  // never write a container this device cannot decode
+  if (s != DLIC_OK) return s;
   cudaStream_t st = my_stream();
   Scratch sc(st);
   uint8_t *d_img, *d_out;
@@ -553,12 +599,16 @@ dlic_status dlic_encode(const dlic_model* m, const uint8_t* img, uint32_t width,
 }
 
 static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_t len, const uint16_t* tables,
-                                 uint8_t* img, size_t cap) {
+                                 uint8_t* img, size_t cap, uint32_t unit_lo = 0, uint32_t unit_hi = 0) {
   dlic_header h;
   dlic_status s = peek(bits, len, &h, nullptr);
   if (s != DLIC_OK) return s;
   if (m && memcmp(h.model_sha256, m->sha, 32) != 0)
     return fail(DLIC_E_MODEL_HASH_MISMATCH, "container was coded with another model");
+  if (m && h.numerics != NUMERICS_REV)
+    return fail(DLIC_E_VERSION_MISMATCH, "container tables come from another arithmetic revision (numerics " +
+                                             std::to_string(h.numerics) + ", this build " +
+                                             std::to_string(NUMERICS_REV) + ")");
   if (!img || cap < (size_t)h.width * h.height) return fail(DLIC_E_BUFFER_TOO_SMALL, "image buffer");
   if (m) {
     s = check_model_gpu(m);
@@ -573,6 +623,15 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
   s = make_plan(h.width, h.height, 1, &o, p);
   if (s != DLIC_OK) return s;
   if (p.spi != h.n_streams) return fail(DLIC_E_CORRUPT_CONTAINER, "stream count does not match the header dims");
+  const bool part = unit_hi > 0;  // dlic_decode_units: only units [unit_lo, unit_hi)
+  if (part) {
+    s = restrict_units(p, unit_lo, unit_hi);
+    if (s != DLIC_OK) return s;
+  }
+  if (!tables) {
+    s = check_schedulable(p);
+    if (s != DLIC_OK) return s;
+  }
   cudaStream_t st = my_stream();
   Scratch sc(st);
   uint8_t *d_bits, *d_img;
@@ -593,7 +652,9 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
   memcpy(pin + 16, bits, len);
   CUDA_TRY(cudaMemcpyAsync(d_meta, pin, 16, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(d_bits, pin + 16, len, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(launch_dec_prep(p, d_bits, d_meta, d_meta + 1, d_sbase, d_slen, d_status, st));
+  CUDA_TRY(launch_dec_prep(p, d_bits, d_meta, d_meta + 1, d_sbase, d_slen, d_status, st, tables == nullptr));
+  if (part)  // pixels outside the unit range come back untouched (pageable copy: no staging reuse)
+    CUDA_TRY(cudaMemcpyAsync(d_img, img, (size_t)h.width * h.height, cudaMemcpyHostToDevice, st));
   if (tables) {
     uint16_t* d_tab;
     const size_t tb = (size_t)h.width * h.height * NOUT * 2;
@@ -752,6 +813,8 @@ dlic_status dlic_encode_batch(const dlic_model* m, const uint8_t* imgs, uint32_t
   Plan p;
   s = make_plan(width, height, n, opts, p);
   if (s != DLIC_OK) return s;
+  s = check_schedulable(p);
+  if (s != DLIC_OK) return s;
   cudaStream_t st = my_stream();
   Scratch sc(st);
   const size_t npx = (size_t)n * width * height;
@@ -809,6 +872,8 @@ dlic_status dlic_decode_batch(const dlic_model* m, const uint8_t* bits, size_t l
     if (s != DLIC_OK) return s;
     if (memcmp(h.model_sha256, m->sha, 32) != 0)
       return fail(DLIC_E_MODEL_HASH_MISMATCH, "container was coded with another model");
+    if (h.numerics != NUMERICS_REV)
+      return fail(DLIC_E_VERSION_MISMATCH, "container tables come from another arithmetic revision");
     if (i == 0) {
       h0 = h;
     } else if (h.width != h0.width || h.height != h0.height || h.precision != h0.precision ||
@@ -823,6 +888,8 @@ dlic_status dlic_decode_batch(const dlic_model* m, const uint8_t* bits, size_t l
   s = make_plan(h0.width, h0.height, n, &o, p);
   if (s != DLIC_OK) return s;
   if (p.spi != h0.n_streams) return fail(DLIC_E_CORRUPT_CONTAINER, "stream count does not match the header dims");
+  s = check_schedulable(p);
+  if (s != DLIC_OK) return s;
   cudaStream_t st = my_stream();
   Scratch sc(st);
   uint8_t *d_bits, *d_imgs;
@@ -872,39 +939,153 @@ dlic_status dlic_encode_batch_device(const dlic_model* m, const uint8_t* d_imgs,
   s = make_plan(width, height, n, opts, p);
   if (s != DLIC_OK) return s;
   if (out_capacity < p.max_container * n) return fail(DLIC_E_BUFFER_TOO_SMALL, "out_capacity < n * max bytes");
+  s = check_schedulable(p);
+  if (s != DLIC_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   Scratch sc(st);
   return run_encode(m, p, d_imgs, d_out, p.max_container, d_sizes, st, sc);
 }
 
 dlic_status dlic_decode_batch_device(const dlic_model* m, const uint8_t* d_bits, const uint64_t* h_offsets,
-                                     uint32_t n, const dlic_header* h_header, uint8_t* d_imgs, int32_t* d_status,
-                                     void* cuda_stream) {
-  if (!d_bits || !h_offsets || !h_header || !d_imgs || n == 0) return fail(DLIC_E_INVALID_ARG, "null pointer");
+                                     const uint64_t* h_lengths, uint32_t n, const dlic_header* h_header,
+                                     uint8_t* d_imgs, int32_t* d_status, void* cuda_stream) {
+  if (!d_bits || !h_offsets || !h_lengths || !h_header || !d_imgs || n == 0)
+    return fail(DLIC_E_INVALID_ARG, "null pointer");
+  if (!d_status) return fail(DLIC_E_INVALID_ARG, "d_status is required: lane-invariant failures are reported there");
   dlic_status s = check_model_gpu(m);
   if (s != DLIC_OK) return s;
   if (memcmp(h_header->model_sha256, m->sha, 32) != 0)
     return fail(DLIC_E_MODEL_HASH_MISMATCH, "container was coded with another model");
+  if (h_header->numerics != NUMERICS_REV)
+    return fail(DLIC_E_VERSION_MISMATCH, "container tables come from another arithmetic revision");
   dlic_opts o = opts_of(*h_header);
   Plan p;
   s = make_plan(h_header->width, h_header->height, n, &o, p);
   if (s != DLIC_OK) return s;
+  s = check_schedulable(p);
+  if (s != DLIC_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   Scratch sc(st);
-  uint64_t* d_off;
+  uint64_t* d_meta;  // [0, n) offsets, [n, 2n) lengths
   uint32_t *d_sbase, *d_slen;
-  int32_t* d_st = d_status;
-  CUDA_TRY(sc.alloc(&d_off, 8ull * n));
+  CUDA_TRY(sc.alloc(&d_meta, 16ull * n));
   CUDA_TRY(sc.alloc(&d_sbase, 4ull * n * p.spi));
   CUDA_TRY(sc.alloc(&d_slen, 4ull * n * p.spi));
-  if (!d_st) CUDA_TRY(sc.alloc(&d_st, 4ull * n));
-  CUDA_TRY(cudaMemcpyAsync(d_off, h_offsets, 8ull * n, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(launch_dec_prep(p, d_bits, d_off, nullptr, d_sbase, d_slen, d_st, st));
+  CUDA_TRY(cudaMemcpyAsync(d_meta, h_offsets, 8ull * n, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_meta + n, h_lengths, 8ull * n, cudaMemcpyHostToDevice, st));
+  // k_dec_prep checks every header and stream size against its container's
+  // length before k_decode reads a byte of payload (failures -> d_status[i])
+  CUDA_TRY(launch_dec_prep(p, d_bits, d_meta, d_meta + n, d_sbase, d_slen, d_status, st));
   ev_begin("decode", st);
-  CUDA_TRY(launch_decode(p, m->dw(), d_bits, d_off, d_sbase, d_slen, d_imgs, d_st, st));
+  CUDA_TRY(launch_decode(p, m->dw(), d_bits, d_meta, d_sbase, d_slen, d_imgs, d_status, st));
   ev_end("decode", st);
   return DLIC_OK;
 }
+
+// ---- unit ranges (multi-GPU sharding of one image's independent tiles)
+dlic_status dlic_unit_streams(uint32_t width, uint32_t height, const dlic_opts* opts, uint32_t unit_lo,
+                              uint32_t unit_hi, uint32_t* first_stream, uint32_t* n_streams) {
+  if (!first_stream || !n_streams) return fail(DLIC_E_INVALID_ARG, "null pointer");
+  Plan p;
+  dlic_status s = make_plan(width, height, 1, opts, p);
+  if (s != DLIC_OK) return s;
+  s = restrict_units(p, unit_lo, unit_hi);
+  if (s != DLIC_OK) return s;
+  *first_stream = p.s_lo;
+  *n_streams = p.s_cnt;
+  return DLIC_OK;
+}
+
+dlic_status dlic_encode_units(const dlic_model* m, const uint8_t* img, uint32_t width, uint32_t height,
+                              size_t row_stride, const dlic_opts* opts, uint32_t unit_lo, uint32_t unit_hi,
+                              uint8_t** payload, size_t* payload_len, uint32_t* stream_sizes) {
+  if (!img || !payload || !payload_len || !stream_sizes) return fail(DLIC_E_INVALID_ARG, "null pointer");
+  if (row_stride == 0) row_stride = width;
+  if (row_stride < width) return fail(DLIC_E_SHAPE_MISMATCH, "row_stride < width");
+  dlic_status s = check_model_gpu(m);
+  if (s != DLIC_OK) return s;
+  Plan p;
+  s = make_plan(width, height, 1, opts, p);
+  if (s != DLIC_OK) return s;
+  s = restrict_units(p, unit_lo, unit_hi);
+  if (s != DLIC_OK) return s;
+  s = check_schedulable(p);
+  if (s != DLIC_OK) return s;
+  cudaStream_t st = my_stream();
+  Scratch sc(st);
+  uint8_t *d_img, *d_out;
+  uint64_t* d_size;
+  uint32_t* d_words = nullptr;
+  CUDA_TRY(sc.alloc(&d_img, (size_t)width * height));
+  CUDA_TRY(sc.alloc(&d_out, p.max_container));
+  CUDA_TRY(sc.alloc(&d_size, 8));
+  CUDA_TRY(cudaMemcpy2DAsync(d_img, width, img, row_stride, width, height, cudaMemcpyHostToDevice, st));
+  s = run_encode(m, p, d_img, d_out, p.max_container, d_size, st, sc, &d_words);
+  if (s != DLIC_OK) return s;
+  uint64_t n = 0;
+  std::vector<uint32_t> words(p.s_cnt);
+  CUDA_TRY(cudaMemcpyAsync(&n, d_size, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(words.data(), d_words + p.s_lo, 4ull * p.s_cnt, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (n > p.max_container) return fail(DLIC_E_CUDA, "payload size out of range");
+  uint8_t* res = static_cast<uint8_t*>(malloc(n ? n : 1));
+  if (!res) return fail(DLIC_E_OUT_OF_MEMORY, "malloc");
+  CUDA_TRY(cudaMemcpyAsync(res, d_out, n, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (uint32_t i = 0; i < p.s_cnt; ++i) stream_sizes[i] = 2u * words[i];
+  *payload = res;
+  *payload_len = n;
+  return DLIC_OK;
+}
+
+dlic_status dlic_container_build(uint32_t width, uint32_t height, const dlic_opts* opts, const uint8_t* model_sha256,
+                                 const uint32_t* stream_sizes, uint32_t n_streams, const uint8_t* payload,
+                                 size_t payload_len, uint8_t** out, size_t* out_len) {
+  if (!stream_sizes || !model_sha256 || !out || !out_len || (!payload && payload_len))
+    return fail(DLIC_E_INVALID_ARG, "null pointer");
+  Plan p;
+  dlic_status s = make_plan(width, height, 1, opts, p);
+  if (s != DLIC_OK) return s;
+  if (n_streams != p.spi) return fail(DLIC_E_SHAPE_MISMATCH, "stream count does not match (width, height, opts)");
+  uint64_t tot = 0;
+  for (uint32_t i = 0; i < n_streams; ++i) {
+    if (stream_sizes[i] & 1u) return fail(DLIC_E_CORRUPT_CONTAINER, "odd stream size");
+    tot += stream_sizes[i];
+  }
+  if (tot != payload_len) return fail(DLIC_E_SHAPE_MISMATCH, "payload length != sum of stream sizes");
+  const size_t n = p.hdr_bytes + payload_len;
+  uint8_t* o = static_cast<uint8_t*>(malloc(n));
+  if (!o) return fail(DLIC_E_OUT_OF_MEMORY, "malloc");
+  auto w16 = [&](size_t at, uint32_t v) { o[at] = (uint8_t)v; o[at + 1] = (uint8_t)(v >> 8); };
+  auto w32 = [&](size_t at, uint32_t v) { for (int i = 0; i < 4; ++i) o[at + i] = (uint8_t)(v >> (8 * i)); };
+  memcpy(o, "DLIC", 4);
+  o[4] = (uint8_t)CONTAINER_VERSION;
+  o[5] = (uint8_t)p.precision;
+  o[6] = 1;
+  o[7] = 0;
+  w32(8, width);
+  w32(12, height);
+  w16(16, p.hdr_tw);
+  w16(18, p.hdr_th);
+  w16(20, p.G);
+  w16(22, NUMERICS_REV);
+  memcpy(o + 24, model_sha256, 32);
+  w32(56, p.spi);
+  for (uint32_t i = 0; i < n_streams; ++i) w32(HDR_FIXED + 4 * (size_t)i, stream_sizes[i]);
+  if (payload_len) memcpy(o + p.hdr_bytes, payload, payload_len);
+  *out = o;
+  *out_len = n;
+  return DLIC_OK;
+}
+
+dlic_status dlic_decode_units(const dlic_model* m, const uint8_t* bits, size_t len, uint32_t unit_lo,
+                              uint32_t unit_hi, uint8_t* img, size_t img_capacity) {
+  if (!m) return fail(DLIC_E_INVALID_ARG, "null model");
+  if (unit_hi <= unit_lo) return fail(DLIC_E_INVALID_ARG, "empty unit range");
+  return decode_common(m, bits, len, nullptr, img, img_capacity, unit_lo, unit_hi);
+}
+
+uint32_t dlic_numerics_rev(void) { return NUMERICS_REV; }
 
 dlic_status dlic_info(char* buf, size_t cap) {
   int dev = 0, n = 0;

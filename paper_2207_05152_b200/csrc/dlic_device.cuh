@@ -44,6 +44,16 @@ constexpr float Q1_SCALE = 65279.0f;  // 2^16 - 257 (R5, Q1')
 #ifndef DLIC_POLY_FROM
 #define DLIC_POLY_FROM 6
 #endif
+// Arithmetic revision of the density estimator + softmax/Q1' (container
+// header field "numerics"): the integer tables are a function of the exact
+// instruction sequence (engine K order, layer-1 split, epilogue rounding, the
+// MUFU/polynomial exp split), so a container decodes only with a build of the
+// same revision.  Bump NUMERICS_BASE on any change that can alter a table bit;
+// the exp split is folded in so that a -DDLIC_POLY_FROM variant build can never
+// decode another build's containers.  Value 0 is reserved for the oracle's own
+// arithmetic (fp64 / bf16-emulated network, fp64 softmax).
+constexpr uint32_t NUMERICS_BASE = 1;
+constexpr uint32_t NUMERICS_REV = (NUMERICS_BASE << 8) | (uint32_t)DLIC_POLY_FROM;
 
 // Layer-1 K order of the bf16 engine.  K position p = 10u + i belongs to
 // thread u = 2j + h (column group j, half h), which feeds A packed columns

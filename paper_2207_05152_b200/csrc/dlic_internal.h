@@ -15,13 +15,19 @@ struct Plan {
   uint32_t gpt, gpl;   // groups per full-height tile / per last-row tile
   uint32_t spi;        // streams per image
   uint32_t cap_words;  // scratch words per stream (2G + G*tw)
-  uint32_t hdr_bytes;  // 58 + 4*spi
+  uint32_t hdr_bytes;  // HDR_FIXED + 4*spi
   uint32_t precision;
-  uint32_t tiles_per_unit;  // ceil(tw*th / 128) 128-pixel MLP tiles
-  uint32_t nc;              // CTAs per decode cluster (slots = 128*nc >= ceil(tw/3))
+  uint32_t tiles_per_unit;  // ceil(tw*th / 64) 64-pixel MLP tiles
+  uint32_t nc;              // CTAs per decode cluster (slots = 64*nc >= ceil(tw/3))
   uint32_t hdr_tw, hdr_th;  // tile fields as written in the header (0,0 = untiled)
   uint64_t max_container;   // hdr_bytes + per-stream worst case
+  // unit range of this launch: units [u_lo, u_lo + u_cnt) of the batch, i.e.
+  // streams [s_lo, s_lo + s_cnt) (the whole batch unless a *_units call)
+  uint32_t u_lo, u_cnt, s_lo, s_cnt;
 };
+
+constexpr uint32_t HDR_FIXED = 60;  // container header bytes before the size table (version 2)
+constexpr uint32_t CONTAINER_VERSION = 2;
 
 struct Unit {
   uint32_t img, x0, y0, w, h, first_stream, ngroups;
@@ -78,10 +84,10 @@ cudaError_t launch_rans_enc(const Plan& p, const uint32_t* d_fc, uint16_t* d_scr
                             cudaStream_t st);
 cudaError_t launch_container(const Plan& p, const uint8_t* model_sha, const uint32_t* d_words,
                              const uint16_t* d_scratch, uint8_t* d_out, uint64_t out_stride,
-                             uint64_t* d_sizes, uint64_t* d_stream_dst, cudaStream_t st);
+                             uint64_t* d_sizes, uint64_t* d_stream_dst, cudaStream_t st, bool payload_only = false);
 cudaError_t launch_dec_prep(const Plan& p, const uint8_t* d_bits, const uint64_t* d_cont_off,
                             const uint64_t* d_cont_len, uint32_t* d_sbase, uint32_t* d_slen,
-                            int32_t* d_status, cudaStream_t st);
+                            int32_t* d_status, cudaStream_t st, bool check_numerics = true);
 cudaError_t launch_decode(const Plan& p, const DevWeights& w, const uint8_t* d_bits, const uint64_t* d_cont_off,
                           const uint32_t* d_sbase, const uint32_t* d_slen, uint8_t* d_imgs, int32_t* d_status,
                           cudaStream_t st, unsigned long long* prof = nullptr);
@@ -90,6 +96,9 @@ cudaError_t launch_rans_dec_tables(const Plan& p, const uint8_t* d_bits, const u
                                    const uint32_t* d_slen, const uint16_t* d_tables, uint8_t* d_out,
                                    int32_t* d_status, cudaStream_t st);
 
+// how many decode clusters of nc CTAs (dynamic smem `smem`) the device can
+// co-schedule (cudaOccupancyMaxActiveClusters); 0 = the launch cannot run
+int dec_max_active_clusters(uint32_t precision, uint32_t nc, size_t smem);
 size_t dec_smem_bytes(uint32_t precision, uint32_t max_groups);
 size_t dec_smem_limit();
 size_t enc_smem_bytes(uint32_t precision);

@@ -175,7 +175,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int row = tile_row();
   typename EngineSel<PREC>::T eng;
   engine_setup<PREC>(eng, smem, w, bar, &tslot);
-  const uint64_t total = (uint64_t)p.n_img * p.upi * p.tiles_per_unit;
+  // tiles of units [u_lo, u_lo + u_cnt) (global tile index = tbase + k)
+  const uint64_t tbase = (uint64_t)p.u_lo * p.tiles_per_unit;
+  const uint64_t total = (uint64_t)p.u_cnt * p.tiles_per_unit;
   const bool dbg = dbg_logits || dbg_probs || dbg_freqs;
 
   // this thread's pixel of a tile (64 consecutive pixels of a unit in raster
@@ -233,7 +235,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   if (dbg) {  // debug exports: one tile at a time
 #pragma unroll 1
-    for (uint64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    for (uint64_t tile = tbase + blockIdx.x; tile < tbase + total; tile += gridDim.x) {
       Px x = pixel(tile);
       load_sym(x);
       auto get = getter(x);
@@ -274,8 +276,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // each CTA takes a contiguous range of tiles: consecutive 64-pixel tiles
   // share most of their 9-row windows, which then hit L1
   const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
-  const uint64_t tend = min(total, per * (blockIdx.x + 1));
-  uint64_t tile = per * blockIdx.x;
+  const uint64_t tend = tbase + min(total, per * (blockIdx.x + 1));
+  uint64_t tile = tbase + per * blockIdx.x;
   if (tile < tend) {
     Px cur = pixel(tile);
     {
@@ -359,9 +361,15 @@ using EngB = TcEngineT<320, 448, 448, true>;
 
 size_t enc_pp_smem_bytes() { return WIMG_BYTES + BIAS_BYTES + ENC_PP_XS_BYTES; }
 
+// DBG: parity tap of this production kernel -- per pixel (image raster order)
+// the biased logits, the probabilities the quantiser used and the integer
+// table, written from inside the same instruction sequence (R8), so tests can
+// compare the production encoder itself with the oracle.
+template <bool DBG>
 __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
     k_enc_pp(Plan p, DevWeights w, const uint8_t* __restrict__ imgs, uint32_t* __restrict__ fc,
-             unsigned long long* __restrict__ prof) {
+             unsigned long long* __restrict__ prof, float* __restrict__ dbg_logits, float* __restrict__ dbg_probs,
+             uint16_t* __restrict__ dbg_freqs) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bars[2];  // mma[0], mma[1] (tcgen05.commit)
   __shared__ uint32_t tslot;
@@ -388,10 +396,12 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
   ea.xs = xsb;
   eb.xs = xsb + NXS_SMEM * NGRP * ROWS;
 
-  const uint64_t total = (uint64_t)p.n_img * p.upi * p.tiles_per_unit;
+  // tiles of units [u_lo, u_lo + u_cnt), contiguous ranges per CTA
+  const uint64_t tbase = (uint64_t)p.u_lo * p.tiles_per_unit;
+  const uint64_t total = (uint64_t)p.u_cnt * p.tiles_per_unit;
   const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
-  const uint64_t t0 = per * blockIdx.x;
-  const uint64_t tend = min(total, per * (blockIdx.x + 1));
+  const uint64_t t0 = tbase + per * blockIdx.x;
+  const uint64_t tend = tbase + min(total, per * (blockIdx.x + 1));
   const uint32_t ntl = t0 < tend ? (uint32_t)(tend - t0) : 0u;  // tiles of this CTA
   const uint32_t npairs = (ntl + 1) / 2;
 
@@ -431,6 +441,7 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
     int fr = 0, fcol = 0;
     const uint8_t* fimg = imgs;
     uint64_t ffc = 0;
+    uint64_t fgi = 0;  // DBG: image-raster index of the unit's pixel (0, 0)
     auto set_unit = [&](uint32_t u) {
       const Unit un = unit_info(p, u);
       fu = u;
@@ -441,6 +452,7 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
       fcol = row - fr * (int)un.w;
       fimg = imgs + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
       ffc = un.fc_off;
+      fgi = (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
     };
     if (t0 < tend) {
       const uint32_t u0 = (uint32_t)(t0 / p.tiles_per_unit);
@@ -472,6 +484,7 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
     struct Px {
       uint64_t fci;
       int sym;
+      uint64_t gi;  // DBG only
     };
     // the cursor's tile -> layer-1 input of a slot; fresh taps, symbol.
     // Thread u = 2j + h reads window row dr = u - 8 (taps dc = -6..2) and,
@@ -511,6 +524,7 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
       Px o;
       o.fci = ffc + q;
       o.sym = valid ? (int)__ldg(tp) : -1;
+      o.gi = fgi + (uint64_t)fr * p.W + (uint64_t)fcol;
       if (live) advance();
       return o;
     };
@@ -543,11 +557,19 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
     auto finish = [&](auto& eng, uint32_t (&v)[32], const Px& x) {
       Q1Work<true> qw;
       qw.s1a(eng, v);
+      const int c0 = 64 * col_grp() + 32 * half_id();
+      if constexpr (DBG) {  // biased logits of this thread's 32 columns
+        if (dbg_logits && x.sym >= 0)
+          for (int i = 0; i < 32; ++i) dbg_logits[x.gi * NOUT + c0 + i] = __uint_as_float(v[i]);
+      }
       qw.template s1b<0, 16>(v);
       qw.s1c();
       qw.x1(eng);
-      qw.sA(eng, v, x.sym, nullptr);
+      qw.sA(eng, v, x.sym, DBG && dbg_probs && x.sym >= 0 ? dbg_probs + x.gi * NOUT : nullptr);
       qw.x2(eng);
+      if constexpr (DBG) {
+        if (dbg_freqs && x.sym >= 0) q1_store_freqs(v, qw.r, dbg_freqs + x.gi * NOUT);
+      }
       write_fc(x, qw);
     };
     if (npairs > 0) {
@@ -644,10 +666,9 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
 // already in decoder order (t asc, r asc).
 __global__ void __launch_bounds__(128) k_rans_enc(Plan p, const uint32_t* __restrict__ fc,
                                                   uint16_t* __restrict__ scratch, uint32_t* __restrict__ words) {
-  const uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t s = p.s_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t nstreams = p.n_img * p.spi;
-  if (s >= nstreams) return;  // warp-uniform
+  if (s >= p.s_lo + p.s_cnt) return;  // warp-uniform
   uint32_t u, g;
   stream_info(p, s, u, g);
   const Unit un = unit_info(p, u);
@@ -721,16 +742,31 @@ __device__ __forceinline__ void put_u32(uint8_t* o, uint32_t v) {
   o[3] = (uint8_t)(v >> 24);
 }
 
+// Header (version 2) + the prefix sum of the stream
+// sizes = each stream's byte offset.  payload_only (unit-range calls): no
+// header, offsets relative to the payload start, streams [s_lo, s_lo + s_cnt).
 __global__ void k_container(Plan p, Sha sha, const uint32_t* __restrict__ words, uint8_t* __restrict__ out,
-                            uint64_t stride, uint64_t* __restrict__ sizes, uint64_t* __restrict__ dst) {
+                            uint64_t stride, uint64_t* __restrict__ sizes, uint64_t* __restrict__ dst,
+                            int payload_only) {
   const uint32_t img = blockIdx.x;
   uint8_t* o = out + (uint64_t)img * stride;
+  if (payload_only) {
+    if (threadIdx.x == 0) {
+      uint64_t off = 0;
+      for (uint32_t s = p.s_lo; s < p.s_lo + p.s_cnt; ++s) {
+        dst[s] = off;
+        off += 2ull * words[s];
+      }
+      sizes[0] = off;
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     o[0] = 'D';
     o[1] = 'L';
     o[2] = 'I';
     o[3] = 'C';
-    o[4] = 1;  // version
+    o[4] = (uint8_t)CONTAINER_VERSION;
     o[5] = (uint8_t)p.precision;
     o[6] = 1;  // window id (R1)
     o[7] = 0;  // fill (R2)
@@ -739,12 +775,13 @@ __global__ void k_container(Plan p, Sha sha, const uint32_t* __restrict__ words,
     put_u16(o + 16, p.hdr_tw);
     put_u16(o + 18, p.hdr_th);
     put_u16(o + 20, p.G);
-    for (int i = 0; i < 32; ++i) o[22 + i] = sha.b[i];
-    put_u32(o + 54, p.spi);
+    put_u16(o + 22, NUMERICS_REV);  // arithmetic revision of the tables (decode must match)
+    for (int i = 0; i < 32; ++i) o[24 + i] = sha.b[i];
+    put_u32(o + 56, p.spi);
     uint64_t off = p.hdr_bytes;
     for (uint32_t s = 0; s < p.spi; ++s) {
       const uint32_t sz = 2u * words[(uint64_t)img * p.spi + s];
-      put_u32(o + 58 + 4 * s, sz);
+      put_u32(o + HDR_FIXED + 4 * s, sz);
       dst[(uint64_t)img * p.spi + s] = off;
       off += sz;
     }
@@ -756,7 +793,7 @@ __global__ void __launch_bounds__(128) k_copy(Plan p, const uint32_t* __restrict
                                               const uint16_t* __restrict__ scratch,
                                               const uint64_t* __restrict__ dst, uint8_t* __restrict__ out,
                                               uint64_t stride) {
-  const uint32_t s = blockIdx.x;
+  const uint32_t s = p.s_lo + blockIdx.x;
   uint32_t u, g;
   stream_info(p, s, u, g);
   const Unit un = unit_info(p, u);
@@ -850,21 +887,21 @@ __device__ __forceinline__ uint32_t get_u16(const uint8_t* b) { return (uint32_t
 
 __global__ void k_dec_prep(Plan p, const uint8_t* __restrict__ bits, const uint64_t* __restrict__ cont_off,
                            const uint64_t* __restrict__ cont_len, uint32_t* __restrict__ sbase,
-                           uint32_t* __restrict__ slen, int32_t* __restrict__ status) {
+                           uint32_t* __restrict__ slen, int32_t* __restrict__ status, int check_numerics) {
   const uint32_t img = blockIdx.x * blockDim.x + threadIdx.x;
   if (img >= p.n_img) return;
   const uint8_t* b = bits + cont_off[img];
-  const uint64_t len = cont_len ? cont_len[img] : ~0ull;
+  const uint64_t len = cont_len[img];  // required: every read below stays inside [b, b + len)
   int err = 0;
-  if (b[0] != 'D' || b[1] != 'L' || b[2] != 'I' || b[3] != 'C') err = 6;
-  else if (b[4] != 1 || b[6] != 1 || b[7] != 0) err = 5;
+  if (len < HDR_FIXED || b[0] != 'D' || b[1] != 'L' || b[2] != 'I' || b[3] != 'C') err = 6;
+  else if (b[4] != CONTAINER_VERSION || b[6] != 1 || b[7] != 0 || (check_numerics && get_u16(b + 22) != NUMERICS_REV)) err = 5;
   else if (get_u32(b + 8) != p.W || get_u32(b + 12) != p.H || get_u16(b + 16) != p.hdr_tw ||
            get_u16(b + 18) != p.hdr_th || get_u16(b + 20) != p.G || b[5] != p.precision ||
-           get_u32(b + 54) != p.spi)
+           get_u32(b + 56) != p.spi || p.hdr_bytes > len)
     err = 2;
   uint64_t off = p.hdr_bytes;
   for (uint32_t s = 0; s < p.spi; ++s) {
-    uint32_t sz = err ? 0u : get_u32(b + 58 + 4 * s);
+    uint32_t sz = err ? 0u : get_u32(b + HDR_FIXED + 4 * s);
     if ((sz & 1u) || off + sz > len) {
       err = 6;
       sz = 0;
@@ -873,7 +910,7 @@ __global__ void k_dec_prep(Plan p, const uint8_t* __restrict__ bits, const uint6
     slen[(uint64_t)img * p.spi + s] = err ? 0u : sz / 2;
     off += sz;
   }
-  if (cont_len && off != len && !err) err = 6;
+  if (off != len && !err) err = 6;
   status[img] = err;
 }
 
@@ -919,7 +956,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
   Prof pf;
   pf.on = PROF && threadIdx.x == 32;  // a row thread
   const uint32_t rank = NC > 1 ? cluster_rank() : 0u;
-  const uint32_t u = blockIdx.x / NC;
+  const uint32_t u = p.u_lo + blockIdx.x / NC;
   const Unit un = unit_info(p, u);
 
   typename EngineSel<PREC>::T eng;
@@ -1410,18 +1447,25 @@ static cudaError_t set_smem(K kern, size_t bytes) {
 cudaError_t launch_enc_mlp(const Plan& p, const DevWeights& w, const uint8_t* d_imgs, uint32_t* d_fc,
                            float* dbg_logits, float* dbg_probs, uint16_t* dbg_freqs, cudaStream_t st,
                            int num_sms) {
-  const uint64_t total = (uint64_t)p.n_img * p.upi * p.tiles_per_unit;
+  const uint64_t total = (uint64_t)p.u_cnt * p.tiles_per_unit;
   const uint32_t grid = (uint32_t)(total < (uint64_t)num_sms ? total : (uint64_t)num_sms);
   const size_t sm = enc_smem_bytes(p.precision);
-  if (p.precision == 1 && !dbg_logits && !dbg_probs && !dbg_freqs) {
+  if (p.precision == 1 && (dbg_logits || dbg_probs || dbg_freqs)) {
+    // parity tap: the production kernel with its debug exports
     const size_t sp = enc_pp_smem_bytes();
-    cudaError_t e = set_smem(k_enc_pp, sp);
+    cudaError_t e = set_smem(k_enc_pp<true>, sp);
+    if (e != cudaSuccess) return e;
+    k_enc_pp<true><<<grid, ENC_PP_THREADS, sp, st>>>(p, w, d_imgs, d_fc, nullptr, dbg_logits, dbg_probs, dbg_freqs);
+  } else if (p.precision == 1) {
+    const size_t sp = enc_pp_smem_bytes();
+    cudaError_t e = set_smem(k_enc_pp<false>, sp);
     if (e != cudaSuccess) return e;
     static unsigned long long* d_prof = nullptr;
     const bool prof = getenv("DLIC_PROF_ENC") != nullptr;
     if (prof && !d_prof) cudaMalloc(&d_prof, 16 * 8);
     if (prof) cudaMemsetAsync(d_prof, 0, 16 * 8, st);
-    k_enc_pp<<<grid, ENC_PP_THREADS, sp, st>>>(p, w, d_imgs, d_fc, prof ? d_prof : nullptr);
+    k_enc_pp<false><<<grid, ENC_PP_THREADS, sp, st>>>(p, w, d_imgs, d_fc, prof ? d_prof : nullptr, nullptr, nullptr,
+                                                     nullptr);
     if (prof) {
       unsigned long long h[16];
       cudaMemcpyAsync(h, d_prof, 16 * 8, cudaMemcpyDeviceToHost, st);
@@ -1433,10 +1477,6 @@ cudaError_t launch_enc_mlp(const Plan& p, const DevWeights& w, const uint8_t* d_
               h[2] / np, h[3] / np, h[4] / np, h[5] / np, h[6] / np, h[7] / np, h[11] / np, h[12] / np, h[9] / np,
               h[8] / np);
     }
-  } else if (p.precision == 1) {
-    cudaError_t e = set_smem(k_enc_mlp<1>, sm);
-    if (e != cudaSuccess) return e;
-    k_enc_mlp<1><<<grid, NTHREADS, sm, st>>>(p, w, d_imgs, d_fc, dbg_logits, dbg_probs, dbg_freqs);
   } else {
     cudaError_t e = set_smem(k_enc_mlp<0>, sm);
     if (e != cudaSuccess) return e;
@@ -1447,25 +1487,27 @@ cudaError_t launch_enc_mlp(const Plan& p, const DevWeights& w, const uint8_t* d_
 
 cudaError_t launch_rans_enc(const Plan& p, const uint32_t* d_fc, uint16_t* d_scratch, uint32_t* d_words,
                             cudaStream_t st) {
-  const uint32_t ns = p.n_img * p.spi;
-  k_rans_enc<<<(ns + 3) / 4, 128, 0, st>>>(p, d_fc, d_scratch, d_words);
+  if (p.s_cnt == 0) return cudaSuccess;
+  k_rans_enc<<<(p.s_cnt + 3) / 4, 128, 0, st>>>(p, d_fc, d_scratch, d_words);
   return cudaGetLastError();
 }
 
 cudaError_t launch_container(const Plan& p, const uint8_t* model_sha, const uint32_t* d_words,
                              const uint16_t* d_scratch, uint8_t* d_out, uint64_t out_stride, uint64_t* d_sizes,
-                             uint64_t* d_stream_dst, cudaStream_t st) {
+                             uint64_t* d_stream_dst, cudaStream_t st, bool payload_only) {
   Sha sha;
   for (int i = 0; i < 32; ++i) sha.b[i] = model_sha ? model_sha[i] : 0;
-  k_container<<<p.n_img, 32, 0, st>>>(p, sha, d_words, d_out, out_stride, d_sizes, d_stream_dst);
-  k_copy<<<p.n_img * p.spi, 128, 0, st>>>(p, d_words, d_scratch, d_stream_dst, d_out, out_stride);
+  k_container<<<payload_only ? 1u : p.n_img, 32, 0, st>>>(p, sha, d_words, d_out, out_stride, d_sizes,
+                                                           d_stream_dst, payload_only ? 1 : 0);
+  if (p.s_cnt > 0) k_copy<<<p.s_cnt, 128, 0, st>>>(p, d_words, d_scratch, d_stream_dst, d_out, out_stride);
   return cudaGetLastError();
 }
 
 cudaError_t launch_dec_prep(const Plan& p, const uint8_t* d_bits, const uint64_t* d_cont_off,
                             const uint64_t* d_cont_len, uint32_t* d_sbase, uint32_t* d_slen, int32_t* d_status,
-                            cudaStream_t st) {
-  k_dec_prep<<<(p.n_img + 63) / 64, 64, 0, st>>>(p, d_bits, d_cont_off, d_cont_len, d_sbase, d_slen, d_status);
+                            cudaStream_t st, bool check_numerics) {
+  k_dec_prep<<<(p.n_img + 63) / 64, 64, 0, st>>>(p, d_bits, d_cont_off, d_cont_len, d_sbase, d_slen, d_status,
+                                                 check_numerics ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -1478,7 +1520,7 @@ static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uin
   cudaError_t e = set_smem(k_decode<PREC, PROF>, sm);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.n_img * p.upi * p.nc);
+  cfg.gridDim = dim3(p.u_cnt * p.nc);
   cfg.blockDim = dim3(dec_block(PREC));
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
@@ -1495,6 +1537,35 @@ static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uin
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k_decode<PREC, PROF>, p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status,
                             prof);
+}
+
+template <int PREC>
+static int max_clusters_t(uint32_t nc, size_t sm) {
+  if (set_smem(k_decode<PREC, false>, sm) != cudaSuccess) return 0;
+  if (nc > 8 && cudaFuncSetAttribute(k_decode<PREC, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                    cudaSuccess)
+    return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nc);
+  cfg.blockDim = dim3(dec_block(PREC));
+  cfg.dynamicSmemBytes = sm;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = nc;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_decode<PREC, false>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int dec_max_active_clusters(uint32_t precision, uint32_t nc, size_t smem) {
+  return precision == 1 ? max_clusters_t<1>(nc, smem) : max_clusters_t<0>(nc, smem);
 }
 
 cudaError_t launch_decode(const Plan& p, const DevWeights& w, const uint8_t* d_bits, const uint64_t* d_cont_off,

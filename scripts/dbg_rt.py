@@ -13,7 +13,7 @@ for (h, w, g) in [(1, 1, 32), (1, 2, 32), (1, 13, 32), (2, 1, 32), (5, 8, 1)]:
         bits = dl.dlic_encode(m, img, precision=prec, group_rows=g)
         fc = dl.dlic_debug_mlp(m, img, precision=prec, group_rows=g, logits=False, probs=False, freqs=False)["fc"]
         ob = codec.encode_with_tables((fc & 0xFFFF).astype(np.int64), (fc >> 16).astype(np.int64), w, h, prec, g,
-                                      0, 0, model_io.digest(blob))
+                                      0, 0, model_io.digest(blob), dl.dlic_numerics_rev())
         try:
             d = dl.dlic_decode(m, bits)
             res = "ok" if np.array_equal(d, img) else "MISMATCH %s vs %s" % (d.ravel()[:8], img.ravel()[:8])

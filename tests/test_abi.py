@@ -27,7 +27,7 @@ def test_exports_every_declared_symbol(dl):
     names = set(re.findall(r"\b(dlic_[a-z0-9_]+)\s*\(", hdr))
     assert len(names) >= 20
     for n in sorted(names):
-        assert hasattr(dl._lib, n), n
+        assert hasattr(dl._L(), n), n
 
 
 def test_model_blob_hash_agrees_with_hashlib(dl, trained_blob):
@@ -63,7 +63,7 @@ def test_invalid_options_rejected(dl):
     assert dl.dlic_max_container_bytes(100, 100, 1, 3) == 0          # G must divide 32
     assert dl.dlic_max_container_bytes(4000, 10, 1, 32) == 0         # untiled width > 3072
     assert dl.dlic_max_container_bytes(4000, 10, 1, 32, (768, 720)) > 0
-    assert dl._lib.dlic_status_str(7) == b"model hash mismatch"
+    assert dl._L().dlic_status_str(7) == b"model hash mismatch"
 
 
 def test_no_cpu_fallback_without_gpu(dl, trained_blob):
@@ -78,3 +78,43 @@ def test_no_cpu_fallback_without_gpu(dl, trained_blob):
 def test_info_reports(dl):
     s = dl.dlic_info()
     assert "sm_100a" in s and "bf16_tcgen05" in s
+
+
+def test_container_build_and_unit_streams_agree_with_oracle_framing(dl):
+    """Host-only framing calls (no GPU): dlic_container_build frames the same
+    bytes as the oracle's container writer given the same streams, and
+    dlic_unit_streams partitions the streams by unit (tile-major, Q16)."""
+    rng = np.random.default_rng(3)
+    for (w, h, g, tile) in ((40, 30, 8, (16, 12)), (13, 5, 32, (0, 0)), (100, 70, 4, (30, 33))):
+        units = container.tiles(w, h, *tile)
+        streams = []
+        per_unit = []
+        for (_, _, tw, th) in units:
+            k = -(-th // g)
+            per_unit.append(k)
+            streams += [rng.integers(0, 256, 2 * int(rng.integers(2, 40)), dtype=np.uint8).tobytes() for _ in range(k)]
+        sha = bytes(rng.integers(0, 256, 32, dtype=np.uint8))
+        num = dl.dlic_numerics_rev()
+        ref = container.write(w, h, 1, g, tile[0], tile[1], sha, streams, num)
+        got = dl.dlic_container_build(w, h, sha, [len(s) for s in streams], b"".join(streams), 1, g, tile)
+        assert got == ref
+        assert dl.dlic_peek(got)["numerics"] == num and container.parse(got)["numerics"] == num
+        first = 0
+        for u, k in enumerate(per_unit):
+            assert dl.dlic_unit_streams(w, h, u, u + 1, 1, g, tile) == (first, k)
+            first += k
+        assert dl.dlic_unit_streams(w, h, 0, len(units), 1, g, tile) == (0, len(streams))
+        with pytest.raises(dl.DlicError):
+            dl.dlic_unit_streams(w, h, 0, len(units) + 1, 1, g, tile)
+        with pytest.raises(dl.DlicError):   # sizes must sum to the payload
+            dl.dlic_container_build(w, h, sha, [len(s) for s in streams], b"".join(streams)[:-2], 1, g, tile)
+
+
+def test_peek_rejects_other_container_versions(dl):
+    blob = model_io.save(synth.he_uniform_layers((78, 8, 256), seed=1))
+    b = bytearray(codec.encode(synth.random_image(9, 7, seed=1, kind="smooth"), blob, 1, 4))
+    assert dl.dlic_peek(bytes(b))["numerics"] == 0            # the oracle's own arithmetic
+    b[4] = 1                                                   # round-1 layout
+    with pytest.raises(dl.DlicError) as e:
+        dl.dlic_peek(bytes(b))
+    assert e.value.status == 5

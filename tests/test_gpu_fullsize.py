@@ -19,7 +19,16 @@ from oracle import codec, container, mlp, model_io, window
 
 pytestmark = pytest.mark.gpu
 
-BF16_TOL = 2e-2
+# bf16 path vs the oracle's bf16 definition (per row, L_inf / max|logit|).
+# Measured on 77k rows of the production encoder (scripts/measure_tol.py,
+# profiles/r2_tol.txt): median 1.7e-7, p99 2.6e-7, p99.9 9.2e-4, max 3.6e-3.
+# Rows whose bf16 activation roundings all agree with the oracle's differ only
+# by the fp32 accumulation order (~1e-6); a row where one hidden activation
+# rounds the other way (the fp32 sum sits within ~1e-6 of a bf16 midpoint)
+# moves by up to 2^-8 |w a| / |z| per flip.  Bars: max 8e-3
+# (2.2x the worst row seen) and p99 <= 1e-5 (the flip-free population).
+BF16_TOL = 8e-3
+BF16_P99 = 1e-5
 
 
 @pytest.fixture(scope="module")
@@ -42,7 +51,7 @@ def _oracle_bytes(dl, trained, blob, img, tile):
     h, w = img.shape
     fc = dl.dlic_debug_mlp(trained, img, precision=1, tile=tile, logits=False, probs=False, freqs=False)["fc"]
     return codec.encode_with_tables((fc & 0xFFFF).astype(np.int64), (fc >> 16).astype(np.int64), w, h, 1, 32,
-                                    tile[0], tile[1], model_io.digest(blob))
+                                    tile[0], tile[1], model_io.digest(blob), dl.dlic_numerics_rev())
 
 
 def _sampled_logits_ok(dl, trained, blob, img, tile, n=256, seed=0):
@@ -85,7 +94,7 @@ def _batch_roundtrip(dl, trained, imgs, tile):
     hdr = dl.dlic_peek(host[:sizes[0]].tobytes())
     d_dec = torch.empty_like(d_imgs)
     d_st = torch.zeros(n, dtype=torch.int32, device="cuda")
-    dl.dlic_decode_batch_device(trained, d_out, offs, hdr, d_dec, d_st)
+    dl.dlic_decode_batch_device(trained, d_out, offs, [int(x) for x in sizes], hdr, d_dec, d_st)
     torch.cuda.synchronize()
     assert d_st.cpu().numpy().tolist() == [0] * n
     assert np.array_equal(d_dec.cpu().numpy(), imgs)

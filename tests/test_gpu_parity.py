@@ -19,7 +19,16 @@ from oracle import codec, container, mlp, model_io, quant, streams, window
 
 pytestmark = pytest.mark.gpu
 
-BF16_TOL = 2e-2
+# bf16 path vs the oracle's bf16 definition (per row, L_inf / max|logit|).
+# Measured on 77k rows of the production encoder (scripts/measure_tol.py,
+# profiles/r2_tol.txt): median 1.7e-7, p99 2.6e-7, p99.9 9.2e-4, max 3.6e-3.
+# Rows whose bf16 activation roundings all agree with the oracle's differ only
+# by the fp32 accumulation order (~1e-6); a row where one hidden activation
+# rounds the other way (the fp32 sum sits within ~1e-6 of a bf16 midpoint)
+# moves by up to 2^-8 |w a| / |z| per flip.  Bars: max 8e-3
+# (2.2x the worst row seen) and p99 <= 1e-5 (the flip-free population).
+BF16_TOL = 8e-3
+BF16_P99 = 1e-5
 
 
 @pytest.fixture(scope="module")
@@ -60,7 +69,7 @@ def _rand_tables(h, w, seed, alpha=0.3):
 def test_rans_bit_exact_vs_oracle_same_tables(dl, h, w, g, tile):
     ft, img, fs, cs = _rand_tables(h, w, seed=h * 1000 + w)
     sha = bytes(range(32))
-    ob = codec.encode_with_tables(fs, cs, w, h, 1, g, tile[0], tile[1], sha)
+    ob = codec.encode_with_tables(fs, cs, w, h, 1, g, tile[0], tile[1], sha, dl.dlic_numerics_rev())
     fc = (fs | (cs << 16)).astype(np.uint32)
     gb = dl.dlic_rans_encode_tables(fc, precision=1, group_rows=g, tile=tile, model_sha=sha)
     assert gb == ob
@@ -72,7 +81,7 @@ def test_rans_bit_exact_vs_oracle_same_tables(dl, h, w, g, tile):
 
 def test_rans_decode_detects_corruption(dl):
     ft, img, fs, cs = _rand_tables(24, 20, seed=5)
-    ob = codec.encode_with_tables(fs, cs, 20, 24, 1, 8, 0, 0, bytes(32))
+    ob = codec.encode_with_tables(fs, cs, 20, 24, 1, 8, 0, 0, bytes(32), dl.dlic_numerics_rev())
     hdr = container.parse(ob)
     bad = bytearray(ob)
     bad[hdr["header_bytes"] + 6] ^= 0x10
@@ -97,6 +106,8 @@ def test_mlp_logits_vs_oracle(dl, trained, trained_blob, prec):
     rel = np.abs(out["logits"] - ref).max(-1) / np.maximum(np.abs(ref).max(-1), 1e-6)
     tol = 1e-4 if prec == 0 else BF16_TOL
     assert rel.max() <= tol, (prec, float(rel.max()))
+    if prec == 1:
+        assert np.quantile(rel, 0.99) <= BF16_P99, float(np.quantile(rel, 0.99))
     # integer tables follow exactly from the exported probabilities (fp32 decides)
     f_or = quant.q1(out["probs"].reshape(-1, 256)).reshape(37, 61, 256)
     assert np.array_equal(out["freqs"].astype(np.int64), f_or)
@@ -133,14 +144,14 @@ def test_roundtrip_and_oracle_bytes(dl, trained, trained_blob, prec, h, w, g, ti
     fc = dl.dlic_debug_mlp(trained, img, precision=prec, group_rows=g, tile=tile, logits=False, probs=False,
                            freqs=False)["fc"]
     ob = codec.encode_with_tables((fc & 0xFFFF).astype(np.int64), (fc >> 16).astype(np.int64), w, h, prec, g,
-                                  tile[0], tile[1], model_io.digest(trained_blob))
+                                  tile[0], tile[1], model_io.digest(trained_blob), dl.dlic_numerics_rev())
     assert ob == bits
     hd = dl.dlic_peek(bits)
     assert hd["precision"] == prec and hd["group_rows"] == g and hd["header_bytes"] + hd["payload_bytes"] == len(bits)
 
 
 def test_wide_unit_uses_clusters(dl, trained):
-    # W = 700 -> 234 rows per front -> 2-CTA cluster; W = 1100 -> 4 CTAs
+    # W = 700 -> 234 rows per front -> 4-CTA cluster (64 slots each); W = 1100 -> 367 rows -> 8 CTAs
     for w, h in ((700, 40), (1100, 24)):
         img = synth.natural_like(w, h, seed=w)
         for prec in (1, 0):
@@ -199,7 +210,7 @@ def test_c2_full_size_bf16_roundtrip_sampled_oracle_and_bpp_gate(dl, trained, tr
     g = out["logits"][rows, cols]
     ref = _oracle_logits(layers, img, 1, rows, cols)
     rel = np.abs(g - ref).max(-1) / np.maximum(np.abs(ref).max(-1), 1e-6)
-    assert rel.max() <= BF16_TOL
+    assert rel.max() <= BF16_TOL and np.quantile(rel, 0.99) <= BF16_P99
 
 
 def test_batch_device_api_matches_single(dl, trained):
@@ -219,7 +230,7 @@ def test_batch_device_api_matches_single(dl, trained):
     hdr = dl.dlic_peek(host[:sizes[0]].tobytes())
     d_dec = torch.empty_like(d_imgs)
     d_st = torch.zeros(6, dtype=torch.int32, device="cuda")
-    dl.dlic_decode_batch_device(trained, d_out, offs, hdr, d_dec, d_st)
+    dl.dlic_decode_batch_device(trained, d_out, offs, [int(x) for x in sizes], hdr, d_dec, d_st)
     torch.cuda.synchronize()
     assert d_st.cpu().numpy().tolist() == [0] * 6
     assert np.array_equal(d_dec.cpu().numpy(), imgs)

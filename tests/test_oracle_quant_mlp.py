@@ -133,3 +133,35 @@ def test_batch_consistency():
     full = mlp.logits_path(layers, x, 0)
     for i in (0, 17, 299):
         assert np.array_equal(full[i], mlp.logits_path(layers, x[i:i + 1], 0)[0])
+
+
+def test_bf16_hidden_activations_are_rerounded_hand_derived():
+    # One hidden unit: z1 = 1*1 + 2^-9 = 1 + 2^-9 exactly (fp32).  bf16 has an
+    # 8-bit significand, so the next representable value above 1 is 1 + 2^-7;
+    # 1 + 2^-9 lies below the midpoint 1 + 2^-8 and rounds DOWN to 1.  The
+    # output layer (weight 1, bias 0) therefore returns exactly 1.0.  Without
+    # the re-rounding it would return 1 + 2^-9.
+    layers = [(np.array([[1.0]], np.float32), np.array([2.0 ** -9], np.float32)),
+              (np.array([[1.0]], np.float32), np.array([0.0], np.float32))]
+    assert mlp.forward_bf16(layers, np.array([[1.0]]))[0, 0] == 1.0
+    assert mlp.forward_fp64(layers, np.array([[1.0]]))[0, 0] == 1.0 + 2.0 ** -9
+    # 1 + 3*2^-9 lies above the midpoint 1 + 2^-8 -> rounds UP to 1 + 2^-7
+    layers[0] = (layers[0][0], np.array([3 * 2.0 ** -9], np.float32))
+    assert mlp.forward_bf16(layers, np.array([[1.0]]))[0, 0] == 1.0 + 2.0 ** -7
+    # the exact midpoint 1 + 2^-8 ties to even (1.0, significand ...0)
+    layers[0] = (layers[0][0], np.array([2.0 ** -8], np.float32))
+    assert mlp.forward_bf16(layers, np.array([[1.0]]))[0, 0] == 1.0
+
+
+def test_bf16_bias_is_added_in_fp32_to_the_fp32_rounded_sum_hand_derived():
+    # Output layer only: inputs (1, 2^-30) with weights (1, 1) are bf16-exact and
+    # their exact sum is 1 + 2^-30, which rounds to 1.0 in fp32 (ulp 2^-23).
+    # Adding the bias 2^-24 in fp32: 1 + 2^-24 is the midpoint of [1, 1 + 2^-23]
+    # and ties to even -> exactly 1.0.  An fp64 bias add would give
+    # 1 + 2^-24 + 2^-30, which is above the midpoint and rounds to 1 + 2^-23
+    # when the logit is stored as fp32 (logits_path).
+    layers = [(np.array([[1.0], [1.0]], np.float32), np.array([2.0 ** -24], np.float32))]
+    x = np.array([[1.0, 2.0 ** -30]])
+    assert mlp.forward_bf16(layers, x)[0, 0] == 1.0
+    assert mlp.logits_path(layers, x, 1)[0, 0] == np.float32(1.0)
+    assert mlp.logits_path(layers, x, 0)[0, 0] == np.float32(1.0 + 2.0 ** -23)    # fp64 path, for contrast
