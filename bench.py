@@ -9,11 +9,17 @@ image per GPU), bf16 tcgen05 path, trained P100K weights, G = 32.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dlic|reference]
                   [--config C2] [--batch B] [--precision bf16|fp32]
 
-N > 1 runs under torchrun (one process per GPU, NCCL): every rank codes its own
-images (weak scaling; units are independent, P:103 lanes never cross images);
-the only collective is the all_gather of container sizes (north_star).
---impl reference times the CPU oracle (oracle/) on a bounded sample of the
-same workload (rank 0 only).
+N > 1: one process per GPU over NCCL.  `bench.py --gpus N` without WORLD_SIZE
+in the environment re-launches itself under torch.distributed.run with N
+ranks (127.0.0.1 rendezvous); under torchrun WORLD_SIZE must equal N.  Every
+rank codes its own images (weak scaling; units are independent, P:103 lanes
+never cross images) through paper_2207_05152_b200.dist.coded_step, whose only
+collective is the all_gather of container sizes (north_star) -- the function
+tests/test_dist.py runs under gloo.  C4 additionally reports one frame's 15
+tiles split across the ranks (dist.encode_units_distributed, strong scaling)
+under "strong_units".
+--impl reference times the CPU oracle (oracle/) on the same workload (rank 0
+only; C2: the whole image per step).
 """
 
 from __future__ import annotations
@@ -54,7 +60,22 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tile", default="", help="WxH independent tiles (default: the config's)")
     ap.add_argument("--no-variants", action="store_true", help="skip the strip-tiled C2 side measurement")
+    ap.add_argument("--no-strong", action="store_true", help="skip C4's unit-split (strong scaling) measurement")
     return ap.parse_args()
+
+
+def relaunch_distributed(args):
+    """`--gpus N` (N > 1) outside torchrun: run this script under
+    torch.distributed.run with N ranks on this node and return its exit code
+    (rank 0 prints the JSON line)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def load_peaks():
@@ -128,6 +149,10 @@ def dist_setup(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws != args.gpus:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%d (launch N ranks for N GPUs)" % (args.gpus, ws))
+    if ws > torch.cuda.device_count():
+        raise SystemExit("bench.py: %d ranks but %d visible GPUs" % (ws, torch.cuda.device_count()))
     if ws > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -192,7 +217,29 @@ def measure_variant(dl, model, d_imgs, prec, g, tile, reps=5):
 
 
 def default_batch(cfg):
-    return {"C1": 1, "C2": 1, "C3": 64, "C4": 1, "C5": 8}[cfg]
+    # C3: 512 slices across 8 GPUs = 64 per GPU; C5: "batch of 64" per GPU
+    # (960 tiles of 768x720 -> 26 waves of 37 four-CTA clusters: no tail)
+    return {"C1": 1, "C2": 1, "C3": 64, "C4": 1, "C5": 64}[cfg]
+
+
+def cpu_info():
+    """CPU model and the BLAS thread count the oracle runs with."""
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    except Exception:
+        pass
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "blas_threads": blas}
 
 
 # ------------------------------------------------------------------ reference arm (CPU oracle)
@@ -216,7 +263,9 @@ def run_reference(args):
     with open(os.path.join(ROOT, "fixtures", "p100k_trained.dlicmdl"), "rb") as fh:
         blob = fh.read()
     img = images_for(args, 0, 1)[0]
-    sh, sw = min(img.shape[0], 256), min(img.shape[1], 384)   # ~3-4 s of oracle work per step
+    # one whole image per step for C1-C3 (C2: ~10 s of oracle work); larger
+    # configs: the top-left 768x512 of the first image (~10 s)
+    sh, sw = min(img.shape[0], 512), min(img.shape[1], 768)
     sample = np.ascontiguousarray(img[:sh, :sw])
     prec = 1 if args.precision == "bf16" else 0
     g, _ = opts_for(args.config)
@@ -231,12 +280,9 @@ def run_reference(args):
             times.append(dt)
     ms = statistics.mean(times) * 1e3
     mpx = sample.size / (ms / 1e3) / 1e6
-    cores = 1
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count() or 1
+    ci = cpu_info()
+    cores = ci["blas_threads"] or ci["logical_cpus"] or 1
+    whole = sample.shape == img.shape
     line = {
         "impl": "reference", "metric": METRIC, "value": mpx,
         "unit": "Mpixel/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -244,10 +290,12 @@ def run_reference(args):
         "dtype": "f64-accum bf16-emulated" if prec else "f64", "data": "synthetic",
         "config": dict(arm_config(args, default_batch(args.config) if not args.batch else args.batch,
                                   img.shape[1], img.shape[0], tile_for(args)[1], g, ws),
-                       sample="per step the oracle codes a top-left %dx%d crop of one image (untiled)" % (sw, sh)),
-        "cpu_baseline": {"value": mpx, "unit": "Mpixel/s", "cores": cores, "kind": "oracle",
-                         "sample": "top-left %dx%d crop of the %s image, oracle encode+decode per step"
-                                   % (sw, sh, args.config)},
+                       sample=("per step the oracle codes one whole %dx%d image (untiled)" % (sw, sh)) if whole
+                       else "per step the oracle codes a top-left %dx%d crop of one image (untiled)" % (sw, sh)),
+        "cpu_baseline": dict({"value": mpx, "unit": "Mpixel/s", "cores": cores, "kind": "oracle",
+                              "sample": ("the whole %s image (%dx%d), oracle encode+decode per step" % (args.config, sw, sh))
+                              if whole else "top-left %dx%d crop of the %s image, oracle encode+decode per step"
+                              % (sw, sh, args.config)}, **ci),
         "e2e": {"value": mpx, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -266,19 +314,79 @@ def cpu_baseline_sample(args, img):
     out = codec.decode(b, blob)
     dt = time.perf_counter() - t0
     assert np.array_equal(out, sample)
-    cores = os.cpu_count() or 1
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
-    except Exception:
-        pass
-    return {"value": sample.size / dt / 1e6, "unit": "Mpixel/s", "cores": cores, "kind": "oracle",
-            "sample": "top-left %dx%d crop of the %s image: oracle encode+decode (%.1f s)" % (sw, sh, args.config, dt)}
+    ci = cpu_info()
+    cores = ci["blas_threads"] or ci["logical_cpus"] or 1
+    return dict({"value": sample.size / dt / 1e6, "unit": "Mpixel/s", "cores": cores, "kind": "oracle",
+                 "sample": "top-left %dx%d crop of the %s image: oracle encode+decode (%.1f s)"
+                           % (sw, sh, args.config, dt)}, **ci)
+
+
+def measure_strong_units(dl, model, img, prec, g, tile, ws, rank, dev, args):
+    """C4: ONE frame's tiles split across the ranks (strong scaling), through
+    the public unit-range calls with host buffers: each rank codes its units
+    (dlic_encode_units: H2D of the frame, D2H of its payload), the stream sizes
+    are all-gathered (dist.encode_units_distributed), then each rank decodes
+    its units (dlic_decode_units).  Timed per frame as the max over ranks."""
+    import torch
+    from paper_2207_05152_b200 import dist as dd
+    h, w = img.shape
+    n_units = dl.dlic_peek(dl.dlic_encode(model, img, prec, g, tile))["n_units"]
+    out = np.zeros_like(img)
+    state = {}
+
+    def enc(lo, hi):
+        return dl.dlic_encode_units(model, img, lo, hi, prec, g, tile)
+
+    def frame():
+        if ws > 1:
+            payload, rng, soffs, all_ssz = dd.encode_units_distributed(enc, n_units)
+        else:
+            payload, ssz = enc(0, n_units)
+            rng, all_ssz = (0, n_units), ssz
+        state["rng"] = rng
+        # a rank decodes its own units of the container (framed here from
+        # the gathered sizes; every payload byte of its range is its own)
+        lo, hi = rng
+        if hi > lo:
+            first, nst = dl.dlic_unit_streams(w, h, lo, hi, prec, g, tile)
+            sizes = [int(x) for x in all_ssz]
+            full = bytearray(sum(sizes))
+            off = sum(sizes[:first])
+            full[off:off + len(payload)] = payload
+            bits = dl.dlic_container_build(w, h, model.sha256(), sizes, bytes(full), prec, g, tile)
+            dl.dlic_decode_units(model, bits, lo, hi, out)
+
+    for _ in range(args.warmup):
+        frame()
+    times = []
+    for _ in range(args.steps):
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        frame()
+        torch.cuda.synchronize()
+        times.append((time.perf_counter() - t0) * 1e3)
+    ms = statistics.mean(times)
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        allt = [torch.empty_like(t) for _ in range(ws)]
+        torch.distributed.all_gather(allt, t)
+        ms = max(float(x[0]) for x in allt)
+    lo, hi = state["rng"]
+    tiles = [(x0, y0) for y0 in range(0, h, tile[1]) for x0 in range(0, w, tile[0])]
+    for (x0, y0) in tiles[lo:hi]:
+        assert np.array_equal(out[y0:y0 + tile[1], x0:x0 + tile[0]], img[y0:y0 + tile[1], x0:x0 + tile[0]])
+    return {"scaling": "strong", "what": "one 1920x1080 frame, its %d tiles split across %d rank(s); host buffers, "
+            "encode+decode per frame, max over ranks" % (n_units, ws), "ms_per_frame": ms,
+            "mpx_s": img.size / (ms / 1e3) / 1e6, "units_per_rank": hi - lo}
 
 
 # ------------------------------------------------------------------ product arm
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args))
     if args.impl == "reference":
         run_reference(args)
         return
@@ -316,13 +424,21 @@ def main():
     total_bytes = int(sizes.sum())
     payload = total_bytes - n * hdr["header_bytes"]
 
-    def step():
+    from paper_2207_05152_b200 import dist as dd
+
+    def encode_local():
         dl.dlic_encode_batch_device(model, d_imgs, prec, g, tile, d_out=d_out, d_sizes=d_sizes)
-        if ws > 1:
-            import torch.distributed as dist
-            gathered = [torch.empty_like(d_sizes) for _ in range(ws)]
-            dist.all_gather(gathered, d_sizes)      # the only collective: container sizes
+        return d_sizes
+
+    def decode_local():
         dl.dlic_decode_batch_device(model, d_out, offs, lens, hdr, d_dec, d_status)
+
+    def step():
+        if ws > 1:   # the only collective: all_gather of the container sizes (dist.coded_step)
+            dd.coded_step(encode_local, decode_local)
+        else:
+            encode_local()
+            decode_local()
 
     for _ in range(args.warmup):
         step()
@@ -392,6 +508,10 @@ def main():
         e2e = {"value": ws * px_rank / (em / 1e3) / 1e6, "unit": "Mpixel/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": em}
 
+    strong = None
+    if args.config == "C4" and tile != (0, 0) and not args.no_strong:
+        strong = measure_strong_units(dl, model, imgs[0], prec, g, tile, ws, rank, dev, args)
+
     variants = None
     if rank == 0 and ws == 1 and args.config == "C2" and tile == (0, 0) and not args.no_variants:
         # the same image as 4 independent 768x128 strips (north_star: "independent
@@ -405,7 +525,7 @@ def main():
         achieved = dec_flops / (t_dec / 1e3) / 1e12
         # fp32 path runs on CUDA-core FFMA: 148 SMs x 128 FMA/clk x 2 x sm_max
         peak = peaks["bf16_tflops"] if prec == 1 else 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-        traffic = None
+        traffic = None   # dram bytes per k_decode launch from a stored ncu --set full capture (not this run)
         try:
             with open(os.path.join(ROOT, "profiles", "decode_traffic.json")) as fh:
                 traffic = json.load(fh).get("%s_%s" % (args.config, args.precision))
@@ -432,6 +552,8 @@ def main():
             "roofline": {"kernel": "k_decode<%s>" % args.precision, "bound": "tensor" if prec == 1 else "alu", "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": src + (" bf16_tflops" if prec == 1 else " sm_max_mhz x 148 SM x 128 FFMA x 2 (DESIGN.md)"),
+                         "traffic_source": "stored ncu --set full capture of this config's k_decode launch "
+                                           "(profiles/decode_traffic.json), not measured in this run",
                          "latency_floor_ms": floor_ms, "latency_frac": floor_ms / t_dec},
             # the throughput-bound encoder MLP (all pixels at once) against the same peak
             "roofline_encode": {"kernel": "k_enc_pp" if prec == 1 else "k_enc_mlp<fp32>",
@@ -441,6 +563,7 @@ def main():
                                 "frac": FLOP_PER_PX * px_rank / (mlp_ms / 1e3) / 1e12 / peak,
                                 "note": "M=64 tcgen05 tiles cost as M=128: ceiling 0.5 of peak (DESIGN.md)"},
             "variants": variants,
+            "strong_units": strong,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": 6 * args.steps,

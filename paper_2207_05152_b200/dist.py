@@ -1,13 +1,24 @@
-"""Multi-GPU sharding of independent units (images) — one process per GPU.
+"""Multi-GPU sharding of independent units — one process per GPU.
 
-Units never exchange payload (P:103 lanes are per row, Q16 tiles/images are
-independent), so ranks take disjoint contiguous blocks of the batch and code
-them on their own device.  The single collective is an all_gather of the
-per-image container sizes (north_star: "NCCL is used only for the final gather
-of stream sizes"), from which every rank derives the global byte offsets of its
-containers in the batch index.  The plan/offset logic is pure Python so it is
-tested with the gloo backend on CPU (tests/test_dist.py); the device work is
-the C-ABI batch calls.
+Units never exchange payload: the rANS coder instances are per pixel row
+ and tiles/images are independent units with fill 0 at their borders
+(reading Q16), so ranks take disjoint contiguous blocks of units and code them
+on their own device.  The single collective is an all_gather of container (or
+stream) sizes (north_star: "NCCL is used only for the final gather of stream
+sizes"), from which every rank derives the global byte offsets of its output.
+
+Two granularities, both used by bench.py and covered by the world-size-2 gloo
+tests (tests/test_dist.py) with the same functions:
+  * coded_step      -- weak scaling: every rank codes its own batch of images
+                       (device batch API); per step one all_gather of the
+                       per-image container sizes, on the device (no host sync);
+  * encode_units_distributed / decode_units_distributed -- one image's tiles
+                       split across ranks (C4: "tiled into independent streams
+                       across 1/2/4/8 B200"): each rank codes a unit range
+                       (dlic_encode_units), the per-stream sizes are gathered,
+                       and any rank frames the container (dlic_container_build).
+The coding itself is passed in as callables, so the same code runs with the
+C-ABI on GPUs and with the oracle under gloo on CPU.
 """
 
 from __future__ import annotations
@@ -23,7 +34,8 @@ def shard_range(n_units: int, world: int, rank: int):
 
 
 def global_offsets(all_sizes):
-    """Exclusive prefix sum over ranks' size lists (rank-major, unit order)."""
+    """Exclusive prefix sum over ranks' size lists (rank-major, unit order);
+    the last entry is the total."""
     flat = np.concatenate([np.asarray(s, dtype=np.int64).reshape(-1) for s in all_sizes])
     off = np.zeros(len(flat) + 1, dtype=np.int64)
     np.cumsum(flat, out=off[1:])
@@ -31,44 +43,80 @@ def global_offsets(all_sizes):
 
 
 def gather_sizes(local_sizes, group=None):
-    """all_gather of per-unit container sizes (int64); the only collective.
-    Works on any torch.distributed backend; with NCCL the tensor must be on
-    the rank's device.  Ranks may hold different unit counts."""
+    """all_gather of per-unit sizes (int64) when ranks hold DIFFERENT counts
+    (host lists in, host arrays out).  Works on any backend; with NCCL the
+    tensors live on the rank's device."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    t = torch.as_tensor(local_sizes, dtype=torch.int64)
-    if dist.get_backend(group) == "nccl":
-        t = t.cuda()
-    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
-    ns = [torch.empty_like(n) for _ in range(world)]
-    dist.all_gather(ns, n, group=group)
-    m = int(max(int(x) for x in ns))
-    pad = torch.zeros(m, dtype=torch.int64, device=t.device)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else None
+    t = torch.as_tensor(np.asarray(local_sizes, dtype=np.int64), dtype=torch.int64, device=dev)
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=dev)
+    ns = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(ns, n, group=group)
+    counts = [int(x) for x in ns.cpu()]
+    m = max(counts)
+    pad = torch.zeros(m, dtype=torch.int64, device=dev)
     pad[: t.numel()] = t
-    outs = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(outs, pad, group=group)
-    return [o[: int(k)].cpu().numpy() for o, k in zip(outs, ns)]
+    out = torch.empty(world * m, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    out = out.cpu().numpy().reshape(world, m)
+    return [out[r, :counts[r]] for r in range(world)]
 
 
-def encode_batch_distributed(encode_shard, images, group=None):
-    """Encode `images` (n, H, W) across the ranks of `group`.
+def exchange_sizes_device(d_sizes, group=None):
+    """The weak-scaling step's only collective: all_gather of this rank's
+    per-image container sizes (equal counts on every rank), tensor in, tensor
+    out (world, n), stream-ordered -- no host synchronisation."""
+    import torch
+    import torch.distributed as dist
 
-    encode_shard(shard) -> list of container bytes (the caller binds the
-    device path, e.g. dlic_encode_batch_device on this rank's GPU).
-    Returns (my_containers, my_first_unit, offsets) where offsets[i] is the
-    global byte offset of unit i in the concatenated batch and offsets[-1] the
-    total; every rank can write its containers at its own offsets without any
-    payload exchange."""
+    world = dist.get_world_size(group)
+    src = d_sizes.contiguous().reshape(-1)
+    out = torch.empty(world * src.numel(), dtype=src.dtype, device=src.device)
+    dist.all_gather_into_tensor(out, src, group=group)
+    return out.view((world,) + tuple(d_sizes.shape))
+
+
+def offsets_device(all_sizes):
+    """Exclusive scan of the gathered (world, n) sizes in rank-major order
+    (each rank's byte offset of its containers in the job's output)."""
+    flat = all_sizes.reshape(-1)
+    return flat.cumsum(0) - flat
+
+
+def coded_step(encode_local, decode_local, group=None):
+    """One weak-scaling step on this rank: encode_local() codes the rank's
+    batch and returns its per-image sizes (a tensor); the sizes are
+    all-gathered and scanned into global offsets (the only exchange); then
+    decode_local() decodes the rank's containers.  Returns (all_sizes,
+    offsets) as tensors."""
+    sizes = encode_local()
+    all_sizes = exchange_sizes_device(sizes, group)
+    offs = offsets_device(all_sizes)
+    decode_local()
+    return all_sizes, offs
+
+
+def encode_units_distributed(encode_units, n_units: int, group=None):
+    """One image's units split across the ranks of `group`.
+
+    encode_units(lo, hi) -> (payload bytes, per-stream sizes) codes units
+    [lo, hi) (dlic_encode_units on this rank's GPU).  The per-stream sizes
+    are all-gathered (the only exchange).  Returns (my_payload, (lo, hi),
+    stream_offsets, all_stream_sizes): stream_offsets[k] is the payload byte
+    offset of stream k (the last entry the payload total), so every rank knows
+    where its payload goes; any rank frames the header from all_stream_sizes
+    (dlic_container_build) without seeing another rank's payload."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    lo, hi = shard_range(len(images), world, rank)
-    mine = encode_shard(images[lo:hi]) if hi > lo else []
-    sizes = gather_sizes([len(b) for b in mine], group)
-    return mine, lo, global_offsets(sizes)
+    lo, hi = shard_range(n_units, world, rank)
+    payload, ssz = encode_units(lo, hi) if hi > lo else (b"", [])
+    all_ssz = gather_sizes(ssz, group)
+    return payload, (lo, hi), global_offsets(all_ssz), np.concatenate([np.asarray(s, np.int64) for s in all_ssz])
 
 
 def assemble(parts_by_rank, offsets):
@@ -80,3 +128,14 @@ def assemble(parts_by_rank, offsets):
             out[offsets[i]:offsets[i + 1]] = b
             i += 1
     return bytes(out)
+
+
+def decode_units_distributed(decode_units, n_units: int, group=None):
+    """Each rank decodes its unit range of one container (no exchange);
+    decode_units(lo, hi) writes those units' pixels.  Returns the range."""
+    import torch.distributed as dist
+
+    lo, hi = shard_range(n_units, dist.get_world_size(group), dist.get_rank(group))
+    if hi > lo:
+        decode_units(lo, hi)
+    return lo, hi
