@@ -61,7 +61,7 @@ def _sweep_cases(n=112, seed=2024):
         g = int(rng.choice([1, 2, 4, 8, 16, 32]))
         tiled = rng.random() < 0.3 and w > 4 and h > 4
         tile = (int(rng.integers(3, w)), int(rng.integers(3, h))) if tiled else (0, 0)
-        while -(-(tile[1] or h) // g) > 300:   # the decoder keeps <= ~320 group cursors in shared memory
+        while -(-(tile[1] or h) // g) > 200:   # the decoder keeps <= ~250 group cursors in shared memory
             g *= 2
         # fp32 (CUDA-core engine, ~0.14 ms per front) only on shapes with few fronts
         prec = 0 if (rng.random() < 0.25 and w + 3 * h < 1500) else 1
@@ -100,7 +100,7 @@ def test_too_many_groups_per_unit_is_rejected_up_front(dl, trained):
     with pytest.raises(dl.DlicError) as e:
         dl.dlic_encode(trained, img, precision=1, group_rows=1)
     assert e.value.status == 1
-    assert np.array_equal(dl.dlic_decode(trained, dl.dlic_encode(trained, img, group_rows=2)), img)
+    assert np.array_equal(dl.dlic_decode(trained, dl.dlic_encode(trained, img, group_rows=4)), img)
 
 
 def test_c4_untiled_16_cta_cluster(dl, trained, trained_blob):
