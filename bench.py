@@ -39,6 +39,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FLOP_PER_PX = 216576            # P100K, SURVEY App. A item 1 (2 * sum K*N)
+# model fixtures: (file, metadata reals per image or None, description)
+MODELS = {
+    "p100k": ("p100k_trained.dlicmdl", None,
+              "P100K briefly trained by the oracle (fixtures/p100k_trained.dlicmdl)"),
+    "pool-meta": ("p100k_pool_meta.dlicmdl", [0.9, 3.0, 1.25],
+                  "P100K-pool-meta: 78+3 metadata inputs, avg-pool 2 after layers 1 and 3, seeded random "
+                  "(fixtures/p100k_pool_meta.dlicmdl; pooling folded into the next layer, metadata into a "
+                  "per-image layer-1 bias: the tensor-core chain runs P100K's shapes, 216,576 FLOP/px)"),
+}
 CONFIG_DESC = {
     "C1": "C1 32x32 gradient+noise, single stream (G=32=H)",
     "C2": "C2 768x512 Kodak-shaped natural-like, 1 image per GPU per step",
@@ -61,6 +70,8 @@ def parse():
     ap.add_argument("--tile", default="", help="WxH independent tiles (default: the config's)")
     ap.add_argument("--no-variants", action="store_true", help="skip the strip-tiled C2 side measurement")
     ap.add_argument("--no-strong", action="store_true", help="skip C4's unit-split (strong scaling) measurement")
+    ap.add_argument("--model", default="p100k", choices=list(MODELS),
+                    help="p100k: trained fixture; pool-meta: the f4 network (pooling + 3 metadata inputs)")
     return ap.parse_args()
 
 
@@ -250,7 +261,7 @@ def arm_config(args, n, W, H, tile, g, ws):
     """The config object of the JSON line (both arms)."""
     return {"workload": CONFIG_DESC[args.config], "images_per_gpu": n, "width": W, "height": H,
             "tile": list(tile), "group_rows": g, "precision": args.precision,
-            "weights": "P100K briefly trained by the oracle (fixtures/p100k_trained.dlicmdl)",
+            "weights": MODELS[args.model][2],
             "l2": "flushed between timed steps (256 MiB write, untimed)", "parallelism": "dp%d" % ws}
 
 
@@ -260,8 +271,9 @@ def run_reference(args):
     if rank != 0:
         return
     from oracle import codec  # the one other place bench.py executes oracle/
-    with open(os.path.join(ROOT, "fixtures", "p100k_trained.dlicmdl"), "rb") as fh:
+    with open(os.path.join(ROOT, "fixtures", MODELS[args.model][0]), "rb") as fh:
         blob = fh.read()
+    meta = MODELS[args.model][1]
     img = images_for(args, 0, 1)[0]
     # one whole image per step for C1-C3 (C2: ~10 s of oracle work); larger
     # configs: the top-left 768x512 of the first image (~10 s)
@@ -272,7 +284,7 @@ def run_reference(args):
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        b = codec.encode(sample, blob, prec, g)
+        b = codec.encode(sample, blob, prec, g, meta=meta)
         out = codec.decode(b, blob)
         dt = time.perf_counter() - t0
         assert np.array_equal(out, sample)
@@ -304,13 +316,13 @@ def run_reference(args):
 def cpu_baseline_sample(args, img):
     """Oracle (as it stands) on a bounded sample of the workload (~10 s)."""
     from oracle import codec
-    with open(os.path.join(ROOT, "fixtures", "p100k_trained.dlicmdl"), "rb") as fh:
+    with open(os.path.join(ROOT, "fixtures", MODELS[args.model][0]), "rb") as fh:
         blob = fh.read()
     sh, sw = min(img.shape[0], 512), min(img.shape[1], 768)   # C2: the whole image (~10-15 s)
     sample = np.ascontiguousarray(img[:sh, :sw])
     prec = 1 if args.precision == "bf16" else 0
     t0 = time.perf_counter()
-    b = codec.encode(sample, blob, prec, 32)
+    b = codec.encode(sample, blob, prec, 32, meta=MODELS[args.model][1])
     out = codec.decode(b, blob)
     dt = time.perf_counter() - t0
     assert np.array_equal(out, sample)
@@ -395,13 +407,14 @@ def main():
     import paper_2207_05152_b200 as dl
 
     dev = torch.device("cuda", local)
-    with open(os.path.join(ROOT, "fixtures", "p100k_trained.dlicmdl"), "rb") as fh:
+    with open(os.path.join(ROOT, "fixtures", MODELS[args.model][0]), "rb") as fh:
         blob = fh.read()
     model = dl.dlic_model_load(blob, local)
     prec = 1 if args.precision == "bf16" else 0
     g, tile = tile_for(args)
     n = args.batch or default_batch(args.config)
     imgs = images_for(args, rank, n)
+    meta = None if MODELS[args.model][1] is None else np.tile(np.array(MODELS[args.model][1], np.float32), (n, 1))
     _, H, W = imgs.shape
     px_rank = n * H * W
     stream = torch.cuda.current_stream(dev)
@@ -412,7 +425,7 @@ def main():
     dl.dlic_set_timing(True)
 
     # first pass: planning header + correctness check of this batch
-    d_out, d_sizes, stride = dl.dlic_encode_batch_device(model, d_imgs, prec, g, tile)
+    d_out, d_sizes, stride = dl.dlic_encode_batch_device(model, d_imgs, prec, g, tile, meta=meta)
     torch.cuda.synchronize()
     sizes = d_sizes.cpu().numpy()
     hdr = dl.dlic_peek(d_out[:int(sizes[0])].cpu().numpy().tobytes())
@@ -427,7 +440,7 @@ def main():
     from paper_2207_05152_b200 import dist as dd
 
     def encode_local():
-        dl.dlic_encode_batch_device(model, d_imgs, prec, g, tile, d_out=d_out, d_sizes=d_sizes)
+        dl.dlic_encode_batch_device(model, d_imgs, prec, g, tile, d_out=d_out, d_sizes=d_sizes, meta=meta)
         return d_sizes
 
     def decode_local():
@@ -485,11 +498,11 @@ def main():
             t0 = time.perf_counter()
             tot_in = tot_out = 0
             if n == 1:  # the paper's calls: encode(image) -> bits, decode(bits) -> image
-                b = dl.dlic_encode(model, pin_imgs[0], prec, g, tile)
+                b = dl.dlic_encode(model, pin_imgs[0], prec, g, tile, meta=None if meta is None else meta[0])
                 back = dl.dlic_decode(model, b)[None]
                 nb = len(b)
             else:  # the same calls over the rank's batch: one H2D and one D2H each way
-                blob, sizes = dl.dlic_encode_batch(model, pin_imgs, prec, g, tile)
+                blob, sizes = dl.dlic_encode_batch(model, pin_imgs, prec, g, tile, meta=meta)
                 back = dl.dlic_decode_batch(model, blob, sizes)
                 nb = len(blob)
             tot_in = pin_imgs.nbytes + nb
@@ -509,11 +522,11 @@ def main():
                "d2h_bytes_per_step": d2h, "ms_per_step": em}
 
     strong = None
-    if args.config == "C4" and tile != (0, 0) and not args.no_strong:
+    if args.config == "C4" and tile != (0, 0) and not args.no_strong and meta is None:
         strong = measure_strong_units(dl, model, imgs[0], prec, g, tile, ws, rank, dev, args)
 
     variants = None
-    if rank == 0 and ws == 1 and args.config == "C2" and tile == (0, 0) and not args.no_variants:
+    if rank == 0 and ws == 1 and args.config == "C2" and tile == (0, 0) and not args.no_variants and meta is None:
         # the same image as 4 independent 768x128 strips (north_star: "independent
         # image tiles with their own streams"): 1149 instead of 2301 fronts
         variants = {"strips_768x128": measure_variant(dl, model, d_imgs, prec, g, (768, 128))}

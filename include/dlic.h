@@ -52,7 +52,7 @@ typedef enum {
   DLIC_E_BUFFER_TOO_SMALL = 11,
   DLIC_E_CUDA = 12,            /* CUDA runtime / launch failure, or no sm_100 device */
   DLIC_E_OUT_OF_MEMORY = 13,
-  DLIC_E_UNSUPPORTED_MODEL = 14 /* the GPU engines implement 78->128x5->256 (P100K) */
+  DLIC_E_UNSUPPORTED_MODEL = 14 /* topology outside the GPU engines' (see dlic_model_load) */
 } dlic_status;
 
 /* Precision path of the density estimator (recorded in the container; both
@@ -65,11 +65,18 @@ enum { DLIC_PREC_FP32 = 0, DLIC_PREC_BF16 = 1 };
 
 typedef struct dlic_model dlic_model; /* opaque; immutable after load */
 
+#define DLIC_MAX_META 8
+
 typedef struct {
   uint32_t precision;  /* DLIC_PREC_* */
   uint32_t group_rows; /* G: rows per interleaved stream (R7); 0 -> 32 */
   uint32_t tile_w;     /* independent tiles (Q16); 0,0 = untiled */
   uint32_t tile_h;
+  /* metadata inputs: n_meta raw reals per image, HOST array
+   * meta[i * n_meta + k] for image i of a call (single-image calls: i = 0).
+   * n_meta must equal the model's metadata feature count (0 = none). */
+  uint32_t n_meta;
+  const float* meta;
 } dlic_opts;
 
 /* Container (version 2, little-endian):
@@ -77,22 +84,36 @@ typedef struct {
  *   u32 width, u32 height, u16 tile_w, u16 tile_h (0,0 = untiled; Q16),
  *   u16 G (rows per stream, R7), u16 numerics (arithmetic revision of the
  *   tables, see dlic_numerics_rev), 32-byte SHA-256 of the model file,
- *   u32 n_streams, u32 sizes[n_streams] (bytes), then the streams tile-major,
- *   group-major within a tile.  Each stream: the group's flushed rANS states
- *   (rows ascending, hi word then lo word) followed by its renormalisation
- *   words in decoder order (front ascending, row ascending), 16-bit LE words. */
+ *   u32 n_streams, u32 sizes[n_streams] (bytes), u32 n_meta, f32
+ *   meta[n_meta] (the image's raw metadata reals, uncompressed), then
+ *   the streams tile-major, group-major within a tile.  Each stream: the
+ *   group's flushed rANS states (rows ascending, hi word then lo word)
+ *   followed by its renormalisation words in decoder order (front ascending,
+ *   row ascending), 16-bit LE words. */
 typedef struct {
   uint32_t width, height, precision, group_rows, tile_w, tile_h, n_streams, n_units;
   uint32_t numerics; /* arithmetic revision recorded by the encoder */
+  uint32_t n_meta;   /* metadata reals stored in the container */
+  float meta[DLIC_MAX_META];
   uint8_t model_sha256[32];
   uint64_t payload_bytes, header_bytes;
 } dlic_header;
 
 /* ---- models --------------------------------------------------------------
  * "DLICMDL1" blob: magic, u16 layers, per layer {u32 in, u32 out,
- * u8 act, u8 pool, f32 W[in][out] row-major, f32 b[out]}, u16 meta count,
- * SHA-256 of all preceding bytes.  Uploads fp32 and bf16 device copies to
- * `cuda_device`.  Errors: DLIC_E_CORRUPT_MODEL, DLIC_E_CUDA. */
+ * u8 act, u8 pool group g (0 = none), f32 W[in][out] row-major, f32 b[out]},
+ * u16 metadata feature count n, n x f32 (min, max), SHA-256 of all preceding
+ * bytes.  Uploads fp32 and bf16 device copies to `cuda_device`.
+ * The GPU engines run six dense layers with 128-unit hidden layers and 256
+ * outputs ("P100K"), on 78 window inputs + n <= 8 metadata inputs
+ * (min-max normalised with the stored constants), with optional average
+ * pooling of g = 2^k units after any hidden layer ("two optional
+ * pooling layers"; the next layer then has 128 / g inputs).  Pooling is linear
+ * and is folded into the next layer's weights at load (W' = P^T W: exact in
+ * bf16 and fp32 because 1/g is a power of two); the metadata inputs are
+ * folded into a per-image layer-1 bias by a kernel at each call.  Other
+ * topologies load (hash, dlic_peek) but encode/decode return
+ * DLIC_E_UNSUPPORTED_MODEL.  Errors: DLIC_E_CORRUPT_MODEL, DLIC_E_CUDA. */
 dlic_status dlic_model_load(const void* bytes, size_t len, int cuda_device, dlic_model** out);
 /* Same from arrays: dims[n_layers+1]; W[l] row-major [dims[l]][dims[l+1]]
  * float32; b[l] float32[dims[l+1]].  The blob (and its hash) is built here. */

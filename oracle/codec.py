@@ -21,12 +21,22 @@ import numpy as np
 from . import container, mlp, model_io, quant, schedule, streams, window
 
 
+def _net(layers):
+    """`layers` is a list of (W, b), or the dict of model_io.load_net (+ the
+    image's normalised metadata under "meta_norm")."""
+    if isinstance(layers, dict):
+        return layers["layers"], layers.get("pool"), layers.get("meta_norm")
+    return layers, None, None
+
+
 def unit_front_tables(layers, precision: int, img: np.ndarray, rows, cols):
     """Tables for the pixels (rows, cols) of one front of one unit image.
 
-    P:90: one matrix per front, one row per pixel neighbourhood."""
-    x = window.features(window.gather_many(img, rows, cols))
-    logits = mlp.logits_path(layers, x, precision)
+    P:90: one matrix per front, one row per pixel neighbourhood (window
+    features, then the image's metadata features)."""
+    lay, pool, meta_norm = _net(layers)
+    x = window.net_inputs(img, rows, cols, meta_norm)
+    logits = mlp.logits_path(lay, x, precision, pool)
     p, f, c = quant.tables_from_logits(logits)
     return logits, p, f, c
 
@@ -66,7 +76,7 @@ def all_pixel_tables(layers, precision: int, img: np.ndarray, chunk: int = 65536
 
 def encode_with_tables(fs_img: np.ndarray, cs_img: np.ndarray, width: int, height: int,
                        precision: int, group_rows: int, tile_w: int, tile_h: int,
-                       model_sha: bytes, numerics: int = container.ORACLE_NUMERICS) -> bytes:
+                       model_sha: bytes, numerics: int = container.ORACLE_NUMERICS, meta=None) -> bytes:
     """Container from given per-pixel (f_s, c_s) of the true symbols — the
     "oracle fed the same integer tables" leg (north_star).  `numerics` is the
     header field naming the arithmetic that produced the tables (the caller's;
@@ -75,12 +85,16 @@ def encode_with_tables(fs_img: np.ndarray, cs_img: np.ndarray, width: int, heigh
     for (x0, y0, tw, th) in container.tiles(width, height, tile_w, tile_h):
         sts = streams.encode_unit(fs_img[y0:y0 + th, x0:x0 + tw], cs_img[y0:y0 + th, x0:x0 + tw], group_rows)
         out += [streams.rans.words_to_bytes(s) for s in sts]
-    return container.write(width, height, precision, group_rows, tile_w, tile_h, model_sha, out, numerics)
+    return container.write(width, height, precision, group_rows, tile_w, tile_h, model_sha, out, numerics, meta)
 
 
 def encode(img: np.ndarray, model_blob: bytes, precision: int = 0, group_rows: int = 32,
-           tile_w: int = 0, tile_h: int = 0) -> bytes:
-    layers = model_io.load(model_blob)
+           tile_w: int = 0, tile_h: int = 0, meta=None) -> bytes:
+    """meta: the image's raw metadata reals (the model's metadata inputs, P:210);
+    stored uncompressed in the container."""
+    net = model_io.load_net(model_blob)
+    net["meta_norm"] = window.meta_features(meta, net["meta_range"])
+    layers = net
     h, w = img.shape
     fs = np.zeros((h, w), np.int64)
     cs = np.zeros((h, w), np.int64)
@@ -88,7 +102,8 @@ def encode(img: np.ndarray, model_blob: bytes, precision: int = 0, group_rows: i
         f_u, c_u = unit_tables_by_front(layers, precision, np.ascontiguousarray(img[y0:y0 + th, x0:x0 + tw]))
         fs[y0:y0 + th, x0:x0 + tw] = f_u
         cs[y0:y0 + th, x0:x0 + tw] = c_u
-    return encode_with_tables(fs, cs, w, h, precision, group_rows, tile_w, tile_h, model_io.digest(model_blob))
+    return encode_with_tables(fs, cs, w, h, precision, group_rows, tile_w, tile_h, model_io.digest(model_blob),
+                              meta=meta)
 
 
 class ModelHashMismatch(Exception):
@@ -116,7 +131,8 @@ def decode(blob: bytes, model_blob: bytes) -> np.ndarray:
         raise ModelHashMismatch()
     if hdr["numerics"] != container.ORACLE_NUMERICS:         # tables of another arithmetic
         raise container.CorruptContainer("numerics revision %d is not the oracle's" % hdr["numerics"])
-    layers = model_io.load(model_blob)
+    layers = model_io.load_net(model_blob)
+    layers["meta_norm"] = window.meta_features(hdr["meta"], layers["meta_range"])   # re-read from the container
     prec = hdr["precision"]
     out = np.zeros((hdr["height"], hdr["width"]), np.uint8)
     for (x0, y0, tw, th), sts in _split_streams(hdr):
@@ -150,7 +166,8 @@ def raster_decode(blob: bytes, model_blob: bytes) -> np.ndarray:
         raise ValueError("raster decoder needs G = 1")
     if hdr["numerics"] != container.ORACLE_NUMERICS:
         raise container.CorruptContainer("numerics revision %d is not the oracle's" % hdr["numerics"])
-    layers = model_io.load(model_blob)
+    layers = model_io.load_net(model_blob)
+    layers["meta_norm"] = window.meta_features(hdr["meta"], layers["meta_range"])
     prec = hdr["precision"]
     out = np.zeros((hdr["height"], hdr["width"]), np.uint8)
     for (x0, y0, tw, th), sts in _split_streams(hdr):

@@ -17,12 +17,17 @@ of DESIGN.md "Container", version 2), little-endian:
   off 24  32s SHA-256 of the model file
   off 56  u32 n_streams
   off 60  u32 sizes[n_streams]  (bytes per stream)
+  then    u32 n_meta, f32 meta[n_meta]: the image's raw metadata reals, stored
+          uncompressed (P:211 "We store the metadata uncompressed"; the
+          decoder re-reads them as network inputs)
   then the streams, tile-major (tiles row-major), group-major within a tile.
 """
 
 from __future__ import annotations
 
 import struct
+
+import numpy as np
 
 MAGIC = b"DLIC"
 VERSION = 2
@@ -47,12 +52,14 @@ def tiles(width: int, height: int, tile_w: int, tile_h: int):
 
 
 def write(width, height, precision, group_rows, tile_w, tile_h, model_sha, stream_bytes,
-          numerics=ORACLE_NUMERICS) -> bytes:
+          numerics=ORACLE_NUMERICS, meta=None) -> bytes:
     assert len(model_sha) == 32
     hdr = MAGIC + struct.pack("<BBBBIIHHHH", VERSION, precision, WINDOW_ID, 0, width, height,
                               tile_w, tile_h, group_rows, numerics)
     hdr += model_sha + struct.pack("<I", len(stream_bytes))
     hdr += b"".join(struct.pack("<I", len(s)) for s in stream_bytes)
+    m = np.asarray(meta if meta is not None else [], dtype="<f4").reshape(-1)
+    hdr += struct.pack("<I", len(m)) + m.tobytes()
     return hdr + b"".join(stream_bytes)
 
 
@@ -68,6 +75,14 @@ def parse(blob: bytes):
         raise CorruptContainer("size table")
     sizes = struct.unpack_from("<%dI" % n, blob, HEADER_FIXED)
     off = HEADER_FIXED + 4 * n
+    if len(blob) < off + 4:
+        raise CorruptContainer("metadata block")
+    (nm,) = struct.unpack_from("<I", blob, off)
+    if nm > 255 or len(blob) < off + 4 + 4 * nm:
+        raise CorruptContainer("metadata block")
+    meta = np.frombuffer(blob, dtype="<f4", count=nm, offset=off + 4).astype(np.float32)
+    off += 4 + 4 * nm
+    hdr_bytes = off
     streams = []
     for s in sizes:
         if s % 2 or off + s > len(blob):
@@ -77,4 +92,4 @@ def parse(blob: bytes):
     if off != len(blob):
         raise CorruptContainer("trailing bytes")
     return dict(width=w, height=h, precision=prec, tile_w=tw, tile_h=th, group_rows=g, numerics=num,
-                model_sha=sha, streams=streams, header_bytes=HEADER_FIXED + 4 * n)
+                model_sha=sha, streams=streams, header_bytes=hdr_bytes, meta=meta)

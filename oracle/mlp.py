@@ -13,6 +13,13 @@ Readings: hidden activation ReLU (R4); optional pooling omitted
 Layers are (W [in][out] float32, b [out] float32).  This module returns the
 LOGITS (pre-softmax); softmax lives in quant.py.
 
+Optional pooling ("two optional pooling layers between the first and
+second and the third and fourth layer"; semantics for flat vectors unstated,
+reading R11 = SPEC S:249): pool[i] = g > 0 averages contiguous groups of g
+units of layer i's activation (after ReLU) before layer i+1.  In the bf16
+definition the average is taken exactly over the bf16-rounded activations
+(no re-rounding of the average: it enters the next layer's exact products).
+
 Precision variants:
   forward_fp64   exact reference (fp64 throughout);
   forward_fp32   numpy float32 matmul (checks fp32 is within 1e-6 of fp64);
@@ -42,23 +49,35 @@ def flops_per_pixel(dims) -> int:
     return 2 * sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1))
 
 
-def forward_fp64(layers, x: np.ndarray) -> np.ndarray:
+def avg_pool(h: np.ndarray, g: int) -> np.ndarray:
+    """Average over contiguous groups of g units (last axis), exact in fp64."""
+    if not g:
+        return h
+    h = np.asarray(h, dtype=np.float64)
+    return h.reshape(h.shape[:-1] + (h.shape[-1] // g, g)).sum(-1) / g
+
+
+def forward_fp64(layers, x: np.ndarray, pool=None) -> np.ndarray:
     h = np.asarray(x, dtype=np.float64)
     n = len(layers)
     for i, (w, b) in enumerate(layers):
         h = h @ np.asarray(w, np.float64) + np.asarray(b, np.float64)
         if i < n - 1:
             h = np.maximum(h, 0.0)
+            if pool is not None:
+                h = avg_pool(h, pool[i])
     return h
 
 
-def forward_fp32(layers, x: np.ndarray) -> np.ndarray:
+def forward_fp32(layers, x: np.ndarray, pool=None) -> np.ndarray:
     h = np.asarray(x, dtype=np.float32)
     n = len(layers)
     for i, (w, b) in enumerate(layers):
         h = h @ np.asarray(w, np.float32) + np.asarray(b, np.float32)
         if i < n - 1:
             h = np.maximum(h, np.float32(0))
+            if pool is not None and pool[i]:
+                h = avg_pool(h, pool[i]).astype(np.float32)
     return h
 
 
@@ -73,9 +92,10 @@ def bf16_round(a: np.ndarray) -> np.ndarray:
     return u.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
-def forward_bf16(layers, x: np.ndarray) -> np.ndarray:
+def forward_bf16(layers, x: np.ndarray, pool=None) -> np.ndarray:
     """bf16 operands, exact (fp64) accumulation; activations re-rounded to
-    bf16 after bias+ReLU computed in fp32 (the GPU epilogue's precision)."""
+    bf16 after bias+ReLU computed in fp32 (the GPU epilogue's precision);
+    pooling (if any) averages the bf16 activations exactly."""
     h = bf16_round(np.asarray(x, dtype=np.float64))
     n = len(layers)
     for i, (w, b) in enumerate(layers):
@@ -83,15 +103,17 @@ def forward_bf16(layers, x: np.ndarray) -> np.ndarray:
         z = (acc.astype(np.float32) + np.asarray(b, np.float32)).astype(np.float64)
         if i < n - 1:
             h = bf16_round(np.maximum(z, 0.0))
+            if pool is not None:
+                h = avg_pool(h, pool[i])
         else:
             h = z
     return h
 
 
-def logits_path(layers, x: np.ndarray, precision: int) -> np.ndarray:
+def logits_path(layers, x: np.ndarray, precision: int, pool=None) -> np.ndarray:
     """Logits used by the oracle codec: fp64 (0) or bf16 emulation (1), as fp32."""
     if precision == 0:
-        return forward_fp64(layers, x).astype(np.float32)
+        return forward_fp64(layers, x, pool).astype(np.float32)
     if precision == 1:
-        return forward_bf16(layers, x).astype(np.float32)
+        return forward_bf16(layers, x, pool).astype(np.float32)
     raise ValueError("precision")

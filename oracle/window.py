@@ -67,3 +67,26 @@ def gather_many(img: np.ndarray, rows: np.ndarray, cols: np.ndarray, fill: int =
 def features(x: np.ndarray) -> np.ndarray:
     """Network inputs v / 256 (reading R2; exact in fp32 and bf16)."""
     return np.asarray(x, dtype=np.float64) / 256.0
+
+
+def meta_features(meta, meta_range) -> np.ndarray:
+    """Metadata features ("including metadata as a feature"; reading R12 =
+    SPEC S:252): raw per-image reals m_k min-max normalised with the model's
+    constants, (m_k - min_k) / (max_k - min_k), in IEEE binary32 (each step
+    rounded once), appended after the 78 pixel features.  Returns float64
+    holding the binary32 values."""
+    m = np.asarray(meta if meta is not None else [], dtype=np.float32).reshape(-1)
+    if len(m) != len(meta_range):
+        raise ValueError("metadata count %d != model's %d" % (len(m), len(meta_range)))
+    lo = np.array([r[0] for r in meta_range], dtype=np.float32)
+    hi = np.array([r[1] for r in meta_range], dtype=np.float32)
+    return ((m - lo) / (hi - lo)).astype(np.float32).astype(np.float64)
+
+
+def net_inputs(img: np.ndarray, rows, cols, meta_norm=None) -> np.ndarray:
+    """Network input rows: 78 window features, then the metadata features
+    (identical for every pixel of the image)."""
+    x = features(gather_many(img, rows, cols))
+    if meta_norm is None or len(meta_norm) == 0:
+        return x
+    return np.concatenate([x, np.broadcast_to(np.asarray(meta_norm, np.float64), (x.shape[0], len(meta_norm)))], 1)

@@ -31,15 +31,20 @@ c_u8p = ctypes.POINTER(ctypes.c_uint8)
 c_u8pp = ctypes.POINTER(c_u8p)
 
 
+MAX_META = 8
+
+
 class dlic_opts(ctypes.Structure):
     _fields_ = [("precision", ctypes.c_uint32), ("group_rows", ctypes.c_uint32),
-                ("tile_w", ctypes.c_uint32), ("tile_h", ctypes.c_uint32)]
+                ("tile_w", ctypes.c_uint32), ("tile_h", ctypes.c_uint32),
+                ("n_meta", ctypes.c_uint32), ("meta", ctypes.POINTER(ctypes.c_float))]
 
 
 class dlic_header(ctypes.Structure):
     _fields_ = [("width", ctypes.c_uint32), ("height", ctypes.c_uint32), ("precision", ctypes.c_uint32),
                 ("group_rows", ctypes.c_uint32), ("tile_w", ctypes.c_uint32), ("tile_h", ctypes.c_uint32),
                 ("n_streams", ctypes.c_uint32), ("n_units", ctypes.c_uint32), ("numerics", ctypes.c_uint32),
+                ("n_meta", ctypes.c_uint32), ("meta", ctypes.c_float * MAX_META),
                 ("model_sha256", ctypes.c_uint8 * 32),
                 ("payload_bytes", ctypes.c_uint64), ("header_bytes", ctypes.c_uint64)]
 
@@ -127,8 +132,16 @@ def _check(s):
         raise DlicError(s, _L().dlic_last_error().decode(errors="replace"))
 
 
-def _opts(precision=PREC_BF16, group_rows=32, tile=(0, 0)):
-    return dlic_opts(precision, group_rows, tile[0], tile[1])
+def _opts(precision=PREC_BF16, group_rows=32, tile=(0, 0), meta=None):
+    """meta: raw metadata reals, (n_meta,) for one image or (n, n_meta) for a
+    batch.  The returned struct keeps the float32 array alive."""
+    o = dlic_opts(precision, group_rows, tile[0], tile[1], 0, None)
+    if meta is not None:
+        m = np.ascontiguousarray(np.asarray(meta, dtype=np.float32))
+        o._meta_keep = m
+        o.n_meta = m.shape[-1] if m.ndim else 1
+        o.meta = m.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+    return o
 
 
 def _take(ptr, n) -> bytes:
@@ -193,13 +206,14 @@ def dlic_model_blob_check(blob: bytes) -> bytes:
 
 
 # ------------------------------------------------------------------ codec
-def dlic_encode(model: Model, img: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0)) -> bytes:
+def dlic_encode(model: Model, img: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0),
+                meta=None) -> bytes:
     img = np.ascontiguousarray(img, dtype=np.uint8)
     assert img.ndim == 2
     h, w = img.shape
     out = c_u8p()
     n = ctypes.c_size_t()
-    o = _opts(precision, group_rows, tile)
+    o = _opts(precision, group_rows, tile, meta)
     _check(_L().dlic_encode(model.handle, img.ctypes.data, w, h, w, ctypes.byref(o), ctypes.byref(out),
                             ctypes.byref(n)))
     return _take(out, n.value)
@@ -208,8 +222,9 @@ def dlic_encode(model: Model, img: np.ndarray, precision=PREC_BF16, group_rows=3
 def dlic_peek(bits: bytes) -> dict:
     hd = dlic_header()
     _check(_L().dlic_peek(bits, len(bits), ctypes.byref(hd)))
-    d = {k: getattr(hd, k) for k, _ in dlic_header._fields_ if k != "model_sha256"}
+    d = {k: getattr(hd, k) for k, _ in dlic_header._fields_ if k not in ("model_sha256", "meta")}
     d["model_sha256"] = bytes(hd.model_sha256)
+    d["meta"] = np.array(hd.meta[:hd.n_meta], dtype=np.float32)
     return d
 
 
@@ -220,14 +235,15 @@ def dlic_decode(model: Model, bits: bytes) -> np.ndarray:
     return img
 
 
-def dlic_encode_batch(model: Model, imgs: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0)):
-    """imgs (n, H, W) u8 host -> (blob, sizes): the n containers back to back."""
+def dlic_encode_batch(model: Model, imgs: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0), meta=None):
+    """imgs (n, H, W) u8 host -> (blob, sizes): the n containers back to back.
+    meta: (n, n_meta) raw metadata reals per image."""
     imgs = np.ascontiguousarray(imgs, dtype=np.uint8)
     n, h, w = imgs.shape
     out = c_u8p()
     tot = ctypes.c_size_t()
     sizes = np.zeros(n, np.uint64)
-    o = _opts(precision, group_rows, tile)
+    o = _opts(precision, group_rows, tile, meta)
     _check(_L().dlic_encode_batch(model.handle, imgs.ctypes.data, n, w, h, ctypes.byref(o), ctypes.byref(out),
                                   ctypes.byref(tot), sizes.ctypes.data))
     return _take(out, tot.value), [int(x) for x in sizes]
@@ -245,19 +261,19 @@ def dlic_decode_batch(model: Model, blob: bytes, sizes) -> np.ndarray:
     return imgs
 
 
-def dlic_max_container_bytes(width, height, precision=PREC_BF16, group_rows=32, tile=(0, 0)) -> int:
-    o = _opts(precision, group_rows, tile)
+def dlic_max_container_bytes(width, height, precision=PREC_BF16, group_rows=32, tile=(0, 0), meta=None) -> int:
+    o = _opts(precision, group_rows, tile, meta)
     return int(_L().dlic_max_container_bytes(width, height, ctypes.byref(o)))
 
 
 # ------------------------------------------------------------------ parity taps
 def dlic_rans_encode_tables(fc: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0),
-                            model_sha: bytes | None = None) -> bytes:
+                            model_sha: bytes | None = None, meta=None) -> bytes:
     fc = np.ascontiguousarray(fc, dtype=np.uint32)
     h, w = fc.shape
     out = c_u8p()
     n = ctypes.c_size_t()
-    o = _opts(precision, group_rows, tile)
+    o = _opts(precision, group_rows, tile, meta)
     sha = ctypes.create_string_buffer(model_sha, 32) if model_sha else None
     _check(_L().dlic_rans_encode_tables(fc.ctypes.data, w, h, ctypes.byref(o), sha, ctypes.byref(out),
                                         ctypes.byref(n)))
@@ -274,7 +290,7 @@ def dlic_rans_decode_tables(bits: bytes, freq_tables: np.ndarray) -> np.ndarray:
 
 
 def dlic_debug_mlp(model: Model, img: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0),
-                   logits=True, probs=True, freqs=True, fc=True) -> dict:
+                   logits=True, probs=True, freqs=True, fc=True, meta=None) -> dict:
     img = np.ascontiguousarray(img, dtype=np.uint8)
     h, w = img.shape
     out = {}
@@ -282,7 +298,7 @@ def dlic_debug_mlp(model: Model, img: np.ndarray, precision=PREC_BF16, group_row
     pb = np.empty((h, w, 256), np.float32) if probs else None
     fq = np.empty((h, w, 256), np.uint16) if freqs else None
     f = np.empty((h, w), np.uint32) if fc else None
-    o = _opts(precision, group_rows, tile)
+    o = _opts(precision, group_rows, tile, meta)
     _check(_L().dlic_debug_mlp(model.handle, img.ctypes.data, w, h, ctypes.byref(o),
                                lg.ctypes.data if logits else None, pb.ctypes.data if probs else None,
                                fq.ctypes.data if freqs else None, f.ctypes.data if fc else None))
@@ -300,19 +316,19 @@ def _stream_handle(stream):
 
 
 def dlic_encode_batch_device(model: Model, d_imgs, precision=PREC_BF16, group_rows=32, tile=(0, 0),
-                             d_out=None, d_sizes=None, stream=None):
+                             d_out=None, d_sizes=None, stream=None, meta=None):
     """d_imgs: torch uint8 CUDA tensor (n, H, W).  Returns (d_out, d_sizes, stride):
     container i occupies d_out[i*stride : i*stride + d_sizes[i]]."""
     import torch
     n, h, w = d_imgs.shape
-    stride = dlic_max_container_bytes(w, h, precision, group_rows, tile)
+    stride = dlic_max_container_bytes(w, h, precision, group_rows, tile, meta)
     if stride == 0:
         raise DlicError(1, "unsupported options")
     if d_out is None:
         d_out = torch.empty(n * stride, dtype=torch.uint8, device=d_imgs.device)
     if d_sizes is None:
         d_sizes = torch.empty(n, dtype=torch.int64, device=d_imgs.device)
-    o = _opts(precision, group_rows, tile)
+    o = _opts(precision, group_rows, tile, meta)
     _check(_L().dlic_encode_batch_device(model.handle, _vp(d_imgs.data_ptr()), n, w, h, ctypes.byref(o),
                                          _vp(d_out.data_ptr()), d_out.numel(), _vp(d_sizes.data_ptr()),
                                          _stream_handle(stream)))
@@ -332,6 +348,9 @@ def dlic_decode_batch_device(model: Model, d_bits, h_offsets, h_lengths, header:
     for k, _ in dlic_header._fields_:
         if k == "model_sha256":
             ctypes.memmove(hd.model_sha256, header["model_sha256"], 32)
+        elif k == "meta":
+            for i, v in enumerate(header.get("meta", [])):
+                hd.meta[i] = float(v)
         else:
             setattr(hd, k, header[k])
     _check(_L().dlic_decode_batch_device(model.handle, _vp(d_bits.data_ptr()), offs.ctypes.data, lens.ctypes.data,
@@ -341,35 +360,35 @@ def dlic_decode_batch_device(model: Model, d_bits, h_offsets, h_lengths, header:
 
 
 # ------------------------------------------------------------------ unit ranges (one image across GPUs)
-def dlic_unit_streams(width, height, unit_lo, unit_hi, precision=PREC_BF16, group_rows=32, tile=(0, 0)):
+def dlic_unit_streams(width, height, unit_lo, unit_hi, precision=PREC_BF16, group_rows=32, tile=(0, 0), meta=None):
     """(first_stream, n_streams) of units [unit_lo, unit_hi)."""
     a, b = ctypes.c_uint32(), ctypes.c_uint32()
-    o = _opts(precision, group_rows, tile)
+    o = _opts(precision, group_rows, tile, meta)
     _check(_L().dlic_unit_streams(width, height, ctypes.byref(o), unit_lo, unit_hi, ctypes.byref(a), ctypes.byref(b)))
     return a.value, b.value
 
 
 def dlic_encode_units(model: Model, img: np.ndarray, unit_lo: int, unit_hi: int, precision=PREC_BF16,
-                      group_rows=32, tile=(0, 0)):
+                      group_rows=32, tile=(0, 0), meta=None):
     """Code units [unit_lo, unit_hi) of img -> (payload bytes, stream sizes list)."""
     img = np.ascontiguousarray(img, dtype=np.uint8)
     h, w = img.shape
-    _, ns = dlic_unit_streams(w, h, unit_lo, unit_hi, precision, group_rows, tile)
+    _, ns = dlic_unit_streams(w, h, unit_lo, unit_hi, precision, group_rows, tile, meta)
     sizes = np.zeros(ns, np.uint32)
     out = c_u8p()
     n = ctypes.c_size_t()
-    o = _opts(precision, group_rows, tile)
+    o = _opts(precision, group_rows, tile, meta)
     _check(_L().dlic_encode_units(model.handle, img.ctypes.data, w, h, w, ctypes.byref(o), unit_lo, unit_hi,
                                   ctypes.byref(out), ctypes.byref(n), sizes.ctypes.data))
     return _take(out, n.value), [int(x) for x in sizes]
 
 
 def dlic_container_build(width, height, model_sha: bytes, stream_sizes, payload: bytes, precision=PREC_BF16,
-                         group_rows=32, tile=(0, 0)) -> bytes:
+                         group_rows=32, tile=(0, 0), meta=None) -> bytes:
     sz = np.ascontiguousarray(np.asarray(stream_sizes, dtype=np.uint32))
     out = c_u8p()
     n = ctypes.c_size_t()
-    o = _opts(precision, group_rows, tile)
+    o = _opts(precision, group_rows, tile, meta)
     sha = ctypes.create_string_buffer(model_sha, 32)
     _check(_L().dlic_container_build(width, height, ctypes.byref(o), sha, sz.ctypes.data, len(sz), payload,
                                      len(payload), ctypes.byref(out), ctypes.byref(n)))

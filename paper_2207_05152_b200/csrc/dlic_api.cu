@@ -30,11 +30,14 @@ struct dlic_model {
   std::vector<uint8_t> blob;  // the "DLICMDL1" bytes
   uint8_t sha[32];
   std::vector<uint32_t> dims;
-  bool p100k = false;
+  bool p100k = false;  // topology the GPU engines run (see dlic_model_load)
+  uint32_t n_meta = 0;
   uint8_t* d_wimg = nullptr;
   float* d_bias = nullptr;
   float* d_w32 = nullptr;
-  DevWeights dw() const { return DevWeights{d_wimg, d_bias, d_w32}; }
+  float* d_wmeta = nullptr;  // metadata rows of W1 [n_meta][HID] fp32
+  float* d_range = nullptr;  // (min, max) per metadata feature
+  DevWeights dw(const float* b1img = nullptr) const { return DevWeights{d_wimg, d_bias, d_w32, b1img}; }
 };
 
 namespace {
@@ -174,6 +177,8 @@ uint16_t rd16(const uint8_t* p) { return (uint16_t)(p[0] | (p[1] << 8)); }
 struct ParsedModel {
   std::vector<uint32_t> dims;
   std::vector<std::vector<float>> W, b;
+  std::vector<uint32_t> pool;        // pooling group after each layer (0 = none)
+  std::vector<float> meta_range;     // (min, max) per metadata feature
 };
 
 dlic_status parse_model(const uint8_t* d, size_t len, ParsedModel& pm, uint8_t sha_out[32]) {
@@ -189,10 +194,16 @@ dlic_status parse_model(const uint8_t* d, size_t len, ParsedModel& pm, uint8_t s
   for (uint32_t l = 0; l < nl; ++l) {
     if (off + 10 > body) return fail(DLIC_E_CORRUPT_MODEL, "truncated layer header");
     const uint32_t in = rd32(d + off), outd = rd32(d + off + 4);
+    const uint32_t g = d[off + 9];
     off += 10;
+    if (l > 0) {  // dims chain after the previous layer's pooling
+      const uint32_t gp = pm.pool.back() ? pm.pool.back() : 1u;
+      if (pm.dims.back() % gp != 0 || pm.dims.back() / gp != in)
+        return fail(DLIC_E_CORRUPT_MODEL, "layer dims do not chain");
+    }
     if (l == 0) pm.dims.push_back(in);
-    else if (pm.dims.back() != in) return fail(DLIC_E_CORRUPT_MODEL, "layer dims do not chain");
     pm.dims.push_back(outd);
+    pm.pool.push_back(g);
     const size_t nw = (size_t)in * outd;
     if (in == 0 || outd == 0 || off + 4 * (nw + outd) > body) return fail(DLIC_E_CORRUPT_MODEL, "truncated weights");
     std::vector<float> w(nw), bb(outd);
@@ -205,6 +216,12 @@ dlic_status parse_model(const uint8_t* d, size_t len, ParsedModel& pm, uint8_t s
   }
   if (off + 2 > body) return fail(DLIC_E_CORRUPT_MODEL, "truncated meta");
   const uint32_t nmeta = rd16(d + off);
+  if (off + 2 + 8 * (size_t)nmeta > body) return fail(DLIC_E_CORRUPT_MODEL, "truncated metadata ranges");
+  for (uint32_t k = 0; k < 2 * nmeta; ++k) {
+    float v;
+    memcpy(&v, d + off + 2 + 4 * k, 4);
+    pm.meta_range.push_back(v);
+  }
   off += 2 + 8 * (size_t)nmeta;
   if (off != body) return fail(DLIC_E_CORRUPT_MODEL, "model length");
   if (sha_out) memcpy(sha_out, h, 32);
@@ -218,16 +235,45 @@ uint16_t bf16_bits(float f) {
   return u;
 }
 
-dlic_status upload_model(dlic_model* m, const ParsedModel& pm) {
-  const uint32_t want[7] = {KIN, HID, HID, HID, HID, HID, NOUT};
-  m->p100k = pm.dims.size() == 7 && std::equal(pm.dims.begin(), pm.dims.end(), want);
-  m->dims = pm.dims;
+// Fold a pooled network into the engines' shape: average pooling of g units
+// after layer l is linear, so layer l+1 with K = 128/g inputs becomes an
+// equivalent layer with K = 128 whose row k is W[k / g] / g (exact in fp32 and
+// bf16: g is a power of two).  Returns false for topologies outside the engines.
+static bool engine_weights(const ParsedModel& pm, std::vector<std::vector<float>>& W, uint32_t& n_meta) {
+  if (pm.W.size() != (size_t)NLAYER) return false;
+  if (pm.dims[0] < (uint32_t)KIN || pm.dims[0] > (uint32_t)KIN + DLIC_MAX_META) return false;
+  n_meta = pm.dims[0] - KIN;
+  if (pm.meta_range.size() != 2 * (size_t)n_meta) return false;
+  for (int l = 0; l < NLAYER; ++l)
+    if (pm.dims[l + 1] != (uint32_t)layer_n(l)) return false;  // outputs 128 x5, 256
+  if (pm.pool[NLAYER - 1] != 0) return false;
+  W.assign(NLAYER, {});
+  W[0] = pm.W[0];
+  for (int l = 1; l < NLAYER; ++l) {
+    const uint32_t g = pm.pool[l - 1] ? pm.pool[l - 1] : 1u;
+    if (g & (g - 1)) return false;  // powers of two only (exact 1/g)
+    const uint32_t N = (uint32_t)layer_n(l);
+    W[l].resize((size_t)HID * N);
+    for (uint32_t k = 0; k < (uint32_t)HID; ++k)
+      for (uint32_t n = 0; n < N; ++n) W[l][(size_t)k * N + n] = pm.W[l][(size_t)(k / g) * N + n] / (float)g;
+  }
+  return true;
+}
+
+dlic_status upload_model(dlic_model* m, const ParsedModel& pm_in) {
+  m->dims = pm_in.dims;
+  std::vector<std::vector<float>> Wf;
+  uint32_t n_meta = 0;
+  m->p100k = engine_weights(pm_in, Wf, n_meta);
   if (!m->p100k) return DLIC_OK;  // loadable; GPU engines refuse it at encode/decode
+  m->n_meta = n_meta;
+  ParsedModel pm = pm_in;
+  pm.W = Wf;  // pooling folded; W1 keeps its KIN + n_meta rows (the packers below read rows < KIN)
   // bf16 UMMA image: layer l, element (n, k) of B = W^T at
   // (k/8)*(N/8)*128 + (n/8)*128 + (n%8)*16 + (k%8)*2   (K-major, no swizzle)
   std::vector<uint8_t> img(WIMG_BYTES, 0);
   for (int l = 0; l < NLAYER; ++l) {
-    const int K = layer_k(l), N = layer_n(l), Kr = (int)pm.dims[l];
+    const int K = layer_k(l), N = layer_n(l), Kr = l == 0 ? KIN : K;  // W1's metadata rows: d_wmeta
     for (int k = 0; k < K; ++k)
       for (int n = 0; n < N; ++n) {
         const int kt = l == 0 ? kpos_tap(k) : k;  // layer 1: the engine's K order
@@ -259,6 +305,15 @@ dlic_status upload_model(dlic_model* m, const ParsedModel& pm) {
     memcpy(&w32[f32_off(l)], pm.W[l].data(), 4 * (size_t)K * N);
     memcpy(&w32[f32_off(l) + (size_t)K * N], pm.b[l].data(), 4 * (size_t)N);
   }
+  if (n_meta) {  // metadata rows of W1 and their normalisation constants
+    std::vector<float> wm((size_t)n_meta * HID);
+    for (uint32_t k = 0; k < n_meta; ++k)
+      for (int n = 0; n < HID; ++n) wm[(size_t)k * HID + n] = pm.W[0][(size_t)(KIN + k) * HID + n];
+    CUDA_TRY(cudaMalloc(&m->d_wmeta, wm.size() * 4));
+    CUDA_TRY(cudaMalloc(&m->d_range, pm.meta_range.size() * 4));
+    CUDA_TRY(cudaMemcpy(m->d_wmeta, wm.data(), wm.size() * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(m->d_range, pm.meta_range.data(), pm.meta_range.size() * 4, cudaMemcpyHostToDevice));
+  }
   CUDA_TRY(cudaMalloc(&m->d_wimg, WIMG_BYTES));
   CUDA_TRY(cudaMalloc(&m->d_bias, bias.size() * 4));
   CUDA_TRY(cudaMalloc(&m->d_w32, w32.size() * 4));
@@ -270,9 +325,10 @@ dlic_status upload_model(dlic_model* m, const ParsedModel& pm) {
 
 // ---------------------------------------------------------------- planning
 dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Plan& p) {
-  dlic_opts d = {DLIC_PREC_BF16, 32, 0, 0};
+  dlic_opts d = {DLIC_PREC_BF16, 32, 0, 0, 0, nullptr};
   if (o) d = *o;
   if (d.group_rows == 0) d.group_rows = 32;
+  if (d.n_meta > DLIC_MAX_META) return fail(DLIC_E_INVALID_ARG, "more than DLIC_MAX_META metadata reals");
   if (W == 0 || H == 0 || n == 0) return fail(DLIC_E_INVALID_ARG, "empty image or batch");
   if (W > 65535 * 16 || H > 65535 * 16) return fail(DLIC_E_INVALID_ARG, "image too large");
   if (d.precision > 1) return fail(DLIC_E_INVALID_ARG, "precision must be 0 (fp32) or 1 (bf16)");
@@ -299,7 +355,8 @@ dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Pl
   if (dec_smem_bytes(d.precision, std::max(p.gpt, (H - (p.nty - 1) * p.th + p.G - 1) / p.G)) > dec_smem_limit())
     return fail(DLIC_E_INVALID_ARG, "too many row groups per unit for the decoder's shared memory: raise group_rows or tile");
   p.cap_words = 2 * p.G + p.G * p.tw;
-  p.hdr_bytes = HDR_FIXED + 4 * p.spi;
+  p.n_meta = d.n_meta;
+  p.hdr_bytes = HDR_FIXED + 4 * p.spi + 4 + 4 * p.n_meta;  // + the metadata block
   p.u_lo = 0;
   p.u_cnt = n * p.upi;
   p.s_lo = 0;
@@ -323,9 +380,19 @@ dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Pl
 
 dlic_status check_model_gpu(const dlic_model* m) {
   if (!m) return fail(DLIC_E_INVALID_ARG, "null model");
-  if (!m->p100k) return fail(DLIC_E_UNSUPPORTED_MODEL, "GPU engines implement 78->128x5->256 (P100K)");
+  if (!m->p100k)
+    return fail(DLIC_E_UNSUPPORTED_MODEL, "GPU engines implement (78 + n_meta <= 8)->128x5->256 with optional "
+                                          "power-of-two average pooling after hidden layers");
   return check_device(m->device);
 }
+
+// Per-image layer-1 biases with the metadata inputs folded in (k_meta_bias),
+// or null when the model has none.  Raw reals from the host array `h_meta`
+// ([n_img][n_meta], encode) or from the containers' metadata blocks on the
+// device (`d_bits` + `d_cont_off`, decode).
+dlic_status meta_bias(const dlic_model* m, const Plan& p, const float* h_meta, const uint8_t* d_bits,
+                      const uint64_t* d_cont_off, cudaStream_t st, Scratch& sc, const float** out,
+                      float** d_meta_out = nullptr);
 
 // Restrict p to units [lo, hi) of image 0 (unit-range calls).
 dlic_status restrict_units(Plan& p, uint32_t lo, uint32_t hi) {
@@ -391,6 +458,13 @@ dlic_status peek(const uint8_t* b, size_t len, dlic_header* h, std::vector<uint3
     tot += z;
     if (sizes) (*sizes)[s] = z;
   }
+  // metadata block: u32 n, f32 raw reals
+  if (o.header_bytes + 4 > len) return fail(DLIC_E_CORRUPT_CONTAINER, "metadata block");
+  o.n_meta = rd32(b + o.header_bytes);
+  if (o.n_meta > DLIC_MAX_META || o.header_bytes + 4 + 4ull * o.n_meta > len)
+    return fail(DLIC_E_CORRUPT_CONTAINER, "metadata block");
+  for (uint32_t k = 0; k < o.n_meta; ++k) memcpy(&o.meta[k], b + o.header_bytes + 4 + 4 * k, 4);
+  o.header_bytes += 4 + 4ull * o.n_meta;
   if (o.header_bytes + tot != len) return fail(DLIC_E_CORRUPT_CONTAINER, "container length");
   o.payload_bytes = tot;
   const bool tiled = o.tile_w && o.tile_h;
@@ -407,6 +481,8 @@ dlic_opts opts_of(const dlic_header& h) {
   o.group_rows = h.group_rows;
   o.tile_w = h.tile_w;
   o.tile_h = h.tile_h;
+  o.n_meta = h.n_meta;
+  o.meta = h.meta;  // points into h
   return o;
 }
 
@@ -422,9 +498,49 @@ cudaError_t h2d(void* dst, const void* src, size_t n, cudaStream_t st) {
   return cudaMemcpyAsync(dst, pin, n, cudaMemcpyHostToDevice, st);
 }
 
+// metadata staging: a pageable copy would block the host mid-pipeline; the
+// event marks the buffer's last copy, so reuse waits for that copy only
+thread_local Pinned g_pin_meta;
+thread_local cudaEvent_t g_pin_meta_ev = nullptr;
+
+dlic_status meta_bias(const dlic_model* m, const Plan& p, const float* h_meta, const uint8_t* d_bits,
+                      const uint64_t* d_cont_off, cudaStream_t st, Scratch& sc, const float** out,
+                      float** d_meta_out) {
+  *out = nullptr;
+  if (d_meta_out) *d_meta_out = nullptr;
+  if (p.n_meta != m->n_meta)
+    return fail(DLIC_E_SHAPE_MISMATCH, "metadata count " + std::to_string(p.n_meta) + " != the model's " +
+                                           std::to_string(m->n_meta));
+  if (m->n_meta == 0) return DLIC_OK;
+  if (!d_bits && !h_meta) return fail(DLIC_E_INVALID_ARG, "the model needs metadata (opts.meta)");
+  float* d_out;
+  float* d_meta = nullptr;
+  CUDA_TRY(sc.alloc(&d_out, 4ull * p.n_img * HID));
+  if (!d_bits) {
+    const size_t nb = 4ull * p.n_img * p.n_meta;
+    CUDA_TRY(sc.alloc(&d_meta, nb));
+    void* pin = g_pin_meta.get(nb);
+    if (pin) {
+      if (!g_pin_meta_ev) CUDA_TRY(cudaEventCreateWithFlags(&g_pin_meta_ev, cudaEventDisableTiming));
+      else CUDA_TRY(cudaEventSynchronize(g_pin_meta_ev));  // the buffer's previous copy is done
+      memcpy(pin, h_meta, nb);
+      CUDA_TRY(cudaMemcpyAsync(d_meta, pin, nb, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaEventRecord(g_pin_meta_ev, st));
+    } else {
+      CUDA_TRY(cudaMemcpyAsync(d_meta, h_meta, nb, cudaMemcpyHostToDevice, st));
+    }
+    if (d_meta_out) *d_meta_out = d_meta;
+  }
+  CUDA_TRY(launch_meta_bias(p.n_img, p.n_meta, d_meta, d_bits, d_cont_off, HDR_FIXED + 4u * p.spi + 4u, m->d_range,
+                            m->d_wmeta, m->d_bias, p.precision, d_out, st));
+  *out = d_out;
+  return DLIC_OK;
+}
+
 // encode pipeline on device buffers (shared by dlic_encode and the batch API)
 dlic_status run_encode(const dlic_model* m, const Plan& p, const uint8_t* d_imgs, uint8_t* d_out, uint64_t stride,
-                       uint64_t* d_sizes, cudaStream_t st, Scratch& sc, uint32_t** words_out = nullptr) {
+                       uint64_t* d_sizes, cudaStream_t st, Scratch& sc, const float* h_meta,
+                       uint32_t** words_out = nullptr) {
   uint32_t* d_fc;
   uint16_t* d_scr;
   uint32_t* d_words;
@@ -435,14 +551,18 @@ dlic_status run_encode(const dlic_model* m, const Plan& p, const uint8_t* d_imgs
   CUDA_TRY(sc.alloc(&d_scr, 2ull * p.cap_words * ns));
   CUDA_TRY(sc.alloc(&d_words, 4 * ns));
   CUDA_TRY(sc.alloc(&d_dst, 8 * ns));
+  const float* b1img = nullptr;
+  float* d_meta = nullptr;  // raw reals, also for the containers' metadata blocks
+  dlic_status s = meta_bias(m, p, h_meta, nullptr, nullptr, st, sc, &b1img, &d_meta);
+  if (s != DLIC_OK) return s;
   ev_begin("mlp", st);
-  CUDA_TRY(launch_enc_mlp(p, m->dw(), d_imgs, d_fc, nullptr, nullptr, nullptr, st, num_sms(m->device)));
+  CUDA_TRY(launch_enc_mlp(p, m->dw(b1img), d_imgs, d_fc, nullptr, nullptr, nullptr, st, num_sms(m->device)));
   ev_end("mlp", st);
   ev_begin("rans_enc", st);
   CUDA_TRY(launch_rans_enc(p, d_fc, d_scr, d_words, st));
   ev_end("rans_enc", st);
   ev_begin("compact", st);
-  CUDA_TRY(launch_container(p, m->sha, d_words, d_scr, d_out, stride, d_sizes, d_dst, st, words_out != nullptr));
+  CUDA_TRY(launch_container(p, m->sha, d_words, d_scr, d_out, stride, d_sizes, d_dst, st, words_out != nullptr, d_meta));
   ev_end("compact", st);
   if (words_out) *words_out = d_words;
   return DLIC_OK;
@@ -535,6 +655,8 @@ void dlic_model_free(dlic_model* m) {
   if (m->d_wimg) cudaFree(m->d_wimg);
   if (m->d_bias) cudaFree(m->d_bias);
   if (m->d_w32) cudaFree(m->d_w32);
+  if (m->d_wmeta) cudaFree(m->d_wmeta);
+  if (m->d_range) cudaFree(m->d_range);
   delete m;
 }
 
@@ -579,7 +701,7 @@ dlic_status dlic_encode(const dlic_model* m, const uint8_t* img, uint32_t width,
   } else {
     CUDA_TRY(cudaMemcpy2DAsync(d_img, width, img, row_stride, width, height, cudaMemcpyHostToDevice, st));
   }
-  s = run_encode(m, p, d_img, d_out, p.max_container, d_size, st, sc);
+  s = run_encode(m, p, d_img, d_out, p.max_container, d_size, st, sc, opts ? opts->meta : nullptr);
   if (s != DLIC_OK) return s;
   uint64_t* hs = static_cast<uint64_t*>(g_pin_out.get(p.max_container + 64));
   if (!hs) return fail(DLIC_E_OUT_OF_MEMORY, "pinned staging");
@@ -671,7 +793,10 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
       CUDA_TRY(cudaMemsetAsync(d_prof, 0, 300 * 8, st));
     }
     ev_begin("decode", st);
-    CUDA_TRY(launch_decode(p, m->dw(), d_bits, d_meta, d_sbase, d_slen, d_img, d_status, st, d_prof));
+    const float* b1img = nullptr;  // metadata re-read from the container (device)
+    s = meta_bias(m, p, nullptr, d_bits, d_meta, st, sc, &b1img);
+    if (s != DLIC_OK) return s;
+    CUDA_TRY(launch_decode(p, m->dw(b1img), d_bits, d_meta, d_sbase, d_slen, d_img, d_status, st, d_prof));
     ev_end("decode", st);
     if (prof) {
       unsigned long long hp[40];
@@ -750,7 +875,14 @@ dlic_status dlic_rans_encode_tables(const uint32_t* fc, uint32_t width, uint32_t
   CUDA_TRY(sc.alloc(&d_out, p.max_container));
   CUDA_TRY(cudaMemcpyAsync(d_fc, fcu.data(), 4ull * width * height, cudaMemcpyHostToDevice, st));
   CUDA_TRY(launch_rans_enc(p, d_fc, d_scr, d_words, st));
-  CUDA_TRY(launch_container(p, model_sha256, d_words, d_scr, d_out, p.max_container, d_size, d_dst, st));
+  float* d_mraw = nullptr;
+  if (p.n_meta) {
+    if (!opts->meta) return fail(DLIC_E_INVALID_ARG, "opts.n_meta > 0 but opts.meta is null");
+    CUDA_TRY(sc.alloc(&d_mraw, 4ull * p.n_meta));
+    CUDA_TRY(cudaMemcpyAsync(d_mraw, opts->meta, 4ull * p.n_meta, cudaMemcpyHostToDevice, st));
+  }
+  CUDA_TRY(launch_container(p, model_sha256, d_words, d_scr, d_out, p.max_container, d_size, d_dst, st, false,
+                            d_mraw));
   uint64_t n = 0;
   CUDA_TRY(cudaMemcpyAsync(&n, d_size, 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -784,7 +916,10 @@ dlic_status dlic_debug_mlp(const dlic_model* m, const uint8_t* img, uint32_t wid
   if (probs) CUDA_TRY(sc.alloc(&d_pb, 4 * npx * NOUT));
   if (freqs) CUDA_TRY(sc.alloc(&d_fq, 2 * npx * NOUT));
   CUDA_TRY(cudaMemcpyAsync(d_img, img, npx, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(launch_enc_mlp(p, m->dw(), d_img, d_fc, d_lg, d_pb, d_fq, st, num_sms(m->device)));
+  const float* b1img = nullptr;
+  s = meta_bias(m, p, opts ? opts->meta : nullptr, nullptr, nullptr, st, sc, &b1img);
+  if (s != DLIC_OK) return s;
+  CUDA_TRY(launch_enc_mlp(p, m->dw(b1img), d_img, d_fc, d_lg, d_pb, d_fq, st, num_sms(m->device)));
   if (logits) CUDA_TRY(cudaMemcpyAsync(logits, d_lg, 4 * npx * NOUT, cudaMemcpyDeviceToHost, st));
   if (probs) CUDA_TRY(cudaMemcpyAsync(probs, d_pb, 4 * npx * NOUT, cudaMemcpyDeviceToHost, st));
   if (freqs) CUDA_TRY(cudaMemcpyAsync(freqs, d_fq, 2 * npx * NOUT, cudaMemcpyDeviceToHost, st));
@@ -824,7 +959,7 @@ dlic_status dlic_encode_batch(const dlic_model* m, const uint8_t* imgs, uint32_t
   CUDA_TRY(sc.alloc(&d_out, p.max_container * n));
   CUDA_TRY(sc.alloc(&d_sizes, 8ull * n));
   CUDA_TRY(h2d(d_imgs, imgs, npx, st));
-  s = run_encode(m, p, d_imgs, d_out, p.max_container, d_sizes, st, sc);
+  s = run_encode(m, p, d_imgs, d_out, p.max_container, d_sizes, st, sc, opts ? opts->meta : nullptr);
   if (s != DLIC_OK) return s;
   std::vector<uint64_t> hs(n);
   CUDA_TRY(cudaMemcpyAsync(hs.data(), d_sizes, 8ull * n, cudaMemcpyDeviceToHost, st));
@@ -911,8 +1046,11 @@ dlic_status dlic_decode_batch(const dlic_model* m, const uint8_t* bits, size_t l
   CUDA_TRY(cudaMemcpyAsync(d_meta, meta.data(), 16ull * n, cudaMemcpyHostToDevice, st));
   CUDA_TRY(h2d(d_bits, bits, len, st));
   CUDA_TRY(launch_dec_prep(p, d_bits, d_meta, d_meta + n, d_sbase, d_slen, d_status, st));
+  const float* b1img = nullptr;
+  s = meta_bias(m, p, nullptr, d_bits, d_meta, st, sc, &b1img);
+  if (s != DLIC_OK) return s;
   ev_begin("decode", st);
-  CUDA_TRY(launch_decode(p, m->dw(), d_bits, d_meta, d_sbase, d_slen, d_imgs, d_status, st));
+  CUDA_TRY(launch_decode(p, m->dw(b1img), d_bits, d_meta, d_sbase, d_slen, d_imgs, d_status, st));
   ev_end("decode", st);
   uint8_t* ho = static_cast<uint8_t*>(g_pin_out.get(npx + 4ull * n + 64));
   if (!ho) return fail(DLIC_E_OUT_OF_MEMORY, "pinned staging");
@@ -943,7 +1081,7 @@ dlic_status dlic_encode_batch_device(const dlic_model* m, const uint8_t* d_imgs,
   if (s != DLIC_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   Scratch sc(st);
-  return run_encode(m, p, d_imgs, d_out, p.max_container, d_sizes, st, sc);
+  return run_encode(m, p, d_imgs, d_out, p.max_container, d_sizes, st, sc, opts ? opts->meta : nullptr);
 }
 
 dlic_status dlic_decode_batch_device(const dlic_model* m, const uint8_t* d_bits, const uint64_t* h_offsets,
@@ -976,8 +1114,11 @@ dlic_status dlic_decode_batch_device(const dlic_model* m, const uint8_t* d_bits,
   // k_dec_prep checks every header and stream size against its container's
   // length before k_decode reads a byte of payload (failures -> d_status[i])
   CUDA_TRY(launch_dec_prep(p, d_bits, d_meta, d_meta + n, d_sbase, d_slen, d_status, st));
+  const float* b1img = nullptr;  // every container's metadata block, re-read on the device
+  s = meta_bias(m, p, nullptr, d_bits, d_meta, st, sc, &b1img);
+  if (s != DLIC_OK) return s;
   ev_begin("decode", st);
-  CUDA_TRY(launch_decode(p, m->dw(), d_bits, d_meta, d_sbase, d_slen, d_imgs, d_status, st));
+  CUDA_TRY(launch_decode(p, m->dw(b1img), d_bits, d_meta, d_sbase, d_slen, d_imgs, d_status, st));
   ev_end("decode", st);
   return DLIC_OK;
 }
@@ -1020,7 +1161,7 @@ dlic_status dlic_encode_units(const dlic_model* m, const uint8_t* img, uint32_t 
   CUDA_TRY(sc.alloc(&d_out, p.max_container));
   CUDA_TRY(sc.alloc(&d_size, 8));
   CUDA_TRY(cudaMemcpy2DAsync(d_img, width, img, row_stride, width, height, cudaMemcpyHostToDevice, st));
-  s = run_encode(m, p, d_img, d_out, p.max_container, d_size, st, sc, &d_words);
+  s = run_encode(m, p, d_img, d_out, p.max_container, d_size, st, sc, opts ? opts->meta : nullptr, &d_words);
   if (s != DLIC_OK) return s;
   uint64_t n = 0;
   std::vector<uint32_t> words(p.s_cnt);
@@ -1047,6 +1188,7 @@ dlic_status dlic_container_build(uint32_t width, uint32_t height, const dlic_opt
   dlic_status s = make_plan(width, height, 1, opts, p);
   if (s != DLIC_OK) return s;
   if (n_streams != p.spi) return fail(DLIC_E_SHAPE_MISMATCH, "stream count does not match (width, height, opts)");
+  if (p.n_meta && !opts->meta) return fail(DLIC_E_INVALID_ARG, "opts.n_meta > 0 but opts.meta is null");
   uint64_t tot = 0;
   for (uint32_t i = 0; i < n_streams; ++i) {
     if (stream_sizes[i] & 1u) return fail(DLIC_E_CORRUPT_CONTAINER, "odd stream size");
@@ -1072,6 +1214,13 @@ dlic_status dlic_container_build(uint32_t width, uint32_t height, const dlic_opt
   memcpy(o + 24, model_sha256, 32);
   w32(56, p.spi);
   for (uint32_t i = 0; i < n_streams; ++i) w32(HDR_FIXED + 4 * (size_t)i, stream_sizes[i]);
+  const size_t mo = HDR_FIXED + 4 * (size_t)n_streams;  // metadata block
+  w32(mo, p.n_meta);
+  for (uint32_t k = 0; k < p.n_meta; ++k) {
+    uint32_t u;
+    memcpy(&u, &opts->meta[k], 4);
+    w32(mo + 4 + 4 * k, u);
+  }
   if (payload_len) memcpy(o + p.hdr_bytes, payload, payload_len);
   *out = o;
   *out_len = n;

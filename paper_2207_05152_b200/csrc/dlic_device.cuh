@@ -434,6 +434,7 @@ struct TcEngineT {
   uint32_t phase;
   uint32_t* xs;        // XS: shared exchange words [NXS_SMEM][NGRP][ROWS]
   uint32_t bar2;       // decoder (DEC_NSPLIT): completion of the hidden layers' columns [64,128)
+  const float* b0;     // layer-1 biases (HID): `bias`, or the tile's image's metadata-folded bias (global)
 
   __device__ __forceinline__ uint32_t lane_off() const { return ((threadIdx.x >> 5) & 3u) << 21; }
 
@@ -544,7 +545,7 @@ struct TcEngineT {
   // this thread's 16 biases of layer l (loaded before the MMA wait, so the
   // adds after the TMEM load are register-only)
   __device__ __forceinline__ void load_bias(int l, float2 (&bq)[8]) const {
-    const float4* b4 = reinterpret_cast<const float4*>(bias + 32 * col_grp() + 16 * half_id() + l * HID);
+    const float4* b4 = reinterpret_cast<const float4*>((l == 0 ? b0 : bias + l * HID) + 32 * col_grp() + 16 * half_id());
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const float4 b = b4[q];
@@ -790,7 +791,8 @@ struct Fp32Engine {
   float* buf0;
   float* buf1;
   uint32_t* xbuf;
-  const float* w;  // global fp32 blob (f32_off layout)
+  const float* w;   // global fp32 blob (f32_off layout)
+  const float* b0;  // per-image layer-1 biases (metadata folded in), or null: the blob's
 
   __device__ __forceinline__ void put_input(int k, float x) const { buf0[k * ROWS + tile_row()] = x; }
 
@@ -819,7 +821,7 @@ struct Fp32Engine {
       float* out = (l & 1) ? buf0 : buf1;
       const int K = f32_k(l), N = layer_n(l);
       const float* W = w + f32_off(l);
-      const float* B = W + K * N;
+      const float* B = (l == 0 && b0) ? b0 : W + K * N;
       const int n8 = N / 8;
 #pragma unroll 1
       for (int n0 = j * 2 * n8 + h * n8; n0 < j * 2 * n8 + (h + 1) * n8; n0 += 16) {

@@ -24,6 +24,7 @@ struct Plan {
   // unit range of this launch: units [u_lo, u_lo + u_cnt) of the batch, i.e.
   // streams [s_lo, s_lo + s_cnt) (the whole batch unless a *_units call)
   uint32_t u_lo, u_cnt, s_lo, s_cnt;
+  uint32_t n_meta;  // metadata reals per image (container block: 4 + 4 n_meta bytes after the size table)
 };
 
 constexpr uint32_t HDR_FIXED = 60;  // container header bytes before the size table (version 2)
@@ -72,7 +73,21 @@ struct DevWeights {
   const uint8_t* wimg;  // bf16 core-matrix image, WIMG_BYTES
   const float* bias;    // BIAS_TOTAL floats
   const float* w32;     // fp32 blob (f32_off layout)
+  // per-image layer-1 bias with the metadata inputs folded in ([n_img][HID]
+  // fp32, k_meta_bias), or null (no metadata: the model's own b1)
+  const float* b1img;
 };
+
+// Metadata inputs -> per-image layer-1 bias: out[i][n] = b1[n] +
+// sum_k m'_ik W1[78 + k][n], m' = (m - min) / (max - min) in binary32; bf16
+// path: m' and W rounded to bf16 (exact products), sum in fp32 k ascending,
+// then + b1; fp32 path: the same with fp32 operands (fma chain).
+// raw reals from d_meta[i][k] (encode), or, when d_bits is set, from the
+// metadata block of container i at d_bits + d_cont_off[i] + meta_off (decode)
+cudaError_t launch_meta_bias(uint32_t n_img, uint32_t n_meta, const float* d_meta, const uint8_t* d_bits,
+                             const uint64_t* d_cont_off, uint32_t meta_off, const float* d_range,
+                             const float* d_wmeta, const float* d_b1, uint32_t precision, float* d_out,
+                             cudaStream_t st);
 
 struct Timing;  // optional CUDA-event timing, owned by the API layer
 
@@ -84,7 +99,8 @@ cudaError_t launch_rans_enc(const Plan& p, const uint32_t* d_fc, uint16_t* d_scr
                             cudaStream_t st);
 cudaError_t launch_container(const Plan& p, const uint8_t* model_sha, const uint32_t* d_words,
                              const uint16_t* d_scratch, uint8_t* d_out, uint64_t out_stride,
-                             uint64_t* d_sizes, uint64_t* d_stream_dst, cudaStream_t st, bool payload_only = false);
+                             uint64_t* d_sizes, uint64_t* d_stream_dst, cudaStream_t st, bool payload_only = false,
+                             const float* d_meta = nullptr);
 cudaError_t launch_dec_prep(const Plan& p, const uint8_t* d_bits, const uint64_t* d_cont_off,
                             const uint64_t* d_cont_len, uint32_t* d_sbase, uint32_t* d_slen,
                             int32_t* d_status, cudaStream_t st, bool check_numerics = true);

@@ -92,6 +92,7 @@ __device__ __forceinline__ uint8_t* engine_setup(typename EngineSel<PREC>::T& en
     eng.tmem = *tslot;
     eng.wsmem = smem_u32(smem);
     eng.bias = reinterpret_cast<const float*>(smem + WIMG_BYTES);
+    eng.b0 = eng.bias;
     eng.bar = smem_u32(bar);
     eng.phase = 0;
     return smem + WIMG_BYTES + BIAS_BYTES;
@@ -100,6 +101,7 @@ __device__ __forceinline__ uint8_t* engine_setup(typename EngineSel<PREC>::T& en
     eng.buf1 = eng.buf0 + NOUT * ROWS;
     eng.xbuf = reinterpret_cast<uint32_t*>(smem + F32_BUF_BYTES);
     eng.w = w.w32;
+    eng.b0 = nullptr;
     return smem + F32_BUF_BYTES + F32_X_BYTES;
   }
 }
@@ -199,6 +201,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (u != cu) {
       cu = u;
       cun = unit_info(p, u);
+      if (w.b1img) eng.b0 = w.b1img + (uint64_t)cun.img * HID;  // the tile's image's metadata-folded layer-1 bias
     }
     const uint32_t q = kt * (uint32_t)ROWS + (uint32_t)row;
     x.valid = q < cun.w * cun.h;
@@ -390,6 +393,7 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
   ea.tmem = eb.tmem = tslot;
   ea.wsmem = eb.wsmem = smem_u32(smem);
   ea.bias = eb.bias = reinterpret_cast<const float*>(smem + WIMG_BYTES);
+  ea.b0 = eb.b0 = ea.bias;
   ea.bar = smem_u32(&bars[0]);
   eb.bar = smem_u32(&bars[1]);
   ea.phase = eb.phase = 0;
@@ -442,6 +446,7 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
     const uint8_t* fimg = imgs;
     uint64_t ffc = 0;
     uint64_t fgi = 0;  // DBG: image-raster index of the unit's pixel (0, 0)
+    const float* fb0 = ea.bias;  // layer-1 biases of the cursor's image
     auto set_unit = [&](uint32_t u) {
       const Unit un = unit_info(p, u);
       fu = u;
@@ -453,6 +458,7 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
       fimg = imgs + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
       ffc = un.fc_off;
       fgi = (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
+      if (w.b1img) fb0 = w.b1img + (uint64_t)un.img * HID;
     };
     if (t0 < tend) {
       const uint32_t u0 = (uint32_t)(t0 / p.tiles_per_unit);
@@ -518,6 +524,7 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
         a[k] = pack_bf16(x0, x1);
       }
       eng.put_input(a);
+      eng.b0 = fb0;  // the slot's layer-1 bias until its next feed
       // fresh taps (0,-1) and (-1,+2)
       xa = u8_unit((valid && fcol >= 1) ? (uint32_t)__ldg(tp - 1) : 0u);
       xb = u8_unit((valid && fr >= 1 && fcol + 2 < (int)fw) ? (uint32_t)__ldg(tp - p.W + 2) : 0u);
@@ -747,7 +754,7 @@ __device__ __forceinline__ void put_u32(uint8_t* o, uint32_t v) {
 // header, offsets relative to the payload start, streams [s_lo, s_lo + s_cnt).
 __global__ void k_container(Plan p, Sha sha, const uint32_t* __restrict__ words, uint8_t* __restrict__ out,
                             uint64_t stride, uint64_t* __restrict__ sizes, uint64_t* __restrict__ dst,
-                            int payload_only) {
+                            int payload_only, const float* __restrict__ meta) {
   const uint32_t img = blockIdx.x;
   uint8_t* o = out + (uint64_t)img * stride;
   if (payload_only) {
@@ -779,6 +786,10 @@ __global__ void k_container(Plan p, Sha sha, const uint32_t* __restrict__ words,
     for (int i = 0; i < 32; ++i) o[24 + i] = sha.b[i];
     put_u32(o + 56, p.spi);
     uint64_t off = p.hdr_bytes;
+    // metadata block after the size table: u32 n, f32 raw reals
+    uint8_t* mb = o + HDR_FIXED + 4u * p.spi;
+    put_u32(mb, p.n_meta);
+    for (uint32_t k = 0; k < p.n_meta; ++k) put_u32(mb + 4 + 4 * k, __float_as_uint(meta[(uint64_t)img * p.n_meta + k]));
     for (uint32_t s = 0; s < p.spi; ++s) {
       const uint32_t sz = 2u * words[(uint64_t)img * p.spi + s];
       put_u32(o + HDR_FIXED + 4 * s, sz);
@@ -897,7 +908,7 @@ __global__ void k_dec_prep(Plan p, const uint8_t* __restrict__ bits, const uint6
   else if (b[4] != CONTAINER_VERSION || b[6] != 1 || b[7] != 0 || (check_numerics && get_u16(b + 22) != NUMERICS_REV)) err = 5;
   else if (get_u32(b + 8) != p.W || get_u32(b + 12) != p.H || get_u16(b + 16) != p.hdr_tw ||
            get_u16(b + 18) != p.hdr_th || get_u16(b + 20) != p.G || b[5] != p.precision ||
-           get_u32(b + 56) != p.spi || p.hdr_bytes > len)
+           get_u32(b + 56) != p.spi || p.hdr_bytes > len || get_u32(b + HDR_FIXED + 4u * p.spi) != p.n_meta)
     err = 2;
   uint64_t off = p.hdr_bytes;
   for (uint32_t s = 0; s < p.spi; ++s) {
@@ -962,6 +973,15 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
   typename EngineSel<PREC>::T eng;
   uint8_t* ring = engine_setup<PREC>(eng, smem, w, bar, &tslot);
   if constexpr (PREC == 1) eng.bar2 = smem_u32(&bar[2]);
+  if (w.b1img) {  // the unit's image's metadata-folded layer-1 bias
+    if constexpr (PREC == 1) {
+      __syncthreads();  // engine_setup's bias copy is complete
+      float* b1 = const_cast<float*>(eng.bias);
+      for (uint32_t i = threadIdx.x; i < (uint32_t)HID; i += blockDim.x) b1[i] = w.b1img[(uint64_t)un.img * HID + i];
+    } else {
+      eng.b0 = w.b1img + (uint64_t)un.img * HID;
+    }
+  }
   uint32_t* cursor = reinterpret_cast<uint32_t*>(ring + RING_BYTES + 16);  // 16 zero bytes after the ring
   uint32_t* s_sbase = cursor + ((un.ngroups + 3u) & ~3u);                   // per-group stream table
   uint32_t* s_slen = s_sbase + ((un.ngroups + 3u) & ~3u);
@@ -1438,6 +1458,41 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
   if (NC > 1) cluster_sync_all();  // keep DSMEM alive until every CTA is done
 }
 
+// ------------------------------------------------------------ metadata -> layer-1 bias
+// One thread per (image, hidden unit): out = b1 + sum_k m'_k W1[78 + k] (see
+// dlic_internal.h); the per-image constant part of layer 1 (P:210 metadata
+// features are the same for every pixel of an image).
+__device__ __forceinline__ float bf16_rn(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+__global__ void k_meta_bias(uint32_t n_img, uint32_t n_meta, const float* __restrict__ meta,
+                            const uint8_t* __restrict__ bits, const uint64_t* __restrict__ cont_off,
+                            uint32_t meta_off, const float* __restrict__ range, const float* __restrict__ wmeta,
+                            const float* __restrict__ b1, uint32_t precision, float* __restrict__ out) {
+  const uint32_t i = blockIdx.x, n = threadIdx.x;
+  if (i >= n_img || n >= (uint32_t)HID) return;
+  float acc = 0.0f;
+  for (uint32_t k = 0; k < n_meta; ++k) {
+    const float lo = range[2 * k], hi = range[2 * k + 1];
+    // raw real: from the host-supplied array (encode) or re-read from the
+    // container's metadata block (decode)
+    const float raw = bits ? __uint_as_float(get_u32(bits + cont_off[i] + meta_off + 4u * k))
+                           : meta[(uint64_t)i * n_meta + k];
+    const float m = __fdiv_rn(__fsub_rn(raw, lo), __fsub_rn(hi, lo));
+    const float wv = wmeta[k * HID + n];
+    if (precision == 1) acc = __fadd_rn(acc, __fmul_rn(bf16_rn(m), bf16_rn(wv)));  // exact product
+    else acc = __fmaf_rn(m, wv, acc);
+  }
+  out[(uint64_t)i * HID + n] = __fadd_rn(b1[n], acc);
+}
+
+cudaError_t launch_meta_bias(uint32_t n_img, uint32_t n_meta, const float* d_meta, const uint8_t* d_bits,
+                             const uint64_t* d_cont_off, uint32_t meta_off, const float* d_range,
+                             const float* d_wmeta, const float* d_b1, uint32_t precision, float* d_out,
+                             cudaStream_t st) {
+  k_meta_bias<<<n_img, HID, 0, st>>>(n_img, n_meta, d_meta, d_bits, d_cont_off, meta_off, d_range, d_wmeta, d_b1,
+                                     precision, d_out);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------ launchers
 template <class K>
 static cudaError_t set_smem(K kern, size_t bytes) {
@@ -1494,11 +1549,11 @@ cudaError_t launch_rans_enc(const Plan& p, const uint32_t* d_fc, uint16_t* d_scr
 
 cudaError_t launch_container(const Plan& p, const uint8_t* model_sha, const uint32_t* d_words,
                              const uint16_t* d_scratch, uint8_t* d_out, uint64_t out_stride, uint64_t* d_sizes,
-                             uint64_t* d_stream_dst, cudaStream_t st, bool payload_only) {
+                             uint64_t* d_stream_dst, cudaStream_t st, bool payload_only, const float* d_meta) {
   Sha sha;
   for (int i = 0; i < 32; ++i) sha.b[i] = model_sha ? model_sha[i] : 0;
   k_container<<<payload_only ? 1u : p.n_img, 32, 0, st>>>(p, sha, d_words, d_out, out_stride, d_sizes,
-                                                           d_stream_dst, payload_only ? 1 : 0);
+                                                           d_stream_dst, payload_only ? 1 : 0, d_meta);
   if (p.s_cnt > 0) k_copy<<<p.s_cnt, 128, 0, st>>>(p, d_words, d_scratch, d_stream_dst, d_out, out_stride);
   return cudaGetLastError();
 }

@@ -4,6 +4,10 @@ fixtures/p100k_trained.dlicmdl — P100K (78->128x5->256) briefly trained on
 synthetic "natural-like" crops (SURVEY §8(d) C2 generator, sigma_tex=2,
 sigma_n=1), as north_star allows ("briefly trained by the oracle on synthetic
 smooth-plus-noise images").  Run: python scripts/make_fixtures.py
+fixtures/p100k_pool_meta.dlicmdl — the §8(f) f4 network (78 + 3 metadata
+inputs -> 128 -> [avg 2] -> 128 -> 128 -> [avg 2] -> 128 -> 128 -> 256),
+seeded He-uniform weights (the GPU tests' model); written alone by
+python scripts/make_fixtures.py pool_meta
 """
 
 import os
@@ -43,5 +47,22 @@ def main():
     print("wrote", out)
 
 
+POOL = [2, 0, 2, 0, 0, 0]
+META_RANGE = [(0.0, 2.0), (0.0, 10.0), (0.5, 6.0)]
+
+
+def pool_meta():
+    layers = synth.he_uniform_pooled(81, [128, 128, 128, 128, 128, 256], POOL, seed=7, bias_scale=0.1)
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "fixtures",
+                       "p100k_pool_meta.dlicmdl")
+    with open(out, "wb") as fh:
+        fh.write(model_io.save(layers, pool=POOL, meta_range=META_RANGE))
+    print("wrote", out)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "pool_meta":
+        pool_meta()
+    else:
+        main()
+        pool_meta()

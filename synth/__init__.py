@@ -18,4 +18,4 @@ from .images import (  # noqa: F401
     config_images,
     CONFIGS,
 )
-from .weights import he_uniform_layers, zero_layers  # noqa: F401
+from .weights import he_uniform_layers, he_uniform_pooled, zero_layers  # noqa: F401
