@@ -111,7 +111,7 @@ class ModelHashMismatch(Exception):
 
 
 def _split_streams(hdr):
-    """Per-unit lists of word streams, in container order."""
+    """Per-unit lists of word streams, in container order (one slice)."""
     units = container.tiles(hdr["width"], hdr["height"], hdr["tile_w"], hdr["tile_h"])
     allw = [streams.rans.bytes_to_words(s) for s in hdr["streams"]]
     per = []
@@ -206,3 +206,107 @@ def payload_bits_estimate(fs: np.ndarray) -> float:
 
 def sha256(b: bytes) -> bytes:
     return hashlib.sha256(b).digest()
+
+
+# ---- volumes (§8(f) f2): the 3D window R13, slices in order ------
+def unit_tables_by_front_3d(net, precision: int, img: np.ndarray, prev):
+    """(f_s, c_s) of one slice unit, front by front (2D order within the
+    slice); the lower-layer taps come from `prev` (the same unit of the
+    slice below, or None for slice 0).  The 3D wavefront (R14) only overlaps
+    these per-slice fronts in time; the tables are the same."""
+    lay, pool, meta_norm = _net(net)
+    h, w = img.shape
+    fs = np.zeros((h, w), np.int64)
+    cs = np.zeros((h, w), np.int64)
+    for t in range(schedule.n_fronts(w, h)):
+        pix = schedule.front(t, w, h)
+        if not pix:
+            continue
+        rows = np.array([q[0] for q in pix], dtype=np.int64)
+        cols = np.array([q[1] for q in pix], dtype=np.int64)
+        x = window.net_inputs_3d(img, prev, rows, cols, meta_norm)
+        _, f, c = quant.tables_from_logits(mlp.logits_path(lay, x, precision, pool))
+        sym = img[rows, cols].astype(np.int64)
+        fs[rows, cols] = f[np.arange(len(pix)), sym]
+        cs[rows, cols] = c[np.arange(len(pix)), sym]
+    return fs, cs
+
+
+def encode_volume_with_tables(fs_vol, cs_vol, width, height, precision, group_rows, tile_w, tile_h, model_sha,
+                              numerics: int = container.ORACLE_NUMERICS, meta=None) -> bytes:
+    """One container for the volume (window id 2): slice-major streams, each
+    slice's units as in the 2D container."""
+    out = []
+    for z in range(fs_vol.shape[0]):
+        for (x0, y0, tw, th) in container.tiles(width, height, tile_w, tile_h):
+            sts = streams.encode_unit(fs_vol[z, y0:y0 + th, x0:x0 + tw], cs_vol[z, y0:y0 + th, x0:x0 + tw],
+                                      group_rows)
+            out += [streams.rans.words_to_bytes(s) for s in sts]
+    return container.write(width, height, precision, group_rows, tile_w, tile_h, model_sha, out, numerics, meta,
+                           container.WINDOW_3D)
+
+
+def encode_volume(vol: np.ndarray, model_blob: bytes, precision: int = 0, group_rows: int = 32,
+                  tile_w: int = 0, tile_h: int = 0, meta=None) -> bytes:
+    """vol (D, H, W) u8.  The model's inputs: 87 (+ metadata)."""
+    net = model_io.load_net(model_blob)
+    net["meta_norm"] = window.meta_features(meta, net["meta_range"])
+    d, h, w = vol.shape
+    fs = np.zeros((d, h, w), np.int64)
+    cs = np.zeros((d, h, w), np.int64)
+    for z in range(d):
+        for (x0, y0, tw, th) in container.tiles(w, h, tile_w, tile_h):
+            prev = None if z == 0 else np.ascontiguousarray(vol[z - 1, y0:y0 + th, x0:x0 + tw])
+            f_u, c_u = unit_tables_by_front_3d(net, precision, np.ascontiguousarray(vol[z, y0:y0 + th, x0:x0 + tw]),
+                                               prev)
+            fs[z, y0:y0 + th, x0:x0 + tw] = f_u
+            cs[z, y0:y0 + th, x0:x0 + tw] = c_u
+    return encode_volume_with_tables(fs, cs, w, h, precision, group_rows, tile_w, tile_h,
+                                     model_io.digest(model_blob), meta=meta)
+
+
+def _split_volume(hdr):
+    """[slice][unit] -> ((x0, y0, tw, th), word streams)."""
+    sps = container.streams_per_slice(hdr["width"], hdr["height"], hdr["tile_w"], hdr["tile_h"], hdr["group_rows"])
+    out = []
+    for z in range(hdr["depth"]):
+        sub = dict(hdr, streams=hdr["streams"][z * sps:(z + 1) * sps])
+        out.append(_split_streams(sub))
+    return out
+
+
+def decode_volume(blob: bytes, model_blob: bytes) -> np.ndarray:
+    """Slice by slice (the dependency order of the 3D wavefront, R14)."""
+    hdr = container.parse(blob)
+    if hdr["window"] != container.WINDOW_3D:
+        raise container.CorruptContainer("not a volume container")
+    if hdr["model_sha"] != model_io.digest(model_blob):
+        raise ModelHashMismatch()
+    if hdr["numerics"] != container.ORACLE_NUMERICS:
+        raise container.CorruptContainer("numerics revision %d is not the oracle's" % hdr["numerics"])
+    net = model_io.load_net(model_blob)
+    net["meta_norm"] = window.meta_features(hdr["meta"], net["meta_range"])
+    lay, pool, meta_norm = _net(net)
+    prec = hdr["precision"]
+    out = np.zeros((hdr["depth"], hdr["height"], hdr["width"]), np.uint8)
+    for z, units in enumerate(_split_volume(hdr)):
+        for (x0, y0, tw, th), sts in units:
+            prev = None if z == 0 else np.ascontiguousarray(out[z - 1, y0:y0 + th, x0:x0 + tw])
+
+            def ft(t, rows, cols, img, prev=prev):
+                x = window.net_inputs_3d(img, prev, rows, cols, meta_norm)
+                _, f, c = quant.tables_from_logits(mlp.logits_path(lay, x, prec, pool))
+                return f, c
+            out[z, y0:y0 + th, x0:x0 + tw] = streams.decode_unit(sts, tw, th, hdr["group_rows"], ft)
+    return out
+
+
+def decode_volume_with_tables(blob: bytes, freq_tables: np.ndarray) -> np.ndarray:
+    """freq_tables (D, H, W, 256)."""
+    hdr = container.parse(blob)
+    out = np.zeros((hdr["depth"], hdr["height"], hdr["width"]), np.uint8)
+    for z, units in enumerate(_split_volume(hdr)):
+        for (x0, y0, tw, th), sts in units:
+            out[z, y0:y0 + th, x0:x0 + tw] = streams.decode_unit_with_tables(
+                sts, freq_tables[z, y0:y0 + th, x0:x0 + tw], hdr["group_rows"])
+    return out

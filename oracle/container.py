@@ -5,7 +5,9 @@ of DESIGN.md "Container", version 2), little-endian:
   off  0  4s  magic "DLIC"
   off  4  u8  version (2)
   off  5  u8  precision path (0 = fp32, 1 = bf16)
-  off  6  u8  window id (1 = 9x9 causal, 78 inputs; R1)
+  off  6  u8  window id (1 = 9x9 causal, 78 inputs, R1; 2 = the 3D window of
+              R13: 78 + a 3x3 box in the slice below, 87 inputs -- the
+              container then holds a whole volume, streams slice-major)
   off  7  u8  fill value (0; R2)
   off  8  u32 width        off 12 u32 height
   off 16  u16 tile_w       off 18 u16 tile_h    (0, 0 = untiled)
@@ -32,6 +34,7 @@ import numpy as np
 MAGIC = b"DLIC"
 VERSION = 2
 WINDOW_ID = 1
+WINDOW_3D = 2
 HEADER_FIXED = 60
 ORACLE_NUMERICS = 0
 
@@ -51,10 +54,14 @@ def tiles(width: int, height: int, tile_w: int, tile_h: int):
     return out
 
 
+def streams_per_slice(width, height, tile_w, tile_h, group_rows) -> int:
+    return sum(-(-th // group_rows) for (_, _, _, th) in tiles(width, height, tile_w, tile_h))
+
+
 def write(width, height, precision, group_rows, tile_w, tile_h, model_sha, stream_bytes,
-          numerics=ORACLE_NUMERICS, meta=None) -> bytes:
+          numerics=ORACLE_NUMERICS, meta=None, window_id=WINDOW_ID) -> bytes:
     assert len(model_sha) == 32
-    hdr = MAGIC + struct.pack("<BBBBIIHHHH", VERSION, precision, WINDOW_ID, 0, width, height,
+    hdr = MAGIC + struct.pack("<BBBBIIHHHH", VERSION, precision, window_id, 0, width, height,
                               tile_w, tile_h, group_rows, numerics)
     hdr += model_sha + struct.pack("<I", len(stream_bytes))
     hdr += b"".join(struct.pack("<I", len(s)) for s in stream_bytes)
@@ -67,7 +74,7 @@ def parse(blob: bytes):
     if len(blob) < HEADER_FIXED or blob[:4] != MAGIC:
         raise CorruptContainer("magic")
     ver, prec, win, fill, w, h, tw, th, g, num = struct.unpack_from("<BBBBIIHHHH", blob, 4)
-    if ver != VERSION or win != WINDOW_ID or fill != 0 or prec > 1 or g == 0:
+    if ver != VERSION or win not in (WINDOW_ID, WINDOW_3D) or fill != 0 or prec > 1 or g == 0:
         raise CorruptContainer("header fields")
     sha = blob[24:56]
     (n,) = struct.unpack_from("<I", blob, 56)
@@ -91,5 +98,8 @@ def parse(blob: bytes):
         off += s
     if off != len(blob):
         raise CorruptContainer("trailing bytes")
+    sps = streams_per_slice(w, h, tw, th, g)
+    if n % sps or (win == WINDOW_ID and n != sps):
+        raise CorruptContainer("stream count")
     return dict(width=w, height=h, precision=prec, tile_w=tw, tile_h=th, group_rows=g, numerics=num,
-                model_sha=sha, streams=streams, header_bytes=hdr_bytes, meta=meta)
+                model_sha=sha, streams=streams, header_bytes=hdr_bytes, meta=meta, window=win, depth=n // sps)

@@ -50,3 +50,29 @@ def front_rows(t: int, width: int, height: int, lag: int = LAG):
     lo = max(0, -(-(t - width + 1) // lag))
     hi = min(height - 1, t // lag)
     return lo, hi
+
+
+# ---- 3D wavefront ("We overlap 2D wavefronts to decode all layers
+# at once.  The wavefronts are shifted in each layer in such a way that the
+# pixels used in the neighborhood window in the layer above are already
+# decoded").  Reading R14: slice z runs the 2D schedule delayed by z * lag3d
+# steps; the minimal lag3d makes every lower-layer tap (z-1, r+dr, c+dc) of a
+# pixel precede it: 1 + max over the 3D box of (dc + L dr) (= 5 for the 3x3
+# box and L = 3).  The decoder may use any larger lag (more slack); the
+# bitstream does not depend on it (each slice's streams follow its own 2D
+# order).
+def slice_lag(offsets_3d=window.OFFSETS_3D, lag: int = LAG) -> int:
+    return 1 + max(dc + lag * dr for dr, dc in offsets_3d)
+
+
+LAG3D = slice_lag()
+
+
+def step_3d(z: int, r: int, c: int, lag3d: int = LAG3D, lag: int = LAG) -> int:
+    return z * lag3d + step(r, c, lag)
+
+
+def n_fronts_3d(width: int, height: int, depth: int, lag3d: int = LAG3D) -> int:
+    if depth <= 0:
+        return 0
+    return n_fronts(width, height) + lag3d * (depth - 1)

@@ -90,3 +90,39 @@ def net_inputs(img: np.ndarray, rows, cols, meta_norm=None) -> np.ndarray:
     if meta_norm is None or len(meta_norm) == 0:
         return x
     return np.concatenate([x, np.broadcast_to(np.asarray(meta_norm, np.float64), (x.shape[0], len(meta_norm)))], 1)
+
+
+# ---- 3D window ("we choose a 2-layered window"; Fig. 6 right: the
+# window in the layer below is shifted down by WS).  Reading R13: the 78-tap
+# causal window in slice z (the top layer, holding the pixel of interest) plus
+# a 3x3 box in slice z-1 centred on the target (dr, dc in {-1, 0, 1}, row-major,
+# i.e. WS = 1: one row below the target), 87 inputs; fill 0 outside the slice
+# and below slice 0.
+OFFSETS_3D = tuple((dr, dc) for dr in (-1, 0, 1) for dc in (-1, 0, 1))
+N_INPUTS_3D = N_INPUTS + len(OFFSETS_3D)
+
+
+def gather_many_3d(prev: np.ndarray | None, rows, cols, shape, fill: int = FILL) -> np.ndarray:
+    """(n, 9) lower-layer taps of the targets (rows, cols) from slice z-1
+    (`prev`, or None for slice 0: all fill)."""
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    if prev is None:
+        return np.full((len(rows), len(OFFSETS_3D)), fill, dtype=np.int64)
+    h, w = shape
+    pad = np.full((h + 2, w + 2), fill, dtype=np.int64)
+    pad[1:1 + h, 1:1 + w] = prev
+    dr = np.array([o[0] for o in OFFSETS_3D], dtype=np.int64)
+    dc = np.array([o[1] for o in OFFSETS_3D], dtype=np.int64)
+    return pad[rows[:, None] + dr[None, :] + 1, cols[:, None] + dc[None, :] + 1]
+
+
+def net_inputs_3d(img: np.ndarray, prev, rows, cols, meta_norm=None) -> np.ndarray:
+    """87 (+ metadata) network inputs: the 2D window, the lower-layer box, then
+    the metadata features."""
+    x = features(gather_many(img, rows, cols))
+    x3 = features(gather_many_3d(prev, rows, cols, img.shape))
+    out = np.concatenate([x, x3], 1)
+    if meta_norm is None or len(meta_norm) == 0:
+        return out
+    return np.concatenate([out, np.broadcast_to(np.asarray(meta_norm, np.float64), (out.shape[0], len(meta_norm)))], 1)
