@@ -47,6 +47,10 @@ MODELS = {
                   "P100K-pool-meta: 78+3 metadata inputs, avg-pool 2 after layers 1 and 3, seeded random "
                   "(fixtures/p100k_pool_meta.dlicmdl; pooling folded into the next layer, metadata into a "
                   "per-image layer-1 bias: the tensor-core chain runs P100K's shapes, 216,576 FLOP/px)"),
+    "3d": ("p100k_3d.dlicmdl", None,
+           "P100K-3D: 78 + the 3x3 box of the slice below (87 inputs) -> 128x5 -> 256, seeded random "
+           "(fixtures/p100k_3d.dlicmdl; the 9 lower taps enter layer 1 through the bias term, 2,304 FLOP/px on "
+           "the CUDA cores on top of P100K's 216,576 on the tensor cores)"),
 }
 CONFIG_DESC = {
     "C1": "C1 32x32 gradient+noise, single stream (G=32=H)",
@@ -70,6 +74,9 @@ def parse():
     ap.add_argument("--tile", default="", help="WxH independent tiles (default: the config's)")
     ap.add_argument("--no-variants", action="store_true", help="skip the strip-tiled C2 side measurement")
     ap.add_argument("--no-strong", action="store_true", help="skip C4's unit-split (strong scaling) measurement")
+    ap.add_argument("--volume", type=int, default=0,
+                    help="volume depth: code each group of D consecutive images as one volume (3D window; "
+                         "--model 3d; default 32 with it)")
     ap.add_argument("--model", default="p100k", choices=list(MODELS),
                     help="p100k: trained fixture; pool-meta: the f4 network (pooling + 3 metadata inputs)")
     return ap.parse_args()
@@ -173,6 +180,20 @@ def dist_setup(args):
     return ws, rank, local
 
 
+def synth_volumes(args, rank, n, vd):
+    import synth
+    vols = [synth.mri_like_volume(256, vd, seed=100 * rank + v) for v in range(n // vd)]
+    return np.ascontiguousarray(np.concatenate(vols)[:, :args_h(args), :args_w(args)])
+
+
+def args_h(args):
+    return {"C1": 32, "C2": 512, "C3": 256, "C4": 1080, "C5": 2160}[args.config]
+
+
+def args_w(args):
+    return {"C1": 32, "C2": 768, "C3": 256, "C4": 1920, "C5": 3840}[args.config]
+
+
 def images_for(args, rank, n):
     import synth
     cfg = args.config
@@ -257,12 +278,20 @@ def cpu_info():
 METRIC = "encode+decode Mpixel/s (8-bit gray, round trip) and bpp"
 
 
+def volume_depth(args):
+    if args.model == "3d":
+        return args.volume or 32
+    return 0
+
+
 def arm_config(args, n, W, H, tile, g, ws):
     """The config object of the JSON line (both arms)."""
-    return {"workload": CONFIG_DESC[args.config], "images_per_gpu": n, "width": W, "height": H,
+    vd = volume_depth(args)
+    extra = {"volume_depth": vd, "volumes_per_gpu": n // vd} if vd else {}
+    return dict({"workload": CONFIG_DESC[args.config], "images_per_gpu": n, "width": W, "height": H,
             "tile": list(tile), "group_rows": g, "precision": args.precision,
             "weights": MODELS[args.model][2],
-            "l2": "flushed between timed steps (256 MiB write, untimed)", "parallelism": "dp%d" % ws}
+            "l2": "flushed between timed steps (256 MiB write, untimed)", "parallelism": "dp%d" % ws}, **extra)
 
 
 def run_reference(args):
@@ -281,11 +310,19 @@ def run_reference(args):
     sample = np.ascontiguousarray(img[:sh, :sw])
     prec = 1 if args.precision == "bf16" else 0
     g, _ = opts_for(args.config)
+    vd = volume_depth(args)
+    if vd:   # the oracle's volume coder on the first 4 slices of a volume (~5-10 s)
+        sample = synth_volumes(args, 0, vd, vd)[:4]
+        sh, sw = sample.shape[1:]
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        b = codec.encode(sample, blob, prec, g, meta=meta)
-        out = codec.decode(b, blob)
+        if vd:
+            b = codec.encode_volume(sample, blob, prec, g, meta=meta)
+            out = codec.decode_volume(b, blob)
+        else:
+            b = codec.encode(sample, blob, prec, g, meta=meta)
+            out = codec.decode(b, blob)
         dt = time.perf_counter() - t0
         assert np.array_equal(out, sample)
         if i >= args.warmup:
@@ -294,7 +331,8 @@ def run_reference(args):
     mpx = sample.size / (ms / 1e3) / 1e6
     ci = cpu_info()
     cores = ci["blas_threads"] or ci["logical_cpus"] or 1
-    whole = sample.shape == img.shape
+    whole = sample.shape == img.shape or vd > 0
+    what = ("%d slices %dx%d of a volume (3D window)" % (sample.shape[0], sw, sh)) if vd else None
     line = {
         "impl": "reference", "metric": METRIC, "value": mpx,
         "unit": "Mpixel/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -302,10 +340,12 @@ def run_reference(args):
         "dtype": "f64-accum bf16-emulated" if prec else "f64", "data": "synthetic",
         "config": dict(arm_config(args, default_batch(args.config) if not args.batch else args.batch,
                                   img.shape[1], img.shape[0], tile_for(args)[1], g, ws),
-                       sample=("per step the oracle codes one whole %dx%d image (untiled)" % (sw, sh)) if whole
+                       sample=("per step the oracle codes " + what) if vd else
+                       ("per step the oracle codes one whole %dx%d image (untiled)" % (sw, sh)) if whole
                        else "per step the oracle codes a top-left %dx%d crop of one image (untiled)" % (sw, sh)),
         "cpu_baseline": dict({"value": mpx, "unit": "Mpixel/s", "cores": cores, "kind": "oracle",
-                              "sample": ("the whole %s image (%dx%d), oracle encode+decode per step" % (args.config, sw, sh))
+                              "sample": what if vd else
+                              ("the whole %s image (%dx%d), oracle encode+decode per step" % (args.config, sw, sh))
                               if whole else "top-left %dx%d crop of the %s image, oracle encode+decode per step"
                               % (sw, sh, args.config)}, **ci),
         "e2e": {"value": mpx, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -321,9 +361,15 @@ def cpu_baseline_sample(args, img):
     sh, sw = min(img.shape[0], 512), min(img.shape[1], 768)   # C2: the whole image (~10-15 s)
     sample = np.ascontiguousarray(img[:sh, :sw])
     prec = 1 if args.precision == "bf16" else 0
+    vd = volume_depth(args)
     t0 = time.perf_counter()
-    b = codec.encode(sample, blob, prec, 32, meta=MODELS[args.model][1])
-    out = codec.decode(b, blob)
+    if vd:
+        sample = synth_volumes(args, 0, vd, vd)[:4]
+        b = codec.encode_volume(sample, blob, prec, 32)
+        out = codec.decode_volume(b, blob)
+    else:
+        b = codec.encode(sample, blob, prec, 32, meta=MODELS[args.model][1])
+        out = codec.decode(b, blob)
     dt = time.perf_counter() - t0
     assert np.array_equal(out, sample)
     ci = cpu_info()
@@ -414,6 +460,11 @@ def main():
     g, tile = tile_for(args)
     n = args.batch or default_batch(args.config)
     imgs = images_for(args, rank, n)
+    vd = volume_depth(args)
+    if vd and n % vd:
+        raise SystemExit("bench.py: %d images per GPU is not a multiple of the volume depth %d" % (n, vd))
+    if vd:  # slices of a volume: consecutive MRI-like slices of one volume (synth.mri_like_slices)
+        imgs = synth_volumes(args, rank, n, vd)
     meta = None if MODELS[args.model][1] is None else np.tile(np.array(MODELS[args.model][1], np.float32), (n, 1))
     _, H, W = imgs.shape
     px_rank = n * H * W
@@ -425,22 +476,23 @@ def main():
     dl.dlic_set_timing(True)
 
     # first pass: planning header + correctness check of this batch
-    d_out, d_sizes, stride = dl.dlic_encode_batch_device(model, d_imgs, prec, g, tile, meta=meta)
+    d_out, d_sizes, stride = dl.dlic_encode_batch_device(model, d_imgs, prec, g, tile, meta=meta, volume_depth=vd)
     torch.cuda.synchronize()
     sizes = d_sizes.cpu().numpy()
     hdr = dl.dlic_peek(d_out[:int(sizes[0])].cpu().numpy().tobytes())
-    offs = [i * stride for i in range(n)]
+    offs = [i * stride for i in range(len(sizes))]
     lens = [int(x) for x in sizes]       # the encoder is deterministic: every step writes these sizes
     dl.dlic_decode_batch_device(model, d_out, offs, lens, hdr, d_dec, d_status)
     torch.cuda.synchronize()
     assert int(d_status.abs().sum()) == 0 and torch.equal(d_dec, d_imgs), "round trip failed"
     total_bytes = int(sizes.sum())
-    payload = total_bytes - n * hdr["header_bytes"]
+    payload = total_bytes - len(sizes) * hdr["header_bytes"]
 
     from paper_2207_05152_b200 import dist as dd
 
     def encode_local():
-        dl.dlic_encode_batch_device(model, d_imgs, prec, g, tile, d_out=d_out, d_sizes=d_sizes, meta=meta)
+        dl.dlic_encode_batch_device(model, d_imgs, prec, g, tile, d_out=d_out, d_sizes=d_sizes, meta=meta,
+                                    volume_depth=vd)
         return d_sizes
 
     def decode_local():
@@ -497,7 +549,11 @@ def main():
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             tot_in = tot_out = 0
-            if n == 1:  # the paper's calls: encode(image) -> bits, decode(bits) -> image
+            if vd:  # the volume calls: one container per volume
+                blob, sizes_e = dl.dlic_encode_batch(model, pin_imgs, prec, g, tile, meta=meta, volume_depth=vd)
+                back = dl.dlic_decode_batch(model, blob, sizes_e)
+                nb = len(blob)
+            elif n == 1:  # the paper's calls: encode(image) -> bits, decode(bits) -> image
                 b = dl.dlic_encode(model, pin_imgs[0], prec, g, tile, meta=None if meta is None else meta[0])
                 back = dl.dlic_decode(model, b)[None]
                 nb = len(b)

@@ -77,6 +77,13 @@ typedef struct {
    * n_meta must equal the model's metadata feature count (0 = none). */
   uint32_t n_meta;
   const float* meta;
+  /* volumes (3D window R13 + overlapped 3D wavefront R14):
+   * 0 = 2D images (container window id 1, the 78-tap window); D >= 1 = each
+   * group of D consecutive images of a call is one volume (slices in order)
+   * coded into ONE container (window id 2, streams slice-major); requires a
+   * model with 87 (+ n_meta) inputs.  Metadata (n_meta reals) is then per
+   * volume: meta[v * n_meta + k]. */
+  uint32_t volume_depth;
 } dlic_opts;
 
 /* Container (version 2, little-endian):
@@ -93,6 +100,7 @@ typedef struct {
 typedef struct {
   uint32_t width, height, precision, group_rows, tile_w, tile_h, n_streams, n_units;
   uint32_t numerics; /* arithmetic revision recorded by the encoder */
+  uint32_t depth;    /* slices: 0 for a 2D image (window id 1), D for a volume (window id 2) */
   uint32_t n_meta;   /* metadata reals stored in the container */
   float meta[DLIC_MAX_META];
   uint8_t model_sha256[32];
@@ -105,7 +113,8 @@ typedef struct {
  * u16 metadata feature count n, n x f32 (min, max), SHA-256 of all preceding
  * bytes.  Uploads fp32 and bf16 device copies to `cuda_device`.
  * The GPU engines run six dense layers with 128-unit hidden layers and 256
- * outputs ("P100K"), on 78 window inputs + n <= 8 metadata inputs
+ * outputs ("P100K"), on 78 window inputs (or 87 for volumes: + the 3x3
+ * box of the slice below, R13) + n <= 8 metadata inputs
  * (min-max normalised with the stored constants), with optional average
  * pooling of g = 2^k units after any hidden layer ("two optional
  * pooling layers"; the next layer then has 128 / g inputs).  Pooling is linear
@@ -153,7 +162,8 @@ dlic_status dlic_peek(const uint8_t* bits, size_t len, dlic_header* out);
  * DLIC_E_VERSION_MISMATCH.  0 is reserved for the CPU oracle's arithmetic. */
 uint32_t dlic_numerics_rev(void);
 
-/* Upper bound of the container size for (width, height, opts). */
+/* Upper bound of the container size for (width, height, opts): one image, or
+ * one volume of opts->volume_depth slices. */
 size_t dlic_max_container_bytes(uint32_t width, uint32_t height, const dlic_opts* opts);
 
 void dlic_free(void* p);
@@ -165,9 +175,10 @@ const char* dlic_last_error(void);
  * dlic_encode produces for that image alone).  One host->device copy of all
  * images and one device->host copy of all containers per call.
  * encode: imgs = n*height*width bytes (image i at imgs + i*width*height,
- * row-major); *out = library-allocated buffer (dlic_free) holding the n
- * containers back to back, *out_len its total size, sizes[i] (caller array of
- * n) the size of container i.
+ * row-major); *out = library-allocated buffer (dlic_free) holding the
+ * containers back to back (n, or n / opts->volume_depth for volumes), *out_len
+ * its total size, sizes[i] (caller array, one per container) the size of
+ * container i.
  * decode: container i at bits + offsets[i] (offsets ascending, all containers
  * of the same width/height/options and model); writes n*width*height bytes to
  * imgs.  Each header is checked on the host (hash before any pixel work), each
@@ -206,6 +217,16 @@ dlic_status dlic_decode_batch_device(const dlic_model* m, const uint8_t* d_bits,
                                      const uint64_t* h_offsets, const uint64_t* h_lengths,
                                      uint32_t n, const dlic_header* h_header, uint8_t* d_imgs,
                                      int32_t* d_status, void* cuda_stream);
+
+/* ---- volumes (§8(f) f2): the paper's MRI coder ----------------
+ * vol = depth slices of width x height (slice z at vol + z*height*row_stride...
+ * contiguous, row_stride = width).  One container per volume (window id 2).
+ * Decode runs every slice's wavefront at once, each slice delayed behind the
+ * one below by the 3D window's reach (the 3D wavefront). */
+dlic_status dlic_encode_volume(const dlic_model* m, const uint8_t* vol, uint32_t width, uint32_t height,
+                               uint32_t depth, const dlic_opts* opts, uint8_t** out, size_t* out_len);
+dlic_status dlic_decode_volume(const dlic_model* m, const uint8_t* bits, size_t len, uint8_t* vol,
+                               size_t vol_capacity);
 
 /* ---- unit ranges: one image's independent tiles split across GPUs ---------
  * (north_star: "independent image tiles with their own streams are

@@ -37,13 +37,15 @@ MAX_META = 8
 class dlic_opts(ctypes.Structure):
     _fields_ = [("precision", ctypes.c_uint32), ("group_rows", ctypes.c_uint32),
                 ("tile_w", ctypes.c_uint32), ("tile_h", ctypes.c_uint32),
-                ("n_meta", ctypes.c_uint32), ("meta", ctypes.POINTER(ctypes.c_float))]
+                ("n_meta", ctypes.c_uint32), ("meta", ctypes.POINTER(ctypes.c_float)),
+                ("volume_depth", ctypes.c_uint32)]
 
 
 class dlic_header(ctypes.Structure):
     _fields_ = [("width", ctypes.c_uint32), ("height", ctypes.c_uint32), ("precision", ctypes.c_uint32),
                 ("group_rows", ctypes.c_uint32), ("tile_w", ctypes.c_uint32), ("tile_h", ctypes.c_uint32),
                 ("n_streams", ctypes.c_uint32), ("n_units", ctypes.c_uint32), ("numerics", ctypes.c_uint32),
+                ("depth", ctypes.c_uint32),
                 ("n_meta", ctypes.c_uint32), ("meta", ctypes.c_float * MAX_META),
                 ("model_sha256", ctypes.c_uint8 * 32),
                 ("payload_bytes", ctypes.c_uint64), ("header_bytes", ctypes.c_uint64)]
@@ -99,6 +101,9 @@ def _setup(lib):
          ctypes.c_uint32, _vp, ctypes.c_size_t, c_u8pp, ctypes.POINTER(ctypes.c_size_t))
     _sig(lib, "dlic_decode_units", _st, _vp, _vp, ctypes.c_size_t, ctypes.c_uint32, ctypes.c_uint32, _vp,
          ctypes.c_size_t)
+    _sig(lib, "dlic_encode_volume", _st, _vp, _vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+         ctypes.POINTER(dlic_opts), c_u8pp, ctypes.POINTER(ctypes.c_size_t))
+    _sig(lib, "dlic_decode_volume", _st, _vp, _vp, ctypes.c_size_t, _vp, ctypes.c_size_t)
 
 
 def _L():
@@ -132,10 +137,11 @@ def _check(s):
         raise DlicError(s, _L().dlic_last_error().decode(errors="replace"))
 
 
-def _opts(precision=PREC_BF16, group_rows=32, tile=(0, 0), meta=None):
+def _opts(precision=PREC_BF16, group_rows=32, tile=(0, 0), meta=None, volume_depth=0):
     """meta: raw metadata reals, (n_meta,) for one image or (n, n_meta) for a
-    batch.  The returned struct keeps the float32 array alive."""
-    o = dlic_opts(precision, group_rows, tile[0], tile[1], 0, None)
+    batch.  volume_depth: 0 = 2D images, D = volumes of D slices.  The
+    returned struct keeps the float32 array alive."""
+    o = dlic_opts(precision, group_rows, tile[0], tile[1], 0, None, volume_depth)
     if meta is not None:
         m = np.ascontiguousarray(np.asarray(meta, dtype=np.float32))
         o._meta_keep = m
@@ -235,45 +241,50 @@ def dlic_decode(model: Model, bits: bytes) -> np.ndarray:
     return img
 
 
-def dlic_encode_batch(model: Model, imgs: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0), meta=None):
-    """imgs (n, H, W) u8 host -> (blob, sizes): the n containers back to back.
-    meta: (n, n_meta) raw metadata reals per image."""
+def dlic_encode_batch(model: Model, imgs: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0), meta=None,
+                      volume_depth=0):
+    """imgs (n, H, W) u8 host -> (blob, sizes): the containers back to back
+    (n, or n / volume_depth volumes).  meta: raw metadata reals per container."""
     imgs = np.ascontiguousarray(imgs, dtype=np.uint8)
     n, h, w = imgs.shape
     out = c_u8p()
     tot = ctypes.c_size_t()
-    sizes = np.zeros(n, np.uint64)
-    o = _opts(precision, group_rows, tile, meta)
+    sizes = np.zeros(n // volume_depth if volume_depth else n, np.uint64)
+    o = _opts(precision, group_rows, tile, meta, volume_depth)
     _check(_L().dlic_encode_batch(model.handle, imgs.ctypes.data, n, w, h, ctypes.byref(o), ctypes.byref(out),
                                   ctypes.byref(tot), sizes.ctypes.data))
     return _take(out, tot.value), [int(x) for x in sizes]
 
 
 def dlic_decode_batch(model: Model, blob: bytes, sizes) -> np.ndarray:
-    """n containers back to back (sizes[i] bytes each) -> (n, H, W) u8."""
+    """containers back to back (sizes[i] bytes each) -> (n, H, W) u8 (a volume
+    container contributes its depth slices)."""
     sizes = [int(x) for x in sizes]
     offs = np.zeros(len(sizes), np.uint64)
     offs[1:] = np.cumsum(sizes[:-1])
     hd = dlic_peek(blob[:sizes[0]])
-    imgs = np.empty((len(sizes), hd["height"], hd["width"]), np.uint8)
+    imgs = np.empty((len(sizes) * max(1, hd["depth"]), hd["height"], hd["width"]), np.uint8)
     _check(_L().dlic_decode_batch(model.handle, blob, len(blob), offs.ctypes.data, len(sizes), imgs.ctypes.data,
                                   imgs.size))
     return imgs
 
 
-def dlic_max_container_bytes(width, height, precision=PREC_BF16, group_rows=32, tile=(0, 0), meta=None) -> int:
-    o = _opts(precision, group_rows, tile, meta)
+def dlic_max_container_bytes(width, height, precision=PREC_BF16, group_rows=32, tile=(0, 0), meta=None,
+                             volume_depth=0) -> int:
+    """Per container (a volume container holds volume_depth slices)."""
+    o = _opts(precision, group_rows, tile, meta, volume_depth)
     return int(_L().dlic_max_container_bytes(width, height, ctypes.byref(o)))
 
 
 # ------------------------------------------------------------------ parity taps
 def dlic_rans_encode_tables(fc: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0),
                             model_sha: bytes | None = None, meta=None) -> bytes:
+    """fc (H, W), or (D, H, W) for a volume container."""
     fc = np.ascontiguousarray(fc, dtype=np.uint32)
-    h, w = fc.shape
+    h, w = fc.shape[-2:]
     out = c_u8p()
     n = ctypes.c_size_t()
-    o = _opts(precision, group_rows, tile, meta)
+    o = _opts(precision, group_rows, tile, meta, fc.shape[0] if fc.ndim == 3 else 0)
     sha = ctypes.create_string_buffer(model_sha, 32) if model_sha else None
     _check(_L().dlic_rans_encode_tables(fc.ctypes.data, w, h, ctypes.byref(o), sha, ctypes.byref(out),
                                         ctypes.byref(n)))
@@ -283,22 +294,25 @@ def dlic_rans_encode_tables(fc: np.ndarray, precision=PREC_BF16, group_rows=32, 
 def dlic_rans_decode_tables(bits: bytes, freq_tables: np.ndarray) -> np.ndarray:
     hd = dlic_peek(bits)
     ft = np.ascontiguousarray(freq_tables, dtype=np.uint16)
-    assert ft.shape == (hd["height"], hd["width"], 256)
-    img = np.empty((hd["height"], hd["width"]), np.uint8)
+    shape = ((hd["depth"],) if hd["depth"] else ()) + (hd["height"], hd["width"])
+    assert ft.shape == shape + (256,)
+    img = np.empty(shape, np.uint8)
     _check(_L().dlic_rans_decode_tables(bits, len(bits), ft.ctypes.data, img.ctypes.data))
     return img
 
 
 def dlic_debug_mlp(model: Model, img: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0),
                    logits=True, probs=True, freqs=True, fc=True, meta=None) -> dict:
+    """img (H, W), or (D, H, W) for a volume (3D window)."""
     img = np.ascontiguousarray(img, dtype=np.uint8)
-    h, w = img.shape
+    h, w = img.shape[-2:]
+    lead = img.shape[:-2]
     out = {}
-    lg = np.empty((h, w, 256), np.float32) if logits else None
-    pb = np.empty((h, w, 256), np.float32) if probs else None
-    fq = np.empty((h, w, 256), np.uint16) if freqs else None
-    f = np.empty((h, w), np.uint32) if fc else None
-    o = _opts(precision, group_rows, tile, meta)
+    lg = np.empty(lead + (h, w, 256), np.float32) if logits else None
+    pb = np.empty(lead + (h, w, 256), np.float32) if probs else None
+    fq = np.empty(lead + (h, w, 256), np.uint16) if freqs else None
+    f = np.empty(lead + (h, w), np.uint32) if fc else None
+    o = _opts(precision, group_rows, tile, meta, img.shape[0] if img.ndim == 3 else 0)
     _check(_L().dlic_debug_mlp(model.handle, img.ctypes.data, w, h, ctypes.byref(o),
                                lg.ctypes.data if logits else None, pb.ctypes.data if probs else None,
                                fq.ctypes.data if freqs else None, f.ctypes.data if fc else None))
@@ -316,19 +330,20 @@ def _stream_handle(stream):
 
 
 def dlic_encode_batch_device(model: Model, d_imgs, precision=PREC_BF16, group_rows=32, tile=(0, 0),
-                             d_out=None, d_sizes=None, stream=None, meta=None):
+                             d_out=None, d_sizes=None, stream=None, meta=None, volume_depth=0):
     """d_imgs: torch uint8 CUDA tensor (n, H, W).  Returns (d_out, d_sizes, stride):
     container i occupies d_out[i*stride : i*stride + d_sizes[i]]."""
     import torch
     n, h, w = d_imgs.shape
-    stride = dlic_max_container_bytes(w, h, precision, group_rows, tile, meta)
+    stride = dlic_max_container_bytes(w, h, precision, group_rows, tile, meta, volume_depth)
     if stride == 0:
         raise DlicError(1, "unsupported options")
+    nc = n // volume_depth if volume_depth else n
     if d_out is None:
-        d_out = torch.empty(n * stride, dtype=torch.uint8, device=d_imgs.device)
+        d_out = torch.empty(nc * stride, dtype=torch.uint8, device=d_imgs.device)
     if d_sizes is None:
-        d_sizes = torch.empty(n, dtype=torch.int64, device=d_imgs.device)
-    o = _opts(precision, group_rows, tile, meta)
+        d_sizes = torch.empty(nc, dtype=torch.int64, device=d_imgs.device)
+    o = _opts(precision, group_rows, tile, meta, volume_depth)
     _check(_L().dlic_encode_batch_device(model.handle, _vp(d_imgs.data_ptr()), n, w, h, ctypes.byref(o),
                                          _vp(d_out.data_ptr()), d_out.numel(), _vp(d_sizes.data_ptr()),
                                          _stream_handle(stream)))
@@ -403,6 +418,26 @@ def dlic_decode_units(model: Model, bits: bytes, unit_lo: int, unit_hi: int, img
     assert img.flags.c_contiguous and img.dtype == np.uint8
     _check(_L().dlic_decode_units(model.handle, bits, len(bits), unit_lo, unit_hi, img.ctypes.data, img.size))
     return img
+
+
+def dlic_encode_volume(model: Model, vol: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0),
+                       meta=None) -> bytes:
+    """vol (D, H, W) u8 -> one volume container (3D window)."""
+    vol = np.ascontiguousarray(vol, dtype=np.uint8)
+    d, h, w = vol.shape
+    out = c_u8p()
+    n = ctypes.c_size_t()
+    o = _opts(precision, group_rows, tile, meta)
+    _check(_L().dlic_encode_volume(model.handle, vol.ctypes.data, w, h, d, ctypes.byref(o), ctypes.byref(out),
+                                   ctypes.byref(n)))
+    return _take(out, n.value)
+
+
+def dlic_decode_volume(model: Model, bits: bytes) -> np.ndarray:
+    hd = dlic_peek(bits)
+    vol = np.empty((hd["depth"], hd["height"], hd["width"]), np.uint8)
+    _check(_L().dlic_decode_volume(model.handle, bits, len(bits), vol.ctypes.data, vol.size))
+    return vol
 
 
 def dlic_numerics_rev() -> int:

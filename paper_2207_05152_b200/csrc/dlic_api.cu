@@ -32,6 +32,7 @@ struct dlic_model {
   std::vector<uint32_t> dims;
   bool p100k = false;  // topology the GPU engines run (see dlic_model_load)
   uint32_t n_meta = 0;
+  bool in3d = false;   // 87 window inputs: the 3D window (R13)
   uint8_t* d_wimg = nullptr;
   float* d_bias = nullptr;
   float* d_w32 = nullptr;
@@ -239,11 +240,14 @@ uint16_t bf16_bits(float f) {
 // after layer l is linear, so layer l+1 with K = 128/g inputs becomes an
 // equivalent layer with K = 128 whose row k is W[k / g] / g (exact in fp32 and
 // bf16: g is a power of two).  Returns false for topologies outside the engines.
-static bool engine_weights(const ParsedModel& pm, std::vector<std::vector<float>>& W, uint32_t& n_meta) {
+static bool engine_weights(const ParsedModel& pm, std::vector<std::vector<float>>& W, uint32_t& n_meta,
+                           bool& in3d) {
   if (pm.W.size() != (size_t)NLAYER) return false;
-  if (pm.dims[0] < (uint32_t)KIN || pm.dims[0] > (uint32_t)KIN + DLIC_MAX_META) return false;
-  n_meta = pm.dims[0] - KIN;
-  if (pm.meta_range.size() != 2 * (size_t)n_meta) return false;
+  n_meta = (uint32_t)(pm.meta_range.size() / 2);
+  if (n_meta > DLIC_MAX_META) return false;
+  const uint32_t kwin = pm.dims[0] - n_meta;  // window inputs: 78 (2D) or 87 (3D)
+  if (kwin != (uint32_t)KIN && kwin != (uint32_t)KIN3) return false;
+  in3d = kwin == (uint32_t)KIN3;
   for (int l = 0; l < NLAYER; ++l)
     if (pm.dims[l + 1] != (uint32_t)layer_n(l)) return false;  // outputs 128 x5, 256
   if (pm.pool[NLAYER - 1] != 0) return false;
@@ -264,9 +268,12 @@ dlic_status upload_model(dlic_model* m, const ParsedModel& pm_in) {
   m->dims = pm_in.dims;
   std::vector<std::vector<float>> Wf;
   uint32_t n_meta = 0;
-  m->p100k = engine_weights(pm_in, Wf, n_meta);
+  bool in3d = false;
+  m->p100k = engine_weights(pm_in, Wf, n_meta, in3d);
   if (!m->p100k) return DLIC_OK;  // loadable; GPU engines refuse it at encode/decode
   m->n_meta = n_meta;
+  m->in3d = in3d;
+  const uint32_t kwin = in3d ? (uint32_t)KIN3 : (uint32_t)KIN;  // metadata rows follow the window rows
   ParsedModel pm = pm_in;
   pm.W = Wf;  // pooling folded; W1 keeps its KIN + n_meta rows (the packers below read rows < KIN)
   // bf16 UMMA image: layer l, element (n, k) of B = W^T at
@@ -284,7 +291,7 @@ dlic_status upload_model(dlic_model* m, const ParsedModel& pm_in) {
         memcpy(&img[a], &u, 2);
       }
   }
-  std::vector<float> bias(BIAS_TOTAL + FRESH_FLOATS);
+  std::vector<float> bias(BIAS_TOTAL + FRESH_FLOATS + (in3d ? W3D_WORDS : 0));
   for (int l = 0; l < NLAYER; ++l)
     for (int n = 0; n < layer_n(l); ++n) bias[(l < NLAYER - 1 ? l * HID : BIAS_OFF_LAST) + n] = pm.b[l][n];
   // fresh-tap weights (bf16-rounded like the MMA image), float4 per pair n, n+1
@@ -299,16 +306,28 @@ dlic_status upload_model(dlic_model* m, const ParsedModel& pm_in) {
     bias[q] = bf16f(pm.W[0][(size_t)TAP_FA * HID + n]);
     bias[q + 2] = bf16f(pm.W[0][(size_t)TAP_FB * HID + n]);
   }
-  std::vector<float> w32(f32_off(NLAYER));
+  if (in3d) {  // lower-layer (3D) tap weights, bf16 pairs: word k*64 + n/2 = (W[78+k][n], W[78+k][n+1])
+    for (int k = 0; k < 9; ++k)
+      for (int n = 0; n < HID; n += 2) {
+        const uint32_t lo = bf16_bits(pm.W[0][(size_t)(KIN + k) * HID + n]);
+        const uint32_t hi = bf16_bits(pm.W[0][(size_t)(KIN + k) * HID + n + 1]);
+        const uint32_t u = lo | (hi << 16);
+        memcpy(&bias[W3D_OFF + (size_t)k * (HID / 2) + n / 2], &u, 4);
+      }
+  }
+  // fp32 blob: layer 0 has the window rows (78 or 87), the others as packed
+  std::vector<float> w32(f32_off(NLAYER) + (in3d ? (size_t)(KIN3 - KIN) * HID : 0));
+  size_t o32 = 0;
   for (int l = 0; l < NLAYER; ++l) {
-    const int K = f32_k(l), N = layer_n(l);
-    memcpy(&w32[f32_off(l)], pm.W[l].data(), 4 * (size_t)K * N);
-    memcpy(&w32[f32_off(l) + (size_t)K * N], pm.b[l].data(), 4 * (size_t)N);
+    const int K = l == 0 ? (int)kwin : f32_k(l), N = layer_n(l);
+    memcpy(&w32[o32], pm.W[l].data(), 4 * (size_t)K * N);
+    memcpy(&w32[o32 + (size_t)K * N], pm.b[l].data(), 4 * (size_t)N);
+    o32 += (size_t)K * N + N;
   }
   if (n_meta) {  // metadata rows of W1 and their normalisation constants
     std::vector<float> wm((size_t)n_meta * HID);
     for (uint32_t k = 0; k < n_meta; ++k)
-      for (int n = 0; n < HID; ++n) wm[(size_t)k * HID + n] = pm.W[0][(size_t)(KIN + k) * HID + n];
+      for (int n = 0; n < HID; ++n) wm[(size_t)k * HID + n] = pm.W[0][(size_t)(kwin + k) * HID + n];
     CUDA_TRY(cudaMalloc(&m->d_wmeta, wm.size() * 4));
     CUDA_TRY(cudaMalloc(&m->d_range, pm.meta_range.size() * 4));
     CUDA_TRY(cudaMemcpy(m->d_wmeta, wm.data(), wm.size() * 4, cudaMemcpyHostToDevice));
@@ -325,7 +344,7 @@ dlic_status upload_model(dlic_model* m, const ParsedModel& pm_in) {
 
 // ---------------------------------------------------------------- planning
 dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Plan& p) {
-  dlic_opts d = {DLIC_PREC_BF16, 32, 0, 0, 0, nullptr};
+  dlic_opts d = {DLIC_PREC_BF16, 32, 0, 0, 0, nullptr, 0};
   if (o) d = *o;
   if (d.group_rows == 0) d.group_rows = 32;
   if (d.n_meta > DLIC_MAX_META) return fail(DLIC_E_INVALID_ARG, "more than DLIC_MAX_META metadata reals");
@@ -352,11 +371,19 @@ dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Pl
   const uint32_t hl = H - (p.nty - 1) * p.th;
   p.gpl = (hl + p.G - 1) / p.G;
   p.spi = (p.nty - 1) * p.ntx * p.gpt + p.ntx * p.gpl;
-  if (dec_smem_bytes(d.precision, std::max(p.gpt, (H - (p.nty - 1) * p.th + p.G - 1) / p.G)) > dec_smem_limit())
+  if (dec_smem_bytes(d.precision, std::max(p.gpt, (H - (p.nty - 1) * p.th + p.G - 1) / p.G),
+                     d.volume_depth > 0 ? 1u : 0u) > dec_smem_limit())
     return fail(DLIC_E_INVALID_ARG, "too many row groups per unit for the decoder's shared memory: raise group_rows or tile");
   p.cap_words = 2 * p.G + p.G * p.tw;
   p.n_meta = d.n_meta;
-  p.hdr_bytes = HDR_FIXED + 4 * p.spi + 4 + 4 * p.n_meta;  // + the metadata block
+  // volumes: depth slices per container (window id 2); 2D: one image each
+  p.w3d = d.volume_depth > 0 ? 1u : 0u;
+  p.depth = d.volume_depth > 0 ? d.volume_depth : 1u;
+  if (n % p.depth) return fail(DLIC_E_SHAPE_MISMATCH, "image count is not a multiple of volume_depth");
+  p.n_cont = n / p.depth;
+  if ((uint64_t)p.spi * p.depth >= (1ull << 24)) return fail(DLIC_E_INVALID_ARG, "too many streams per volume");
+  p.spc = p.spi * p.depth;
+  p.hdr_bytes = HDR_FIXED + 4 * p.spc + 4 + 4 * p.n_meta;  // + the metadata block
   p.u_lo = 0;
   p.u_cnt = n * p.upi;
   p.s_lo = 0;
@@ -373,7 +400,7 @@ dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Pl
     }
   if (p.nc == 0) return fail(DLIC_E_INVALID_ARG, "unit wider than 3072 px: use tiles (tile_w <= 3072)");
   uint64_t mc = p.hdr_bytes;
-  mc += (uint64_t)p.spi * (4ull * p.G + 2ull * p.G * p.tw);
+  mc += (uint64_t)p.spc * (4ull * p.G + 2ull * p.G * p.tw);
   p.max_container = (mc + 15) & ~15ull;
   return DLIC_OK;
 }
@@ -412,7 +439,7 @@ dlic_status check_schedulable(const Plan& p) {
   static std::map<std::tuple<int, uint32_t, uint32_t, size_t>, int> cache;
   int dev = 0;
   cudaGetDevice(&dev);
-  const size_t sm = dec_smem_bytes(p.precision, std::max(p.gpt, p.gpl));
+  const size_t sm = dec_smem_bytes(p.precision, std::max(p.gpt, p.gpl), p.w3d);
   const auto key = std::make_tuple(dev, p.precision, p.nc, sm);
   int n;
   {
@@ -435,7 +462,8 @@ dlic_status check_schedulable(const Plan& p) {
 dlic_status peek(const uint8_t* b, size_t len, dlic_header* h, std::vector<uint32_t>* sizes) {
   if (!b || len < HDR_FIXED) return fail(DLIC_E_CORRUPT_CONTAINER, "container shorter than its header");
   if (memcmp(b, "DLIC", 4) != 0) return fail(DLIC_E_CORRUPT_CONTAINER, "container magic");
-  if (b[4] != CONTAINER_VERSION || b[6] != 1) return fail(DLIC_E_VERSION_MISMATCH, "container version/window");
+  if (b[4] != CONTAINER_VERSION || (b[6] != 1 && b[6] != 2))
+    return fail(DLIC_E_VERSION_MISMATCH, "container version/window");
   if (b[7] != 0 || b[5] > 1) return fail(DLIC_E_CORRUPT_CONTAINER, "container fill/precision");
   dlic_header o = {};
   o.width = rd32(b + 8);
@@ -470,7 +498,13 @@ dlic_status peek(const uint8_t* b, size_t len, dlic_header* h, std::vector<uint3
   const bool tiled = o.tile_w && o.tile_h;
   const uint32_t tw = tiled ? std::min<uint32_t>(o.tile_w, o.width) : o.width;
   const uint32_t th = tiled ? std::min<uint32_t>(o.tile_h, o.height) : o.height;
-  o.n_units = ((o.width + tw - 1) / tw) * ((o.height + th - 1) / th);
+  const uint32_t ntx = (o.width + tw - 1) / tw, nty = (o.height + th - 1) / th;
+  const uint64_t spi = (uint64_t)(nty - 1) * ntx * ((th + o.group_rows - 1) / o.group_rows) +
+                       (uint64_t)ntx * ((o.height - (nty - 1) * th + o.group_rows - 1) / o.group_rows);
+  if (spi == 0 || o.n_streams % spi) return fail(DLIC_E_CORRUPT_CONTAINER, "stream count");
+  o.depth = b[6] == 2 ? (uint32_t)(o.n_streams / spi) : 0u;
+  if (b[6] == 1 && o.n_streams != spi) return fail(DLIC_E_CORRUPT_CONTAINER, "stream count");
+  o.n_units = ntx * nty * (o.depth ? o.depth : 1u);
   *h = o;
   return DLIC_OK;
 }
@@ -483,6 +517,7 @@ dlic_opts opts_of(const dlic_header& h) {
   o.tile_h = h.tile_h;
   o.n_meta = h.n_meta;
   o.meta = h.meta;  // points into h
+  o.volume_depth = h.depth;
   return o;
 }
 
@@ -508,6 +543,9 @@ dlic_status meta_bias(const dlic_model* m, const Plan& p, const float* h_meta, c
                       float** d_meta_out) {
   *out = nullptr;
   if (d_meta_out) *d_meta_out = nullptr;
+  if ((p.w3d != 0) != m->in3d)
+    return fail(DLIC_E_SHAPE_MISMATCH, m->in3d ? "a 3D-window model codes volumes (opts.volume_depth >= 1)"
+                                               : "volumes need a 3D-window model (87 window inputs)");
   if (p.n_meta != m->n_meta)
     return fail(DLIC_E_SHAPE_MISMATCH, "metadata count " + std::to_string(p.n_meta) + " != the model's " +
                                            std::to_string(m->n_meta));
@@ -515,9 +553,9 @@ dlic_status meta_bias(const dlic_model* m, const Plan& p, const float* h_meta, c
   if (!d_bits && !h_meta) return fail(DLIC_E_INVALID_ARG, "the model needs metadata (opts.meta)");
   float* d_out;
   float* d_meta = nullptr;
-  CUDA_TRY(sc.alloc(&d_out, 4ull * p.n_img * HID));
+  CUDA_TRY(sc.alloc(&d_out, 4ull * p.n_cont * HID));
   if (!d_bits) {
-    const size_t nb = 4ull * p.n_img * p.n_meta;
+    const size_t nb = 4ull * p.n_cont * p.n_meta;
     CUDA_TRY(sc.alloc(&d_meta, nb));
     void* pin = g_pin_meta.get(nb);
     if (pin) {
@@ -531,9 +569,19 @@ dlic_status meta_bias(const dlic_model* m, const Plan& p, const float* h_meta, c
     }
     if (d_meta_out) *d_meta_out = d_meta;
   }
-  CUDA_TRY(launch_meta_bias(p.n_img, p.n_meta, d_meta, d_bits, d_cont_off, HDR_FIXED + 4u * p.spi + 4u, m->d_range,
+  CUDA_TRY(launch_meta_bias(p.n_cont, p.n_meta, d_meta, d_bits, d_cont_off, HDR_FIXED + 4u * p.spc + 4u, m->d_range,
                             m->d_wmeta, m->d_bias, p.precision, d_out, st));
   *out = d_out;
+  return DLIC_OK;
+}
+
+// volumes: the decoder's unit ticket + per-unit progress flags (zeroed)
+dlic_status alloc_sync(const Plan& p, Scratch& sc, cudaStream_t st, uint32_t** out) {
+  *out = nullptr;
+  const size_t n = sync_words(p);
+  if (!n) return DLIC_OK;
+  CUDA_TRY(sc.alloc(out, 4 * n));
+  CUDA_TRY(cudaMemsetAsync(*out, 0, 4 * n, st));
   return DLIC_OK;
 }
 
@@ -667,8 +715,8 @@ dlic_status dlic_model_sha256(const dlic_model* m, uint8_t out[32]) {
 }
 
 size_t dlic_max_container_bytes(uint32_t width, uint32_t height, const dlic_opts* opts) {
-  Plan p;
-  if (make_plan(width, height, 1, opts, p) != DLIC_OK) return 0;
+  Plan p;  // one container: one image, or one volume of volume_depth slices
+  if (make_plan(width, height, opts && opts->volume_depth ? opts->volume_depth : 1u, opts, p) != DLIC_OK) return 0;
   return p.max_container;
 }
 
@@ -731,7 +779,9 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
     return fail(DLIC_E_VERSION_MISMATCH, "container tables come from another arithmetic revision (numerics " +
                                              std::to_string(h.numerics) + ", this build " +
                                              std::to_string(NUMERICS_REV) + ")");
-  if (!img || cap < (size_t)h.width * h.height) return fail(DLIC_E_BUFFER_TOO_SMALL, "image buffer");
+  const uint32_t nsl = h.depth ? h.depth : 1u;  // slices (a volume container holds depth of them)
+  const size_t npx = (size_t)h.width * h.height * nsl;
+  if (!img || cap < npx) return fail(DLIC_E_BUFFER_TOO_SMALL, "image buffer");
   if (m) {
     s = check_model_gpu(m);
   } else {
@@ -742,10 +792,11 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
   if (s != DLIC_OK) return s;
   dlic_opts o = opts_of(h);
   Plan p;
-  s = make_plan(h.width, h.height, 1, &o, p);
+  s = make_plan(h.width, h.height, nsl, &o, p);
   if (s != DLIC_OK) return s;
-  if (p.spi != h.n_streams) return fail(DLIC_E_CORRUPT_CONTAINER, "stream count does not match the header dims");
+  if (p.spc != h.n_streams) return fail(DLIC_E_CORRUPT_CONTAINER, "stream count does not match the header dims");
   const bool part = unit_hi > 0;  // dlic_decode_units: only units [unit_lo, unit_hi)
+  if (part && p.depth > 1) return fail(DLIC_E_INVALID_ARG, "unit ranges are for 2D images");
   if (part) {
     s = restrict_units(p, unit_lo, unit_hi);
     if (s != DLIC_OK) return s;
@@ -761,9 +812,9 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
   int32_t* d_status;
   uint64_t* d_meta;  // [0] = container offset (0), [1] = length
   CUDA_TRY(sc.alloc(&d_bits, len));
-  CUDA_TRY(sc.alloc(&d_img, (size_t)h.width * h.height));
-  CUDA_TRY(sc.alloc(&d_sbase, 4ull * p.spi));
-  CUDA_TRY(sc.alloc(&d_slen, 4ull * p.spi));
+  CUDA_TRY(sc.alloc(&d_img, npx));
+  CUDA_TRY(sc.alloc(&d_sbase, 4ull * p.spc));
+  CUDA_TRY(sc.alloc(&d_slen, 4ull * p.spc));
   CUDA_TRY(sc.alloc(&d_status, 4));
   CUDA_TRY(sc.alloc(&d_meta, 16));
   uint8_t* pin = static_cast<uint8_t*>(g_pin_in.get(len + 16));
@@ -776,10 +827,10 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
   CUDA_TRY(cudaMemcpyAsync(d_bits, pin + 16, len, cudaMemcpyHostToDevice, st));
   CUDA_TRY(launch_dec_prep(p, d_bits, d_meta, d_meta + 1, d_sbase, d_slen, d_status, st, tables == nullptr));
   if (part)  // pixels outside the unit range come back untouched (pageable copy: no staging reuse)
-    CUDA_TRY(cudaMemcpyAsync(d_img, img, (size_t)h.width * h.height, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(d_img, img, npx, cudaMemcpyHostToDevice, st));
   if (tables) {
     uint16_t* d_tab;
-    const size_t tb = (size_t)h.width * h.height * NOUT * 2;
+    const size_t tb = npx * NOUT * 2;
     CUDA_TRY(sc.alloc(&d_tab, tb));
     CUDA_TRY(cudaMemcpyAsync(d_tab, tables, tb, cudaMemcpyHostToDevice, st));
     ev_begin("decode", st);
@@ -796,31 +847,37 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
     const float* b1img = nullptr;  // metadata re-read from the container (device)
     s = meta_bias(m, p, nullptr, d_bits, d_meta, st, sc, &b1img);
     if (s != DLIC_OK) return s;
-    CUDA_TRY(launch_decode(p, m->dw(b1img), d_bits, d_meta, d_sbase, d_slen, d_img, d_status, st, d_prof));
+    uint32_t* d_sync;
+    s = alloc_sync(p, sc, st, &d_sync);
+    if (s != DLIC_OK) return s;
+    CUDA_TRY(launch_decode(p, m->dw(b1img), d_bits, d_meta, d_sbase, d_slen, d_img, d_status, st, d_prof, d_sync));
     ev_end("decode", st);
     if (prof) {
       unsigned long long hp[40];
       CUDA_TRY(cudaMemcpyAsync(hp, d_prof, 40 * 8, cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
       const double ctas = (double)p.n_img * p.upi * p.nc;
-      const double T = (double)(p.tw + 3 * (p.th - 1));
+      const double T = (double)(p.tw + 3 * (p.th - 1));  // per-slice fronts
       const char* nm[11] = {"top", "gather", "put", "mlp", "pass1", "xchg", "bar7", "passA", "search", "rans",
                             "barrier"};
       fprintf(stderr, "[dlic prof] cycles per front per CTA:");
       for (int k = 0; k < 11; ++k) fprintf(stderr, " %s %.0f", nm[k], hp[k] / ctas / T);
       fprintf(stderr, "\n[dlic prof] network per front (sum over layers): sync %.0f issue+hook %.0f mma-wait %.0f "
               "epilogue %.0f\n", hp[16] / ctas / T, hp[17] / ctas / T, hp[18] / ctas / T, hp[19] / ctas / T);
+      if (p.w3d)
+        fprintf(stderr, "[dlic prof] 3D: waits for the slice below %.3f per front per CTA, %.0f cycles per wait\n",
+                hp[24] / ctas / T, hp[24] ? (double)hp[25] / hp[24] : 0.0);
     }
   }
-  uint8_t* ho = static_cast<uint8_t*>(g_pin_out.get((size_t)h.width * h.height + 64));
+  uint8_t* ho = static_cast<uint8_t*>(g_pin_out.get(npx + 64));
   if (!ho) return fail(DLIC_E_OUT_OF_MEMORY, "pinned staging");
   CUDA_TRY(cudaMemcpyAsync(ho, d_status, 4, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(ho + 64, d_img, (size_t)h.width * h.height, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(ho + 64, d_img, npx, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   int32_t stat;
   memcpy(&stat, ho, 4);
   if (stat != 0) return fail((dlic_status)stat, "lane invariant / framing check failed on the device");
-  memcpy(img, ho + 64, (size_t)h.width * h.height);
+  memcpy(img, ho + 64, npx);
   return DLIC_OK;
 }
 
@@ -834,7 +891,7 @@ dlic_status dlic_rans_decode_tables(const uint8_t* bits, size_t len, const uint1
   dlic_header h;
   dlic_status s = peek(bits, len, &h, nullptr);
   if (s != DLIC_OK) return s;
-  return decode_common(nullptr, bits, len, freq_tables, img, (size_t)h.width * h.height);
+  return decode_common(nullptr, bits, len, freq_tables, img, (size_t)h.width * h.height * (h.depth ? h.depth : 1u));
 }
 
 dlic_status dlic_rans_encode_tables(const uint32_t* fc, uint32_t width, uint32_t height, const dlic_opts* opts,
@@ -844,21 +901,24 @@ dlic_status dlic_rans_encode_tables(const uint32_t* fc, uint32_t width, uint32_t
   cudaGetDevice(&dev);
   dlic_status s = check_device(dev);
   if (s != DLIC_OK) return s;
+  const uint32_t nsl = opts && opts->volume_depth ? opts->volume_depth : 1u;  // a volume: fc[z][r][c]
+  const size_t npx = (size_t)width * height * nsl;
   Plan p;
-  s = make_plan(width, height, 1, opts, p);
+  s = make_plan(width, height, nsl, opts, p);
   if (s != DLIC_OK) return s;
   // tables must be valid: f >= 1 and c + f <= 2^16
-  for (size_t i = 0; i < (size_t)width * height; ++i) {
+  for (size_t i = 0; i < npx; ++i) {
     const uint32_t f = fc[i] & 0xFFFF, c = fc[i] >> 16;
     if (f == 0) return fail(DLIC_E_ZERO_FREQUENCY, "f_s == 0");
     if (c + f > 65536) return fail(DLIC_E_SUM_MISMATCH, "c_s + f_s > 2^16");
   }
   // fc arrives in image raster order; the kernels read it unit by unit
-  std::vector<uint32_t> fcu((size_t)width * height);
-  for (uint32_t u = 0; u < p.upi; ++u) {
+  std::vector<uint32_t> fcu(npx);
+  for (uint32_t u = 0; u < p.upi * nsl; ++u) {
     const Unit un = unit_info(p, u);
+    const size_t sl = (size_t)un.img * width * height;
     for (uint32_t r = 0; r < un.h; ++r)
-      memcpy(&fcu[un.fc_off + (size_t)r * un.w], &fc[(size_t)(un.y0 + r) * width + un.x0], 4ull * un.w);
+      memcpy(&fcu[un.fc_off + (size_t)r * un.w], &fc[sl + (size_t)(un.y0 + r) * width + un.x0], 4ull * un.w);
   }
   cudaStream_t st = my_stream();
   Scratch sc(st);
@@ -866,14 +926,14 @@ dlic_status dlic_rans_encode_tables(const uint32_t* fc, uint32_t width, uint32_t
   uint16_t* d_scr;
   uint64_t *d_dst, *d_size;
   uint8_t* d_out;
-  const uint64_t ns = p.spi;
-  CUDA_TRY(sc.alloc(&d_fc, 4ull * width * height));
+  const uint64_t ns = p.spc;
+  CUDA_TRY(sc.alloc(&d_fc, 4ull * npx));
   CUDA_TRY(sc.alloc(&d_scr, 2ull * p.cap_words * ns));
   CUDA_TRY(sc.alloc(&d_words, 4 * ns));
   CUDA_TRY(sc.alloc(&d_dst, 8 * ns));
   CUDA_TRY(sc.alloc(&d_size, 8));
   CUDA_TRY(sc.alloc(&d_out, p.max_container));
-  CUDA_TRY(cudaMemcpyAsync(d_fc, fcu.data(), 4ull * width * height, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_fc, fcu.data(), 4ull * npx, cudaMemcpyHostToDevice, st));
   CUDA_TRY(launch_rans_enc(p, d_fc, d_scr, d_words, st));
   float* d_mraw = nullptr;
   if (p.n_meta) {
@@ -900,12 +960,13 @@ dlic_status dlic_debug_mlp(const dlic_model* m, const uint8_t* img, uint32_t wid
   if (!img) return fail(DLIC_E_INVALID_ARG, "null image");
   dlic_status s = check_model_gpu(m);
   if (s != DLIC_OK) return s;
+  const uint32_t nsl = opts && opts->volume_depth ? opts->volume_depth : 1u;  // a volume: img holds nsl slices
   Plan p;
-  s = make_plan(width, height, 1, opts, p);
+  s = make_plan(width, height, nsl, opts, p);
   if (s != DLIC_OK) return s;
   cudaStream_t st = my_stream();
   Scratch sc(st);
-  const size_t npx = (size_t)width * height;
+  const size_t npx = (size_t)width * height * nsl;
   uint8_t* d_img;
   uint32_t* d_fc;
   float *d_lg = nullptr, *d_pb = nullptr;
@@ -930,10 +991,11 @@ dlic_status dlic_debug_mlp(const dlic_model* m, const uint8_t* img, uint32_t wid
   }
   CUDA_TRY(cudaStreamSynchronize(st));
   if (fc) {
-    for (uint32_t u = 0; u < p.upi; ++u) {
+    for (uint32_t u = 0; u < p.upi * nsl; ++u) {
       const Unit un = unit_info(p, u);
+      const size_t sl = (size_t)un.img * width * height;
       for (uint32_t r = 0; r < un.h; ++r)
-        memcpy(&fc[(size_t)(un.y0 + r) * width + un.x0], &fcu[un.fc_off + (size_t)r * un.w], 4ull * un.w);
+        memcpy(&fc[sl + (size_t)(un.y0 + r) * width + un.x0], &fcu[un.fc_off + (size_t)r * un.w], 4ull * un.w);
     }
   }
   return DLIC_OK;
@@ -956,16 +1018,17 @@ dlic_status dlic_encode_batch(const dlic_model* m, const uint8_t* imgs, uint32_t
   uint8_t *d_imgs, *d_out;
   uint64_t* d_sizes;
   CUDA_TRY(sc.alloc(&d_imgs, npx));
-  CUDA_TRY(sc.alloc(&d_out, p.max_container * n));
-  CUDA_TRY(sc.alloc(&d_sizes, 8ull * n));
+  const uint32_t nc = p.n_cont;  // containers (volumes hold volume_depth images each)
+  CUDA_TRY(sc.alloc(&d_out, p.max_container * nc));
+  CUDA_TRY(sc.alloc(&d_sizes, 8ull * nc));
   CUDA_TRY(h2d(d_imgs, imgs, npx, st));
   s = run_encode(m, p, d_imgs, d_out, p.max_container, d_sizes, st, sc, opts ? opts->meta : nullptr);
   if (s != DLIC_OK) return s;
-  std::vector<uint64_t> hs(n);
-  CUDA_TRY(cudaMemcpyAsync(hs.data(), d_sizes, 8ull * n, cudaMemcpyDeviceToHost, st));
+  std::vector<uint64_t> hs(nc);
+  CUDA_TRY(cudaMemcpyAsync(hs.data(), d_sizes, 8ull * nc, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   uint64_t total = 0;
-  for (uint32_t i = 0; i < n; ++i) {
+  for (uint32_t i = 0; i < nc; ++i) {
     if (hs[i] > p.max_container) return fail(DLIC_E_CUDA, "container size out of range");
     total += hs[i];
   }
@@ -973,7 +1036,7 @@ dlic_status dlic_encode_batch(const dlic_model* m, const uint8_t* imgs, uint32_t
   uint8_t* d_pack;
   CUDA_TRY(sc.alloc(&d_pack, total));
   uint64_t off = 0;
-  for (uint32_t i = 0; i < n; ++i) {
+  for (uint32_t i = 0; i < nc; ++i) {
     CUDA_TRY(cudaMemcpyAsync(d_pack + off, d_out + (size_t)i * p.max_container, hs[i], cudaMemcpyDeviceToDevice,
                              st));
     off += hs[i];
@@ -985,7 +1048,7 @@ dlic_status dlic_encode_batch(const dlic_model* m, const uint8_t* imgs, uint32_t
   uint8_t* res = static_cast<uint8_t*>(malloc(total ? total : 1));
   if (!res) return fail(DLIC_E_OUT_OF_MEMORY, "malloc");
   memcpy(res, hb, total);
-  for (uint32_t i = 0; i < n; ++i) sizes[i] = hs[i];
+  for (uint32_t i = 0; i < nc; ++i) sizes[i] = hs[i];
   *out = res;
   *out_len = total;
   return DLIC_OK;
@@ -1011,18 +1074,18 @@ dlic_status dlic_decode_batch(const dlic_model* m, const uint8_t* bits, size_t l
       return fail(DLIC_E_VERSION_MISMATCH, "container tables come from another arithmetic revision");
     if (i == 0) {
       h0 = h;
-    } else if (h.width != h0.width || h.height != h0.height || h.precision != h0.precision ||
+    } else if (h.width != h0.width || h.height != h0.height || h.precision != h0.precision || h.depth != h0.depth ||
                h.group_rows != h0.group_rows || h.tile_w != h0.tile_w || h.tile_h != h0.tile_h) {
       return fail(DLIC_E_SHAPE_MISMATCH, "batch containers differ in dims or options");
     }
   }
-  const size_t npx = (size_t)n * h0.width * h0.height;
+  const size_t npx = (size_t)n * h0.width * h0.height * (h0.depth ? h0.depth : 1u);
   if (img_capacity < npx) return fail(DLIC_E_BUFFER_TOO_SMALL, "image buffer");
   dlic_opts o = opts_of(h0);
   Plan p;
-  s = make_plan(h0.width, h0.height, n, &o, p);
+  s = make_plan(h0.width, h0.height, n * (h0.depth ? h0.depth : 1u), &o, p);
   if (s != DLIC_OK) return s;
-  if (p.spi != h0.n_streams) return fail(DLIC_E_CORRUPT_CONTAINER, "stream count does not match the header dims");
+  if (p.spc != h0.n_streams) return fail(DLIC_E_CORRUPT_CONTAINER, "stream count does not match the header dims");
   s = check_schedulable(p);
   if (s != DLIC_OK) return s;
   cudaStream_t st = my_stream();
@@ -1034,8 +1097,8 @@ dlic_status dlic_decode_batch(const dlic_model* m, const uint8_t* bits, size_t l
   CUDA_TRY(sc.alloc(&d_bits, len));
   CUDA_TRY(sc.alloc(&d_imgs, npx));
   CUDA_TRY(sc.alloc(&d_meta, 16ull * n));
-  CUDA_TRY(sc.alloc(&d_sbase, 4ull * n * p.spi));
-  CUDA_TRY(sc.alloc(&d_slen, 4ull * n * p.spi));
+  CUDA_TRY(sc.alloc(&d_sbase, 4ull * n * p.spc));
+  CUDA_TRY(sc.alloc(&d_slen, 4ull * n * p.spc));
   CUDA_TRY(sc.alloc(&d_status, 4ull * n));
   CUDA_TRY(cudaMemsetAsync(d_status, 0, 4ull * n, st));
   std::vector<uint64_t> meta(2ull * n);
@@ -1050,7 +1113,10 @@ dlic_status dlic_decode_batch(const dlic_model* m, const uint8_t* bits, size_t l
   s = meta_bias(m, p, nullptr, d_bits, d_meta, st, sc, &b1img);
   if (s != DLIC_OK) return s;
   ev_begin("decode", st);
-  CUDA_TRY(launch_decode(p, m->dw(b1img), d_bits, d_meta, d_sbase, d_slen, d_imgs, d_status, st));
+  uint32_t* d_sync;
+  s = alloc_sync(p, sc, st, &d_sync);
+  if (s != DLIC_OK) return s;
+  CUDA_TRY(launch_decode(p, m->dw(b1img), d_bits, d_meta, d_sbase, d_slen, d_imgs, d_status, st, nullptr, d_sync));
   ev_end("decode", st);
   uint8_t* ho = static_cast<uint8_t*>(g_pin_out.get(npx + 4ull * n + 64));
   if (!ho) return fail(DLIC_E_OUT_OF_MEMORY, "pinned staging");
@@ -1076,7 +1142,8 @@ dlic_status dlic_encode_batch_device(const dlic_model* m, const uint8_t* d_imgs,
   Plan p;
   s = make_plan(width, height, n, opts, p);
   if (s != DLIC_OK) return s;
-  if (out_capacity < p.max_container * n) return fail(DLIC_E_BUFFER_TOO_SMALL, "out_capacity < n * max bytes");
+  if (out_capacity < p.max_container * p.n_cont)
+    return fail(DLIC_E_BUFFER_TOO_SMALL, "out_capacity < containers * max bytes");
   s = check_schedulable(p);
   if (s != DLIC_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
@@ -1098,7 +1165,7 @@ dlic_status dlic_decode_batch_device(const dlic_model* m, const uint8_t* d_bits,
     return fail(DLIC_E_VERSION_MISMATCH, "container tables come from another arithmetic revision");
   dlic_opts o = opts_of(*h_header);
   Plan p;
-  s = make_plan(h_header->width, h_header->height, n, &o, p);
+  s = make_plan(h_header->width, h_header->height, n * (h_header->depth ? h_header->depth : 1u), &o, p);
   if (s != DLIC_OK) return s;
   s = check_schedulable(p);
   if (s != DLIC_OK) return s;
@@ -1107,8 +1174,8 @@ dlic_status dlic_decode_batch_device(const dlic_model* m, const uint8_t* d_bits,
   uint64_t* d_meta;  // [0, n) offsets, [n, 2n) lengths
   uint32_t *d_sbase, *d_slen;
   CUDA_TRY(sc.alloc(&d_meta, 16ull * n));
-  CUDA_TRY(sc.alloc(&d_sbase, 4ull * n * p.spi));
-  CUDA_TRY(sc.alloc(&d_slen, 4ull * n * p.spi));
+  CUDA_TRY(sc.alloc(&d_sbase, 4ull * n * p.spc));
+  CUDA_TRY(sc.alloc(&d_slen, 4ull * n * p.spc));
   CUDA_TRY(cudaMemcpyAsync(d_meta, h_offsets, 8ull * n, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(d_meta + n, h_lengths, 8ull * n, cudaMemcpyHostToDevice, st));
   // k_dec_prep checks every header and stream size against its container's
@@ -1118,9 +1185,33 @@ dlic_status dlic_decode_batch_device(const dlic_model* m, const uint8_t* d_bits,
   s = meta_bias(m, p, nullptr, d_bits, d_meta, st, sc, &b1img);
   if (s != DLIC_OK) return s;
   ev_begin("decode", st);
-  CUDA_TRY(launch_decode(p, m->dw(b1img), d_bits, d_meta, d_sbase, d_slen, d_imgs, d_status, st));
+  uint32_t* d_sync;
+  s = alloc_sync(p, sc, st, &d_sync);
+  if (s != DLIC_OK) return s;
+  CUDA_TRY(launch_decode(p, m->dw(b1img), d_bits, d_meta, d_sbase, d_slen, d_imgs, d_status, st, nullptr, d_sync));
   ev_end("decode", st);
   return DLIC_OK;
+}
+
+// ---- volumes (§8(f) f2)
+dlic_status dlic_encode_volume(const dlic_model* m, const uint8_t* vol, uint32_t width, uint32_t height,
+                               uint32_t depth, const dlic_opts* opts, uint8_t** out, size_t* out_len) {
+  if (depth == 0) return fail(DLIC_E_INVALID_ARG, "depth = 0");
+  dlic_opts o = opts ? *opts : dlic_opts{DLIC_PREC_BF16, 32, 0, 0, 0, nullptr, 0};
+  o.volume_depth = depth;
+  uint64_t size = 0;
+  return dlic_encode_batch(m, vol, depth, width, height, &o, out, out_len, &size);
+}
+
+dlic_status dlic_decode_volume(const dlic_model* m, const uint8_t* bits, size_t len, uint8_t* vol,
+                               size_t vol_capacity) {
+  if (!m) return fail(DLIC_E_INVALID_ARG, "null model");
+  dlic_header h;
+  dlic_status s = peek(bits, len, &h, nullptr);
+  if (s != DLIC_OK) return s;
+  if (h.depth == 0) return fail(DLIC_E_SHAPE_MISMATCH, "not a volume container (window id 1)");
+  const uint64_t off = 0;
+  return dlic_decode_batch(m, bits, len, &off, 1, vol, vol_capacity);
 }
 
 // ---- unit ranges (multi-GPU sharding of one image's independent tiles)
@@ -1187,7 +1278,7 @@ dlic_status dlic_container_build(uint32_t width, uint32_t height, const dlic_opt
   Plan p;
   dlic_status s = make_plan(width, height, 1, opts, p);
   if (s != DLIC_OK) return s;
-  if (n_streams != p.spi) return fail(DLIC_E_SHAPE_MISMATCH, "stream count does not match (width, height, opts)");
+  if (n_streams != p.spc) return fail(DLIC_E_SHAPE_MISMATCH, "stream count does not match (width, height, opts)");
   if (p.n_meta && !opts->meta) return fail(DLIC_E_INVALID_ARG, "opts.n_meta > 0 but opts.meta is null");
   uint64_t tot = 0;
   for (uint32_t i = 0; i < n_streams; ++i) {

@@ -29,6 +29,7 @@ namespace dlic {
 
 // ---------------------------------------------------------------- constants
 constexpr int KIN = 78;        // causal 9x9 window (R1)
+constexpr int KIN3 = 87;       // + the 3x3 box of the slice below (3D window R13)
 constexpr int KPAD = 80;       // layer-1 K padded to a multiple of 16 for kind::f16
 constexpr int HID = 128;       // P100K hidden width (R4)
 constexpr int NOUT = 256;      // 8-bit alphabet
@@ -89,6 +90,13 @@ constexpr int TAP_FB = 71;  // (dr, dc) = (-1, +2)
 constexpr int FRESH_OFF = BIAS_TOTAL;
 constexpr int FRESH_FLOATS = 2 * HID;
 constexpr uint32_t BIAS_BYTES = (BIAS_TOTAL + FRESH_FLOATS) * 4;
+// 3D models: the 9 lower-layer taps' layer-1 weights after the fresh table,
+// bf16 pairs [9][HID/2] (2,304 B; only loaded for 3D plans).  Their
+// contribution is added to the layer-1 bias term on the CUDA cores (the taps
+// were decoded long before, so it never waits), keeping the MMA at K = 80.
+constexpr int W3D_OFF = BIAS_TOTAL + FRESH_FLOATS;
+constexpr int W3D_WORDS = 9 * HID / 2;
+constexpr uint32_t W3D_BYTES = W3D_WORDS * 4;
 
 // fp32 weight blob: per layer W[K][N] then b[N]; K of layer 0 is KIN (78)
 __host__ __device__ constexpr int f32_k(int l) { return l == 0 ? KIN : HID; }
@@ -649,8 +657,8 @@ struct TcEngineT {
   static __device__ __forceinline__ uint32_t dcol_of(int l) { return (l & 1) ? DEC_D_ODD : 128u - DEC_D_ODD; }
   // group j signals on named barrier 8 + j (its 4 warps arrive, the issuer
   // warp syncs: 160 threads)
-  template <class Hook>
-  __device__ __forceinline__ void run_rest_ws(float xa, float xb, Hook&& hook) {
+  template <class Hook, class Pre0>
+  __device__ __forceinline__ void run_rest_ws(float xa, float xb, Hook&& hook, Pre0&& pre0) {
     float2 bq[8];
     const uint32_t gbar = 8u + (uint32_t)col_grp();
     auto signal = [&]() {
@@ -658,6 +666,7 @@ struct TcEngineT {
       asm volatile("bar.arrive %0, 160;" ::"r"(gbar) : "memory");
     };
     load_bias(0, bq);
+    pre0(bq);  // 3D window: the lower layer's term joins the layer-1 bias (add_w3d)
     wait_mma_g();
     epilogue_at<true>(dcol_of(0), bq, xa, xb, ao_of(1));
     signal();
@@ -791,8 +800,9 @@ struct Fp32Engine {
   float* buf0;
   float* buf1;
   uint32_t* xbuf;
-  const float* w;   // global fp32 blob (f32_off layout)
+  const float* w;   // global fp32 blob (f32_off layout, layer 0 with k0 rows)
   const float* b0;  // per-image layer-1 biases (metadata folded in), or null: the blob's
+  int k0 = KIN;     // layer-1 inputs: 78, or 87 for the 3D window (R13)
 
   __device__ __forceinline__ void put_input(int k, float x) const { buf0[k * ROWS + tile_row()] = x; }
 
@@ -819,8 +829,8 @@ struct Fp32Engine {
       quad_sync();  // this layer's inputs (written by the row's 8 threads) are complete
       const float* in = (l & 1) ? buf1 : buf0;
       float* out = (l & 1) ? buf0 : buf1;
-      const int K = f32_k(l), N = layer_n(l);
-      const float* W = w + f32_off(l);
+      const int K = l == 0 ? k0 : f32_k(l), N = layer_n(l);
+      const float* W = w + f32_off(l) + (l > 0 ? (uint32_t)(k0 - KIN) * HID : 0u);
       const float* B = (l == 0 && b0) ? b0 : W + K * N;
       const int n8 = N / 8;
 #pragma unroll 1
@@ -872,6 +882,37 @@ struct Fp32Engine {
     for (int g = 0; g < NGRP; ++g) v[g] = xbuf[(slot * NGRP + g) * ROWS + tile_row()];
   }
 };
+
+// ------------------------------------------------- 3D window: the lower layer
+// The 9 taps of the slice below (R13) enter layer 1 through the bias term:
+// for this thread's 16 columns [32j+16h, +16), pre_n = sum_k x_k w_kn (x_k =
+// v_k / 256, w bf16; fp32 FMA, k ascending, from 0: the first product is
+// exact) and b'_n = b_n + pre_n (fp32 RN).  The encoder and the decoder call
+// this same routine, so their layer-1 inputs stay bit-identical (R8).
+// taps: bytes 0-3 / 4-7 / 8 of the 9 taps (row-major 3x3 box) in t[0..2].
+__device__ __forceinline__ void add_w3d(const float* bias, const uint32_t (&t)[3], float2 (&bq)[8]) {
+  const uint4* w3 = reinterpret_cast<const uint4*>(bias + W3D_OFF) + 4 * col_grp() + 2 * half_id();
+  f2 acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = f2_make(0.0f, 0.0f);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    const uint32_t v = (t[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+    const float x = __fadd_rn(__uint_as_float(0x3F800000u | (v << 15)), -1.0f);  // v / 256, exact
+    const f2 xx = f2_make(x, x);
+    const uint4 wa = w3[k * (HID / 8)], wb = w3[k * (HID / 8) + 1];  // 8 bf16 pairs = 16 columns
+    const uint32_t wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      acc[q] = f2_fma(xx, f2_bits(wv[q] << 16, wv[q] & 0xFFFF0000u), acc[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    float a0, a1;
+    f2_split(f2_add(f2_make(bq[q].x, bq[q].y), acc[q]), a0, a1);
+    bq[q] = make_float2(a0, a1);
+  }
+}
 
 // ------------------------------------------------- softmax -> Q1' -> CDF
 // Reading R5 (Q1'), per row; thread (j, h) owns logits [64j+32h, +32):

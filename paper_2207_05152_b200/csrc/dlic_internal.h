@@ -24,7 +24,11 @@ struct Plan {
   // unit range of this launch: units [u_lo, u_lo + u_cnt) of the batch, i.e.
   // streams [s_lo, s_lo + s_cnt) (the whole batch unless a *_units call)
   uint32_t u_lo, u_cnt, s_lo, s_cnt;
-  uint32_t n_meta;  // metadata reals per image (container block: 4 + 4 n_meta bytes after the size table)
+  uint32_t n_meta;  // metadata reals per container (block: 4 + 4 n_meta bytes after the size table)
+  // volumes (§8(f) f2): `depth` consecutive images (slices) form one volume
+  // and one container (window id 2, slice-major streams); 2D: depth 1
+  uint32_t depth, n_cont, spc;  // slices per container, containers, streams per container
+  uint32_t w3d;                 // 3D window (R13): 9 taps from the slice below
 };
 
 constexpr uint32_t HDR_FIXED = 60;  // container header bytes before the size table (version 2)
@@ -106,7 +110,9 @@ cudaError_t launch_dec_prep(const Plan& p, const uint8_t* d_bits, const uint64_t
                             int32_t* d_status, cudaStream_t st, bool check_numerics = true);
 cudaError_t launch_decode(const Plan& p, const DevWeights& w, const uint8_t* d_bits, const uint64_t* d_cont_off,
                           const uint32_t* d_sbase, const uint32_t* d_slen, uint8_t* d_imgs, int32_t* d_status,
-                          cudaStream_t st, unsigned long long* prof = nullptr);
+                          cudaStream_t st, unsigned long long* prof = nullptr, uint32_t* d_sync = nullptr);
+// volumes: d_sync = zeroed u32 [1 + units] (unit ticket + per-unit progress; sync_words)
+inline size_t sync_words(const Plan& p) { return p.w3d ? 1u + (size_t)p.u_lo + p.u_cnt : 0u; }
 
 cudaError_t launch_rans_dec_tables(const Plan& p, const uint8_t* d_bits, const uint32_t* d_sbase,
                                    const uint32_t* d_slen, const uint16_t* d_tables, uint8_t* d_out,
@@ -115,8 +121,8 @@ cudaError_t launch_rans_dec_tables(const Plan& p, const uint8_t* d_bits, const u
 // how many decode clusters of nc CTAs (dynamic smem `smem`) the device can
 // co-schedule (cudaOccupancyMaxActiveClusters); 0 = the launch cannot run
 int dec_max_active_clusters(uint32_t precision, uint32_t nc, size_t smem);
-size_t dec_smem_bytes(uint32_t precision, uint32_t max_groups);
+size_t dec_smem_bytes(uint32_t precision, uint32_t max_groups, uint32_t w3d = 0);
 size_t dec_smem_limit();
-size_t enc_smem_bytes(uint32_t precision);
+size_t enc_smem_bytes(uint32_t precision, uint32_t w3d = 0);
 
 }  // namespace dlic

@@ -46,12 +46,19 @@ constexpr uint32_t F32_BUF_BYTES = (NOUT + HID) * ROWS * 4u;          // 98304
 constexpr uint32_t F32_X_BYTES = NXSLOT * NGRP * ROWS * 4u;          // 7168
 constexpr uint32_t MAX_DYN_SMEM = 232448 - 1024;                     // 227 KB minus static (k_decode: 896 B)
 
-size_t enc_smem_bytes(uint32_t precision) {
-  return precision == 1 ? WIMG_BYTES + BIAS_BYTES : F32_BUF_BYTES + F32_X_BYTES;
+// bias region in shared memory: biases + fresh-tap table (+ the 3D taps'
+// weights for volume plans)
+__host__ __device__ inline uint32_t bias_bytes(uint32_t w3d) { return BIAS_BYTES + (w3d ? W3D_BYTES : 0u); }
+size_t enc_smem_bytes(uint32_t precision, uint32_t w3d) {
+  return precision == 1 ? WIMG_BYTES + bias_bytes(w3d) : F32_BUF_BYTES + F32_X_BYTES;
 }
 static uint32_t cursor_bytes(uint32_t ngroups) { return (ngroups * 4u + 15u) & ~15u; }
-size_t dec_smem_bytes(uint32_t precision, uint32_t max_groups) {
-  return enc_smem_bytes(precision) + RING_BYTES + 16 + 3 * cursor_bytes(max_groups);
+// 3D decoder (bf16): lower-layer taps of each slot for the current and the
+// next step, [2][ROWS][3] words (filled by the rANS warp)
+constexpr uint32_t T3_BYTES = 2u * ROWS * 3u * 4u;
+size_t dec_smem_bytes(uint32_t precision, uint32_t max_groups, uint32_t w3d) {
+  return enc_smem_bytes(precision, w3d) + RING_BYTES + 16 + 3 * cursor_bytes(max_groups) +
+         (w3d && precision == 1 ? T3_BYTES : 0u);
 }
 size_t dec_smem_limit() { return MAX_DYN_SMEM; }
 
@@ -77,10 +84,10 @@ __device__ __forceinline__ void load_smem(uint8_t* dst, const void* src, uint32_
 // end of the engine's shared-memory region.
 template <int PREC>
 __device__ __forceinline__ uint8_t* engine_setup(typename EngineSel<PREC>::T& eng, uint8_t* smem, const DevWeights& w,
-                                                 uint64_t* bar, uint32_t* tslot) {  // bar: 2 mbarriers
+                                                 uint64_t* bar, uint32_t* tslot, uint32_t w3d) {  // bar: 2 mbarriers
   if constexpr (PREC == 1) {
     load_smem(smem, w.wimg, WIMG_BYTES);
-    load_smem(smem + WIMG_BYTES, w.bias, BIAS_BYTES);
+    load_smem(smem + WIMG_BYTES, w.bias, bias_bytes(w3d));
     if (threadIdx.x < 32) tmem_alloc(smem_u32(tslot), TM_COLS);
     if (threadIdx.x == 0) {
       mbar_init(smem_u32(bar), 1);
@@ -95,13 +102,14 @@ __device__ __forceinline__ uint8_t* engine_setup(typename EngineSel<PREC>::T& en
     eng.b0 = eng.bias;
     eng.bar = smem_u32(bar);
     eng.phase = 0;
-    return smem + WIMG_BYTES + BIAS_BYTES;
+    return smem + WIMG_BYTES + bias_bytes(w3d);
   } else {
     eng.buf0 = reinterpret_cast<float*>(smem);
     eng.buf1 = eng.buf0 + NOUT * ROWS;
     eng.xbuf = reinterpret_cast<uint32_t*>(smem + F32_BUF_BYTES);
     eng.w = w.w32;
     eng.b0 = nullptr;
+    eng.k0 = w3d ? KIN3 : KIN;
     return smem + F32_BUF_BYTES + F32_X_BYTES;
   }
 }
@@ -129,7 +137,7 @@ __device__ __forceinline__ void tap_of(int u, int i, int& dr, int& dc) {
   }
 }
 template <int PREC, class Eng, class Get>
-__device__ __forceinline__ void feed(const Eng& eng, Get get) {
+__device__ __forceinline__ void feed(const Eng& eng, Get get, const uint32_t (*t3)[3] = nullptr) {
   const int u = 2 * col_grp() + half_id();
   if constexpr (PREC == 1) {
     // v/256 exactly: (1 + v/256) has v in the top 8 mantissa bits; minus 1 is exact.
@@ -155,6 +163,11 @@ __device__ __forceinline__ void feed(const Eng& eng, Get get) {
       if (i < 9 || u < 6)
         eng.put_input(i < 9 ? 9 * u + i : 72 + u, __fadd_rn(__uint_as_float(0x3F800000u | (get(dr, dc) << 15)), -1.0f));
     }
+    if (t3) {  // 3D window: lower-layer tap u at input 78 + u, thread 0 also tap 8
+      const uint32_t v = ((*t3)[u >> 2] >> (8 * (u & 3))) & 0xFFu;
+      eng.put_input(KIN + u, __fadd_rn(__uint_as_float(0x3F800000u | (v << 15)), -1.0f));
+      if (u == 0) eng.put_input(KIN + 8, __fadd_rn(__uint_as_float(0x3F800000u | ((*t3)[2] & 0xFFu) << 15), -1.0f));
+    }
   }
 }
 
@@ -176,7 +189,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __shared__ uint32_t tslot;
   const int row = tile_row();
   typename EngineSel<PREC>::T eng;
-  engine_setup<PREC>(eng, smem, w, bar, &tslot);
+  engine_setup<PREC>(eng, smem, w, bar, &tslot, p.w3d);
   // tiles of units [u_lo, u_lo + u_cnt) (global tile index = tbase + k)
   const uint64_t tbase = (uint64_t)p.u_lo * p.tiles_per_unit;
   const uint64_t total = (uint64_t)p.u_cnt * p.tiles_per_unit;
@@ -187,7 +200,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // its divisions) is recomputed only when a tile starts a new unit.
   struct Px {
     bool valid;
-    int r, c, uw, sym;
+    int r, c, uw, uh, z, sym;
     const uint8_t* img;
     uint64_t gi, fci;
   };
@@ -201,13 +214,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (u != cu) {
       cu = u;
       cun = unit_info(p, u);
-      if (w.b1img) eng.b0 = w.b1img + (uint64_t)cun.img * HID;  // the tile's image's metadata-folded layer-1 bias
+      if (w.b1img) eng.b0 = w.b1img + (uint64_t)(cun.img / p.depth) * HID;  // the tile's image's metadata-folded layer-1 bias
     }
     const uint32_t q = kt * (uint32_t)ROWS + (uint32_t)row;
     x.valid = q < cun.w * cun.h;
     x.r = x.valid ? (int)(q / cun.w) : 0;
     x.c = x.valid ? (int)(q - (uint32_t)x.r * cun.w) : 0;
     x.uw = (int)cun.w;
+    x.uh = (int)cun.h;
+    x.z = (int)(cun.img % p.depth);
     x.img = imgs + (uint64_t)cun.img * p.W * p.H + (uint64_t)cun.y0 * p.W + cun.x0;
     x.sym = 0;  // loaded by load_sym() when needed (its L2 latency off the tile start)
     x.gi = (uint64_t)cun.img * p.W * p.H + (uint64_t)(cun.y0 + x.r) * p.W + (cun.x0 + x.c);
@@ -235,6 +250,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       return ok ? v : 0u;
     };
   };
+  // 3D window: the 3x3 box of the previous slice (same unit; fill 0 outside it, below slice 0)
+  auto lower = [&](const Px& x, uint32_t (&t3)[3]) {
+    t3[0] = t3[1] = t3[2] = 0u;
+    for (int k = 0; k < 9; ++k) {
+      const int rr = x.r + k / 3 - 1, cc = x.c + k % 3 - 1;
+      const bool ok = x.valid && x.z > 0 && rr >= 0 && rr < x.uh && cc >= 0 && cc < x.uw;
+      const uint32_t v = ok ? (uint32_t)__ldg(x.img - (uint64_t)p.W * p.H + (int64_t)rr * p.W + cc) : 0u;
+      t3[k >> 2] |= v << (8 * (k & 3));
+    }
+  };
+  auto feed_x = [&](const Px& x, auto& get) {
+    if (p.w3d) {
+      uint32_t t3[3];
+      lower(x, t3);
+      feed<PREC>(eng, get, &t3);
+    } else {
+      feed<PREC>(eng, get);
+    }
+  };
 
   if (dbg) {  // debug exports: one tile at a time
 #pragma unroll 1
@@ -242,7 +276,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       Px x = pixel(tile);
       load_sym(x);
       auto get = getter(x);
-      feed<PREC>(eng, get);
+      feed_x(x, get);
       eng.start_l0();
       eng.run_rest(u8_unit(get(0, -1)), u8_unit(get(-1, 2)), [](int) {});
       const uint32_t v = q1_encode(eng, x.sym, (x.valid && dbg_probs) ? dbg_probs + x.gi * NOUT : nullptr,
@@ -285,7 +319,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     Px cur = pixel(tile);
     {
       auto get = getter(cur);
-      feed<PREC>(eng, get);
+      feed_x(cur, get);
       eng.start_l0();
       if (tile + 1 < tend) prefetch_px(pixel(tile + 1));
       eng.run_rest(u8_unit(get(0, -1)), u8_unit(get(-1, 2)), [](int) {});
@@ -301,7 +335,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         Px nx = pixel(nxt);
         auto get = getter(nx);
         if constexpr (PREC == 0) quad_sync();  // fp32: the logits buffer also holds the inputs
-        feed<PREC>(eng, get);
+        feed_x(nx, get);
         eng.start_l0();
         // tile k's softmax -> Q1' stages in the MMA waits of tile k+1's
         // layers 2-6 (the last, N=256, has the longest wait); tile k+2's
@@ -362,13 +396,13 @@ constexpr uint32_t ENC_PP_XS_BYTES = 2u * NXS_SMEM * NGRP * ROWS * 4u;
 using EngA = TcEngineT<0, 256, 256, true>;
 using EngB = TcEngineT<320, 448, 448, true>;
 
-size_t enc_pp_smem_bytes() { return WIMG_BYTES + BIAS_BYTES + ENC_PP_XS_BYTES; }
+size_t enc_pp_smem_bytes(uint32_t w3d) { return WIMG_BYTES + bias_bytes(w3d) + ENC_PP_XS_BYTES; }
 
 // DBG: parity tap of this production kernel -- per pixel (image raster order)
 // the biased logits, the probabilities the quantiser used and the integer
 // table, written from inside the same instruction sequence (R8), so tests can
 // compare the production encoder itself with the oracle.
-template <bool DBG>
+template <bool DBG, bool W3D>
 __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
     k_enc_pp(Plan p, DevWeights w, const uint8_t* __restrict__ imgs, uint32_t* __restrict__ fc,
              unsigned long long* __restrict__ prof, float* __restrict__ dbg_logits, float* __restrict__ dbg_probs,
@@ -377,7 +411,7 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
   __shared__ uint64_t bars[2];  // mma[0], mma[1] (tcgen05.commit)
   __shared__ uint32_t tslot;
   load_smem(smem, w.wimg, WIMG_BYTES);
-  load_smem(smem + WIMG_BYTES, w.bias, BIAS_BYTES);
+  load_smem(smem + WIMG_BYTES, w.bias, bias_bytes(W3D));
   if (threadIdx.x < 32) tmem_alloc(smem_u32(&tslot), TM_COLS);
   if (threadIdx.x == 0) {
     mbar_init(smem_u32(&bars[0]), 1);
@@ -389,7 +423,7 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
   tc_fence_after();
   EngA ea;
   EngB eb;
-  uint32_t* xsb = reinterpret_cast<uint32_t*>(smem + WIMG_BYTES + BIAS_BYTES);
+  uint32_t* xsb = reinterpret_cast<uint32_t*>(smem + WIMG_BYTES + bias_bytes(W3D));
   ea.tmem = eb.tmem = tslot;
   ea.wsmem = eb.wsmem = smem_u32(smem);
   ea.bias = eb.bias = reinterpret_cast<const float*>(smem + WIMG_BYTES);
@@ -447,6 +481,7 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
     uint64_t ffc = 0;
     uint64_t fgi = 0;  // DBG: image-raster index of the unit's pixel (0, 0)
     const float* fb0 = ea.bias;  // layer-1 biases of the cursor's image
+    uint32_t fh = 1, fz = 0;     // W3D: unit height, slice index in its volume
     auto set_unit = [&](uint32_t u) {
       const Unit un = unit_info(p, u);
       fu = u;
@@ -458,7 +493,9 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
       fimg = imgs + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
       ffc = un.fc_off;
       fgi = (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
-      if (w.b1img) fb0 = w.b1img + (uint64_t)un.img * HID;
+      if (w.b1img) fb0 = w.b1img + (uint64_t)(un.img / p.depth) * HID;
+      fh = un.h;
+      fz = un.img % p.depth;
     };
     if (t0 < tend) {
       const uint32_t u0 = (uint32_t)(t0 / p.tiles_per_unit);
@@ -490,7 +527,8 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
     struct Px {
       uint64_t fci;
       int sym;
-      uint64_t gi;  // DBG only
+      uint64_t gi;     // DBG only
+      uint32_t t3[3];  // W3D only: the 3x3 box of the slice below (R13), bytes row-major
     };
     // the cursor's tile -> layer-1 input of a slot; fresh taps, symbol.
     // Thread u = 2j + h reads window row dr = u - 8 (taps dc = -6..2) and,
@@ -532,6 +570,17 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
       o.fci = ffc + q;
       o.sym = valid ? (int)__ldg(tp) : -1;
       o.gi = fgi + (uint64_t)fr * p.W + (uint64_t)fcol;
+      if constexpr (W3D) {  // same unit of the previous slice (fill 0 outside it and below slice 0)
+        const uint8_t* lp = fimg - (uint64_t)p.W * p.H;
+        o.t3[0] = o.t3[1] = o.t3[2] = 0u;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+          const int rr = fr + k / 3 - 1, cc = fcol + k % 3 - 1;
+          const bool ok = valid && fz > 0 && rr >= 0 && rr < (int)fh && cc >= 0 && cc < (int)fw;
+          const uint32_t v = ok ? (uint32_t)__ldg(lp + (int64_t)rr * p.W + cc) : 0u;
+          o.t3[k >> 2] |= v << (8 * (k & 3));
+        }
+      }
       if (live) advance();
       return o;
     };
@@ -601,10 +650,12 @@ __global__ void __launch_bounds__(ENC_PP_THREADS, 1)
         // epilogue releases that slot's next layer.  Layer 1 adds the fresh
         // taps in its epilogue (same split as the decoder).
         ea.load_bias(0, bq);
+        if constexpr (W3D) add_w3d(ea.bias, A.t3, bq);
         ea.wait_mma();
         ea.template epilogue<true>(bq, xaA, xbA);
         signal(0);
         eb.load_bias(0, bq);
+        if constexpr (W3D) add_w3d(eb.bias, B.t3, bq);
         eb.wait_mma();
         eb.template epilogue<true>(bq, xaB, xbB);
         signal(1);
@@ -755,7 +806,7 @@ __device__ __forceinline__ void put_u32(uint8_t* o, uint32_t v) {
 __global__ void k_container(Plan p, Sha sha, const uint32_t* __restrict__ words, uint8_t* __restrict__ out,
                             uint64_t stride, uint64_t* __restrict__ sizes, uint64_t* __restrict__ dst,
                             int payload_only, const float* __restrict__ meta) {
-  const uint32_t img = blockIdx.x;
+  const uint32_t img = blockIdx.x;  // container index (a volume = depth slices)
   uint8_t* o = out + (uint64_t)img * stride;
   if (payload_only) {
     if (threadIdx.x == 0) {
@@ -775,7 +826,7 @@ __global__ void k_container(Plan p, Sha sha, const uint32_t* __restrict__ words,
     o[3] = 'C';
     o[4] = (uint8_t)CONTAINER_VERSION;
     o[5] = (uint8_t)p.precision;
-    o[6] = 1;  // window id (R1)
+    o[6] = p.w3d ? 2 : 1;  // window id (R1; 2 = the 3D window R13, a volume)
     o[7] = 0;  // fill (R2)
     put_u32(o + 8, p.W);
     put_u32(o + 12, p.H);
@@ -784,16 +835,16 @@ __global__ void k_container(Plan p, Sha sha, const uint32_t* __restrict__ words,
     put_u16(o + 20, p.G);
     put_u16(o + 22, NUMERICS_REV);  // arithmetic revision of the tables (decode must match)
     for (int i = 0; i < 32; ++i) o[24 + i] = sha.b[i];
-    put_u32(o + 56, p.spi);
+    put_u32(o + 56, p.spc);
     uint64_t off = p.hdr_bytes;
     // metadata block after the size table: u32 n, f32 raw reals
-    uint8_t* mb = o + HDR_FIXED + 4u * p.spi;
+    uint8_t* mb = o + HDR_FIXED + 4u * p.spc;
     put_u32(mb, p.n_meta);
     for (uint32_t k = 0; k < p.n_meta; ++k) put_u32(mb + 4 + 4 * k, __float_as_uint(meta[(uint64_t)img * p.n_meta + k]));
-    for (uint32_t s = 0; s < p.spi; ++s) {
-      const uint32_t sz = 2u * words[(uint64_t)img * p.spi + s];
+    for (uint32_t s = 0; s < p.spc; ++s) {
+      const uint32_t sz = 2u * words[(uint64_t)img * p.spc + s];
       put_u32(o + HDR_FIXED + 4 * s, sz);
-      dst[(uint64_t)img * p.spi + s] = off;
+      dst[(uint64_t)img * p.spc + s] = off;
       off += sz;
     }
     sizes[img] = off;
@@ -811,7 +862,7 @@ __global__ void __launch_bounds__(128) k_copy(Plan p, const uint32_t* __restrict
   const uint32_t nr = min(p.G, un.h - g * p.G);
   const uint32_t nw = words[s], ns = 2 * nr, ne = nw - ns;
   const uint16_t* region = scratch + (uint64_t)s * p.cap_words;
-  uint16_t* o = reinterpret_cast<uint16_t*>(out + (uint64_t)un.img * stride + dst[s]);
+  uint16_t* o = reinterpret_cast<uint16_t*>(out + (uint64_t)(un.img / p.depth) * stride + dst[s]);
   for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x)
     o[i] = i < ns ? region[i] : region[p.cap_words - ne + (i - ns)];
 }
@@ -879,13 +930,13 @@ __global__ void __launch_bounds__(128) k_rans_dec_tables(Plan p, const uint8_t* 
   }
   if (lane_ok && x != RANS_L) err = err ? err : 6;
   if (lane == 0 && cur != sl) err = err ? err : 6;
-  if (err) atomicMax(status + un.img, err);
+  if (err) atomicMax(status + un.img / p.depth, err);
 }
 
 cudaError_t launch_rans_dec_tables(const Plan& p, const uint8_t* d_bits, const uint32_t* d_sbase,
                                    const uint32_t* d_slen, const uint16_t* d_tables, uint8_t* d_out,
                                    int32_t* d_status, cudaStream_t st) {
-  const uint32_t ns = p.n_img * p.spi;
+  const uint32_t ns = p.n_img * p.spi;  // == n_cont * spc
   k_rans_dec_tables<<<(ns + 3) / 4, 128, 0, st>>>(p, d_bits, d_sbase, d_slen, d_tables, d_out, d_status);
   return cudaGetLastError();
 }
@@ -899,26 +950,28 @@ __device__ __forceinline__ uint32_t get_u16(const uint8_t* b) { return (uint32_t
 __global__ void k_dec_prep(Plan p, const uint8_t* __restrict__ bits, const uint64_t* __restrict__ cont_off,
                            const uint64_t* __restrict__ cont_len, uint32_t* __restrict__ sbase,
                            uint32_t* __restrict__ slen, int32_t* __restrict__ status, int check_numerics) {
-  const uint32_t img = blockIdx.x * blockDim.x + threadIdx.x;
-  if (img >= p.n_img) return;
+  const uint32_t img = blockIdx.x * blockDim.x + threadIdx.x;  // container index
+  if (img >= p.n_cont) return;
   const uint8_t* b = bits + cont_off[img];
   const uint64_t len = cont_len[img];  // required: every read below stays inside [b, b + len)
   int err = 0;
   if (len < HDR_FIXED || b[0] != 'D' || b[1] != 'L' || b[2] != 'I' || b[3] != 'C') err = 6;
-  else if (b[4] != CONTAINER_VERSION || b[6] != 1 || b[7] != 0 || (check_numerics && get_u16(b + 22) != NUMERICS_REV)) err = 5;
+  else if (b[4] != CONTAINER_VERSION || b[6] != (p.w3d ? 2 : 1) || b[7] != 0 ||
+           (check_numerics && get_u16(b + 22) != NUMERICS_REV))
+    err = 5;
   else if (get_u32(b + 8) != p.W || get_u32(b + 12) != p.H || get_u16(b + 16) != p.hdr_tw ||
            get_u16(b + 18) != p.hdr_th || get_u16(b + 20) != p.G || b[5] != p.precision ||
-           get_u32(b + 56) != p.spi || p.hdr_bytes > len || get_u32(b + HDR_FIXED + 4u * p.spi) != p.n_meta)
+           get_u32(b + 56) != p.spc || p.hdr_bytes > len || get_u32(b + HDR_FIXED + 4u * p.spc) != p.n_meta)
     err = 2;
   uint64_t off = p.hdr_bytes;
-  for (uint32_t s = 0; s < p.spi; ++s) {
+  for (uint32_t s = 0; s < p.spc; ++s) {
     uint32_t sz = err ? 0u : get_u32(b + HDR_FIXED + 4 * s);
     if ((sz & 1u) || off + sz > len) {
       err = 6;
       sz = 0;
     }
-    sbase[(uint64_t)img * p.spi + s] = (uint32_t)off;
-    slen[(uint64_t)img * p.spi + s] = err ? 0u : sz / 2;
+    sbase[(uint64_t)img * p.spc + s] = (uint32_t)off;
+    slen[(uint64_t)img * p.spc + s] = err ? 0u : sz / 2;
     off += sz;
   }
   if (off != len && !err) err = 6;
@@ -949,14 +1002,16 @@ constexpr int DEC_THREADS = NTHREADS + 32;
 // bf16: one more warp (the 18th) only issues the network's MMAs (run_rest_ws)
 __host__ __device__ constexpr int dec_block(int prec) { return prec == 1 ? DEC_THREADS + 32 : DEC_THREADS; }
 
-template <int PREC, bool PROF>
+template <int PREC, bool PROF, bool W3D>
 __global__ void __launch_bounds__(dec_block(PREC), 1)
     k_decode(Plan p, DevWeights w, const uint8_t* __restrict__ bits, const uint64_t* __restrict__ cont_off,
              const uint32_t* __restrict__ sbase, const uint32_t* __restrict__ slen, uint8_t* __restrict__ out,
-             int32_t* __restrict__ status, unsigned long long* __restrict__ prof) {
+             int32_t* __restrict__ status, unsigned long long* __restrict__ prof, uint32_t* __restrict__ sync) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar[3];  // 0 MMA completion, 1 a_ready (16 row warps), 2 spare
   __shared__ uint32_t tslot;
+  __shared__ uint32_t s_tick;   // 3D: this cluster's unit ticket (rank 0's copy is authoritative)
+  __shared__ uint32_t s_lower;  // 3D: steps the slice below has published (a lower bound)
   __shared__ uint32_t s_slot[ROWS];  // the row's rANS slot x & 0xFFFF (rANS warp -> the row's 8 threads)
   __shared__ uint2 s_res[ROWS];      // (f_s, c_s) of the decoded symbol (finder -> rANS warp, next front)
   const uint32_t lane = lane_id();
@@ -967,24 +1022,47 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
   Prof pf;
   pf.on = PROF && threadIdx.x == 32;  // a row thread
   const uint32_t rank = NC > 1 ? cluster_rank() : 0u;
-  const uint32_t u = p.u_lo + blockIdx.x / NC;
+  // Volumes (3D wavefront): the unit of slice z waits for the same
+  // unit of slice z-1, so units are handed out in order through a ticket:
+  // a cluster only ever waits for clusters that were dispatched before it.
+  // sync[0] = ticket, sync[1 + u] = steps unit u has published.
+  auto unit_of_cluster = [&]() -> uint32_t {
+    if (!W3D) return blockIdx.x / NC;
+    if (rank == 0 && threadIdx.x == 0) s_tick = atomicAdd(sync, 1u);
+    if (NC > 1) {
+      cluster_sync_all();
+      uint32_t v;
+      asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(map_cluster(smem_u32(&s_tick), 0)) : "memory");
+      cluster_sync_all();  // rank 0's ticket read by every CTA before anyone moves on
+      return v;
+    }
+    __syncthreads();
+    return s_tick;
+  };
+  const uint32_t u = p.u_lo + unit_of_cluster();
   const Unit un = unit_info(p, u);
+  const uint32_t DEPTH = W3D ? p.depth : 1u;  // images per container (2D: 1, compile-time)
+  const int zsl = W3D ? (int)(un.img % DEPTH) : 0;  // slice index in its volume
+  uint32_t* const my_done = W3D ? sync + 1 + u : nullptr;
+  const uint32_t* const lower_done = W3D && zsl > 0 ? sync + 1 + (u - p.upi) : nullptr;
+  if (W3D && threadIdx.x == 0) s_lower = 0;
 
   typename EngineSel<PREC>::T eng;
-  uint8_t* ring = engine_setup<PREC>(eng, smem, w, bar, &tslot);
+  uint8_t* ring = engine_setup<PREC>(eng, smem, w, bar, &tslot, p.w3d);
   if constexpr (PREC == 1) eng.bar2 = smem_u32(&bar[2]);
   if (w.b1img) {  // the unit's image's metadata-folded layer-1 bias
     if constexpr (PREC == 1) {
       __syncthreads();  // engine_setup's bias copy is complete
       float* b1 = const_cast<float*>(eng.bias);
-      for (uint32_t i = threadIdx.x; i < (uint32_t)HID; i += blockDim.x) b1[i] = w.b1img[(uint64_t)un.img * HID + i];
+      for (uint32_t i = threadIdx.x; i < (uint32_t)HID; i += blockDim.x) b1[i] = w.b1img[(uint64_t)(un.img / DEPTH) * HID + i];
     } else {
-      eng.b0 = w.b1img + (uint64_t)un.img * HID;
+      eng.b0 = w.b1img + (uint64_t)(un.img / DEPTH) * HID;
     }
   }
   uint32_t* cursor = reinterpret_cast<uint32_t*>(ring + RING_BYTES + 16);  // 16 zero bytes after the ring
   uint32_t* s_sbase = cursor + ((un.ngroups + 3u) & ~3u);                   // per-group stream table
   uint32_t* s_slen = s_sbase + ((un.ngroups + 3u) & ~3u);
+  uint32_t* s_t3 = s_slen + ((un.ngroups + 3u) & ~3u);  // W3D bf16: [2][ROWS][3]
   for (uint32_t i = threadIdx.x; i < RING_BYTES / 16; i += blockDim.x)
     reinterpret_cast<int4*>(ring)[i] = make_int4(0, 0, 0, 0);
   const uint32_t G = p.G;
@@ -1004,7 +1082,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
   if (NC > 1) cluster_sync_all();
   else __syncthreads();
 
-  const uint8_t* cbase = bits + cont_off[un.img];
+  const uint8_t* cbase = bits + cont_off[un.img / DEPTH];
   const int uw = (int)un.w, uh = (int)un.h;
   const int T = uw + 3 * (uh - 1);
   int err = 0;
@@ -1019,6 +1097,55 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
     c = t - 3 * r;
     return r <= rhi;
   };
+  // 3D (bf16): the rANS warp loads the 3x3 box of the slice below for each of
+  // its CTA's 64 slots one step ahead into s_t3[step & 1] (its own slack:
+  // after publishing the step's slots), waiting first until the slice below
+  // has published the steps it needs (its pixels up to 4 steps past the
+  // slot's, stored one step after decoding: done >= step + 5).  L2 loads
+  // (.cg): this SM may hold stale L1 lines of the slice below.
+  const uint8_t* lower_img = out + (uint64_t)(un.img - (zsl > 0 ? 1u : 0u)) * p.W * p.H +
+                             (uint64_t)un.y0 * p.W + un.x0;
+  auto wait_lower = [&](int need) {
+    if (!lower_done) return;
+    for (long long spins = 0;; ++spins) {
+      uint32_t v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(lower_done) : "memory");
+      if ((int)v >= need) break;
+      if (spins > (1ll << 26)) {  // watchdog: corrupt, never a hang
+        err = 6;
+        break;
+      }
+    }
+  };
+  auto lower_box = [&](int r, int c, bool act, uint32_t (&t)[3]) {
+    t[0] = t[1] = t[2] = 0u;
+    if (!lower_done || !act) return;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int rr = r + k / 3 - 1, cc = c + k % 3 - 1;
+      const bool ok = rr >= 0 && rr < uh && cc >= 0 && cc < uw;
+      const uint32_t v = ok ? (uint32_t)__ldcg(lower_img + (int64_t)rr * p.W + cc) : 0u;
+      t[k >> 2] |= v << (8 * (k & 3));
+    }
+  };
+  auto fill_t3 = [&](int t) {  // rANS warp: both 32-slot halves at step t
+    wait_lower(t + 5);
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      int r, c;
+      const bool act = slot_rc(rank * ROWS + 32u * hf + lane, t, r, c);
+      uint32_t tt[3];
+      lower_box(r, c, act, tt);
+      uint32_t* d = s_t3 + ((uint32_t)(t & 1) * ROWS + 32u * hf + lane) * 3u;
+      d[0] = tt[0];
+      d[1] = tt[1];
+      d[2] = tt[2];
+    }
+  };
+  if constexpr (W3D && PREC == 1) {
+    if (threadIdx.x < 32) fill_t3(0);
+    __syncthreads();
+  }
   auto front_end = [&]() {
     if (NC > 1) cluster_sync_all();
     else __syncthreads();
@@ -1138,7 +1265,20 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         s_slot[32 * hf + lane] = xs[hf] & 0xFFFFu;
       }
       asm volatile("bar.arrive 7, %0;" ::"n"(DEC_THREADS) : "memory");  // slots of front t published
+      if constexpr (W3D && PREC == 1) {
+        if (t + 1 < T) fill_t3(t + 1);
+      }
       front_end();
+      if (W3D && lane == 0) {
+        // the cluster barrier released every pixel store of steps <= t - 1
+        // (each is stored in the step after it is decoded): publish them
+        if (rank == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(my_done), "r"((uint32_t)t) : "memory");
+        if (PREC == 0 && lower_done) {  // fp32: progress of the slice below, for the row warps
+          uint32_t v;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(lower_done) : "memory");
+          *(volatile uint32_t*)&s_lower = v;
+        }
+      }
     }
     if (T > 0) {  // the last front's steps
       prefetch(0, T - 1);
@@ -1209,6 +1349,40 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
     // Early part of a front (one front ahead): the 76 taps decoded before the
     // preceding front -> layer-1 input (the two fresh taps' weights are zero in
     // the MMA image; fp32: overwritten by run_rest).
+    // 3D window: the 3x3 box of the slice below for the next step's pixel,
+    // loaded in that step's predecessor (layer-3 MMA wait) once the slice
+    // below has published the steps it needs (its pixels up to step t+5 of
+    // this slice's clock: the box reaches (r+1, c+1), 4 steps after (r, c);
+    // pixels are stored one step after they are decoded).  L2 loads (.cg):
+    // this SM may hold stale L1 lines of the slice below.
+    uint32_t t3[3] = {0u, 0u, 0u}, t3n[3] = {0u, 0u, 0u};
+    auto load_lower = [&](int rn, int cn, bool act, int need) {  // fp32 engine: the row warps load directly
+      t3n[0] = t3n[1] = t3n[2] = 0u;
+      if (!lower_done || !act) return;
+      if ((int)*(volatile uint32_t*)&s_lower < need) {
+        const long long w0 = PROF ? clock64() : 0;
+        if (PROF && pf.on) atomicAdd(prof + 24, 1ull);  // waits (profiled thread)
+        for (long long spins = 0;; ++spins) {
+          uint32_t v;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(lower_done) : "memory");
+          if ((int)v >= need) {
+            if (PROF && pf.on) atomicAdd(prof + 25, (unsigned long long)(clock64() - w0));
+            break;
+          }
+          if (spins > (1ll << 26)) {  // watchdog: corrupt, never a hang
+            err = 6;
+            break;
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        const int rr = rn + k / 3 - 1, cc = cn + k % 3 - 1;
+        const bool ok = rr >= 0 && rr < uh && cc >= 0 && cc < uw;
+        const uint32_t v = ok ? (uint32_t)__ldcg(lower_img + (int64_t)rr * p.W + cc) : 0u;
+        t3n[k >> 2] |= v << (8 * (k & 3));
+      }
+    };
     auto early_put = [&](int r, int c) {
       const uint8_t* bp = ring_at(r, c) + gu;
       uint32_t tv[10];
@@ -1230,6 +1404,10 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
 #pragma unroll
         for (int i = 0; i < 10; ++i)
           if (i < 9 || gu < 6) eng.put_input(i < 9 ? 9 * gu + i : 72 + gu, u8_unit(tv[i]));
+        if (W3D) {  // the lower-layer taps enter the fp32 network as inputs 78..86
+          eng.put_input(KIN + gu, u8_unit((t3n[gu >> 2] >> (8 * (gu & 3))) & 0xFFu));
+          if (gu == 0) eng.put_input(KIN + 8, u8_unit(t3n[2] & 0xFFu));
+        }
       }
     };
     // does any slot of this CTA hold an active row at front t (uniform)
@@ -1290,6 +1468,12 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
     int r, c;
     bool active = slot_rc(S, 0, r, c);
     bool any = cta_any(0);
+    if constexpr (W3D && PREC == 0) {  // step 0's lower taps (later steps load theirs a step ahead)
+      load_lower(r, c, active, 5);
+      t3[0] = t3n[0];
+      t3[1] = t3n[1];
+      t3[2] = t3n[2];
+    }
     early_gather(r, c);
     early_signal(r, c);
     issue_early(any);
@@ -1327,11 +1511,17 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
           eng.run_rest_ws(xa, xb, [&](int l) {
             if (l == 1 && optr) *optr = (uint8_t)opix;
             if (l == 2) early_gather(rn, cn);
+          }, [&](float2 (&bq)[8]) {
+            if constexpr (W3D) {  // this step's lower taps (s_t3, written by the rANS warp last step)
+              const uint32_t* q = s_t3 + ((uint32_t)(t & 1) * ROWS + (uint32_t)row) * 3u;
+              const uint32_t tt[3] = {q[0], q[1], q[2]};
+              add_w3d(eng.bias, tt, bq);
+            }
           });
         } else {
           eng.run_rest(xa, xb, [&](int l) {
             if (l == 1 && optr) *optr = (uint8_t)opix;
-            (void)l;
+            if constexpr (W3D) { if (l == 2) load_lower(rn, cn, active_n, t + 6); }
           }, PROF ? &pf : nullptr);
         }
         pf.mark(3);
@@ -1391,6 +1581,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       } else {
         asm volatile("bar.sync 7, %0;" ::"n"(DEC_THREADS) : "memory");  // keep the barrier in step
         if (optr) *optr = (uint8_t)opix;
+        if constexpr (W3D && PREC == 0) load_lower(rn, cn, active_n, t + 6);
         early_gather(rn, cn);
         early_signal(rn, cn);
       }
@@ -1437,6 +1628,9 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       c = cn;
       active = active_n;
       any = any_n;
+      t3[0] = t3n[0];
+      t3[1] = t3n[1];
+      t3[2] = t3n[2];
       rn = rn2;
       cn = cn2;
       active_n = active_n2;
@@ -1453,9 +1647,12 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
   for (uint32_t g = threadIdx.x; g < un.ngroups; g += blockDim.x) {
     if ((((G * g) & (NS - 1)) >> 6) == rank && cursor[g] != slen[un.first_stream + g]) err = 6;
   }
-  if (err) atomicMax(status + un.img, err);
+  if (err) atomicMax(status + un.img / DEPTH, err);
   engine_teardown<PREC>(eng);
   if (NC > 1) cluster_sync_all();  // keep DSMEM alive until every CTA is done
+  else if (W3D) __syncthreads();
+  if (W3D && rank == 0 && threadIdx.x == 0)  // every pixel of the unit is stored (the barrier released them)
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(my_done), "r"(0x7FFFFFFFu) : "memory");
 }
 
 // ------------------------------------------------------------ metadata -> layer-1 bias
@@ -1504,23 +1701,24 @@ cudaError_t launch_enc_mlp(const Plan& p, const DevWeights& w, const uint8_t* d_
                            int num_sms) {
   const uint64_t total = (uint64_t)p.u_cnt * p.tiles_per_unit;
   const uint32_t grid = (uint32_t)(total < (uint64_t)num_sms ? total : (uint64_t)num_sms);
-  const size_t sm = enc_smem_bytes(p.precision);
+  const size_t sm = enc_smem_bytes(p.precision, p.w3d);
   if (p.precision == 1 && (dbg_logits || dbg_probs || dbg_freqs)) {
     // parity tap: the production kernel with its debug exports
-    const size_t sp = enc_pp_smem_bytes();
-    cudaError_t e = set_smem(k_enc_pp<true>, sp);
+    const size_t sp = enc_pp_smem_bytes(p.w3d);
+    auto k = p.w3d ? k_enc_pp<true, true> : k_enc_pp<true, false>;
+    cudaError_t e = set_smem(k, sp);
     if (e != cudaSuccess) return e;
-    k_enc_pp<true><<<grid, ENC_PP_THREADS, sp, st>>>(p, w, d_imgs, d_fc, nullptr, dbg_logits, dbg_probs, dbg_freqs);
+    k<<<grid, ENC_PP_THREADS, sp, st>>>(p, w, d_imgs, d_fc, nullptr, dbg_logits, dbg_probs, dbg_freqs);
   } else if (p.precision == 1) {
-    const size_t sp = enc_pp_smem_bytes();
-    cudaError_t e = set_smem(k_enc_pp<false>, sp);
+    const size_t sp = enc_pp_smem_bytes(p.w3d);
+    auto kp = p.w3d ? k_enc_pp<false, true> : k_enc_pp<false, false>;
+    cudaError_t e = set_smem(kp, sp);
     if (e != cudaSuccess) return e;
     static unsigned long long* d_prof = nullptr;
     const bool prof = getenv("DLIC_PROF_ENC") != nullptr;
     if (prof && !d_prof) cudaMalloc(&d_prof, 16 * 8);
     if (prof) cudaMemsetAsync(d_prof, 0, 16 * 8, st);
-    k_enc_pp<false><<<grid, ENC_PP_THREADS, sp, st>>>(p, w, d_imgs, d_fc, prof ? d_prof : nullptr, nullptr, nullptr,
-                                                     nullptr);
+    kp<<<grid, ENC_PP_THREADS, sp, st>>>(p, w, d_imgs, d_fc, prof ? d_prof : nullptr, nullptr, nullptr, nullptr);
     if (prof) {
       unsigned long long h[16];
       cudaMemcpyAsync(h, d_prof, 16 * 8, cudaMemcpyDeviceToHost, st);
@@ -1552,7 +1750,7 @@ cudaError_t launch_container(const Plan& p, const uint8_t* model_sha, const uint
                              uint64_t* d_stream_dst, cudaStream_t st, bool payload_only, const float* d_meta) {
   Sha sha;
   for (int i = 0; i < 32; ++i) sha.b[i] = model_sha ? model_sha[i] : 0;
-  k_container<<<payload_only ? 1u : p.n_img, 32, 0, st>>>(p, sha, d_words, d_out, out_stride, d_sizes,
+  k_container<<<payload_only ? 1u : p.n_cont, 32, 0, st>>>(p, sha, d_words, d_out, out_stride, d_sizes,
                                                            d_stream_dst, payload_only ? 1 : 0, d_meta);
   if (p.s_cnt > 0) k_copy<<<p.s_cnt, 128, 0, st>>>(p, d_words, d_scratch, d_stream_dst, d_out, out_stride);
   return cudaGetLastError();
@@ -1561,7 +1759,7 @@ cudaError_t launch_container(const Plan& p, const uint8_t* model_sha, const uint
 cudaError_t launch_dec_prep(const Plan& p, const uint8_t* d_bits, const uint64_t* d_cont_off,
                             const uint64_t* d_cont_len, uint32_t* d_sbase, uint32_t* d_slen, int32_t* d_status,
                             cudaStream_t st, bool check_numerics) {
-  k_dec_prep<<<(p.n_img + 63) / 64, 64, 0, st>>>(p, d_bits, d_cont_off, d_cont_len, d_sbase, d_slen, d_status,
+  k_dec_prep<<<(p.n_cont + 63) / 64, 64, 0, st>>>(p, d_bits, d_cont_off, d_cont_len, d_sbase, d_slen, d_status,
                                                  check_numerics ? 1 : 0);
   return cudaGetLastError();
 }
@@ -1570,9 +1768,10 @@ template <int PREC, bool PROF>
 static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uint8_t* d_bits,
                                    const uint64_t* d_cont_off, const uint32_t* d_sbase, const uint32_t* d_slen,
                                    uint8_t* d_imgs, int32_t* d_status, cudaStream_t st,
-                                   unsigned long long* prof) {
-  const size_t sm = dec_smem_bytes(PREC, p.gpt > p.gpl ? p.gpt : p.gpl);
-  cudaError_t e = set_smem(k_decode<PREC, PROF>, sm);
+                                   unsigned long long* prof, uint32_t* d_sync) {
+  const size_t sm = dec_smem_bytes(PREC, p.gpt > p.gpl ? p.gpt : p.gpl, p.w3d);
+  auto kern = p.w3d ? k_decode<PREC, PROF, true> : k_decode<PREC, PROF, false>;
+  cudaError_t e = set_smem(kern, sm);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.u_cnt * p.nc);
@@ -1580,7 +1779,7 @@ static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uin
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
   if (p.nc > 8) {
-    e = cudaFuncSetAttribute(k_decode<PREC, PROF>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchAttribute at[1];
@@ -1590,14 +1789,14 @@ static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uin
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_decode<PREC, PROF>, p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status,
-                            prof);
+  return cudaLaunchKernelEx(&cfg, kern, p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status,
+                            prof, d_sync);
 }
 
 template <int PREC>
 static int max_clusters_t(uint32_t nc, size_t sm) {
-  if (set_smem(k_decode<PREC, false>, sm) != cudaSuccess) return 0;
-  if (nc > 8 && cudaFuncSetAttribute(k_decode<PREC, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+  if (set_smem(k_decode<PREC, false, false>, sm) != cudaSuccess) return 0;
+  if (nc > 8 && cudaFuncSetAttribute(k_decode<PREC, false, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
                     cudaSuccess)
     return 0;
   cudaLaunchConfig_t cfg = {};
@@ -1612,7 +1811,7 @@ static int max_clusters_t(uint32_t nc, size_t sm) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k_decode<PREC, false>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, k_decode<PREC, false, false>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -1625,15 +1824,15 @@ int dec_max_active_clusters(uint32_t precision, uint32_t nc, size_t smem) {
 
 cudaError_t launch_decode(const Plan& p, const DevWeights& w, const uint8_t* d_bits, const uint64_t* d_cont_off,
                           const uint32_t* d_sbase, const uint32_t* d_slen, uint8_t* d_imgs, int32_t* d_status,
-                          cudaStream_t st, unsigned long long* prof) {
+                          cudaStream_t st, unsigned long long* prof, uint32_t* d_sync) {
   if (prof) {
     if (p.precision == 1)
-      return launch_decode_t<1, true>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof);
-    return launch_decode_t<0, true>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof);
+      return launch_decode_t<1, true>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof, d_sync);
+    return launch_decode_t<0, true>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof, d_sync);
   }
   if (p.precision == 1)
-    return launch_decode_t<1, false>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof);
-  return launch_decode_t<0, false>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof);
+    return launch_decode_t<1, false>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof, d_sync);
+  return launch_decode_t<0, false>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof, d_sync);
 }
 
 }  // namespace dlic

@@ -51,6 +51,16 @@ POOL = [2, 0, 2, 0, 0, 0]
 META_RANGE = [(0.0, 2.0), (0.0, 10.0), (0.5, 6.0)]
 
 
+def p100k_3d():
+    """fixtures/p100k_3d.dlicmdl: the §8(f) f2 network (87 = 78 + the 3x3 box
+    of the slice below -> 128x5 -> 256), seeded He-uniform weights."""
+    layers = synth.he_uniform_layers((87, 128, 128, 128, 128, 128, 256), seed=11, bias_scale=0.1)
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "fixtures", "p100k_3d.dlicmdl")
+    with open(out, "wb") as fh:
+        fh.write(model_io.save(layers))
+    print("wrote", out)
+
+
 def pool_meta():
     layers = synth.he_uniform_pooled(81, [128, 128, 128, 128, 128, 256], POOL, seed=7, bias_scale=0.1)
     out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "fixtures",
@@ -63,6 +73,9 @@ def pool_meta():
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "pool_meta":
         pool_meta()
+    elif len(sys.argv) > 1 and sys.argv[1] == "3d":
+        p100k_3d()
     else:
         main()
         pool_meta()
+        p100k_3d()
