@@ -39,6 +39,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FLOP_PER_PX = 216576            # P100K, SURVEY App. A item 1 (2 * sum K*N)
+FLOP_PER_PX_P350K = 695296      # P350K: 2 * (78*256 + 4*256*256 + 256*256)
+# per front, layers 2-6 are a dependent MMA chain (layer 1 is issued a front
+# early), M=64 tiles costing as M=128 (8192 FLOP/clk/SM): P100K 4 x 8 x 64 +
+# 8 x 128 = 3072 cycles; P350K 5 x 16 x 128 = 10240 cycles
+FRONT_FLOOR_CYC = {"p350k": 10240}
 # model fixtures: (file, metadata reals per image or None, description)
 MODELS = {
     "p100k": ("p100k_trained.dlicmdl", None,
@@ -47,6 +52,10 @@ MODELS = {
                   "P100K-pool-meta: 78+3 metadata inputs, avg-pool 2 after layers 1 and 3, seeded random "
                   "(fixtures/p100k_pool_meta.dlicmdl; pooling folded into the next layer, metadata into a "
                   "per-image layer-1 bias: the tensor-core chain runs P100K's shapes, 216,576 FLOP/px)"),
+    "p350k": ("p350k_seeded.dlicmdl", None,
+              "P350K: 78 -> 256x5 -> 256 (349,184 parameters, reading R4), seeded He-uniform "
+              "(fixtures/p350k_seeded.dlicmdl); bf16 only, weights streamed from L2 through a TMA ring "
+              "(engine 2, 695,296 FLOP/px)"),
     "3d": ("p100k_3d.dlicmdl", None,
            "P100K-3D: 78 + the 3x3 box of the slice below (87 inputs) -> 128x5 -> 256, seeded random "
            "(fixtures/p100k_3d.dlicmdl; the 9 lower taps enter layer 1 through the bias term, 2,304 FLOP/px on "
@@ -590,7 +599,8 @@ def main():
     if rank == 0:
         peaks, src = load_peaks()
         # dominant kernel: the wavefront decoder (latency-bound front chain)
-        dec_flops = FLOP_PER_PX * px_rank
+        fpp = FLOP_PER_PX_P350K if args.model == "p350k" else FLOP_PER_PX
+        dec_flops = fpp * px_rank
         achieved = dec_flops / (t_dec / 1e3) / 1e12
         # fp32 path runs on CUDA-core FFMA: 148 SMs x 128 FMA/clk x 2 x sm_max
         peak = peaks["bf16_tflops"] if prec == 1 else 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
@@ -602,9 +612,7 @@ def main():
             pass
         tw, th = (W, H) if tile == (0, 0) else (min(tile[0], W), min(tile[1], H))
         T = tw + 3 * (th - 1)
-        # per front, layers 2-6 are a dependent MMA chain (layer 1 is issued a
-        # front early): 4 x 8 x 64 + 8 x 128 = 3072 cycles at M=64
-        floor_ms = T * 3072 / (peaks.get("sm_max_mhz", 1965.0) * 1e3)
+        floor_ms = T * FRONT_FLOOR_CYC.get(args.model, 3072) / (peaks.get("sm_max_mhz", 1965.0) * 1e3)
         cpu = cpu_baseline_sample(args, imgs[0]) if ws == 1 else None   # N=1 only (contract)
         line = {
             "metric": METRIC,
@@ -618,18 +626,19 @@ def main():
             "decode_mpx_s": ws * px_rank / (t_dec / 1e3) / 1e6,
             "encode_ms": t_enc, "decode_ms": t_dec, "mlp_ms": mlp_ms,
             "bpp_total": 8.0 * total_bytes / px_rank, "bpp_payload": 8.0 * payload / px_rank,
-            "roofline": {"kernel": "k_decode<%s>" % args.precision, "bound": "tensor" if prec == 1 else "alu", "achieved": achieved,
+            "roofline": {"kernel": "k_decode<%s>" % (2 if args.model == "p350k" else args.precision), "bound": "tensor" if prec == 1 else "alu", "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": src + (" bf16_tflops" if prec == 1 else " sm_max_mhz x 148 SM x 128 FFMA x 2 (DESIGN.md)"),
                          "traffic_source": "stored ncu --set full capture of this config's k_decode launch "
                                            "(profiles/decode_traffic.json), not measured in this run",
                          "latency_floor_ms": floor_ms, "latency_frac": floor_ms / t_dec},
             # the throughput-bound encoder MLP (all pixels at once) against the same peak
-            "roofline_encode": {"kernel": "k_enc_pp" if prec == 1 else "k_enc_mlp<fp32>",
+            "roofline_encode": {"kernel": ("k_enc_mlp<2>" if args.model == "p350k" else "k_enc_pp") if prec == 1
+                                else "k_enc_mlp<fp32>",
                                 "bound": "tensor" if prec == 1 else "alu",
-                                "achieved": FLOP_PER_PX * px_rank / (mlp_ms / 1e3) / 1e12, "peak": peak,
+                                "achieved": fpp * px_rank / (mlp_ms / 1e3) / 1e12, "peak": peak,
                                 "unit": "TFLOP/s",
-                                "frac": FLOP_PER_PX * px_rank / (mlp_ms / 1e3) / 1e12 / peak,
+                                "frac": fpp * px_rank / (mlp_ms / 1e3) / 1e12 / peak,
                                 "note": "M=64 tcgen05 tiles cost as M=128: ceiling 0.5 of peak (DESIGN.md)"},
             "variants": variants,
             "strong_units": strong,

@@ -21,6 +21,7 @@
 #include "../../include/dlic.h"
 #include "dlic_device.cuh"
 #include "dlic_internal.h"
+#include "dlic_stream.cuh"
 #include "sha256.h"
 
 using namespace dlic;
@@ -31,6 +32,7 @@ struct dlic_model {
   uint8_t sha[32];
   std::vector<uint32_t> dims;
   bool p100k = false;  // topology the GPU engines run (see dlic_model_load)
+  bool p350k = false;  // 78 -> 256 x5 -> 256 (§8(f) f1): bf16 only, streamed weights (engine 2)
   uint32_t n_meta = 0;
   bool in3d = false;   // 87 window inputs: the 3D window (R13)
   uint8_t* d_wimg = nullptr;
@@ -264,11 +266,65 @@ static bool engine_weights(const ParsedModel& pm, std::vector<std::vector<float>
   return true;
 }
 
+// P350K (reading R4): 78 window inputs -> 256 x5 -> 256 logits, no pooling,
+// no metadata.
+static bool is_p350k(const ParsedModel& pm) {
+  if (pm.W.size() != (size_t)NLAYER || !pm.meta_range.empty() || pm.dims[0] != (uint32_t)KIN) return false;
+  for (int l = 0; l < NLAYER; ++l)
+    if (pm.dims[l + 1] != (uint32_t)SH || pm.pool[l] != 0) return false;
+  return true;
+}
+
+// The P350K slice stream (dlic_stream.cuh): 85 K=16 slices of 8 KB, layer 1
+// first (K in the engine's kpos_tap order, the fresh taps zero), each in the
+// UMMA no-swizzle K-major core-matrix layout of an N=256 operand; biases
+// [5][256] + [256] and the fresh-tap table (bf16-rounded, float4 per pair).
+static dlic_status upload_p350k(dlic_model* m, const ParsedModel& pm) {
+  std::vector<uint8_t> img(SWIMG_BYTES, 0);
+  for (int l = 0; l < NLAYER; ++l) {
+    const int K = l == 0 ? KPAD : SH;
+    for (int k = 0; k < K; ++k)
+      for (int n = 0; n < SH; ++n) {
+        const int kt = l == 0 ? kpos_tap(k) : k;
+        const bool fresh = l == 0 && (kt == TAP_FA || kt == TAP_FB);
+        const float v = kt >= 0 && kt < (l == 0 ? KIN : SH) && !fresh ? pm.W[l][(size_t)kt * SH + n] : 0.0f;
+        const uint16_t u = bf16_bits(v);
+        const int kk = k / 16, kl = k % 16;
+        const size_t a = (size_t)s_slice(l, kk) * SL_BYTES + (size_t)(kl / 8) * (SH / 8) * 128 +
+                         (size_t)(n / 8) * 128 + (n % 8) * 16 + (kl % 8) * 2;
+        memcpy(&img[a], &u, 2);
+      }
+  }
+  std::vector<float> bias(SBIAS_BYTES / 4, 0.0f);
+  for (int l = 0; l < NLAYER; ++l)
+    for (int n = 0; n < SH; ++n) bias[(size_t)l * SH + n] = pm.b[l][n];
+  auto bf16f = [](float v) {
+    const uint32_t u = (uint32_t)bf16_bits(v) << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+  };
+  for (int n = 0; n < SH; ++n) {
+    const size_t q = SB_FRESH + 4 * (size_t)(n / 2) + (n & 1);
+    bias[q] = bf16f(pm.W[0][(size_t)TAP_FA * SH + n]);
+    bias[q + 2] = bf16f(pm.W[0][(size_t)TAP_FB * SH + n]);
+  }
+  CUDA_TRY(cudaMalloc(&m->d_wimg, SWIMG_BYTES));
+  CUDA_TRY(cudaMalloc(&m->d_bias, bias.size() * 4));
+  CUDA_TRY(cudaMemcpy(m->d_wimg, img.data(), SWIMG_BYTES, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(m->d_bias, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice));
+  return DLIC_OK;
+}
+
 dlic_status upload_model(dlic_model* m, const ParsedModel& pm_in) {
   m->dims = pm_in.dims;
   std::vector<std::vector<float>> Wf;
   uint32_t n_meta = 0;
   bool in3d = false;
+  if (is_p350k(pm_in)) {
+    m->p350k = true;
+    return upload_p350k(m, pm_in);
+  }
   m->p100k = engine_weights(pm_in, Wf, n_meta, in3d);
   if (!m->p100k) return DLIC_OK;  // loadable; GPU engines refuse it at encode/decode
   m->n_meta = n_meta;
@@ -343,7 +399,8 @@ dlic_status upload_model(dlic_model* m, const ParsedModel& pm_in) {
 }
 
 // ---------------------------------------------------------------- planning
-dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Plan& p) {
+dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Plan& p,
+                      const dlic_model* m = nullptr) {
   dlic_opts d = {DLIC_PREC_BF16, 32, 0, 0, 0, nullptr, 0};
   if (o) d = *o;
   if (d.group_rows == 0) d.group_rows = 32;
@@ -360,6 +417,14 @@ dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Pl
   p.n_img = n;
   p.G = d.group_rows;
   p.precision = d.precision;
+  p.engine = d.precision;
+  if (m && m->p350k) {  // §8(f) f1: the streamed bf16 engine only
+    if (d.precision != DLIC_PREC_BF16)
+      return fail(DLIC_E_UNSUPPORTED_MODEL, "the 78->256x5->256 (P350K) model runs in bf16 only");
+    if (d.volume_depth > 0 || d.n_meta > 0)
+      return fail(DLIC_E_UNSUPPORTED_MODEL, "the P350K engine has no volume or metadata inputs");
+    p.engine = 2;
+  }
   p.tw = tiled ? std::min(d.tile_w, W) : W;
   p.th = tiled ? std::min(d.tile_h, H) : H;
   p.hdr_tw = tiled ? d.tile_w : 0;
@@ -371,7 +436,7 @@ dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Pl
   const uint32_t hl = H - (p.nty - 1) * p.th;
   p.gpl = (hl + p.G - 1) / p.G;
   p.spi = (p.nty - 1) * p.ntx * p.gpt + p.ntx * p.gpl;
-  if (dec_smem_bytes(d.precision, std::max(p.gpt, (H - (p.nty - 1) * p.th + p.G - 1) / p.G),
+  if (dec_smem_bytes(p.engine, std::max(p.gpt, (H - (p.nty - 1) * p.th + p.G - 1) / p.G),
                      d.volume_depth > 0 ? 1u : 0u) > dec_smem_limit())
     return fail(DLIC_E_INVALID_ARG, "too many row groups per unit for the decoder's shared memory: raise group_rows or tile");
   p.cap_words = 2 * p.G + p.G * p.tw;
@@ -407,9 +472,9 @@ dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Pl
 
 dlic_status check_model_gpu(const dlic_model* m) {
   if (!m) return fail(DLIC_E_INVALID_ARG, "null model");
-  if (!m->p100k)
+  if (!m->p100k && !m->p350k)
     return fail(DLIC_E_UNSUPPORTED_MODEL, "GPU engines implement (78 + n_meta <= 8)->128x5->256 with optional "
-                                          "power-of-two average pooling after hidden layers");
+                                          "power-of-two average pooling after hidden layers, and 78->256x5->256");
   return check_device(m->device);
 }
 
@@ -439,8 +504,8 @@ dlic_status check_schedulable(const Plan& p) {
   static std::map<std::tuple<int, uint32_t, uint32_t, size_t>, int> cache;
   int dev = 0;
   cudaGetDevice(&dev);
-  const size_t sm = dec_smem_bytes(p.precision, std::max(p.gpt, p.gpl), p.w3d);
-  const auto key = std::make_tuple(dev, p.precision, p.nc, sm);
+  const size_t sm = dec_smem_bytes(p.engine, std::max(p.gpt, p.gpl), p.w3d);
+  const auto key = std::make_tuple(dev, p.engine, p.nc, sm);
   int n;
   {
     std::lock_guard<std::mutex> l(mu);
@@ -448,7 +513,7 @@ dlic_status check_schedulable(const Plan& p) {
     if (it != cache.end()) {
       n = it->second;
     } else {
-      n = dec_max_active_clusters(p.precision, p.nc, sm);
+      n = dec_max_active_clusters(p.engine, p.nc, sm);
       cache[key] = n;
     }
   }
@@ -733,7 +798,7 @@ dlic_status dlic_encode(const dlic_model* m, const uint8_t* img, uint32_t width,
   dlic_status s = check_model_gpu(m);
   if (s != DLIC_OK) return s;
   Plan p;
-  s = make_plan(width, height, 1, opts, p);
+  s = make_plan(width, height, 1, opts, p, m);
   if (s != DLIC_OK) return s;
   s = check_schedulable(p);  // never write a container this device cannot decode
   if (s != DLIC_OK) return s;
@@ -792,7 +857,7 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
   if (s != DLIC_OK) return s;
   dlic_opts o = opts_of(h);
   Plan p;
-  s = make_plan(h.width, h.height, nsl, &o, p);
+  s = make_plan(h.width, h.height, nsl, &o, p, m);
   if (s != DLIC_OK) return s;
   if (p.spc != h.n_streams) return fail(DLIC_E_CORRUPT_CONTAINER, "stream count does not match the header dims");
   const bool part = unit_hi > 0;  // dlic_decode_units: only units [unit_lo, unit_hi)
@@ -962,7 +1027,7 @@ dlic_status dlic_debug_mlp(const dlic_model* m, const uint8_t* img, uint32_t wid
   if (s != DLIC_OK) return s;
   const uint32_t nsl = opts && opts->volume_depth ? opts->volume_depth : 1u;  // a volume: img holds nsl slices
   Plan p;
-  s = make_plan(width, height, nsl, opts, p);
+  s = make_plan(width, height, nsl, opts, p, m);
   if (s != DLIC_OK) return s;
   cudaStream_t st = my_stream();
   Scratch sc(st);
@@ -1008,7 +1073,7 @@ dlic_status dlic_encode_batch(const dlic_model* m, const uint8_t* imgs, uint32_t
   dlic_status s = check_model_gpu(m);
   if (s != DLIC_OK) return s;
   Plan p;
-  s = make_plan(width, height, n, opts, p);
+  s = make_plan(width, height, n, opts, p, m);
   if (s != DLIC_OK) return s;
   s = check_schedulable(p);
   if (s != DLIC_OK) return s;
@@ -1083,7 +1148,7 @@ dlic_status dlic_decode_batch(const dlic_model* m, const uint8_t* bits, size_t l
   if (img_capacity < npx) return fail(DLIC_E_BUFFER_TOO_SMALL, "image buffer");
   dlic_opts o = opts_of(h0);
   Plan p;
-  s = make_plan(h0.width, h0.height, n * (h0.depth ? h0.depth : 1u), &o, p);
+  s = make_plan(h0.width, h0.height, n * (h0.depth ? h0.depth : 1u), &o, p, m);
   if (s != DLIC_OK) return s;
   if (p.spc != h0.n_streams) return fail(DLIC_E_CORRUPT_CONTAINER, "stream count does not match the header dims");
   s = check_schedulable(p);
@@ -1140,7 +1205,7 @@ dlic_status dlic_encode_batch_device(const dlic_model* m, const uint8_t* d_imgs,
   dlic_status s = check_model_gpu(m);
   if (s != DLIC_OK) return s;
   Plan p;
-  s = make_plan(width, height, n, opts, p);
+  s = make_plan(width, height, n, opts, p, m);
   if (s != DLIC_OK) return s;
   if (out_capacity < p.max_container * p.n_cont)
     return fail(DLIC_E_BUFFER_TOO_SMALL, "out_capacity < containers * max bytes");
@@ -1165,7 +1230,7 @@ dlic_status dlic_decode_batch_device(const dlic_model* m, const uint8_t* d_bits,
     return fail(DLIC_E_VERSION_MISMATCH, "container tables come from another arithmetic revision");
   dlic_opts o = opts_of(*h_header);
   Plan p;
-  s = make_plan(h_header->width, h_header->height, n * (h_header->depth ? h_header->depth : 1u), &o, p);
+  s = make_plan(h_header->width, h_header->height, n * (h_header->depth ? h_header->depth : 1u), &o, p, m);
   if (s != DLIC_OK) return s;
   s = check_schedulable(p);
   if (s != DLIC_OK) return s;
@@ -1237,7 +1302,7 @@ dlic_status dlic_encode_units(const dlic_model* m, const uint8_t* img, uint32_t 
   dlic_status s = check_model_gpu(m);
   if (s != DLIC_OK) return s;
   Plan p;
-  s = make_plan(width, height, 1, opts, p);
+  s = make_plan(width, height, 1, opts, p, m);
   if (s != DLIC_OK) return s;
   s = restrict_units(p, unit_lo, unit_hi);
   if (s != DLIC_OK) return s;

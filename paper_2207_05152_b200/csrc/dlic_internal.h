@@ -29,6 +29,11 @@ struct Plan {
   // and one container (window id 2, slice-major streams); 2D: depth 1
   uint32_t depth, n_cont, spc;  // slices per container, containers, streams per container
   uint32_t w3d;                 // 3D window (R13): 9 taps from the slice below
+  // the network engine the kernels instantiate: 0 fp32 FFMA (P100K), 1 bf16
+  // tcgen05 with resident weights (P100K), 2 bf16 tcgen05 with weights
+  // streamed from L2 (P350K, dlic_stream.cuh).  The header keeps `precision`.
+  uint32_t engine;
+  uint32_t prof;  // diagnostics only (DLIC_PROF_STREAM): issuer cycle counters
 };
 
 constexpr uint32_t HDR_FIXED = 60;  // container header bytes before the size table (version 2)
@@ -74,7 +79,7 @@ __host__ __device__ inline void stream_info(const Plan& p, uint32_t s, uint32_t&
 
 // weights as uploaded at model load
 struct DevWeights {
-  const uint8_t* wimg;  // bf16 core-matrix image, WIMG_BYTES
+  const uint8_t* wimg;  // bf16 core-matrix image, WIMG_BYTES (P350K: the SWIMG_BYTES slice stream)
   const float* bias;    // BIAS_TOTAL floats
   const float* w32;     // fp32 blob (f32_off layout)
   // per-image layer-1 bias with the metadata inputs folded in ([n_img][HID]
@@ -120,9 +125,10 @@ cudaError_t launch_rans_dec_tables(const Plan& p, const uint8_t* d_bits, const u
 
 // how many decode clusters of nc CTAs (dynamic smem `smem`) the device can
 // co-schedule (cudaOccupancyMaxActiveClusters); 0 = the launch cannot run
-int dec_max_active_clusters(uint32_t precision, uint32_t nc, size_t smem);
-size_t dec_smem_bytes(uint32_t precision, uint32_t max_groups, uint32_t w3d = 0);
+// (engine: Plan::engine)
+int dec_max_active_clusters(uint32_t engine, uint32_t nc, size_t smem);
+size_t dec_smem_bytes(uint32_t engine, uint32_t max_groups, uint32_t w3d = 0);
 size_t dec_smem_limit();
-size_t enc_smem_bytes(uint32_t precision, uint32_t w3d = 0);
+size_t enc_smem_bytes(uint32_t engine, uint32_t w3d = 0);
 
 }  // namespace dlic

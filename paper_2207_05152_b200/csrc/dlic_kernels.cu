@@ -22,6 +22,7 @@
 
 #include "dlic_device.cuh"
 #include "dlic_internal.h"
+#include "dlic_stream.cuh"
 
 
 
@@ -49,7 +50,10 @@ constexpr uint32_t MAX_DYN_SMEM = 232448 - 1024;                     // 227 KB m
 // bias region in shared memory: biases + fresh-tap table (+ the 3D taps'
 // weights for volume plans)
 __host__ __device__ inline uint32_t bias_bytes(uint32_t w3d) { return BIAS_BYTES + (w3d ? W3D_BYTES : 0u); }
+// `precision` here is the ENGINE: 0 fp32 FFMA, 1 bf16 P100K (resident
+// weights), 2 bf16 P350K (streamed weights, dlic_stream.cuh)
 size_t enc_smem_bytes(uint32_t precision, uint32_t w3d) {
+  if (precision == 2) return SENG_BYTES;
   return precision == 1 ? WIMG_BYTES + bias_bytes(w3d) : F32_BUF_BYTES + F32_X_BYTES;
 }
 static uint32_t cursor_bytes(uint32_t ngroups) { return (ngroups * 4u + 15u) & ~15u; }
@@ -58,7 +62,7 @@ static uint32_t cursor_bytes(uint32_t ngroups) { return (ngroups * 4u + 15u) & ~
 constexpr uint32_t T3_BYTES = 2u * ROWS * 3u * 4u;
 size_t dec_smem_bytes(uint32_t precision, uint32_t max_groups, uint32_t w3d) {
   return enc_smem_bytes(precision, w3d) + RING_BYTES + 16 + 3 * cursor_bytes(max_groups) +
-         (w3d && precision == 1 ? T3_BYTES : 0u);
+         (w3d && precision == 1 ? T3_BYTES : 0u);  // (engine index, see enc_smem_bytes)
 }
 size_t dec_smem_limit() { return MAX_DYN_SMEM; }
 
@@ -73,6 +77,10 @@ template <>
 struct EngineSel<0> {
   using T = Fp32Engine;
 };
+template <>
+struct EngineSel<2> {
+  using T = TcStream;
+};
 
 __device__ __forceinline__ void load_smem(uint8_t* dst, const void* src, uint32_t bytes) {
   const int4* s4 = reinterpret_cast<const int4*>(src);
@@ -85,7 +93,34 @@ __device__ __forceinline__ void load_smem(uint8_t* dst, const void* src, uint32_
 template <int PREC>
 __device__ __forceinline__ uint8_t* engine_setup(typename EngineSel<PREC>::T& eng, uint8_t* smem, const DevWeights& w,
                                                  uint64_t* bar, uint32_t* tslot, uint32_t w3d) {  // bar: 2 mbarriers
-  if constexpr (PREC == 1) {
+  if constexpr (PREC == 2) {  // P350K: layer 1 | ring | biases | full[S] empty[S]; layers 2-6 streamed
+    load_smem(smem + SENG_L1, w.wimg, SL1_BYTES);
+    load_smem(smem + SENG_BIAS, w.bias, SBIAS_BYTES);
+    const uint32_t bars = smem_u32(smem + SENG_BARS);
+    if (threadIdx.x < 32) tmem_alloc(smem_u32(tslot), TM_COLS);
+    if (threadIdx.x == 0) {
+      mbar_init(smem_u32(bar), 1);
+      mbar_init(smem_u32(bar + 1), NTHREADS / 32);  // layer-1 input ready (row warps)
+      for (int i = 0; i < 2 * S_STAGES; ++i) mbar_init(bars + 8u * (uint32_t)i, 1);
+      fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    eng.tmem = *tslot;
+    eng.bias = reinterpret_cast<const float*>(smem + SENG_BIAS);
+    eng.b0 = eng.bias;
+    eng.bar = smem_u32(bar);
+    eng.bar2 = eng.bar;
+    eng.phase = 0;
+    eng.ring = smem_u32(smem + SENG_RING);
+    eng.l1s = smem_u32(smem + SENG_L1);
+    eng.full0 = bars;
+    eng.empty0 = bars + 8u * S_STAGES;
+    eng.wstream = w.wimg;
+    eng.aready = smem_u32(bar + 1);
+    return smem + SENG_BYTES;
+  } else if constexpr (PREC == 1) {
     load_smem(smem, w.wimg, WIMG_BYTES);
     load_smem(smem + WIMG_BYTES, w.bias, bias_bytes(w3d));
     if (threadIdx.x < 32) tmem_alloc(smem_u32(tslot), TM_COLS);
@@ -116,7 +151,7 @@ __device__ __forceinline__ uint8_t* engine_setup(typename EngineSel<PREC>::T& en
 
 template <int PREC>
 __device__ __forceinline__ void engine_teardown(typename EngineSel<PREC>::T& eng) {
-  if constexpr (PREC == 1) {
+  if constexpr (PREC >= 1) {
     tc_fence_before();
     __syncthreads();
     if (threadIdx.x < 32) tmem_dealloc(eng.tmem, TM_COLS);
@@ -139,7 +174,7 @@ __device__ __forceinline__ void tap_of(int u, int i, int& dr, int& dc) {
 template <int PREC, class Eng, class Get>
 __device__ __forceinline__ void feed(const Eng& eng, Get get, const uint32_t (*t3)[3] = nullptr) {
   const int u = 2 * col_grp() + half_id();
-  if constexpr (PREC == 1) {
+  if constexpr (PREC >= 1) {
     // v/256 exactly: (1 + v/256) has v in the top 8 mantissa bits; minus 1 is exact.
     const f2 m1 = f2_make(-1.0f, -1.0f);
     uint32_t a[5];
@@ -180,8 +215,11 @@ __device__ __forceinline__ float u8_unit(uint32_t v) {
 // Persistent CTAs over 64-pixel tiles of the units' raster order.  Thread
 // (row, j, h): pixel = tile*64 + row; (j, h) owns inputs [20j+10h, +10),
 // hidden columns [32j+16h, +16) and logits [64j+32h, +32) (dlic_device.cuh).
+// PREC 2 (P350K, TcStream): one more warp streams the weights and issues the
+// MMAs (TcStream::issue_tiles); the row warps run the same code as PREC 0.
+__host__ __device__ constexpr int enc_block(int prec) { return prec == 2 ? NTHREADS + 32 : NTHREADS; }
 template <int PREC>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(enc_block(PREC), 1)
     k_enc_mlp(Plan p, DevWeights w, const uint8_t* __restrict__ imgs, uint32_t* __restrict__ fc,
               float* __restrict__ dbg_logits, float* __restrict__ dbg_probs, uint16_t* __restrict__ dbg_freqs) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -194,6 +232,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint64_t tbase = (uint64_t)p.u_lo * p.tiles_per_unit;
   const uint64_t total = (uint64_t)p.u_cnt * p.tiles_per_unit;
   const bool dbg = dbg_logits || dbg_probs || dbg_freqs;
+  if constexpr (PREC == 2) {
+    if (threadIdx.x >= NTHREADS) {  // weight stream + MMA issuer: one network per tile of this CTA
+      // (the row warps take the one-tile-at-a-time loop: with 17 warps a
+      // thread has 96 registers, too few to hold a tile's logits across the
+      // next tile's network)
+      const uint64_t n = total > blockIdx.x ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+      uint64_t pt = 0;
+      int pk = 0;
+      auto next = [&](int& c) -> bool {  // the 20 chunks of every tile's network, in order
+        if (pt >= n) return false;
+        c = pk;
+        if (++pk == CH_NET) {
+          pk = 0;
+          ++pt;
+        }
+        return true;
+      };
+      eng.prof = p.prof != 0;
+      eng.mode = p.prof;
+      eng.issue_tiles(n, next);
+      engine_teardown<PREC>(eng);
+      return;
+    }
+  }
 
   // this thread's pixel of a tile (64 consecutive pixels of a unit in raster
   // order).  The pipelined loop walks its tiles in order, so the unit (and
@@ -270,17 +332,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   };
 
-  if (dbg) {  // debug exports: one tile at a time
+  if (dbg || PREC == 2) {  // debug exports (and P350K): one tile at a time
 #pragma unroll 1
     for (uint64_t tile = tbase + blockIdx.x; tile < tbase + total; tile += gridDim.x) {
+      const long long c0 = clock64();
       Px x = pixel(tile);
       load_sym(x);
       auto get = getter(x);
       feed_x(x, get);
       eng.start_l0();
+      const long long c1 = clock64();
       eng.run_rest(u8_unit(get(0, -1)), u8_unit(get(-1, 2)), [](int) {});
+      const long long c2 = clock64();
       const uint32_t v = q1_encode(eng, x.sym, (x.valid && dbg_probs) ? dbg_probs + x.gi * NOUT : nullptr,
                                    (x.valid && dbg_freqs) ? dbg_freqs + x.gi * NOUT : nullptr, dbg_freqs != nullptr);
+      if constexpr (PREC == 2) {
+        if (p.prof && threadIdx.x == 0) {
+          atomicAdd(&g_sprof[5], (unsigned long long)(c1 - c0));
+          atomicAdd(&g_sprof[6], (unsigned long long)(c2 - c1));
+          atomicAdd(&g_sprof[7], (unsigned long long)(clock64() - c2));
+        }
+      }
       if (dbg_logits) {  // raw logits (bias added) of this thread's 32 columns
         uint32_t lv[32];
         eng.ld32(lv);
@@ -289,6 +361,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int cc = 64 * col_grp() + 32 * half_id() + i;
             float l = __uint_as_float(lv[i]);
             if constexpr (PREC == 1) l = __fadd_rn(l, eng.bias[BIAS_OFF_LAST + cc]);
+            if constexpr (PREC == 2) l = __fadd_rn(l, eng.bias[SB_LAST + cc]);
             dbg_logits[x.gi * NOUT + cc] = l;
           }
       }
@@ -1000,7 +1073,7 @@ __global__ void k_dec_prep(Plan p, const uint8_t* __restrict__ bits, const uint6
 constexpr int DEC_THREADS = NTHREADS + 32;
 
 // bf16: one more warp (the 18th) only issues the network's MMAs (run_rest_ws)
-__host__ __device__ constexpr int dec_block(int prec) { return prec == 1 ? DEC_THREADS + 32 : DEC_THREADS; }
+__host__ __device__ constexpr int dec_block(int prec) { return prec >= 1 ? DEC_THREADS + 32 : DEC_THREADS; }
 
 template <int PREC, bool PROF, bool W3D>
 __global__ void __launch_bounds__(dec_block(PREC), 1)
@@ -1049,7 +1122,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
 
   typename EngineSel<PREC>::T eng;
   uint8_t* ring = engine_setup<PREC>(eng, smem, w, bar, &tslot, p.w3d);
-  if constexpr (PREC == 1) eng.bar2 = smem_u32(&bar[2]);
+  if constexpr (PREC == 1) eng.bar2 = smem_u32(&bar[2]);  // (TcStream: no half-layer split)
   if (w.b1img) {  // the unit's image's metadata-folded layer-1 bias
     if constexpr (PREC == 1) {
       __syncthreads();  // engine_setup's bias copy is complete
@@ -1288,9 +1361,9 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       apply(1, T - 1);
     }
     __syncthreads();  // (1) cursors final
-  } else if (PREC == 1 && threadIdx.x >= DEC_THREADS) {
+  } else if (PREC >= 1 && threadIdx.x >= DEC_THREADS) {
     // ======================================================= MMA issuer warp (bf16)
-    if constexpr (PREC == 1) {
+    if constexpr (PREC >= 1) {
       uint32_t aph = 0;
       auto any_t = [&](int t) -> bool {  // does any slot of this CTA hold an active row at front t
         const int rlo = t - uw + 1 > 0 ? (t - uw + 3) / 3 : 0;
@@ -1300,20 +1373,42 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         const uint32_t d = m - b < (uint32_t)ROWS ? 0u : ((b - m) & (NS - 1));
         return rlo + (int)d <= rhi;
       };
+      // P350K weight stream: the chunks of layers 2-6 (20 per network) of
+      // every front this CTA has an active row on, in order
+      int pr_t = 0, pr_k = 0;
+      auto next_slice = [&](int& c) -> bool {
+        while (pr_t < T) {
+          if (pr_k < CH_NET && any_t(pr_t)) {
+            c = pr_k++;
+            return true;
+          }
+          ++pr_t;
+          pr_k = 0;
+        }
+        return false;
+      };
       // layer 1 of front t over the 76 early taps, once every row warp has
       // written them and loaded the previous logits (a_ready)
       auto issue_l0 = [&](bool a) {
         if (a) {
           mbar_wait(a_ready, aph);
-          eng.issue_slices(0, 0, KPAD / 16, TcEngine::dcol_of(0));
-          eng.commit_both();
+          if constexpr (PREC == 2) {
+            eng.issue_l0();
+          } else {
+            eng.issue_slices(0, 0, KPAD / 16, TcEngine::dcol_of(0));
+            eng.commit_both();
+          }
         }
         aph ^= 1u;  // every row warp arrives once per front
       };
+      if constexpr (PREC == 2) eng.produce(next_slice);  // prime the ring
       issue_l0(any_t(0));
 #pragma unroll 1
       for (int t = 0; t < T; ++t) {
-        if (any_t(t)) eng.dec_issue_network();
+        if (any_t(t)) {
+          if constexpr (PREC == 2) eng.issue_network(next_slice);
+          else eng.dec_issue_network();
+        }
         const bool an = any_t(t + 1);
         if (NC > 1) {
           cluster_arrive();
@@ -1389,7 +1484,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
 #pragma unroll
       for (int i = 0; i < 9; ++i) tv[i] = bp[(i - 6) * RING_ROWS];
       tv[9] = bp[g9];
-      if constexpr (PREC == 1) {
+      if constexpr (PREC >= 1) {
         const f2 m1 = f2_make(-1.0f, -1.0f);
         uint32_t a[5];
 #pragma unroll
@@ -1427,10 +1522,10 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
     // follow this thread's load of the logits (the MMA overwrites them).
     // fp32: the input shares the logits buffer.
     auto early_gather = [&](int rn, int cn) {
-      if constexpr (PREC == 1) early_put(rn, cn);
+      if constexpr (PREC >= 1) early_put(rn, cn);
     };
     auto early_signal = [&](int rn, int cn) {
-      if constexpr (PREC == 1) {
+      if constexpr (PREC >= 1) {
         tc_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -1507,12 +1602,12 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         pf.mark(1);
         // network; the previous front's pixel goes to HBM in the layer-2 MMA
         // wait, the next front's early gather in the layer-3 MMA wait
-        if constexpr (PREC == 1) {
+        if constexpr (PREC >= 1) {
           eng.run_rest_ws(xa, xb, [&](int l) {
             if (l == 1 && optr) *optr = (uint8_t)opix;
             if (l == 2) early_gather(rn, cn);
-          }, [&](float2 (&bq)[8]) {
-            if constexpr (W3D) {  // this step's lower taps (s_t3, written by the rANS warp last step)
+          }, [&](auto& bq) {
+            if constexpr (W3D && PREC == 1) {  // this step's lower taps (s_t3, written by the rANS warp last step)
               const uint32_t* q = s_t3 + ((uint32_t)(t & 1) * ROWS + (uint32_t)row) * 3u;
               const uint32_t tt[3] = {q[0], q[1], q[2]};
               add_w3d(eng.bias, tt, bq);
@@ -1701,15 +1796,35 @@ cudaError_t launch_enc_mlp(const Plan& p, const DevWeights& w, const uint8_t* d_
                            int num_sms) {
   const uint64_t total = (uint64_t)p.u_cnt * p.tiles_per_unit;
   const uint32_t grid = (uint32_t)(total < (uint64_t)num_sms ? total : (uint64_t)num_sms);
-  const size_t sm = enc_smem_bytes(p.precision, p.w3d);
-  if (p.precision == 1 && (dbg_logits || dbg_probs || dbg_freqs)) {
+  const size_t sm = enc_smem_bytes(p.engine, p.w3d);
+  if (p.engine == 2) {  // P350K: streamed weights, one tile chain per CTA (+ debug exports)
+    cudaError_t e = set_smem(k_enc_mlp<2>, sm);
+    if (e != cudaSuccess) return e;
+    const bool prof = getenv("DLIC_PROF_STREAM") != nullptr;
+    Plan pp = p;
+    if (prof) {
+      pp.prof = 1u | (uint32_t)atoi(getenv("DLIC_PROF_STREAM"));
+      unsigned long long z[8] = {};
+      cudaMemcpyToSymbolAsync(g_sprof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+    }
+    k_enc_mlp<2><<<grid, enc_block(2), sm, st>>>(pp, w, d_imgs, d_fc, dbg_logits, dbg_probs, dbg_freqs);
+    if (prof) {
+      unsigned long long h[8];
+      cudaMemcpyFromSymbolAsync(h, g_sprof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      const double ns = (double)h[4];
+      fprintf(stderr, "[stream prof] per chunk (issuer, cycles): data wait %.0f  stage wait %.0f  epilogue wait %.0f  "
+              "total %.0f  (chunks %llu) | per tile (row thread 0): feed %.0f network %.0f q1 %.0f\n", h[0] / ns,
+              h[1] / ns, h[2] / ns, h[3] / ns, h[4], h[5] / (ns / CH_NET), h[6] / (ns / CH_NET), h[7] / (ns / CH_NET));
+    }
+  } else if (p.engine == 1 && (dbg_logits || dbg_probs || dbg_freqs)) {
     // parity tap: the production kernel with its debug exports
     const size_t sp = enc_pp_smem_bytes(p.w3d);
     auto k = p.w3d ? k_enc_pp<true, true> : k_enc_pp<true, false>;
     cudaError_t e = set_smem(k, sp);
     if (e != cudaSuccess) return e;
     k<<<grid, ENC_PP_THREADS, sp, st>>>(p, w, d_imgs, d_fc, nullptr, dbg_logits, dbg_probs, dbg_freqs);
-  } else if (p.precision == 1) {
+  } else if (p.engine == 1) {
     const size_t sp = enc_pp_smem_bytes(p.w3d);
     auto kp = p.w3d ? k_enc_pp<false, true> : k_enc_pp<false, false>;
     cudaError_t e = set_smem(kp, sp);
@@ -1770,7 +1885,10 @@ static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uin
                                    uint8_t* d_imgs, int32_t* d_status, cudaStream_t st,
                                    unsigned long long* prof, uint32_t* d_sync) {
   const size_t sm = dec_smem_bytes(PREC, p.gpt > p.gpl ? p.gpt : p.gpl, p.w3d);
-  auto kern = p.w3d ? k_decode<PREC, PROF, true> : k_decode<PREC, PROF, false>;
+  auto kern = k_decode<PREC, PROF, false>;
+  if constexpr (PREC < 2) {  // (P350K: no volumes)
+    if (p.w3d) kern = k_decode<PREC, PROF, true>;
+  }
   cudaError_t e = set_smem(kern, sm);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -1818,13 +1936,16 @@ static int max_clusters_t(uint32_t nc, size_t sm) {
   return n;
 }
 
-int dec_max_active_clusters(uint32_t precision, uint32_t nc, size_t smem) {
-  return precision == 1 ? max_clusters_t<1>(nc, smem) : max_clusters_t<0>(nc, smem);
+int dec_max_active_clusters(uint32_t engine, uint32_t nc, size_t smem) {
+  if (engine == 2) return max_clusters_t<2>(nc, smem);
+  return engine == 1 ? max_clusters_t<1>(nc, smem) : max_clusters_t<0>(nc, smem);
 }
 
 cudaError_t launch_decode(const Plan& p, const DevWeights& w, const uint8_t* d_bits, const uint64_t* d_cont_off,
                           const uint32_t* d_sbase, const uint32_t* d_slen, uint8_t* d_imgs, int32_t* d_status,
                           cudaStream_t st, unsigned long long* prof, uint32_t* d_sync) {
+  if (p.engine == 2)
+    return launch_decode_t<2, false>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof, d_sync);
   if (prof) {
     if (p.precision == 1)
       return launch_decode_t<1, true>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof, d_sync);

@@ -1,0 +1,318 @@
+// dlic_stream.cuh — the P350K engine (§8(f) f1): the paper's larger network
+// ("The number of neurons in the hidden layers varies between 128
+// neurons to 4096 neurons"; Table I ~350K row; reading R4: 78 ->
+// 256 x5 -> 256, 349,184 parameters).
+//
+// Its bf16 weights (696,320 B padded) do not fit one SM's shared memory
+// (227 KB).  Layer 1 (5 K=16 slices, 40 KB) stays resident; layers 2-6 (80
+// slices, 640 KB) are STREAMED from L2 for every network evaluation in
+// chunks of 4 slices (32 KB, K=64): every slice is an 8 KB block already in
+// the UMMA no-swizzle K-major core-matrix layout (element (n, k) of slice kk
+// at (k/8 - 2kk)*(N/8)*128 + (n/8)*128 + (n%8)*16 + (k%8)*2), a chunk is 4
+// consecutive slices, so one `cp.async.bulk` (TMA bulk copy, mbarrier
+// complete_tx) moves it into a ring of S_STAGES shared-memory stages.  The
+// MMA-issuer warp is both consumer and producer: before a chunk's 4 MMAs it
+// waits for the chunk's `full` barrier; a `tcgen05.commit` after them arrives
+// on the stage's `empty` barrier; after issuing chunk c it refills the stage
+// of chunk c-1 (whose MMAs are done by then) with the chunk S_STAGES-1
+// positions ahead in its consumption order, so the tensor core always has the
+// next chunk queued and the copies run S_STAGES-2 chunks (>= one layer) ahead.
+// (Per-slice stages measured ~800 issuer cycles per 8 KB slice: an mbarrier
+// try_wait alone costs ~90 cycles, B300_MICROARCH; chunks amortise it.)
+//
+// Per row the arithmetic mirrors TcEngine (the same softmax/Q1'/search code
+// consumes the same 256 logits, 8 threads x 32 columns per row): layer 1 =
+// MMA over the 76 early taps + the two fresh taps' fp32 FMAs in its epilogue,
+// hidden epilogues bias + ReLU + RN-to-bf16, M=64 tiles, K ascending.  The
+// encoder and the decoder run this same code, so tables stay bit-identical
+// (R8).  Hidden layers are N=256 and the accumulator is not double-buffered
+// (TMEM: D [0,256), A [256,384), A0 [384,424), exchange [448,512)), so a layer
+// is issued once every column group's epilogue of the previous layer is done.
+#pragma once
+#include "dlic_device.cuh"
+
+namespace dlic {
+
+constexpr int SH = 256;                     // P350K hidden width
+constexpr uint32_t SL_BYTES = 8192;         // one K=16 slice of an N=256 layer
+constexpr int SL_L0 = KPAD / 16;            // layer 1: 5 slices (76 taps + pads)
+constexpr int SL_H = SH / 16;               // layers 2-6: 16 slices each
+constexpr int SL_NET = 5 * SL_H;            // 80
+constexpr int SL_ALL = SL_L0 + SL_NET;      // 85
+constexpr uint32_t SWIMG_BYTES = SL_ALL * SL_BYTES;  // 696,320
+__host__ __device__ constexpr uint32_t s_slice(int l, int kk) {
+  return (l == 0 ? 0u : (uint32_t)(SL_L0 + (l - 1) * SL_H)) + (uint32_t)kk;
+}
+// biases in shared memory: [5][256] hidden, [256] logits, then the fresh-tap
+// table: float4 per output pair n, n+1 = {wa[n], wa[n+1], wb[n], wb[n+1]}
+constexpr int SB_LAST = 5 * SH;
+constexpr int SB_TOTAL = 5 * SH + NOUT;     // 1536
+constexpr int SB_FRESH = SB_TOTAL;
+constexpr int SB_FRESH_FLOATS = 2 * SH;     // 512
+constexpr uint32_t SBIAS_BYTES = (SB_TOTAL + SB_FRESH_FLOATS) * 4;  // 8,192
+constexpr int CH_SL = 4;                    // slices per streamed chunk
+constexpr uint32_t CH_BYTES = CH_SL * SL_BYTES;  // 32 KB
+constexpr int CH_LAYER = SL_H / CH_SL;      // 4 chunks per hidden layer
+constexpr int CH_NET = SL_NET / CH_SL;      // 20 chunks per network
+constexpr uint32_t SL1_BYTES = SL_L0 * SL_BYTES;  // resident layer 1: 40 KB
+constexpr int S_STAGES = 5;                 // ring depth: 160 KB
+constexpr uint32_t SRING_BYTES = S_STAGES * CH_BYTES;
+constexpr uint32_t SBAR_BYTES = 2 * S_STAGES * 8;
+// shared memory of the engine: layer 1 | ring | biases | full[S] empty[S]
+constexpr uint32_t SENG_L1 = 0, SENG_RING = SL1_BYTES, SENG_BIAS = SL1_BYTES + SRING_BYTES;
+constexpr uint32_t SENG_BARS = SENG_BIAS + SBIAS_BYTES;
+constexpr uint32_t SENG_BYTES = SENG_BARS + SBAR_BYTES;
+constexpr uint32_t TS_D = 0, TS_A = 256, TS_A0 = 384, TS_X = 448;
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+// issuer-side cycle counters (DLIC_PROF_STREAM=1, encoder): [0] waiting
+// for slice data, [1] waiting for a stage's MMA before refilling it, [2]
+// waiting for the previous layer's epilogues, [3] total issuer cycles, [4]
+// slices consumed
+__device__ unsigned long long g_sprof[8];
+
+struct TcStream {
+  uint32_t tmem;
+  const float* bias;       // shared
+  const float* b0;         // layer-1 biases (shared)
+  uint32_t bar, bar2;      // MMA completion (bar2: interface only)
+  uint32_t phase;
+  uint32_t ring, full0, empty0;  // shared addresses
+  uint32_t l1s;                  // resident layer-1 image (shared)
+  uint32_t aready;         // layer-1 input ready: one arrival per row warp
+  const uint8_t* wstream;  // the streamed weight image (global)
+  uint32_t ccnt = 0, pcnt = 0;   // slices consumed / produced (issuer warp)
+  bool prof = false;
+  uint32_t mode = 0;  // diagnostics: bit 1 no copies, bit 2 no MMAs (results invalid)
+  unsigned long long pw[3] = {0, 0, 0};
+
+  __device__ __forceinline__ uint32_t lane_off() const { return ((threadIdx.x >> 5) & 3u) << 21; }
+
+  // ---- row warps
+  // layer-1 input: 5 packed bf16 pairs of this thread (kpos_tap order) at A0
+  __device__ __forceinline__ void put_input(const uint32_t (&a)[5]) const {
+    const uint32_t base = tmem + lane_off() + TS_A0 + 10u * (uint32_t)col_grp();
+    tmem_st4h<5>(base, a);
+    tmem_st1h<5>(base + 4, a[4]);
+  }
+  // this thread's 32 biases of layer l: columns [64j + 32h, +32)
+  __device__ __forceinline__ void load_bias(int l, float2 (&bq)[16]) const {
+    const float4* b4 =
+        reinterpret_cast<const float4*>((l == 0 ? b0 : bias + l * SH) + 64 * col_grp() + 32 * half_id());
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 b = b4[q];
+      bq[2 * q] = make_float2(b.x, b.y);
+      bq[2 * q + 1] = make_float2(b.z, b.w);
+    }
+  }
+  __device__ __forceinline__ void wait_mma() {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    tc_fence_after();
+  }
+  // bias (+ fresh taps for layer 1) + ReLU + RN to bf16 -> A; columns
+  // [64j + 32h, +32) -> packed A columns [32j + 16h, +16)
+  template <bool L0>
+  __device__ __forceinline__ void epilogue(const float2 (&b2)[16], float xa, float xb) const {
+    const uint32_t lo = lane_off();
+    const int j = col_grp(), h = half_id();
+    uint32_t v[32];
+    tmem_ld32h<32>(tmem + lo + TS_D + 64u * (uint32_t)j, v);
+    tc_wait_ld();
+    const float4* fw = reinterpret_cast<const float4*>(bias + SB_FRESH) + 32 * j + 16 * h;
+    const f2 xa2 = f2_make(xa, xa), xb2 = f2_make(xb, xb);
+    uint32_t pk[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      f2 acc = f2_bits(v[2 * q], v[2 * q + 1]);
+      if constexpr (L0) {
+        const float4 w = fw[q];
+        acc = f2_fma(xa2, f2_make(w.x, w.y), acc);
+        acc = f2_fma(xb2, f2_make(w.z, w.w), acc);
+      }
+      float x0, x1;
+      f2_split(f2_add(acc, f2_make(b2[q].x, b2[q].y)), x0, x1);
+      pk[q] = pack_bf16_relu(x0, x1);
+    }
+    tmem_st8h<16>(tmem + lo + TS_A + 32u * (uint32_t)j, pk);
+    tmem_st8h<16>(tmem + lo + TS_A + 32u * (uint32_t)j + 8u, pk + 8);
+    tc_wait_st();
+  }
+  // Layers 1-6 after layer 1's MMA was issued; hook(l) runs in layer l+1's
+  // MMA wait (as TcEngine::run_rest_ws); pre0 is the interface's layer-1 bias
+  // hook (unused: volumes run on the P100K engine).  Column group j signals
+  // on named barrier 8 + j (4 warps + the issuer: 160 threads).
+  template <class Hook, class Pre0>
+  __device__ __forceinline__ void run_rest_ws(float xa, float xb, Hook&& hook, Pre0&&) {
+    float2 bq[16];
+    const uint32_t gbar = 8u + (uint32_t)col_grp();
+    auto signal = [&]() {
+      tc_fence_before();
+      asm volatile("bar.arrive %0, 160;" ::"r"(gbar) : "memory");
+    };
+    load_bias(0, bq);
+    wait_mma();
+    epilogue<true>(bq, xa, xb);
+    signal();
+#pragma unroll 1
+    for (int l = 1; l < NLAYER; ++l) {
+      hook(l);
+      if (l < NLAYER - 1) load_bias(l, bq);
+      wait_mma();
+      if (l < NLAYER - 1) {
+        epilogue<false>(bq, 0.0f, 0.0f);
+        signal();
+      }
+    }
+  }
+  // (encoder) the layer-1 input of this warp is in TMEM and its previous
+  // logits are loaded: the issuer may run layer 1
+  __device__ __forceinline__ void start_l0() const {
+    tc_wait_st();
+    tc_fence_before();
+    __syncwarp();
+    if (lane_id() == 0) mbar_arrive(aready);
+  }
+  template <class Hook>
+  __device__ __forceinline__ void run_rest(float xa, float xb, Hook&& hook, Prof* = nullptr) {
+    run_rest_ws(xa, xb, hook, [](auto&) {});
+  }
+  // softmax interface (as TcEngine): 32 logits of this thread, final biases,
+  // per-row exchange words through TMEM columns [448, 512)
+  __device__ __forceinline__ void ld32(uint32_t (&v)[32]) const {
+    tmem_ld32h<32>(tmem + lane_off() + TS_D + 64u * (uint32_t)col_grp(), v);
+    tc_wait_ld();
+  }
+  __device__ __forceinline__ float2 bias_pair(int i) const {
+    return reinterpret_cast<const float2*>(bias + SB_LAST + 64 * col_grp() + 32 * half_id())[i];
+  }
+  __device__ __forceinline__ void xput(int slot, uint32_t v) const {
+    tmem_st1h<TM_XUP>(tmem + lane_off() + TS_X + 4u * (uint32_t)slot + (uint32_t)col_grp(), v);
+  }
+  __device__ __forceinline__ void xsync() const {
+    tc_wait_st();
+    tc_fence_before();
+    quad_sync();
+    tc_fence_after();
+  }
+  __device__ __forceinline__ void xget8(int slot, uint32_t (&v)[8]) const {
+    tmem_ld8h<TM_XUP>(tmem + lane_off() + TS_X + 4u * (uint32_t)slot, v);
+    tc_wait_ld();
+  }
+  __device__ __forceinline__ void xget4(int slot, uint32_t (&v)[4]) const {
+    tmem_ld4h<TM_XUP>(tmem + lane_off() + TS_X + 4u * (uint32_t)slot, v);
+    tc_wait_ld();
+  }
+
+  // ---- issuer warp (whole converged warp)
+  // produce chunks until pcnt == ccnt + S_STAGES - 1 (or the schedule ends);
+  // next(c) yields the producer's next chunk (0..19 of a network) in
+  // consumption order
+  template <class Next>
+  __device__ __forceinline__ void produce(Next&& next) {
+    while (pcnt < ccnt + (uint32_t)S_STAGES - 1u) {
+      int c;
+      if (!next(c)) return;
+      const uint32_t s = pcnt % (uint32_t)S_STAGES;
+      if (pcnt >= (uint32_t)S_STAGES) {
+        const long long t0 = prof ? clock64() : 0;
+        mbar_wait(empty0 + 8u * s, ((pcnt / (uint32_t)S_STAGES) - 1u) & 1u);
+        if (prof) pw[1] += clock64() - t0;
+      }
+      if (lane_id() == 0) {
+        if (mode & 2u) {
+          mbar_arrive(full0 + 8u * s);
+        } else {
+          mbar_expect_tx(full0 + 8u * s, CH_BYTES);
+          bulk_g2s(ring + s * CH_BYTES, wstream + SL1_BYTES + (uint64_t)c * CH_BYTES, CH_BYTES, full0 + 8u * s);
+        }
+      }
+      __syncwarp();
+      ++pcnt;
+    }
+  }
+  // one chunk: wait for its data, 4 MMAs into D (accumulate unless the
+  // layer's first), release its stage when they complete
+  __device__ __forceinline__ void consume(int cl) {
+    const uint32_t s = ccnt % (uint32_t)S_STAGES;
+    const long long t0 = prof ? clock64() : 0;
+    mbar_wait(full0 + 8u * s, (ccnt / (uint32_t)S_STAGES) & 1u);
+    if (prof) pw[0] += clock64() - t0;
+    tc_fence_after();
+    if (mode & 4u) {
+      if (lane_id() == 0) mbar_arrive(empty0 + 8u * s);
+      __syncwarp();
+    } else {
+      const uint32_t id = umma_idesc(64, SH);
+#pragma unroll
+      for (int i = 0; i < CH_SL; ++i) {
+        const int kk = CH_SL * cl + i;
+        const uint64_t bd = umma_desc(ring + s * CH_BYTES + (uint32_t)i * SL_BYTES, (uint32_t)SH * 16u, 128u);
+        umma_ts_warp(tmem + TS_D, tmem + TS_A + 8u * (uint32_t)kk, bd, id, kk > 0 ? 1u : 0u);
+      }
+      umma_commit_warp(empty0 + 8u * s);
+    }
+    ++ccnt;
+  }
+  // layer 1 from the resident image, committed to `bar`
+  __device__ __forceinline__ void issue_l0() const {
+    tc_fence_after();
+    const uint32_t id = umma_idesc(64, SH);
+#pragma unroll
+    for (int kk = 0; kk < SL_L0; ++kk) {
+      const uint64_t bd = umma_desc(l1s + (uint32_t)kk * SL_BYTES, (uint32_t)SH * 16u, 128u);
+      umma_ts_warp(tmem + TS_D, tmem + TS_A0 + 8u * (uint32_t)kk, bd, id, kk > 0 ? 1u : 0u);
+    }
+    umma_commit_warp(bar);
+  }
+  // (encoder) n networks back to back, each once the row warps signal start_l0
+  template <class Next>
+  __device__ __forceinline__ void issue_tiles(uint64_t n, Next&& next) {
+    const long long t00 = clock64();
+    produce(next);
+    uint32_t aph = 0;
+#pragma unroll 1
+    for (uint64_t k = 0; k < n; ++k) {
+      mbar_wait(aready, aph);
+      aph ^= 1u;
+      issue_l0();
+      issue_network(next);
+    }
+    if (prof && lane_id() == 0) {
+      atomicAdd(&g_sprof[0], pw[0]);
+      atomicAdd(&g_sprof[1], pw[1]);
+      atomicAdd(&g_sprof[2], pw[2]);
+      atomicAdd(&g_sprof[3], (unsigned long long)(clock64() - t00));
+      atomicAdd(&g_sprof[4], (unsigned long long)ccnt);
+    }
+  }
+  // layers 2-6, each once every column group signalled its previous epilogue
+  template <class Next>
+  __device__ __forceinline__ void issue_network(Next&& next) {
+#pragma unroll 1
+    for (int l = 1; l < NLAYER; ++l) {
+      const long long t0 = prof ? clock64() : 0;
+#pragma unroll
+      for (int j = 0; j < NGRP; ++j) asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
+      if (prof) pw[2] += clock64() - t0;
+      tc_fence_after();
+#pragma unroll 1
+      for (int cl = 0; cl < CH_LAYER; ++cl) {
+        consume(cl);
+        produce(next);
+      }
+      umma_commit_warp(bar);
+    }
+  }
+};
+
+}  // namespace dlic

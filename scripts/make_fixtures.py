@@ -61,6 +61,17 @@ def p100k_3d():
     print("wrote", out)
 
 
+def p350k():
+    """fixtures/p350k_seeded.dlicmdl: the §8(f) f1 network P350K (78 -> 256x5
+    -> 256, reading R4), seeded He-uniform weights with biases (the GPU
+    tests' and bench's model)."""
+    layers = synth.he_uniform_layers(mlp.P350K, seed=3, bias_scale=0.1)
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "fixtures", "p350k_seeded.dlicmdl")
+    with open(out, "wb") as fh:
+        fh.write(model_io.save(layers))
+    print("wrote", out)
+
+
 def pool_meta():
     layers = synth.he_uniform_pooled(81, [128, 128, 128, 128, 128, 256], POOL, seed=7, bias_scale=0.1)
     out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "fixtures",
@@ -75,7 +86,10 @@ if __name__ == "__main__":
         pool_meta()
     elif len(sys.argv) > 1 and sys.argv[1] == "3d":
         p100k_3d()
+    elif len(sys.argv) > 1 and sys.argv[1] == "p350k":
+        p350k()
     else:
         main()
         pool_meta()
         p100k_3d()
+        p350k()
