@@ -929,6 +929,9 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
       for (int k = 0; k < 11; ++k) fprintf(stderr, " %s %.0f", nm[k], hp[k] / ctas / T);
       fprintf(stderr, "\n[dlic prof] network per front (sum over layers): sync %.0f issue+hook %.0f mma-wait %.0f "
               "epilogue %.0f\n", hp[16] / ctas / T, hp[17] / ctas / T, hp[18] / ctas / T, hp[19] / ctas / T);
+      if (p.precision == 1)
+        fprintf(stderr, "[dlic prof] issuer per front: network issue %.0f  arrive->layer-1 issued %.0f  cluster wait %.0f\n",
+                hp[26] / ctas / T, hp[27] / ctas / T, hp[28] / ctas / T);
       if (p.w3d)
         fprintf(stderr, "[dlic prof] 3D: waits for the slice below %.3f per front per CTA, %.0f cycles per wait\n",
                 hp[24] / ctas / T, hp[24] ? (double)hp[25] / hp[24] : 0.0);

@@ -1403,21 +1403,38 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       };
       if constexpr (PREC == 2) eng.produce(next_slice);  // prime the ring
       issue_l0(any_t(0));
+      unsigned long long ip[3] = {0, 0, 0};  // PROF: network issue, arrive->l0, l0->wait done
 #pragma unroll 1
       for (int t = 0; t < T; ++t) {
+        const long long i0 = PROF ? clock64() : 0;
         if (any_t(t)) {
           if constexpr (PREC == 2) eng.issue_network(next_slice);
           else eng.dec_issue_network();
         }
         const bool an = any_t(t + 1);
+        const long long i1 = PROF ? clock64() : 0;
+        long long i2 = 0;
         if (NC > 1) {
-          cluster_arrive();
+          if constexpr (PREC == 2) cluster_arrive_relaxed();
+          else cluster_arrive();
           issue_l0(an);
+          if (PROF) i2 = clock64();
           cluster_wait();
         } else {
           issue_l0(an);
+          if (PROF) i2 = clock64();
           __syncthreads();
         }
+        if (PROF) {
+          ip[0] += i1 - i0;
+          ip[1] += i2 - i1;
+          ip[2] += clock64() - i2;
+        }
+      }
+      if (PROF && lane == 0) {
+        atomicAdd(prof + 26, ip[0]);
+        atomicAdd(prof + 27, ip[1]);
+        atomicAdd(prof + 28, ip[2]);
       }
     }
     __syncthreads();  // (1) cursors final
@@ -1944,8 +1961,11 @@ int dec_max_active_clusters(uint32_t engine, uint32_t nc, size_t smem) {
 cudaError_t launch_decode(const Plan& p, const DevWeights& w, const uint8_t* d_bits, const uint64_t* d_cont_off,
                           const uint32_t* d_sbase, const uint32_t* d_slen, uint8_t* d_imgs, int32_t* d_status,
                           cudaStream_t st, unsigned long long* prof, uint32_t* d_sync) {
-  if (p.engine == 2)
+  if (p.engine == 2) {
+    if (prof)
+      return launch_decode_t<2, true>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof, d_sync);
     return launch_decode_t<2, false>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof, d_sync);
+  }
   if (prof) {
     if (p.precision == 1)
       return launch_decode_t<1, true>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof, d_sync);

@@ -18,8 +18,8 @@ args = sys.argv[1:]
 cfg = "C2"
 if args and not args[0].endswith(".so"):
     cfg = args.pop(0)
-blob = os.path.join(ROOT, "fixtures", "p100k_trained.dlicmdl")
-for lib in args:
+blob = os.path.join(ROOT, "fixtures", os.environ.get("DLIC_MODEL_FILE", "p100k_trained.dlicmdl"))
+for lib in args or [os.path.join(ROOT, "paper_2207_05152_b200", "libdlic.so")]:
     env = dict(os.environ, DLIC_LIB=os.path.abspath(lib), DLIC_PROF="1")
     out = subprocess.run([sys.executable, "-c", CHILD % (ROOT, cfg, blob)], env=env, capture_output=True, text=True)
     print(lib)
