@@ -21,6 +21,15 @@ import numpy as np
 from . import container, mlp, model_io, quant, schedule, streams, window
 
 
+def alphabet_bits(layers) -> int:
+    """8 for a 256-output network, 12 for 4096 outputs."""
+    lay = layers["layers"] if isinstance(layers, dict) else layers
+    n = np.asarray(lay[-1][0]).shape[1]
+    if n not in (256, 4096):
+        raise ValueError("output layer must have 256 or 4096 neurons")
+    return 8 if n == 256 else 12
+
+
 def _net(layers):
     """`layers` is a list of (W, b), or the dict of model_io.load_net (+ the
     image's normalised metadata under "meta_norm")."""
@@ -33,9 +42,10 @@ def unit_front_tables(layers, precision: int, img: np.ndarray, rows, cols):
     """Tables for the pixels (rows, cols) of one front of one unit image.
 
     P:90: one matrix per front, one row per pixel neighbourhood (window
-    features, then the image's metadata features)."""
+    features, then the image's metadata features).  The alphabet (8 or 12
+    bits) follows from the network's output width."""
     lay, pool, meta_norm = _net(layers)
-    x = window.net_inputs(img, rows, cols, meta_norm)
+    x = window.net_inputs(img, rows, cols, meta_norm, alphabet_bits(lay))
     logits = mlp.logits_path(lay, x, precision, pool)
     p, f, c = quant.tables_from_logits(logits)
     return logits, p, f, c
@@ -76,7 +86,8 @@ def all_pixel_tables(layers, precision: int, img: np.ndarray, chunk: int = 65536
 
 def encode_with_tables(fs_img: np.ndarray, cs_img: np.ndarray, width: int, height: int,
                        precision: int, group_rows: int, tile_w: int, tile_h: int,
-                       model_sha: bytes, numerics: int = container.ORACLE_NUMERICS, meta=None) -> bytes:
+                       model_sha: bytes, numerics: int = container.ORACLE_NUMERICS, meta=None,
+                       bits: int = 8) -> bytes:
     """Container from given per-pixel (f_s, c_s) of the true symbols — the
     "oracle fed the same integer tables" leg (north_star).  `numerics` is the
     header field naming the arithmetic that produced the tables (the caller's;
@@ -85,7 +96,8 @@ def encode_with_tables(fs_img: np.ndarray, cs_img: np.ndarray, width: int, heigh
     for (x0, y0, tw, th) in container.tiles(width, height, tile_w, tile_h):
         sts = streams.encode_unit(fs_img[y0:y0 + th, x0:x0 + tw], cs_img[y0:y0 + th, x0:x0 + tw], group_rows)
         out += [streams.rans.words_to_bytes(s) for s in sts]
-    return container.write(width, height, precision, group_rows, tile_w, tile_h, model_sha, out, numerics, meta)
+    return container.write(width, height, precision, group_rows, tile_w, tile_h, model_sha, out, numerics, meta,
+                           bits=bits)
 
 
 def encode(img: np.ndarray, model_blob: bytes, precision: int = 0, group_rows: int = 32,
@@ -95,6 +107,9 @@ def encode(img: np.ndarray, model_blob: bytes, precision: int = 0, group_rows: i
     net = model_io.load_net(model_blob)
     net["meta_norm"] = window.meta_features(meta, net["meta_range"])
     layers = net
+    bits = alphabet_bits(net)
+    if np.asarray(img).max(initial=0) >= (1 << bits):
+        raise ValueError("pixel value outside the model's %d-bit alphabet" % bits)
     h, w = img.shape
     fs = np.zeros((h, w), np.int64)
     cs = np.zeros((h, w), np.int64)
@@ -103,7 +118,7 @@ def encode(img: np.ndarray, model_blob: bytes, precision: int = 0, group_rows: i
         fs[y0:y0 + th, x0:x0 + tw] = f_u
         cs[y0:y0 + th, x0:x0 + tw] = c_u
     return encode_with_tables(fs, cs, w, h, precision, group_rows, tile_w, tile_h, model_io.digest(model_blob),
-                              meta=meta)
+                              meta=meta, bits=bits)
 
 
 class ModelHashMismatch(Exception):
@@ -133,20 +148,23 @@ def decode(blob: bytes, model_blob: bytes) -> np.ndarray:
         raise container.CorruptContainer("numerics revision %d is not the oracle's" % hdr["numerics"])
     layers = model_io.load_net(model_blob)
     layers["meta_norm"] = window.meta_features(hdr["meta"], layers["meta_range"])   # re-read from the container
+    if alphabet_bits(layers) != hdr["bits"]:
+        raise container.CorruptContainer("container alphabet does not match the model's output layer")
     prec = hdr["precision"]
-    out = np.zeros((hdr["height"], hdr["width"]), np.uint8)
+    dt = np.uint8 if hdr["bits"] == 8 else np.uint16
+    out = np.zeros((hdr["height"], hdr["width"]), dt)
     for (x0, y0, tw, th), sts in _split_streams(hdr):
         def ft(t, rows, cols, img):
             _, _, f, c = unit_front_tables(layers, prec, img, rows, cols)
             return f, c
-        out[y0:y0 + th, x0:x0 + tw] = streams.decode_unit(sts, tw, th, hdr["group_rows"], ft)
+        out[y0:y0 + th, x0:x0 + tw] = streams.decode_unit(sts, tw, th, hdr["group_rows"], ft, dtype=dt)
     return out
 
 
 def decode_with_tables(blob: bytes, freq_tables: np.ndarray) -> np.ndarray:
     """Decode a container given every pixel's full table (H, W, 256)."""
     hdr = container.parse(blob)
-    out = np.zeros((hdr["height"], hdr["width"]), np.uint8)
+    out = np.zeros((hdr["height"], hdr["width"]), np.uint8 if hdr["bits"] == 8 else np.uint16)
     for (x0, y0, tw, th), sts in _split_streams(hdr):
         out[y0:y0 + th, x0:x0 + tw] = streams.decode_unit_with_tables(
             sts, freq_tables[y0:y0 + th, x0:x0 + tw], hdr["group_rows"])
@@ -169,9 +187,10 @@ def raster_decode(blob: bytes, model_blob: bytes) -> np.ndarray:
     layers = model_io.load_net(model_blob)
     layers["meta_norm"] = window.meta_features(hdr["meta"], layers["meta_range"])
     prec = hdr["precision"]
-    out = np.zeros((hdr["height"], hdr["width"]), np.uint8)
+    dt = np.uint8 if hdr["bits"] == 8 else np.uint16
+    out = np.zeros((hdr["height"], hdr["width"]), dt)
     for (x0, y0, tw, th), sts in _split_streams(hdr):
-        img = np.zeros((th, tw), np.uint8)
+        img = np.zeros((th, tw), dt)
         x = {}
         cur = {}
         for r in range(th):

@@ -8,7 +8,9 @@ of DESIGN.md "Container", version 2), little-endian:
   off  6  u8  window id (1 = 9x9 causal, 78 inputs, R1; 2 = the 3D window of
               R13: 78 + a 3x3 box in the slice below, 87 inputs -- the
               container then holds a whole volume, streams slice-major)
-  off  7  u8  fill value (0; R2)
+  off  7  u8  alphabet: 0 = 8-bit pixels (256 symbols; the fill value 0 of
+              R2 in earlier drafts, so 8-bit containers are unchanged), 12 =
+              12-bit pixels (4096 symbols, reading R15)
   off  8  u32 width        off 12 u32 height
   off 16  u16 tile_w       off 18 u16 tile_h    (0, 0 = untiled)
   off 20  u16 group rows G
@@ -59,9 +61,9 @@ def streams_per_slice(width, height, tile_w, tile_h, group_rows) -> int:
 
 
 def write(width, height, precision, group_rows, tile_w, tile_h, model_sha, stream_bytes,
-          numerics=ORACLE_NUMERICS, meta=None, window_id=WINDOW_ID) -> bytes:
-    assert len(model_sha) == 32
-    hdr = MAGIC + struct.pack("<BBBBIIHHHH", VERSION, precision, window_id, 0, width, height,
+          numerics=ORACLE_NUMERICS, meta=None, window_id=WINDOW_ID, bits=8) -> bytes:
+    assert len(model_sha) == 32 and bits in (8, 12)
+    hdr = MAGIC + struct.pack("<BBBBIIHHHH", VERSION, precision, window_id, 0 if bits == 8 else 12, width, height,
                               tile_w, tile_h, group_rows, numerics)
     hdr += model_sha + struct.pack("<I", len(stream_bytes))
     hdr += b"".join(struct.pack("<I", len(s)) for s in stream_bytes)
@@ -74,7 +76,7 @@ def parse(blob: bytes):
     if len(blob) < HEADER_FIXED or blob[:4] != MAGIC:
         raise CorruptContainer("magic")
     ver, prec, win, fill, w, h, tw, th, g, num = struct.unpack_from("<BBBBIIHHHH", blob, 4)
-    if ver != VERSION or win not in (WINDOW_ID, WINDOW_3D) or fill != 0 or prec > 1 or g == 0:
+    if ver != VERSION or win not in (WINDOW_ID, WINDOW_3D) or fill not in (0, 12) or prec > 1 or g == 0:
         raise CorruptContainer("header fields")
     sha = blob[24:56]
     (n,) = struct.unpack_from("<I", blob, 56)
@@ -102,4 +104,5 @@ def parse(blob: bytes):
     if n % sps or (win == WINDOW_ID and n != sps):
         raise CorruptContainer("stream count")
     return dict(width=w, height=h, precision=prec, tile_w=tw, tile_h=th, group_rows=g, numerics=num,
-                model_sha=sha, streams=streams, header_bytes=hdr_bytes, meta=meta, window=win, depth=n // sps)
+                model_sha=sha, streams=streams, header_bytes=hdr_bytes, meta=meta, window=win, depth=n // sps,
+                bits=8 if fill == 0 else 12)

@@ -38,6 +38,10 @@ import numpy as np
 
 P100K = (78, 128, 128, 128, 128, 128, 256)
 P350K = (78, 256, 256, 256, 256, 256, 256)
+# 12-bit alphabet (P:207-208, 4096 outputs; reading R16): P350K's hidden
+# stack with a 4096-neuron softmax layer, 1,336,064 parameters (Table III
+# "~1,350,000")
+P12 = (78, 256, 256, 256, 256, 256, 4096)
 
 
 def n_params(dims) -> int:

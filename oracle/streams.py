@@ -53,19 +53,19 @@ class CorruptStream(Exception):
 
 
 def decode_unit(streams, width: int, height: int, group_rows: int, front_tables,
-                lag: int = schedule.LAG):
+                lag: int = schedule.LAG, dtype=np.uint8):
     """Wavefront decode of one unit.
 
     front_tables(t, rows, cols, img) -> (freqs, cums), arrays (n, A) for the
     pixels (rows[i], cols[i]) of front t, computed from the partially decoded
     image `img` (the window only holds already-decoded pixels).
-    Returns the decoded (h, w) uint8 image.
+    Returns the decoded (h, w) image (uint8; uint16 for the 12-bit alphabet).
     """
     h, w = height, width
     ng = n_groups(h, group_rows)
     if len(streams) != ng:
         raise CorruptStream("stream count")
-    img = np.zeros((h, w), dtype=np.uint8)
+    img = np.zeros((h, w), dtype=dtype)
     x = {}
     cursor = []
     for g in range(ng):
@@ -114,4 +114,4 @@ def decode_unit_with_tables(streams, freq_tables: np.ndarray, group_rows: int):
     def ft(t, rows, cols, img):
         return freq_tables[rows, cols].astype(np.int64), cum_tables[rows, cols]
 
-    return decode_unit(streams, w, h, group_rows, ft)
+    return decode_unit(streams, w, h, group_rows, ft, dtype=np.uint8 if freq_tables.shape[-1] <= 256 else np.uint16)

@@ -10,6 +10,8 @@ Readings (R1/R2):
   * cells at or after the target in raster order ((0,0), (0,1), (0,2)) are
     masked out and dropped, leaving 78 inputs in row-major order;
   * the dummy value is pixel value 0; features are v / 256.
+  * 12-bit alphabet ("one 12-bit channel, leading to 4096 possible
+    shades of gray"; reading R15): features are v / 4096, the same 78 taps.
 """
 
 from __future__ import annotations
@@ -64,9 +66,11 @@ def gather_many(img: np.ndarray, rows: np.ndarray, cols: np.ndarray, fill: int =
     return pad[(rows[:, None] + dr[None, :] + 8), (cols[:, None] + dc[None, :] + 6)]
 
 
-def features(x: np.ndarray) -> np.ndarray:
-    """Network inputs v / 256 (reading R2; exact in fp32 and bf16)."""
-    return np.asarray(x, dtype=np.float64) / 256.0
+def features(x: np.ndarray, bits: int = 8) -> np.ndarray:
+    """Network inputs v / 2^bits (reading R2: v / 256, exact in fp32 and bf16;
+    R15: v / 4096 for 12-bit pixels, exact in fp32, rounded to bf16 by the bf16
+    definition's input rounding)."""
+    return np.asarray(x, dtype=np.float64) / float(1 << bits)
 
 
 def meta_features(meta, meta_range) -> np.ndarray:
@@ -83,10 +87,10 @@ def meta_features(meta, meta_range) -> np.ndarray:
     return ((m - lo) / (hi - lo)).astype(np.float32).astype(np.float64)
 
 
-def net_inputs(img: np.ndarray, rows, cols, meta_norm=None) -> np.ndarray:
+def net_inputs(img: np.ndarray, rows, cols, meta_norm=None, bits: int = 8) -> np.ndarray:
     """Network input rows: 78 window features, then the metadata features
     (identical for every pixel of the image)."""
-    x = features(gather_many(img, rows, cols))
+    x = features(gather_many(img, rows, cols), bits)
     if meta_norm is None or len(meta_norm) == 0:
         return x
     return np.concatenate([x, np.broadcast_to(np.asarray(meta_norm, np.float64), (x.shape[0], len(meta_norm)))], 1)

@@ -62,16 +62,19 @@ def natural_like(width: int = 768, height: int = 512, seed: int = 0,
     return np.ascontiguousarray(np.clip(np.rint(v), 0, 255).astype(np.uint8))
 
 
-def mri_like_volume(size: int = 256, slices: int = 32, seed: int = 0) -> np.ndarray:
+def mri_like_volume(size: int = 256, slices: int = 32, seed: int = 0, bits: int = 8) -> np.ndarray:
     """C3 "MRI-like" volume (Fig. 5): (slices, size, size) u8.
 
     Rician background |N(0,2)+iN(0,2)|, a head ellipse and 3-8 inner ellipses
     whose smooth intensities (40-220) and radii vary smoothly across slices.
     The histogram is heavily skewed toward the dark background.
+    bits=12 (the paper's MRI bit depth): every intensity and noise
+    scale x16, values in [0, 4095], u16 (the same draws as bits=8).
     """
+    sc = float(1 << (bits - 8))
     rng = np.random.default_rng(seed)
     yy, xx = np.mgrid[0:size, 0:size].astype(np.float64)
-    out = np.empty((slices, size, size), dtype=np.uint8)
+    out = np.empty((slices, size, size), dtype=np.uint8 if bits == 8 else np.uint16)
     n_in = int(rng.integers(3, 9))
     head = dict(cy=size / 2 + rng.uniform(-8, 8), cx=size / 2 + rng.uniform(-8, 8),
                 ry=size * rng.uniform(0.36, 0.44), rx=size * rng.uniform(0.30, 0.38),
@@ -94,7 +97,7 @@ def mri_like_volume(size: int = 256, slices: int = 32, seed: int = 0) -> np.ndar
             m = (((yy - e["cy"] - 20 * z * e["drift"]) / (e["ry"] * shrink)) ** 2
                  + ((xx - e["cx"]) / (e["rx"] * shrink)) ** 2) <= 1.0
             v = np.where(m & hm, e["val"] * (1 + 0.3 * z * e["drift"]) + rng.normal(0, 3, (size, size)), v)
-        out[s] = np.clip(np.rint(v), 0, 255).astype(np.uint8)
+        out[s] = np.clip(np.rint(v * sc), 0, (1 << bits) - 1).astype(out.dtype)
     return out
 
 
