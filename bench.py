@@ -43,7 +43,10 @@ FLOP_PER_PX_P350K = 695296      # P350K: 2 * (78*256 + 4*256*256 + 256*256)
 # per front, layers 2-6 are a dependent MMA chain (layer 1 is issued a front
 # early), M=64 tiles costing as M=128 (8192 FLOP/clk/SM): P100K 4 x 8 x 64 +
 # 8 x 128 = 3072 cycles; P350K 5 x 16 x 128 = 10240 cycles
-FRONT_FLOOR_CYC = {"p350k": 10240}
+FRONT_FLOOR_CYC = {"p350k": 10240, "p12": 4 * 16 * 128 + 2 * 32 * 16 * 64}
+# P12 (12-bit, reading R16): 78 -> 256x5 -> 4096; the head is evaluated twice
+# (two-pass softmax): algorithmic work counts it once
+FLOP_PER_PX_P12 = 2 * (78 * 256 + 4 * 256 * 256 + 256 * 4096)
 # model fixtures: (file, metadata reals per image or None, description)
 MODELS = {
     "p100k": ("p100k_trained.dlicmdl", None,
@@ -56,6 +59,10 @@ MODELS = {
               "P350K: 78 -> 256x5 -> 256 (349,184 parameters, reading R4), seeded He-uniform "
               "(fixtures/p350k_seeded.dlicmdl); bf16 only, weights streamed from L2 through a TMA ring "
               "(engine 2, 695,296 FLOP/px)"),
+    "p12": ("p12_seeded.dlicmdl", None,
+            "P12: 78 -> 256x5 -> 4096 (12-bit alphabet, 1,336,064 parameters, readings R15-R17), seeded "
+            "He-uniform (fixtures/p12_seeded.dlicmdl); bf16 only, streamed weights, two-pass 4096-wide head "
+            "(engine 3); images: 12-bit MRI-like slices (u16)"),
     "3d": ("p100k_3d.dlicmdl", None,
            "P100K-3D: 78 + the 3x3 box of the slice below (87 inputs) -> 128x5 -> 256, seeded random "
            "(fixtures/p100k_3d.dlicmdl; the 9 lower taps enter layer 1 through the bias term, 2,304 FLOP/px on "
@@ -206,6 +213,10 @@ def args_w(args):
 def images_for(args, rank, n):
     import synth
     cfg = args.config
+    if args.model == "p12":   # 12-bit MRI-like slices, 256x256 (C3 geometry)
+        per = 35               # Table III's scan: 256 x 256 x 35
+        vols = [synth.mri_like_volume(256, per, seed=100 * rank + v, bits=12) for v in range((n + per - 1) // per)]
+        return np.ascontiguousarray(np.concatenate(vols)[:n, :args_h(args), :args_w(args)])
     if cfg == "C1":
         return np.stack([synth.gradient_noise(32, 32, seed=rank * 1000 + i) for i in range(n)])
     if cfg == "C2":
@@ -257,7 +268,9 @@ def measure_variant(dl, model, d_imgs, prec, g, tile, reps=5):
             "bpp_total": 8.0 * float(sizes.sum()) / px}
 
 
-def default_batch(cfg):
+def default_batch(cfg, model=None):
+    if model == "p12":
+        return 35
     # C3: 512 slices across 8 GPUs = 64 per GPU; C5: "batch of 64" per GPU
     # (960 tiles of 768x720 -> 26 waves of 37 four-CTA clusters: no tail)
     return {"C1": 1, "C2": 1, "C3": 64, "C4": 1, "C5": 64}[cfg]
@@ -297,7 +310,12 @@ def arm_config(args, n, W, H, tile, g, ws):
     """The config object of the JSON line (both arms)."""
     vd = volume_depth(args)
     extra = {"volume_depth": vd, "volumes_per_gpu": n // vd} if vd else {}
-    return dict({"workload": CONFIG_DESC[args.config], "images_per_gpu": n, "width": W, "height": H,
+    if args.model == "p12":
+        extra = dict(extra, alphabet_bits=12)
+    wl = CONFIG_DESC[args.config]
+    if args.model == "p12":
+        wl = "C3 geometry at the paper's MRI bit depth: 12-bit MRI-like slices 256x256, 35 per GPU (Table III's scan)"
+    return dict({"workload": wl, "images_per_gpu": n, "width": W, "height": H,
             "tile": list(tile), "group_rows": g, "precision": args.precision,
             "weights": MODELS[args.model][2],
             "l2": "flushed between timed steps (256 MiB write, untimed)", "parallelism": "dp%d" % ws}, **extra)
@@ -316,6 +334,8 @@ def run_reference(args):
     # one whole image per step for C1-C3 (C2: ~10 s of oracle work); larger
     # configs: the top-left 768x512 of the first image (~10 s)
     sh, sw = min(img.shape[0], 512), min(img.shape[1], 768)
+    if args.model == "p12":
+        sh, sw = 96, 96
     sample = np.ascontiguousarray(img[:sh, :sw])
     prec = 1 if args.precision == "bf16" else 0
     g, _ = opts_for(args.config)
@@ -368,6 +388,8 @@ def cpu_baseline_sample(args, img):
     with open(os.path.join(ROOT, "fixtures", MODELS[args.model][0]), "rb") as fh:
         blob = fh.read()
     sh, sw = min(img.shape[0], 512), min(img.shape[1], 768)   # C2: the whole image (~10-15 s)
+    if args.model == "p12":   # 4096 outputs: a 96x96 corner (~10-20 s)
+        sh, sw = 96, 96
     sample = np.ascontiguousarray(img[:sh, :sw])
     prec = 1 if args.precision == "bf16" else 0
     vd = volume_depth(args)
@@ -467,7 +489,7 @@ def main():
     model = dl.dlic_model_load(blob, local)
     prec = 1 if args.precision == "bf16" else 0
     g, tile = tile_for(args)
-    n = args.batch or default_batch(args.config)
+    n = args.batch or default_batch(args.config, args.model)
     imgs = images_for(args, rank, n)
     vd = volume_depth(args)
     if vd and n % vd:
@@ -478,7 +500,7 @@ def main():
     _, H, W = imgs.shape
     px_rank = n * H * W
     stream = torch.cuda.current_stream(dev)
-    d_imgs = torch.from_numpy(imgs).to(dev)
+    d_imgs = torch.from_numpy(imgs.view(np.int16) if imgs.dtype == np.uint16 else imgs).to(dev)   # (u16: same bytes)
     d_dec = torch.empty_like(d_imgs)
     d_status = torch.zeros(n, dtype=torch.int32, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
@@ -599,13 +621,15 @@ def main():
     if rank == 0:
         peaks, src = load_peaks()
         # dominant kernel: the wavefront decoder (latency-bound front chain)
-        fpp = FLOP_PER_PX_P350K if args.model == "p350k" else FLOP_PER_PX
+        fpp = {"p350k": FLOP_PER_PX_P350K, "p12": FLOP_PER_PX_P12}.get(args.model, FLOP_PER_PX)
         dec_flops = fpp * px_rank
         achieved = dec_flops / (t_dec / 1e3) / 1e12
         # fp32 path runs on CUDA-core FFMA: 148 SMs x 128 FMA/clk x 2 x sm_max
         peak = peaks["bf16_tflops"] if prec == 1 else 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         traffic = None   # dram bytes per k_decode launch from a stored ncu --set full capture (not this run)
         try:
+            if args.model != "p100k":
+                raise OSError("stored captures are of the P100K decoder")
             with open(os.path.join(ROOT, "profiles", "decode_traffic.json")) as fh:
                 traffic = json.load(fh).get("%s_%s" % (args.config, args.precision))
         except (OSError, ValueError):
@@ -626,14 +650,15 @@ def main():
             "decode_mpx_s": ws * px_rank / (t_dec / 1e3) / 1e6,
             "encode_ms": t_enc, "decode_ms": t_dec, "mlp_ms": mlp_ms,
             "bpp_total": 8.0 * total_bytes / px_rank, "bpp_payload": 8.0 * payload / px_rank,
-            "roofline": {"kernel": "k_decode<%s>" % (2 if args.model == "p350k" else args.precision), "bound": "tensor" if prec == 1 else "alu", "achieved": achieved,
+            "roofline": {"kernel": "k_decode<%s>" % ({"p350k": 2, "p12": 3}.get(args.model, args.precision)), "bound": "tensor" if prec == 1 else "alu", "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": src + (" bf16_tflops" if prec == 1 else " sm_max_mhz x 148 SM x 128 FFMA x 2 (DESIGN.md)"),
                          "traffic_source": "stored ncu --set full capture of this config's k_decode launch "
                                            "(profiles/decode_traffic.json), not measured in this run",
                          "latency_floor_ms": floor_ms, "latency_frac": floor_ms / t_dec},
             # the throughput-bound encoder MLP (all pixels at once) against the same peak
-            "roofline_encode": {"kernel": ("k_enc_mlp<2>" if args.model == "p350k" else "k_enc_pp") if prec == 1
+            "roofline_encode": {"kernel": ({"p350k": "k_enc_mlp<2>", "p12": "k_enc_mlp<3>"}.get(args.model, "k_enc_pp"))
+                                if prec == 1
                                 else "k_enc_mlp<fp32>",
                                 "bound": "tensor" if prec == 1 else "alu",
                                 "achieved": fpp * px_rank / (mlp_ms / 1e3) / 1e12, "peak": peak,

@@ -87,7 +87,8 @@ typedef struct {
 } dlic_opts;
 
 /* Container (version 2, little-endian):
- *   "DLIC", u8 version 2, u8 precision, u8 window id 1 (R1), u8 fill 0 (R2),
+ *   "DLIC", u8 version 2, u8 precision, u8 window id 1 (R1), u8 alphabet (0 =
+ *   8-bit pixels, 12 = 12-bit pixels: P:184-186, R15),
  *   u32 width, u32 height, u16 tile_w, u16 tile_h (0,0 = untiled; Q16),
  *   u16 G (rows per stream, R7), u16 numerics (arithmetic revision of the
  *   tables, see dlic_numerics_rev), 32-byte SHA-256 of the model file,
@@ -105,6 +106,7 @@ typedef struct {
   float meta[DLIC_MAX_META];
   uint8_t model_sha256[32];
   uint64_t payload_bytes, header_bytes;
+  uint32_t bits;     /* alphabet: 8, or 12 (byte 7 = 12; pixels are u16, R15) */
 } dlic_header;
 
 /* ---- models --------------------------------------------------------------
@@ -120,7 +122,16 @@ typedef struct {
  * pooling layers"; the next layer then has 128 / g inputs).  Pooling is linear
  * and is folded into the next layer's weights at load (W' = P^T W: exact in
  * bf16 and fp32 because 1/g is a power of two); the metadata inputs are
- * folded into a per-image layer-1 bias by a kernel at each call.  Other
+ * folded into a per-image layer-1 bias by a kernel at each call.
+ * Two larger networks run on a streamed-weight bf16 engine (weights exceed
+ * one SM's shared memory; layers 2-6 arrive from L2 in 32 KB TMA bulk chunks):
+ *   P350K = 78 -> 256 x5 -> 256 (Table I ~350K; §8(f) f1);
+ *   P12   = 78 -> 256 x5 -> 4096 ("4096 output layer neurons";
+ *           Table III ~1.35M): the 12-bit alphabet.  With a P12
+ *           model every image buffer of the calls below holds u16 pixels
+ *           (values < 4096; byte sizes and capacities double, row_stride
+ *           stays in pixels) and containers carry alphabet byte 12.
+ * Both are bf16 only, without metadata, volumes or unit ranges.  Other
  * topologies load (hash, dlic_peek) but encode/decode return
  * DLIC_E_UNSUPPORTED_MODEL.  Errors: DLIC_E_CORRUPT_MODEL, DLIC_E_CUDA. */
 dlic_status dlic_model_load(const void* bytes, size_t len, int cuda_device, dlic_model** out);

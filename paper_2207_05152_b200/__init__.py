@@ -48,7 +48,7 @@ class dlic_header(ctypes.Structure):
                 ("depth", ctypes.c_uint32),
                 ("n_meta", ctypes.c_uint32), ("meta", ctypes.c_float * MAX_META),
                 ("model_sha256", ctypes.c_uint8 * 32),
-                ("payload_bytes", ctypes.c_uint64), ("header_bytes", ctypes.c_uint64)]
+                ("payload_bytes", ctypes.c_uint64), ("header_bytes", ctypes.c_uint64), ("bits", ctypes.c_uint32)]
 
 
 def _sig(lib, name, res, *args):
@@ -212,9 +212,21 @@ def dlic_model_blob_check(blob: bytes) -> bytes:
 
 
 # ------------------------------------------------------------------ codec
+def _pixels(a) -> np.ndarray:
+    """u16 arrays stay u16 (12-bit alphabet: a P12 model's images), anything
+    else becomes u8."""
+    a = np.asarray(a)
+    return np.ascontiguousarray(a, dtype=np.uint16 if a.dtype == np.uint16 else np.uint8)
+
+
+def _pix_dtype(hd) -> type:
+    return np.uint16 if hd.get("bits", 8) == 12 else np.uint8
+
+
 def dlic_encode(model: Model, img: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0),
                 meta=None) -> bytes:
-    img = np.ascontiguousarray(img, dtype=np.uint8)
+    """img (H, W): u8, or u16 (values < 4096) for a 12-bit (P12) model."""
+    img = _pixels(img)
     assert img.ndim == 2
     h, w = img.shape
     out = c_u8p()
@@ -236,8 +248,8 @@ def dlic_peek(bits: bytes) -> dict:
 
 def dlic_decode(model: Model, bits: bytes) -> np.ndarray:
     hd = dlic_peek(bits)
-    img = np.empty((hd["height"], hd["width"]), np.uint8)
-    _check(_L().dlic_decode(model.handle, bits, len(bits), img.ctypes.data, img.size))
+    img = np.empty((hd["height"], hd["width"]), _pix_dtype(hd))
+    _check(_L().dlic_decode(model.handle, bits, len(bits), img.ctypes.data, img.nbytes))
     return img
 
 
@@ -245,7 +257,7 @@ def dlic_encode_batch(model: Model, imgs: np.ndarray, precision=PREC_BF16, group
                       volume_depth=0):
     """imgs (n, H, W) u8 host -> (blob, sizes): the containers back to back
     (n, or n / volume_depth volumes).  meta: raw metadata reals per container."""
-    imgs = np.ascontiguousarray(imgs, dtype=np.uint8)
+    imgs = _pixels(imgs)
     n, h, w = imgs.shape
     out = c_u8p()
     tot = ctypes.c_size_t()
@@ -263,9 +275,9 @@ def dlic_decode_batch(model: Model, blob: bytes, sizes) -> np.ndarray:
     offs = np.zeros(len(sizes), np.uint64)
     offs[1:] = np.cumsum(sizes[:-1])
     hd = dlic_peek(blob[:sizes[0]])
-    imgs = np.empty((len(sizes) * max(1, hd["depth"]), hd["height"], hd["width"]), np.uint8)
+    imgs = np.empty((len(sizes) * max(1, hd["depth"]), hd["height"], hd["width"]), _pix_dtype(hd))
     _check(_L().dlic_decode_batch(model.handle, blob, len(blob), offs.ctypes.data, len(sizes), imgs.ctypes.data,
-                                  imgs.size))
+                                  imgs.nbytes))
     return imgs
 
 
@@ -303,14 +315,16 @@ def dlic_rans_decode_tables(bits: bytes, freq_tables: np.ndarray) -> np.ndarray:
 
 def dlic_debug_mlp(model: Model, img: np.ndarray, precision=PREC_BF16, group_rows=32, tile=(0, 0),
                    logits=True, probs=True, freqs=True, fc=True, meta=None) -> dict:
-    """img (H, W), or (D, H, W) for a volume (3D window)."""
-    img = np.ascontiguousarray(img, dtype=np.uint8)
+    """img (H, W), or (D, H, W) for a volume (3D window); u16 for a 12-bit
+    (P12) model, whose tables have 4096 entries."""
+    img = _pixels(img)
     h, w = img.shape[-2:]
     lead = img.shape[:-2]
     out = {}
-    lg = np.empty(lead + (h, w, 256), np.float32) if logits else None
-    pb = np.empty(lead + (h, w, 256), np.float32) if probs else None
-    fq = np.empty(lead + (h, w, 256), np.uint16) if freqs else None
+    A = 4096 if img.dtype == np.uint16 else 256
+    lg = np.empty(lead + (h, w, A), np.float32) if logits else None
+    pb = np.empty(lead + (h, w, A), np.float32) if probs else None
+    fq = np.empty(lead + (h, w, A), np.uint16) if freqs else None
     f = np.empty(lead + (h, w), np.uint32) if fc else None
     o = _opts(precision, group_rows, tile, meta, img.shape[0] if img.ndim == 3 else 0)
     _check(_L().dlic_debug_mlp(model.handle, img.ctypes.data, w, h, ctypes.byref(o),
@@ -331,7 +345,7 @@ def _stream_handle(stream):
 
 def dlic_encode_batch_device(model: Model, d_imgs, precision=PREC_BF16, group_rows=32, tile=(0, 0),
                              d_out=None, d_sizes=None, stream=None, meta=None, volume_depth=0):
-    """d_imgs: torch uint8 CUDA tensor (n, H, W).  Returns (d_out, d_sizes, stride):
+    """d_imgs: torch uint8 (uint16 for a P12 model) CUDA tensor (n, H, W).  Returns (d_out, d_sizes, stride):
     container i occupies d_out[i*stride : i*stride + d_sizes[i]]."""
     import torch
     n, h, w = d_imgs.shape
@@ -367,7 +381,7 @@ def dlic_decode_batch_device(model: Model, d_bits, h_offsets, h_lengths, header:
             for i, v in enumerate(header.get("meta", [])):
                 hd.meta[i] = float(v)
         else:
-            setattr(hd, k, header[k])
+            setattr(hd, k, header.get(k, 8) if k == "bits" else header[k])
     _check(_L().dlic_decode_batch_device(model.handle, _vp(d_bits.data_ptr()), offs.ctypes.data, lens.ctypes.data,
                                          len(offs), ctypes.byref(hd), _vp(d_imgs.data_ptr()),
                                          _vp(d_status.data_ptr()) if d_status is not None else None,

@@ -33,6 +33,7 @@ struct dlic_model {
   std::vector<uint32_t> dims;
   bool p100k = false;  // topology the GPU engines run (see dlic_model_load)
   bool p350k = false;  // 78 -> 256 x5 -> 256 (§8(f) f1): bf16 only, streamed weights (engine 2)
+  bool p12 = false;    // 78 -> 256 x5 -> 4096 (§8(f) f3, 12-bit pixels): bf16 only (engine 3)
   uint32_t n_meta = 0;
   bool in3d = false;   // 87 window inputs: the 3D window (R13)
   uint8_t* d_wimg = nullptr;
@@ -266,12 +267,13 @@ static bool engine_weights(const ParsedModel& pm, std::vector<std::vector<float>
   return true;
 }
 
-// P350K (reading R4): 78 window inputs -> 256 x5 -> 256 logits, no pooling,
+// P350K (reading R4): 78 window inputs -> 256 x5 -> 256 logits; P12
+// (R16): the same hidden stack -> 4096 logits (12-bit pixels).  No pooling,
 // no metadata.
-static bool is_p350k(const ParsedModel& pm) {
+static bool is_stream_model(const ParsedModel& pm, uint32_t nout) {
   if (pm.W.size() != (size_t)NLAYER || !pm.meta_range.empty() || pm.dims[0] != (uint32_t)KIN) return false;
   for (int l = 0; l < NLAYER; ++l)
-    if (pm.dims[l + 1] != (uint32_t)SH || pm.pool[l] != 0) return false;
+    if (pm.dims[l + 1] != (l == NLAYER - 1 ? nout : (uint32_t)SH) || pm.pool[l] != 0) return false;
   return true;
 }
 
@@ -279,6 +281,54 @@ static bool is_p350k(const ParsedModel& pm) {
 // first (K in the engine's kpos_tap order, the fresh taps zero), each in the
 // UMMA no-swizzle K-major core-matrix layout of an N=256 operand; biases
 // [5][256] + [256] and the fresh-tap table (bf16-rounded, float4 per pair).
+// P12: layers 1-5 as P350K's, then the head: for each 128-column chunk q,
+// K = 256 in 16 slices of N = 128 (4 KB, the same core-matrix layout with
+// N = 128), two 32 KB stream chunks (K-slices 0-7, 8-15) after layer 5's.
+// Biases: [5][256], the fresh table at SB_FRESH, the 4096 head biases at
+// SB12_HEAD.
+static dlic_status upload_p12(dlic_model* m, const ParsedModel& pm) {
+  std::vector<uint8_t> img(SWIMG12_BYTES, 0);
+  for (int l = 0; l < NLAYER - 1; ++l) {
+    const int K = l == 0 ? KPAD : SH;
+    for (int k = 0; k < K; ++k)
+      for (int n = 0; n < SH; ++n) {
+        const int kt = l == 0 ? kpos_tap(k) : k;
+        const bool fresh = l == 0 && (kt == TAP_FA || kt == TAP_FB);
+        const float v = kt >= 0 && kt < (l == 0 ? KIN : SH) && !fresh ? pm.W[l][(size_t)kt * SH + n] : 0.0f;
+        const uint16_t u = bf16_bits(v);
+        const int kk = k / 16, kl = k % 16;
+        const size_t a = (size_t)s_slice(l, kk) * SL_BYTES + (size_t)(kl / 8) * (SH / 8) * 128 +
+                         (size_t)(n / 8) * 128 + (n % 8) * 16 + (kl % 8) * 2;
+        memcpy(&img[a], &u, 2);
+      }
+  }
+  const size_t head0 = SL1_BYTES + (size_t)CH_HID12 * CH_BYTES;
+  for (int k = 0; k < SH; ++k)
+    for (int n = 0; n < H12_N; ++n) {
+      const int q = n / H12_CN, nl = n % H12_CN, kk = k / 16, kl = k % 16;
+      const uint16_t u = bf16_bits(pm.W[NLAYER - 1][(size_t)k * H12_N + n]);
+      const size_t a = head0 + (size_t)(2 * q + kk / H12_CH_SL) * CH_BYTES + (size_t)(kk % H12_CH_SL) * H12_SL_BYTES +
+                       (size_t)(kl / 8) * (H12_CN / 8) * 128 + (size_t)(nl / 8) * 128 + (nl % 8) * 16 + (kl % 8) * 2;
+      memcpy(&img[a], &u, 2);
+    }
+  std::vector<float> bias(SBIAS12_BYTES / 4, 0.0f);
+  for (int l = 0; l < NLAYER - 1; ++l)
+    for (int n = 0; n < SH; ++n) bias[(size_t)l * SH + n] = pm.b[l][n];
+  for (int n = 0; n < H12_N; ++n) bias[SB12_HEAD + n] = pm.b[NLAYER - 1][n];
+  for (int n = 0; n < SH; ++n) {
+    const size_t q = SB_FRESH + 4 * (size_t)(n / 2) + (n & 1);
+    const uint32_t ua = (uint32_t)bf16_bits(pm.W[0][(size_t)TAP_FA * SH + n]) << 16;
+    const uint32_t ub = (uint32_t)bf16_bits(pm.W[0][(size_t)TAP_FB * SH + n]) << 16;
+    memcpy(&bias[q], &ua, 4);
+    memcpy(&bias[q + 2], &ub, 4);
+  }
+  CUDA_TRY(cudaMalloc(&m->d_wimg, SWIMG12_BYTES));
+  CUDA_TRY(cudaMalloc(&m->d_bias, bias.size() * 4));
+  CUDA_TRY(cudaMemcpy(m->d_wimg, img.data(), SWIMG12_BYTES, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(m->d_bias, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice));
+  return DLIC_OK;
+}
+
 static dlic_status upload_p350k(dlic_model* m, const ParsedModel& pm) {
   std::vector<uint8_t> img(SWIMG_BYTES, 0);
   for (int l = 0; l < NLAYER; ++l) {
@@ -321,9 +371,13 @@ dlic_status upload_model(dlic_model* m, const ParsedModel& pm_in) {
   std::vector<std::vector<float>> Wf;
   uint32_t n_meta = 0;
   bool in3d = false;
-  if (is_p350k(pm_in)) {
+  if (is_stream_model(pm_in, (uint32_t)NOUT)) {
     m->p350k = true;
     return upload_p350k(m, pm_in);
+  }
+  if (is_stream_model(pm_in, (uint32_t)H12_N)) {
+    m->p12 = true;
+    return upload_p12(m, pm_in);
   }
   m->p100k = engine_weights(pm_in, Wf, n_meta, in3d);
   if (!m->p100k) return DLIC_OK;  // loadable; GPU engines refuse it at encode/decode
@@ -418,12 +472,14 @@ dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Pl
   p.G = d.group_rows;
   p.precision = d.precision;
   p.engine = d.precision;
-  if (m && m->p350k) {  // §8(f) f1: the streamed bf16 engine only
+  p.bits = 8;
+  if (m && (m->p350k || m->p12)) {  // §8(f) f1 / f3: the streamed bf16 engines only
     if (d.precision != DLIC_PREC_BF16)
-      return fail(DLIC_E_UNSUPPORTED_MODEL, "the 78->256x5->256 (P350K) model runs in bf16 only");
+      return fail(DLIC_E_UNSUPPORTED_MODEL, "the 78->256x5->256/4096 models run in bf16 only");
     if (d.volume_depth > 0 || d.n_meta > 0)
-      return fail(DLIC_E_UNSUPPORTED_MODEL, "the P350K engine has no volume or metadata inputs");
-    p.engine = 2;
+      return fail(DLIC_E_UNSUPPORTED_MODEL, "the streamed-weight engines have no volume or metadata inputs");
+    p.engine = m->p12 ? 3 : 2;
+    p.bits = m->p12 ? 12 : 8;
   }
   p.tw = tiled ? std::min(d.tile_w, W) : W;
   p.th = tiled ? std::min(d.tile_h, H) : H;
@@ -472,7 +528,7 @@ dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Pl
 
 dlic_status check_model_gpu(const dlic_model* m) {
   if (!m) return fail(DLIC_E_INVALID_ARG, "null model");
-  if (!m->p100k && !m->p350k)
+  if (!m->p100k && !m->p350k && !m->p12)
     return fail(DLIC_E_UNSUPPORTED_MODEL, "GPU engines implement (78 + n_meta <= 8)->128x5->256 with optional "
                                           "power-of-two average pooling after hidden layers, and 78->256x5->256");
   return check_device(m->device);
@@ -529,8 +585,9 @@ dlic_status peek(const uint8_t* b, size_t len, dlic_header* h, std::vector<uint3
   if (memcmp(b, "DLIC", 4) != 0) return fail(DLIC_E_CORRUPT_CONTAINER, "container magic");
   if (b[4] != CONTAINER_VERSION || (b[6] != 1 && b[6] != 2))
     return fail(DLIC_E_VERSION_MISMATCH, "container version/window");
-  if (b[7] != 0 || b[5] > 1) return fail(DLIC_E_CORRUPT_CONTAINER, "container fill/precision");
+  if ((b[7] != 0 && b[7] != 12) || b[5] > 1) return fail(DLIC_E_CORRUPT_CONTAINER, "container alphabet/precision");
   dlic_header o = {};
+  o.bits = b[7] == 12 ? 12 : 8;
   o.width = rd32(b + 8);
   o.height = rd32(b + 12);
   o.tile_w = rd16(b + 16);
@@ -806,13 +863,15 @@ dlic_status dlic_encode(const dlic_model* m, const uint8_t* img, uint32_t width,
   Scratch sc(st);
   uint8_t *d_img, *d_out;
   uint64_t* d_size;
-  CUDA_TRY(sc.alloc(&d_img, (size_t)width * height));
+  const size_t pxb = p.bits == 12 ? 2 : 1;  // bytes per pixel (12-bit: u16)
+  CUDA_TRY(sc.alloc(&d_img, (size_t)width * height * pxb));
   CUDA_TRY(sc.alloc(&d_out, p.max_container));
   CUDA_TRY(sc.alloc(&d_size, 8));
   if (row_stride == width) {
-    CUDA_TRY(h2d(d_img, img, (size_t)width * height, st));
+    CUDA_TRY(h2d(d_img, img, (size_t)width * height * pxb, st));
   } else {
-    CUDA_TRY(cudaMemcpy2DAsync(d_img, width, img, row_stride, width, height, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpy2DAsync(d_img, width * pxb, img, row_stride * pxb, width * pxb, height, cudaMemcpyHostToDevice,
+                               st));
   }
   s = run_encode(m, p, d_img, d_out, p.max_container, d_size, st, sc, opts ? opts->meta : nullptr);
   if (s != DLIC_OK) return s;
@@ -846,7 +905,11 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
                                              std::to_string(NUMERICS_REV) + ")");
   const uint32_t nsl = h.depth ? h.depth : 1u;  // slices (a volume container holds depth of them)
   const size_t npx = (size_t)h.width * h.height * nsl;
-  if (!img || cap < npx) return fail(DLIC_E_BUFFER_TOO_SMALL, "image buffer");
+  const size_t pxb = h.bits == 12 ? 2 : 1;  // bytes per pixel (12-bit: u16)
+  if (m && h.bits != (m->p12 ? 12u : 8u))
+    return fail(DLIC_E_SHAPE_MISMATCH, "container alphabet does not match the model's output layer");
+  if (tables && h.bits != 8) return fail(DLIC_E_INVALID_ARG, "table-fed decode is for 8-bit containers");
+  if (!img || cap < npx * pxb) return fail(DLIC_E_BUFFER_TOO_SMALL, "image buffer");
   if (m) {
     s = check_model_gpu(m);
   } else {
@@ -861,7 +924,7 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
   if (s != DLIC_OK) return s;
   if (p.spc != h.n_streams) return fail(DLIC_E_CORRUPT_CONTAINER, "stream count does not match the header dims");
   const bool part = unit_hi > 0;  // dlic_decode_units: only units [unit_lo, unit_hi)
-  if (part && p.depth > 1) return fail(DLIC_E_INVALID_ARG, "unit ranges are for 2D images");
+  if (part && (p.depth > 1 || p.bits != 8)) return fail(DLIC_E_INVALID_ARG, "unit ranges are for 2D 8-bit images");
   if (part) {
     s = restrict_units(p, unit_lo, unit_hi);
     if (s != DLIC_OK) return s;
@@ -877,7 +940,7 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
   int32_t* d_status;
   uint64_t* d_meta;  // [0] = container offset (0), [1] = length
   CUDA_TRY(sc.alloc(&d_bits, len));
-  CUDA_TRY(sc.alloc(&d_img, npx));
+  CUDA_TRY(sc.alloc(&d_img, npx * pxb));
   CUDA_TRY(sc.alloc(&d_sbase, 4ull * p.spc));
   CUDA_TRY(sc.alloc(&d_slen, 4ull * p.spc));
   CUDA_TRY(sc.alloc(&d_status, 4));
@@ -892,7 +955,7 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
   CUDA_TRY(cudaMemcpyAsync(d_bits, pin + 16, len, cudaMemcpyHostToDevice, st));
   CUDA_TRY(launch_dec_prep(p, d_bits, d_meta, d_meta + 1, d_sbase, d_slen, d_status, st, tables == nullptr));
   if (part)  // pixels outside the unit range come back untouched (pageable copy: no staging reuse)
-    CUDA_TRY(cudaMemcpyAsync(d_img, img, npx, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(d_img, img, npx * pxb, cudaMemcpyHostToDevice, st));
   if (tables) {
     uint16_t* d_tab;
     const size_t tb = npx * NOUT * 2;
@@ -937,15 +1000,15 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
                 hp[24] / ctas / T, hp[24] ? (double)hp[25] / hp[24] : 0.0);
     }
   }
-  uint8_t* ho = static_cast<uint8_t*>(g_pin_out.get(npx + 64));
+  uint8_t* ho = static_cast<uint8_t*>(g_pin_out.get(npx * pxb + 64));
   if (!ho) return fail(DLIC_E_OUT_OF_MEMORY, "pinned staging");
   CUDA_TRY(cudaMemcpyAsync(ho, d_status, 4, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(ho + 64, d_img, npx, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(ho + 64, d_img, npx * pxb, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   int32_t stat;
   memcpy(&stat, ho, 4);
   if (stat != 0) return fail((dlic_status)stat, "lane invariant / framing check failed on the device");
-  memcpy(img, ho + 64, npx);
+  memcpy(img, ho + 64, npx * pxb);
   return DLIC_OK;
 }
 
@@ -1035,23 +1098,25 @@ dlic_status dlic_debug_mlp(const dlic_model* m, const uint8_t* img, uint32_t wid
   cudaStream_t st = my_stream();
   Scratch sc(st);
   const size_t npx = (size_t)width * height * nsl;
+  const size_t pxb = p.bits == 12 ? 2 : 1;                 // bytes per pixel
+  const size_t nout = p.bits == 12 ? (size_t)H12_N : NOUT;  // table entries per pixel
   uint8_t* d_img;
   uint32_t* d_fc;
   float *d_lg = nullptr, *d_pb = nullptr;
   uint16_t* d_fq = nullptr;
-  CUDA_TRY(sc.alloc(&d_img, npx));
+  CUDA_TRY(sc.alloc(&d_img, npx * pxb));
   CUDA_TRY(sc.alloc(&d_fc, 4 * npx));
-  if (logits) CUDA_TRY(sc.alloc(&d_lg, 4 * npx * NOUT));
-  if (probs) CUDA_TRY(sc.alloc(&d_pb, 4 * npx * NOUT));
-  if (freqs) CUDA_TRY(sc.alloc(&d_fq, 2 * npx * NOUT));
-  CUDA_TRY(cudaMemcpyAsync(d_img, img, npx, cudaMemcpyHostToDevice, st));
+  if (logits) CUDA_TRY(sc.alloc(&d_lg, 4 * npx * nout));
+  if (probs) CUDA_TRY(sc.alloc(&d_pb, 4 * npx * nout));
+  if (freqs) CUDA_TRY(sc.alloc(&d_fq, 2 * npx * nout));
+  CUDA_TRY(cudaMemcpyAsync(d_img, img, npx * pxb, cudaMemcpyHostToDevice, st));
   const float* b1img = nullptr;
   s = meta_bias(m, p, opts ? opts->meta : nullptr, nullptr, nullptr, st, sc, &b1img);
   if (s != DLIC_OK) return s;
   CUDA_TRY(launch_enc_mlp(p, m->dw(b1img), d_img, d_fc, d_lg, d_pb, d_fq, st, num_sms(m->device)));
-  if (logits) CUDA_TRY(cudaMemcpyAsync(logits, d_lg, 4 * npx * NOUT, cudaMemcpyDeviceToHost, st));
-  if (probs) CUDA_TRY(cudaMemcpyAsync(probs, d_pb, 4 * npx * NOUT, cudaMemcpyDeviceToHost, st));
-  if (freqs) CUDA_TRY(cudaMemcpyAsync(freqs, d_fq, 2 * npx * NOUT, cudaMemcpyDeviceToHost, st));
+  if (logits) CUDA_TRY(cudaMemcpyAsync(logits, d_lg, 4 * npx * nout, cudaMemcpyDeviceToHost, st));
+  if (probs) CUDA_TRY(cudaMemcpyAsync(probs, d_pb, 4 * npx * nout, cudaMemcpyDeviceToHost, st));
+  if (freqs) CUDA_TRY(cudaMemcpyAsync(freqs, d_fq, 2 * npx * nout, cudaMemcpyDeviceToHost, st));
   std::vector<uint32_t> fcu;
   if (fc) {
     fcu.resize(npx);
@@ -1082,7 +1147,7 @@ dlic_status dlic_encode_batch(const dlic_model* m, const uint8_t* imgs, uint32_t
   if (s != DLIC_OK) return s;
   cudaStream_t st = my_stream();
   Scratch sc(st);
-  const size_t npx = (size_t)n * width * height;
+  const size_t npx = (size_t)n * width * height * (p.bits == 12 ? 2 : 1);  // image bytes
   uint8_t *d_imgs, *d_out;
   uint64_t* d_sizes;
   CUDA_TRY(sc.alloc(&d_imgs, npx));
@@ -1147,7 +1212,9 @@ dlic_status dlic_decode_batch(const dlic_model* m, const uint8_t* bits, size_t l
       return fail(DLIC_E_SHAPE_MISMATCH, "batch containers differ in dims or options");
     }
   }
-  const size_t npx = (size_t)n * h0.width * h0.height * (h0.depth ? h0.depth : 1u);
+  if (h0.bits != (m->p12 ? 12u : 8u))
+    return fail(DLIC_E_SHAPE_MISMATCH, "container alphabet does not match the model's output layer");
+  const size_t npx = (size_t)n * h0.width * h0.height * (h0.depth ? h0.depth : 1u) * (h0.bits == 12 ? 2 : 1);  // bytes
   if (img_capacity < npx) return fail(DLIC_E_BUFFER_TOO_SMALL, "image buffer");
   dlic_opts o = opts_of(h0);
   Plan p;
@@ -1231,6 +1298,8 @@ dlic_status dlic_decode_batch_device(const dlic_model* m, const uint8_t* d_bits,
     return fail(DLIC_E_MODEL_HASH_MISMATCH, "container was coded with another model");
   if (h_header->numerics != NUMERICS_REV)
     return fail(DLIC_E_VERSION_MISMATCH, "container tables come from another arithmetic revision");
+  if (h_header->bits != (m->p12 ? 12u : 8u))
+    return fail(DLIC_E_SHAPE_MISMATCH, "container alphabet does not match the model's output layer");
   dlic_opts o = opts_of(*h_header);
   Plan p;
   s = make_plan(h_header->width, h_header->height, n * (h_header->depth ? h_header->depth : 1u), &o, p, m);
@@ -1303,6 +1372,7 @@ dlic_status dlic_encode_units(const dlic_model* m, const uint8_t* img, uint32_t 
   if (row_stride == 0) row_stride = width;
   if (row_stride < width) return fail(DLIC_E_SHAPE_MISMATCH, "row_stride < width");
   dlic_status s = check_model_gpu(m);
+  if (s == DLIC_OK && m->p12) return fail(DLIC_E_INVALID_ARG, "unit ranges are for 8-bit images");
   if (s != DLIC_OK) return s;
   Plan p;
   s = make_plan(width, height, 1, opts, p, m);

@@ -349,6 +349,9 @@ __device__ __forceinline__ uint32_t map_cluster(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void st_cluster_u8(uint32_t caddr, uint32_t v) {
   asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(caddr), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_cluster_u16(uint32_t caddr, uint32_t v) {
+  asm volatile("st.shared::cluster.u16 [%0], %1;" ::"r"(caddr), "h"((unsigned short)v) : "memory");
+}
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);  // .x = lo (bits 0-15), .y = hi

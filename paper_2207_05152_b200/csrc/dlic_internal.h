@@ -33,6 +33,7 @@ struct Plan {
   // tcgen05 with resident weights (P100K), 2 bf16 tcgen05 with weights
   // streamed from L2 (P350K, dlic_stream.cuh).  The header keeps `precision`.
   uint32_t engine;
+  uint32_t bits;  // alphabet: 8 (u8 pixels) or 12 (u16 pixels, engine 3; container byte 7 = 12)
   uint32_t prof;  // diagnostics only (DLIC_PROF_STREAM): issuer cycle counters
 };
 

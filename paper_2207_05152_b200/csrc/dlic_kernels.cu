@@ -17,6 +17,7 @@
 //               (DSMEM mirror) -> cluster barrier; the rANS step runs one
 //               front late inside the next front's network.
 #include <cstdint>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -53,6 +54,7 @@ __host__ __device__ inline uint32_t bias_bytes(uint32_t w3d) { return BIAS_BYTES
 // `precision` here is the ENGINE: 0 fp32 FFMA, 1 bf16 P100K (resident
 // weights), 2 bf16 P350K (streamed weights, dlic_stream.cuh)
 size_t enc_smem_bytes(uint32_t precision, uint32_t w3d) {
+  if (precision == 3) return SENG12_BYTES;
   if (precision == 2) return SENG_BYTES;
   return precision == 1 ? WIMG_BYTES + bias_bytes(w3d) : F32_BUF_BYTES + F32_X_BYTES;
 }
@@ -61,7 +63,7 @@ static uint32_t cursor_bytes(uint32_t ngroups) { return (ngroups * 4u + 15u) & ~
 // next step, [2][ROWS][3] words (filled by the rANS warp)
 constexpr uint32_t T3_BYTES = 2u * ROWS * 3u * 4u;
 size_t dec_smem_bytes(uint32_t precision, uint32_t max_groups, uint32_t w3d) {
-  return enc_smem_bytes(precision, w3d) + RING_BYTES + 16 + 3 * cursor_bytes(max_groups) +
+  return enc_smem_bytes(precision, w3d) + RING_BYTES * (precision == 3 ? 2u : 1u) + 16 + 3 * cursor_bytes(max_groups) +
          (w3d && precision == 1 ? T3_BYTES : 0u);  // (engine index, see enc_smem_bytes)
 }
 size_t dec_smem_limit() { return MAX_DYN_SMEM; }
@@ -81,6 +83,28 @@ template <>
 struct EngineSel<2> {
   using T = TcStream;
 };
+template <>
+struct EngineSel<3> {
+  using T = TcStream12;
+};
+// decoded pixel storage: 12-bit alphabet (engine 3) in u16, else u8
+template <int PREC>
+using PixT = std::conditional_t<PREC == 3, uint16_t, uint8_t>;
+template <int PREC>
+__host__ __device__ constexpr int pix_bits() { return PREC == 3 ? 12 : 8; }
+// v / 2^BITS exactly (v < 2^BITS): 1 + v/2^BITS has v in the top mantissa bits
+template <int BITS>
+__device__ __forceinline__ float unit_of(uint32_t v) {
+  return __fadd_rn(__uint_as_float(0x3F800000u | (v << (23 - BITS))), -1.0f);
+}
+// a fresh tap as layer-1's epilogue takes it: v / 2^bits as a bf16 operand
+// (exact for 8-bit pixels; 12-bit pixels are rounded like the MMA's taps)
+template <int PREC>
+__device__ __forceinline__ float fresh_in(uint32_t v) {
+  const float x = unit_of<pix_bits<PREC>()>(v);
+  if constexpr (PREC == 3) return __bfloat162float(__float2bfloat16_rn(x));
+  return x;
+}
 
 __device__ __forceinline__ void load_smem(uint8_t* dst, const void* src, uint32_t bytes) {
   const int4* s4 = reinterpret_cast<const int4*>(src);
@@ -93,33 +117,42 @@ __device__ __forceinline__ void load_smem(uint8_t* dst, const void* src, uint32_
 template <int PREC>
 __device__ __forceinline__ uint8_t* engine_setup(typename EngineSel<PREC>::T& eng, uint8_t* smem, const DevWeights& w,
                                                  uint64_t* bar, uint32_t* tslot, uint32_t w3d) {  // bar: 2 mbarriers
-  if constexpr (PREC == 2) {  // P350K: layer 1 | ring | biases | full[S] empty[S]; layers 2-6 streamed
-    load_smem(smem + SENG_L1, w.wimg, SL1_BYTES);
-    load_smem(smem + SENG_BIAS, w.bias, SBIAS_BYTES);
-    const uint32_t bars = smem_u32(smem + SENG_BARS);
+  if constexpr (PREC >= 2) {  // P350K / P12: layer 1 | ring | biases | full[S] empty[S] (| dfull[2] dfree[2])
+    using Cfg = StreamCfg<PREC == 3>;
+    load_smem(smem + Cfg::L1, w.wimg, SL1_BYTES);
+    load_smem(smem + Cfg::BIASO, w.bias, Cfg::BIAS);
+    const uint32_t bars = smem_u32(smem + Cfg::BARS);
     if (threadIdx.x < 32) tmem_alloc(smem_u32(tslot), TM_COLS);
     if (threadIdx.x == 0) {
       mbar_init(smem_u32(bar), 1);
       mbar_init(smem_u32(bar + 1), NTHREADS / 32);  // layer-1 input ready (row warps)
-      for (int i = 0; i < 2 * S_STAGES; ++i) mbar_init(bars + 8u * (uint32_t)i, 1);
+      for (int i = 0; i < 2 * Cfg::S; ++i) mbar_init(bars + 8u * (uint32_t)i, 1);
+      if constexpr (PREC == 3) {
+        for (int i = 0; i < 2; ++i) {
+          mbar_init(bars + 8u * (2 * Cfg::S + i), 1);                 // dfull[b]: tcgen05.commit
+          mbar_init(bars + 8u * (2 * Cfg::S + 2 + i), NTHREADS / 32);  // dfree[b]: the row warps
+        }
+      }
       fence_mbar_init();
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     eng.tmem = *tslot;
-    eng.bias = reinterpret_cast<const float*>(smem + SENG_BIAS);
+    eng.bias = reinterpret_cast<const float*>(smem + Cfg::BIASO);
     eng.b0 = eng.bias;
     eng.bar = smem_u32(bar);
     eng.bar2 = eng.bar;
     eng.phase = 0;
-    eng.ring = smem_u32(smem + SENG_RING);
-    eng.l1s = smem_u32(smem + SENG_L1);
+    eng.ring = smem_u32(smem + Cfg::RINGO);
+    eng.l1s = smem_u32(smem + Cfg::L1);
     eng.full0 = bars;
-    eng.empty0 = bars + 8u * S_STAGES;
+    eng.empty0 = bars + 8u * Cfg::S;
+    eng.dfull0 = bars + 8u * (2 * Cfg::S);
+    eng.dfree0 = bars + 8u * (2 * Cfg::S + 2);
     eng.wstream = w.wimg;
     eng.aready = smem_u32(bar + 1);
-    return smem + SENG_BYTES;
+    return smem + Cfg::BYTES;
   } else if constexpr (PREC == 1) {
     load_smem(smem, w.wimg, WIMG_BYTES);
     load_smem(smem + WIMG_BYTES, w.bias, bias_bytes(w3d));
@@ -174,8 +207,9 @@ __device__ __forceinline__ void tap_of(int u, int i, int& dr, int& dc) {
 template <int PREC, class Eng, class Get>
 __device__ __forceinline__ void feed(const Eng& eng, Get get, const uint32_t (*t3)[3] = nullptr) {
   const int u = 2 * col_grp() + half_id();
+  constexpr int SHIFT = 23 - pix_bits<PREC>();
   if constexpr (PREC >= 1) {
-    // v/256 exactly: (1 + v/256) has v in the top 8 mantissa bits; minus 1 is exact.
+    // v/2^bits exactly: (1 + v/2^bits) has v in the top mantissa bits; minus 1 is exact.
     const f2 m1 = f2_make(-1.0f, -1.0f);
     uint32_t a[5];
 #pragma unroll
@@ -186,7 +220,7 @@ __device__ __forceinline__ void feed(const Eng& eng, Get get, const uint32_t (*t
       const uint32_t v0 = get(dr0, dc0);
       const uint32_t v1 = (q < 4 || u < 6) ? get(dr1, dc1) : 0u;
       float x0, x1;
-      f2_split(f2_add(f2_bits(0x3F800000u | (v0 << 15), 0x3F800000u | (v1 << 15)), m1), x0, x1);
+      f2_split(f2_add(f2_bits(0x3F800000u | (v0 << SHIFT), 0x3F800000u | (v1 << SHIFT)), m1), x0, x1);
       a[q] = pack_bf16(x0, x1);
     }
     eng.put_input(a);
@@ -217,7 +251,7 @@ __device__ __forceinline__ float u8_unit(uint32_t v) {
 // hidden columns [32j+16h, +16) and logits [64j+32h, +32) (dlic_device.cuh).
 // PREC 2 (P350K, TcStream): one more warp streams the weights and issues the
 // MMAs (TcStream::issue_tiles); the row warps run the same code as PREC 0.
-__host__ __device__ constexpr int enc_block(int prec) { return prec == 2 ? NTHREADS + 32 : NTHREADS; }
+__host__ __device__ constexpr int enc_block(int prec) { return prec >= 2 ? NTHREADS + 32 : NTHREADS; }
 template <int PREC>
 __global__ void __launch_bounds__(enc_block(PREC), 1)
     k_enc_mlp(Plan p, DevWeights w, const uint8_t* __restrict__ imgs, uint32_t* __restrict__ fc,
@@ -226,13 +260,16 @@ __global__ void __launch_bounds__(enc_block(PREC), 1)
   __shared__ uint64_t bar[3];  // 0 MMA completion, 2 spare (engine)
   __shared__ uint32_t tslot;
   const int row = tile_row();
+  using Pix = PixT<PREC>;
+  constexpr int BITS = pix_bits<PREC>();
+  const Pix* const imgp = reinterpret_cast<const Pix*>(imgs);
   typename EngineSel<PREC>::T eng;
   engine_setup<PREC>(eng, smem, w, bar, &tslot, p.w3d);
   // tiles of units [u_lo, u_lo + u_cnt) (global tile index = tbase + k)
   const uint64_t tbase = (uint64_t)p.u_lo * p.tiles_per_unit;
   const uint64_t total = (uint64_t)p.u_cnt * p.tiles_per_unit;
   const bool dbg = dbg_logits || dbg_probs || dbg_freqs;
-  if constexpr (PREC == 2) {
+  if constexpr (PREC >= 2) {
     if (threadIdx.x >= NTHREADS) {  // weight stream + MMA issuer: one network per tile of this CTA
       // (the row warps take the one-tile-at-a-time loop: with 17 warps a
       // thread has 96 registers, too few to hold a tile's logits across the
@@ -243,7 +280,7 @@ __global__ void __launch_bounds__(enc_block(PREC), 1)
       auto next = [&](int& c) -> bool {  // the 20 chunks of every tile's network, in order
         if (pt >= n) return false;
         c = pk;
-        if (++pk == CH_NET) {
+        if (++pk == (PREC == 3 ? CH_NET12 : CH_NET)) {
           pk = 0;
           ++pt;
         }
@@ -263,7 +300,7 @@ __global__ void __launch_bounds__(enc_block(PREC), 1)
   struct Px {
     bool valid;
     int r, c, uw, uh, z, sym;
-    const uint8_t* img;
+    const Pix* img;
     uint64_t gi, fci;
   };
   uint32_t cu = 0xFFFFFFFFu;  // cached unit
@@ -285,7 +322,7 @@ __global__ void __launch_bounds__(enc_block(PREC), 1)
     x.uw = (int)cun.w;
     x.uh = (int)cun.h;
     x.z = (int)(cun.img % p.depth);
-    x.img = imgs + (uint64_t)cun.img * p.W * p.H + (uint64_t)cun.y0 * p.W + cun.x0;
+    x.img = imgp + (uint64_t)cun.img * p.W * p.H + (uint64_t)cun.y0 * p.W + cun.x0;
     x.sym = 0;  // loaded by load_sym() when needed (its L2 latency off the tile start)
     x.gi = (uint64_t)cun.img * p.W * p.H + (uint64_t)(cun.y0 + x.r) * p.W + (cun.x0 + x.c);
     x.fci = cun.fc_off + q;
@@ -300,7 +337,7 @@ __global__ void __launch_bounds__(enc_block(PREC), 1)
     if (!x.valid) return;
     const int u = 2 * col_grp() + half_id();
     const int rr = max(x.r + u - 8, 0);
-    const uint8_t* a = x.img + (int64_t)rr * p.W + max(x.c - 6, 0);
+    const Pix* a = x.img + (int64_t)rr * p.W + max(x.c - 6, 0);
     asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
     asm volatile("prefetch.global.L1 [%0];" ::"l"(x.img + (int64_t)x.r * p.W + x.c));
   };
@@ -332,7 +369,7 @@ __global__ void __launch_bounds__(enc_block(PREC), 1)
     }
   };
 
-  if (dbg || PREC == 2) {  // debug exports (and P350K): one tile at a time
+  if (dbg || PREC >= 2) {  // debug exports (and P350K, P12): one tile at a time
 #pragma unroll 1
     for (uint64_t tile = tbase + blockIdx.x; tile < tbase + total; tile += gridDim.x) {
       const long long c0 = clock64();
@@ -342,8 +379,23 @@ __global__ void __launch_bounds__(enc_block(PREC), 1)
       feed_x(x, get);
       eng.start_l0();
       const long long c1 = clock64();
-      eng.run_rest(u8_unit(get(0, -1)), u8_unit(get(-1, 2)), [](int) {});
+      eng.run_rest(fresh_in<PREC>(get(0, -1)), fresh_in<PREC>(get(-1, 2)), [](int) {});
       const long long c2 = clock64();
+      if constexpr (PREC == 3) {  // 12-bit head (R17): (f_s | c_s << 16) from the owning thread
+        Q12Dbg dd{x.valid && dbg_logits ? dbg_logits + x.gi * H12_N : nullptr,
+                   x.valid && dbg_probs ? dbg_probs + x.gi * H12_N : nullptr,
+                   x.valid && dbg_freqs ? dbg_freqs + x.gi * H12_N : nullptr};
+        bool mine;
+        uint32_t fs, cs;
+        q12_row<true>(eng, (uint32_t)x.sym, mine, fs, cs, []() {}, dbg ? &dd : nullptr);
+        if (x.valid && mine) fc[x.fci] = fs | (cs << 16);
+        if (p.prof && threadIdx.x == 0) {
+          atomicAdd(&g_sprof[5], (unsigned long long)(c1 - c0));
+          atomicAdd(&g_sprof[6], (unsigned long long)(c2 - c1));
+          atomicAdd(&g_sprof[7], (unsigned long long)(clock64() - c2));
+        }
+        continue;
+      }
       const uint32_t v = q1_encode(eng, x.sym, (x.valid && dbg_probs) ? dbg_probs + x.gi * NOUT : nullptr,
                                    (x.valid && dbg_freqs) ? dbg_freqs + x.gi * NOUT : nullptr, dbg_freqs != nullptr);
       if constexpr (PREC == 2) {
@@ -900,7 +952,7 @@ __global__ void k_container(Plan p, Sha sha, const uint32_t* __restrict__ words,
     o[4] = (uint8_t)CONTAINER_VERSION;
     o[5] = (uint8_t)p.precision;
     o[6] = p.w3d ? 2 : 1;  // window id (R1; 2 = the 3D window R13, a volume)
-    o[7] = 0;  // fill (R2)
+    o[7] = p.bits == 12 ? 12 : 0;  // alphabet (R15; 0 = 8-bit)
     put_u32(o + 8, p.W);
     put_u32(o + 12, p.H);
     put_u16(o + 16, p.hdr_tw);
@@ -1029,7 +1081,7 @@ __global__ void k_dec_prep(Plan p, const uint8_t* __restrict__ bits, const uint6
   const uint64_t len = cont_len[img];  // required: every read below stays inside [b, b + len)
   int err = 0;
   if (len < HDR_FIXED || b[0] != 'D' || b[1] != 'L' || b[2] != 'I' || b[3] != 'C') err = 6;
-  else if (b[4] != CONTAINER_VERSION || b[6] != (p.w3d ? 2 : 1) || b[7] != 0 ||
+  else if (b[4] != CONTAINER_VERSION || b[6] != (p.w3d ? 2 : 1) || b[7] != (p.bits == 12 ? 12 : 0) ||
            (check_numerics && get_u16(b + 22) != NUMERICS_REV))
     err = 5;
   else if (get_u32(b + 8) != p.W || get_u32(b + 12) != p.H || get_u16(b + 16) != p.hdr_tw ||
@@ -1120,8 +1172,10 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
   const uint32_t* const lower_done = W3D && zsl > 0 ? sync + 1 + (u - p.upi) : nullptr;
   if (W3D && threadIdx.x == 0) s_lower = 0;
 
+  using Pix = PixT<PREC>;
+  constexpr int BITS = pix_bits<PREC>();
   typename EngineSel<PREC>::T eng;
-  uint8_t* ring = engine_setup<PREC>(eng, smem, w, bar, &tslot, p.w3d);
+  Pix* ring = reinterpret_cast<Pix*>(engine_setup<PREC>(eng, smem, w, bar, &tslot, p.w3d));
   if constexpr (PREC == 1) eng.bar2 = smem_u32(&bar[2]);  // (TcStream: no half-layer split)
   if (w.b1img) {  // the unit's image's metadata-folded layer-1 bias
     if constexpr (PREC == 1) {
@@ -1132,11 +1186,11 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       eng.b0 = w.b1img + (uint64_t)(un.img / DEPTH) * HID;
     }
   }
-  uint32_t* cursor = reinterpret_cast<uint32_t*>(ring + RING_BYTES + 16);  // 16 zero bytes after the ring
+  uint32_t* cursor = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(ring + RING_BYTES) + 16);  // 16 zero bytes after the ring
   uint32_t* s_sbase = cursor + ((un.ngroups + 3u) & ~3u);                   // per-group stream table
   uint32_t* s_slen = s_sbase + ((un.ngroups + 3u) & ~3u);
   uint32_t* s_t3 = s_slen + ((un.ngroups + 3u) & ~3u);  // W3D bf16: [2][ROWS][3]
-  for (uint32_t i = threadIdx.x; i < RING_BYTES / 16; i += blockDim.x)
+  for (uint32_t i = threadIdx.x; i < RING_BYTES * sizeof(Pix) / 16; i += blockDim.x)
     reinterpret_cast<int4*>(ring)[i] = make_int4(0, 0, 0, 0);
   const uint32_t G = p.G;
   const uint32_t g_shift = (uint32_t)(__ffs((int)G) - 1);
@@ -1378,7 +1432,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       int pr_t = 0, pr_k = 0;
       auto next_slice = [&](int& c) -> bool {
         while (pr_t < T) {
-          if (pr_k < CH_NET && any_t(pr_t)) {
+          if (pr_k < (PREC == 3 ? CH_NET12 : CH_NET) && any_t(pr_t)) {
             c = pr_k++;
             return true;
           }
@@ -1392,7 +1446,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       auto issue_l0 = [&](bool a) {
         if (a) {
           mbar_wait(a_ready, aph);
-          if constexpr (PREC == 2) {
+          if constexpr (PREC >= 2) {
             eng.issue_l0();
           } else {
             eng.issue_slices(0, 0, KPAD / 16, TcEngine::dcol_of(0));
@@ -1401,21 +1455,21 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         }
         aph ^= 1u;  // every row warp arrives once per front
       };
-      if constexpr (PREC == 2) eng.produce(next_slice);  // prime the ring
+      if constexpr (PREC >= 2) eng.produce(next_slice);  // prime the ring
       issue_l0(any_t(0));
       unsigned long long ip[3] = {0, 0, 0};  // PROF: network issue, arrive->l0, l0->wait done
 #pragma unroll 1
       for (int t = 0; t < T; ++t) {
         const long long i0 = PROF ? clock64() : 0;
         if (any_t(t)) {
-          if constexpr (PREC == 2) eng.issue_network(next_slice);
+          if constexpr (PREC >= 2) eng.issue_network(next_slice);
           else eng.dec_issue_network();
         }
         const bool an = any_t(t + 1);
         const long long i1 = PROF ? clock64() : 0;
         long long i2 = 0;
         if (NC > 1) {
-          if constexpr (PREC == 2) cluster_arrive_relaxed();
+          if constexpr (PREC >= 2) cluster_arrive_relaxed();
           else cluster_arrive();
           issue_l0(an);
           if (PROF) i2 = clock64();
@@ -1442,7 +1496,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
     // ======================================================= row warps
     const int row = tile_row();
     const uint32_t S = rank * ROWS + (uint32_t)row;
-    uint8_t* oimg = out + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
+    Pix* oimg = reinterpret_cast<Pix*>(out) + (uint64_t)un.img * p.W * p.H + (uint64_t)un.y0 * p.W + un.x0;
     const uint32_t ring_s = smem_u32(ring);
     const uint32_t halo_base = NC > 1 ? map_cluster(ring_s, (rank + 1) % NC) : ring_s;
     const uint32_t halo_flip = rank == NC - 1 ? 1u : 0u;  // wrap-around halo feeds the next pass
@@ -1453,7 +1507,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
     int pix = 0;
     // ring base of slot (r, c): window cell (dr, dc) of the K order at
     // bp + (dc)*RING_ROWS for dr = u - 8, tap 9 at bp + g9 (see the ring notes)
-    auto ring_at = [&](int r, int c) -> const uint8_t* {
+    auto ring_at = [&](int r, int c) -> const Pix* {
       const uint32_t col = (uint32_t)c & 31u;
       const uint32_t cb = col < 6u ? col + 32u : col;
       return ring + (((uint32_t)r >> ns_shift) & 1u) * RING_BANK + cb * RING_ROWS + (uint32_t)row;
@@ -1496,7 +1550,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       }
     };
     auto early_put = [&](int r, int c) {
-      const uint8_t* bp = ring_at(r, c) + gu;
+      const Pix* bp = ring_at(r, c) + gu;
       uint32_t tv[10];
 #pragma unroll
       for (int i = 0; i < 9; ++i) tv[i] = bp[(i - 6) * RING_ROWS];
@@ -1507,8 +1561,9 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
 #pragma unroll
         for (int q = 0; q < 5; ++q) {
           float x0, x1;
-          f2_split(f2_add(f2_bits(0x3F800000u | (tv[2 * q] << 15), 0x3F800000u | (tv[2 * q + 1] << 15)), m1), x0,
-                   x1);
+          f2_split(f2_add(f2_bits(0x3F800000u | (tv[2 * q] << (23 - BITS)), 0x3F800000u | (tv[2 * q + 1] << (23 - BITS))),
+                          m1),
+                   x0, x1);
           a[q] = pack_bf16(x0, x1);
         }
         eng.put_input(a);
@@ -1604,7 +1659,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       any_n = any_at(rlo, rhi);
     }
     uint32_t fpo = (uint32_t)(ring_at(r, c) - ring) + 8u;  // the front's fresh-tap ring position
-    uint8_t* optr = nullptr;  // deferred pixel store
+    Pix* optr = nullptr;  // deferred pixel store
     int opix = 0;
     if (pf.on) pf.t = clock64();
 #pragma unroll 1
@@ -1613,15 +1668,15 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       pf.mark(0);
       if (any) {
         // the fresh taps (0,-1) and (-1,+2), decoded on front t-1
-        const uint8_t* fp = ring + fpo;
-        const float xa = u8_unit(fp[-RING_ROWS]);
-        const float xb = u8_unit(fp[2 * RING_ROWS - 1]);
+        const Pix* fp = ring + fpo;
+        const float xa = fresh_in<PREC>(fp[-RING_ROWS]);
+        const float xb = fresh_in<PREC>(fp[2 * RING_ROWS - 1]);
         pf.mark(1);
         // network; the previous front's pixel goes to HBM in the layer-2 MMA
         // wait, the next front's early gather in the layer-3 MMA wait
         if constexpr (PREC >= 1) {
           eng.run_rest_ws(xa, xb, [&](int l) {
-            if (l == 1 && optr) *optr = (uint8_t)opix;
+            if (l == 1 && optr) *optr = (Pix)opix;
             if (l == 2) early_gather(rn, cn);
           }, [&](auto& bq) {
             if constexpr (W3D && PREC == 1) {  // this step's lower taps (s_t3, written by the rANS warp last step)
@@ -1632,7 +1687,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
           });
         } else {
           eng.run_rest(xa, xb, [&](int l) {
-            if (l == 1 && optr) *optr = (uint8_t)opix;
+            if (l == 1 && optr) *optr = (Pix)opix;
             if constexpr (W3D) { if (l == 2) load_lower(rn, cn, active_n, t + 6); }
           }, PROF ? &pf : nullptr);
         }
@@ -1641,7 +1696,9 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         pf.mark(6);  // profile: time spent waiting for the rANS warp's slots
         uint32_t fs, cs;
         bool mine;
-        const int sym = q1_decode(eng, s_slot[row], mine, fs, cs, [&]() { early_signal(rn, cn); }, &pf);
+        int sym;
+        if constexpr (PREC == 3) sym = q12_row<false>(eng, s_slot[row], mine, fs, cs, [&]() { early_signal(rn, cn); });
+        else sym = q1_decode(eng, s_slot[row], mine, fs, cs, [&]() { early_signal(rn, cn); }, &pf);
         // the thread that found the symbol publishes it: own ring, the
         // successor's halo through DSMEM for the CTA's last 8 rows, zero
         // pads, and (f_s, c_s) for the rANS warp (applied next front)
@@ -1651,16 +1708,20 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
           s_res[row] = make_uint2(fs, cs);
           const uint32_t bank = ((uint32_t)r >> ns_shift) & 1u;
           const uint32_t col = (uint32_t)c & 31u;
-          uint8_t* rp = ring + (uint32_t)row + 8u;
-          rp[bank * RING_BANK + col * RING_ROWS] = (uint8_t)sym;
-          if (col < 8u) rp[bank * RING_BANK + (col + 32u) * RING_ROWS] = (uint8_t)sym;
+          Pix* rp = ring + (uint32_t)row + 8u;
+          rp[bank * RING_BANK + col * RING_ROWS] = (Pix)sym;
+          if (col < 8u) rp[bank * RING_BANK + (col + 32u) * RING_ROWS] = (Pix)sym;
           const bool halo = row >= ROWS - 8;
           const uint32_t hb = bank ^ halo_flip;
           const uint32_t hrow = (uint32_t)(row - (ROWS - 8));
           auto hput = [&](uint32_t b, uint32_t pos, uint32_t v) {
             const uint32_t off = b * RING_BANK + pos * RING_ROWS + hrow;
-            if (NC > 1) st_cluster_u8(halo_base + off, v);
-            else ring[off] = (uint8_t)v;
+            if (NC > 1) {
+              if constexpr (sizeof(Pix) == 2) st_cluster_u16(halo_base + 2u * off, v);
+              else st_cluster_u8(halo_base + off, v);
+            } else {
+              ring[off] = (Pix)v;
+            }
           };
           if (halo) {
             hput(hb, col, (uint32_t)sym);
@@ -1692,7 +1753,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         pf.mark(9);
       } else {
         asm volatile("bar.sync 7, %0;" ::"n"(DEC_THREADS) : "memory");  // keep the barrier in step
-        if (optr) *optr = (uint8_t)opix;
+        if (optr) *optr = (Pix)opix;
         if constexpr (W3D && PREC == 0) load_lower(rn, cn, active_n, t + 6);
         early_gather(rn, cn);
         early_signal(rn, cn);
@@ -1749,7 +1810,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       any_n = any_n2;
       fpo = fpo_n;
     }
-    if (optr) *optr = (uint8_t)opix;  // the last front's pixel
+    if (optr) *optr = (Pix)opix;  // the last front's pixel
     __syncthreads();  // (1) cursors final
   }
   if (pf.on) {
@@ -1814,8 +1875,9 @@ cudaError_t launch_enc_mlp(const Plan& p, const DevWeights& w, const uint8_t* d_
   const uint64_t total = (uint64_t)p.u_cnt * p.tiles_per_unit;
   const uint32_t grid = (uint32_t)(total < (uint64_t)num_sms ? total : (uint64_t)num_sms);
   const size_t sm = enc_smem_bytes(p.engine, p.w3d);
-  if (p.engine == 2) {  // P350K: streamed weights, one tile chain per CTA (+ debug exports)
-    cudaError_t e = set_smem(k_enc_mlp<2>, sm);
+  if (p.engine >= 2) {  // P350K / P12: streamed weights, one tile chain per CTA (+ debug exports)
+    auto kern = p.engine == 3 ? k_enc_mlp<3> : k_enc_mlp<2>;
+    cudaError_t e = set_smem(kern, sm);
     if (e != cudaSuccess) return e;
     const bool prof = getenv("DLIC_PROF_STREAM") != nullptr;
     Plan pp = p;
@@ -1824,15 +1886,15 @@ cudaError_t launch_enc_mlp(const Plan& p, const DevWeights& w, const uint8_t* d_
       unsigned long long z[8] = {};
       cudaMemcpyToSymbolAsync(g_sprof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
     }
-    k_enc_mlp<2><<<grid, enc_block(2), sm, st>>>(pp, w, d_imgs, d_fc, dbg_logits, dbg_probs, dbg_freqs);
+    kern<<<grid, enc_block(2), sm, st>>>(pp, w, d_imgs, d_fc, dbg_logits, dbg_probs, dbg_freqs);
     if (prof) {
       unsigned long long h[8];
       cudaMemcpyFromSymbolAsync(h, g_sprof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
-      const double ns = (double)h[4];
+      const double ns = (double)h[4], cpn = p.engine == 3 ? CH_NET12 : CH_NET;
       fprintf(stderr, "[stream prof] per chunk (issuer, cycles): data wait %.0f  stage wait %.0f  epilogue wait %.0f  "
               "total %.0f  (chunks %llu) | per tile (row thread 0): feed %.0f network %.0f q1 %.0f\n", h[0] / ns,
-              h[1] / ns, h[2] / ns, h[3] / ns, h[4], h[5] / (ns / CH_NET), h[6] / (ns / CH_NET), h[7] / (ns / CH_NET));
+              h[1] / ns, h[2] / ns, h[3] / ns, h[4], h[5] / (ns / cpn), h[6] / (ns / cpn), h[7] / (ns / cpn));
     }
   } else if (p.engine == 1 && (dbg_logits || dbg_probs || dbg_freqs)) {
     // parity tap: the production kernel with its debug exports
@@ -1954,6 +2016,7 @@ static int max_clusters_t(uint32_t nc, size_t sm) {
 }
 
 int dec_max_active_clusters(uint32_t engine, uint32_t nc, size_t smem) {
+  if (engine == 3) return max_clusters_t<3>(nc, smem);
   if (engine == 2) return max_clusters_t<2>(nc, smem);
   return engine == 1 ? max_clusters_t<1>(nc, smem) : max_clusters_t<0>(nc, smem);
 }
@@ -1961,6 +2024,8 @@ int dec_max_active_clusters(uint32_t engine, uint32_t nc, size_t smem) {
 cudaError_t launch_decode(const Plan& p, const DevWeights& w, const uint8_t* d_bits, const uint64_t* d_cont_off,
                           const uint32_t* d_sbase, const uint32_t* d_slen, uint8_t* d_imgs, int32_t* d_status,
                           cudaStream_t st, unsigned long long* prof, uint32_t* d_sync) {
+  if (p.engine == 3)
+    return launch_decode_t<3, false>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof, d_sync);
   if (p.engine == 2) {
     if (prof)
       return launch_decode_t<2, true>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof, d_sync);

@@ -55,13 +55,44 @@ constexpr uint32_t CH_BYTES = CH_SL * SL_BYTES;  // 32 KB
 constexpr int CH_LAYER = SL_H / CH_SL;      // 4 chunks per hidden layer
 constexpr int CH_NET = SL_NET / CH_SL;      // 20 chunks per network
 constexpr uint32_t SL1_BYTES = SL_L0 * SL_BYTES;  // resident layer 1: 40 KB
-constexpr int S_STAGES = 5;                 // ring depth: 160 KB
-constexpr uint32_t SRING_BYTES = S_STAGES * CH_BYTES;
-constexpr uint32_t SBAR_BYTES = 2 * S_STAGES * 8;
-// shared memory of the engine: layer 1 | ring | biases | full[S] empty[S]
-constexpr uint32_t SENG_L1 = 0, SENG_RING = SL1_BYTES, SENG_BIAS = SL1_BYTES + SRING_BYTES;
-constexpr uint32_t SENG_BARS = SENG_BIAS + SBIAS_BYTES;
-constexpr uint32_t SENG_BYTES = SENG_BARS + SBAR_BYTES;
+// 12-bit alphabet (§8(f) f3, engine 3; readings R15-R17): P12 = P350K's
+// layers 1-5 and a 4096-neuron output layer.  The head is computed in N=128
+// column chunks (32 per pass) into a double-buffered accumulator (TMEM
+// [0,128) / [128,256)), twice per network: pass 1 takes the row max and sum
+// of exponentials (online), pass 2 recomputes the same logits (the same MMAs
+// on the same operands: bit-identical) for p_i, the integer table and the
+// search.  Each head chunk is K=256 x N=128 (16 slices of 4 KB) = two 32 KB
+// stream chunks.
+constexpr int H12_N = 4096;
+constexpr int H12_CN = 128;                     // head columns per accumulator chunk
+constexpr int H12_NCH = H12_N / H12_CN;         // 32
+constexpr uint32_t H12_SL_BYTES = 4096;         // one K=16 slice of an N=128 chunk
+constexpr int H12_CH_SL = 8;                    // slices per 32 KB stream chunk
+constexpr int H12_STREAM = 2 * H12_NCH;         // 64 stream chunks per pass
+constexpr int CH_HID12 = 4 * CH_LAYER;          // layers 2-5: 16 stream chunks
+constexpr int CH_NET12 = CH_HID12 + 2 * H12_STREAM;  // 144 per network (head twice)
+constexpr uint32_t SWIMG12_BYTES = SL1_BYTES + (uint32_t)(CH_HID12 + H12_STREAM) * CH_BYTES;
+// biases (12-bit): [5][256] layers 1-5, the fresh table at SB_FRESH, head at SB12_HEAD
+constexpr int SB12_HEAD = 2048;
+constexpr uint32_t SBIAS12_BYTES = (SB12_HEAD + H12_N) * 4;  // 24 KB
+constexpr float Q12_SCALE = 61376.0f;           // 2^16 - 4096 - 64 (R17)
+
+template <bool H12>
+struct StreamCfg {
+  static constexpr int S = H12 ? 4 : 5;         // ring stages (160 KB / 128 KB)
+  static constexpr uint32_t RING = S * CH_BYTES;
+  static constexpr uint32_t BIAS = H12 ? SBIAS12_BYTES : SBIAS_BYTES;
+  static constexpr uint32_t L1 = 0, RINGO = SL1_BYTES, BIASO = SL1_BYTES + RING;
+  static constexpr uint32_t BARS = BIASO + BIAS;
+  // full[S] empty[S] (+ 12-bit: dfull[2] dfree[2])
+  static constexpr uint32_t BYTES = BARS + 2 * S * 8 + (H12 ? 32 : 0);
+};
+constexpr int S_STAGES = StreamCfg<false>::S;
+constexpr uint32_t SRING_BYTES = StreamCfg<false>::RING;
+constexpr uint32_t SENG_L1 = 0, SENG_RING = SL1_BYTES, SENG_BIAS = StreamCfg<false>::BIASO;
+constexpr uint32_t SENG_BARS = StreamCfg<false>::BARS;
+constexpr uint32_t SENG_BYTES = StreamCfg<false>::BYTES;
+constexpr uint32_t SENG12_BYTES = StreamCfg<true>::BYTES;
 constexpr uint32_t TS_D = 0, TS_A = 256, TS_A0 = 384, TS_X = 448;
 
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
@@ -79,7 +110,10 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 // slices consumed
 __device__ unsigned long long g_sprof[8];
 
-struct TcStream {
+template <bool H12>
+struct TcStreamT {
+  using Cfg = StreamCfg<H12>;
+  static constexpr int S = Cfg::S;
   uint32_t tmem;
   const float* bias;       // shared
   const float* b0;         // layer-1 biases (shared)
@@ -88,8 +122,10 @@ struct TcStream {
   uint32_t ring, full0, empty0;  // shared addresses
   uint32_t l1s;                  // resident layer-1 image (shared)
   uint32_t aready;         // layer-1 input ready: one arrival per row warp
+  uint32_t dfull0, dfree0; // 12-bit head: accumulator buffer b full / released (+8b)
+  uint32_t hph = 0;        // 12-bit head: dfull parities of buffers 0, 1 (bits 0, 1)
   const uint8_t* wstream;  // the streamed weight image (global)
-  uint32_t ccnt = 0, pcnt = 0;   // slices consumed / produced (issuer warp)
+  uint32_t ccnt = 0, pcnt = 0;   // chunks consumed / produced (issuer warp)
   bool prof = false;
   uint32_t mode = 0;  // diagnostics: bit 1 no copies, bit 2 no MMAs (results invalid)
   unsigned long long pw[3] = {0, 0, 0};
@@ -147,10 +183,11 @@ struct TcStream {
     tmem_st8h<16>(tmem + lo + TS_A + 32u * (uint32_t)j + 8u, pk + 8);
     tc_wait_st();
   }
-  // Layers 1-6 after layer 1's MMA was issued; hook(l) runs in layer l+1's
-  // MMA wait (as TcEngine::run_rest_ws); pre0 is the interface's layer-1 bias
-  // hook (unused: volumes run on the P100K engine).  Column group j signals
-  // on named barrier 8 + j (4 warps + the issuer: 160 threads).
+  // Layers 1-6 (12-bit: 1-5; the head follows in q12_row) after layer 1's
+  // MMA was issued; hook(l) runs in layer l+1's MMA wait (as
+  // TcEngine::run_rest_ws); pre0 is the interface's layer-1 bias hook
+  // (unused: volumes run on the P100K engine).  Column group j signals on
+  // named barrier 8 + j (4 warps + the issuer: 160 threads).
   template <class Hook, class Pre0>
   __device__ __forceinline__ void run_rest_ws(float xa, float xb, Hook&& hook, Pre0&&) {
     float2 bq[16];
@@ -163,8 +200,9 @@ struct TcStream {
     wait_mma();
     epilogue<true>(bq, xa, xb);
     signal();
+    constexpr int LAST = H12 ? NLAYER - 2 : NLAYER - 1;  // 12-bit: stop after layer 5's epilogue
 #pragma unroll 1
-    for (int l = 1; l < NLAYER; ++l) {
+    for (int l = 1; l <= LAST; ++l) {
       hook(l);
       if (l < NLAYER - 1) load_bias(l, bq);
       wait_mma();
@@ -186,8 +224,7 @@ struct TcStream {
   __device__ __forceinline__ void run_rest(float xa, float xb, Hook&& hook, Prof* = nullptr) {
     run_rest_ws(xa, xb, hook, [](auto&) {});
   }
-  // softmax interface (as TcEngine): 32 logits of this thread, final biases,
-  // per-row exchange words through TMEM columns [448, 512)
+  // softmax interface (as TcEngine)
   __device__ __forceinline__ void ld32(uint32_t (&v)[32]) const {
     tmem_ld32h<32>(tmem + lane_off() + TS_D + 64u * (uint32_t)col_grp(), v);
     tc_wait_ld();
@@ -212,20 +249,41 @@ struct TcStream {
     tmem_ld4h<TM_XUP>(tmem + lane_off() + TS_X + 4u * (uint32_t)slot, v);
     tc_wait_ld();
   }
+  // 12-bit head, row side: this thread's 16 logits of head chunk u (pass-major
+  // counter; buffer u & 1, columns [32j + 16h, +16) of the chunk), the buffer
+  // released once loaded
+  __device__ __forceinline__ void head_ld(uint32_t u, uint32_t (&v)[16]) {
+    const uint32_t b = u & 1u;
+    mbar_wait(dfull0 + 8u * b, (hph >> b) & 1u);
+    hph ^= 1u << b;
+    tc_fence_after();
+    tmem_ld16h<16>(tmem + lane_off() + TS_D + H12_CN * b + 32u * (uint32_t)col_grp(), v);
+    tc_wait_ld();
+    tc_fence_before();
+    __syncwarp();
+    if (lane_id() == 0) mbar_arrive(dfree0 + 8u * b);
+  }
 
   // ---- issuer warp (whole converged warp)
-  // produce chunks until pcnt == ccnt + S_STAGES - 1 (or the schedule ends);
-  // next(c) yields the producer's next chunk (0..19 of a network) in
-  // consumption order
+  // global address of stream chunk c of a network (8-bit: 0..19 = layers 2-6;
+  // 12-bit: 0..15 layers 2-5, then the head's 64 chunks twice)
+  __device__ __forceinline__ const uint8_t* chunk_src(int c) const {
+    if constexpr (H12) {
+      if (c >= CH_HID12) c = CH_HID12 + (c - CH_HID12) % H12_STREAM;
+    }
+    return wstream + SL1_BYTES + (uint64_t)c * CH_BYTES;
+  }
+  // produce chunks until pcnt == ccnt + S - 1 (or the schedule ends);
+  // next(c) yields the producer's next chunk of a network in consumption order
   template <class Next>
   __device__ __forceinline__ void produce(Next&& next) {
-    while (pcnt < ccnt + (uint32_t)S_STAGES - 1u) {
+    while (pcnt < ccnt + (uint32_t)S - 1u) {
       int c;
       if (!next(c)) return;
-      const uint32_t s = pcnt % (uint32_t)S_STAGES;
-      if (pcnt >= (uint32_t)S_STAGES) {
+      const uint32_t s = pcnt % (uint32_t)S;
+      if (pcnt >= (uint32_t)S) {
         const long long t0 = prof ? clock64() : 0;
-        mbar_wait(empty0 + 8u * s, ((pcnt / (uint32_t)S_STAGES) - 1u) & 1u);
+        mbar_wait(empty0 + 8u * s, ((pcnt / (uint32_t)S) - 1u) & 1u);
         if (prof) pw[1] += clock64() - t0;
       }
       if (lane_id() == 0) {
@@ -233,24 +291,35 @@ struct TcStream {
           mbar_arrive(full0 + 8u * s);
         } else {
           mbar_expect_tx(full0 + 8u * s, CH_BYTES);
-          bulk_g2s(ring + s * CH_BYTES, wstream + SL1_BYTES + (uint64_t)c * CH_BYTES, CH_BYTES, full0 + 8u * s);
+          bulk_g2s(ring + s * CH_BYTES, chunk_src(c), CH_BYTES, full0 + 8u * s);
         }
       }
       __syncwarp();
       ++pcnt;
     }
   }
-  // one chunk: wait for its data, 4 MMAs into D (accumulate unless the
-  // layer's first), release its stage when they complete
-  __device__ __forceinline__ void consume(int cl) {
-    const uint32_t s = ccnt % (uint32_t)S_STAGES;
+  // one stream chunk: wait for its data, its MMAs into D (N=256: 4 K-slices of
+  // a hidden layer, K-chunk cl; 12-bit head: 8 K-slices of N=128 into buffer
+  // dcol, K-half cl), release its stage when they complete
+  __device__ __forceinline__ void consume(int cl, bool head = false, uint32_t dcol = 0) {
+    const uint32_t s = ccnt % (uint32_t)S;
     const long long t0 = prof ? clock64() : 0;
-    mbar_wait(full0 + 8u * s, (ccnt / (uint32_t)S_STAGES) & 1u);
+    mbar_wait(full0 + 8u * s, (ccnt / (uint32_t)S) & 1u);
     if (prof) pw[0] += clock64() - t0;
     tc_fence_after();
     if (mode & 4u) {
       if (lane_id() == 0) mbar_arrive(empty0 + 8u * s);
       __syncwarp();
+    } else if (head) {
+      const uint32_t id = umma_idesc(64, H12_CN);
+#pragma unroll
+      for (int i = 0; i < H12_CH_SL; ++i) {
+        const int kk = H12_CH_SL * cl + i;
+        const uint64_t bd =
+            umma_desc(ring + s * CH_BYTES + (uint32_t)i * H12_SL_BYTES, (uint32_t)H12_CN * 16u, 128u);
+        umma_ts_warp(tmem + TS_D + dcol, tmem + TS_A + 8u * (uint32_t)kk, bd, id, kk > 0 ? 1u : 0u);
+      }
+      umma_commit_warp(empty0 + 8u * s);
     } else {
       const uint32_t id = umma_idesc(64, SH);
 #pragma unroll
@@ -295,11 +364,14 @@ struct TcStream {
       atomicAdd(&g_sprof[4], (unsigned long long)ccnt);
     }
   }
-  // layers 2-6, each once every column group signalled its previous epilogue
+  // the layers after layer 1, each once every column group signalled its
+  // previous epilogue; 12-bit: layers 2-5, then the head's two passes, each
+  // accumulator chunk once the row warps released its buffer (two chunks ago)
   template <class Next>
   __device__ __forceinline__ void issue_network(Next&& next) {
+    constexpr int NHID = H12 ? NLAYER - 2 : NLAYER - 1;
 #pragma unroll 1
-    for (int l = 1; l < NLAYER; ++l) {
+    for (int l = 1; l <= NHID; ++l) {
       const long long t0 = prof ? clock64() : 0;
 #pragma unroll
       for (int j = 0; j < NGRP; ++j) asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
@@ -312,7 +384,162 @@ struct TcStream {
       }
       umma_commit_warp(bar);
     }
+    if constexpr (H12) {
+      // the last hidden layer's epilogues (A of the head, and D free)
+#pragma unroll
+      for (int j = 0; j < NGRP; ++j) asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
+      tc_fence_after();
+#pragma unroll 1
+      for (uint32_t u = 0; u < 2u * H12_NCH; ++u) {
+        const uint32_t b = u & 1u;
+        if (u >= 2) {  // buffer b held chunk u-2: wait until every row warp loaded it
+          const long long t0 = prof ? clock64() : 0;
+          mbar_wait(dfree0 + 8u * b, ((u >> 1) - 1u) & 1u);
+          if (prof) pw[2] += clock64() - t0;
+          tc_fence_after();
+        }
+#pragma unroll 1
+        for (int cl = 0; cl < 2; ++cl) {
+          consume(cl, true, H12_CN * b);
+          produce(next);
+        }
+        umma_commit_warp(dfull0 + 8u * b);
+      }
+    }
   }
 };
+using TcStream = TcStreamT<false>;
+using TcStream12 = TcStreamT<true>;
+
+// ---------------------------------------------------------------- 12-bit head, row side
+// One pixel row = 8 threads (group j, half h); thread t = 2j + h owns the
+// columns [32j + 16h, +16) of every 128-column chunk q, i.e. symbols
+// 128q + 32j + 16h + i.  Reading R17 on the GPU (the same routine in the
+// encoder and the decoder, R8):
+//   pass 1 (online): per chunk l_i = acc_i + b_i (fp32 RN), c = max of the
+//     16, m' = max(m, c), z = z * 2^((m - m') log2e) + sum_i 2^((l_i - m') log2e)
+//     (MUFU ex2.approx, fixed pair tree); then halves (h = 0 term first) and
+//     groups (((z0 w0 + z1 w1) + z2 w2) + z3 w3, w_g = 2^((m_g - M) log2e))
+//     combine to M, Z; r = rcp_rn(Z);
+//   pass 2: p_i = 2^((l_i - M) log2e) * r, f_i = 1 + floor(p_i * 61376)
+//     (fp32 RN products), the row's running cumulative through one exchange
+//     per chunk; symbol 4095 takes f = 2^16 - c_4095 (the residual, R17).
+// ENC: key = the true symbol -> (f_s, c_s) at the owning thread (mine);
+// decode: key = the slot -> the symbol s with c_s <= slot < c_s + f_s.
+// mid() runs once the last chunk is loaded (the accumulator is free).
+struct Q12Dbg {
+  float* logits;   // [4096] of this row or null
+  float* probs;
+  uint16_t* freqs;
+};
+__device__ __forceinline__ float q12_e(float l, float m) {
+  return ex2_approx(__fmul_rn(__fsub_rn(l, m), 1.4426950408889634f));
+}
+template <bool ENC, class Mid>
+__device__ __forceinline__ int q12_row(TcStream12& e, uint32_t key, bool& mine_out, uint32_t& fs_out,
+                                       uint32_t& cs_out, Mid&& mid, const Q12Dbg* dbg = nullptr) {
+  const int j = col_grp(), h = half_id();
+  const int cb = 32 * j + 16 * h;
+  const float* hb = e.bias + SB12_HEAD + cb;
+  // ---- pass 1
+  float m = -INFINITY, z = 0.0f;
+#pragma unroll 1
+  for (uint32_t q = 0; q < (uint32_t)H12_NCH; ++q) {
+    uint32_t v[16];
+    e.head_ld(q, v);
+    float l[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) l[i] = __fadd_rn(__uint_as_float(v[i]), hb[H12_CN * q + i]);
+    if (dbg && dbg->logits) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) dbg->logits[H12_CN * q + cb + i] = l[i];
+    }
+    float c8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c8[i] = fmaxf(l[2 * i], l[2 * i + 1]);
+    const float c = fmaxf(fmaxf(fmaxf(c8[0], c8[1]), fmaxf(c8[2], c8[3])), fmaxf(fmaxf(c8[4], c8[5]), fmaxf(c8[6], c8[7])));
+    const float mn = fmaxf(m, c);
+    float s8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s8[i] = __fadd_rn(q12_e(l[2 * i], mn), q12_e(l[2 * i + 1], mn));
+    const float s = __fadd_rn(__fadd_rn(__fadd_rn(s8[0], s8[1]), __fadd_rn(s8[2], s8[3])),
+                              __fadd_rn(__fadd_rn(s8[4], s8[5]), __fadd_rn(s8[6], s8[7])));
+    z = __fadd_rn(q > 0 ? __fmul_rn(z, q12_e(m, mn)) : 0.0f, s);
+    m = mn;
+  }
+  // halves: the h = 0 term first on both lanes
+  const float mo = __shfl_xor_sync(0xFFFFFFFFu, m, 16), zo = __shfl_xor_sync(0xFFFFFFFFu, z, 16);
+  const float m_lo = h ? mo : m, m_hi = h ? m : mo, z_lo = h ? zo : z, z_hi = h ? z : zo;
+  const float m2 = fmaxf(m_lo, m_hi);
+  const float z2 = __fadd_rn(__fmul_rn(z_lo, q12_e(m_lo, m2)), __fmul_rn(z_hi, q12_e(m_hi, m2)));
+  e.xput(0, __float_as_uint(m2));
+  e.xput(1, __float_as_uint(z2));
+  e.xsync();
+  uint32_t mm[4], zz[4];
+  e.xget4(0, mm);
+  e.xget4(1, zz);
+  const float M = fmaxf(fmaxf(__uint_as_float(mm[0]), __uint_as_float(mm[1])),
+                        fmaxf(__uint_as_float(mm[2]), __uint_as_float(mm[3])));
+  float Z = __fmul_rn(__uint_as_float(zz[0]), q12_e(__uint_as_float(mm[0]), M));
+#pragma unroll
+  for (int g = 1; g < NGRP; ++g) Z = __fadd_rn(Z, __fmul_rn(__uint_as_float(zz[g]), q12_e(__uint_as_float(mm[g]), M)));
+  const float rz = __frcp_rn(Z);
+  // ---- pass 2
+  float base = 0.0f;  // cumulative frequency before the current chunk (exact integers)
+  bool mine = false;
+  uint32_t fs = 0, cs = 0;
+  int sym = 0;
+  const float keyf = (float)key;
+#pragma unroll 1
+  for (uint32_t q = 0; q < (uint32_t)H12_NCH; ++q) {
+    uint32_t v[16];
+    e.head_ld(H12_NCH + q, v);
+    if (q == H12_NCH - 1) mid();
+    float f[16];
+    float S = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float l = __fadd_rn(__uint_as_float(v[i]), hb[H12_CN * q + i]);
+      const float p = __fmul_rn(q12_e(l, M), rz);
+      f[i] = 1.0f + floorf(__fmul_rn(p, Q12_SCALE));
+      S += f[i];  // integers < 2^24: exact in any order
+      if (dbg && dbg->probs) dbg->probs[H12_CN * q + cb + i] = p;
+    }
+    const float So = __shfl_xor_sync(0xFFFFFFFFu, S, 16);
+    const float Sj = S + So;  // this group's part of the chunk
+    e.xput(2 + (int)(q & 1u), __float_as_uint(Sj));
+    e.xsync();
+    uint32_t g4[4];
+    e.xget4(2 + (int)(q & 1u), g4);
+    float pre = 0.0f, tot = 0.0f;
+#pragma unroll
+    for (int g = 0; g < NGRP; ++g) {
+      const float G = __uint_as_float(g4[g]);
+      pre += g < j ? G : 0.0f;
+      tot += G;
+    }
+    float c = base + pre + (h ? So : 0.0f);  // cumulative before my first column
+    const bool last = q == H12_NCH - 1 && j == NGRP - 1 && h == 1;  // my column 15 is symbol 4095
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int s_i = (int)(H12_CN * q) + cb + i;
+      const float fi = (last && i == 15) ? 65536.0f - c : f[i];
+      if (dbg && dbg->freqs) dbg->freqs[s_i] = (uint16_t)fi;
+      const bool hit = ENC ? (s_i == (int)key) : (!mine && keyf >= c && keyf < c + fi);
+      if (hit) {
+        mine = true;
+        sym = s_i;
+        fs = (uint32_t)fi;
+        cs = (uint32_t)c;
+      }
+      c += fi;
+    }
+    base += tot;
+  }
+  mine_out = mine;
+  fs_out = fs;
+  cs_out = cs;
+  return sym;
+}
 
 }  // namespace dlic

@@ -72,6 +72,17 @@ def p350k():
     print("wrote", out)
 
 
+def p12():
+    """fixtures/p12_seeded.dlicmdl: the §8(f) f3 network P12 (78 -> 256x5 ->
+    4096, 12-bit alphabet, reading R16), seeded He-uniform weights with biases
+    (the GPU tests' and bench's model)."""
+    layers = synth.he_uniform_layers(mlp.P12, seed=5, bias_scale=0.1)
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "fixtures", "p12_seeded.dlicmdl")
+    with open(out, "wb") as fh:
+        fh.write(model_io.save(layers))
+    print("wrote", out)
+
+
 def pool_meta():
     layers = synth.he_uniform_pooled(81, [128, 128, 128, 128, 128, 256], POOL, seed=7, bias_scale=0.1)
     out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "fixtures",
@@ -88,8 +99,11 @@ if __name__ == "__main__":
         p100k_3d()
     elif len(sys.argv) > 1 and sys.argv[1] == "p350k":
         p350k()
+    elif len(sys.argv) > 1 and sys.argv[1] == "p12":
+        p12()
     else:
         main()
         pool_meta()
         p100k_3d()
         p350k()
+        p12()
