@@ -251,7 +251,7 @@ __device__ __forceinline__ float u8_unit(uint32_t v) {
 // hidden columns [32j+16h, +16) and logits [64j+32h, +32) (dlic_device.cuh).
 // PREC 2 (P350K, TcStream): one more warp streams the weights and issues the
 // MMAs (TcStream::issue_tiles); the row warps run the same code as PREC 0.
-__host__ __device__ constexpr int enc_block(int prec) { return prec >= 2 ? NTHREADS + 32 : NTHREADS; }
+__host__ __device__ constexpr int enc_block(int prec) { return prec >= 2 ? NTHREADS + 64 : NTHREADS; }
 template <int PREC>
 __global__ void __launch_bounds__(enc_block(PREC), 1)
     k_enc_mlp(Plan p, DevWeights w, const uint8_t* __restrict__ imgs, uint32_t* __restrict__ fc,
@@ -288,7 +288,12 @@ __global__ void __launch_bounds__(enc_block(PREC), 1)
       };
       eng.prof = p.prof != 0;
       eng.mode = p.prof;
-      eng.issue_tiles(n, next);
+      if (threadIdx.x < NTHREADS + 32) {
+        eng.issue_tiles(n);  // warp 16: MMA issuer
+      } else {
+        eng.produce_all(next);  // warp 17: weight-stream producer
+        if (eng.prof && lane_id() == 0) atomicAdd(&g_sprof[1], eng.pw[1]);
+      }
       engine_teardown<PREC>(eng);
       return;
     }
@@ -1125,7 +1130,10 @@ __global__ void k_dec_prep(Plan p, const uint8_t* __restrict__ bits, const uint6
 constexpr int DEC_THREADS = NTHREADS + 32;
 
 // bf16: one more warp (the 18th) only issues the network's MMAs (run_rest_ws)
-__host__ __device__ constexpr int dec_block(int prec) { return prec >= 1 ? DEC_THREADS + 32 : DEC_THREADS; }
+// bf16: + the MMA issuer warp; streamed engines: + the weight producer warp
+__host__ __device__ constexpr int dec_block(int prec) {
+  return prec >= 2 ? DEC_THREADS + 64 : prec == 1 ? DEC_THREADS + 32 : DEC_THREADS;
+}
 
 template <int PREC, bool PROF, bool W3D>
 __global__ void __launch_bounds__(dec_block(PREC), 1)
@@ -1415,6 +1423,42 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
       apply(1, T - 1);
     }
     __syncthreads();  // (1) cursors final
+  } else if (PREC >= 2 && threadIdx.x >= DEC_THREADS + 32) {
+    // ======================================================= weight-stream producer warp
+    // the chunks of every front this CTA has an active row on, in the
+    // issuer's order: front t's rest after barrier t-1, then up to S-1 chunks
+    // of front t+1 before barrier t (they only need front t's last stages,
+    // whose MMAs complete on their own)
+    if constexpr (PREC >= 2) {
+      auto any_t = [&](int t) -> bool {  // (as the issuer's)
+        const int rlo = t - uw + 1 > 0 ? (t - uw + 3) / 3 : 0;
+        const int rhi = min(uh - 1, t / 3);
+        if (rlo > rhi) return false;
+        const uint32_t m = (uint32_t)rlo & (NS - 1), b = rank * ROWS;
+        const uint32_t d = m - b < (uint32_t)ROWS ? 0u : ((b - m) & (NS - 1));
+        return rlo + (int)d <= rhi;
+      };
+      constexpr int CPN = PREC == 3 ? CH_NET12 : CH_NET;
+      constexpr int LA = EngineSel<PREC>::T::S - 1 < CPN ? EngineSel<PREC>::T::S - 1 : CPN;
+      if (any_t(0))
+        for (int k = 0; k < CPN; ++k) eng.produce_one(k);
+#pragma unroll 1
+      for (int t = 0; t < T; ++t) {
+        const bool an = any_t(t + 1);
+        int done = 0;
+        if (an)
+          for (; done < LA; ++done) eng.produce_one(done);
+        if (NC > 1) {
+          cluster_arrive_relaxed();
+          cluster_wait();
+        } else {
+          __syncthreads();
+        }
+        if (an)
+          for (int k = done; k < CPN; ++k) eng.produce_one(k);
+      }
+    }
+    __syncthreads();  // (1) cursors final
   } else if (PREC >= 1 && threadIdx.x >= DEC_THREADS) {
     // ======================================================= MMA issuer warp (bf16)
     if constexpr (PREC >= 1) {
@@ -1426,20 +1470,6 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         const uint32_t m = (uint32_t)rlo & (NS - 1), b = rank * ROWS;
         const uint32_t d = m - b < (uint32_t)ROWS ? 0u : ((b - m) & (NS - 1));
         return rlo + (int)d <= rhi;
-      };
-      // P350K weight stream: the chunks of layers 2-6 (20 per network) of
-      // every front this CTA has an active row on, in order
-      int pr_t = 0, pr_k = 0;
-      auto next_slice = [&](int& c) -> bool {
-        while (pr_t < T) {
-          if (pr_k < (PREC == 3 ? CH_NET12 : CH_NET) && any_t(pr_t)) {
-            c = pr_k++;
-            return true;
-          }
-          ++pr_t;
-          pr_k = 0;
-        }
-        return false;
       };
       // layer 1 of front t over the 76 early taps, once every row warp has
       // written them and loaded the previous logits (a_ready)
@@ -1455,14 +1485,13 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         }
         aph ^= 1u;  // every row warp arrives once per front
       };
-      if constexpr (PREC >= 2) eng.produce(next_slice);  // prime the ring
       issue_l0(any_t(0));
       unsigned long long ip[3] = {0, 0, 0};  // PROF: network issue, arrive->l0, l0->wait done
 #pragma unroll 1
       for (int t = 0; t < T; ++t) {
         const long long i0 = PROF ? clock64() : 0;
         if (any_t(t)) {
-          if constexpr (PREC >= 2) eng.issue_network(next_slice);
+          if constexpr (PREC >= 2) eng.issue_network();
           else eng.dec_issue_network();
         }
         const bool an = any_t(t + 1);
@@ -1886,7 +1915,7 @@ cudaError_t launch_enc_mlp(const Plan& p, const DevWeights& w, const uint8_t* d_
       unsigned long long z[8] = {};
       cudaMemcpyToSymbolAsync(g_sprof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
     }
-    kern<<<grid, enc_block(2), sm, st>>>(pp, w, d_imgs, d_fc, dbg_logits, dbg_probs, dbg_freqs);
+    kern<<<grid, enc_block(p.engine), sm, st>>>(pp, w, d_imgs, d_fc, dbg_logits, dbg_probs, dbg_freqs);
     if (prof) {
       unsigned long long h[8];
       cudaMemcpyFromSymbolAsync(h, g_sprof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);

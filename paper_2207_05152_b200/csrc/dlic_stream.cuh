@@ -10,15 +10,15 @@
 // the UMMA no-swizzle K-major core-matrix layout (element (n, k) of slice kk
 // at (k/8 - 2kk)*(N/8)*128 + (n/8)*128 + (n%8)*16 + (k%8)*2), a chunk is 4
 // consecutive slices, so one `cp.async.bulk` (TMA bulk copy, mbarrier
-// complete_tx) moves it into a ring of S_STAGES shared-memory stages.  The
-// MMA-issuer warp is both consumer and producer: before a chunk's 4 MMAs it
-// waits for the chunk's `full` barrier; a `tcgen05.commit` after them arrives
-// on the stage's `empty` barrier; after issuing chunk c it refills the stage
-// of chunk c-1 (whose MMAs are done by then) with the chunk S_STAGES-1
-// positions ahead in its consumption order, so the tensor core always has the
-// next chunk queued and the copies run S_STAGES-2 chunks (>= one layer) ahead.
-// (Per-slice stages measured ~800 issuer cycles per 8 KB slice: an mbarrier
-// try_wait alone costs ~90 cycles, B300_MICROARCH; chunks amortise it.)
+// complete_tx) moves it into a ring of S_STAGES shared-memory stages.  Two
+// warps: the PRODUCER walks the chunks in consumption order and refills a
+// stage as soon as its empty barrier says the MMAs that read it completed;
+// the MMA ISSUER only waits for a chunk's `full` barrier, issues its MMAs and
+// commits them to the stage's `empty` barrier.  (The tensor core's issue
+// queue is shallow -- an issuing thread is blocked for most of an MMA's
+// execution, profiles/r1_mb_mma.txt -- so any other work in the issuer idles
+// the tensor core; per-slice stages cost ~800 issuer cycles per 8 KB slice, an
+// mbarrier try_wait alone ~90 cycles, B300_MICROARCH.)
 //
 // Per row the arithmetic mirrors TcEngine (the same softmax/Q1'/search code
 // consumes the same 256 logits, 8 threads x 32 columns per row): layer 1 =
@@ -273,13 +273,11 @@ struct TcStreamT {
     }
     return wstream + SL1_BYTES + (uint64_t)c * CH_BYTES;
   }
-  // produce chunks until pcnt == ccnt + S - 1 (or the schedule ends);
-  // next(c) yields the producer's next chunk of a network in consumption order
-  template <class Next>
-  __device__ __forceinline__ void produce(Next&& next) {
-    while (pcnt < ccnt + (uint32_t)S - 1u) {
-      int c;
-      if (!next(c)) return;
+  // ---- producer warp (whole converged warp): chunk c of a network into the
+  // next ring stage once the stage's previous chunk was consumed (its empty
+  // barrier: the MMAs that read it completed)
+  __device__ __forceinline__ void produce_one(int c) {
+    {
       const uint32_t s = pcnt % (uint32_t)S;
       if (pcnt >= (uint32_t)S) {
         const long long t0 = prof ? clock64() : 0;
@@ -297,6 +295,12 @@ struct TcStreamT {
       __syncwarp();
       ++pcnt;
     }
+  }
+  // produce until next(c) ends the schedule
+  template <class Next>
+  __device__ __forceinline__ void produce_all(Next&& next) {
+    int c;
+    while (next(c)) produce_one(c);
   }
   // one stream chunk: wait for its data, its MMAs into D (N=256: 4 K-slices of
   // a hidden layer, K-chunk cl; 12-bit head: 8 K-slices of N=128 into buffer
@@ -344,17 +348,15 @@ struct TcStreamT {
     umma_commit_warp(bar);
   }
   // (encoder) n networks back to back, each once the row warps signal start_l0
-  template <class Next>
-  __device__ __forceinline__ void issue_tiles(uint64_t n, Next&& next) {
+  __device__ __forceinline__ void issue_tiles(uint64_t n) {
     const long long t00 = clock64();
-    produce(next);
     uint32_t aph = 0;
 #pragma unroll 1
     for (uint64_t k = 0; k < n; ++k) {
       mbar_wait(aready, aph);
       aph ^= 1u;
       issue_l0();
-      issue_network(next);
+      issue_network();
     }
     if (prof && lane_id() == 0) {
       atomicAdd(&g_sprof[0], pw[0]);
@@ -367,8 +369,7 @@ struct TcStreamT {
   // the layers after layer 1, each once every column group signalled its
   // previous epilogue; 12-bit: layers 2-5, then the head's two passes, each
   // accumulator chunk once the row warps released its buffer (two chunks ago)
-  template <class Next>
-  __device__ __forceinline__ void issue_network(Next&& next) {
+  __device__ __forceinline__ void issue_network() {
     constexpr int NHID = H12 ? NLAYER - 2 : NLAYER - 1;
 #pragma unroll 1
     for (int l = 1; l <= NHID; ++l) {
@@ -378,10 +379,7 @@ struct TcStreamT {
       if (prof) pw[2] += clock64() - t0;
       tc_fence_after();
 #pragma unroll 1
-      for (int cl = 0; cl < CH_LAYER; ++cl) {
-        consume(cl);
-        produce(next);
-      }
+      for (int cl = 0; cl < CH_LAYER; ++cl) consume(cl);
       umma_commit_warp(bar);
     }
     if constexpr (H12) {
@@ -398,11 +396,8 @@ struct TcStreamT {
           if (prof) pw[2] += clock64() - t0;
           tc_fence_after();
         }
-#pragma unroll 1
-        for (int cl = 0; cl < 2; ++cl) {
-          consume(cl, true, H12_CN * b);
-          produce(next);
-        }
+        consume(0, true, H12_CN * b);
+        consume(1, true, H12_CN * b);
         umma_commit_warp(dfull0 + 8u * b);
       }
     }
