@@ -22,6 +22,7 @@
 #include "dlic_device.cuh"
 #include "dlic_internal.h"
 #include "dlic_stream.cuh"
+#include "dlic_x3.cuh"
 #include "sha256.h"
 
 using namespace dlic;
@@ -41,7 +42,12 @@ struct dlic_model {
   float* d_w32 = nullptr;
   float* d_wmeta = nullptr;  // metadata rows of W1 [n_meta][HID] fp32
   float* d_range = nullptr;  // (min, max) per metadata feature
-  DevWeights dw(const float* b1img = nullptr) const { return DevWeights{d_wimg, d_bias, d_w32, b1img}; }
+  uint8_t* d_x3img = nullptr;  // fp32 path on tcgen05 (engine 4): hi/lo bf16 limbs (dlic_x3.cuh)
+  float* d_x3bias = nullptr;
+  DevWeights dw(const float* b1img = nullptr, uint32_t engine = 1) const {
+    if (engine == 4) return DevWeights{d_x3img, d_x3bias, d_w32, b1img};
+    return DevWeights{d_wimg, d_bias, d_w32, b1img};
+  }
 };
 
 namespace {
@@ -366,6 +372,68 @@ static dlic_status upload_p350k(dlic_model* m, const ParsedModel& pm) {
   return DLIC_OK;
 }
 
+// The fp32 path's tensor-core image (dlic_x3.cuh): every weight as bf16 hi =
+// bf16_rn(w) and lo = bf16_rn(w - hi).  Layer 1 resident: 5 K-slices x {hi,
+// lo} (N=128, kpos_tap K order, fresh taps zero); then 12 stream chunks of 32
+// KB: layers 2-5 as 2 chunks of 4 K-slices x {hi, lo} (N=128), the logits
+// layer as 4 chunks of 2 K-slices x {hi, lo} (N=256).  Biases fp32: [5][128],
+// [256], fresh table {wa[n], wa[n+1], wb[n], wb[n+1]} (fp32, exact).
+static dlic_status upload_x3(dlic_model* m, const ParsedModel& pm) {
+  std::vector<uint8_t> img(X3_WIMG_BYTES, 0);
+  auto limbs = [](float w, uint16_t& hi, uint16_t& lo) {
+    hi = bf16_bits(w);
+    const uint32_t hu = (uint32_t)hi << 16;
+    float hf;
+    memcpy(&hf, &hu, 4);
+    lo = bf16_bits(w - hf);
+  };
+  // element (n, k) of a K=16 slice of an N-wide operand at slice base `a`
+  auto put = [&](size_t a, int N, int n, int kl, uint16_t u) {
+    memcpy(&img[a + (size_t)(kl / 8) * (N / 8) * 128 + (size_t)(n / 8) * 128 + (n % 8) * 16 + (kl % 8) * 2], &u, 2);
+  };
+  for (int k = 0; k < KPAD; ++k)
+    for (int n = 0; n < HID; ++n) {
+      const int kt = kpos_tap(k);
+      const bool fresh = kt == TAP_FA || kt == TAP_FB;
+      const float w = kt >= 0 && kt < KIN && !fresh ? pm.W[0][(size_t)kt * HID + n] : 0.0f;
+      uint16_t hi, lo;
+      limbs(w, hi, lo);
+      const int kk = k / 16;
+      put((size_t)(2 * kk) * X3_SL, HID, n, k % 16, hi);
+      put((size_t)(2 * kk + 1) * X3_SL, HID, n, k % 16, lo);
+    }
+  for (int l = 1; l < NLAYER; ++l) {
+    const int N = layer_n(l);
+    const bool last = l == NLAYER - 1;
+    const size_t sl = last ? X3_SL_LAST : X3_SL;
+    const int per = last ? 2 : 4;  // K-slices per chunk
+    const size_t c0 = X3_L1_BYTES + (size_t)(l - 1) * 2 * CH_BYTES;  // layers 2-5: 2 chunks each
+    for (int k = 0; k < HID; ++k)
+      for (int n = 0; n < N; ++n) {
+        uint16_t hi, lo;
+        limbs(pm.W[l][(size_t)k * N + n], hi, lo);
+        const int kk = k / 16, cl = kk / per, i = kk % per;
+        const size_t base = c0 + (size_t)cl * CH_BYTES + (size_t)(2 * i) * sl;
+        put(base, N, n, k % 16, hi);
+        put(base + sl, N, n, k % 16, lo);
+      }
+  }
+  std::vector<float> bias(X3_BIAS_BYTES / 4, 0.0f);
+  for (int l = 0; l < NLAYER - 1; ++l)
+    for (int n = 0; n < HID; ++n) bias[(size_t)l * HID + n] = pm.b[l][n];
+  for (int n = 0; n < NOUT; ++n) bias[X3_B_LAST + n] = pm.b[NLAYER - 1][n];
+  for (int n = 0; n < HID; ++n) {
+    const size_t q = X3_B_FRESH + 4 * (size_t)(n / 2) + (n & 1);
+    bias[q] = pm.W[0][(size_t)TAP_FA * HID + n];
+    bias[q + 2] = pm.W[0][(size_t)TAP_FB * HID + n];
+  }
+  CUDA_TRY(cudaMalloc(&m->d_x3img, X3_WIMG_BYTES));
+  CUDA_TRY(cudaMalloc(&m->d_x3bias, bias.size() * 4));
+  CUDA_TRY(cudaMemcpy(m->d_x3img, img.data(), X3_WIMG_BYTES, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(m->d_x3bias, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice));
+  return DLIC_OK;
+}
+
 dlic_status upload_model(dlic_model* m, const ParsedModel& pm_in) {
   m->dims = pm_in.dims;
   std::vector<std::vector<float>> Wf;
@@ -443,6 +511,10 @@ dlic_status upload_model(dlic_model* m, const ParsedModel& pm_in) {
     CUDA_TRY(cudaMemcpy(m->d_wmeta, wm.data(), wm.size() * 4, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(m->d_range, pm.meta_range.data(), pm.meta_range.size() * 4, cudaMemcpyHostToDevice));
   }
+  if (!in3d) {  // the fp32 path's bf16x3 image (engine 4; volumes keep the FFMA engine)
+    dlic_status s = upload_x3(m, pm);
+    if (s != DLIC_OK) return s;
+  }
   CUDA_TRY(cudaMalloc(&m->d_wimg, WIMG_BYTES));
   CUDA_TRY(cudaMalloc(&m->d_bias, bias.size() * 4));
   CUDA_TRY(cudaMalloc(&m->d_w32, w32.size() * 4));
@@ -481,6 +553,8 @@ dlic_status make_plan(uint32_t W, uint32_t H, uint32_t n, const dlic_opts* o, Pl
     p.engine = m->p12 ? 3 : 2;
     p.bits = m->p12 ? 12 : 8;
   }
+  if (m && m->p100k && d.precision == DLIC_PREC_FP32 && d.volume_depth == 0)
+    p.engine = 4;  // fp32 on the tensor cores (bf16x3, dlic_x3.cuh); volumes keep the FFMA engine
   p.tw = tiled ? std::min(d.tile_w, W) : W;
   p.th = tiled ? std::min(d.tile_h, H) : H;
   p.hdr_tw = tiled ? d.tile_w : 0;
@@ -726,7 +800,7 @@ dlic_status run_encode(const dlic_model* m, const Plan& p, const uint8_t* d_imgs
   dlic_status s = meta_bias(m, p, h_meta, nullptr, nullptr, st, sc, &b1img, &d_meta);
   if (s != DLIC_OK) return s;
   ev_begin("mlp", st);
-  CUDA_TRY(launch_enc_mlp(p, m->dw(b1img), d_imgs, d_fc, nullptr, nullptr, nullptr, st, num_sms(m->device)));
+  CUDA_TRY(launch_enc_mlp(p, m->dw(b1img, p.engine), d_imgs, d_fc, nullptr, nullptr, nullptr, st, num_sms(m->device)));
   ev_end("mlp", st);
   ev_begin("rans_enc", st);
   CUDA_TRY(launch_rans_enc(p, d_fc, d_scr, d_words, st));
@@ -823,6 +897,8 @@ void dlic_model_free(dlic_model* m) {
   if (!m) return;
   cudaSetDevice(m->device);
   if (m->d_wimg) cudaFree(m->d_wimg);
+  if (m->d_x3img) cudaFree(m->d_x3img);
+  if (m->d_x3bias) cudaFree(m->d_x3bias);
   if (m->d_bias) cudaFree(m->d_bias);
   if (m->d_w32) cudaFree(m->d_w32);
   if (m->d_wmeta) cudaFree(m->d_wmeta);
@@ -978,7 +1054,7 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
     uint32_t* d_sync;
     s = alloc_sync(p, sc, st, &d_sync);
     if (s != DLIC_OK) return s;
-    CUDA_TRY(launch_decode(p, m->dw(b1img), d_bits, d_meta, d_sbase, d_slen, d_img, d_status, st, d_prof, d_sync));
+    CUDA_TRY(launch_decode(p, m->dw(b1img, p.engine), d_bits, d_meta, d_sbase, d_slen, d_img, d_status, st, d_prof, d_sync));
     ev_end("decode", st);
     if (prof) {
       unsigned long long hp[40];
@@ -1113,7 +1189,7 @@ dlic_status dlic_debug_mlp(const dlic_model* m, const uint8_t* img, uint32_t wid
   const float* b1img = nullptr;
   s = meta_bias(m, p, opts ? opts->meta : nullptr, nullptr, nullptr, st, sc, &b1img);
   if (s != DLIC_OK) return s;
-  CUDA_TRY(launch_enc_mlp(p, m->dw(b1img), d_img, d_fc, d_lg, d_pb, d_fq, st, num_sms(m->device)));
+  CUDA_TRY(launch_enc_mlp(p, m->dw(b1img, p.engine), d_img, d_fc, d_lg, d_pb, d_fq, st, num_sms(m->device)));
   if (logits) CUDA_TRY(cudaMemcpyAsync(logits, d_lg, 4 * npx * nout, cudaMemcpyDeviceToHost, st));
   if (probs) CUDA_TRY(cudaMemcpyAsync(probs, d_pb, 4 * npx * nout, cudaMemcpyDeviceToHost, st));
   if (freqs) CUDA_TRY(cudaMemcpyAsync(freqs, d_fq, 2 * npx * nout, cudaMemcpyDeviceToHost, st));
@@ -1251,7 +1327,7 @@ dlic_status dlic_decode_batch(const dlic_model* m, const uint8_t* bits, size_t l
   uint32_t* d_sync;
   s = alloc_sync(p, sc, st, &d_sync);
   if (s != DLIC_OK) return s;
-  CUDA_TRY(launch_decode(p, m->dw(b1img), d_bits, d_meta, d_sbase, d_slen, d_imgs, d_status, st, nullptr, d_sync));
+  CUDA_TRY(launch_decode(p, m->dw(b1img, p.engine), d_bits, d_meta, d_sbase, d_slen, d_imgs, d_status, st, nullptr, d_sync));
   ev_end("decode", st);
   uint8_t* ho = static_cast<uint8_t*>(g_pin_out.get(npx + 4ull * n + 64));
   if (!ho) return fail(DLIC_E_OUT_OF_MEMORY, "pinned staging");
@@ -1325,7 +1401,7 @@ dlic_status dlic_decode_batch_device(const dlic_model* m, const uint8_t* d_bits,
   uint32_t* d_sync;
   s = alloc_sync(p, sc, st, &d_sync);
   if (s != DLIC_OK) return s;
-  CUDA_TRY(launch_decode(p, m->dw(b1img), d_bits, d_meta, d_sbase, d_slen, d_imgs, d_status, st, nullptr, d_sync));
+  CUDA_TRY(launch_decode(p, m->dw(b1img, p.engine), d_bits, d_meta, d_sbase, d_slen, d_imgs, d_status, st, nullptr, d_sync));
   ev_end("decode", st);
   return DLIC_OK;
 }

@@ -53,7 +53,7 @@ constexpr float Q1_SCALE = 65279.0f;  // 2^16 - 257 (R5, Q1')
 // the exp split is folded in so that a -DDLIC_POLY_FROM variant build can never
 // decode another build's containers.  Value 0 is reserved for the oracle's own
 // arithmetic (fp64 / bf16-emulated network, fp64 softmax).
-constexpr uint32_t NUMERICS_BASE = 1;
+constexpr uint32_t NUMERICS_BASE = 2;  // 2: fp32 path on the tensor cores (bf16x3)
 constexpr uint32_t NUMERICS_REV = (NUMERICS_BASE << 8) | (uint32_t)DLIC_POLY_FROM;
 
 // Layer-1 K order of the bf16 engine.  K position p = 10u + i belongs to

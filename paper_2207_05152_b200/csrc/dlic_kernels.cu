@@ -24,6 +24,7 @@
 #include "dlic_device.cuh"
 #include "dlic_internal.h"
 #include "dlic_stream.cuh"
+#include "dlic_x3.cuh"
 
 
 
@@ -54,8 +55,9 @@ __host__ __device__ inline uint32_t bias_bytes(uint32_t w3d) { return BIAS_BYTES
 // `precision` here is the ENGINE: 0 fp32 FFMA, 1 bf16 P100K (resident
 // weights), 2 bf16 P350K (streamed weights, dlic_stream.cuh)
 size_t enc_smem_bytes(uint32_t precision, uint32_t w3d) {
-  if (precision == 3) return SENG12_BYTES;
-  if (precision == 2) return SENG_BYTES;
+  if (precision == 4) return TcX3::SMEM;
+  if (precision == 3) return TcStream12::SMEM;
+  if (precision == 2) return TcStream::SMEM;
   return precision == 1 ? WIMG_BYTES + bias_bytes(w3d) : F32_BUF_BYTES + F32_X_BYTES;
 }
 static uint32_t cursor_bytes(uint32_t ngroups) { return (ngroups * 4u + 15u) & ~15u; }
@@ -87,6 +89,10 @@ template <>
 struct EngineSel<3> {
   using T = TcStream12;
 };
+template <>
+struct EngineSel<4> {
+  using T = TcX3;
+};
 // decoded pixel storage: 12-bit alphabet (engine 3) in u16, else u8
 template <int PREC>
 using PixT = std::conditional_t<PREC == 3, uint16_t, uint8_t>;
@@ -117,17 +123,18 @@ __device__ __forceinline__ void load_smem(uint8_t* dst, const void* src, uint32_
 template <int PREC>
 __device__ __forceinline__ uint8_t* engine_setup(typename EngineSel<PREC>::T& eng, uint8_t* smem, const DevWeights& w,
                                                  uint64_t* bar, uint32_t* tslot, uint32_t w3d) {  // bar: 2 mbarriers
-  if constexpr (PREC >= 2) {  // P350K / P12: layer 1 | ring | biases | full[S] empty[S] (| dfull[2] dfree[2])
-    using Cfg = StreamCfg<PREC == 3>;
-    load_smem(smem + Cfg::L1, w.wimg, SL1_BYTES);
-    load_smem(smem + Cfg::BIASO, w.bias, Cfg::BIAS);
-    const uint32_t bars = smem_u32(smem + Cfg::BARS);
+  if constexpr (PREC >= 2) {  // streamed engines: layer 1 | ring | biases | full[S] empty[S] (| dfull[2] dfree[2])
+    using E = typename EngineSel<PREC>::T;
+    using Cfg = E;
+    load_smem(smem + E::L1_O, w.wimg, E::L1_BYTES);
+    load_smem(smem + E::BIAS_O, w.bias, E::BIAS_BYTES);
+    const uint32_t bars = smem_u32(smem + E::BARS_O);
     if (threadIdx.x < 32) tmem_alloc(smem_u32(tslot), TM_COLS);
     if (threadIdx.x == 0) {
       mbar_init(smem_u32(bar), 1);
       mbar_init(smem_u32(bar + 1), NTHREADS / 32);  // layer-1 input ready (row warps)
       for (int i = 0; i < 2 * Cfg::S; ++i) mbar_init(bars + 8u * (uint32_t)i, 1);
-      if constexpr (PREC == 3) {
+      if constexpr (E::HEAD) {
         for (int i = 0; i < 2; ++i) {
           mbar_init(bars + 8u * (2 * Cfg::S + i), 1);                 // dfull[b]: tcgen05.commit
           mbar_init(bars + 8u * (2 * Cfg::S + 2 + i), NTHREADS / 32);  // dfree[b]: the row warps
@@ -139,20 +146,20 @@ __device__ __forceinline__ uint8_t* engine_setup(typename EngineSel<PREC>::T& en
     __syncthreads();
     tc_fence_after();
     eng.tmem = *tslot;
-    eng.bias = reinterpret_cast<const float*>(smem + Cfg::BIASO);
+    eng.bias = reinterpret_cast<const float*>(smem + E::BIAS_O);
     eng.b0 = eng.bias;
     eng.bar = smem_u32(bar);
     eng.bar2 = eng.bar;
     eng.phase = 0;
-    eng.ring = smem_u32(smem + Cfg::RINGO);
-    eng.l1s = smem_u32(smem + Cfg::L1);
+    eng.ring = smem_u32(smem + E::RING_O);
+    eng.l1s = smem_u32(smem + E::L1_O);
     eng.full0 = bars;
     eng.empty0 = bars + 8u * Cfg::S;
     eng.dfull0 = bars + 8u * (2 * Cfg::S);
     eng.dfree0 = bars + 8u * (2 * Cfg::S + 2);
     eng.wstream = w.wimg;
     eng.aready = smem_u32(bar + 1);
-    return smem + Cfg::BYTES;
+    return smem + E::SMEM;
   } else if constexpr (PREC == 1) {
     load_smem(smem, w.wimg, WIMG_BYTES);
     load_smem(smem + WIMG_BYTES, w.bias, bias_bytes(w3d));
@@ -280,7 +287,7 @@ __global__ void __launch_bounds__(enc_block(PREC), 1)
       auto next = [&](int& c) -> bool {  // the 20 chunks of every tile's network, in order
         if (pt >= n) return false;
         c = pk;
-        if (++pk == (PREC == 3 ? CH_NET12 : CH_NET)) {
+        if (++pk == EngineSel<PREC>::T::CPN) {
           pk = 0;
           ++pt;
         }
@@ -418,7 +425,7 @@ __global__ void __launch_bounds__(enc_block(PREC), 1)
             const int cc = 64 * col_grp() + 32 * half_id() + i;
             float l = __uint_as_float(lv[i]);
             if constexpr (PREC == 1) l = __fadd_rn(l, eng.bias[BIAS_OFF_LAST + cc]);
-            if constexpr (PREC == 2) l = __fadd_rn(l, eng.bias[SB_LAST + cc]);
+            if constexpr (PREC == 2 || PREC == 4) l = __fadd_rn(l, eng.bias[EngineSel<PREC>::T::LAST_BIAS + cc]);
             dbg_logits[x.gi * NOUT + cc] = l;
           }
       }
@@ -1438,7 +1445,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         const uint32_t d = m - b < (uint32_t)ROWS ? 0u : ((b - m) & (NS - 1));
         return rlo + (int)d <= rhi;
       };
-      constexpr int CPN = PREC == 3 ? CH_NET12 : CH_NET;
+      constexpr int CPN = EngineSel<PREC>::T::CPN;
       constexpr int LA = EngineSel<PREC>::T::S - 1 < CPN ? EngineSel<PREC>::T::S - 1 : CPN;
       if (any_t(0))
         for (int k = 0; k < CPN; ++k) eng.produce_one(k);
@@ -1905,7 +1912,7 @@ cudaError_t launch_enc_mlp(const Plan& p, const DevWeights& w, const uint8_t* d_
   const uint32_t grid = (uint32_t)(total < (uint64_t)num_sms ? total : (uint64_t)num_sms);
   const size_t sm = enc_smem_bytes(p.engine, p.w3d);
   if (p.engine >= 2) {  // P350K / P12: streamed weights, one tile chain per CTA (+ debug exports)
-    auto kern = p.engine == 3 ? k_enc_mlp<3> : k_enc_mlp<2>;
+    auto kern = p.engine == 4 ? k_enc_mlp<4> : p.engine == 3 ? k_enc_mlp<3> : k_enc_mlp<2>;
     cudaError_t e = set_smem(kern, sm);
     if (e != cudaSuccess) return e;
     const bool prof = getenv("DLIC_PROF_STREAM") != nullptr;
@@ -1920,7 +1927,7 @@ cudaError_t launch_enc_mlp(const Plan& p, const DevWeights& w, const uint8_t* d_
       unsigned long long h[8];
       cudaMemcpyFromSymbolAsync(h, g_sprof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
-      const double ns = (double)h[4], cpn = p.engine == 3 ? CH_NET12 : CH_NET;
+      const double ns = (double)h[4], cpn = p.engine == 4 ? TcX3::CPN : p.engine == 3 ? CH_NET12 : CH_NET;
       fprintf(stderr, "[stream prof] per chunk (issuer, cycles): data wait %.0f  stage wait %.0f  epilogue wait %.0f  "
               "total %.0f  (chunks %llu) | per tile (row thread 0): feed %.0f network %.0f q1 %.0f\n", h[0] / ns,
               h[1] / ns, h[2] / ns, h[3] / ns, h[4], h[5] / (ns / cpn), h[6] / (ns / cpn), h[7] / (ns / cpn));
@@ -2045,6 +2052,7 @@ static int max_clusters_t(uint32_t nc, size_t sm) {
 }
 
 int dec_max_active_clusters(uint32_t engine, uint32_t nc, size_t smem) {
+  if (engine == 4) return max_clusters_t<4>(nc, smem);
   if (engine == 3) return max_clusters_t<3>(nc, smem);
   if (engine == 2) return max_clusters_t<2>(nc, smem);
   return engine == 1 ? max_clusters_t<1>(nc, smem) : max_clusters_t<0>(nc, smem);
@@ -2053,6 +2061,8 @@ int dec_max_active_clusters(uint32_t engine, uint32_t nc, size_t smem) {
 cudaError_t launch_decode(const Plan& p, const DevWeights& w, const uint8_t* d_bits, const uint64_t* d_cont_off,
                           const uint32_t* d_sbase, const uint32_t* d_slen, uint8_t* d_imgs, int32_t* d_status,
                           cudaStream_t st, unsigned long long* prof, uint32_t* d_sync) {
+  if (p.engine == 4)
+    return launch_decode_t<4, false>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof, d_sync);
   if (p.engine == 3)
     return launch_decode_t<3, false>(p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status, st, prof, d_sync);
   if (p.engine == 2) {

@@ -114,6 +114,12 @@ template <bool H12>
 struct TcStreamT {
   using Cfg = StreamCfg<H12>;
   static constexpr int S = Cfg::S;
+  // engine layout (shared by the streamed engines, see engine_setup)
+  static constexpr int CPN = H12 ? CH_NET12 : CH_NET;  // stream chunks per network
+  static constexpr uint32_t L1_BYTES = SL1_BYTES, L1_O = Cfg::L1, RING_O = Cfg::RINGO;
+  static constexpr uint32_t BIAS_O = Cfg::BIASO, BIAS_BYTES = Cfg::BIAS, BARS_O = Cfg::BARS, SMEM = Cfg::BYTES;
+  static constexpr bool HEAD = H12;     // dfull/dfree barriers of the 12-bit head
+  static constexpr int LAST_BIAS = SB_LAST;
   uint32_t tmem;
   const float* bias;       // shared
   const float* b0;         // layer-1 biases (shared)
