@@ -1066,8 +1066,7 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
                             "barrier"};
       fprintf(stderr, "[dlic prof] cycles per front per CTA:");
       for (int k = 0; k < 11; ++k) fprintf(stderr, " %s %.0f", nm[k], hp[k] / ctas / T);
-      fprintf(stderr, "\n[dlic prof] network per front (sum over layers): sync %.0f issue+hook %.0f mma-wait %.0f "
-              "epilogue %.0f\n", hp[16] / ctas / T, hp[17] / ctas / T, hp[18] / ctas / T, hp[19] / ctas / T);
+      fprintf(stderr, "\n[dlic prof] sub-phases (pass1 for bf16 decode): ld32 %.0f early-signal %.0f s1a %.0f s1b+s1c %.0f\n", hp[16] / ctas / T, hp[17] / ctas / T, hp[18] / ctas / T, hp[19] / ctas / T);
       if (p.precision == 1)
         fprintf(stderr, "[dlic prof] issuer per front: network issue %.0f  arrive->layer-1 issued %.0f  cluster wait %.0f\n",
                 hp[26] / ctas / T, hp[27] / ctas / T, hp[28] / ctas / T);

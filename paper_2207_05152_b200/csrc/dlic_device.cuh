@@ -45,6 +45,10 @@ constexpr float Q1_SCALE = 65279.0f;  // 2^16 - 257 (R5, Q1')
 #ifndef DLIC_POLY_FROM
 #define DLIC_POLY_FROM 6
 #endif
+// thread whose clock profile the DLIC_PROF decoder records (a row thread)
+#ifndef DLIC_PROF_TID
+#define DLIC_PROF_TID 32
+#endif
 // Arithmetic revision of the density estimator + softmax/Q1' (container
 // header field "numerics"): the integer tables are a function of the exact
 // instruction sequence (engine K order, layer-1 split, epilogue rounding, the
@@ -1153,8 +1157,10 @@ __device__ __forceinline__ Q1Row q1_table(const Eng& e, uint32_t (&v)[32], int s
                                           float* probs, Prof* pf = nullptr) {
   Q1Work<ENC> w;
   w.s1a(e, v);
+  if (pf) pf->mark2(2);
   w.template s1b<0, 16>(v);
   w.s1c();
+  if (pf) pf->mark2(3);
   if (pf) pf->mark(4);
   w.x1(e);
   if (pf) pf->mark(5);
@@ -1225,7 +1231,9 @@ __device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot_u, bool& mi
   float fs, csl;
   uint32_t v[32];
   e.ld32(v);
+  if (pf) pf->mark2(0);
   mid();
+  if (pf) pf->mark2(1);
   const Q1Row r = q1_table<false>(e, v, -1, fs, csl, nullptr, pf);
   const float slot = (float)slot_u;
   const int c0 = 64 * col_grp() + 32 * half_id();

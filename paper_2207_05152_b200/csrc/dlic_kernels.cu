@@ -47,7 +47,7 @@ constexpr uint32_t RING_BANK = (uint32_t)RING_COLS * RING_ROWS;  // 2880
 constexpr uint32_t RING_BYTES = 2u * RING_BANK;               // 5760
 constexpr uint32_t F32_BUF_BYTES = (NOUT + HID) * ROWS * 4u;          // 98304
 constexpr uint32_t F32_X_BYTES = NXSLOT * NGRP * ROWS * 4u;          // 7168
-constexpr uint32_t MAX_DYN_SMEM = 232448 - 1024;                     // 227 KB minus static (k_decode: 896 B)
+constexpr uint32_t MAX_DYN_SMEM = 232448 - 2048;                     // 227 KB minus static (fallback, see dec_smem_limit)
 
 // bias region in shared memory: biases + fresh-tap table (+ the 3D taps'
 // weights for volume plans)
@@ -68,7 +68,10 @@ size_t dec_smem_bytes(uint32_t precision, uint32_t max_groups, uint32_t w3d) {
   return enc_smem_bytes(precision, w3d) + RING_BYTES * (precision == 3 ? 2u : 1u) + 16 + 3 * cursor_bytes(max_groups) +
          (w3d && precision == 1 ? T3_BYTES : 0u);  // (engine index, see enc_smem_bytes)
 }
-size_t dec_smem_limit() { return MAX_DYN_SMEM; }
+// dynamic shared memory a decoder block may use: the device's opt-in limit
+// per block minus k_decode's static shared memory (queried once; the
+// constant is the fallback when no device is visible)
+size_t dec_smem_limit();
 
 // ------------------------------------------------------------ engine setup
 template <int PREC>
@@ -1160,7 +1163,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
   // optional phase profile (thread 0 of each CTA), see Prof in dlic_device.cuh:
   // 0 top 1 gather 2 put 3 mlp 4 pass1 5 exchanges 6 pass2 7 passA 8 search 9 rans 10 barrier
   Prof pf;
-  pf.on = PROF && threadIdx.x == 32;  // a row thread
+  pf.on = PROF && threadIdx.x == DLIC_PROF_TID;  // a row thread
   const uint32_t rank = NC > 1 ? cluster_rank() : 0u;
   // Volumes (3D wavefront): the unit of slice z waits for the same
   // unit of slice z-1, so units are handed out in order through a ticket:
@@ -2024,6 +2027,22 @@ static cudaError_t launch_decode_t(const Plan& p, const DevWeights& w, const uin
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, p, w, d_bits, d_cont_off, d_sbase, d_slen, d_imgs, d_status,
                             prof, d_sync);
+}
+
+size_t dec_smem_limit() {
+  static size_t lim = 0;
+  if (!lim) {
+    int dev = 0, optin = 0;
+    cudaFuncAttributes fa = {};
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess &&
+        cudaFuncGetAttributes(&fa, k_decode<1, false, false>) == cudaSuccess && optin > (int)fa.sharedSizeBytes)
+      lim = (size_t)optin - fa.sharedSizeBytes;
+    else
+      lim = MAX_DYN_SMEM;
+    cudaGetLastError();
+  }
+  return lim;
 }
 
 template <int PREC>
