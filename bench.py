@@ -220,7 +220,7 @@ def images_for(args, rank, n):
     if cfg == "C1":
         return np.stack([synth.gradient_noise(32, 32, seed=rank * 1000 + i) for i in range(n)])
     if cfg == "C2":
-        return np.stack([synth.natural_like(768, 512, seed=rank * 1000 + i) for i in range(n)])
+        return np.stack([synth.c2_image(seed=rank * 1000 + i) for i in range(n)])
     if cfg == "C3":
         return synth.mri_like_slices(n, 256, seed0=rank * 100)
     if cfg == "C4":

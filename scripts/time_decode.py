@@ -1,5 +1,6 @@
-"""Decode-kernel time of one or more libdlic.so builds (A/B across commits or
-experimental variants; no correctness assertion beyond a lossless flag).
+"""Decode-kernel (or, with TIME_WHAT=mlp, encoder-MLP) time of one or more
+libdlic.so builds (A/B across commits or experimental variants; no
+correctness assertion beyond a lossless flag).
 Uses its own minimal ctypes calls (dlic_model_load / dlic_encode /
 dlic_decode / dlic_last_kernel_ms), which every build since round 1 exports.
 python scripts/time_decode.py [C2|C3|C4|C5] lib.so ..."""
@@ -32,7 +33,12 @@ for i in range(8):
     st = lib.dlic_decode(m, bits, len(bits), dec.ctypes.data, dec.size)
     ok = ok and st == 0 and bool((dec == img).all())
     ts.append(lib.dlic_last_kernel_ms(b"decode"))
-print(json.dumps({"decode_ms": sorted(ts)[len(ts)//2], "ok": ok}))
+tm = []
+for i in range(5):
+    assert lib.dlic_encode(m, img.ctypes.data, w, h, w, opts, ctypes.byref(out), ctypes.byref(n)) == 0
+    ok = ok and ctypes.string_at(out, n.value) == bits
+    tm.append(lib.dlic_last_kernel_ms(b"mlp"))
+print(json.dumps({"decode_ms": sorted(ts)[len(ts)//2], "mlp_ms": sorted(tm)[len(tm)//2], "ok": ok}))
 '''
 args = sys.argv[1:]
 cfg = "C2"

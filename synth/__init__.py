@@ -12,6 +12,7 @@ span ~1e4x (P:192, Fig. 5).
 from .images import (  # noqa: F401
     gradient_noise,
     natural_like,
+    c2_image,
     mri_like_volume,
     mri_like_slices,
     random_image,

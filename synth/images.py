@@ -134,6 +134,20 @@ CONFIGS = {
 }
 
 
+# C2's texture and noise levels: chosen so that the trained P100K fixture's
+# information content on the C2 image lies inside the paper's photo range of
+# 3.53-4.27 bpp (Table I): 3.77 bits/px on its top-left 384x256
+# (oracle fp64 network, -log2 p of the true symbol); the generator's defaults
+# (texture 2, noise 1) give 2.81 there.
+C2_SIGMA_TEX = 3.0
+C2_SIGMA_N = 2.0
+
+
+def c2_image(seed: int = 0) -> np.ndarray:
+    """The C2 768x512 photo stand-in (natural_like at C2's texture/noise levels)."""
+    return natural_like(768, 512, seed=seed, sigma_tex=C2_SIGMA_TEX, sigma_n=C2_SIGMA_N)
+
+
 def config_images(name: str, count: int | None = None, seed0: int | None = None) -> np.ndarray:
     """(n, H, W) u8 images for config C1..C5 (optionally only the first `count`)."""
     cfg = CONFIGS[name]
@@ -142,7 +156,7 @@ def config_images(name: str, count: int | None = None, seed0: int | None = None)
         return gradient_noise(32, 32, seed=0 if seed0 is None else seed0)[None]
     if name == "C2":
         s0 = 0 if seed0 is None else seed0
-        return np.stack([natural_like(768, 512, seed=s0 + i) for i in range(n)])
+        return np.stack([c2_image(seed=s0 + i) for i in range(n)])
     if name == "C3":
         return mri_like_slices(n, 256, seed0=0 if seed0 is None else seed0)
     if name == "C4":
