@@ -45,6 +45,10 @@ constexpr float Q1_SCALE = 65279.0f;  // 2^16 - 257 (R5, Q1')
 #ifndef DLIC_POLY_FROM
 #define DLIC_POLY_FROM 6
 #endif
+// 12-bit head (q12_row): column pairs on the FMA-pipe polynomial, of 8
+#ifndef DLIC_Q12_POLY
+#define DLIC_Q12_POLY 0
+#endif
 // thread whose clock profile the DLIC_PROF decoder records (a row thread)
 #ifndef DLIC_PROF_TID
 #define DLIC_PROF_TID 32
@@ -57,8 +61,8 @@ constexpr float Q1_SCALE = 65279.0f;  // 2^16 - 257 (R5, Q1')
 // the exp split is folded in so that a -DDLIC_POLY_FROM variant build can never
 // decode another build's containers.  Value 0 is reserved for the oracle's own
 // arithmetic (fp64 / bf16-emulated network, fp64 softmax).
-constexpr uint32_t NUMERICS_BASE = 2;  // 2: fp32 path on the tensor cores (bf16x3)
-constexpr uint32_t NUMERICS_REV = (NUMERICS_BASE << 8) | (uint32_t)DLIC_POLY_FROM;
+constexpr uint32_t NUMERICS_BASE = 3;  // 2: fp32 path on the tensor cores (bf16x3); 3: packed 12-bit head (fma exp arguments)
+constexpr uint32_t NUMERICS_REV = (NUMERICS_BASE << 8) | (uint32_t)DLIC_POLY_FROM | ((uint32_t)DLIC_Q12_POLY << 4);
 
 // Layer-1 K order of the bf16 engine.  K position p = 10u + i belongs to
 // thread u = 2j + h (column group j, half h), which feeds A packed columns

@@ -416,63 +416,84 @@ using TcStream12 = TcStreamT<true>;
 // One pixel row = 8 threads (group j, half h); thread t = 2j + h owns the
 // columns [32j + 16h, +16) of every 128-column chunk q, i.e. symbols
 // 128q + 32j + 16h + i.  Reading R17 on the GPU (the same routine in the
-// encoder and the decoder, R8):
-//   pass 1 (online): per chunk l_i = acc_i + b_i (fp32 RN), c = max of the
-//     16, m' = max(m, c), z = z * 2^((m - m') log2e) + sum_i 2^((l_i - m') log2e)
-//     (MUFU ex2.approx, fixed pair tree); then halves (h = 0 term first) and
-//     groups (((z0 w0 + z1 w1) + z2 w2) + z3 w3, w_g = 2^((m_g - M) log2e))
+// encoder and the decoder, R8), in packed fp32 pairs (f32x2, each lane IEEE
+// RN like the scalar instruction):
+//   e(x; M) = ex2.approx(fma(x, log2e, -M log2e))
+//   pass 1 (online): per chunk l_i = acc_i + b_i, c = max of the 16 (exact in
+//     any order), m' = max(m, c), z = z e(m; m') + s with s the pair tree
+//     ((e_0 + e_1) + (e_2 + e_3)) + ((e_4 + e_5) + (e_6 + e_7)) over the 8
+//     column pairs (lanes summed last: s = s.x + s.y); then halves (h = 0
+//     term first) and groups (((z0 w0 + z1 w1) + z2 w2) + z3 w3, w_g = e(m_g; M))
 //     combine to M, Z; r = rcp_rn(Z);
-//   pass 2: p_i = 2^((l_i - M) log2e) * r, f_i = 1 + floor(p_i * 61376)
-//     (fp32 RN products), the row's running cumulative through one exchange
-//     per chunk; symbol 4095 takes f = 2^16 - c_4095 (the residual, R17).
-// ENC: key = the true symbol -> (f_s, c_s) at the owning thread (mine);
-// decode: key = the slot -> the symbol s with c_s <= slot < c_s + f_s.
+//   pass 2: p_i = e(l_i; M) r, f_i = 1 + floor(p_i 61376) (RN product, the
+//     floor by a round-toward-minus-infinity add of 2^23), the row's running
+//     cumulative through one exchange of the groups' chunk sums per chunk;
+//     symbol 4095 takes f = 2^16 - c_4095 (the residual, R17).  Only the
+//     thread whose range [c, c + sum of its 16 f) holds the key scans its
+//     columns (decode: the slot; encode: the true symbol's column).
 // mid() runs once the last chunk is loaded (the accumulator is free).
 struct Q12Dbg {
   float* logits;   // [4096] of this row or null
   float* probs;
   uint16_t* freqs;
 };
-__device__ __forceinline__ float q12_e(float l, float m) {
-  return ex2_approx(__fmul_rn(__fsub_rn(l, m), 1.4426950408889634f));
+__device__ __forceinline__ float q12_e(float x, float nml) { return ex2_approx(__fmaf_rn(x, LOG2E, nml)); }
+// pairs i >= 8 - DLIC_Q12_POLY of each thread's 8 column pairs take the
+// FMA-pipe polynomial (f2_exp2_poly) instead of MUFU ex2 (fixed per column)
+__device__ __forceinline__ f2 q12_e2(f2 l, f2 l2e, f2 nml, int i) {
+  const f2 t = f2_fma(l, l2e, nml);
+  if (i >= 8 - DLIC_Q12_POLY) return f2_exp2_poly(t);
+  float t0, t1;
+  f2_split(t, t0, t1);
+  return f2_make(ex2_approx(t0), ex2_approx(t1));
 }
 template <bool ENC, class Mid>
 __device__ __forceinline__ int q12_row(TcStream12& e, uint32_t key, bool& mine_out, uint32_t& fs_out,
                                        uint32_t& cs_out, Mid&& mid, const Q12Dbg* dbg = nullptr) {
   const int j = col_grp(), h = half_id();
   const int cb = 32 * j + 16 * h;
-  const float* hb = e.bias + SB12_HEAD + cb;
+  const float2* hb2 = reinterpret_cast<const float2*>(e.bias + SB12_HEAD + cb);
+  const f2 l2e = f2_splat(LOG2E);
   // ---- pass 1
   float m = -INFINITY, z = 0.0f;
 #pragma unroll 1
   for (uint32_t q = 0; q < (uint32_t)H12_NCH; ++q) {
     uint32_t v[16];
     e.head_ld(q, v);
-    float l[16];
+    f2 l[8];
+    float a[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) l[i] = __fadd_rn(__uint_as_float(v[i]), hb[H12_CN * q + i]);
+    for (int i = 0; i < 8; ++i) {
+      const float2 b = hb2[(H12_CN / 2) * q + i];
+      l[i] = f2_add(f2_bits(v[2 * i], v[2 * i + 1]), f2_make(b.x, b.y));
+      f2_split(l[i], a[2 * i], a[2 * i + 1]);
+    }
     if (dbg && dbg->logits) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) dbg->logits[H12_CN * q + cb + i] = l[i];
+      for (int i = 0; i < 16; ++i) dbg->logits[H12_CN * q + cb + i] = a[i];
     }
-    float c8[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) c8[i] = fmaxf(l[2 * i], l[2 * i + 1]);
-    const float c = fmaxf(fmaxf(fmaxf(c8[0], c8[1]), fmaxf(c8[2], c8[3])), fmaxf(fmaxf(c8[4], c8[5]), fmaxf(c8[6], c8[7])));
+    const float c = fmax3(fmax3(fmax3(a[0], a[1], a[2]), fmax3(a[3], a[4], a[5]), fmax3(a[6], a[7], a[8])),
+                          fmax3(a[9], a[10], a[11]), fmax3(fmax3(a[12], a[13], a[14]), a[15], -INFINITY));
     const float mn = fmaxf(m, c);
-    float s8[8];
+    const float nml = __fmul_rn(-mn, LOG2E);
+    const f2 nml2 = f2_splat(nml);
+    f2 ex[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) s8[i] = __fadd_rn(q12_e(l[2 * i], mn), q12_e(l[2 * i + 1], mn));
-    const float s = __fadd_rn(__fadd_rn(__fadd_rn(s8[0], s8[1]), __fadd_rn(s8[2], s8[3])),
-                              __fadd_rn(__fadd_rn(s8[4], s8[5]), __fadd_rn(s8[6], s8[7])));
-    z = __fadd_rn(q > 0 ? __fmul_rn(z, q12_e(m, mn)) : 0.0f, s);
+    for (int i = 0; i < 8; ++i) ex[i] = q12_e2(l[i], l2e, nml2, i);
+    const f2 s2 = f2_add(f2_add(f2_add(ex[0], ex[1]), f2_add(ex[2], ex[3])),
+                         f2_add(f2_add(ex[4], ex[5]), f2_add(ex[6], ex[7])));
+    float sx, sy;
+    f2_split(s2, sx, sy);
+    const float s = __fadd_rn(sx, sy);
+    z = __fadd_rn(q > 0 ? __fmul_rn(z, q12_e(m, nml)) : 0.0f, s);
     m = mn;
   }
   // halves: the h = 0 term first on both lanes
   const float mo = __shfl_xor_sync(0xFFFFFFFFu, m, 16), zo = __shfl_xor_sync(0xFFFFFFFFu, z, 16);
   const float m_lo = h ? mo : m, m_hi = h ? m : mo, z_lo = h ? zo : z, z_hi = h ? z : zo;
   const float m2 = fmaxf(m_lo, m_hi);
-  const float z2 = __fadd_rn(__fmul_rn(z_lo, q12_e(m_lo, m2)), __fmul_rn(z_hi, q12_e(m_hi, m2)));
+  const float nm2 = __fmul_rn(-m2, LOG2E);
+  const float z2 = __fadd_rn(__fmul_rn(z_lo, q12_e(m_lo, nm2)), __fmul_rn(z_hi, q12_e(m_hi, nm2)));
   e.xput(0, __float_as_uint(m2));
   e.xput(1, __float_as_uint(z2));
   e.xsync();
@@ -481,11 +502,14 @@ __device__ __forceinline__ int q12_row(TcStream12& e, uint32_t key, bool& mine_o
   e.xget4(1, zz);
   const float M = fmaxf(fmaxf(__uint_as_float(mm[0]), __uint_as_float(mm[1])),
                         fmaxf(__uint_as_float(mm[2]), __uint_as_float(mm[3])));
-  float Z = __fmul_rn(__uint_as_float(zz[0]), q12_e(__uint_as_float(mm[0]), M));
+  const float nM = __fmul_rn(-M, LOG2E);
+  float Z = __fmul_rn(__uint_as_float(zz[0]), q12_e(__uint_as_float(mm[0]), nM));
 #pragma unroll
-  for (int g = 1; g < NGRP; ++g) Z = __fadd_rn(Z, __fmul_rn(__uint_as_float(zz[g]), q12_e(__uint_as_float(mm[g]), M)));
+  for (int g = 1; g < NGRP; ++g) Z = __fadd_rn(Z, __fmul_rn(__uint_as_float(zz[g]), q12_e(__uint_as_float(mm[g]), nM)));
   const float rz = __frcp_rn(Z);
   // ---- pass 2
+  const f2 nM2 = f2_splat(nM), rz2 = f2_splat(rz), sc2 = f2_splat(Q12_SCALE);
+  const f2 two23 = f2_splat(8388608.0f), fbias = f2_splat(-8388607.0f);  // y - 2^23 + 1 = 1 + floor(x), exact
   float base = 0.0f;  // cumulative frequency before the current chunk (exact integers)
   bool mine = false;
   uint32_t fs = 0, cs = 0;
@@ -496,19 +520,26 @@ __device__ __forceinline__ int q12_row(TcStream12& e, uint32_t key, bool& mine_o
     uint32_t v[16];
     e.head_ld(H12_NCH + q, v);
     if (q == H12_NCH - 1) mid();
-    float f[16];
-    float S = 0.0f;
+    f2 f[8];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const float l = __fadd_rn(__uint_as_float(v[i]), hb[H12_CN * q + i]);
-      const float p = __fmul_rn(q12_e(l, M), rz);
-      f[i] = 1.0f + floorf(__fmul_rn(p, Q12_SCALE));
-      S += f[i];  // integers < 2^24: exact in any order
-      if (dbg && dbg->probs) dbg->probs[H12_CN * q + cb + i] = p;
+    for (int i = 0; i < 8; ++i) {
+      const float2 b = hb2[(H12_CN / 2) * q + i];
+      const f2 l = f2_add(f2_bits(v[2 * i], v[2 * i + 1]), f2_make(b.x, b.y));
+      const f2 p = f2_mul(q12_e2(l, l2e, nM2, i), rz2);
+      f[i] = f2_add(f2_add_rm(f2_mul(p, sc2), two23), fbias);
+      if (dbg && dbg->probs) {
+        float p0, p1;
+        f2_split(p, p0, p1);
+        dbg->probs[H12_CN * q + cb + 2 * i] = p0;
+        dbg->probs[H12_CN * q + cb + 2 * i + 1] = p1;
+      }
     }
+    const f2 S2 = f2_add(f2_add(f2_add(f[0], f[1]), f2_add(f[2], f[3])), f2_add(f2_add(f[4], f[5]), f2_add(f[6], f[7])));
+    float Sx, Sy;
+    f2_split(S2, Sx, Sy);
+    const float S = Sx + Sy;  // integers < 2^24: exact in any order
     const float So = __shfl_xor_sync(0xFFFFFFFFu, S, 16);
-    const float Sj = S + So;  // this group's part of the chunk
-    e.xput(2 + (int)(q & 1u), __float_as_uint(Sj));
+    e.xput(2 + (int)(q & 1u), __float_as_uint(S + So));  // this group's part of the chunk
     e.xsync();
     uint32_t g4[4];
     e.xget4(2 + (int)(q & 1u), g4);
@@ -519,21 +550,29 @@ __device__ __forceinline__ int q12_row(TcStream12& e, uint32_t key, bool& mine_o
       pre += g < j ? G : 0.0f;
       tot += G;
     }
-    float c = base + pre + (h ? So : 0.0f);  // cumulative before my first column
+    const float c0 = base + pre + (h ? So : 0.0f);  // cumulative before my first column
     const bool last = q == H12_NCH - 1 && j == NGRP - 1 && h == 1;  // my column 15 is symbol 4095
+    const int s0 = (int)(H12_CN * q) + cb;
+    const bool scan = (dbg && dbg->freqs) ||
+                      (ENC ? ((int)key >= s0 && (int)key < s0 + 16) : (keyf >= c0 && (last || keyf < c0 + S)));
+    if (scan) {
+      float fv[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int s_i = (int)(H12_CN * q) + cb + i;
-      const float fi = (last && i == 15) ? 65536.0f - c : f[i];
-      if (dbg && dbg->freqs) dbg->freqs[s_i] = (uint16_t)fi;
-      const bool hit = ENC ? (s_i == (int)key) : (!mine && keyf >= c && keyf < c + fi);
-      if (hit) {
-        mine = true;
-        sym = s_i;
-        fs = (uint32_t)fi;
-        cs = (uint32_t)c;
+      for (int i = 0; i < 8; ++i) f2_split(f[i], fv[2 * i], fv[2 * i + 1]);
+      float c = c0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float fi = (last && i == 15) ? 65536.0f - c : fv[i];
+        if (dbg && dbg->freqs) dbg->freqs[s0 + i] = (uint16_t)fi;
+        const bool hit = ENC ? (s0 + i == (int)key) : (!mine && keyf >= c && keyf < c + fi);
+        if (hit) {
+          mine = true;
+          sym = s0 + i;
+          fs = (uint32_t)fi;
+          cs = (uint32_t)c;
+        }
+        c += fi;
       }
-      c += fi;
     }
     base += tot;
   }
