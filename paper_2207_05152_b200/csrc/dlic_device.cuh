@@ -45,6 +45,15 @@ constexpr float Q1_SCALE = 65279.0f;  // 2^16 - 257 (R5, Q1')
 #ifndef DLIC_POLY_FROM
 #define DLIC_POLY_FROM 6
 #endif
+// the same for column groups 2-3 (logits [128, 256), the decoder's later half)
+#ifndef DLIC_POLY_FROM_HI
+#define DLIC_POLY_FROM_HI DLIC_POLY_FROM
+#endif
+// group max in s1a as a 3-input tree (1) or the sequential chain (0); exact
+// either way
+#ifndef DLIC_MAX_TREE
+#define DLIC_MAX_TREE 0
+#endif
 // 12-bit head (q12_row): column pairs on the FMA-pipe polynomial, of 8
 #ifndef DLIC_Q12_POLY
 #define DLIC_Q12_POLY 0
@@ -62,7 +71,8 @@ constexpr float Q1_SCALE = 65279.0f;  // 2^16 - 257 (R5, Q1')
 // decode another build's containers.  Value 0 is reserved for the oracle's own
 // arithmetic (fp64 / bf16-emulated network, fp64 softmax).
 constexpr uint32_t NUMERICS_BASE = 3;  // 2: fp32 path on the tensor cores (bf16x3); 3: packed 12-bit head (fma exp arguments)
-constexpr uint32_t NUMERICS_REV = (NUMERICS_BASE << 8) | (uint32_t)DLIC_POLY_FROM | ((uint32_t)DLIC_Q12_POLY << 4);
+constexpr uint32_t NUMERICS_REV = (NUMERICS_BASE << 8) | (uint32_t)DLIC_POLY_FROM | ((uint32_t)DLIC_Q12_POLY << 4) |
+                                   (DLIC_POLY_FROM_HI != DLIC_POLY_FROM ? (uint32_t)DLIC_POLY_FROM_HI << 12 : 0u);
 
 // Layer-1 K order of the bf16 engine.  K position p = 10u + i belongs to
 // thread u = 2j + h (column group j, half h), which feeds A packed columns
@@ -1023,7 +1033,16 @@ struct Q1Work {
       f2_split(f2_add(f2_bits(v[2 * q], v[2 * q + 1]), f2_make(b.x, b.y)), l0, l1);
       v[2 * q] = __float_as_uint(l0);
       v[2 * q + 1] = __float_as_uint(l1);
-      mm = fmax3(mm, l0, l1);
+      if (!DLIC_MAX_TREE) mm = fmax3(mm, l0, l1);
+    }
+    if (DLIC_MAX_TREE) {
+      float t1[11];
+#pragma unroll
+      for (int i = 0; i < 10; ++i)
+        t1[i] = fmax3(__uint_as_float(v[3 * i]), __uint_as_float(v[3 * i + 1]), __uint_as_float(v[3 * i + 2]));
+      t1[10] = fmaxf(__uint_as_float(v[30]), __uint_as_float(v[31]));
+      mm = fmax3(fmax3(fmax3(t1[0], t1[1], t1[2]), fmax3(t1[3], t1[4], t1[5]), fmax3(t1[6], t1[7], t1[8])), t1[9],
+                 t1[10]);
     }
     m = fmaxf(mm, __shfl_xor_sync(0xFFFFFFFFu, mm, 16));  // m_j, equal in both halves
     zz = f2_splat(0.0f);
@@ -1032,11 +1051,12 @@ struct Q1Work {
   __device__ __forceinline__ void s1b(uint32_t (&v)[32]) {
     const f2 nm = f2_splat(__fmul_rn(-m, LOG2E));
     const f2 l2e = f2_splat(LOG2E);
+    const int pfrom = col_grp() < 2 ? DLIC_POLY_FROM : DLIC_POLY_FROM_HI;  // (warp-uniform)
 #pragma unroll
     for (int q = Q0; q < Q1; ++q) {
       const f2 t = f2_fma(f2_bits(v[2 * q], v[2 * q + 1]), l2e, nm);
       float e0, e1;
-      if (q % 8 >= DLIC_POLY_FROM) {  // 4 of 16 pairs on the FMA pipe, the rest on MUFU
+      if (q % 8 >= pfrom) {  // 4 of 16 pairs on the FMA pipe, the rest on MUFU (DLIC_POLY_FROM)
         f2_split(f2_exp2_poly(t), e0, e1);
       } else {
         float t0, t1;
@@ -1229,8 +1249,8 @@ __device__ __forceinline__ uint32_t q1_encode(const Eng& e, int sym, float* prob
 // Search: 8-entry block sums from pass A pick the block, a reverse scan of its
 // 8 entries with the monotone test slot < c_{i+1} finds s.  mid() runs (all
 // threads) once the logits are loaded: the network's TMEM output is free.
-template <class Eng, class Mid>
-__device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot_u, bool& mine_out, uint32_t& fs_out,
+template <class Eng, class Slot, class Mid>
+__device__ __forceinline__ int q1_decode(const Eng& e, Slot&& slot_fn, bool& mine_out, uint32_t& fs_out,
                                          uint32_t& cs_out, Mid&& mid, Prof* pf = nullptr) {
   float fs, csl;
   uint32_t v[32];
@@ -1239,7 +1259,7 @@ __device__ __forceinline__ int q1_decode(const Eng& e, uint32_t slot_u, bool& mi
   mid();
   if (pf) pf->mark2(1);
   const Q1Row r = q1_table<false>(e, v, -1, fs, csl, nullptr, pf);
-  const float slot = (float)slot_u;
+  const float slot = (float)slot_fn();  // the row's rANS slot (may wait for the rANS warp)
   const int c0 = 64 * col_grp() + 32 * half_id();
   const float base = q1_base(r);
   const bool last = c0 == NOUT - 32;  // symbol 255 carries the residual R

@@ -30,6 +30,13 @@
 
 namespace dlic {
 
+// decoder: the rANS warp publishes a front's slots on an mbarrier that each
+// row thread waits on right before its symbol search (1), or on named barrier
+// 7 that all 16 row warps sync on after the network (0)
+#ifndef DLIC_SLOT_MBAR
+#define DLIC_SLOT_MBAR 1
+#endif
+
 // Decoded-pixel ring, column-major so the 32 lanes of a warp (consecutive
 // rows) touch distinct shared-memory banks: byte (bank, pos, ringrow) at
 // bank*RING_BANK + pos*RING_ROWS + ringrow.  ringrow = 8 + slot-in-CTA; rows
@@ -1156,6 +1163,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
   __shared__ uint32_t s_tick;   // 3D: this cluster's unit ticket (rank 0's copy is authoritative)
   __shared__ uint32_t s_lower;  // 3D: steps the slice below has published (a lower bound)
   __shared__ uint32_t s_slot[ROWS];  // the row's rANS slot x & 0xFFFF (rANS warp -> the row's 8 threads)
+  __shared__ uint64_t s_sbar;        // DLIC_SLOT_MBAR: front t's slots published (phase t)
   __shared__ uint2 s_res[ROWS];      // (f_s, c_s) of the decoded symbol (finder -> rANS warp, next front)
   const uint32_t lane = lane_id();
   const uint32_t NC = p.nc, NS = ROWS * NC;
@@ -1222,6 +1230,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
   if (threadIdx.x == 0) {
     mbar_init(a_ready, NTHREADS / 32);
     mbar_init(smem_u32(&bar[2]), 1);  // second MMA-completion barrier (DEC_NSPLIT)
+    mbar_init(smem_u32(&s_sbar), 1);  // the rANS warp's lane 0, once per front
     fence_mbar_init();
   }
   if (NC > 1) cluster_sync_all();
@@ -1409,7 +1418,12 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         }
         s_slot[32 * hf + lane] = xs[hf] & 0xFFFFu;
       }
-      asm volatile("bar.arrive 7, %0;" ::"n"(DEC_THREADS) : "memory");  // slots of front t published
+      if constexpr (DLIC_SLOT_MBAR) {  // slots of front t published
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&s_sbar));
+      } else {
+        asm volatile("bar.arrive 7, %0;" ::"n"(DEC_THREADS) : "memory");
+      }
       if constexpr (W3D && PREC == 1) {
         if (t + 1 < T) fill_t3(t + 1);
       }
@@ -1731,13 +1745,20 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
           }, PROF ? &pf : nullptr);
         }
         pf.mark(3);
-        asm volatile("bar.sync 7, %0;" ::"n"(DEC_THREADS) : "memory");  // this front's slots (rANS warp)
+        // this front's slot of my row (the rANS warp's): DLIC_SLOT_MBAR waits
+        // for it only at the symbol search, so the column groups whose
+        // logits land first start their softmax at once
+        auto my_slot = [&]() -> uint32_t {
+          if constexpr (DLIC_SLOT_MBAR) mbar_wait(smem_u32(&s_sbar), (uint32_t)t & 1u);
+          return s_slot[row];
+        };
+        if (!DLIC_SLOT_MBAR || PREC == 3) asm volatile("bar.sync 7, %0;" ::"n"(DEC_THREADS) : "memory");
         pf.mark(6);  // profile: time spent waiting for the rANS warp's slots
         uint32_t fs, cs;
         bool mine;
         int sym;
-        if constexpr (PREC == 3) sym = q12_row<false>(eng, s_slot[row], mine, fs, cs, [&]() { early_signal(rn, cn); });
-        else sym = q1_decode(eng, s_slot[row], mine, fs, cs, [&]() { early_signal(rn, cn); }, &pf);
+        if constexpr (PREC == 3) sym = q12_row<false>(eng, my_slot(), mine, fs, cs, [&]() { early_signal(rn, cn); });
+        else sym = q1_decode(eng, my_slot, mine, fs, cs, [&]() { early_signal(rn, cn); }, &pf);
         // the thread that found the symbol publishes it: own ring, the
         // successor's halo through DSMEM for the CTA's last 8 rows, zero
         // pads, and (f_s, c_s) for the rANS warp (applied next front)
@@ -1791,7 +1812,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         }
         pf.mark(9);
       } else {
-        asm volatile("bar.sync 7, %0;" ::"n"(DEC_THREADS) : "memory");  // keep the barrier in step
+        if (!DLIC_SLOT_MBAR || PREC == 3) asm volatile("bar.sync 7, %0;" ::"n"(DEC_THREADS) : "memory");  // in step
         if (optr) *optr = (Pix)opix;
         if constexpr (W3D && PREC == 0) load_lower(rn, cn, active_n, t + 6);
         early_gather(rn, cn);
