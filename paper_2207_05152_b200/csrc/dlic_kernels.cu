@@ -1202,7 +1202,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
   constexpr int BITS = pix_bits<PREC>();
   typename EngineSel<PREC>::T eng;
   Pix* ring = reinterpret_cast<Pix*>(engine_setup<PREC>(eng, smem, w, bar, &tslot, p.w3d));
-  if constexpr (PREC == 1) eng.bar2 = smem_u32(&bar[2]);  // (TcStream: no half-layer split)
+  if constexpr (PREC != 0 && PREC != 3) eng.bar2 = smem_u32(&bar[2]);  // the decoder's logits halves
   if (w.b1img) {  // the unit's image's metadata-folded layer-1 bias
     if constexpr (PREC == 1) {
       __syncthreads();  // engine_setup's bias copy is complete
@@ -1418,7 +1418,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         }
         s_slot[32 * hf + lane] = xs[hf] & 0xFFFFu;
       }
-      if constexpr (DLIC_SLOT_MBAR) {  // slots of front t published
+      if constexpr (DLIC_SLOT_MBAR && PREC != 3) {  // slots of front t published (12-bit: named barrier 7)
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&s_sbar));
       } else {
@@ -1749,7 +1749,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
         // for it only at the symbol search, so the column groups whose
         // logits land first start their softmax at once
         auto my_slot = [&]() -> uint32_t {
-          if constexpr (DLIC_SLOT_MBAR) mbar_wait(smem_u32(&s_sbar), (uint32_t)t & 1u);
+          if constexpr (DLIC_SLOT_MBAR && PREC != 3) mbar_wait(smem_u32(&s_sbar), (uint32_t)t & 1u);
           return s_slot[row];
         };
         if (!DLIC_SLOT_MBAR || PREC == 3) asm volatile("bar.sync 7, %0;" ::"n"(DEC_THREADS) : "memory");

@@ -133,7 +133,13 @@ struct TcX3 {
     for (int l = 1; l < NLAYER; ++l) {
       hook(l);
       if (l < NLAYER - 1) load_bias(l, bq);
-      wait_mma();
+      if (l == NLAYER - 1 && col_grp() >= 2) {  // logits [128,256): the second half (bar2; == bar in the encoder)
+        mbar_wait(bar2, phase);
+        phase ^= 1u;
+        tc_fence_after();
+      } else {
+        wait_mma();
+      }
       if (l < NLAYER - 1) {
         epilogue<false>(bq, 0.0f, 0.0f);
         signal();
@@ -203,13 +209,16 @@ struct TcX3 {
 
   // ---- MMA issuer warp
   // three MMAs of one K-slice: hi.hi (accumulate unless the layer's first), hi.lo, lo.hi
-  __device__ __forceinline__ void x3_slice(uint32_t whi, uint32_t wlo, uint32_t n, int kk, bool first) const {
-    const uint32_t id = umma_idesc(64, (int)n);
-    const uint64_t bh = umma_desc(whi, n * 16u, 128u), bl = umma_desc(wlo, n * 16u, 128u);
+  // (ni: instruction N, columns [n0, n0 + ni) of a layer of width n)
+  __device__ __forceinline__ void x3_slice(uint32_t whi, uint32_t wlo, uint32_t n, int kk, bool first, uint32_t ni = 0,
+                                           uint32_t n0 = 0) const {
+    const uint32_t id = umma_idesc(64, (int)(ni ? ni : n));
+    const uint32_t bo = (n0 / 8u) * 128u;
+    const uint64_t bh = umma_desc(whi + bo, n * 16u, 128u), bl = umma_desc(wlo + bo, n * 16u, 128u);
     const uint32_t ah = tmem + X3_AHI + 8u * (uint32_t)kk, al = tmem + X3_ALO + 8u * (uint32_t)kk;
-    umma_ts_warp(tmem + TS_D, ah, bh, id, first ? 0u : 1u);
-    umma_ts_warp(tmem + TS_D, ah, bl, id, 1u);
-    umma_ts_warp(tmem + TS_D, al, bh, id, 1u);
+    umma_ts_warp(tmem + TS_D + n0, ah, bh, id, first ? 0u : 1u);
+    umma_ts_warp(tmem + TS_D + n0, ah, bl, id, 1u);
+    umma_ts_warp(tmem + TS_D + n0, al, bh, id, 1u);
   }
   // one stream chunk of layer l (1..5): hidden layers 4 K-slices, the
   // logits layer 2, each {hi, lo}
@@ -250,7 +259,13 @@ struct TcX3 {
       umma_ts_warp(tmem + TS_D, a, bl, id, 1u);
     }
     umma_commit_warp(bar);
+    if (bar2 != bar) umma_commit_warp(bar2);
   }
+  // Decoder (bar2 != bar): every layer completes both barriers, except the
+  // logits layer, issued as two N=128 halves -- [0,128) for all four chunks
+  // (their stages held), committed to bar (column groups 0-1 start their
+  // softmax), then [128,256) from the same stages, committed to bar2.  Per
+  // element the K order is the encoder's single N=256 layer's.
   __device__ __forceinline__ void issue_network() {
 #pragma unroll 1
     for (int l = 1; l < NLAYER; ++l) {
@@ -259,10 +274,38 @@ struct TcX3 {
       for (int j = 0; j < NGRP; ++j) asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
       if (prof) pw[2] += clock64() - t0;
       tc_fence_after();
+      if (l == NLAYER - 1 && bar2 != bar && !(mode & 4u)) {
+#pragma unroll 1
+        for (int cl = 0; cl < 4; ++cl) {
+          const uint32_t c = ccnt + (uint32_t)cl, s = c % (uint32_t)S;
+          mbar_wait(full0 + 8u * s, (c / (uint32_t)S) & 1u);
+          tc_fence_after();
+          const uint32_t base = ring + s * CH_BYTES;
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+            x3_slice(base + (2u * i) * X3_SL_LAST, base + (2u * i + 1u) * X3_SL_LAST, (uint32_t)NOUT, 2 * cl + i,
+                     cl == 0 && i == 0, 128u, 0u);
+        }
+        umma_commit_warp(bar);
+#pragma unroll 1
+        for (int cl = 0; cl < 4; ++cl) {
+          const uint32_t s = (ccnt + (uint32_t)cl) % (uint32_t)S;
+          const uint32_t base = ring + s * CH_BYTES;
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+            x3_slice(base + (2u * i) * X3_SL_LAST, base + (2u * i + 1u) * X3_SL_LAST, (uint32_t)NOUT, 2 * cl + i,
+                     cl == 0 && i == 0, 128u, 128u);
+          umma_commit_warp(empty0 + 8u * s);
+        }
+        ccnt += 4;
+        umma_commit_warp(bar2);
+        continue;
+      }
       const int nch = l < NLAYER - 1 ? 2 : 4;
 #pragma unroll 1
       for (int cl = 0; cl < nch; ++cl) consume(l, cl);
       umma_commit_warp(bar);
+      if (bar2 != bar) umma_commit_warp(bar2);
     }
   }
   __device__ __forceinline__ void issue_tiles(uint64_t n) {
