@@ -154,10 +154,6 @@ constexpr uint32_t DEC_D_ODD = DEC_SPLIT_LOGITS ? 0u : 128u;
 #ifndef DLIC_LOGIT_EARLY
 #define DLIC_LOGIT_EARLY 1
 #endif
-// decoder logits committed 3:1 (groups 0-2, then group 3) instead of 2:2
-#ifndef DLIC_LOGIT31
-#define DLIC_LOGIT31 1
-#endif
 #ifndef DLIC_NSPLIT_ORDER
 #define DLIC_NSPLIT_ORDER 1
 #endif
@@ -568,8 +564,8 @@ struct TcEngineT {
   }
   // decoder: column groups 0-1 wait on `bar`, groups 2-3 on `bar2` (the two
   // N=64 halves of a hidden layer complete separately)
-  __device__ __forceinline__ void wait_mma_g(int ng = 2) {
-    if (DEC_NSPLIT) mbar_wait(col_grp() < ng ? bar : bar2, phase);
+  __device__ __forceinline__ void wait_mma_g() {
+    if (DEC_NSPLIT) mbar_wait(col_grp() < 2 ? bar : bar2, phase);
     else mbar_wait(bar, phase);
     phase ^= 1u;
     tc_fence_after();
@@ -705,7 +701,7 @@ struct TcEngineT {
     for (int l = 1; l < NLAYER; ++l) {
       hook(l);
       if (l < NLAYER - 1) load_bias(l, bq);
-      wait_mma_g(l == NLAYER - 1 && DLIC_LOGIT31 ? 3 : 2);  // logits: groups 0-2 on bar (DLIC_LOGIT31)
+      wait_mma_g();
       if (l < NLAYER - 1) {
 #if DLIC_EPI2H
         epilogue_2h(dcol_of(l), ao_of(l + 1), bq);
@@ -760,26 +756,6 @@ struct TcEngineT {
           issue_slices(l, 2 * j, 2 * j + 2, TM_D, 128, 0, ao_of(l));
         }
 #if DLIC_LOGIT_EARLY
-        if (DEC_NSPLIT && DLIC_LOGIT31) {
-          // 3:1 -- groups 0-2's logits [0,192) on bar, group 3's [192,256) on
-          // bar2.  Columns [128,192) overlap the last hidden accumulator's
-          // columns [0,64), which only groups 0-1 read: their K-slices 0-3
-          // go once group 1 signalled; [192,256) (read by groups 2-3) after
-          // group 3.  Per element the K order is still 0..7.
-          asm volatile("bar.sync 8, 160;" ::: "memory");
-          issue_slices(l, 0, 2, TM_D, 128, 0, ao_of(l));
-          asm volatile("bar.sync 9, 160;" ::: "memory");
-          issue_slices(l, 2, 4, TM_D, 128, 0, ao_of(l));
-          issue_slices(l, 0, 4, TM_D + 128u, 64, 128, ao_of(l));
-          asm volatile("bar.sync 10, 160;" ::: "memory");
-          issue_slices(l, 4, 6, TM_D, 192, 0, ao_of(l));
-          asm volatile("bar.sync 11, 160;" ::: "memory");
-          issue_slices(l, 6, 8, TM_D, 192, 0, ao_of(l));
-          umma_commit_warp(bar);
-          issue_slices(l, 0, 8, TM_D + 192u, 64, 192, ao_of(l));
-          umma_commit_warp(bar2);
-          continue;
-        }
         if (DEC_NSPLIT) {  // groups 0-1's logits are columns [0,128): their softmax may start
           umma_commit_warp(bar);
           issue_slices(l, 0, 8, TM_D + 128u, 128, 128, ao_of(l));

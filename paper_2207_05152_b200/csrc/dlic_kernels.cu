@@ -1202,7 +1202,7 @@ __global__ void __launch_bounds__(dec_block(PREC), 1)
   constexpr int BITS = pix_bits<PREC>();
   typename EngineSel<PREC>::T eng;
   Pix* ring = reinterpret_cast<Pix*>(engine_setup<PREC>(eng, smem, w, bar, &tslot, p.w3d));
-  if constexpr (PREC != 0 && PREC != 3) eng.bar2 = smem_u32(&bar[2]);  // the decoder's logits halves
+  if constexpr (PREC == 1 || PREC == 4) eng.bar2 = smem_u32(&bar[2]);  // the decoder's logits halves (P350K: none, measured slower)
   if (w.b1img) {  // the unit's image's metadata-folded layer-1 bias
     if constexpr (PREC == 1) {
       __syncthreads();  // engine_setup's bias copy is complete

@@ -211,13 +211,7 @@ struct TcStreamT {
     for (int l = 1; l <= LAST; ++l) {
       hook(l);
       if (l < NLAYER - 1) load_bias(l, bq);
-      if (!H12 && l == NLAYER - 1 && col_grp() >= 2) {  // logits [128,256): the second half (bar2; == bar in the encoder)
-        mbar_wait(bar2, phase);
-        phase ^= 1u;
-        tc_fence_after();
-      } else {
-        wait_mma();
-      }
+      wait_mma();
       if (l < NLAYER - 1) {
         epilogue<false>(bq, 0.0f, 0.0f);
         signal();
@@ -358,7 +352,6 @@ struct TcStreamT {
       umma_ts_warp(tmem + TS_D, tmem + TS_A0 + 8u * (uint32_t)kk, bd, id, kk > 0 ? 1u : 0u);
     }
     umma_commit_warp(bar);
-    if (!H12 && bar2 != bar) umma_commit_warp(bar2);
   }
   // (encoder) n networks back to back, each once the row warps signal start_l0
   __device__ __forceinline__ void issue_tiles(uint64_t n) {
@@ -391,40 +384,9 @@ struct TcStreamT {
       for (int j = 0; j < NGRP; ++j) asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
       if (prof) pw[2] += clock64() - t0;
       tc_fence_after();
-      if (!H12 && l == NLAYER - 1 && bar2 != bar && !(mode & 4u)) {
-        // decoder: the logits as two N=128 halves -- [0,128) from all
-        // CH_LAYER chunks (their stages held), committed to bar (column
-        // groups 0-1 start their softmax), then [128,256) from the same
-        // stages, committed to bar2; per element the encoder's K order
-        const uint32_t id = umma_idesc(64, SH / 2);
-#pragma unroll 1
-        for (int hf = 0; hf < 2; ++hf) {
-#pragma unroll 1
-          for (int cl = 0; cl < CH_LAYER; ++cl) {
-            const uint32_t c = ccnt + (uint32_t)cl, st = c % (uint32_t)S;
-            if (hf == 0) {
-              mbar_wait(full0 + 8u * st, (c / (uint32_t)S) & 1u);
-              tc_fence_after();
-            }
-#pragma unroll
-            for (int i = 0; i < CH_SL; ++i) {
-              const int kk = CH_SL * cl + i;
-              const uint64_t bd = umma_desc(ring + st * CH_BYTES + (uint32_t)i * SL_BYTES + (uint32_t)hf * (SH / 16) * 128u,
-                                            (uint32_t)SH * 16u, 128u);
-              umma_ts_warp(tmem + TS_D + (uint32_t)hf * (SH / 2), tmem + TS_A + 8u * (uint32_t)kk, bd, id,
-                           kk > 0 ? 1u : 0u);
-            }
-            if (hf == 1) umma_commit_warp(empty0 + 8u * st);
-          }
-          umma_commit_warp(hf == 0 ? bar : bar2);
-        }
-        ccnt += (uint32_t)CH_LAYER;
-        continue;
-      }
 #pragma unroll 1
       for (int cl = 0; cl < CH_LAYER; ++cl) consume(cl);
       umma_commit_warp(bar);
-      if (!H12 && bar2 != bar) umma_commit_warp(bar2);
     }
     if constexpr (H12) {
       // the last hidden layer's epilogues (A of the head, and D free)

@@ -52,4 +52,4 @@ for rep in range(2):
         out = subprocess.run([sys.executable, "-c", CHILD % (ROOT, os.path.abspath(lib), cfg, blob, prec)],
                              capture_output=True, text=True)
         line = [l for l in out.stdout.splitlines() if l.startswith("{")]
-        print(lib, line[-1] if line else out.stderr[-400:])
+        print(lib, line[-1] if line else out.stderr[-400:], flush=True)
