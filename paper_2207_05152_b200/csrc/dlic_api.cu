@@ -16,6 +16,7 @@
 #include <tuple>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/dlic.h"
@@ -133,6 +134,29 @@ cudaStream_t my_stream() {
     dev = cur;
   }
   return s;
+}
+
+// host copy between a user buffer and pinned staging: large copies (batches
+// of images or containers, tens to hundreds of MB) are split across host
+// threads -- one thread's memcpy runs at a fraction of the host's memory
+// bandwidth and would dominate the end-to-end time of the batch calls
+void par_memcpy(void* dst, const void* src, size_t n) {
+  constexpr size_t MIN_SPLIT = 8u << 20;
+  const unsigned hw = std::thread::hardware_concurrency();
+  const unsigned nt = (unsigned)std::min<size_t>(std::min(hw ? hw : 1u, 16u), n / MIN_SPLIT);
+  if (nt <= 1) {
+    memcpy(dst, src, n);
+    return;
+  }
+  const size_t chunk = ((n + nt - 1) / nt + 63) & ~(size_t)63;
+  std::vector<std::thread> th;
+  th.reserve(nt - 1);
+  for (unsigned i = 1; i < nt; ++i) {
+    const size_t a = std::min(n, (size_t)i * chunk), b = std::min(n, a + chunk);
+    if (b > a) th.emplace_back([=]() { memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a); });
+  }
+  memcpy(dst, src, std::min(n, chunk));
+  for (auto& t : th) t.join();
 }
 
 // pinned staging buffers (per thread, grown on demand)
@@ -725,7 +749,7 @@ cudaError_t h2d(void* dst, const void* src, size_t n, cudaStream_t st) {
   if (!pin) return cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st);
   cudaError_t e = cudaStreamSynchronize(st);  // staging buffer may still be in flight
   if (e != cudaSuccess) return e;
-  memcpy(pin, src, n);
+  par_memcpy(pin, src, n);
   return cudaMemcpyAsync(dst, pin, n, cudaMemcpyHostToDevice, st);
 }
 
@@ -962,7 +986,7 @@ dlic_status dlic_encode(const dlic_model* m, const uint8_t* img, uint32_t width,
   CUDA_TRY(cudaStreamSynchronize(st));
   uint8_t* res = static_cast<uint8_t*>(malloc(n));
   if (!res) return fail(DLIC_E_OUT_OF_MEMORY, "malloc");
-  memcpy(res, hb, n);
+  par_memcpy(res, hb, n);
   *out = res;
   *out_len = n;
   return DLIC_OK;
@@ -1026,7 +1050,7 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
   CUDA_TRY(cudaStreamSynchronize(st));
   uint64_t meta[2] = {0, (uint64_t)len};
   memcpy(pin, meta, 16);
-  memcpy(pin + 16, bits, len);
+  par_memcpy(pin + 16, bits, len);
   CUDA_TRY(cudaMemcpyAsync(d_meta, pin, 16, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(d_bits, pin + 16, len, cudaMemcpyHostToDevice, st));
   CUDA_TRY(launch_dec_prep(p, d_bits, d_meta, d_meta + 1, d_sbase, d_slen, d_status, st, tables == nullptr));
@@ -1083,7 +1107,7 @@ static dlic_status decode_common(const dlic_model* m, const uint8_t* bits, size_
   int32_t stat;
   memcpy(&stat, ho, 4);
   if (stat != 0) return fail((dlic_status)stat, "lane invariant / framing check failed on the device");
-  memcpy(img, ho + 64, npx * pxb);
+  par_memcpy(img, ho + 64, npx * pxb);
   return DLIC_OK;
 }
 
@@ -1255,7 +1279,7 @@ dlic_status dlic_encode_batch(const dlic_model* m, const uint8_t* imgs, uint32_t
   CUDA_TRY(cudaStreamSynchronize(st));
   uint8_t* res = static_cast<uint8_t*>(malloc(total ? total : 1));
   if (!res) return fail(DLIC_E_OUT_OF_MEMORY, "malloc");
-  memcpy(res, hb, total);
+  par_memcpy(res, hb, total);
   for (uint32_t i = 0; i < nc; ++i) sizes[i] = hs[i];
   *out = res;
   *out_len = total;
@@ -1339,7 +1363,7 @@ dlic_status dlic_decode_batch(const dlic_model* m, const uint8_t* bits, size_t l
     if (stat != 0) return fail((dlic_status)stat, "lane invariant / framing check failed on the device (image " +
                                                       std::to_string(i) + ")");
   }
-  memcpy(imgs, ho + ((4ull * n + 63) & ~63ull), npx);
+  par_memcpy(imgs, ho + ((4ull * n + 63) & ~63ull), npx);
   return DLIC_OK;
 }
 
