@@ -64,6 +64,10 @@ struct TcX3 {
   unsigned long long pw[3] = {0, 0, 0};
 
   __device__ __forceinline__ uint32_t lane_off() const { return ((threadIdx.x >> 5) & 3u) << 21; }
+  // hidden accumulators alternate between D columns [128,256) (layers 1, 3,
+  // 5) and [0,128) (2, 4): layer l+1's first K-chunk is issued once column
+  // groups 0-1 signalled, while groups 2-3 still read layer l's accumulator
+  static __device__ __forceinline__ uint32_t dcol(int l) { return (l & 1) ? 0u : 128u; }
 
   // ---- row warps
   __device__ __forceinline__ void put_input(const uint32_t (&a)[5]) const {
@@ -90,11 +94,11 @@ struct TcX3 {
   // bias (+ the fresh taps in fp32 for layer 1) + ReLU, split into bf16 hi and
   // lo limbs -> A_hi, A_lo packed columns [16j + 8h, +8)
   template <bool L0>
-  __device__ __forceinline__ void epilogue(const float2 (&b2)[8], float xa, float xb) const {
+  __device__ __forceinline__ void epilogue(const float2 (&b2)[8], float xa, float xb, uint32_t dc) const {
     const uint32_t lo = lane_off();
     const int j = col_grp(), h = half_id();
     uint32_t v[16];
-    tmem_ld16h<16>(tmem + lo + TS_D + 32u * (uint32_t)j, v);
+    tmem_ld16h<16>(tmem + lo + TS_D + dc + 32u * (uint32_t)j, v);
     tc_wait_ld();
     const float4* fw = reinterpret_cast<const float4*>(bias + X3_B_FRESH) + 16 * j + 8 * h;
     uint32_t phi[8], plo[8];
@@ -127,7 +131,7 @@ struct TcX3 {
     };
     load_bias(0, bq);
     wait_mma();
-    epilogue<true>(bq, xa, xb);
+    epilogue<true>(bq, xa, xb, dcol(0));
     signal();
 #pragma unroll 1
     for (int l = 1; l < NLAYER; ++l) {
@@ -141,7 +145,7 @@ struct TcX3 {
         wait_mma();
       }
       if (l < NLAYER - 1) {
-        epilogue<false>(bq, 0.0f, 0.0f);
+        epilogue<false>(bq, 0.0f, 0.0f, dcol(l));
         signal();
       }
     }
@@ -209,16 +213,17 @@ struct TcX3 {
 
   // ---- MMA issuer warp
   // three MMAs of one K-slice: hi.hi (accumulate unless the layer's first), hi.lo, lo.hi
-  // (ni: instruction N, columns [n0, n0 + ni) of a layer of width n)
-  __device__ __forceinline__ void x3_slice(uint32_t whi, uint32_t wlo, uint32_t n, int kk, bool first, uint32_t ni = 0,
-                                           uint32_t n0 = 0) const {
+  // (ni: instruction N, columns [n0, n0 + ni) of a layer of width n, into D
+  // columns [dc, dc + ni))
+  __device__ __forceinline__ void x3_slice(uint32_t whi, uint32_t wlo, uint32_t n, int kk, bool first, uint32_t ni,
+                                           uint32_t n0, uint32_t dc) const {
     const uint32_t id = umma_idesc(64, (int)(ni ? ni : n));
     const uint32_t bo = (n0 / 8u) * 128u;
     const uint64_t bh = umma_desc(whi + bo, n * 16u, 128u), bl = umma_desc(wlo + bo, n * 16u, 128u);
     const uint32_t ah = tmem + X3_AHI + 8u * (uint32_t)kk, al = tmem + X3_ALO + 8u * (uint32_t)kk;
-    umma_ts_warp(tmem + TS_D + n0, ah, bh, id, first ? 0u : 1u);
-    umma_ts_warp(tmem + TS_D + n0, ah, bl, id, 1u);
-    umma_ts_warp(tmem + TS_D + n0, al, bh, id, 1u);
+    umma_ts_warp(tmem + TS_D + dc, ah, bh, id, first ? 0u : 1u);
+    umma_ts_warp(tmem + TS_D + dc, ah, bl, id, 1u);
+    umma_ts_warp(tmem + TS_D + dc, al, bh, id, 1u);
   }
   // one stream chunk of layer l (1..5): hidden layers 4 K-slices, the
   // logits layer 2, each {hi, lo}
@@ -235,13 +240,14 @@ struct TcX3 {
     } else if (l < NLAYER - 1) {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        x3_slice(base + (2u * i) * X3_SL, base + (2u * i + 1u) * X3_SL, (uint32_t)HID, 4 * cl + i, cl == 0 && i == 0);
+        x3_slice(base + (2u * i) * X3_SL, base + (2u * i + 1u) * X3_SL, (uint32_t)HID, 4 * cl + i, cl == 0 && i == 0, 0u,
+                 0u, dcol(l));
       umma_commit_warp(empty0 + 8u * s);
     } else {
 #pragma unroll
       for (int i = 0; i < 2; ++i)
         x3_slice(base + (2u * i) * X3_SL_LAST, base + (2u * i + 1u) * X3_SL_LAST, (uint32_t)NOUT, 2 * cl + i,
-                 cl == 0 && i == 0);
+                 cl == 0 && i == 0, 0u, 0u, 0u);
       umma_commit_warp(empty0 + 8u * s);
     }
     ++ccnt;
@@ -255,8 +261,8 @@ struct TcX3 {
       const uint32_t a = tmem + TS_A0 + 8u * (uint32_t)kk;
       const uint64_t bh = umma_desc(l1s + (2u * kk) * X3_SL, (uint32_t)HID * 16u, 128u);
       const uint64_t bl = umma_desc(l1s + (2u * kk + 1u) * X3_SL, (uint32_t)HID * 16u, 128u);
-      umma_ts_warp(tmem + TS_D, a, bh, id, kk > 0 ? 1u : 0u);
-      umma_ts_warp(tmem + TS_D, a, bl, id, 1u);
+      umma_ts_warp(tmem + TS_D + dcol(0), a, bh, id, kk > 0 ? 1u : 0u);
+      umma_ts_warp(tmem + TS_D + dcol(0), a, bl, id, 1u);
     }
     umma_commit_warp(bar);
     if (bar2 != bar) umma_commit_warp(bar2);
@@ -270,13 +276,32 @@ struct TcX3 {
 #pragma unroll 1
     for (int l = 1; l < NLAYER; ++l) {
       const long long t0 = prof ? clock64() : 0;
-#pragma unroll
-      for (int j = 0; j < NGRP; ++j) asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
-      if (prof) pw[2] += clock64() - t0;
-      tc_fence_after();
-      if (l == NLAYER - 1 && bar2 != bar && !(mode & 4u)) {
+      if (l < NLAYER - 1) {
+        // hidden layer: K-chunk 0 (column groups 0-1's activations) once they
+        // signalled, chunk 1 once groups 2-3 did (double-buffered D: the
+        // previous layer's accumulator is still read meanwhile)
+#pragma unroll 1
+        for (int cl = 0; cl < 2; ++cl) {
+          asm volatile("bar.sync %0, 160;" ::"r"(8 + 2 * cl) : "memory");
+          asm volatile("bar.sync %0, 160;" ::"r"(9 + 2 * cl) : "memory");
+          if (prof) pw[2] += clock64() - t0;
+          tc_fence_after();
+          consume(l, cl);
+        }
+        umma_commit_warp(bar);
+        if (bar2 != bar) umma_commit_warp(bar2);
+        continue;
+      }
+      if (bar2 != bar && !(mode & 4u)) {
+        // decoder logits as two N=128 halves: [0,128) (the accumulator the
+        // last hidden layer did not use) K-chunk cl once column group cl
+        // signalled, the chunks' stages held, committed to bar (groups 0-1
+        // start their softmax); then [128,256) from the same stages after
+        // every group, committed to bar2.  Per element the encoder's K order.
 #pragma unroll 1
         for (int cl = 0; cl < 4; ++cl) {
+          asm volatile("bar.sync %0, 160;" ::"r"(8 + cl) : "memory");
+          tc_fence_after();
           const uint32_t c = ccnt + (uint32_t)cl, s = c % (uint32_t)S;
           mbar_wait(full0 + 8u * s, (c / (uint32_t)S) & 1u);
           tc_fence_after();
@@ -284,8 +309,9 @@ struct TcX3 {
 #pragma unroll
           for (int i = 0; i < 2; ++i)
             x3_slice(base + (2u * i) * X3_SL_LAST, base + (2u * i + 1u) * X3_SL_LAST, (uint32_t)NOUT, 2 * cl + i,
-                     cl == 0 && i == 0, 128u, 0u);
+                     cl == 0 && i == 0, 128u, 0u, 0u);
         }
+        if (prof) pw[2] += clock64() - t0;
         umma_commit_warp(bar);
 #pragma unroll 1
         for (int cl = 0; cl < 4; ++cl) {
@@ -294,16 +320,20 @@ struct TcX3 {
 #pragma unroll
           for (int i = 0; i < 2; ++i)
             x3_slice(base + (2u * i) * X3_SL_LAST, base + (2u * i + 1u) * X3_SL_LAST, (uint32_t)NOUT, 2 * cl + i,
-                     cl == 0 && i == 0, 128u, 128u);
+                     cl == 0 && i == 0, 128u, 128u, 128u);
           umma_commit_warp(empty0 + 8u * s);
         }
         ccnt += 4;
         umma_commit_warp(bar2);
         continue;
       }
-      const int nch = l < NLAYER - 1 ? 2 : 4;
+      // (encoder) the logits over [0,256) once every group's last epilogue is done
+#pragma unroll
+      for (int j = 0; j < NGRP; ++j) asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
+      if (prof) pw[2] += clock64() - t0;
+      tc_fence_after();
 #pragma unroll 1
-      for (int cl = 0; cl < nch; ++cl) consume(l, cl);
+      for (int cl = 0; cl < 4; ++cl) consume(l, cl);
       umma_commit_warp(bar);
       if (bar2 != bar) umma_commit_warp(bar2);
     }
