@@ -17,6 +17,18 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running CPU test")
 
 
+def pytest_collection_modifyitems(config, items):
+    """GPU tests get a per-test watchdog (pytest-timeout, thread method: it
+    ends the process even inside a blocking CUDA call), so a kernel that never
+    completes fails the run instead of hanging the box.  The whole GPU suite
+    takes ~30 s on a B200."""
+    if not config.pluginmanager.hasplugin("timeout"):
+        return
+    for item in items:
+        if item.get_closest_marker("gpu") is not None and item.get_closest_marker("timeout") is None:
+            item.add_marker(pytest.mark.timeout(300, method="thread"))
+
+
 def golden(name):
     with open(os.path.join(GOLDEN, name)) as fh:
         return json.load(fh)
