@@ -276,12 +276,15 @@ __global__ void __launch_bounds__(enc_block(PREC), 1)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar[3];  // 0 MMA completion, 2 spare (engine)
   __shared__ uint32_t tslot;
+  __shared__ uint32_t s_nq[2];  // 12-bit: the tile's pass-2 chunk count, (tile ordinal << 8 | n), by tile parity
+  if (threadIdx.x < 2) s_nq[threadIdx.x] = 0u;
   const int row = tile_row();
   using Pix = PixT<PREC>;
   constexpr int BITS = pix_bits<PREC>();
   const Pix* const imgp = reinterpret_cast<const Pix*>(imgs);
   typename EngineSel<PREC>::T eng;
   engine_setup<PREC>(eng, smem, w, bar, &tslot, p.w3d);
+  if constexpr (PREC == 3) eng.nq2s = s_nq;  // (engine_setup's barrier orders the zeroing above)
   // tiles of units [u_lo, u_lo + u_cnt) (global tile index = tbase + k)
   const uint64_t tbase = (uint64_t)p.u_lo * p.tiles_per_unit;
   const uint64_t total = (uint64_t)p.u_cnt * p.tiles_per_unit;
@@ -294,12 +297,20 @@ __global__ void __launch_bounds__(enc_block(PREC), 1)
       const uint64_t n = total > blockIdx.x ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
       uint64_t pt = 0;
       int pk = 0;
-      auto next = [&](int& c) -> bool {  // the 20 chunks of every tile's network, in order
+      int tlen = EngineSel<PREC>::T::CPN;  // chunks of the current tile (12-bit: 80 + 2 x its pass-2 chunks)
+      auto next = [&](int& c) -> bool {  // every tile's network chunks, in order
         if (pt >= n) return false;
+        if constexpr (PREC == 3) {
+          if (pk == CH_HID12 + H12_STREAM) {  // the tile's pass 2 starts: its length, published before start_l0
+            mbar_wait(eng.aready, (uint32_t)pt & 1u);
+            tlen = CH_HID12 + H12_STREAM + 2 * (int)(s_nq[pt & 1u] & 0xFFu);
+          }
+        }
         c = pk;
-        if (++pk == EngineSel<PREC>::T::CPN) {
+        if (++pk == tlen) {
           pk = 0;
           ++pt;
+          tlen = EngineSel<PREC>::T::CPN;
         }
         return true;
       };
@@ -392,13 +403,26 @@ __global__ void __launch_bounds__(enc_block(PREC), 1)
   };
 
   if (dbg || PREC >= 2) {  // debug exports (and P350K, P12): one tile at a time
+    uint32_t kt = 0;  // this CTA's tile ordinal
 #pragma unroll 1
-    for (uint64_t tile = tbase + blockIdx.x; tile < tbase + total; tile += gridDim.x) {
+    for (uint64_t tile = tbase + blockIdx.x; tile < tbase + total; tile += gridDim.x, ++kt) {
       const long long c0 = clock64();
       Px x = pixel(tile);
       load_sym(x);
       auto get = getter(x);
       feed_x(x, get);
+      uint32_t nq2 = (uint32_t)H12_NCH;
+      if constexpr (PREC == 3) {
+        // the second head pass only needs the chunks up to the tile's largest
+        // true symbol (c_s sums the f of the symbols below s; the f of each
+        // chunk are the decoder's): count published for the issuer and the
+        // producer before start_l0, read back after a row-warp barrier
+        const uint32_t mq = dbg ? (uint32_t)H12_NCH : (x.valid ? (uint32_t)x.sym / (uint32_t)H12_CN + 1u : 1u);
+        const uint32_t wq = __reduce_max_sync(0xFFFFFFFFu, mq);
+        if (lane_id() == 0) atomicMax(&s_nq[kt & 1u], (kt << 8) | wq);
+        row_sync();
+        nq2 = s_nq[kt & 1u] & 0xFFu;
+      }
       eng.start_l0();
       const long long c1 = clock64();
       eng.run_rest(fresh_in<PREC>(get(0, -1)), fresh_in<PREC>(get(-1, 2)), [](int) {});
@@ -409,7 +433,7 @@ __global__ void __launch_bounds__(enc_block(PREC), 1)
                    x.valid && dbg_freqs ? dbg_freqs + x.gi * H12_N : nullptr};
         bool mine;
         uint32_t fs, cs;
-        q12_row<true>(eng, (uint32_t)x.sym, mine, fs, cs, []() {}, dbg ? &dd : nullptr);
+        q12_row<true>(eng, (uint32_t)x.sym, mine, fs, cs, []() {}, dbg ? &dd : nullptr, nq2);
         if (x.valid && mine) fc[x.fci] = fs | (cs << 16);
         if (p.prof && threadIdx.x == 0) {
           atomicAdd(&g_sprof[5], (unsigned long long)(c1 - c0));

@@ -130,6 +130,8 @@ struct TcStreamT {
   uint32_t aready;         // layer-1 input ready: one arrival per row warp
   uint32_t dfull0, dfree0; // 12-bit head: accumulator buffer b full / released (+8b)
   uint32_t hph = 0;        // 12-bit head: dfull parities of buffers 0, 1 (bits 0, 1)
+  uint32_t huse = 0;       // 12-bit head: accumulator-chunk uses so far (buffer = huse & 1; both sides)
+  uint32_t* nq2s = nullptr;  // 12-bit encoder: per-tile pass-2 chunk counts ([2], tile-tagged), shared
   const uint8_t* wstream;  // the streamed weight image (global)
   uint32_t ccnt = 0, pcnt = 0;   // chunks consumed / produced (issuer warp)
   bool prof = false;
@@ -258,8 +260,8 @@ struct TcStreamT {
   // 12-bit head, row side: this thread's 16 logits of head chunk u (pass-major
   // counter; buffer u & 1, columns [32j + 16h, +16) of the chunk), the buffer
   // released once loaded
-  __device__ __forceinline__ void head_ld(uint32_t u, uint32_t (&v)[16]) {
-    const uint32_t b = u & 1u;
+  __device__ __forceinline__ void head_ld(uint32_t (&v)[16]) {
+    const uint32_t b = huse++ & 1u;
     mbar_wait(dfull0 + 8u * b, (hph >> b) & 1u);
     hph ^= 1u << b;
     tc_fence_after();
@@ -354,6 +356,7 @@ struct TcStreamT {
     umma_commit_warp(bar);
   }
   // (encoder) n networks back to back, each once the row warps signal start_l0
+  // (12-bit: with the tile's pass-2 chunk count, written before that signal)
   __device__ __forceinline__ void issue_tiles(uint64_t n) {
     const long long t00 = clock64();
     uint32_t aph = 0;
@@ -362,7 +365,8 @@ struct TcStreamT {
       mbar_wait(aready, aph);
       aph ^= 1u;
       issue_l0();
-      issue_network();
+      if constexpr (H12) issue_network(nq2s ? (nq2s[k & 1u] & 0xFFu) : (uint32_t)H12_NCH);
+      else issue_network();
     }
     if (prof && lane_id() == 0) {
       atomicAdd(&g_sprof[0], pw[0]);
@@ -375,7 +379,9 @@ struct TcStreamT {
   // the layers after layer 1, each once every column group signalled its
   // previous epilogue; 12-bit: layers 2-5, then the head's two passes, each
   // accumulator chunk once the row warps released its buffer (two chunks ago)
-  __device__ __forceinline__ void issue_network() {
+  // 12-bit: nq2 = head chunks of the second pass (the encoder stops after the
+  // chunk holding its tile's largest true symbol; the decoder runs all 32)
+  __device__ __forceinline__ void issue_network(uint32_t nq2 = (uint32_t)H12_NCH) {
     constexpr int NHID = H12 ? NLAYER - 2 : NLAYER - 1;
 #pragma unroll 1
     for (int l = 1; l <= NHID; ++l) {
@@ -394,9 +400,9 @@ struct TcStreamT {
       for (int j = 0; j < NGRP; ++j) asm volatile("bar.sync %0, 160;" ::"r"(8 + j) : "memory");
       tc_fence_after();
 #pragma unroll 1
-      for (uint32_t u = 0; u < 2u * H12_NCH; ++u) {
-        const uint32_t b = u & 1u;
-        if (u >= 2) {  // buffer b held chunk u-2: wait until every row warp loaded it
+      for (uint32_t i = 0; i < (uint32_t)H12_NCH + nq2; ++i) {
+        const uint32_t u = huse++, b = u & 1u;
+        if (u >= 2) {  // buffer b held use u-2: wait until every row warp loaded it
           const long long t0 = prof ? clock64() : 0;
           mbar_wait(dfree0 + 8u * b, ((u >> 1) - 1u) & 1u);
           if (prof) pw[2] += clock64() - t0;
@@ -449,7 +455,8 @@ __device__ __forceinline__ f2 q12_e2(f2 l, f2 l2e, f2 nml, int i) {
 }
 template <bool ENC, class Mid>
 __device__ __forceinline__ int q12_row(TcStream12& e, uint32_t key, bool& mine_out, uint32_t& fs_out,
-                                       uint32_t& cs_out, Mid&& mid, const Q12Dbg* dbg = nullptr) {
+                                       uint32_t& cs_out, Mid&& mid, const Q12Dbg* dbg = nullptr,
+                                       uint32_t nq2 = (uint32_t)H12_NCH) {
   const int j = col_grp(), h = half_id();
   const int cb = 32 * j + 16 * h;
   const float2* hb2 = reinterpret_cast<const float2*>(e.bias + SB12_HEAD + cb);
@@ -459,7 +466,7 @@ __device__ __forceinline__ int q12_row(TcStream12& e, uint32_t key, bool& mine_o
 #pragma unroll 1
   for (uint32_t q = 0; q < (uint32_t)H12_NCH; ++q) {
     uint32_t v[16];
-    e.head_ld(q, v);
+    e.head_ld(v);
     f2 l[8];
     float a[16];
 #pragma unroll
@@ -516,10 +523,10 @@ __device__ __forceinline__ int q12_row(TcStream12& e, uint32_t key, bool& mine_o
   int sym = 0;
   const float keyf = (float)key;
 #pragma unroll 1
-  for (uint32_t q = 0; q < (uint32_t)H12_NCH; ++q) {
+  for (uint32_t q = 0; q < nq2; ++q) {
     uint32_t v[16];
-    e.head_ld(H12_NCH + q, v);
-    if (q == H12_NCH - 1) mid();
+    e.head_ld(v);
+    if (q == nq2 - 1) mid();
     f2 f[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
