@@ -32,7 +32,10 @@ namespace dlic {
 
 // decoder: the rANS warp publishes a front's slots on an mbarrier that each
 // row thread waits on right before its symbol search (1), or on named barrier
-// 7 that all 16 row warps sync on after the network (0)
+// 7 that all 16 row warps sync on after the network (0).  With 1 the column
+// groups whose logits half lands first start their softmax at once (C2
+// decode 10.92 -> 10.50 ms).  The 12-bit engine keeps barrier 7 either way
+// (its head has no early half; its key is read before the second pass).
 #ifndef DLIC_SLOT_MBAR
 #define DLIC_SLOT_MBAR 1
 #endif
